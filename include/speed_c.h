@@ -1,0 +1,313 @@
+/*
+ * speed_c.h — C-ABI of the B200-native SPEED (arXiv 2308.14129) parallel-training
+ * hot path: SEP partitioning, subgraph induction, the PAC lockstep trainer and the
+ * per-partition TGN training step on sm_100a.
+ *
+ * The reference (speedpart, /root/reference/proj) exposes a C++ value-type API
+ * and no FFI; every entry point below names the reference declaration it
+ * replaces (file:line under /root/reference/proj/include/speedpart/). Bindings
+ * (ctypes / cgo / JNI) for these are shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain pointers + sizes, caller-owned buffers; opaque handles own library
+ *    memory and are released with their *_destroy function.
+ *  - Every call returns spd_status with the reference CLI's exit-code numbering
+ *    (tools/speedpart_main.cpp:436-447): 0 ok, 1 usage, 2 data (DataError,
+ *    errors.hpp:10-20), 3 internal (InternalError, errors.hpp:23-32; also
+ *    CUDA / NCCL failures). The reference's error code string ("UnsortedStream",
+ *    "NonChronological", ...) and detail are readable per thread through
+ *    spd_last_error_code()/spd_last_error_detail(). No exception crosses the ABI.
+ *  - There is no CPU fallback: device entry points fail with status 3 and code
+ *    "CudaError" when no sm_100 device is present.
+ */
+#ifndef SPEED_C_H
+#define SPEED_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t spd_status;
+enum { SPD_OK = 0, SPD_USAGE = 1, SPD_DATA = 2, SPD_INTERNAL = 3 };
+
+const char* spd_last_error_code(void);
+const char* spd_last_error_detail(void);
+const char* spd_version(void);
+
+/* One timestamped interaction event; byte-identical to speedpart::TemporalEdge
+ * (types.hpp:15-21): {u32 src, u32 dst, f64 ts}, 16 bytes. */
+typedef struct spd_edge {
+    uint32_t src;
+    uint32_t dst;
+    double ts;
+} spd_edge;
+
+/* ---------------------------------------------------------------- L1 stream */
+
+/* gen_powerlaw (graph_io.hpp:34). out: `edges` records. Bit-identical stream. */
+spd_status spd_gen_powerlaw(uint32_t nodes, uint64_t edges, double alpha, uint64_t seed,
+                            spd_edge* out, uint32_t* node_count, double* t_max);
+
+/* chrono_split (graph_io.hpp:27): positional 3-way split sizes. */
+spd_status spd_chrono_split(uint64_t n, double f_train, double f_val, uint64_t* n_train,
+                            uint64_t* n_val, uint64_t* n_test);
+
+/* -------------------------------------------------------- L2 partitioning */
+
+/* compute_centrality (centrality.hpp:41). cent: node_count doubles. */
+spd_status spd_compute_centrality(const spd_edge* e, uint64_t n, uint32_t node_count,
+                                  double t_max, double beta, int32_t normalize_ts,
+                                  double* cent, double* t_max_out);
+/* compute_degree_centrality (centrality.hpp:44). */
+spd_status spd_compute_degree_centrality(const spd_edge* e, uint64_t n, uint32_t node_count,
+                                         double* cent);
+/* select_hubs (centrality.hpp:48). base_all: HubBase::All if nonzero. hubs: capacity
+ * node_count, ascending on return. */
+spd_status spd_select_hubs(const double* cent, uint32_t node_count, double k, int32_t base_all,
+                           uint32_t* hubs, uint64_t* n_hubs);
+
+/* PartitionerConfig (partitioner.hpp:11-17). cent may be shorter than node_count
+ * (CentralityTable::of returns 0 past its end, centrality.hpp:17). */
+typedef struct spd_partitioner_config {
+    int32_t num_parts;
+    double lambda;
+    double epsilon;
+    const double* cent;
+    uint32_t cent_count;
+    const uint32_t* hubs;
+    uint64_t n_hubs;
+    double k;
+} spd_partitioner_config;
+
+/* PartitionAssignment (partitioner.hpp:40-47). */
+typedef struct spd_assignment spd_assignment;
+
+/* partition_stream (partitioner.hpp:62) — bit-identical edge_part / node_parts / shared. */
+spd_status spd_partition_stream(const spd_edge* e, uint64_t n, uint32_t node_count,
+                                const spd_partitioner_config* cfg, spd_assignment** out);
+/* partition_unrestricted (partitioner.hpp:66). */
+spd_status spd_partition_unrestricted(const spd_edge* e, uint64_t n, uint32_t node_count,
+                                      const spd_partitioner_config* cfg, spd_assignment** out);
+/* score (partitioner.hpp:50-51) on an explicit PartitionState
+ * (sizes[num_parts], maxsize, minsize, A-sets as CSR over node_count). */
+spd_status spd_score(uint32_t i, uint32_t j, int32_t p, const spd_partitioner_config* cfg,
+                     const uint64_t* sizes, uint64_t maxsize, uint64_t minsize,
+                     uint32_t node_count, const uint64_t* a_off, const int32_t* a_parts,
+                     double* out);
+/* Build an assignment from external node_parts (the CLI's load_assignment,
+ * speedpart_main.cpp:135-179). edge_part may be NULL. */
+spd_status spd_assignment_from_parts(uint32_t node_count, int32_t num_parts, const uint64_t* np_off,
+                                     const int32_t* np_parts, const int32_t* edge_part,
+                                     uint64_t n_edges, uint64_t discards,
+                                     spd_assignment** out);
+void spd_assignment_destroy(spd_assignment* a);
+spd_status spd_assignment_info(const spd_assignment* a, int32_t* num_parts, uint32_t* node_count,
+                               uint64_t* n_edges, uint64_t* n_shared, uint64_t* discards,
+                               uint64_t* np_total, double* k_eff);
+spd_status spd_assignment_edge_part(const spd_assignment* a, int32_t* out);
+spd_status spd_assignment_node_parts(const spd_assignment* a, uint64_t* off, int32_t* parts);
+spd_status spd_assignment_shared(const spd_assignment* a, uint32_t* out);
+
+/* assign_eval_edges (partitioner.hpp:74-81). */
+typedef struct spd_eval_routing spd_eval_routing;
+spd_status spd_assign_eval_edges(const spd_edge* val, uint64_t n_val, const spd_edge* test,
+                                 uint64_t n_test, const spd_assignment* a,
+                                 spd_eval_routing** out);
+/* which: 0 = val, 1 = test. count[num_parts]; idx: per-partition lists back to back. */
+spd_status spd_eval_routing_counts(const spd_eval_routing* r, int32_t which, uint64_t* counts,
+                                   uint64_t* unroutable);
+spd_status spd_eval_routing_edges(const spd_eval_routing* r, int32_t which, uint64_t* idx);
+void spd_eval_routing_destroy(spd_eval_routing* r);
+
+/* ------------------------------------------------- L4 subgraphs and shuffle */
+
+/* induce_subgraphs (pac_sim.hpp:102-104). Each subgraph keeps, next to its
+ * time-ordered edges, the stream position (global edge id) of every edge. */
+typedef struct spd_subgraphs spd_subgraphs;
+spd_status spd_induce_subgraphs(const spd_edge* e, uint64_t n, uint32_t node_count,
+                                const uint64_t* np_off, const int32_t* np_parts, uint32_t np_count,
+                                int32_t num_parts, spd_subgraphs** out);
+/* simulate's shuffle branch (pac_sim.cpp:313-324): induce on explicit node groups;
+ * also returns how many edges the groups induce that no small part does
+ * (`recovered`, pac_sim.cpp:325-326) when small_off/small_nodes are given. */
+spd_status spd_induce_groups(const spd_edge* e, uint64_t n, uint32_t node_count,
+                             const uint64_t* group_off, const uint32_t* group_nodes,
+                             int32_t n_groups, const uint64_t* small_off,
+                             const uint32_t* small_nodes, int32_t n_small,
+                             spd_subgraphs** out, uint64_t* recovered);
+/* Build a subgraph set from explicit per-subgraph node lists and time-ordered
+ * edge lists (CSR over n; eids may be NULL = position in each list). */
+spd_status spd_subgraphs_from_lists(int32_t n, const uint64_t* node_off, const uint32_t* nodes,
+                                    const uint64_t* edge_off, const spd_edge* edges,
+                                    const uint64_t* eids, spd_subgraphs** out);
+spd_status spd_subgraphs_count(const spd_subgraphs* s, int32_t* count);
+spd_status spd_subgraph_sizes(const spd_subgraphs* s, int32_t p, uint64_t* n_nodes,
+                              uint64_t* n_edges);
+spd_status spd_subgraph_nodes(const spd_subgraphs* s, int32_t p, uint32_t* out);
+spd_status spd_subgraph_edges(const spd_subgraphs* s, int32_t p, spd_edge* out, uint64_t* eids);
+void spd_subgraphs_destroy(spd_subgraphs* s);
+
+/* shuffle_combine (pac_sim.hpp:108-110). out_off: num_workers+1; out_nodes:
+ * capacity small_off[n_small]. */
+spd_status spd_shuffle_combine(const uint64_t* small_off, const uint32_t* small_nodes,
+                               uint64_t n_small, int32_t num_workers, uint64_t epoch_seed,
+                               uint64_t* out_off, uint32_t* out_nodes);
+
+/* ------------------------------------------- L4 surrogate model (parity mode) */
+
+/* ModelParams::seeded (pac_sim.hpp:54). w_m: d*3d row-major, omega: d. */
+spd_status spd_model_seeded(int32_t d, uint64_t seed, double* w_m, double* omega, double* gamma);
+
+/* MemoryStore (pac_sim.hpp:19-39), resident in device HBM (f64 state + f64 last_ts). */
+typedef struct spd_memstore spd_memstore;
+spd_status spd_memstore_create(uint32_t node_count, int32_t d, int32_t device,
+                               spd_memstore** out);
+void spd_memstore_destroy(spd_memstore* m);
+spd_status spd_memstore_upload(spd_memstore* m, const double* state, const double* last_ts);
+spd_status spd_memstore_download(const spd_memstore* m, double* state, double* last_ts);
+spd_status spd_memstore_reset(spd_memstore* m);
+spd_status spd_memstore_copy(spd_memstore* dst, const spd_memstore* src);
+/* MemoryStore::digest (pac_sim.cpp:18-26): 16 hex chars + NUL. */
+spd_status spd_memstore_digest(const spd_memstore* m, char* out17);
+
+/* model_update (pac_sim.hpp:59) over a run of edges, applied in order on the GPU. */
+spd_status spd_model_update(spd_memstore* m, const spd_edge* e, uint64_t n, const double* w_m,
+                            const double* omega, double gamma);
+
+/* sync_shared (pac_sim.hpp:125-126). average: SyncStrategy::Average if nonzero. */
+spd_status spd_sync_shared(spd_memstore* const* mems, int32_t W, const uint32_t* shared,
+                           uint64_t n_shared, int32_t average);
+
+/* EpochReport (pac_sim.hpp:75-81) + StepLog (pac_sim.hpp:88-100). Arrays are caller
+ * owned and sized W (digests 17*W). Log arrays optional (log_cap 0 = no log):
+ * log_steps 4*log_cap u64 (global_step, worker, loop, batch_in_loop), snapshot
+ * worker ids + 17-char digests, log_cap entries each. */
+typedef struct spd_epoch_report {
+    uint64_t* batches;
+    uint64_t* loops;
+    uint64_t sync_events;
+    char* digests;
+    uint64_t log_cap;
+    uint64_t* log_steps;
+    uint64_t n_log;
+    int32_t* snap_worker;
+    char* snap_digests;
+    uint64_t n_snap;
+} spd_epoch_report;
+
+/* run_epoch (pac_sim.hpp:117-120) on device memory stores. */
+spd_status spd_run_epoch(const spd_subgraphs* subs, spd_memstore* const* mems, int32_t W,
+                         const double* w_m, const double* omega, double gamma,
+                         const uint32_t* shared, uint64_t n_shared, int32_t average,
+                         uint64_t batch_size, spd_epoch_report* rep);
+
+/* SimConfig (pac_sim.hpp:63-73). */
+typedef struct spd_sim_config {
+    int32_t num_workers;
+    int32_t num_small_parts;
+    int32_t shuffle;
+    int32_t average;
+    uint64_t batch_size;
+    int32_t epochs;
+    int32_t d;
+    uint64_t model_seed;
+    uint64_t shuffle_seed;
+} spd_sim_config;
+
+/* simulate (pac_sim.hpp:132-133). Per-epoch outputs (caller owned):
+ * recovered[epochs], sync_events[epochs], loops[epochs*W], digests[17*epochs*W]. */
+spd_status spd_simulate(const spd_edge* e, uint64_t n, uint32_t node_count,
+                        const spd_assignment* a, const spd_sim_config* cfg, int32_t device,
+                        uint64_t* recovered, uint64_t* sync_events, uint64_t* loops,
+                        char* digests, uint64_t* total_sync);
+
+/* ---------------------------------------------------- TGN training hot path */
+
+/* Builder-defined TGN step: identity
+ * message, last-message aggregation, GRU memory, 1-layer multi-head temporal
+ * attention over the k most recent neighbours, MergeLayer decoder, BCE, Adam. */
+typedef struct spd_tgn_config {
+    int32_t d_mem;       /* memory / embedding dim (TGN default 100; multiple of 4) */
+    int32_t d_time;      /* time-encoding dim (multiple of 4) */
+    int32_t d_edge;      /* edge-feature dim (0 = no features) */
+    int32_t n_neighbors; /* recent-k */
+    int32_t n_heads;
+    uint64_t batch_size;
+    float lr;
+    float beta1, beta2, adam_eps;
+    uint64_t seed_init;  /* parameter init */
+    uint64_t seed_feat;  /* synthetic edge features */
+    uint64_t seed_neg;   /* negative sampling */
+    int32_t sync_average;/* epoch-end shared-node sync: 1 average (default), 0 max-ts */
+    int32_t gemm_mode;   /* 0 = FP32 FFMA, 1 = tcgen05 BF16 (tolerance-gated) */
+} spd_tgn_config;
+
+typedef struct spd_tgn_trainer spd_tgn_trainer;
+
+/* One trainer owns the workers (partitions) this process trains, one device.
+ * `workers` lists which subgraphs of `subs` it owns; across processes the
+ * lists partition [0, count). world>1 joins an NCCL communicator from
+ * nccl_id (128 bytes from spd_nccl_unique_id) for the per-step gradient
+ * all-reduce and the epoch-end shared-node sync. shared: global ids of SEP's
+ * shared hubs (PartitionAssignment::shared). edge ids in `subs` index the
+ * synthetic feature generator. */
+spd_status spd_tgn_create(const spd_tgn_config* cfg, const spd_subgraphs* subs,
+                          const int32_t* workers, int32_t n_workers, const uint32_t* shared,
+                          uint64_t n_shared, uint32_t node_count, int32_t rank, int32_t world,
+                          const void* nccl_id, int32_t device, spd_tgn_trainer** out);
+void spd_tgn_destroy(spd_tgn_trainer* t);
+spd_status spd_nccl_unique_id(void* out128);
+
+/* Number of lockstep global steps in one epoch = max_w ceil(|E_w| / B) over ALL
+ * workers (run_epoch, pac_sim.cpp:221-234). */
+spd_status spd_tgn_epoch_steps(const spd_tgn_trainer* t, uint64_t* steps);
+/* Begin an epoch: positions to loop start (memory reset, pac_sim.cpp:238). */
+spd_status spd_tgn_begin_epoch(spd_tgn_trainer* t, int32_t epoch);
+/* One global step: every local worker trains one batch, gradients are
+ * all-reduced (mean over all workers), Adam updates. loss_out: per local
+ * worker mean BCE of the batch (device->host read), may be NULL. */
+spd_status spd_tgn_step(spd_tgn_trainer* t, float* loss_out);
+/* Epoch end: restore loop-end snapshots + shared sync (pac_sim.cpp:259-260). */
+spd_status spd_tgn_end_epoch(spd_tgn_trainer* t);
+/* Whole epoch (begin + steps + end). */
+spd_status spd_tgn_run_epoch(spd_tgn_trainer* t, int32_t epoch, double* mean_loss);
+
+/* Score edges (u,v,t) with eids for features against the current memory; no
+ * training; memory is then updated with these events (TGN evaluation). Positive
+ * edges are scored together with one sampled negative each (seed, stream).
+ * Edges are in GLOBAL node ids; `worker` selects the local worker. */
+spd_status spd_tgn_evaluate(spd_tgn_trainer* t, int32_t worker, const spd_edge* e,
+                            const uint64_t* eids, uint64_t n, uint64_t neg_seed,
+                            float* pos_scores, float* neg_scores);
+
+/* Introspection for parity tests. */
+spd_status spd_tgn_param_count(const spd_tgn_trainer* t, uint64_t* n);
+spd_status spd_tgn_get_params(const spd_tgn_trainer* t, float* out);
+spd_status spd_tgn_set_params(spd_tgn_trainer* t, const float* in);
+spd_status spd_tgn_get_grads(const spd_tgn_trainer* t, float* out);
+/* worker-local memory (n_local_nodes x d_mem f32, last_update f64) */
+spd_status spd_tgn_local_nodes(const spd_tgn_trainer* t, int32_t worker, uint64_t* n,
+                               uint32_t* global_ids);
+spd_status spd_tgn_get_memory(const spd_tgn_trainer* t, int32_t worker, float* mem,
+                              double* last_update);
+spd_status spd_tgn_set_memory(spd_tgn_trainer* t, int32_t worker, const float* mem,
+                              const double* last_update);
+/* Debug taps of the last step for worker: embeddings [3B x d_mem] (src,dst,neg),
+ * negatives [B] (global ids), neighbour ids [3B x k] (global, UINT32_MAX = pad). */
+spd_status spd_tgn_last_step(const spd_tgn_trainer* t, int32_t worker, uint64_t* b,
+                             float* emb, uint32_t* negs, uint32_t* nbr_ids, float* loss);
+/* Timing of the last step's dominant kernel (CUDA events on its stream). */
+spd_status spd_tgn_kernel_times(const spd_tgn_trainer* t, float* ms, int32_t* n_kernels,
+                                char* names, int32_t name_stride, int32_t cap);
+
+/* Synthetic edge feature generator (identical on host and device): value of
+ * feature column c of edge eid, BF16-exact. */
+float spd_edge_feature(uint64_t seed, uint64_t eid, uint32_t c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPEED_C_H */

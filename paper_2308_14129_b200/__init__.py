@@ -1,0 +1,601 @@
+"""B200-native SPEED (arXiv 2308.14129) parallel-training hot path.
+
+Python mirror of the reference's C++ API surface (speedpart; names, argument
+meaning and error behaviour follow /root/reference/proj/include/speedpart/*.hpp)
+over the product C-ABI (include/speed_c.h, libspeed_b200.so). Host
+partitioning runs in the library's C++; memory stores, the surrogate parity
+trainer and the TGN training step run on the B200. There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from ._lib import (EDGE_DTYPE, EpochReportC, PartitionerConfigC, SimConfigC, lib, ptr,
+                   u32, u64, i32, f64, f32)
+
+__all__ = [
+    "EDGE_DTYPE", "DataError", "InternalError", "UsageError", "EdgeStream", "ChronoSplit",
+    "gen_powerlaw", "chrono_split", "make_stream", "CentralityTable", "HubSet", "HubBase",
+    "compute_centrality", "compute_degree_centrality", "select_hubs", "PartitionerConfig",
+    "PartitionState", "PartitionAssignment", "score", "partition_stream",
+    "partition_unrestricted", "EvalRouting", "assign_eval_edges", "SubGraph",
+    "induce_subgraphs", "shuffle_combine", "ModelParams", "MemoryStore", "model_update",
+    "SyncStrategy", "sync_shared", "StepLog", "EpochReport", "run_epoch", "SimConfig",
+    "SimReport", "simulate", "kDiscarded",
+]
+
+kDiscarded = -1  # types.hpp:12
+
+
+# --------------------------------------------------------------- errors
+class SpeedError(RuntimeError):
+    def __init__(self, code: str, detail: str):
+        super().__init__(f"{code}: {detail}")
+        self.code = code
+        self.detail = detail
+
+
+class UsageError(SpeedError):
+    pass
+
+
+class DataError(SpeedError):  # errors.hpp:10-20 (CLI exit 2)
+    pass
+
+
+class InternalError(SpeedError):  # errors.hpp:23-32 (CLI exit 3)
+    pass
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    code = (lib.spd_last_error_code() or b"").decode()
+    detail = (lib.spd_last_error_detail() or b"").decode()
+    cls = {1: UsageError, 2: DataError}.get(status, InternalError)
+    raise cls(code, detail)
+
+
+# --------------------------------------------------------------- streams
+@dataclass
+class EdgeStream:
+    """types.hpp:25-32. ``edges`` is a structured array of EDGE_DTYPE."""
+    edges: np.ndarray = field(default_factory=lambda: np.zeros(0, EDGE_DTYPE))
+    node_count: int = 0
+    t_max: float = 0.0
+
+    def empty(self) -> bool:
+        return len(self.edges) == 0
+
+    def size(self) -> int:
+        return len(self.edges)
+
+    def __len__(self) -> int:
+        return len(self.edges)
+
+
+def make_stream(edges: Iterable[tuple], node_count: int) -> EdgeStream:
+    """Test helper (test_pac_sim.cpp:20-26): t_max = max ts."""
+    arr = np.array([tuple(e) for e in edges], dtype=EDGE_DTYPE)
+    t_max = float(arr["ts"].max()) if len(arr) else 0.0
+    return EdgeStream(arr, int(node_count), t_max)
+
+
+def _edges(a) -> np.ndarray:
+    if isinstance(a, EdgeStream):
+        a = a.edges
+    a = np.ascontiguousarray(a, dtype=EDGE_DTYPE)
+    return a
+
+
+def gen_powerlaw(nodes: int, edges: int, alpha: float, seed: int) -> EdgeStream:
+    """graph_io.hpp:34 — bit-identical synthetic power-law TIG."""
+    out = np.empty(int(edges), dtype=EDGE_DTYPE)
+    nc = u32()
+    tm = f64()
+    _check(lib.spd_gen_powerlaw(nodes, edges, alpha, seed, ptr(out), C.byref(nc), C.byref(tm)))
+    return EdgeStream(out, nc.value, tm.value)
+
+
+@dataclass
+class ChronoSplit:  # types.hpp:35-43
+    train: EdgeStream
+    val: EdgeStream
+    test: EdgeStream
+    f_train: float
+    f_val: float
+    f_test: float
+
+
+def _sub(s: EdgeStream, lo: int, hi: int) -> EdgeStream:
+    e = s.edges[lo:hi].copy()
+    return EdgeStream(e, s.node_count, float(e["ts"].max()) if len(e) else 0.0)
+
+
+def chrono_split(s: EdgeStream, f_train: float, f_val: float) -> ChronoSplit:
+    """graph_io.hpp:27."""
+    a, b, c = u64(), u64(), u64()
+    _check(lib.spd_chrono_split(len(s.edges), f_train, f_val, C.byref(a), C.byref(b), C.byref(c)))
+    n_tr, n_va = a.value, b.value
+    return ChronoSplit(_sub(s, 0, n_tr), _sub(s, n_tr, n_tr + n_va), _sub(s, n_tr + n_va, len(s)),
+                       f_train, f_val, 1.0 - f_train - f_val)
+
+
+# ------------------------------------------------------------ centrality
+@dataclass
+class CentralityTable:  # centrality.hpp:13-20
+    cent: np.ndarray
+    beta: float = 0.0
+    t_max: float = 0.0
+
+    def of(self, i: int) -> float:
+        return float(self.cent[i]) if i < len(self.cent) else 0.0
+
+    def active_count(self) -> int:
+        return int((self.cent > 0).sum())
+
+
+class HubBase(enum.IntEnum):  # centrality.hpp:32-35
+    Active = 0
+    All = 1
+
+
+@dataclass
+class HubSet:  # centrality.hpp:22-30
+    hubs: np.ndarray
+    is_hub: np.ndarray
+    k: float = 0.0
+
+    def contains(self, i: int) -> bool:
+        return i < len(self.is_hub) and bool(self.is_hub[i])
+
+    @staticmethod
+    def from_ids(ids: Sequence[int], node_count: int, k: float) -> "HubSet":
+        h = np.array(sorted(int(x) for x in ids), dtype=np.uint32)
+        is_hub = np.zeros(node_count, dtype=np.uint8)
+        is_hub[h] = 1
+        return HubSet(h, is_hub, k)
+
+
+def compute_centrality(s: EdgeStream, beta: float, normalize_ts: bool = True) -> CentralityTable:
+    """centrality.hpp:41 (Eq. 1, order-exact f64 accumulation)."""
+    e = _edges(s)
+    cent = np.zeros(s.node_count, dtype=np.float64)
+    tm = f64()
+    _check(lib.spd_compute_centrality(ptr(e), len(e), s.node_count, s.t_max, beta,
+                                      1 if normalize_ts else 0, ptr(cent, f64), C.byref(tm)))
+    return CentralityTable(cent, beta, tm.value)
+
+
+def compute_degree_centrality(s: EdgeStream) -> CentralityTable:
+    e = _edges(s)
+    cent = np.zeros(s.node_count, dtype=np.float64)
+    _check(lib.spd_compute_degree_centrality(ptr(e), len(e), s.node_count, ptr(cent, f64)))
+    return CentralityTable(cent, 0.0, s.t_max)
+
+
+def select_hubs(c: CentralityTable, k: float, base: HubBase = HubBase.Active) -> HubSet:
+    """centrality.hpp:48."""
+    cent = np.ascontiguousarray(c.cent, dtype=np.float64)
+    hubs = np.zeros(max(1, len(cent)), dtype=np.uint32)
+    n = u64()
+    _check(lib.spd_select_hubs(ptr(cent, f64), len(cent), k, int(base), ptr(hubs, u32), C.byref(n)))
+    return HubSet.from_ids(hubs[: n.value], len(cent), k)
+
+
+# ----------------------------------------------------------- partitioner
+@dataclass
+class PartitionerConfig:  # partitioner.hpp:11-17
+    num_parts: int = 1
+    lambda_: float = 1.0
+    epsilon: float = 1.0
+    hub_set: HubSet | None = None
+    centrality: CentralityTable | None = None
+
+
+@dataclass
+class PartitionState:  # partitioner.hpp:21-36
+    sizes: list
+    assigned: list
+    maxsize: int = 0
+    minsize: int = 0
+
+
+@dataclass
+class PartitionAssignment:  # partitioner.hpp:40-47
+    edge_part: np.ndarray
+    node_parts: list
+    shared: np.ndarray
+    discard_count: int = 0
+    num_parts: int = 1
+    k_eff: float = 0.0
+    np_off: np.ndarray | None = None
+    np_parts: np.ndarray | None = None
+
+    def csr(self):
+        if self.np_off is None:
+            off = np.zeros(len(self.node_parts) + 1, dtype=np.uint64)
+            off[1:] = np.cumsum([len(v) for v in self.node_parts])
+            flat = [p for v in self.node_parts for p in v]
+            self.np_off = off
+            self.np_parts = np.array(flat if flat else [0], dtype=np.int32)
+        return self.np_off, self.np_parts
+
+
+class _CfgHolder:
+    """Keeps numpy buffers alive while a PartitionerConfigC points at them."""
+
+    def __init__(self, cfg: PartitionerConfig, node_count: int):
+        cent = cfg.centrality.cent if cfg.centrality is not None else np.zeros(0)
+        self.cent = np.ascontiguousarray(cent, dtype=np.float64)
+        hubs = cfg.hub_set.hubs if cfg.hub_set is not None else np.zeros(0)
+        self.hubs = np.ascontiguousarray(hubs, dtype=np.uint32)
+        k = cfg.hub_set.k if cfg.hub_set is not None else 0.0
+        self.c = PartitionerConfigC(cfg.num_parts, cfg.lambda_, cfg.epsilon,
+                                    ptr(self.cent, f64) if len(self.cent) else None,
+                                    len(self.cent), ptr(self.hubs, u32) if len(self.hubs) else None,
+                                    len(self.hubs), k)
+
+
+def _assignment_from_handle(h) -> PartitionAssignment:
+    npart, nc, ne, ns, dis, npt = i32(), u32(), u64(), u64(), u64(), u64()
+    keff = f64()
+    _check(lib.spd_assignment_info(h, C.byref(npart), C.byref(nc), C.byref(ne), C.byref(ns),
+                                   C.byref(dis), C.byref(npt), C.byref(keff)))
+    ep = np.empty(ne.value, dtype=np.int32)
+    off = np.empty(nc.value + 1, dtype=np.uint64)
+    parts = np.empty(max(1, npt.value), dtype=np.int32)
+    shared = np.empty(max(1, ns.value), dtype=np.uint32)
+    _check(lib.spd_assignment_edge_part(h, ptr(ep, i32)))
+    _check(lib.spd_assignment_node_parts(h, ptr(off, u64), ptr(parts, i32)))
+    _check(lib.spd_assignment_shared(h, ptr(shared, u32)))
+    lib.spd_assignment_destroy(h)
+    node_parts = [parts[off[i]:off[i + 1]].tolist() for i in range(nc.value)]
+    return PartitionAssignment(ep, node_parts, shared[: ns.value], dis.value, npart.value,
+                               keff.value, off, parts[: npt.value] if npt.value else parts[:0])
+
+
+def _partition(fn, s: EdgeStream, cfg: PartitionerConfig) -> PartitionAssignment:
+    e = _edges(s)
+    holder = _CfgHolder(cfg, s.node_count)
+    h = C.c_void_p()
+    _check(fn(ptr(e), len(e), s.node_count, C.byref(holder.c), C.byref(h)))
+    return _assignment_from_handle(h)
+
+
+def partition_stream(s: EdgeStream, cfg: PartitionerConfig) -> PartitionAssignment:
+    """partitioner.hpp:62 — SEP (Alg. 1), bit-identical assignment."""
+    return _partition(lib.spd_partition_stream, s, cfg)
+
+
+def partition_unrestricted(s: EdgeStream, cfg: PartitionerConfig) -> PartitionAssignment:
+    """partitioner.hpp:66."""
+    return _partition(lib.spd_partition_unrestricted, s, cfg)
+
+
+def score(i: int, j: int, p: int, st: PartitionState, cfg: PartitionerConfig) -> float:
+    """partitioner.hpp:50-51."""
+    n = len(st.assigned)
+    holder = _CfgHolder(cfg, n)
+    sizes = np.array(st.sizes, dtype=np.uint64)
+    off = np.zeros(n + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(v) for v in st.assigned])
+    flat = np.array([q for v in st.assigned for q in v] or [0], dtype=np.int32)
+    out = f64()
+    _check(lib.spd_score(i, j, p, C.byref(holder.c), ptr(sizes, u64), st.maxsize, st.minsize, n,
+                         ptr(off, u64), ptr(flat, i32), C.byref(out)))
+    return out.value
+
+
+def assignment_handle(pa: PartitionAssignment, n_edges: int | None = None):
+    off, parts = pa.csr()
+    off = np.ascontiguousarray(off, dtype=np.uint64)
+    parts = np.ascontiguousarray(parts if len(parts) else np.zeros(1, np.int32), dtype=np.int32)
+    ep = np.ascontiguousarray(pa.edge_part, dtype=np.int32) if pa.edge_part is not None else None
+    h = C.c_void_p()
+    _check(lib.spd_assignment_from_parts(len(off) - 1, pa.num_parts, ptr(off, u64), ptr(parts, i32),
+                                         ptr(ep, i32) if ep is not None and len(ep) else None,
+                                         len(ep) if ep is not None else 0, pa.discard_count,
+                                         C.byref(h)))
+    return h
+
+
+@dataclass
+class EvalRouting:  # partitioner.hpp:74-79
+    val_edges: list
+    test_edges: list
+    val_unroutable: int = 0
+    test_unroutable: int = 0
+
+
+def assign_eval_edges(split: ChronoSplit, pa: PartitionAssignment) -> EvalRouting:
+    """partitioner.hpp:81."""
+    ah = assignment_handle(pa)
+    v, t = _edges(split.val), _edges(split.test)
+    h = C.c_void_p()
+    try:
+        _check(lib.spd_assign_eval_edges(ptr(v), len(v), ptr(t), len(t), ah, C.byref(h)))
+    finally:
+        lib.spd_assignment_destroy(ah)
+    out = []
+    unr = []
+    for which in (0, 1):
+        counts = np.zeros(pa.num_parts, dtype=np.uint64)
+        un = u64()
+        _check(lib.spd_eval_routing_counts(h, which, ptr(counts, u64), C.byref(un)))
+        idx = np.zeros(max(1, int(counts.sum())), dtype=np.uint64)
+        _check(lib.spd_eval_routing_edges(h, which, ptr(idx, u64)))
+        lists, o = [], 0
+        for c in counts:
+            lists.append(idx[o:o + int(c)].tolist())
+            o += int(c)
+        out.append(lists)
+        unr.append(un.value)
+    lib.spd_eval_routing_destroy(h)
+    return EvalRouting(out[0], out[1], unr[0], unr[1])
+
+
+# ------------------------------------------------------------- subgraphs
+@dataclass
+class SubGraph:  # pac_sim.hpp:12-15 (+ stream positions for feature lookup)
+    nodes: np.ndarray
+    edges: np.ndarray
+    eids: np.ndarray
+
+
+def _subgraphs_from_handle(h) -> list:
+    cnt = i32()
+    _check(lib.spd_subgraphs_count(h, C.byref(cnt)))
+    subs = []
+    for p in range(cnt.value):
+        nn, ne = u64(), u64()
+        _check(lib.spd_subgraph_sizes(h, p, C.byref(nn), C.byref(ne)))
+        nodes = np.empty(nn.value, dtype=np.uint32)
+        edges = np.empty(ne.value, dtype=EDGE_DTYPE)
+        eids = np.empty(ne.value, dtype=np.uint64)
+        if nn.value:
+            _check(lib.spd_subgraph_nodes(h, p, ptr(nodes, u32)))
+        if ne.value:
+            _check(lib.spd_subgraph_edges(h, p, ptr(edges), ptr(eids, u64)))
+        subs.append(SubGraph(nodes, edges, eids))
+    return subs
+
+
+def induce_subgraphs(s: EdgeStream, node_parts, num_parts: int) -> list:
+    """pac_sim.hpp:102-104."""
+    e = _edges(s)
+    off = np.zeros(len(node_parts) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(v) for v in node_parts])
+    flat = np.array([p for v in node_parts for p in v] or [0], dtype=np.int32)
+    h = C.c_void_p()
+    _check(lib.spd_induce_subgraphs(ptr(e), len(e), s.node_count, ptr(off, u64), ptr(flat, i32),
+                                    len(node_parts), num_parts, C.byref(h)))
+    try:
+        return _subgraphs_from_handle(h)
+    finally:
+        lib.spd_subgraphs_destroy(h)
+
+
+def subgraphs_handle(subs: Sequence[SubGraph]):
+    """Opaque spd_subgraphs* for a list of SubGraph (caller destroys)."""
+    n = len(subs)
+    no = np.zeros(n + 1, dtype=np.uint64)
+    eo = np.zeros(n + 1, dtype=np.uint64)
+    no[1:] = np.cumsum([len(g.nodes) for g in subs])
+    eo[1:] = np.cumsum([len(g.edges) for g in subs])
+    nodes = np.concatenate([np.asarray(g.nodes, np.uint32) for g in subs] + [np.zeros(1, np.uint32)])
+    edges = np.concatenate([_edges(g.edges) for g in subs] + [np.zeros(1, EDGE_DTYPE)])
+    eids = np.concatenate([np.asarray(g.eids if g.eids is not None else np.arange(len(g.edges)),
+                                      np.uint64) for g in subs] + [np.zeros(1, np.uint64)])
+    h = C.c_void_p()
+    _check(lib.spd_subgraphs_from_lists(n, ptr(no, u64), ptr(nodes, u32), ptr(eo, u64), ptr(edges),
+                                        ptr(eids, u64), C.byref(h)))
+    return h
+
+
+def shuffle_combine(small: Sequence[Sequence[int]], num_workers: int, epoch_seed: int) -> list:
+    """pac_sim.hpp:108-110."""
+    off = np.zeros(len(small) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(v) for v in small])
+    flat = np.array([x for v in small for x in v] or [0], dtype=np.uint32)
+    out_off = np.zeros(max(1, num_workers) + 1, dtype=np.uint64)
+    out = np.zeros(max(1, len(flat)), dtype=np.uint32)
+    _check(lib.spd_shuffle_combine(ptr(off, u64), ptr(flat, u32), len(small), num_workers,
+                                   epoch_seed, ptr(out_off, u64), ptr(out, u32)))
+    return [out[out_off[g]:out_off[g + 1]].tolist() for g in range(num_workers)]
+
+
+# ------------------------------------------------- surrogate (parity mode)
+@dataclass
+class ModelParams:  # pac_sim.hpp:47-55
+    d: int = 8
+    gamma: float = 0.5
+    w_m: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    omega: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+    @staticmethod
+    def seeded(d: int, seed: int) -> "ModelParams":
+        w = np.zeros(max(1, d * 3 * d), dtype=np.float64)
+        om = np.zeros(max(1, d), dtype=np.float64)
+        g = f64()
+        _check(lib.spd_model_seeded(d, seed, ptr(w, f64), ptr(om, f64), C.byref(g)))
+        return ModelParams(d, g.value, w, om)
+
+
+class MemoryStore:
+    """pac_sim.hpp:19-39, resident in HBM of `device` (f64 rows + f64 clock)."""
+
+    def __init__(self, node_count: int, d: int, device: int = 0):
+        self.node_count = int(node_count)
+        self.d = int(d)
+        self.device = device
+        self._h = C.c_void_p()
+        _check(lib.spd_memstore_create(self.node_count, self.d, device, C.byref(self._h)))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.spd_memstore_destroy(h)
+            self._h = None
+
+    def download(self):
+        st = np.zeros(self.node_count * self.d, dtype=np.float64)
+        ts = np.zeros(self.node_count, dtype=np.float64)
+        _check(lib.spd_memstore_download(self._h, ptr(st, f64), ptr(ts, f64)))
+        return st.reshape(self.node_count, self.d), ts
+
+    def upload(self, state, last_ts):
+        st = np.ascontiguousarray(state, dtype=np.float64).reshape(-1)
+        ts = np.ascontiguousarray(last_ts, dtype=np.float64)
+        _check(lib.spd_memstore_upload(self._h, ptr(st, f64), ptr(ts, f64)))
+
+    @property
+    def state(self) -> np.ndarray:
+        return self.download()[0]
+
+    @property
+    def last_ts(self) -> np.ndarray:
+        return self.download()[1]
+
+    def row(self, i: int) -> np.ndarray:
+        return self.state[i]
+
+    def reset(self):
+        _check(lib.spd_memstore_reset(self._h))
+
+    def copy_from(self, other: "MemoryStore"):
+        _check(lib.spd_memstore_copy(self._h, other._h))
+
+    def digest(self) -> str:
+        buf = C.create_string_buffer(17)
+        _check(lib.spd_memstore_digest(self._h, buf))
+        return buf.value.decode()
+
+
+def model_update(mem: MemoryStore, edges, model: ModelParams) -> None:
+    """pac_sim.hpp:59, for one edge or a run of edges (applied in order)."""
+    if isinstance(edges, tuple):
+        edges = [edges]
+    e = np.array([tuple(x) for x in edges], dtype=EDGE_DTYPE) if isinstance(edges, list) else _edges(edges)
+    w = np.ascontiguousarray(model.w_m, dtype=np.float64)
+    om = np.ascontiguousarray(model.omega, dtype=np.float64)
+    _check(lib.spd_model_update(mem._h, ptr(e), len(e), ptr(w, f64), ptr(om, f64), model.gamma))
+
+
+class SyncStrategy(enum.IntEnum):  # pac_sim.hpp:61
+    MaxTimestamp = 0
+    Average = 1
+
+
+def sync_shared(mems: Sequence[MemoryStore], shared, strategy: SyncStrategy) -> None:
+    """pac_sim.hpp:125-126."""
+    arr = (C.c_void_p * max(1, len(mems)))(*[m._h for m in mems])
+    sh = np.ascontiguousarray(np.asarray(list(shared), dtype=np.uint32))
+    _check(lib.spd_sync_shared(arr, len(mems), ptr(sh, u32) if len(sh) else None, len(sh),
+                               int(strategy)))
+
+
+@dataclass
+class StepLog:  # pac_sim.hpp:88-100
+    steps: list = field(default_factory=list)      # (global_step, worker, loop, batch_in_loop)
+    snapshots: list = field(default_factory=list)  # (worker, digest)
+
+
+@dataclass
+class EpochReport:  # pac_sim.hpp:75-81
+    batches: list
+    loops: list
+    recovered: int = 0
+    sync_events: int = 0
+    digests: list = field(default_factory=list)
+
+
+def run_epoch(subgraphs: Sequence[SubGraph], mems: Sequence[MemoryStore], model: ModelParams,
+              shared, sync: SyncStrategy, batch_size: int, log: StepLog | None = None) -> EpochReport:
+    """pac_sim.hpp:117-120 — lockstep loop-within-epoch on device memory stores."""
+    W = len(subgraphs)
+    if len(mems) != W:
+        raise DataError("ConfigMismatch", "one memory store per worker required")
+    h = subgraphs_handle(subgraphs)
+    try:
+        arr = (C.c_void_p * max(1, W))(*[m._h for m in mems])
+        sh = np.ascontiguousarray(np.asarray(list(shared), dtype=np.uint32))
+        batches = np.zeros(max(1, W), dtype=np.uint64)
+        loops = np.zeros(max(1, W), dtype=np.uint64)
+        digests = C.create_string_buffer(17 * max(1, W))
+        rep = EpochReportC()
+        rep.batches = ptr(batches, u64)
+        rep.loops = ptr(loops, u64)
+        rep.digests = C.cast(digests, C.c_void_p)
+        if log is not None:
+            cap = 1 << 16
+            steps = np.zeros(4 * cap, dtype=np.uint64)
+            snap_w = np.zeros(cap, dtype=np.int32)
+            snap_d = C.create_string_buffer(17 * cap)
+            rep.log_cap = cap
+            rep.log_steps = ptr(steps, u64)
+            rep.snap_worker = ptr(snap_w, i32)
+            rep.snap_digests = C.cast(snap_d, C.c_void_p)
+        w = np.ascontiguousarray(model.w_m, dtype=np.float64)
+        om = np.ascontiguousarray(model.omega, dtype=np.float64)
+        _check(lib.spd_run_epoch(h, arr, W, ptr(w, f64), ptr(om, f64), model.gamma,
+                                 ptr(sh, u32) if len(sh) else None, len(sh), int(sync), batch_size,
+                                 C.byref(rep)))
+    finally:
+        lib.spd_subgraphs_destroy(h)
+    if log is not None:
+        for k in range(rep.n_log):
+            log.steps.append(tuple(int(x) for x in steps[4 * k:4 * k + 4]))
+        for k in range(rep.n_snap):
+            log.snapshots.append((int(snap_w[k]), snap_d.raw[17 * k:17 * k + 16].decode()))
+    dg = [digests.raw[17 * w:17 * w + 16].decode() for w in range(W)]
+    return EpochReport(batches[:W].tolist(), loops[:W].tolist(), 0, rep.sync_events, dg)
+
+
+@dataclass
+class SimConfig:  # pac_sim.hpp:63-73
+    num_workers: int = 1
+    num_small_parts: int = 1
+    shuffle: bool = False
+    sync: SyncStrategy = SyncStrategy.MaxTimestamp
+    batch_size: int = 1
+    epochs: int = 1
+    d: int = 8
+    model_seed: int = 0
+    shuffle_seed: int = 0
+
+
+@dataclass
+class SimReport:  # pac_sim.hpp:83-86
+    epochs: list
+    sync_events: int = 0
+
+
+def simulate(s: EdgeStream, pa: PartitionAssignment, cfg: SimConfig, device: int = 0) -> SimReport:
+    """pac_sim.hpp:132-133."""
+    e = _edges(s)
+    ah = assignment_handle(pa)
+    E = max(1, cfg.epochs)
+    W = max(1, cfg.num_workers)
+    rec = np.zeros(E, np.uint64)
+    syn = np.zeros(E, np.uint64)
+    loops = np.zeros(E * W, np.uint64)
+    dg = C.create_string_buffer(17 * E * W)
+    tot = u64()
+    c = SimConfigC(cfg.num_workers, cfg.num_small_parts, int(cfg.shuffle), int(cfg.sync),
+                   cfg.batch_size, cfg.epochs, cfg.d, cfg.model_seed, cfg.shuffle_seed)
+    try:
+        _check(lib.spd_simulate(ptr(e), len(e), s.node_count, ah, C.byref(c), device, ptr(rec, u64),
+                                ptr(syn, u64), ptr(loops, u64), C.cast(dg, C.c_void_p), C.byref(tot)))
+    finally:
+        lib.spd_assignment_destroy(ah)
+    eps = []
+    for ep in range(cfg.epochs):
+        digs = [dg.raw[17 * (ep * W + w):17 * (ep * W + w) + 16].decode() for w in range(W)]
+        eps.append(EpochReport([], loops[ep * W:(ep + 1) * W].tolist(), int(rec[ep]), int(syn[ep]), digs))
+    return SimReport(eps, tot.value)
