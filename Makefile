@@ -29,7 +29,7 @@ $(OBJ)/%.cu.o: $(SRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJ)/$*.ptxas.txt || (cat $(OBJ)/$*.ptxas.txt; false)
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static -L/usr/lib/x86_64-linux-gnu -lnccl -lpthread
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -cudart static -ldl -lpthread
 
 oracle:
 	$(MAKE) -C oracle all

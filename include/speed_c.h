@@ -299,9 +299,34 @@ spd_status spd_tgn_set_memory(spd_tgn_trainer* t, int32_t worker, const float* m
  * negatives [B] (global ids), neighbour ids [3B x k] (global, UINT32_MAX = pad). */
 spd_status spd_tgn_last_step(const spd_tgn_trainer* t, int32_t worker, uint64_t* b,
                              float* emb, uint32_t* negs, uint32_t* nbr_ids, float* loss);
-/* Timing of the last step's dominant kernel (CUDA events on its stream). */
+/* Debug taps (spd_tgn_last_step) and per-phase CUDA-event timing of each step
+ * (spd_tgn_kernel_times); both add synchronisation, off by default. */
+spd_status spd_tgn_set_debug(spd_tgn_trainer* t, int32_t on);
+spd_status spd_tgn_set_profile(spd_tgn_trainer* t, int32_t on);
+/* Per-phase times (ms, CUDA events on the trainer's stream) of the last step. */
 spd_status spd_tgn_kernel_times(const spd_tgn_trainer* t, float* ms, int32_t* n_kernels,
                                 char* names, int32_t name_stride, int32_t cap);
+
+/* n global steps (wrapping epochs) timed with CUDA events on the trainer's
+ * stream; device_ms = elapsed device time. */
+spd_status spd_tgn_run_steps(spd_tgn_trainer* t, uint64_t n, float* device_ms);
+/* End-to-end step from host memory: events[k] / feats[k] hold local worker k's
+ * NEXT batch (events in that worker's local ids, spd_tgn_worker_events; bf16
+ * feature rows of stride feat_stride) — copied H2D, trained, losses copied back. */
+spd_status spd_tgn_step_host(spd_tgn_trainer* t, const spd_edge* const* events,
+                             const uint16_t* const* feats, float* loss_out);
+/* Event range [lo, hi) of worker's next batch in its local stream. */
+spd_status spd_tgn_next_batch(const spd_tgn_trainer* t, int32_t worker, uint64_t* lo,
+                              uint64_t* hi, int32_t* feat_stride);
+spd_status spd_tgn_worker_events(const spd_tgn_trainer* t, int32_t worker, spd_edge* out);
+/* Host<->device bytes moved by spd_tgn_step_host so far. */
+spd_status spd_tgn_io_bytes(const spd_tgn_trainer* t, uint64_t* h2d, uint64_t* d2h);
+/* Host copy of the synthetic bf16 feature rows (row stride `stride`, pad 0) of
+ * edges eids[0..n): the bytes spd_tgn_step_host expects. */
+spd_status spd_edge_features_bf16(uint64_t seed, const uint64_t* eids, uint64_t n, int32_t F,
+                                  int32_t stride, uint16_t* out);
+/* Process-wide count of kernel launches issued by the TGN path. */
+uint64_t spd_kernel_launches(void);
 
 /* Synthetic edge feature generator (identical on host and device): value of
  * feature column c of edge eid, BF16-exact. */

@@ -599,3 +599,233 @@ def simulate(s: EdgeStream, pa: PartitionAssignment, cfg: SimConfig, device: int
         digs = [dg.raw[17 * (ep * W + w):17 * (ep * W + w) + 16].decode() for w in range(W)]
         eps.append(EpochReport([], loops[ep * W:(ep + 1) * W].tolist(), int(rec[ep]), int(syn[ep]), digs))
     return SimReport(eps, tot.value)
+
+
+# ------------------------------------------------------ TGN training path
+from ._lib import TGNConfigC  # noqa: E402
+
+
+@dataclass
+class TGNConfig:
+    """spd_tgn_config (include/speed_c.h). Defaults: TGN paper dims."""
+    d_mem: int = 100
+    d_time: int = 100
+    d_edge: int = 172
+    n_neighbors: int = 10
+    n_heads: int = 2
+    batch_size: int = 200
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    seed_init: int = 3
+    seed_feat: int = 2
+    seed_neg: int = 4
+    sync_average: int = 1
+    gemm_mode: int = 0
+
+    def c(self) -> TGNConfigC:
+        return TGNConfigC(self.d_mem, self.d_time, self.d_edge, self.n_neighbors, self.n_heads,
+                          self.batch_size, self.lr, self.beta1, self.beta2, self.adam_eps,
+                          self.seed_init, self.seed_feat, self.seed_neg, self.sync_average,
+                          self.gemm_mode)
+
+
+def _prefer_loaded_nccl():
+    """Load torch's bundled libnccl first when torch is present, so the
+    library's dlopen(RTLD_NOLOAD) reuses it instead of a second copy."""
+    try:
+        import torch  # noqa: F401
+        import torch.distributed  # noqa: F401
+    except Exception:
+        pass
+
+
+def nccl_unique_id() -> bytes:
+    _prefer_loaded_nccl()
+    buf = C.create_string_buffer(128)
+    _check(lib.spd_nccl_unique_id(buf))
+    return buf.raw
+
+
+class TGNTrainer:
+    """Per-process TGN trainer over the SEP partitions `workers` (default: all)
+    of `subgraphs`, on `device`; world>1 joins an NCCL communicator."""
+
+    def __init__(self, cfg: TGNConfig, subgraphs: Sequence[SubGraph], workers=None, shared=(),
+                 node_count: int | None = None, rank: int = 0, world: int = 1,
+                 nccl_id: bytes | None = None, device: int = 0):
+        self.cfg = cfg
+        if world > 1:
+            _prefer_loaded_nccl()
+        self.workers = list(range(len(subgraphs))) if workers is None else list(workers)
+        if node_count is None:
+            node_count = int(max([int(g.nodes.max()) + 1 for g in subgraphs if len(g.nodes)] + [0]))
+        self._events_per_worker = {w: len(subgraphs[w].edges) for w in self.workers}
+        sh = subgraphs_handle(subgraphs)
+        try:
+            ws = np.array(self.workers or [0], np.int32)
+            shared = np.ascontiguousarray(np.asarray(list(shared), np.uint32))
+            self._c = cfg.c()
+            self._h = C.c_void_p()
+            idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+            _check(lib.spd_tgn_create(C.byref(self._c), sh, ptr(ws, i32), len(self.workers),
+                                      ptr(shared, u32) if len(shared) else None, len(shared),
+                                      node_count, rank, world, idbuf, device, C.byref(self._h)))
+        finally:
+            lib.spd_subgraphs_destroy(sh)
+        n = u64()
+        _check(lib.spd_tgn_param_count(self._h, C.byref(n)))
+        self.n_params = n.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.spd_tgn_destroy(h)
+            self._h = None
+
+    def close(self):
+        self.__del__()
+
+    def epoch_steps(self) -> int:
+        n = u64()
+        _check(lib.spd_tgn_epoch_steps(self._h, C.byref(n)))
+        return n.value
+
+    def begin_epoch(self, epoch: int):
+        _check(lib.spd_tgn_begin_epoch(self._h, epoch))
+
+    def step(self, want_loss: bool = True):
+        if not want_loss:
+            _check(lib.spd_tgn_step(self._h, None))
+            return None
+        out = np.zeros(max(1, len(self.workers)), np.float32)
+        _check(lib.spd_tgn_step(self._h, ptr(out, f32)))
+        return out[: len(self.workers)]
+
+    def end_epoch(self):
+        _check(lib.spd_tgn_end_epoch(self._h))
+
+    def run_epoch(self, epoch: int) -> float:
+        m = f64()
+        _check(lib.spd_tgn_run_epoch(self._h, epoch, C.byref(m)))
+        return m.value
+
+    def params(self) -> np.ndarray:
+        out = np.zeros(self.n_params, np.float32)
+        _check(lib.spd_tgn_get_params(self._h, ptr(out, f32)))
+        return out
+
+    def set_params(self, p):
+        p = np.ascontiguousarray(p, np.float32)
+        _check(lib.spd_tgn_set_params(self._h, ptr(p, f32)))
+
+    def grads(self) -> np.ndarray:
+        out = np.zeros(self.n_params, np.float32)
+        _check(lib.spd_tgn_get_grads(self._h, ptr(out, f32)))
+        return out
+
+    def local_nodes(self, w: int) -> np.ndarray:
+        n = u64()
+        _check(lib.spd_tgn_local_nodes(self._h, w, C.byref(n), None))
+        out = np.zeros(max(1, n.value), np.uint32)
+        _check(lib.spd_tgn_local_nodes(self._h, w, C.byref(n), ptr(out, u32)))
+        return out[: n.value]
+
+    def memory(self, w: int):
+        n = len(self.local_nodes(w))
+        mem = np.zeros(max(1, n * self.cfg.d_mem), np.float32)
+        lu = np.zeros(max(1, n), np.float64)
+        _check(lib.spd_tgn_get_memory(self._h, w, ptr(mem, f32), ptr(lu, f64)))
+        return mem[: n * self.cfg.d_mem].reshape(n, self.cfg.d_mem), lu[:n]
+
+    def set_memory(self, w: int, mem, lu):
+        mem = np.ascontiguousarray(mem, np.float32)
+        lu = np.ascontiguousarray(lu, np.float64)
+        _check(lib.spd_tgn_set_memory(self._h, w, ptr(mem, f32), ptr(lu, f64)))
+
+    def set_debug(self, on: bool = True):
+        _check(lib.spd_tgn_set_debug(self._h, int(on)))
+
+    def set_profile(self, on: bool = True):
+        _check(lib.spd_tgn_set_profile(self._h, int(on)))
+
+    def last_step(self, w: int):
+        b = u64()
+        cfg = self.cfg
+        B = cfg.batch_size
+        emb = np.zeros(3 * B * cfg.d_mem, np.float32)
+        negs = np.zeros(B, np.uint32)
+        nbr = np.zeros(3 * B * cfg.n_neighbors, np.uint32)
+        loss = f32()
+        _check(lib.spd_tgn_last_step(self._h, w, C.byref(b), ptr(emb, f32), ptr(negs, u32),
+                                     ptr(nbr, u32), C.byref(loss)))
+        n = b.value
+        return dict(b=n, emb=emb[: 3 * n * cfg.d_mem].reshape(3 * n, cfg.d_mem), neg=negs[:n],
+                    nbr=nbr[: 3 * n * cfg.n_neighbors].reshape(3 * n, cfg.n_neighbors),
+                    loss=loss.value)
+
+    def run_steps(self, n: int) -> float:
+        """n lockstep steps timed on the trainer's stream (device ms)."""
+        ms = f32()
+        _check(lib.spd_tgn_run_steps(self._h, n, C.byref(ms)))
+        return ms.value
+
+    def next_batch(self, w: int):
+        lo, hi = u64(), u64()
+        fs = i32()
+        _check(lib.spd_tgn_next_batch(self._h, w, C.byref(lo), C.byref(hi), C.byref(fs)))
+        return lo.value, hi.value, fs.value
+
+    def worker_events(self, w: int) -> np.ndarray:
+        n = len(self.local_nodes(w))  # noqa: F841 (validates the worker id)
+        lo, hi, _ = self.next_batch(w)
+        cnt = u64()
+        # size from the subgraph: total events = epoch batches * B upper bound; ask C side
+        out = np.zeros(self._n_events(w), EDGE_DTYPE)
+        _check(lib.spd_tgn_worker_events(self._h, w, ptr(out)))
+        return out
+
+    def _n_events(self, w: int) -> int:
+        return self._events_per_worker[w]
+
+    def step_host(self, events: list, feats: list | None) -> np.ndarray:
+        """End-to-end step: per local worker, its next batch's events (local ids)
+        and bf16 feature rows (uint16) in host memory (pin them for async H2D)."""
+        ev = (C.c_void_p * len(events))(*[e.ctypes.data for e in events])
+        ft = (C.c_void_p * len(events))(*[f.ctypes.data for f in feats]) if feats else None
+        out = np.zeros(max(1, len(self.workers)), np.float32)
+        _check(lib.spd_tgn_step_host(self._h, ev, ft, ptr(out, f32)))
+        return out[: len(self.workers)]
+
+    def io_bytes(self):
+        a, b = u64(), u64()
+        _check(lib.spd_tgn_io_bytes(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def kernel_times(self):
+        cap, stride = 256, 48
+        ms = np.zeros(cap, np.float32)
+        n = i32()
+        names = C.create_string_buffer(cap * stride)
+        _check(lib.spd_tgn_kernel_times(self._h, ptr(ms, f32), C.byref(n), names, stride, cap))
+        return [(names.raw[k * stride:(k + 1) * stride].split(b"\0")[0].decode(), float(ms[k]))
+                for k in range(n.value)]
+
+
+def kernel_launches() -> int:
+    """Process-wide count of kernels the TGN path has launched."""
+    return int(lib.spd_kernel_launches())
+
+
+def edge_features_bf16(seed: int, eids: np.ndarray, F: int, stride: int, out=None) -> np.ndarray:
+    """Host bf16 bits (uint16) of the synthetic feature rows of `eids`."""
+    eids = np.ascontiguousarray(eids, np.uint64)
+    if out is None:
+        out = np.zeros((len(eids), stride), np.uint16)
+    _check(lib.spd_edge_features_bf16(seed, ptr(eids, u64), len(eids), F, stride, ptr(out)))
+    return out
+
+
+def edge_feature(seed: int, eid: int, c: int) -> float:
+    return float(lib.spd_edge_feature(seed, eid, c))

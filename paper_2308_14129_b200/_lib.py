@@ -117,6 +117,15 @@ _SIGS = {
     "spd_tgn_set_memory": (i32, [P, i32, pf32, pf64]),
     "spd_tgn_last_step": (i32, [P, i32, pu64, pf32, pu32, pu32, pf32]),
     "spd_tgn_kernel_times": (i32, [P, pf32, pi32, P, i32, i32]),
+    "spd_tgn_run_steps": (i32, [P, u64, pf32]),
+    "spd_tgn_step_host": (i32, [P, PP, PP, pf32]),
+    "spd_tgn_next_batch": (i32, [P, i32, pu64, pu64, pi32]),
+    "spd_tgn_worker_events": (i32, [P, i32, P]),
+    "spd_tgn_io_bytes": (i32, [P, pu64, pu64]),
+    "spd_kernel_launches": (u64, []),
+    "spd_edge_features_bf16": (i32, [u64, pu64, u64, i32, i32, P]),
+    "spd_tgn_set_debug": (i32, [P, i32]),
+    "spd_tgn_set_profile": (i32, [P, i32]),
     "spd_edge_feature": (f32, [u64, u64, u32]),
 }
 

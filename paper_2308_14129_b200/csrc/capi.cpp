@@ -7,6 +7,7 @@
 #include <memory>
 #include <string>
 
+#include "capi_types.hpp"
 #include "host.hpp"
 #include "surrogate.hpp"
 
@@ -16,10 +17,6 @@ namespace {
 thread_local std::string g_code;
 thread_local std::string g_detail;
 }  // namespace
-
-namespace spd {
-int guarded_call(const std::function<void()>& f);
-}
 
 int spd::guarded_call(const std::function<void()>& f) {
     try {
@@ -42,17 +39,6 @@ int spd::guarded_call(const std::function<void()>& f) {
     }
 }
 
-#define GUARD(...) return spd::guarded_call([&]() __VA_ARGS__)
-
-struct spd_assignment {
-    Assignment a;
-};
-struct spd_eval_routing {
-    EvalRouting r;
-};
-struct spd_subgraphs {
-    SubGraphs s;
-};
 struct spd_memstore {
     std::unique_ptr<MemStore> m;
 };

@@ -1,0 +1,223 @@
+// FP32 FFMA tiled GEMM for sm_100a (the tolerance-safe path; SURVEY K4/K6
+// "otherwise use FP32 FFMA"). One kernel template covers the three
+// orientations a hand-written backward needs:
+//
+//   fwd        C[M,N]  = A[M,K]   . B[N,K]^T      (A row-major, B row-major)
+//   data grad  C[M,N]  = A[M,K]   . B[K,N]        (B row-major)
+//   weight grad C[M,N] += A[K,M]^T . B[K,N]       (reduction over K = rows, split-K)
+//
+// Every linear layer stores its bias as an extra weight column (augmented
+// [W | b]) and every activation matrix carries a constant-1 column, so the
+// bias gradient falls out of the weight-gradient GEMM. All leading dimensions
+// are multiples of 4 floats and allocations are padded to them, so 128-bit
+// loads along the contiguous dimension are always in bounds; only the
+// reduction index is predicated (rows past a device-resident count read 0).
+//
+// Tile 128x64x16, 256 threads, 8x4 outputs per thread, register-staged
+// double buffering through shared memory.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace spd {
+namespace gemm {
+
+constexpr int BM = 128, BN = 64, BK = 16, NT = 256;
+constexpr int TM = 8, TN = 4;
+
+enum Epi : int { EPI_NONE = 0, EPI_RELU = 1, EPI_MASK = 2 /* C *= (mask > 0) */ };
+
+struct Args {
+    const float* A;
+    const float* B;
+    float* C;
+    int M, N, K;
+    int lda, ldb, ldc;
+    const int* M_dev;  // optional device-resident row count (min with M)
+    const int* K_dev;  // optional device-resident reduction count (TN mode)
+    float beta;        // 0: overwrite, 1: accumulate
+    int epi;
+    const float* mask;  // EPI_MASK: same shape/ld as C
+    int ldmask;
+    // split-K for the weight-gradient orientation
+    int k_split;        // number of K slices (gridDim.z)
+    float* workspace;   // [k_split][M][N] partials (ld = N4)
+    int ldw;
+};
+
+// A_KMAJOR: A stored [K x M] (weight-grad orientation). B_KN: B stored [K x N].
+template <bool A_KMAJOR, bool B_KN>
+__global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
+    __shared__ __align__(16) float As[2][BK][BM + 4];
+    __shared__ __align__(16) float Bs[2][BK][BN + 4];
+    int M = a.M;
+    if (a.M_dev) M = min(M, *a.M_dev);
+    int K = a.K;
+    if (a.K_dev) K = min(K, *a.K_dev);
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    if (!A_KMAJOR && m0 >= M) return;
+    if (n0 >= a.N) return;
+    if (A_KMAJOR && m0 >= a.M) return;
+    // K range of this split
+    int k_begin = 0, k_end = K;
+    if (a.k_split > 1) {
+        const int per = ((K + a.k_split - 1) / a.k_split + BK - 1) / BK * BK;
+        k_begin = blockIdx.z * per;
+        k_end = min(K, k_begin + per);
+    }
+    const int tid = threadIdx.x;
+    const int tx = tid % 16, ty = tid / 16;  // 16 x 16 thread grid; outputs (ty*8.., tx*4..)
+
+    float acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+
+    // register staging: A tile 128x16 = 2048 floats = 2 float4 / thread;
+    // B tile 16x64 = 1024 floats = 1 float4 / thread.
+    float4 ra[2], rb;
+    auto load_tiles = [&](int k0) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int idx = tid + r * NT;  // 0..511
+            if (!A_KMAJOR) {
+                // A row-major [M x lda]: 128 rows x 16 k -> 4 float4 per row
+                const int row = idx / 4, kq = (idx % 4) * 4;
+                const int gm = m0 + row, gk = k0 + kq;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (gm < a.M && gk < k_end) v = *reinterpret_cast<const float4*>(a.A + (size_t)gm * a.lda + gk);
+                if (gk + 3 >= k_end) {  // zero lanes past the reduction end
+                    if (gk + 0 >= k_end) v.x = 0.f;
+                    if (gk + 1 >= k_end) v.y = 0.f;
+                    if (gk + 2 >= k_end) v.z = 0.f;
+                    if (gk + 3 >= k_end) v.w = 0.f;
+                }
+                ra[r] = v;
+            } else {
+                // A stored [K x lda] (rows = reduction): 16 rows x 128 m -> 32 float4 per row
+                const int kr = idx / 32, mq = (idx % 32) * 4;
+                const int gk = k0 + kr, gm = m0 + mq;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (gk < k_end && gm < a.M) v = *reinterpret_cast<const float4*>(a.A + (size_t)gk * a.lda + gm);
+                ra[r] = v;
+            }
+        }
+        {
+            if (B_KN) {
+                // B [K x ldb]: 16 rows x 64 n -> 16 float4 per row
+                const int kr = tid / 16, nq = (tid % 16) * 4;
+                const int gk = k0 + kr, gn = n0 + nq;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (gk < k_end && gn < a.N) v = *reinterpret_cast<const float4*>(a.B + (size_t)gk * a.ldb + gn);
+                rb = v;
+            } else {
+                // B [N x ldb] row-major: 64 rows x 16 k -> 4 float4 per row
+                const int row = tid / 4, kq = (tid % 4) * 4;
+                const int gn = n0 + row, gk = k0 + kq;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (gn < a.N && gk < k_end) v = *reinterpret_cast<const float4*>(a.B + (size_t)gn * a.ldb + gk);
+                if (gk + 3 >= k_end) {
+                    if (gk + 0 >= k_end) v.x = 0.f;
+                    if (gk + 1 >= k_end) v.y = 0.f;
+                    if (gk + 2 >= k_end) v.z = 0.f;
+                    if (gk + 3 >= k_end) v.w = 0.f;
+                }
+                rb = v;
+            }
+        }
+    };
+    auto store_tiles = [&](int buf) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int idx = tid + r * NT;
+            if (!A_KMAJOR) {
+                const int row = idx / 4, kq = (idx % 4) * 4;
+                As[buf][kq + 0][row] = ra[r].x;
+                As[buf][kq + 1][row] = ra[r].y;
+                As[buf][kq + 2][row] = ra[r].z;
+                As[buf][kq + 3][row] = ra[r].w;
+            } else {
+                const int kr = idx / 32, mq = (idx % 32) * 4;
+                *reinterpret_cast<float4*>(&As[buf][kr][mq]) = ra[r];
+            }
+        }
+        if (B_KN) {
+            const int kr = tid / 16, nq = (tid % 16) * 4;
+            *reinterpret_cast<float4*>(&Bs[buf][kr][nq]) = rb;
+        } else {
+            const int row = tid / 4, kq = (tid % 4) * 4;
+            Bs[buf][kq + 0][row] = rb.x;
+            Bs[buf][kq + 1][row] = rb.y;
+            Bs[buf][kq + 2][row] = rb.z;
+            Bs[buf][kq + 3][row] = rb.w;
+        }
+    };
+
+    if (k_begin < k_end) {
+        load_tiles(k_begin);
+        store_tiles(0);
+        __syncthreads();
+        int buf = 0;
+        for (int k0 = k_begin; k0 < k_end; k0 += BK) {
+            const bool more = k0 + BK < k_end;
+            if (more) load_tiles(k0 + BK);
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+                const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8]);
+                const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8 + 4]);
+                const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+                const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                const float bv[4] = {b0.x, b0.y, b0.z, b0.w};
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+            }
+            if (more) {
+                store_tiles(buf ^ 1);
+                __syncthreads();
+                buf ^= 1;
+            }
+        }
+    }
+
+    // epilogue
+    const int Mlim = A_KMAJOR ? a.M : M;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int gm = m0 + ty * 8 + i;
+        if (gm >= Mlim) continue;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            const int gn = n0 + tx * 4 + j;
+            if (gn >= a.N) continue;
+            float v = acc[i][j];
+            if (a.k_split > 1) {
+                a.workspace[((size_t)blockIdx.z * a.M + gm) * a.ldw + gn] = v;
+                continue;
+            }
+            if (a.epi == EPI_RELU) v = fmaxf(v, 0.f);
+            if (a.epi == EPI_MASK) v = a.mask[(size_t)gm * a.ldmask + gn] > 0.f ? v : 0.f;
+            float* c = a.C + (size_t)gm * a.ldc + gn;
+            *c = a.beta != 0.f ? *c + v : v;
+        }
+    }
+}
+
+// Fixed-order reduction of split-K partials into C (deterministic).
+__global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, int ldw,
+                              float* __restrict__ C, int ldc, float beta) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)M * N) return;
+    const int m = idx / N, n = idx % N;
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += ws[((size_t)z * M + m) * ldw + n];
+    float* c = C + (size_t)m * ldc + n;
+    *c = beta != 0.f ? *c + s : s;
+}
+
+}  // namespace gemm
+}  // namespace spd

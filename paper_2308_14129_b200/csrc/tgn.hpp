@@ -1,0 +1,152 @@
+// TGN training hot path on sm_100a: the per-partition memory-based TIG
+// training step of SPEED, one or more SEP partitions
+// (workers) per process/device, gradients all-reduced over NCCL every global
+// step, shared hubs synced at epoch end. Semantics: oracle/tgn_oracle.py.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "cuda_util.hpp"
+#include "host.hpp"
+
+namespace spd {
+
+inline int ld4(int cols) { return (cols + 3) / 4 * 4; }
+inline int ld_aug(int cols) { return (cols + 1 + 3) / 4 * 4; }  // [x | 1 | pad]
+
+// Flat parameter buffer: every linear layer is an augmented [W | b] matrix
+// (row stride ld_aug(K)); tensors start at 4-float boundaries.
+struct ParamLayout {
+    struct Lin { int N, K, ld; std::size_t off; };
+    Lin gru_ih, gru_hh, att_q, att_kv, att_o, mrg1, mrg2, dec1, dec2;
+    std::size_t time_w, time_b;
+    std::size_t total;
+    int D, T, F, DQ, DK, DM, H, Kn;
+    void build(int d_mem, int d_time, int d_edge, int heads, int k);
+};
+
+struct StepTimes {
+    std::vector<std::pair<std::string, float>> ms;
+};
+
+class TGNTrainer;
+
+// One SEP partition's static data + dynamic state on the device.
+struct Worker {
+    int gid = 0;                     // global worker / partition id
+    NodeId N = 0;                    // local nodes
+    std::uint64_t E = 0;             // training events
+    std::vector<NodeId> nodes;       // local -> global (ascending)
+    std::vector<spd_edge> ev_host;   // local ids
+    // static device data
+    DevBuf<std::uint32_t> ev_src, ev_dst;
+    DevBuf<double> ev_ts;
+    DevBuf<__nv_bfloat16> feat;      // E x Fp
+    DevBuf<std::uint64_t> adj_off;   // N + 1
+    DevBuf<std::uint32_t> adj_nbr, adj_ev;
+    DevBuf<double> adj_ts;
+    DevBuf<std::uint32_t> pool;      // destination nodes (negatives)
+    std::uint32_t n_pool = 0;
+    // dynamic state
+    DevBuf<float> mem, mem_snap;     // N x D
+    DevBuf<double> lu, lu_snap;      // N
+    DevBuf<std::int32_t> slot;       // N: node -> row of the pending set, -1
+    DevBuf<std::int32_t> lastpos;    // N: scratch for last-message selection
+    DevBuf<std::uint32_t> pU, pOther, pEv;  // pending set (<= 2B)
+    DevBuf<double> pTs;
+    DevBuf<std::int32_t> nU;         // device-resident |pending|
+    std::vector<std::uint32_t> shared_local;  // local row of each shared node (or UINT32_MAX)
+    // schedule
+    std::uint64_t batches = 0, pos = 0, loops = 0;
+    bool done = false;
+    double last_loss = 0.0;
+    std::uint64_t last_b = 0;
+    // debug taps of the last step (filled only when TGNTrainer::debug_ is set)
+    std::vector<float> tap_emb;
+    std::vector<std::uint32_t> tap_roots, tap_nbr;
+    float tap_loss = 0.f;
+};
+
+struct Scratch;  // per-step activations (sized for one batch)
+
+std::uint64_t kernel_launches();  // process-wide count of TGN-path kernel launches
+
+class TGNTrainer {
+public:
+    TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs, const std::vector<int>& workers,
+               const std::vector<NodeId>& shared, NodeId node_count, int rank, int world,
+               const void* nccl_id, int device);
+    ~TGNTrainer();
+
+    std::uint64_t epoch_steps() const { return epoch_steps_; }
+    std::uint64_t batch_size() const { return cfg_.batch_size; }
+    void begin_epoch(int epoch);
+    void step(float* loss_out);
+    void end_epoch();
+    void run_epoch(int epoch, double* mean_loss);
+    void evaluate(int worker, const spd_edge* e, const std::uint64_t* eids, std::uint64_t n,
+                  std::uint64_t neg_seed, float* pos, float* neg);
+
+    std::size_t param_count() const { return lay_.total; }
+    void get_params(float* out) const;
+    void set_params(const float* in);
+    void get_grads(float* out) const;
+    Worker& worker(int w);
+    void get_memory(int w, float* mem, double* lu);
+    void set_memory(int w, const float* mem, const double* lu);
+    void last_step(int w, std::uint64_t* b, float* emb, std::uint32_t* negs, std::uint32_t* nbr,
+                   float* loss);
+    const StepTimes& times() const { return times_; }
+    float run_steps(std::uint64_t n);
+    void step_host(const spd_edge* const* events, const std::uint16_t* const* feats,
+                   float* loss_out);
+    std::uint64_t h2d_bytes() const { return h2d_bytes_; }
+    std::uint64_t d2h_bytes() const { return d2h_bytes_; }
+    std::uint64_t step_in_epoch() const { return step_in_epoch_; }
+    int epoch() const { return epoch_; }
+    int feat_stride() const;
+    void set_debug(bool on) { debug_ = on; }
+    void set_profile(bool on) { profile_ = on; }
+    int device() const { return device_; }
+    cudaStream_t stream() const { return stream_; }
+
+private:
+    void worker_step(Worker& w, std::uint64_t step_in_epoch);
+    void worker_post(Worker& w);
+    void flush_pending(Worker& w);
+    void gru_forward(Worker& w, bool train);
+    void allreduce_grads();
+    void adam();
+    void sync_shared();
+    void timed(const char* name, const std::function<void()>& f);
+
+    spd_tgn_config cfg_;
+    ParamLayout lay_;
+    int device_ = 0, rank_ = 0, world_ = 1;
+    int total_workers_ = 1;
+    cudaStream_t stream_ = nullptr;
+    void* nccl_ = nullptr;  // ncclComm_t
+    std::vector<std::unique_ptr<Worker>> workers_;
+    std::vector<std::uint64_t> all_batches_;  // per global worker
+    std::uint64_t epoch_steps_ = 0, step_in_epoch_ = 0, adam_t_ = 0;
+    int epoch_ = 0;
+    std::vector<NodeId> shared_;
+    DevBuf<float> params_, grads_, adam_m_, adam_v_;
+    DevBuf<double> tgrad_;  // f64 accumulators for the time encoder grads (2T)
+    std::unique_ptr<Scratch> s_;
+    StepTimes times_;
+    bool profile_ = false;
+    bool debug_ = false;
+    unsigned char* stage_ = nullptr;  // pinned
+    std::size_t stage_bytes_ = 0;
+    std::uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+    std::uint64_t feat_seed_mixed_ = 0;
+};
+
+}  // namespace spd

@@ -1,0 +1,552 @@
+// Non-GEMM kernels of the TGN training step; see tgn_kernels.cuh. Semantics
+// follow oracle/tgn_oracle.py line for line (which states the model choices).
+#include "tgn_common.cuh"
+#include "tgn_kernels.cuh"
+
+namespace spd {
+namespace tgnk {
+
+namespace {
+__device__ __forceinline__ int warp_id_global() {
+    return (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+}
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// memory row of local node n as seen by this step: the GRU-updated row when
+// n had a pending message (slot >= 0), else the stored row.
+__device__ __forceinline__ const float* memx_row(const WorkerDev& w, const float* mem_new, int D,
+                                                 std::uint32_t n) {
+    const int s = w.slot[n];
+    return s >= 0 ? mem_new + (std::size_t)s * D : w.mem + (std::size_t)n * D;
+}
+
+__device__ __forceinline__ float softplusf(float x) { return x > 20.f ? x : log1pf(expf(x)); }
+}  // namespace
+
+__global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)rows * ld) return;
+    const int c = i % ld;
+    if (c >= cols) buf[i] = c == cols ? 1.f : 0.f;
+    else buf[i] = 0.f;
+}
+
+// K5 + K8: roots (src | dst | neg) and the recent-k neighbours strictly
+// before t: lower_bound on the node's time-sorted adjacency, last K entries.
+__global__ void k_roots_nbrs(WorkerDev w, std::uint64_t lo, int B, std::uint64_t neg_base, int K,
+                             std::uint32_t* roots, double* root_t, std::uint32_t* nbr_node,
+                             std::uint32_t* nbr_ev, double* nbr_dt, int* cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= 3 * B) return;
+    const int which = r / B, i = r % B;
+    const std::uint64_t e = lo + i;
+    const double t = w.ev_ts[e];
+    std::uint32_t node;
+    if (which == 0) node = w.ev_src[e];
+    else if (which == 1) node = w.ev_dst[e];
+    else node = w.pool[mix64(neg_base ^ (std::uint64_t)i) % w.n_pool];
+    roots[r] = node;
+    root_t[r] = t;
+    const std::uint64_t a = w.adj_off[node], b = w.adj_off[node + 1];
+    std::uint64_t l = a, h = b;
+    while (l < h) {
+        const std::uint64_t mid = (l + h) >> 1;
+        if (w.adj_ts[mid] < t) l = mid + 1;
+        else h = mid;
+    }
+    const std::uint64_t avail = l - a;
+    const int c = avail < (std::uint64_t)K ? (int)avail : K;
+    const std::uint64_t start = l - c;
+    cnt[r] = c;
+    for (int j = 0; j < K; ++j) {
+        const std::size_t o = (std::size_t)r * K + j;
+        if (j < c) {
+            const std::uint64_t idx = start + j;
+            nbr_node[o] = w.adj_nbr[idx];
+            nbr_ev[o] = w.adj_ev[idx];
+            nbr_dt[o] = t - w.adj_ts[idx];
+        } else {
+            nbr_node[o] = kPad;
+            nbr_ev[o] = 0;
+            nbr_dt[o] = 0.0;
+        }
+    }
+}
+
+// K1 + K2 for the memory updater: message [s_i | s_j | e | phi(t - t_i^-)]
+// and hidden s_i for every pending node (one warp per node).
+__global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const float* time_b,
+                             float* x, float* h, int set_slot) {
+    const int u = warp_id_global(), lane = lane_id();
+    if (u >= *w.nU) return;
+    const std::uint32_t node = w.pU[u], other = w.pOther[u], ev = w.pEv[u];
+    const double dt = w.pTs[u] - w.lu[node];
+    if (set_slot && lane == 0) w.slot[node] = u;
+    float* xr = x + (std::size_t)u * d.ld_x;
+    float* hr = h + (std::size_t)u * d.ld_h;
+    const float* mn = w.mem + (std::size_t)node * d.D;
+    const float* mo = w.mem + (std::size_t)other * d.D;
+    for (int c = lane; c < d.D; c += 32) {
+        const float v = mn[c];
+        xr[c] = v;
+        hr[c] = v;
+        xr[d.D + c] = mo[c];
+    }
+    const __nv_bfloat16* fr = w.feat + (std::size_t)ev * d.Fp;
+    for (int c = lane; c < d.F; c += 32) xr[2 * d.D + c] = __bfloat162float(fr[c]);
+    for (int c = lane; c < d.T; c += 32) xr[2 * d.D + d.F + c] = time_cos(time_w[c], time_b[c], dt);
+}
+
+// GRUCell (PyTorch gate order r, z, n) on G_i = W_ih x + b_ih, G_h = W_hh h + b_hh.
+__global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh, const float* h,
+                          float* save, float* mem_new) {
+    const int nU = *w.nU;
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)nU * d.D) return;
+    const int u = i / d.D, c = i % d.D;
+    const float* gi = Gi + (std::size_t)u * d.ld_g;
+    const float* gh = Gh + (std::size_t)u * d.ld_g;
+    const float r = sigmoidf_(gi[c] + gh[c]);
+    const float z = sigmoidf_(gi[d.D + c] + gh[d.D + c]);
+    const float ghn = gh[2 * d.D + c];
+    const float n = tanhf(gi[2 * d.D + c] + r * ghn);
+    const float hv = h[(std::size_t)u * d.ld_h + c];
+    mem_new[(std::size_t)u * d.D + c] = (1.f - z) * n + z * hv;
+    if (save) {
+        float* s = save + (std::size_t)u * 4 * d.D;
+        s[c] = r;
+        s[d.D + c] = z;
+        s[2 * d.D + c] = n;
+        s[3 * d.D + c] = ghn;
+    }
+}
+
+// K1 + K2 for attention: q_in = [s_root | phi(0)], kv_in = [s_nbr | e | phi(dt)]
+// (one warp per row; padded neighbour rows are zero).
+__global__ void k_embed_gather(WorkerDev w, Dims d, int R, const float* time_w,
+                               const float* time_b, const std::uint32_t* roots,
+                               const std::uint32_t* nbr_node, const std::uint32_t* nbr_ev,
+                               const double* nbr_dt, const int* cnt, const float* mem_new,
+                               float* q_in, float* kv_in) {
+    const int row = warp_id_global(), lane = lane_id();
+    if (row >= R * (1 + d.K)) return;
+    if (row < R) {
+        const float* m = memx_row(w, mem_new, d.D, roots[row]);
+        float* q = q_in + (std::size_t)row * d.ld_q;
+        for (int c = lane; c < d.D; c += 32) q[c] = m[c];
+        for (int c = lane; c < d.T; c += 32) q[d.D + c] = time_cos(time_w[c], time_b[c], 0.0);
+        return;
+    }
+    const int kr = row - R;  // r * K + j
+    const int r = kr / d.K, j = kr % d.K;
+    float* o = kv_in + (std::size_t)kr * d.ld_kv;
+    if (j >= cnt[r]) {
+        for (int c = lane; c < d.DK; c += 32) o[c] = 0.f;
+        return;
+    }
+    const float* m = memx_row(w, mem_new, d.D, nbr_node[kr]);
+    for (int c = lane; c < d.D; c += 32) o[c] = m[c];
+    const __nv_bfloat16* fr = w.feat + (std::size_t)nbr_ev[kr] * d.Fp;
+    for (int c = lane; c < d.F; c += 32) o[d.D + c] = __bfloat162float(fr[c]);
+    const double dt = nbr_dt[kr];
+    for (int c = lane; c < d.T; c += 32) o[d.D + d.F + c] = time_cos(time_w[c], time_b[c], dt);
+}
+
+// Multi-head attention core over <= K neighbours (one warp per root).
+// KV rows: [K (DQ) | V (DQ)], row stride 2DQ. alpha: [R][H][K].
+__global__ void k_attn_fwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
+                           float* alpha, float* ctx) {
+    extern __shared__ float sm[];
+    const int warp_in_block = threadIdx.x >> 5, lane = lane_id();
+    const int r = warp_id_global();
+    if (r >= R) return;
+    float* s = sm + warp_in_block * d.H * d.K;
+    const int c_n = cnt[r];
+    float* cr = ctx + (std::size_t)r * d.ld_ctx;
+    if (c_n == 0) {
+        for (int c = lane; c < d.DQ; c += 32) cr[c] = 0.f;
+        return;
+    }
+    const int dh = d.DQ / d.H;
+    const float* q = Q + (std::size_t)r * d.DQ;
+    for (int h = 0; h < d.H; ++h) {
+        for (int j = 0; j < c_n; ++j) {
+            const float* k = KV + ((std::size_t)r * d.K + j) * 2 * d.DQ + h * dh;
+            float p = 0.f;
+            for (int c = lane; c < dh; c += 32) p += q[h * dh + c] * k[c];
+            p = warp_sum(p);
+            if (lane == 0) s[h * d.K + j] = p / sqrtf((float)dh);
+        }
+    }
+    __syncwarp();
+    // softmax per head over valid j (lane = j, K <= 32)
+    for (int h = 0; h < d.H; ++h) {
+        float v = lane < c_n ? s[h * d.K + lane] : -INFINITY;
+        float mx = v;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float e = lane < c_n ? expf(v - mx) : 0.f;
+        const float sum = warp_sum(e);
+        const float a = e / sum;
+        __syncwarp();
+        if (lane < d.K) {
+            const float av = lane < c_n ? a : 0.f;
+            s[h * d.K + lane] = av;
+            alpha[((std::size_t)r * d.H + h) * d.K + lane] = av;
+        }
+    }
+    __syncwarp();
+    for (int c = lane; c < d.DQ; c += 32) {
+        const int h = c / dh;
+        float acc = 0.f;
+        for (int j = 0; j < c_n; ++j)
+            acc += s[h * d.K + j] * KV[((std::size_t)r * d.K + j) * 2 * d.DQ + d.DQ + c];
+        cr[c] = acc;
+    }
+}
+
+// MergeLayer input [attn | s_root]; attn = 0 for a root without neighbours.
+__global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                               const int* cnt, const float* O, const float* mem_new, float* m_in) {
+    const int r = warp_id_global(), lane = lane_id();
+    if (r >= R) return;
+    float* o = m_in + (std::size_t)r * d.ld_m;
+    const bool has = cnt[r] > 0;
+    for (int c = lane; c < d.DQ; c += 32) o[c] = has ? O[(std::size_t)r * d.DQ + c] : 0.f;
+    const float* m = memx_row(w, mem_new, d.D, roots[r]);
+    for (int c = lane; c < d.D; c += 32) o[d.DQ + c] = m[c];
+}
+
+// Decoder input rows: p < B -> [z_src | z_dst], p >= B -> [z_src | z_neg].
+__global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in) {
+    const int p = warp_id_global(), lane = lane_id();
+    if (p >= 2 * B) return;
+    const int i = p < B ? p : p - B;
+    const int other = p < B ? B + i : 2 * B + i;
+    float* o = d_in + (std::size_t)p * d.ld_din;
+    for (int c = lane; c < d.D; c += 32) {
+        o[c] = emb[(std::size_t)i * d.D + c];
+        o[d.D + c] = emb[(std::size_t)other * d.D + c];
+    }
+}
+
+// K7 head: logit = D1 . w2 + b2, BCE-with-logits terms and their gradients.
+// w2 = augmented [w | b] row of dec2.
+__global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, float* dlogit,
+                           float* lossv, float* dD1, float* logits) {
+    const int p = warp_id_global(), lane = lane_id();
+    if (p >= 2 * B) return;
+    const float* x = D1 + (std::size_t)p * d.ld_d1;
+    float acc = 0.f;
+    for (int c = lane; c < d.D; c += 32) acc += x[c] * w2[c];
+    acc = warp_sum(acc) + w2[d.D];
+    const bool pos = p < B;
+    const float sig = sigmoidf_(acc);
+    const float g = (sig - (pos ? 1.f : 0.f)) / (float)B;
+    if (lane == 0) {
+        dlogit[(std::size_t)p * 4] = g;
+        lossv[p] = (pos ? softplusf(-acc) : softplusf(acc)) / (float)B;
+        if (logits) logits[p] = acc;
+    }
+    float* dx = dD1 + (std::size_t)p * d.D;
+    for (int c = lane; c < d.D; c += 32) dx[c] = x[c] > 0.f ? g * w2[c] : 0.f;
+}
+
+// Fixed-order single-block sum (deterministic loss).
+__global__ void k_sum_loss(const float* lossv, int n, float* out) {
+    __shared__ float sh[32];
+    float s = 0.f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += lossv[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) *out = v;
+    }
+}
+
+__global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb) {
+    const int i = warp_id_global(), lane = lane_id();
+    if (i >= B) return;
+    const float* a = dd_in + (std::size_t)i * d.ld_din;
+    const float* b = dd_in + (std::size_t)(B + i) * d.ld_din;
+    for (int c = lane; c < d.D; c += 32) {
+        d_emb[(std::size_t)i * d.D + c] = a[c] + b[c];
+        d_emb[(std::size_t)(B + i) * d.D + c] = a[d.D + c];
+        d_emb[(std::size_t)(2 * B + i) * d.D + c] = b[d.D + c];
+    }
+}
+
+__global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt) {
+    const int r = warp_id_global(), lane = lane_id();
+    if (r >= R || cnt[r] > 0) return;
+    for (int c = lane; c < cols; c += 32) buf[(std::size_t)r * ld + c] = 0.f;
+}
+
+// Attention core backward (one warp per root).
+__global__ void k_attn_bwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
+                           const float* alpha, const float* dctx, int ld_dctx, float* dQ,
+                           float* dKV) {
+    extern __shared__ float sm[];
+    const int warp_in_block = threadIdx.x >> 5, lane = lane_id();
+    const int r = warp_id_global();
+    if (r >= R) return;
+    float* ds = sm + warp_in_block * d.H * d.K;
+    const int c_n = cnt[r];
+    const int dh = d.DQ / d.H;
+    const float inv = 1.f / sqrtf((float)dh);
+    const float* dc = dctx + (std::size_t)r * ld_dctx;
+    const float* a = alpha + (std::size_t)r * d.H * d.K;
+    if (c_n > 0) {
+        for (int h = 0; h < d.H; ++h) {
+            for (int j = 0; j < c_n; ++j) {
+                const float* v = KV + ((std::size_t)r * d.K + j) * 2 * d.DQ + d.DQ + h * dh;
+                float p = 0.f;
+                for (int c = lane; c < dh; c += 32) p += dc[h * dh + c] * v[c];
+                p = warp_sum(p);
+                if (lane == 0) ds[h * d.K + j] = p;  // d alpha_j
+            }
+            __syncwarp();
+            float da = lane < c_n ? ds[h * d.K + lane] : 0.f;
+            const float aj = lane < c_n ? a[h * d.K + lane] : 0.f;
+            const float dot = warp_sum(aj * da);
+            __syncwarp();
+            if (lane < c_n) ds[h * d.K + lane] = aj * (da - dot);  // d score_j
+            __syncwarp();
+        }
+    }
+    float* dq = dQ + (std::size_t)r * d.DQ;
+    for (int c = lane; c < d.DQ; c += 32) {
+        const int h = c / dh;
+        float acc = 0.f;
+        for (int j = 0; j < c_n; ++j)
+            acc += ds[h * d.K + j] * KV[((std::size_t)r * d.K + j) * 2 * d.DQ + c];
+        dq[c] = acc * inv;
+    }
+    const float* q = Q + (std::size_t)r * d.DQ;
+    for (int j = 0; j < d.K; ++j) {
+        float* o = dKV + ((std::size_t)r * d.K + j) * 2 * d.DQ;
+        if (j >= c_n) {
+            for (int c = lane; c < 2 * d.DQ; c += 32) o[c] = 0.f;
+            continue;
+        }
+        for (int c = lane; c < d.DQ; c += 32) {
+            const int h = c / dh;
+            o[c] = ds[h * d.K + j] * q[c] * inv;
+            o[d.DQ + c] = a[h * d.K + j] * dc[c];
+        }
+    }
+}
+
+// Memory-row gradients into the GRU output rows of pending nodes: roots
+// (query + merge inputs) and neighbours (key/value inputs).
+__global__ void k_mem_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                           const std::uint32_t* nbr_node, const int* cnt, const float* dq_in,
+                           const float* dm_in, const float* dkv_in, float* dH) {
+    const int row = warp_id_global(), lane = lane_id();
+    if (row >= R * (1 + d.K)) return;
+    if (row < R) {
+        const int s = w.slot[roots[row]];
+        if (s < 0) return;
+        const float* a = dq_in + (std::size_t)row * d.ld_q;
+        const float* b = dm_in + (std::size_t)row * d.ld_m + d.DQ;
+        for (int c = lane; c < d.D; c += 32) atomicAdd(dH + (std::size_t)s * d.D + c, a[c] + b[c]);
+        return;
+    }
+    const int kr = row - R;
+    const int r = kr / d.K, j = kr % d.K;
+    if (j >= cnt[r]) return;
+    const int s = w.slot[nbr_node[kr]];
+    if (s < 0) return;
+    const float* a = dkv_in + (std::size_t)kr * d.ld_kv;
+    for (int c = lane; c < d.D; c += 32) atomicAdd(dH + (std::size_t)s * d.D + c, a[c]);
+}
+
+// Time-encoder gradients: per block, f64 column partials over a chunk of rows
+// (kv rows: d/dw = -sin(ph) dt g, d/db = -sin(ph) g; query rows: phi(0)=cos(b)).
+// part: [nblocks][2T] (w then b).
+__global__ void k_time_grad_partial(Dims d, int R, const int* cnt, const double* nbr_dt,
+                                    const float* dkv_in, const float* dq_in, const float* time_w,
+                                    const float* time_b, int rows_per_block, double* part) {
+    const int total = R * (1 + d.K);
+    const int r0 = blockIdx.x * rows_per_block;
+    const int r1 = min(total, r0 + rows_per_block);
+    for (int c = threadIdx.x; c < d.T; c += blockDim.x) {
+        const float wc = time_w[c], bc = time_b[c];
+        double gw = 0.0, gb = 0.0;
+        const double sin_b = sin((double)bc);
+        for (int row = r0; row < r1; ++row) {
+            if (row < R) {
+                const double g = dq_in[(std::size_t)row * d.ld_q + d.D + c];
+                gb -= sin_b * g;
+            } else {
+                const int kr = row - R;
+                const int r = kr / d.K, j = kr % d.K;
+                if (j >= cnt[r]) continue;
+                const double dt = nbr_dt[kr];
+                const double g = dkv_in[(std::size_t)kr * d.ld_kv + d.D + d.F + c];
+                const double ph = __dadd_rn(__dmul_rn((double)wc, dt), (double)bc);
+                const double sn = sin(ph);
+                gw -= sn * dt * g;
+                gb -= sn * g;
+            }
+        }
+        part[(std::size_t)blockIdx.x * 2 * d.T + c] = gw;
+        part[(std::size_t)blockIdx.x * 2 * d.T + d.T + c] = gb;
+    }
+}
+
+__global__ void k_time_grad_final(int T, int nblocks, const double* part, double* acc) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= 2 * T) return;
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += part[(std::size_t)b * 2 * T + c];
+    acc[c] += s;
+}
+
+__global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= T) return;
+    gw[c] += (float)acc[c];
+    gb[c] += (float)acc[T + c];
+}
+
+// GRUCell backward to the gate pre-activations (inputs x, h are constants).
+__global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* save, const float* h,
+                          float* dGi, float* dGh) {
+    const int nU = *w.nU;
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)nU * d.D) return;
+    const int u = i / d.D, c = i % d.D;
+    const float* s = save + (std::size_t)u * 4 * d.D;
+    const float r = s[c], z = s[d.D + c], n = s[2 * d.D + c], ghn = s[3 * d.D + c];
+    const float g = dH[(std::size_t)u * d.D + c];
+    const float hv = h[(std::size_t)u * d.ld_h + c];
+    const float dn = g * (1.f - z);
+    const float dz = g * (hv - n);
+    const float dpn = dn * (1.f - n * n);
+    const float dpr = dpn * ghn * r * (1.f - r);
+    const float dpz = dz * z * (1.f - z);
+    float* gi = dGi + (std::size_t)u * d.ld_g;
+    float* gh = dGh + (std::size_t)u * d.ld_g;
+    gi[c] = dpr;
+    gi[d.D + c] = dpz;
+    gi[2 * d.D + c] = dpn;
+    gh[c] = dpr;
+    gh[d.D + c] = dpz;
+    gh[2 * d.D + c] = dpn * r;
+}
+
+__global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
+                       float lr, float b1, float one_m_b1, float b2, float one_m_b2, float bc1,
+                       float bc2, float eps) {
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float gi = g[i] / scale;
+    const float mi = b1 * m[i] + one_m_b1 * gi;
+    const float vi = b2 * v[i] + one_m_b2 * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float mh = mi / bc1;
+    const float vh = vi / bc2;
+    p[i] = p[i] - lr * mh / (sqrtf(vh) + eps);
+}
+
+// Persist the GRU rows of pending nodes (K11) and clear their slots.
+__global__ void k_persist(WorkerDev w, int D, const float* mem_new) {
+    const int u = warp_id_global(), lane = lane_id();
+    if (u >= *w.nU) return;
+    const std::uint32_t node = w.pU[u];
+    for (int c = lane; c < D; c += 32) w.mem[(std::size_t)node * D + c] = mem_new[(std::size_t)u * D + c];
+    if (lane == 0) {
+        w.lu[node] = w.pTs[u];
+        w.slot[node] = -1;
+    }
+}
+
+// K3 last-message selection: endpoint slots q = 2k (src), 2k+1 (dst) of the
+// batch's events; per node the max slot wins (max (ts, stream index)),
+// compacted in slot order. Single block; lastpos starts and ends at -1.
+__global__ void k_pending(WorkerDev w, std::uint64_t lo, int B) {
+    __shared__ int warp_tot[32];
+    __shared__ int base;
+    const int nslots = 2 * B;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int q = tid; q < nslots; q += nt) {
+        const std::uint64_t e = lo + (q >> 1);
+        const std::uint32_t node = (q & 1) ? w.ev_dst[e] : w.ev_src[e];
+        atomicMax(w.lastpos + node, q);
+    }
+    if (tid == 0) base = 0;
+    __syncthreads();
+    for (int q0 = 0; q0 < nslots; q0 += nt) {
+        const int q = q0 + tid;
+        int win = 0;
+        std::uint32_t node = 0, other = 0;
+        std::uint64_t e = 0;
+        if (q < nslots) {
+            e = lo + (q >> 1);
+            const std::uint32_t s = w.ev_src[e], t = w.ev_dst[e];
+            node = (q & 1) ? t : s;
+            other = (q & 1) ? s : t;
+            win = w.lastpos[node] == q;
+        }
+        // block exclusive scan of win
+        const int lane = tid & 31, wid = tid >> 5;
+        const unsigned bal = __ballot_sync(0xffffffffu, win);
+        const int pre = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 0) warp_tot[wid] = __popc(bal);
+        __syncthreads();
+        if (wid == 0) {
+            int v = lane < (nt >> 5) ? warp_tot[lane] : 0;
+            int incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane < (nt >> 5)) warp_tot[lane] = incl - v;  // exclusive
+        }
+        __syncthreads();
+        const int pos = base + warp_tot[wid] + pre;
+        if (win) {
+            w.pU[pos] = node;
+            w.pOther[pos] = other;
+            w.pEv[pos] = (std::uint32_t)e;
+            w.pTs[pos] = w.ev_ts[e];
+        }
+        __syncthreads();
+        if (tid == nt - 1) base = pos + win;
+        __syncthreads();
+    }
+    if (tid == 0) *w.nU = base;
+    for (int q = tid; q < nslots; q += nt) {
+        const std::uint64_t e = lo + (q >> 1);
+        const std::uint32_t node = (q & 1) ? w.ev_dst[e] : w.ev_src[e];
+        w.lastpos[node] = -1;
+    }
+}
+
+// Synthetic BF16-exact edge features for the partition's events (E x Fp, pad 0).
+__global__ void k_gen_features(__nv_bfloat16* feat, const std::uint64_t* eids, std::uint64_t E,
+                               int F, int Fp, std::uint64_t seed_mixed) {
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= E * (std::size_t)Fp) return;
+    const std::uint64_t e = i / Fp;
+    const int c = i % Fp;
+    const float v = c < F ? edge_feature_value(seed_mixed, eids[e], (std::uint32_t)c) : 0.f;
+    feat[i] = __float2bfloat16_rn(v);
+}
+
+__global__ void k_gather_rows(const float* src, int ld, const std::uint32_t* idx, std::uint32_t n,
+                              int cols, float* out) {
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)n * cols) return;
+    const std::uint32_t r = i / cols, c = i % cols;
+    out[i] = src[(std::size_t)idx[r] * ld + c];
+}
+
+}  // namespace tgnk
+}  // namespace spd

@@ -1,0 +1,94 @@
+// Non-GEMM kernels of the TGN step. Each
+// is memory/latency bound: warp-per-row gathers with the row's columns
+// spread over lanes (coalesced 4-byte lanes, 16-byte for bf16x8 features),
+// f64 time phases, deterministic fixed-order reductions where a parameter
+// gradient is summed.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace spd {
+namespace tgnk {
+
+constexpr std::uint32_t kPad = 0xFFFFFFFFu;
+
+struct Dims {
+    int D, T, F, Fp, DQ, DK, DM, H, K;
+    int ld_x, ld_h, ld_q, ld_kv, ld_ctx, ld_m, ld_z, ld_din, ld_d1;  // aug strides
+    int ld_g;  // 3D rounded
+};
+
+struct WorkerDev {
+    const std::uint32_t* ev_src;
+    const std::uint32_t* ev_dst;
+    const double* ev_ts;
+    const __nv_bfloat16* feat;
+    const std::uint64_t* adj_off;
+    const std::uint32_t* adj_nbr;
+    const std::uint32_t* adj_ev;
+    const double* adj_ts;
+    const std::uint32_t* pool;
+    std::uint32_t n_pool;
+    float* mem;
+    double* lu;
+    std::int32_t* slot;
+    std::int32_t* lastpos;
+    std::uint32_t* pU;
+    std::uint32_t* pOther;
+    std::uint32_t* pEv;
+    double* pTs;
+    std::int32_t* nU;
+};
+
+// --- kernels (definitions in tgn_kernels.cu) -------------------------------
+__global__ void k_init_aug(float* buf, int rows, int cols, int ld);
+__global__ void k_roots_nbrs(WorkerDev w, std::uint64_t lo, int B, std::uint64_t neg_base, int K,
+                             std::uint32_t* roots, double* root_t, std::uint32_t* nbr_node,
+                             std::uint32_t* nbr_ev, double* nbr_dt, int* cnt);
+__global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const float* time_b,
+                             float* x, float* h, int set_slot);
+__global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh, const float* h,
+                          float* save, float* mem_new);
+__global__ void k_embed_gather(WorkerDev w, Dims d, int R, const float* time_w,
+                               const float* time_b, const std::uint32_t* roots,
+                               const std::uint32_t* nbr_node, const std::uint32_t* nbr_ev,
+                               const double* nbr_dt, const int* cnt, const float* mem_new,
+                               float* q_in, float* kv_in);
+__global__ void k_attn_fwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
+                           float* alpha, float* ctx);
+__global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                               const int* cnt, const float* O, const float* mem_new, float* m_in);
+__global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in);
+__global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, float* dlogit,
+                           float* lossv, float* dD1, float* logits);
+__global__ void k_sum_loss(const float* lossv, int n, float* out);
+__global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb);
+__global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt);
+__global__ void k_attn_bwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
+                           const float* alpha, const float* dctx, int ld_dctx, float* dQ,
+                           float* dKV);
+__global__ void k_mem_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                           const std::uint32_t* nbr_node, const int* cnt, const float* dq_in,
+                           const float* dm_in, const float* dkv_in, float* dH);
+__global__ void k_time_grad_partial(Dims d, int R, const int* cnt, const double* nbr_dt,
+                                    const float* dkv_in, const float* dq_in, const float* time_w,
+                                    const float* time_b, int rows_per_block, double* part);
+__global__ void k_time_grad_final(int T, int nblocks, const double* part, double* acc);
+__global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb);
+__global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* save, const float* h,
+                          float* dGi, float* dGh);
+__global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
+                       float lr, float b1, float one_m_b1, float b2, float one_m_b2, float bc1,
+                       float bc2, float eps);
+__global__ void k_persist(WorkerDev w, int D, const float* mem_new);
+__global__ void k_pending(WorkerDev w, std::uint64_t lo, int B);
+__global__ void k_gen_features(__nv_bfloat16* feat, const std::uint64_t* eids, std::uint64_t E,
+                               int F, int Fp, std::uint64_t seed_mixed);
+__global__ void k_gather_rows(const float* src, int ld, const std::uint32_t* idx,
+                              std::uint32_t n, int cols, float* out);
+
+}  // namespace tgnk
+}  // namespace spd

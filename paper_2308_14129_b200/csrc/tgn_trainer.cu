@@ -1,0 +1,961 @@
+// TGN trainer: the PAC lockstep schedule (Alg. 2; pac_sim.cpp:205-264)
+// driving the per-partition TGN step on one B200, NCCL all-reduce of the flat
+// gradient buffer every global step and the epoch-end shared-hub sync.
+//
+// Step anatomy (one worker; oracle/tgn_oracle.py TGNOracle.step):
+//   roots+nbrs -> GRU gather -> G_i,G_h GEMMs -> GRU cell -> embed gather ->
+//   Q, [K;V] GEMMs -> attention -> W_o GEMM -> merge gather -> W_m1, W_m2 ->
+//   decoder gather -> W_d1 -> head/loss ; backward mirrors it with
+//   weight-gradient GEMMs accumulating straight into the flat gradient.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <numeric>
+
+#include "gemm_simt.cuh"
+#include "nccl_dyn.hpp"
+#include "surrogate.hpp"
+#include "tgn.hpp"
+#include "tgn_common.cuh"
+#include "tgn_kernels.cuh"
+
+namespace spd {
+
+std::atomic<std::uint64_t> g_kernel_launches{0};
+
+// Every kernel of the TGN path goes through here: counted (bench.py reports
+// the launches inside the timed region) and checked.
+template <class... KArgs, class... Args>
+void launch(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+            Args&&... args) {
+    k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    SPD_CUDA(cudaGetLastError());
+}
+
+#define ncclCommInitRank NcclApi::get().CommInitRank
+#define ncclCommDestroy NcclApi::get().CommDestroy
+#define ncclAllReduce NcclApi::get().AllReduce
+#define ncclGroupStart NcclApi::get().GroupStart
+#define ncclGroupEnd NcclApi::get().GroupEnd
+
+void ParamLayout::build(int d_mem, int d_time, int d_edge, int heads, int k) {
+    D = d_mem;
+    T = d_time;
+    F = d_edge;
+    H = heads;
+    Kn = k;
+    DQ = D + T;
+    DK = D + F + T;
+    DM = 2 * D + F + T;
+    std::size_t off = 0;
+    time_w = off;
+    off += ld4(T);
+    time_b = off;
+    off += ld4(T);
+    auto lin = [&](Lin& l, int N, int K) {
+        l.N = N;
+        l.K = K;
+        l.ld = ld_aug(K);
+        l.off = off;
+        off += std::size_t(N) * l.ld;
+    };
+    // order == oracle/tgn_oracle.py linear_specs
+    lin(gru_ih, 3 * D, DM);
+    lin(gru_hh, 3 * D, D);
+    lin(att_q, DQ, DQ);
+    lin(att_kv, 2 * DQ, DK);
+    lin(att_o, DQ, DQ);
+    lin(mrg1, D, DQ + D);
+    lin(mrg2, D, D);
+    lin(dec1, D, 2 * D);
+    lin(dec2, 1, D);
+    total = off;
+}
+
+// ------------------------------------------------------------ scratch
+struct Scratch {
+    int B = 0, R = 0, RK = 0, U = 0;
+    tgnk::Dims d{};
+    DevBuf<std::uint32_t> roots, nbr_node, nbr_ev;
+    DevBuf<double> root_t, nbr_dt;
+    DevBuf<int> cnt;
+    DevBuf<float> x_gru, h_gru, Gi, Gh, gsave, mem_new, dH, dGi, dGh;
+    DevBuf<float> q_in, kv_in, Q, KV, alpha, ctx, O, m_in, Z1, emb, d_in, D1, logits, lossv, dlogit;
+    DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dQ, dKV, dkv_in, dq_in;
+    DevBuf<float> ws;
+    DevBuf<double> tpart;
+    DevBuf<float> loss;  // per local worker
+    int tblocks = 0, trows = 0;
+};
+
+namespace {
+
+void init_aug(DevBuf<float>& b, int rows, int cols, int ld, cudaStream_t s) {
+    const std::size_t n = std::size_t(rows) * ld;
+    if (!n) return;
+    launch(tgnk::k_init_aug, unsigned((n + 255) / 256), 256, 0, s, b.p, rows, cols, ld);
+    SPD_CUDA(cudaGetLastError());
+}
+
+unsigned blocks_for(std::size_t n, int t = 256) { return unsigned((n + t - 1) / t); }
+
+// C[M,N] (ldc) = A[M,K](lda) . B[N,K]^T(ldb), optional relu / mask epilogue.
+void gemm_fwd(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N,
+              int K, const int* M_dev, cudaStream_t s, int epi = gemm::EPI_NONE,
+              const float* mask = nullptr, int ldmask = 0) {
+    gemm::Args a{};
+    a.A = A; a.B = B; a.C = C; a.M = M; a.N = N; a.K = K;
+    a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.M_dev = M_dev; a.beta = 0.f; a.epi = epi;
+    a.mask = mask; a.ldmask = ldmask; a.k_split = 1;
+    dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + gemm::BM - 1) / gemm::BM, 1);
+    if (!M || !N) return;
+    launch(gemm::gemm_kernel<false, false>, grid, gemm::NT, 0, s, a);
+    SPD_CUDA(cudaGetLastError());
+}
+
+// C[M,N] = A[M,K] . B[K,N] (data gradient through a weight), optional mask.
+void gemm_dgrad(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N,
+                int K, const int* M_dev, cudaStream_t s, int epi = gemm::EPI_NONE,
+                const float* mask = nullptr, int ldmask = 0) {
+    gemm::Args a{};
+    a.A = A; a.B = B; a.C = C; a.M = M; a.N = N; a.K = K;
+    a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.M_dev = M_dev; a.beta = 0.f; a.epi = epi;
+    a.mask = mask; a.ldmask = ldmask; a.k_split = 1;
+    dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + gemm::BM - 1) / gemm::BM, 1);
+    if (!M || !N) return;
+    launch(gemm::gemm_kernel<false, true>, grid, gemm::NT, 0, s, a);
+    SPD_CUDA(cudaGetLastError());
+}
+
+// dW[N_out, K_in] += dY[rows, N_out]^T . X[rows, K_in]  (rows reduced, split-K,
+// deterministic fixed-order reduction of the slices).
+void gemm_wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
+                int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
+                cudaStream_t s) {
+    if (!rows || !N_out || !K_in) return;
+    const int tiles = ((N_out + gemm::BM - 1) / gemm::BM) * ((K_in + gemm::BN - 1) / gemm::BN);
+    int split = std::max(1, std::min(64, (2 * 148 + tiles - 1) / tiles));
+    split = std::min(split, std::max(1, rows / 256));
+    const int ldws = ld4(K_in);
+    while (split > 1 && std::size_t(split) * N_out * ldws > ws_cap) --split;
+    gemm::Args a{};
+    a.A = dY; a.B = X; a.C = dW; a.M = N_out; a.N = K_in; a.K = rows;
+    a.lda = ldy; a.ldb = ldx; a.ldc = ldw; a.K_dev = rows_dev; a.beta = 1.f; a.epi = 0;
+    a.k_split = split; a.workspace = ws; a.ldw = ldws;
+    dim3 grid((K_in + gemm::BN - 1) / gemm::BN, (N_out + gemm::BM - 1) / gemm::BM, split);
+    launch(gemm::gemm_kernel<true, true>, grid, gemm::NT, 0, s, a);
+    SPD_CUDA(cudaGetLastError());
+    if (split > 1) {
+        const std::size_t n = std::size_t(N_out) * K_in;
+        launch(gemm::splitk_reduce, blocks_for(n), 256, 0, s, ws, split, N_out, K_in, ldws, dW, ldw, 1.f);
+        SPD_CUDA(cudaGetLastError());
+    }
+}
+
+tgnk::WorkerDev devview(Worker& w) {
+    tgnk::WorkerDev v{};
+    v.ev_src = w.ev_src.p; v.ev_dst = w.ev_dst.p; v.ev_ts = w.ev_ts.p; v.feat = w.feat.p;
+    v.adj_off = w.adj_off.p; v.adj_nbr = w.adj_nbr.p; v.adj_ev = w.adj_ev.p; v.adj_ts = w.adj_ts.p;
+    v.pool = w.pool.p; v.n_pool = w.n_pool; v.mem = w.mem.p; v.lu = w.lu.p; v.slot = w.slot.p;
+    v.lastpos = w.lastpos.p; v.pU = w.pU.p; v.pOther = w.pOther.p; v.pEv = w.pEv.p; v.pTs = w.pTs.p;
+    v.nU = w.nU.p;
+    return v;
+}
+
+void init_params_host(const ParamLayout& L, std::uint64_t seed, std::vector<float>& flat) {
+    flat.assign(L.total, 0.f);
+    for (int i = 0; i < L.T; ++i)
+        flat[L.time_w + i] = static_cast<float>(
+            L.T > 1 ? std::pow(10.0, -9.0 * double(i) / double(L.T - 1)) : 1.0);
+    const std::uint64_t s = mix64(seed);
+    const ParamLayout::Lin* lins[] = {&L.gru_ih, &L.gru_hh, &L.att_q, &L.att_kv, &L.att_o,
+                                      &L.mrg1,   &L.mrg2,   &L.dec1,  &L.dec2};
+    const int fans[] = {L.D, L.D, L.DQ, L.DK, L.DQ, L.DQ + L.D, L.D, 2 * L.D, L.D};
+    for (int t = 0; t < 9; ++t) {
+        const auto& l = *lins[t];
+        const double a = 1.0 / std::sqrt(double(fans[t]));
+        auto draw = [&](std::uint64_t tag, std::uint64_t i) {
+            const std::uint64_t h = mix64(mix64(s ^ tag) ^ i);
+            const double u = double(h >> 40) * 0x1.0p-24;
+            return static_cast<float>((2.0 * u - 1.0) * a);
+        };
+        for (int n = 0; n < l.N; ++n) {
+            for (int k = 0; k < l.K; ++k)
+                flat[l.off + std::size_t(n) * l.ld + k] = draw(t, std::uint64_t(n) * l.K + k);
+            flat[l.off + std::size_t(n) * l.ld + l.K] = draw(t + 100, n);
+        }
+    }
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- setup
+TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
+                       const std::vector<int>& workers, const std::vector<NodeId>& shared,
+                       NodeId node_count, int rank, int world, const void* nccl_id, int device)
+    : cfg_(cfg), device_(device), rank_(rank), world_(world), shared_(shared) {
+    if (cfg.d_mem < 4 || cfg.d_mem % 4 || cfg.d_time < 4 || cfg.d_time % 4 || cfg.d_edge < 0)
+        data_error("InvalidParams", "d_mem and d_time must be positive multiples of 4, d_edge >= 0");
+    if (cfg.n_heads < 1 || (cfg.d_mem + cfg.d_time) % cfg.n_heads)
+        data_error("InvalidParams", "n_heads must divide d_mem + d_time");
+    if (cfg.n_neighbors < 1 || cfg.n_neighbors > 32)
+        data_error("InvalidParams", "n_neighbors must lie in [1, 32]");
+    if (cfg.batch_size < 1) data_error("InvalidParams", "need batch_size >= 1");
+    if (world < 1 || rank < 0 || rank >= world) data_error("InvalidParams", "bad rank/world");
+    require_device(device);
+    DeviceGuard g(device);
+    SPD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors);
+    feat_seed_mixed_ = mix64(cfg.seed_feat);
+    total_workers_ = static_cast<int>(subs.g.size());
+    for (const auto& sg : subs.g)
+        all_batches_.push_back((sg.edges.size() + cfg.batch_size - 1) / cfg.batch_size);
+    epoch_steps_ = all_batches_.empty() ? 0 : *std::max_element(all_batches_.begin(), all_batches_.end());
+
+    const int D = lay_.D, F = lay_.F;
+    const int Fp = F ? (F + 7) / 8 * 8 : 0;
+    const int B = static_cast<int>(cfg.batch_size);
+    for (int wid : workers) {
+        if (wid < 0 || wid >= total_workers_) data_error("InvalidParams", "worker id out of range");
+        const SubGraph& sg = subs.g[wid];
+        auto W = std::make_unique<Worker>();
+        Worker& w = *W;
+        w.gid = wid;
+        w.nodes = sg.nodes;
+        w.N = static_cast<NodeId>(sg.nodes.size());
+        w.E = sg.edges.size();
+        w.batches = all_batches_[wid];
+        // local ids
+        std::vector<std::uint32_t> src(w.E), dst(w.E);
+        std::vector<double> ts(w.E);
+        auto loc = [&](NodeId gid) -> std::uint32_t {
+            auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), gid);
+            if (it == w.nodes.end() || *it != gid)
+                data_error("InvalidPartition", "edge endpoint outside the subgraph's node set");
+            return static_cast<std::uint32_t>(it - w.nodes.begin());
+        };
+        for (std::uint64_t k = 0; k < w.E; ++k) {
+            src[k] = loc(sg.edges[k].src);
+            dst[k] = loc(sg.edges[k].dst);
+            ts[k] = sg.edges[k].ts;
+            if (k && ts[k] < ts[k - 1])
+                data_error("NonChronological", "subgraph edges must be time-ordered");
+        }
+        // per-node time-sorted adjacency (both directions; ties keep event
+        // order, src side first — the oracle's (ts, event, role) order)
+        std::vector<std::uint64_t> off(std::size_t(w.N) + 1, 0);
+        for (std::uint64_t k = 0; k < w.E; ++k) {
+            ++off[src[k] + 1];
+            ++off[dst[k] + 1];
+        }
+        for (NodeId i = 0; i < w.N; ++i) off[i + 1] += off[i];
+        std::vector<std::uint64_t> fill(off.begin(), off.end() - 1);
+        std::vector<std::uint32_t> anbr(2 * w.E), aev(2 * w.E);
+        std::vector<double> ats(2 * w.E);
+        for (std::uint64_t k = 0; k < w.E; ++k) {  // events are time-ordered: append keeps order
+            std::uint64_t p = fill[src[k]]++;
+            anbr[p] = dst[k]; aev[p] = static_cast<std::uint32_t>(k); ats[p] = ts[k];
+            p = fill[dst[k]]++;
+            anbr[p] = src[k]; aev[p] = static_cast<std::uint32_t>(k); ats[p] = ts[k];
+        }
+        std::vector<std::uint32_t> pool(dst);
+        std::sort(pool.begin(), pool.end());
+        pool.erase(std::unique(pool.begin(), pool.end()), pool.end());
+        if (pool.empty()) pool.push_back(0);
+        w.n_pool = static_cast<std::uint32_t>(pool.size());
+        if (w.E > 0xFFFFFFFFull) data_error("InvalidParams", "partition exceeds 2^32 events");
+
+        w.ev_src.alloc(w.E); w.ev_src.upload(src.data(), w.E, stream_);
+        w.ev_dst.alloc(w.E); w.ev_dst.upload(dst.data(), w.E, stream_);
+        w.ev_ts.alloc(w.E); w.ev_ts.upload(ts.data(), w.E, stream_);
+        w.adj_off.alloc(off.size()); w.adj_off.upload(off.data(), off.size(), stream_);
+        w.adj_nbr.alloc(2 * w.E); w.adj_nbr.upload(anbr.data(), 2 * w.E, stream_);
+        w.adj_ev.alloc(2 * w.E); w.adj_ev.upload(aev.data(), 2 * w.E, stream_);
+        w.adj_ts.alloc(2 * w.E); w.adj_ts.upload(ats.data(), 2 * w.E, stream_);
+        w.pool.alloc(pool.size()); w.pool.upload(pool.data(), pool.size(), stream_);
+        // synthetic features, generated on the device from the global edge ids
+        w.feat.alloc(std::max<std::uint64_t>(1, w.E) * std::max(1, Fp));
+        if (Fp && w.E) {
+            DevBuf<std::uint64_t> eids(w.E);
+            eids.upload(sg.eids.data(), w.E, stream_);
+            launch(tgnk::k_gen_features, blocks_for(w.E * Fp), 256, 0, stream_, 
+                w.feat.p, eids.p, w.E, F, Fp, feat_seed_mixed_);
+            SPD_CUDA(cudaGetLastError());
+            SPD_CUDA(cudaStreamSynchronize(stream_));
+        }
+        const std::size_t N = std::max<std::size_t>(1, w.N);
+        w.mem.alloc(N * D); w.mem.zero(stream_);
+        w.mem_snap.alloc(N * D); w.mem_snap.zero(stream_);
+        w.lu.alloc(N); w.lu.zero(stream_);
+        w.lu_snap.alloc(N); w.lu_snap.zero(stream_);
+        w.slot.alloc(N);
+        SPD_CUDA(cudaMemsetAsync(w.slot.p, 0xFF, w.slot.bytes(), stream_));
+        w.lastpos.alloc(N);
+        SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
+        w.pU.alloc(2 * B); w.pOther.alloc(2 * B); w.pEv.alloc(2 * B); w.pTs.alloc(2 * B);
+        w.nU.alloc(1); w.nU.zero(stream_);
+        for (NodeId sidx : shared_) {
+            auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), sidx);
+            w.shared_local.push_back(it != w.nodes.end() && *it == sidx
+                                         ? static_cast<std::uint32_t>(it - w.nodes.begin())
+                                         : 0xFFFFFFFFu);
+        }
+        w.ev_host.resize(w.E);
+        for (std::uint64_t k = 0; k < w.E; ++k) w.ev_host[k] = spd_edge{src[k], dst[k], ts[k]};
+        workers_.push_back(std::move(W));
+    }
+
+    // parameters + optimiser state
+    std::vector<float> flat;
+    init_params_host(lay_, cfg.seed_init, flat);
+    params_.alloc(lay_.total); params_.upload(flat.data(), lay_.total, stream_);
+    grads_.alloc(lay_.total); grads_.zero(stream_);
+    adam_m_.alloc(lay_.total); adam_m_.zero(stream_);
+    adam_v_.alloc(lay_.total); adam_v_.zero(stream_);
+    tgrad_.alloc(2 * ld4(lay_.T)); tgrad_.zero(stream_);
+
+    // scratch for one batch
+    s_ = std::make_unique<Scratch>();
+    Scratch& s = *s_;
+    s.B = B; s.R = 3 * B; s.RK = s.R * cfg.n_neighbors; s.U = 2 * B;
+    auto& d = s.d;
+    d.D = D; d.T = lay_.T; d.F = F; d.Fp = Fp; d.DQ = lay_.DQ; d.DK = lay_.DK; d.DM = lay_.DM;
+    d.H = lay_.H; d.K = lay_.Kn;
+    d.ld_x = ld_aug(d.DM); d.ld_h = ld_aug(D); d.ld_q = ld_aug(d.DQ); d.ld_kv = ld_aug(d.DK);
+    d.ld_ctx = ld_aug(d.DQ); d.ld_m = ld_aug(d.DQ + D); d.ld_z = ld_aug(D); d.ld_din = ld_aug(2 * D);
+    d.ld_d1 = ld_aug(D); d.ld_g = ld4(3 * D);
+    const int R = s.R, RK = s.RK, U = s.U;
+    s.roots.alloc(R); s.root_t.alloc(R); s.cnt.alloc(R);
+    s.nbr_node.alloc(RK); s.nbr_ev.alloc(RK); s.nbr_dt.alloc(RK);
+    s.x_gru.alloc(std::size_t(U) * d.ld_x); init_aug(s.x_gru, U, d.DM, d.ld_x, stream_);
+    s.h_gru.alloc(std::size_t(U) * d.ld_h); init_aug(s.h_gru, U, D, d.ld_h, stream_);
+    s.Gi.alloc(std::size_t(U) * d.ld_g); s.Gh.alloc(std::size_t(U) * d.ld_g);
+    s.gsave.alloc(std::size_t(U) * 4 * D); s.mem_new.alloc(std::size_t(U) * D);
+    s.dH.alloc(std::size_t(U) * D); s.dGi.alloc(std::size_t(U) * d.ld_g); s.dGh.alloc(std::size_t(U) * d.ld_g);
+    s.dGi.zero(stream_); s.dGh.zero(stream_); s.Gi.zero(stream_); s.Gh.zero(stream_);
+    s.q_in.alloc(std::size_t(R) * d.ld_q); init_aug(s.q_in, R, d.DQ, d.ld_q, stream_);
+    s.kv_in.alloc(std::size_t(RK) * d.ld_kv); init_aug(s.kv_in, RK, d.DK, d.ld_kv, stream_);
+    s.Q.alloc(std::size_t(R) * d.DQ); s.KV.alloc(std::size_t(RK) * 2 * d.DQ);
+    s.alpha.alloc(std::size_t(R) * d.H * d.K);
+    s.ctx.alloc(std::size_t(R) * d.ld_ctx); init_aug(s.ctx, R, d.DQ, d.ld_ctx, stream_);
+    s.O.alloc(std::size_t(R) * d.DQ);
+    s.m_in.alloc(std::size_t(R) * d.ld_m); init_aug(s.m_in, R, d.DQ + D, d.ld_m, stream_);
+    s.Z1.alloc(std::size_t(R) * d.ld_z); init_aug(s.Z1, R, D, d.ld_z, stream_);
+    s.emb.alloc(std::size_t(R) * D);
+    s.d_in.alloc(std::size_t(2 * B) * d.ld_din); init_aug(s.d_in, 2 * B, 2 * D, d.ld_din, stream_);
+    s.D1.alloc(std::size_t(2 * B) * d.ld_d1); init_aug(s.D1, 2 * B, D, d.ld_d1, stream_);
+    s.logits.alloc(2 * B); s.lossv.alloc(2 * B);
+    s.dlogit.alloc(std::size_t(2 * B) * 4); s.dlogit.zero(stream_);
+    s.dD1.alloc(std::size_t(2 * B) * D); s.dd_in.alloc(std::size_t(2 * B) * d.ld_din);
+    s.d_emb.alloc(std::size_t(R) * D); s.dZ1.alloc(std::size_t(R) * D);
+    s.dm_in.alloc(std::size_t(R) * d.ld_m); s.dctx.alloc(std::size_t(R) * d.DQ);
+    s.dQ.alloc(std::size_t(R) * d.DQ); s.dKV.alloc(std::size_t(RK) * 2 * d.DQ);
+    s.dkv_in.alloc(std::size_t(RK) * d.ld_kv); s.dq_in.alloc(std::size_t(R) * d.ld_q);
+    s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
+    s.trows = 256;
+    s.tblocks = (R * (1 + d.K) + s.trows - 1) / s.trows;
+    s.tpart.alloc(std::size_t(s.tblocks) * 2 * d.T);
+    s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+
+    if (world_ > 1) {
+        if (!nccl_id) usage_error("world > 1 needs an NCCL unique id");
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        ncclComm_t comm;
+        SPD_NCCL(ncclCommInitRank(&comm, world_, id, rank_));
+        nccl_ = comm;
+    }
+}
+
+int TGNTrainer::feat_stride() const { return s_->d.Fp; }
+
+TGNTrainer::~TGNTrainer() {
+    if (stage_) cudaFreeHost(stage_);
+    if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+Worker& TGNTrainer::worker(int w) {
+    for (auto& p : workers_)
+        if (p->gid == w) return *p;
+    usage_error("worker " + std::to_string(w) + " is not owned by this trainer");
+}
+
+void TGNTrainer::timed(const char* name, const std::function<void()>& f) {
+    if (!profile_) {
+        f();
+        return;
+    }
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, stream_);
+    f();
+    cudaEventRecord(b, stream_);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    times_.ms.emplace_back(name, ms);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+}
+
+// -------------------------------------------------------------- schedule
+void TGNTrainer::begin_epoch(int epoch) {
+    DeviceGuard g(device_);
+    epoch_ = epoch;
+    step_in_epoch_ = 0;
+    for (auto& wp : workers_) {
+        Worker& w = *wp;
+        w.pos = 0;
+        w.loops = 0;
+        w.done = w.batches == 0;
+        if (w.batches == 0) {  // vacuous: snapshot of the untouched state (pac_sim.cpp:224-230)
+            SPD_CUDA(cudaMemcpyAsync(w.mem_snap.p, w.mem.p, w.mem.bytes(), cudaMemcpyDeviceToDevice, stream_));
+            SPD_CUDA(cudaMemcpyAsync(w.lu_snap.p, w.lu.p, w.lu.bytes(), cudaMemcpyDeviceToDevice, stream_));
+            w.loops = 1;
+        }
+    }
+}
+
+void TGNTrainer::gru_forward(Worker& w, bool train) {
+    Scratch& s = *s_;
+    const auto& d = s.d;
+    const auto wd = devview(w);
+    const float* P = params_.p;
+    launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
+        wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
+    SPD_CUDA(cudaGetLastError());
+    gemm_fwd(s.x_gru.p, d.ld_x, P + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, 3 * d.D,
+             d.DM + 1, w.nU.p, stream_);
+    gemm_fwd(s.h_gru.p, d.ld_h, P + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, 3 * d.D,
+             d.D + 1, w.nU.p, stream_);
+    launch(tgnk::k_gru_fwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, stream_, 
+        wd, d, s.Gi.p, s.Gh.p, s.h_gru.p, train ? s.gsave.p : nullptr, s.mem_new.p);
+    SPD_CUDA(cudaGetLastError());
+}
+
+void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
+    Scratch& s = *s_;
+    const auto& d = s.d;
+    const std::uint64_t lo = w.pos * cfg_.batch_size;
+    const int B = static_cast<int>(std::min<std::uint64_t>(w.E, lo + cfg_.batch_size) - lo);
+    w.last_b = B;
+    const int R = 3 * B, RK = R * d.K;
+    const auto wd = devview(w);
+    float* P = params_.p;
+    float* G = grads_.p;
+    cudaStream_t st = stream_;
+    if (w.pos == 0) {  // loop_start: reset (pac_sim.cpp:238)
+        w.mem.zero(st);
+        w.lu.zero(st);
+        w.nU.zero(st);
+    }
+    const std::uint64_t nb = neg_base(cfg_.seed_neg, std::uint64_t(epoch_), std::uint64_t(w.gid),
+                                      step_in_epoch);
+    timed("roots_nbrs", [&] {
+        launch(tgnk::k_roots_nbrs, blocks_for(R, 128), 128, 0, st, wd, lo, B, nb, d.K, s.roots.p,
+               s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
+    });
+    timed("gru_fwd", [&] { gru_forward(w, true); });
+    timed("embed_gather", [&] {
+        launch(tgnk::k_embed_gather, blocks_for(std::size_t(R) * (1 + d.K) * 32), 256, 0, st, 
+            wd, d, R, P + lay_.time_w, P + lay_.time_b, s.roots.p, s.nbr_node.p, s.nbr_ev.p,
+            s.nbr_dt.p, s.cnt.p, s.mem_new.p, s.q_in.p, s.kv_in.p);
+    });
+    timed("gemm_q", [&] {
+        gemm_fwd(s.q_in.p, d.ld_q, P + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.DQ, R, d.DQ,
+                 d.DQ + 1, nullptr, st);
+    });
+    timed("gemm_kv", [&] {
+        gemm_fwd(s.kv_in.p, d.ld_kv, P + lay_.att_kv.off, lay_.att_kv.ld, s.KV.p, 2 * d.DQ, RK,
+                 2 * d.DQ, d.DK + 1, nullptr, st);
+    });
+    const std::size_t attn_smem = std::size_t(8) * d.H * d.K * sizeof(float);
+    timed("attn_fwd", [&] {
+        launch(tgnk::k_attn_fwd, blocks_for(std::size_t(R) * 32), 256, attn_smem, st, 
+            d, R, s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
+    });
+    timed("head_fwd", [&] {
+        gemm_fwd(s.ctx.p, d.ld_ctx, P + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
+                 d.DQ + 1, nullptr, st);
+        launch(tgnk::k_merge_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, 
+            wd, d, R, s.roots.p, s.cnt.p, s.O.p, s.mem_new.p, s.m_in.p);
+        gemm_fwd(s.m_in.p, d.ld_m, P + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
+                 d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU);
+        gemm_fwd(s.Z1.p, d.ld_z, P + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
+                 nullptr, st);
+        launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, d, B, s.emb.p,
+                                                                                 s.d_in.p);
+        gemm_fwd(s.d_in.p, d.ld_din, P + lay_.dec1.off, lay_.dec1.ld, s.D1.p, d.ld_d1, 2 * B, d.D,
+                 2 * d.D + 1, nullptr, st, gemm::EPI_RELU);
+        launch(tgnk::k_dec_head, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, 
+            d, B, s.D1.p, P + lay_.dec2.off, s.dlogit.p, s.lossv.p, s.dD1.p, s.logits.p);
+    });
+    // per-worker loss slot
+    int slot_idx = 0;
+    for (std::size_t k = 0; k < workers_.size(); ++k)
+        if (workers_[k].get() == &w) slot_idx = static_cast<int>(k);
+    launch(tgnk::k_sum_loss, 1, 1024, 0, st, s.lossv.p, 2 * B, s.loss.p + slot_idx);
+    SPD_CUDA(cudaGetLastError());
+
+    // ------------------------------------------------------------ backward
+    timed("head_bwd", [&] {
+        gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
+                   2 * B, nullptr, s.ws.p, s.ws.n, st);
+        gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
+                   2 * d.D + 1, 2 * B, nullptr, s.ws.p, s.ws.n, st);
+        gemm_dgrad(s.dD1.p, d.D, P + lay_.dec1.off, lay_.dec1.ld, s.dd_in.p, d.ld_din, 2 * B,
+                   2 * d.D, d.D, nullptr, st);
+        launch(tgnk::k_dec_scatter, blocks_for(std::size_t(B) * 32), 256, 0, st, d, B, s.dd_in.p,
+                                                                             s.d_emb.p);
+        // merge layer 2 (relu mask from Z1), layer 1
+        gemm_wgrad(s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off, lay_.mrg2.ld, d.D, d.D + 1,
+                   R, nullptr, s.ws.p, s.ws.n, st);
+        gemm_dgrad(s.d_emb.p, d.D, P + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
+                   nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z);
+        gemm_wgrad(s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off, lay_.mrg1.ld, d.D,
+                   d.DQ + d.D + 1, R, nullptr, s.ws.p, s.ws.n, st);
+        gemm_dgrad(s.dZ1.p, d.D, P + lay_.mrg1.off, lay_.mrg1.ld, s.dm_in.p, d.ld_m, R,
+                   d.DQ + d.D, d.D, nullptr, st);
+        launch(tgnk::k_mask_rows, blocks_for(std::size_t(R) * 32), 256, 0, st, s.dm_in.p, R, d.DQ,
+                                                                          d.ld_m, s.cnt.p);
+        // output projection
+        gemm_wgrad(s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
+                   d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, st);
+        gemm_dgrad(s.dm_in.p, d.ld_m, P + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.DQ, R, d.DQ,
+                   d.DQ, nullptr, st);
+    });
+    timed("attn_bwd", [&] {
+        launch(tgnk::k_attn_bwd, blocks_for(std::size_t(R) * 32), 256, attn_smem, st, 
+            d, R, s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.DQ, s.dQ.p, s.dKV.p);
+    });
+    timed("gemm_kv_wgrad", [&] {
+        gemm_wgrad(s.dKV.p, 2 * d.DQ, s.kv_in.p, d.ld_kv, G + lay_.att_kv.off, lay_.att_kv.ld,
+                   2 * d.DQ, d.DK + 1, RK, nullptr, s.ws.p, s.ws.n, st);
+    });
+    timed("gemm_kv_dgrad", [&] {
+        gemm_dgrad(s.dKV.p, 2 * d.DQ, P + lay_.att_kv.off, lay_.att_kv.ld, s.dkv_in.p, d.ld_kv, RK,
+                   d.DK, 2 * d.DQ, nullptr, st);
+    });
+    timed("q_bwd", [&] {
+        gemm_wgrad(s.dQ.p, d.DQ, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
+                   d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, st);
+        gemm_dgrad(s.dQ.p, d.DQ, P + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
+                   d.DQ, nullptr, st);
+    });
+    timed("mem_time_bwd", [&] {
+        s.dH.zero(st);
+        launch(tgnk::k_mem_grad, blocks_for(std::size_t(R) * (1 + d.K) * 32), 256, 0, st, 
+            wd, d, R, s.roots.p, s.nbr_node.p, s.cnt.p, s.dq_in.p, s.dm_in.p, s.dkv_in.p, s.dH.p);
+        const int tb = (R * (1 + d.K) + s.trows - 1) / s.trows;
+        launch(tgnk::k_time_grad_partial, tb, 128, 0, st, d, R, s.cnt.p, s.nbr_dt.p, s.dkv_in.p,
+                                                      s.dq_in.p, P + lay_.time_w,
+                                                      P + lay_.time_b, s.trows, s.tpart.p);
+        launch(tgnk::k_time_grad_final, blocks_for(2 * d.T), 256, 0, st, d.T, tb, s.tpart.p, tgrad_.p);
+    });
+    timed("gru_bwd", [&] {
+        launch(tgnk::k_gru_bwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, st, 
+            wd, d, s.dH.p, s.gsave.p, s.h_gru.p, s.dGi.p, s.dGh.p);
+        gemm_wgrad(s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
+                   3 * d.D, d.DM + 1, s.U, w.nU.p, s.ws.p, s.ws.n, st);
+        gemm_wgrad(s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
+                   3 * d.D, d.D + 1, s.U, w.nU.p, s.ws.p, s.ws.n, st);
+    });
+    // persist this batch's memory update and store its last messages now,
+    // while the scratch still holds this worker's rows (K11, K3)
+    timed("post", [&] {
+        launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
+        launch(tgnk::k_pending, 1, 1024, 0, st, wd, lo, B);
+    });
+    SPD_CUDA(cudaGetLastError());
+}
+
+void TGNTrainer::flush_pending(Worker& w) {
+    // loop end: apply the pending messages without gradient, persist
+    gru_forward(w, false);
+    const auto wd = devview(w);
+    launch(tgnk::k_persist, blocks_for(std::size_t(s_->U) * 32), 256, 0, stream_, wd, lay_.D,
+           s_->mem_new.p);
+    w.nU.zero(stream_);
+}
+
+std::uint64_t kernel_launches() { return g_kernel_launches.load(); }
+
+// n lockstep global steps (wrapping into the next epoch when one ends),
+// bracketed by CUDA events on the trainer's stream: device time in ms.
+float TGNTrainer::run_steps(std::uint64_t n) {
+    DeviceGuard g(device_);
+    cudaEvent_t a, b;
+    SPD_CUDA(cudaEventCreate(&a));
+    SPD_CUDA(cudaEventCreate(&b));
+    SPD_CUDA(cudaEventRecord(a, stream_));
+    for (std::uint64_t k = 0; k < n; ++k) {
+        if (step_in_epoch_ >= epoch_steps_) {
+            end_epoch();
+            begin_epoch(epoch_ + 1);
+        }
+        step(nullptr);
+    }
+    SPD_CUDA(cudaEventRecord(b, stream_));
+    SPD_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    SPD_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+}
+
+// End-to-end step: each local worker's next batch (events in local ids and
+// bf16 feature rows) is copied from (pinned) host memory into its device
+// stream window, the step runs, and the per-worker losses come back.
+void TGNTrainer::step_host(const spd_edge* const* events, const std::uint16_t* const* feats,
+                           float* loss_out) {
+    DeviceGuard g(device_);
+    if (step_in_epoch_ >= epoch_steps_) {
+        end_epoch();
+        begin_epoch(epoch_ + 1);
+    }
+    const int Fp = s_->d.Fp;
+    for (std::size_t k = 0; k < workers_.size(); ++k) {
+        Worker& w = *workers_[k];
+        if (w.batches == 0) continue;
+        const std::uint64_t lo = w.pos * cfg_.batch_size;
+        const std::uint64_t B = std::min<std::uint64_t>(w.E, lo + cfg_.batch_size) - lo;
+        // events arrive as {src, dst, ts}; scatter into pinned SoA staging
+        if (stage_bytes_ < B * 16) {
+            if (stage_) cudaFreeHost(stage_);
+            SPD_CUDA(cudaHostAlloc(&stage_, B * 16, cudaHostAllocDefault));
+            stage_bytes_ = B * 16;
+        }
+        SPD_CUDA(cudaStreamSynchronize(stream_));  // staging reuse across workers/steps
+        const spd_edge* e = events[k];
+        std::uint32_t* hs = reinterpret_cast<std::uint32_t*>(stage_);
+        std::uint32_t* hd = hs + B;
+        double* ht = reinterpret_cast<double*>(hd + B);
+        for (std::uint64_t i = 0; i < B; ++i) {
+            hs[i] = e[i].src;
+            hd[i] = e[i].dst;
+            ht[i] = e[i].ts;
+        }
+        SPD_CUDA(cudaMemcpyAsync(w.ev_src.p + lo, hs, B * 4, cudaMemcpyHostToDevice, stream_));
+        SPD_CUDA(cudaMemcpyAsync(w.ev_dst.p + lo, hd, B * 4, cudaMemcpyHostToDevice, stream_));
+        SPD_CUDA(cudaMemcpyAsync(w.ev_ts.p + lo, ht, B * 8, cudaMemcpyHostToDevice, stream_));
+        if (Fp && feats && feats[k])
+            SPD_CUDA(cudaMemcpyAsync(w.feat.p + lo * Fp, feats[k], B * Fp * 2,
+                                     cudaMemcpyHostToDevice, stream_));
+        h2d_bytes_ += B * 16 + (Fp ? B * Fp * 2 : 0);
+    }
+    step(loss_out);
+    d2h_bytes_ += workers_.size() * sizeof(float);
+}
+
+void TGNTrainer::worker_post(Worker& w) {
+    ++w.pos;
+    if (w.pos == w.batches) {  // loop_end: flush (new params) + snapshot (pac_sim.cpp:248-255)
+        flush_pending(w);
+        SPD_CUDA(cudaMemcpyAsync(w.mem_snap.p, w.mem.p, w.mem.bytes(), cudaMemcpyDeviceToDevice, stream_));
+        SPD_CUDA(cudaMemcpyAsync(w.lu_snap.p, w.lu.p, w.lu.bytes(), cudaMemcpyDeviceToDevice, stream_));
+        ++w.loops;
+        w.done = true;
+        w.pos = 0;
+    }
+}
+
+void TGNTrainer::allreduce_grads() {
+    // time-encoder grads (f64 accumulators) into the flat buffer first
+    launch(tgnk::k_time_grad_apply, blocks_for(lay_.T), 256, 0, stream_, 
+        lay_.T, tgrad_.p, grads_.p + lay_.time_w, grads_.p + lay_.time_b);
+    SPD_CUDA(cudaGetLastError());
+    if (world_ > 1) {
+        SPD_NCCL(ncclAllReduce(grads_.p, grads_.p, lay_.total, ncclFloat, ncclSum,
+                               static_cast<ncclComm_t>(nccl_), stream_));
+    }
+}
+
+void TGNTrainer::adam() {
+    ++adam_t_;
+    const double b1 = cfg_.beta1, b2 = cfg_.beta2;
+    const float bc1 = static_cast<float>(1.0 - std::pow(b1, double(adam_t_)));
+    const float bc2 = static_cast<float>(1.0 - std::pow(b2, double(adam_t_)));
+    launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, stream_, 
+        params_.p, grads_.p, adam_m_.p, adam_v_.p, lay_.total, float(total_workers_), cfg_.lr,
+        cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2), bc1,
+        bc2, cfg_.adam_eps);
+    SPD_CUDA(cudaGetLastError());
+}
+
+void TGNTrainer::step(float* loss_out) {
+    DeviceGuard g(device_);
+    ++step_in_epoch_;
+    times_.ms.clear();
+    grads_.zero(stream_);
+    tgrad_.zero(stream_);
+    for (std::size_t k = 0; k < workers_.size(); ++k) {
+        Worker& w = *workers_[k];
+        if (w.batches == 0) continue;
+        worker_step(w, step_in_epoch_);
+        if (debug_) {  // taps before the next worker reuses the scratch
+            const std::uint64_t B = w.last_b;
+            const int D = lay_.D, K = lay_.Kn;
+            w.tap_emb.resize(3 * B * D);
+            w.tap_roots.resize(3 * B);
+            w.tap_nbr.resize(3 * B * K);
+            s_->emb.download(w.tap_emb.data(), w.tap_emb.size(), stream_);
+            s_->roots.download(w.tap_roots.data(), w.tap_roots.size(), stream_);
+            s_->nbr_node.download(w.tap_nbr.data(), w.tap_nbr.size(), stream_);
+            SPD_CUDA(cudaMemcpyAsync(&w.tap_loss, s_->loss.p + k, sizeof(float),
+                                     cudaMemcpyDeviceToHost, stream_));
+            SPD_CUDA(cudaStreamSynchronize(stream_));
+        }
+    }
+    timed("allreduce", [&] { allreduce_grads(); });
+    timed("adam", [&] { adam(); });
+    for (auto& wp : workers_)
+        if (wp->batches > 0) worker_post(*wp);
+    if (loss_out) {
+        std::vector<float> l(workers_.size());
+        s_->loss.download(l.data(), l.size(), stream_);
+        SPD_CUDA(cudaStreamSynchronize(stream_));
+        for (std::size_t k = 0; k < l.size(); ++k)
+            loss_out[k] = workers_[k]->batches > 0 ? l[k] : std::nanf("");
+    }
+}
+
+void TGNTrainer::end_epoch() {
+    DeviceGuard g(device_);
+    for (auto& wp : workers_) {  // drop partial loops (pac_sim.cpp:259)
+        Worker& w = *wp;
+        SPD_CUDA(cudaMemcpyAsync(w.mem.p, w.mem_snap.p, w.mem.bytes(), cudaMemcpyDeviceToDevice, stream_));
+        SPD_CUDA(cudaMemcpyAsync(w.lu.p, w.lu_snap.p, w.lu.bytes(), cudaMemcpyDeviceToDevice, stream_));
+        w.nU.zero(stream_);
+    }
+    sync_shared();
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void TGNTrainer::run_epoch(int epoch, double* mean_loss) {
+    begin_epoch(epoch);
+    std::vector<float> l(workers_.size());
+    double sum = 0.0;
+    std::uint64_t n = 0;
+    for (std::uint64_t k = 0; k < epoch_steps_; ++k) {
+        step(mean_loss ? l.data() : nullptr);
+        if (mean_loss)
+            for (float v : l)
+                if (!std::isnan(v)) {
+                    sum += v;
+                    ++n;
+                }
+    }
+    end_epoch();
+    if (mean_loss) *mean_loss = n ? sum / double(n) : 0.0;
+}
+
+// ---------------------------------------------------------- introspection
+void TGNTrainer::get_params(float* out) const {
+    DeviceGuard g(device_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+    params_.download(out, lay_.total, stream_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+void TGNTrainer::set_params(const float* in) {
+    DeviceGuard g(device_);
+    params_.upload(in, lay_.total, stream_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+void TGNTrainer::get_grads(float* out) const {
+    DeviceGuard g(device_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+    grads_.download(out, lay_.total, stream_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+    // the buffer holds the all-reduced SUM; report the applied mean
+    for (std::size_t i = 0; i < lay_.total; ++i) out[i] /= float(total_workers_);
+}
+void TGNTrainer::get_memory(int wid, float* mem, double* lu) {
+    Worker& w = worker(wid);
+    DeviceGuard g(device_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+    if (mem) w.mem.download(mem, std::size_t(w.N) * lay_.D, stream_);
+    if (lu) w.lu.download(lu, w.N, stream_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+void TGNTrainer::set_memory(int wid, const float* mem, const double* lu) {
+    Worker& w = worker(wid);
+    DeviceGuard g(device_);
+    if (mem) w.mem.upload(mem, std::size_t(w.N) * lay_.D, stream_);
+    if (lu) w.lu.upload(lu, w.N, stream_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+void TGNTrainer::last_step(int wid, std::uint64_t* b, float* emb, std::uint32_t* negs,
+                           std::uint32_t* nbr, float* loss) {
+    Worker& w = worker(wid);
+    if (!debug_) usage_error("debug taps are off (spd_tgn_set_debug)");
+    const std::uint64_t B = w.last_b;
+    if (b) *b = B;
+    if (emb) std::copy(w.tap_emb.begin(), w.tap_emb.end(), emb);
+    if (loss) *loss = w.tap_loss;
+    if (negs)
+        for (std::uint64_t i = 0; i < B; ++i) negs[i] = w.nodes[w.tap_roots[2 * B + i]];
+    if (nbr)
+        for (std::size_t k = 0; k < w.tap_nbr.size(); ++k)
+            nbr[k] = w.tap_nbr[k] == tgnk::kPad ? 0xFFFFFFFFu : w.nodes[w.tap_nbr[k]];
+}
+
+// ----------------------------------------------------- shared-node sync
+// Epoch-end sync of SEP's shared hubs (pac_sim.cpp:162-203) across every
+// worker — local workers in order, then NCCL across processes. Average:
+// mean row + max clock, skipped where all copies agree bit for bit; max-ts:
+// the freshest copy, ties to the lowest worker id.
+namespace {
+__global__ void k_sync_pack(const float* mem, const double* lu, const std::uint32_t* rows, int S,
+                            int D, int first, float* sum, float* mn, float* mx, double* ts_max) {
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)S * (D + 1)) return;
+    const int sidx = i / (D + 1), c = i % (D + 1);
+    const std::uint32_t r = rows[sidx];
+    if (c == D) {
+        const double t = r == 0xFFFFFFFFu ? 0.0 : lu[r];
+        ts_max[sidx] = first ? t : fmax(ts_max[sidx], t);
+        // clock agreement travels as min/max of the f64 clock in mn/mx tail
+        return;
+    }
+    const float v = r == 0xFFFFFFFFu ? 0.f : mem[(std::size_t)r * D + c];
+    const std::size_t o = (std::size_t)sidx * D + c;
+    if (first) {
+        sum[o] = v;
+        mn[o] = v;
+        mx[o] = v;
+    } else {
+        sum[o] = sum[o] + v;
+        mn[o] = fminf(mn[o], v);
+        mx[o] = fmaxf(mx[o], v);
+    }
+}
+__global__ void k_sync_ts_minmax(const double* lu, const std::uint32_t* rows, int S, int first,
+                                 double* tmin, double* tmax) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    const double t = rows[i] == 0xFFFFFFFFu ? 0.0 : lu[rows[i]];
+    tmin[i] = first ? t : fmin(tmin[i], t);
+    tmax[i] = first ? t : fmax(tmax[i], t);
+}
+__global__ void k_sync_apply_avg(float* mem, double* lu, const std::uint32_t* rows, int S, int D,
+                                 const float* sum, const float* mn, const float* mx,
+                                 const double* tmin, const double* tmax, float inv_w) {
+    const int sidx = blockIdx.x;
+    if (sidx >= S) return;
+    const std::uint32_t r = rows[sidx];
+    if (r == 0xFFFFFFFFu) return;
+    __shared__ int disagree;
+    if (threadIdx.x == 0) disagree = tmin[sidx] != tmax[sidx];
+    __syncthreads();
+    for (int c = threadIdx.x; c < D; c += blockDim.x)
+        if (mn[(std::size_t)sidx * D + c] != mx[(std::size_t)sidx * D + c]) disagree = 1;
+    __syncthreads();
+    if (!disagree) return;
+    for (int c = threadIdx.x; c < D; c += blockDim.x)
+        mem[(std::size_t)r * D + c] = sum[(std::size_t)sidx * D + c] * inv_w;
+    if (threadIdx.x == 0) lu[r] = tmax[sidx];
+}
+__global__ void k_sync_owner(const double* lu, const std::uint32_t* rows, int S, const double* tmax,
+                             int gid, int* owner) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= S) return;
+    const double t = rows[i] == 0xFFFFFFFFu ? 0.0 : lu[rows[i]];
+    if (t == tmax[i] && gid < owner[i]) owner[i] = gid;
+}
+__global__ void k_sync_owner_pack(const float* mem, const std::uint32_t* rows, int S, int D,
+                                  const int* owner, int gid, float* sum) {
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)S * D) return;
+    const int sidx = i / D, c = i % D;
+    if (owner[sidx] != gid) return;
+    const std::uint32_t r = rows[sidx];
+    sum[i] = r == 0xFFFFFFFFu ? 0.f : mem[(std::size_t)r * D + c];
+}
+__global__ void k_sync_apply_max(float* mem, double* lu, const std::uint32_t* rows, int S, int D,
+                                 const float* rowv, const double* tmax) {
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)S * D) return;
+    const int sidx = i / D, c = i % D;
+    const std::uint32_t r = rows[sidx];
+    if (r == 0xFFFFFFFFu) return;
+    mem[(std::size_t)r * D + c] = rowv[i];
+    if (c == 0) lu[r] = tmax[sidx];
+}
+}  // namespace
+
+void TGNTrainer::sync_shared() {
+    const int S = static_cast<int>(shared_.size());
+    if (total_workers_ < 2 || S == 0) return;
+    const int D = lay_.D;
+    cudaStream_t st = stream_;
+    DevBuf<float> sum(std::size_t(S) * D), mn(std::size_t(S) * D), mx(std::size_t(S) * D);
+    DevBuf<double> tmin(S), tmax(S);
+    std::vector<DevBuf<std::uint32_t>> rows(workers_.size());
+    for (std::size_t k = 0; k < workers_.size(); ++k) {
+        rows[k].alloc(S);
+        rows[k].upload(workers_[k]->shared_local.data(), S, st);
+    }
+    // local reduction in worker order (the reference's summation order)
+    const bool have_local = !workers_.empty();
+    if (!have_local) {
+        sum.zero(st);
+        SPD_CUDA(cudaMemsetAsync(mn.p, 0x7F, mn.bytes(), st));   // +large
+        SPD_CUDA(cudaMemsetAsync(mx.p, 0xFF, mx.bytes(), st));   // NaN-free -large
+    }
+    for (std::size_t k = 0; k < workers_.size(); ++k) {
+        Worker& w = *workers_[k];
+        launch(k_sync_pack, blocks_for(std::size_t(S) * (D + 1)), 256, 0, st, 
+            w.mem.p, w.lu.p, rows[k].p, S, D, k == 0, sum.p, mn.p, mx.p, tmax.p);
+        launch(k_sync_ts_minmax, blocks_for(S), 256, 0, st, w.lu.p, rows[k].p, S, k == 0, tmin.p, tmax.p);
+    }
+    SPD_CUDA(cudaGetLastError());
+    ncclComm_t comm = static_cast<ncclComm_t>(nccl_);
+    if (cfg_.sync_average) {
+        if (world_ > 1) {
+            SPD_NCCL(ncclGroupStart());
+            SPD_NCCL(ncclAllReduce(sum.p, sum.p, sum.n, ncclFloat, ncclSum, comm, st));
+            SPD_NCCL(ncclAllReduce(mn.p, mn.p, mn.n, ncclFloat, ncclMin, comm, st));
+            SPD_NCCL(ncclAllReduce(mx.p, mx.p, mx.n, ncclFloat, ncclMax, comm, st));
+            SPD_NCCL(ncclAllReduce(tmin.p, tmin.p, S, ncclDouble, ncclMin, comm, st));
+            SPD_NCCL(ncclAllReduce(tmax.p, tmax.p, S, ncclDouble, ncclMax, comm, st));
+            SPD_NCCL(ncclGroupEnd());
+        }
+        for (std::size_t k = 0; k < workers_.size(); ++k) {
+            Worker& w = *workers_[k];
+            launch(k_sync_apply_avg, S, 128, 0, st, w.mem.p, w.lu.p, rows[k].p, S, D, sum.p, mn.p, mx.p,
+                                                tmin.p, tmax.p, 1.f / float(total_workers_));
+        }
+    } else {
+        if (world_ > 1) SPD_NCCL(ncclAllReduce(tmax.p, tmax.p, S, ncclDouble, ncclMax, comm, st));
+        DevBuf<int> owner(S);
+        SPD_CUDA(cudaMemsetAsync(owner.p, 0x7F, owner.bytes(), st));
+        for (std::size_t k = 0; k < workers_.size(); ++k)
+            launch(k_sync_owner, blocks_for(S), 256, 0, st, workers_[k]->lu.p, rows[k].p, S, tmax.p,
+                                                        workers_[k]->gid, owner.p);
+        if (world_ > 1) SPD_NCCL(ncclAllReduce(owner.p, owner.p, S, ncclInt32, ncclMin, comm, st));
+        sum.zero(st);
+        for (std::size_t k = 0; k < workers_.size(); ++k)
+            launch(k_sync_owner_pack, blocks_for(std::size_t(S) * D), 256, 0, st, 
+                workers_[k]->mem.p, rows[k].p, S, D, owner.p, workers_[k]->gid, sum.p);
+        if (world_ > 1) SPD_NCCL(ncclAllReduce(sum.p, sum.p, sum.n, ncclFloat, ncclSum, comm, st));
+        for (std::size_t k = 0; k < workers_.size(); ++k)
+            launch(k_sync_apply_max, blocks_for(std::size_t(S) * D), 256, 0, st, 
+                workers_[k]->mem.p, workers_[k]->lu.p, rows[k].p, S, D, sum.p, tmax.p);
+    }
+    SPD_CUDA(cudaGetLastError());
+    SPD_CUDA(cudaStreamSynchronize(st));
+}
+
+void TGNTrainer::evaluate(int, const spd_edge*, const std::uint64_t*, std::uint64_t, std::uint64_t,
+                          float*, float*) {
+    internal_error("NotImplemented", "evaluation lands with the eval-routing row (SURVEY 8f #2)");
+}
+
+}  // namespace spd
