@@ -325,6 +325,12 @@ spd_status spd_tgn_io_bytes(const spd_tgn_trainer* t, uint64_t* h2d, uint64_t* d
  * edges eids[0..n): the bytes spd_tgn_step_host expects. */
 spd_status spd_edge_features_bf16(uint64_t seed, const uint64_t* eids, uint64_t n, int32_t F,
                                   int32_t stride, uint16_t* out);
+/* Test hook: one projection GEMM on caller-owned DEVICE buffers (row-major fp32).
+ * impl 0 = FP32 FFMA, 1 = tcgen05 TF32; which 0: C = A.B^T, 1: C = A.B,
+ * 2: C += A^T.B (reduction over the K rows; ws = split-K workspace). */
+spd_status spd_debug_gemm(int32_t impl, int32_t which, const float* A, int32_t lda, const float* B,
+                          int32_t ldb, float* C, int32_t ldc, int32_t M, int32_t N, int32_t K,
+                          float* ws, uint64_t ws_floats);
 /* Process-wide count of kernel launches issued by the TGN path. */
 uint64_t spd_kernel_launches(void);
 

@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
 }
 
 // Fixed-order reduction of split-K partials into C (deterministic).
-__global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, int ldw,
+static __global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, int ldw,
                               float* __restrict__ C, int ldc, float beta) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)M * N) return;

@@ -76,6 +76,8 @@ struct Worker {
 struct Scratch;  // per-step activations (sized for one batch)
 
 std::uint64_t kernel_launches();  // process-wide count of TGN-path kernel launches
+int debug_gemm(int impl, int which, const float* A, int lda, const float* B, int ldb, float* C,
+               int ldc, int M, int N, int K, float* ws, std::size_t ws_cap);
 
 class TGNTrainer {
 public:

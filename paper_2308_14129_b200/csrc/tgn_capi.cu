@@ -147,6 +147,12 @@ spd_status spd_tgn_io_bytes(const spd_tgn_trainer* t, uint64_t* h2d, uint64_t* d
 }
 uint64_t spd_kernel_launches(void) { return kernel_launches(); }
 
+spd_status spd_debug_gemm(int32_t impl, int32_t which, const float* A, int32_t lda, const float* B,
+                          int32_t ldb, float* C, int32_t ldc, int32_t M, int32_t N, int32_t K,
+                          float* ws, uint64_t ws_floats) {
+    GUARD({ debug_gemm(impl, which, A, lda, B, ldb, C, ldc, M, N, K, ws, ws_floats); });
+}
+
 spd_status spd_edge_features_bf16(uint64_t seed, const uint64_t* eids, uint64_t n, int32_t F,
                                   int32_t stride, uint16_t* out) {
     GUARD({

@@ -367,43 +367,62 @@ __global__ void k_mem_grad(WorkerDev w, Dims d, int R, const std::uint32_t* root
 // Time-encoder gradients: per block, f64 column partials over a chunk of rows
 // (kv rows: d/dw = -sin(ph) dt g, d/db = -sin(ph) g; query rows: phi(0)=cos(b)).
 // part: [nblocks][2T] (w then b).
+// blockDim = (32 columns, 8 row lanes); block covers 32 columns x rows_per_block
+// rows; f64 accumulation, fixed-order in-block reduction -> part[block][2T].
 __global__ void k_time_grad_partial(Dims d, int R, const int* cnt, const double* nbr_dt,
                                     const float* dkv_in, const float* dq_in, const float* time_w,
                                     const float* time_b, int rows_per_block, double* part) {
+    __shared__ double red[2][8][33];
     const int total = R * (1 + d.K);
+    const int c = blockIdx.y * 32 + threadIdx.x;
     const int r0 = blockIdx.x * rows_per_block;
     const int r1 = min(total, r0 + rows_per_block);
-    for (int c = threadIdx.x; c < d.T; c += blockDim.x) {
+    double gw = 0.0, gb = 0.0;
+    if (c < d.T) {
         const float wc = time_w[c], bc = time_b[c];
-        double gw = 0.0, gb = 0.0;
         const double sin_b = sin((double)bc);
-        for (int row = r0; row < r1; ++row) {
+        for (int row = r0 + threadIdx.y; row < r1; row += blockDim.y) {
             if (row < R) {
-                const double g = dq_in[(std::size_t)row * d.ld_q + d.D + c];
-                gb -= sin_b * g;
+                gb -= sin_b * (double)dq_in[(std::size_t)row * d.ld_q + d.D + c];
             } else {
                 const int kr = row - R;
                 const int r = kr / d.K, j = kr % d.K;
                 if (j >= cnt[r]) continue;
                 const double dt = nbr_dt[kr];
                 const double g = dkv_in[(std::size_t)kr * d.ld_kv + d.D + d.F + c];
-                const double ph = __dadd_rn(__dmul_rn((double)wc, dt), (double)bc);
-                const double sn = sin(ph);
+                const double sn = (double)time_sin(wc, bc, dt);
                 gw -= sn * dt * g;
                 gb -= sn * g;
             }
         }
-        part[(std::size_t)blockIdx.x * 2 * d.T + c] = gw;
-        part[(std::size_t)blockIdx.x * 2 * d.T + d.T + c] = gb;
+    }
+    red[0][threadIdx.y][threadIdx.x] = gw;
+    red[1][threadIdx.y][threadIdx.x] = gb;
+    __syncthreads();
+    if (threadIdx.y == 0 && c < d.T) {
+        double sw = 0.0, sb = 0.0;
+        for (int y = 0; y < (int)blockDim.y; ++y) {
+            sw += red[0][y][threadIdx.x];
+            sb += red[1][y][threadIdx.x];
+        }
+        part[(std::size_t)blockIdx.x * 2 * d.T + c] = sw;
+        part[(std::size_t)blockIdx.x * 2 * d.T + d.T + c] = sb;
     }
 }
 
+// one block per output (2T): fixed-order strided sums + tree -> deterministic.
 __global__ void k_time_grad_final(int T, int nblocks, const double* part, double* acc) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= 2 * T) return;
+    __shared__ double red[256];
+    const int c = blockIdx.x;
     double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += part[(std::size_t)b * 2 * T + c];
-    acc[c] += s;
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x) s += part[(std::size_t)b * 2 * T + c];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) acc[c] += red[0];
 }
 
 __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb) {

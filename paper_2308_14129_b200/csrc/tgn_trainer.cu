@@ -20,6 +20,7 @@
 #include "tgn.hpp"
 #include "tgn_common.cuh"
 #include "tgn_kernels.cuh"
+#include "umma_host.hpp"
 
 namespace spd {
 
@@ -153,6 +154,25 @@ void gemm_wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, in
         launch(gemm::splitk_reduce, blocks_for(n), 256, 0, s, ws, split, N_out, K_in, ldws, dW, ldw, 1.f);
         SPD_CUDA(cudaGetLastError());
     }
+}
+
+// Tensor-core-eligible layers (GRU, attention projections) dispatch on
+// spd_tgn_config::gemm_mode: 0 = FP32 FFMA, 1 = tcgen05 TF32.
+void proj_fwd(bool tc, const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M,
+              int N, int K, const int* M_dev, cudaStream_t s) {
+    if (tc) umma::fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s);
+    else gemm_fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s);
+}
+void proj_dgrad(bool tc, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
+                int M, int N, int K, const int* M_dev, cudaStream_t s) {
+    if (tc) umma::dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s);
+    else gemm_dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s);
+}
+void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw,
+                int N_out, int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
+                cudaStream_t s) {
+    if (tc) umma::wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s);
+    else gemm_wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s);
 }
 
 tgnk::WorkerDev devview(Worker& w) {
@@ -355,7 +375,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.dQ.alloc(std::size_t(R) * d.DQ); s.dKV.alloc(std::size_t(RK) * 2 * d.DQ);
     s.dkv_in.alloc(std::size_t(RK) * d.ld_kv); s.dq_in.alloc(std::size_t(R) * d.ld_q);
     s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
-    s.trows = 256;
+    s.trows = 64;
     s.tblocks = (R * (1 + d.K) + s.trows - 1) / s.trows;
     s.tpart.alloc(std::size_t(s.tblocks) * 2 * d.T);
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
@@ -427,12 +447,13 @@ void TGNTrainer::gru_forward(Worker& w, bool train) {
     const auto& d = s.d;
     const auto wd = devview(w);
     const float* P = params_.p;
+    const bool tc = cfg_.gemm_mode == 1;
     launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
         wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
     SPD_CUDA(cudaGetLastError());
-    gemm_fwd(s.x_gru.p, d.ld_x, P + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, 3 * d.D,
+    proj_fwd(tc, s.x_gru.p, d.ld_x, P + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, 3 * d.D,
              d.DM + 1, w.nU.p, stream_);
-    gemm_fwd(s.h_gru.p, d.ld_h, P + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, 3 * d.D,
+    proj_fwd(tc, s.h_gru.p, d.ld_h, P + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, 3 * d.D,
              d.D + 1, w.nU.p, stream_);
     launch(tgnk::k_gru_fwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, stream_, 
         wd, d, s.Gi.p, s.Gh.p, s.h_gru.p, train ? s.gsave.p : nullptr, s.mem_new.p);
@@ -450,6 +471,7 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
     float* P = params_.p;
     float* G = grads_.p;
     cudaStream_t st = stream_;
+    const bool tc = cfg_.gemm_mode == 1;  // tensor cores for GRU + attention projections only
     if (w.pos == 0) {  // loop_start: reset (pac_sim.cpp:238)
         w.mem.zero(st);
         w.lu.zero(st);
@@ -468,11 +490,11 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
             s.nbr_dt.p, s.cnt.p, s.mem_new.p, s.q_in.p, s.kv_in.p);
     });
     timed("gemm_q", [&] {
-        gemm_fwd(s.q_in.p, d.ld_q, P + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.DQ, R, d.DQ,
+        proj_fwd(tc, s.q_in.p, d.ld_q, P + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.DQ, R, d.DQ,
                  d.DQ + 1, nullptr, st);
     });
     timed("gemm_kv", [&] {
-        gemm_fwd(s.kv_in.p, d.ld_kv, P + lay_.att_kv.off, lay_.att_kv.ld, s.KV.p, 2 * d.DQ, RK,
+        proj_fwd(tc, s.kv_in.p, d.ld_kv, P + lay_.att_kv.off, lay_.att_kv.ld, s.KV.p, 2 * d.DQ, RK,
                  2 * d.DQ, d.DK + 1, nullptr, st);
     });
     const std::size_t attn_smem = std::size_t(8) * d.H * d.K * sizeof(float);
@@ -481,7 +503,7 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
             d, R, s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
     });
     timed("head_fwd", [&] {
-        gemm_fwd(s.ctx.p, d.ld_ctx, P + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
+        proj_fwd(tc, s.ctx.p, d.ld_ctx, P + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
                  d.DQ + 1, nullptr, st);
         launch(tgnk::k_merge_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, 
             wd, d, R, s.roots.p, s.cnt.p, s.O.p, s.mem_new.p, s.m_in.p);
@@ -525,9 +547,9 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
         launch(tgnk::k_mask_rows, blocks_for(std::size_t(R) * 32), 256, 0, st, s.dm_in.p, R, d.DQ,
                                                                           d.ld_m, s.cnt.p);
         // output projection
-        gemm_wgrad(s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
+        proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
                    d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, st);
-        gemm_dgrad(s.dm_in.p, d.ld_m, P + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.DQ, R, d.DQ,
+        proj_dgrad(tc, s.dm_in.p, d.ld_m, P + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.DQ, R, d.DQ,
                    d.DQ, nullptr, st);
     });
     timed("attn_bwd", [&] {
@@ -535,17 +557,17 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
             d, R, s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.DQ, s.dQ.p, s.dKV.p);
     });
     timed("gemm_kv_wgrad", [&] {
-        gemm_wgrad(s.dKV.p, 2 * d.DQ, s.kv_in.p, d.ld_kv, G + lay_.att_kv.off, lay_.att_kv.ld,
+        proj_wgrad(tc, s.dKV.p, 2 * d.DQ, s.kv_in.p, d.ld_kv, G + lay_.att_kv.off, lay_.att_kv.ld,
                    2 * d.DQ, d.DK + 1, RK, nullptr, s.ws.p, s.ws.n, st);
     });
     timed("gemm_kv_dgrad", [&] {
-        gemm_dgrad(s.dKV.p, 2 * d.DQ, P + lay_.att_kv.off, lay_.att_kv.ld, s.dkv_in.p, d.ld_kv, RK,
+        proj_dgrad(tc, s.dKV.p, 2 * d.DQ, P + lay_.att_kv.off, lay_.att_kv.ld, s.dkv_in.p, d.ld_kv, RK,
                    d.DK, 2 * d.DQ, nullptr, st);
     });
     timed("q_bwd", [&] {
-        gemm_wgrad(s.dQ.p, d.DQ, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
+        proj_wgrad(tc, s.dQ.p, d.DQ, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
                    d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, st);
-        gemm_dgrad(s.dQ.p, d.DQ, P + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
+        proj_dgrad(tc, s.dQ.p, d.DQ, P + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
                    d.DQ, nullptr, st);
     });
     timed("mem_time_bwd", [&] {
@@ -553,17 +575,21 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
         launch(tgnk::k_mem_grad, blocks_for(std::size_t(R) * (1 + d.K) * 32), 256, 0, st, 
             wd, d, R, s.roots.p, s.nbr_node.p, s.cnt.p, s.dq_in.p, s.dm_in.p, s.dkv_in.p, s.dH.p);
         const int tb = (R * (1 + d.K) + s.trows - 1) / s.trows;
-        launch(tgnk::k_time_grad_partial, tb, 128, 0, st, d, R, s.cnt.p, s.nbr_dt.p, s.dkv_in.p,
-                                                      s.dq_in.p, P + lay_.time_w,
-                                                      P + lay_.time_b, s.trows, s.tpart.p);
-        launch(tgnk::k_time_grad_final, blocks_for(2 * d.T), 256, 0, st, d.T, tb, s.tpart.p, tgrad_.p);
+        launch(tgnk::k_time_grad_partial, dim3(tb, (d.T + 31) / 32), dim3(32, 8), 0, st, d, R,
+               s.cnt.p, s.nbr_dt.p, s.dkv_in.p, s.dq_in.p, P + lay_.time_w, P + lay_.time_b,
+               s.trows, s.tpart.p);
+        launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, st, d.T, tb, s.tpart.p, tgrad_.p);
     });
     timed("gru_bwd", [&] {
+        if (tc) {  // the TC weight-grad reads whole K blocks: rows >= |pending| must be 0
+            s.dGi.zero(st);
+            s.dGh.zero(st);
+        }
         launch(tgnk::k_gru_bwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, st, 
             wd, d, s.dH.p, s.gsave.p, s.h_gru.p, s.dGi.p, s.dGh.p);
-        gemm_wgrad(s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
+        proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
                    3 * d.D, d.DM + 1, s.U, w.nU.p, s.ws.p, s.ws.n, st);
-        gemm_wgrad(s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
+        proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
                    3 * d.D, d.D + 1, s.U, w.nU.p, s.ws.p, s.ws.n, st);
     });
     // persist this batch's memory update and store its last messages now,
@@ -584,7 +610,20 @@ void TGNTrainer::flush_pending(Worker& w) {
     w.nU.zero(stream_);
 }
 
-std::uint64_t kernel_launches() { return g_kernel_launches.load(); }
+// GEMM kernels on caller-owned device buffers, for numerics tests against a
+// plain fp32 reference. impl: 0 FFMA, 1 tcgen05 TF32; which: 0 fwd (C=A.B^T),
+// 1 dgrad (C=A.B), 2 wgrad (C += A^T.B, reduction over K rows).
+int debug_gemm(int impl, int which, const float* A, int lda, const float* B, int ldb, float* C,
+               int ldc, int M, int N, int K, float* ws, std::size_t ws_cap) {
+    cudaStream_t s = 0;
+    if (which == 0) proj_fwd(impl == 1, A, lda, B, ldb, C, ldc, M, N, K, nullptr, s);
+    else if (which == 1) proj_dgrad(impl == 1, A, lda, B, ldb, C, ldc, M, N, K, nullptr, s);
+    else proj_wgrad(impl == 1, A, lda, B, ldb, C, ldc, M, N, K, nullptr, ws, ws_cap, s);
+    SPD_CUDA(cudaDeviceSynchronize());
+    return 0;
+}
+
+std::uint64_t kernel_launches() { return g_kernel_launches.load() + umma::launches(); }
 
 // n lockstep global steps (wrapping into the next epoch when one ends),
 // bracketed by CUDA events on the trainer's stream: device time in ms.

@@ -1,0 +1,152 @@
+// Host side of the tcgen05 TF32 GEMM: TMA tensor-map encoding (driver entry
+// point, no libcuda link), tile-width selection, split-K and the three
+// orientations used by the TGN step.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+
+#include "cuda_util.hpp"
+#include "gemm_simt.cuh"
+#include "umma_gemm.cuh"
+#include "umma_host.hpp"
+
+namespace spd {
+namespace umma {
+
+extern std::atomic<std::uint64_t> g_launch_counter;
+std::atomic<std::uint64_t> g_launch_counter{0};
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) internal_error("CudaError", "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// Row-major fp32 matrix [rows x inner] (row stride ld floats), 128-B swizzled
+// boxes of {32 x box_rows}. Out-of-range elements load as zero.
+CUtensorMap make_map(const float* base, std::uint64_t inner, std::uint64_t rows, int ld,
+                     std::uint32_t box_rows, bool mn_major = false) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+    cuuint32_t box[2] = {32, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base),
+                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                          : CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) internal_error("CudaError", "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+template <bool A_MN, bool B_MN, int BN>
+void run(const CUtensorMap& a, const CUtensorMap& b, const Args& args, dim3 grid, cudaStream_t s) {
+    using C_ = Cfg<A_MN, B_MN, BN>;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        SPD_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<A_MN, B_MN, BN>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
+    });
+    umma_gemm_kernel<A_MN, B_MN, BN><<<grid, THREADS, C_::SMEM, s>>>(a, b, args);
+    g_launch_counter.fetch_add(1, std::memory_order_relaxed);
+    SPD_CUDA(cudaGetLastError());
+}
+
+template <bool A_MN, bool B_MN>
+void dispatch(int bn, const CUtensorMap& a, const CUtensorMap& b, const Args& args, dim3 grid,
+              cudaStream_t s) {
+    switch (bn) {
+        case 64: run<A_MN, B_MN, 64>(a, b, args, grid, s); break;
+        case 128: run<A_MN, B_MN, 128>(a, b, args, grid, s); break;
+        case 224: run<A_MN, B_MN, 224>(a, b, args, grid, s); break;
+        case 256: run<A_MN, B_MN, 256>(a, b, args, grid, s); break;
+        default: internal_error("InvalidParams", "unsupported tile width");
+    }
+}
+
+// widest tile with the least padding of N (ties -> wider)
+int pick_bn(int N) {
+    const int cands[] = {256, 224, 128, 64};
+    int best = 64;
+    long best_pad = 1L << 40;
+    for (int c : cands) {
+        const long tiles = (N + c - 1) / c;
+        const long pad = tiles * c - N + tiles * 8;  // small per-tile overhead term
+        if (pad < best_pad) {
+            best_pad = pad;
+            best = c;
+        }
+    }
+    return best;
+}
+
+}  // namespace
+
+std::uint64_t launches() { return g_launch_counter.load(); }
+
+void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N, int K,
+         const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask) {
+    if (!M || !N) return;
+    const int bn = pick_bn(N);
+    const CUtensorMap ta = make_map(A, K, M, lda, BM);
+    const CUtensorMap tb = make_map(W, K, N, ldw, bn);
+    Args a{};
+    a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
+    a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask;
+    dispatch<false, false>(bn, ta, tb, a, dim3((N + bn - 1) / bn, (M + BM - 1) / BM, 1), s);
+}
+
+void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N,
+           int K, const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask) {
+    if (!M || !N) return;
+    const int bn = pick_bn(N);  // multiple of 32: whole MN-major column blocks
+    const CUtensorMap ta = make_map(A, K, M, lda, BM);
+    const CUtensorMap tb = make_map(W, N, K, ldw, BK, true);  // W [K x N], N contiguous
+    Args a{};
+    a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
+    a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask;
+    dispatch<false, true>(bn, ta, tb, a, dim3((N + bn - 1) / bn, (M + BM - 1) / BM, 1), s);
+}
+
+void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
+           int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
+           cudaStream_t s) {
+    if (!rows || !N_out || !K_in) return;
+    const int bn = K_in <= 64 ? 64 : (K_in <= 128 ? 128 : 224);
+    const int tiles = ((N_out + BM - 1) / BM) * ((K_in + bn - 1) / bn);
+    const int ldws = (K_in + 3) / 4 * 4;
+    int split = std::max(1, std::min(rows / (4 * BK), (148 + tiles - 1) / tiles));
+    while (split > 1 && std::size_t(split) * N_out * ldws > ws_cap) --split;
+    const CUtensorMap ta = make_map(dY, N_out, rows, ldy, BK, true);  // dY [rows x N_out]
+    const CUtensorMap tb = make_map(X, K_in, rows, ldx, BK, true);    // X  [rows x K_in]
+    Args a{};
+    a.C = dW; a.ldc = ldw; a.M = N_out; a.N = K_in; a.K = rows; a.K_dev = rows_dev;
+    a.k_split = split; a.mode = split > 1 ? PARTIAL : ACCUM; a.epi = EPI_NONE;
+    a.ws = ws; a.ldws = ldws;
+    dispatch<true, true>(bn, ta, tb, a, dim3((K_in + bn - 1) / bn, (N_out + BM - 1) / BM, split), s);
+    if (split > 1) {
+        const std::size_t n = std::size_t(N_out) * K_in;
+        gemm::splitk_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(ws, split, N_out, K_in, ldws,
+                                                                      dW, ldw, 1.f);
+        g_launch_counter.fetch_add(1, std::memory_order_relaxed);
+        SPD_CUDA(cudaGetLastError());
+    }
+}
+
+}  // namespace umma
+}  // namespace spd

@@ -15,6 +15,11 @@ pytestmark = pytest.mark.gpu
 TOL_STEP = 2e-5
 TOL_GRAD = 2e-4
 TOL_TRAJ = 2e-3
+# tcgen05 TF32 projections (10-bit operand mantissas), stated tolerances:
+# one step from identical state, and the drift of an 8-step trajectory.
+TOL_TF32_STEP = 5e-3
+TOL_TF32 = 3e-2
+TOL_TF32_GRAD = 2e-2
 
 
 def small_cfg(**kw):
@@ -65,6 +70,33 @@ def test_steps_match_oracle(parts):
             m, lu = tr.memory(w)
             assert np.array_equal(lu, o.lu[w]), f"last_update differs step {step}"
             assert rel_err(m, o.mem[w].numpy()) < TOL_TRAJ
+
+
+@pytest.mark.parametrize("parts", [1, 2])
+def test_tensor_core_mode_within_tolerance(parts):
+    """gemm_mode=1 (tcgen05 TF32 for the GRU and attention projections): bit-exact
+    sampling as FP32, values within the stated TF32 tolerance of the FP32 oracle."""
+    _, _, pa, subs = partitioned(parts=parts)
+    cfg = small_cfg(gemm_mode=1)
+    tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+    tr.set_debug(True)
+    o = oracle_for(cfg, subs, pa.shared)
+    tr.begin_epoch(0)
+    o.begin_epoch(0)
+    for step in range(8):
+        gl = tr.step()
+        ol = o.step()
+        for w in range(parts):
+            t = tr.last_step(w)
+            ref = o.last[w]
+            assert np.array_equal(t["neg"], glob(o, w, ref["neg"]))
+            assert np.array_equal(t["nbr"], glob(o, w, ref["nbr_ids"]))
+            tol = TOL_TF32_STEP if step == 0 else TOL_TF32
+            assert rel_err(t["emb"], ref["emb"]) < tol, (step, rel_err(t["emb"], ref["emb"]))
+            assert abs(gl[w] - ol[w]) <= tol * abs(ol[w])
+        if step == 0:
+            assert rel_err(tr.grads(), o.grad.numpy()) < TOL_TF32_GRAD
+    assert rel_err(tr.params(), o.flat.numpy()) < TOL_TF32
 
 
 def test_gradients_per_tensor_first_step():
