@@ -156,6 +156,13 @@ spd_status spd_shuffle_combine(const uint64_t* small_off, const uint32_t* small_
                                uint64_t n_small, int32_t num_workers, uint64_t epoch_seed,
                                uint64_t* out_off, uint32_t* out_nodes);
 
+/* The PAC lockstep schedule of run_epoch (pac_sim.cpp:215-257) on the host:
+ * n_steps global steps; log (optional, 4*cap u64) = StepRecord rows
+ * (global_step, worker, loop, batch_in_loop); batches/loops per worker (W each). */
+spd_status spd_lockstep_schedule(const spd_subgraphs* s, uint64_t batch_size, uint64_t* n_steps,
+                                 uint64_t* log, uint64_t cap, uint64_t* n_log, uint64_t* batches,
+                                 uint64_t* loops);
+
 /* ------------------------------------------- L4 surrogate model (parity mode) */
 
 /* ModelParams::seeded (pac_sim.hpp:54). w_m: d*3d row-major, omega: d. */

@@ -410,6 +410,26 @@ def shuffle_combine(small: Sequence[Sequence[int]], num_workers: int, epoch_seed
     return [out[out_off[g]:out_off[g + 1]].tolist() for g in range(num_workers)]
 
 
+def lockstep_schedule(subgraphs: Sequence[SubGraph], batch_size: int):
+    """Host evaluation of run_epoch's Alg. 2 schedule: (n_steps, StepLog rows,
+    batches, loops) — identical on every rank of a multi-GPU run."""
+    h = subgraphs_handle(subgraphs)
+    W = len(subgraphs)
+    try:
+        n = u64()
+        cap = 1 << 20
+        log = np.zeros(4 * cap, np.uint64)
+        nl = u64()
+        b = np.zeros(max(1, W), np.uint64)
+        lp = np.zeros(max(1, W), np.uint64)
+        _check(lib.spd_lockstep_schedule(h, batch_size, C.byref(n), ptr(log, u64), cap, C.byref(nl),
+                                         ptr(b, u64), ptr(lp, u64)))
+    finally:
+        lib.spd_subgraphs_destroy(h)
+    rows = [tuple(int(x) for x in log[4 * k:4 * k + 4]) for k in range(nl.value)]
+    return n.value, rows, b[:W].tolist(), lp[:W].tolist()
+
+
 # ------------------------------------------------- surrogate (parity mode)
 @dataclass
 class ModelParams:  # pac_sim.hpp:47-55

@@ -84,6 +84,7 @@ _SIGS = {
     "spd_subgraph_edges": (i32, [P, i32, P, pu64]),
     "spd_subgraphs_destroy": (None, [P]),
     "spd_shuffle_combine": (i32, [pu64, pu32, u64, i32, u64, pu64, pu32]),
+    "spd_lockstep_schedule": (i32, [P, u64, pu64, pu64, u64, pu64, pu64, pu64]),
     "spd_model_seeded": (i32, [i32, u64, pf64, pf64, pf64]),
     "spd_memstore_create": (i32, [u32, i32, i32, PP]),
     "spd_memstore_destroy": (None, [P]),

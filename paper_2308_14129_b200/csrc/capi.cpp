@@ -330,6 +330,53 @@ spd_status spd_shuffle_combine(const uint64_t* small_off, const uint32_t* small_
     });
 }
 
+// Alg. 2 lockstep schedule on the host (pac_sim.cpp:215-257 without the model):
+// global steps = max_w ceil(|E_w|/B); per step every non-vacuous worker takes one
+// batch, looping workers restart. Every rank of a multi-GPU run evaluates this
+// identically from the same SEP assignment, so no collective is needed for it.
+spd_status spd_lockstep_schedule(const spd_subgraphs* s, uint64_t batch_size, uint64_t* n_steps,
+                                 uint64_t* log, uint64_t cap, uint64_t* n_log, uint64_t* batches,
+                                 uint64_t* loops) {
+    GUARD({
+        if (batch_size < 1) data_error("InvalidParams", "need batch_size >= 1");
+        const std::size_t W = s->s.g.size();
+        std::vector<std::uint64_t> nb(W), lp(W, 0), pos(W, 0);
+        std::vector<std::uint8_t> done(W, 0);
+        for (std::size_t w = 0; w < W; ++w) {
+            nb[w] = (s->s.g[w].edges.size() + batch_size - 1) / batch_size;
+            if (nb[w] == 0) {
+                lp[w] = 1;
+                done[w] = 1;
+            }
+        }
+        std::uint64_t step = 0, k = 0;
+        while (!std::all_of(done.begin(), done.end(), [](std::uint8_t f) { return f != 0; })) {
+            ++step;
+            for (std::size_t w = 0; w < W; ++w) {
+                if (nb[w] == 0) continue;
+                if (log && k < cap) {
+                    log[4 * k + 0] = step;
+                    log[4 * k + 1] = w;
+                    log[4 * k + 2] = lp[w] + 1;
+                    log[4 * k + 3] = pos[w] + 1;
+                }
+                ++k;
+                if (++pos[w] == nb[w]) {
+                    ++lp[w];
+                    done[w] = 1;
+                    pos[w] = 0;
+                }
+            }
+        }
+        if (n_steps) *n_steps = step;
+        if (n_log) *n_log = std::min(k, cap);
+        for (std::size_t w = 0; w < W; ++w) {
+            if (batches) batches[w] = nb[w];
+            if (loops) loops[w] = lp[w];
+        }
+    });
+}
+
 // ------------------------------------------------------------ surrogate
 
 spd_status spd_model_seeded(int32_t d, uint64_t seed, double* w_m, double* omega, double* gamma) {
