@@ -107,7 +107,8 @@ class TGNConfig:
 
 
 def ld_aug(k: int) -> int:
-    return (k + 1 + 3) // 4 * 4
+    """Row stride of an augmented [W | b | 0-pad] matrix: whole 128-B lines."""
+    return (k + 1 + 31) // 32 * 32
 
 
 def linear_specs(c: TGNConfig):
@@ -285,8 +286,10 @@ class TGNOracle:
         phi0 = torch.cos(P["time_b"].double()).float()
         q_in = torch.cat([memx[roots], phi0.expand(R, T)], 1)
         Q = q_in @ P["att_w_q"].T + P["att_b_q"]
-        kv_in = torch.cat([memx[nb_node.reshape(-1)], wd.feat[nb_ev.reshape(-1)],
-                           time_enc(P["time_w"], P["time_b"], nb_dt.reshape(-1))], 1)
+        # key/value input [s_nbr | phi(dt) | e]: the differentiable columns first
+        kv_in = torch.cat([memx[nb_node.reshape(-1)],
+                           time_enc(P["time_w"], P["time_b"], nb_dt.reshape(-1)),
+                           wd.feat[nb_ev.reshape(-1)]], 1)
         Kt = (kv_in @ P["att_w_k"].T + P["att_b_k"]).view(R, K, -1)
         Vt = (kv_in @ P["att_w_v"].T + P["att_b_v"]).view(R, K, -1)
         DQ = D + T

@@ -1,20 +1,22 @@
 // FP32 FFMA tiled GEMM for sm_100a (the tolerance-safe path; SURVEY K4/K6
-// "otherwise use FP32 FFMA"). One kernel template covers the three
-// orientations a hand-written backward needs:
+// "otherwise use FP32 FFMA"; the merge and decoder layers always use it).
+// One kernel template covers the three orientations a hand-written backward
+// needs:
 //
-//   fwd        C[M,N]  = A[M,K]   . B[N,K]^T      (A row-major, B row-major)
-//   data grad  C[M,N]  = A[M,K]   . B[K,N]        (B row-major)
-//   weight grad C[M,N] += A[K,M]^T . B[K,N]       (reduction over K = rows, split-K)
+//   fwd         C[M,N]  = A[M,K]   . B[N,K]^T      (A row-major, B row-major)
+//   data grad   C[M,N]  = A[M,K]   . B[K,N]        (B row-major)
+//   weight grad C[M,N] += A[K,M]^T . B[K,N]        (reduction over K = rows, split-K)
 //
 // Every linear layer stores its bias as an extra weight column (augmented
 // [W | b]) and every activation matrix carries a constant-1 column, so the
-// bias gradient falls out of the weight-gradient GEMM. All leading dimensions
-// are multiples of 4 floats and allocations are padded to them, so 128-bit
-// loads along the contiguous dimension are always in bounds; only the
-// reduction index is predicated (rows past a device-resident count read 0).
+// bias gradient falls out of the weight-gradient GEMM. Leading dimensions are
+// multiples of 4 floats and allocations are padded to them, so 128-bit loads
+// along the contiguous dimension are always in bounds; only the reduction
+// index is predicated (rows past a device-resident count read 0).
 //
-// Tile 128x64x16, 256 threads, 8x4 outputs per thread, register-staged
-// double buffering through shared memory.
+// Tile BM x 64 x 16 (BM = 128 or 64: the launcher picks 64 when 128-row tiles
+// would leave SMs idle), 256 threads, (BM/16) x 4 outputs per thread,
+// register-staged double buffering through shared memory.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,8 +26,7 @@
 namespace spd {
 namespace gemm {
 
-constexpr int BM = 128, BN = 64, BK = 16, NT = 256;
-constexpr int TM = 8, TN = 4;
+constexpr int BN = 64, BK = 16, NT = 256, TN = 4;
 
 enum Epi : int { EPI_NONE = 0, EPI_RELU = 1, EPI_MASK = 2 /* C *= (mask > 0) */ };
 
@@ -43,13 +44,15 @@ struct Args {
     int ldmask;
     // split-K for the weight-gradient orientation
     int k_split;        // number of K slices (gridDim.z)
-    float* workspace;   // [k_split][M][N] partials (ld = N4)
+    float* workspace;   // [k_split][M][N] partials (ld = ldw)
     int ldw;
 };
 
 // A_KMAJOR: A stored [K x M] (weight-grad orientation). B_KN: B stored [K x N].
-template <bool A_KMAJOR, bool B_KN>
+template <bool A_KMAJOR, bool B_KN, int BM>
 __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
+    constexpr int TM = BM / 16;       // rows per thread
+    constexpr int AV = BM * BK / 4 / NT;  // float4 A loads per thread (2 or 1)
     __shared__ __align__(16) float As[2][BK][BM + 4];
     __shared__ __align__(16) float Bs[2][BK][BN + 4];
     int M = a.M;
@@ -60,7 +63,6 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
     if (!A_KMAJOR && m0 >= M) return;
     if (n0 >= a.N) return;
     if (A_KMAJOR && m0 >= a.M) return;
-    // K range of this split
     int k_begin = 0, k_end = K;
     if (a.k_split > 1) {
         const int per = ((K + a.k_split - 1) / a.k_split + BK - 1) / BK * BK;
@@ -68,7 +70,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
         k_end = min(K, k_begin + per);
     }
     const int tid = threadIdx.x;
-    const int tx = tid % 16, ty = tid / 16;  // 16 x 16 thread grid; outputs (ty*8.., tx*4..)
+    const int tx = tid % 16, ty = tid / 16;  // outputs (ty*TM.., tx*4..)
 
     float acc[TM][TN];
 #pragma unroll
@@ -76,62 +78,52 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
-    // register staging: A tile 128x16 = 2048 floats = 2 float4 / thread;
-    // B tile 16x64 = 1024 floats = 1 float4 / thread.
-    float4 ra[2], rb;
+    float4 ra[AV], rb;
+    auto zero_tail = [&](float4& v, int gk) {
+        if (gk + 3 >= k_end) {
+            if (gk + 0 >= k_end) v.x = 0.f;
+            if (gk + 1 >= k_end) v.y = 0.f;
+            if (gk + 2 >= k_end) v.z = 0.f;
+            if (gk + 3 >= k_end) v.w = 0.f;
+        }
+    };
     auto load_tiles = [&](int k0) {
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int idx = tid + r * NT;  // 0..511
-            if (!A_KMAJOR) {
-                // A row-major [M x lda]: 128 rows x 16 k -> 4 float4 per row
+        for (int r = 0; r < AV; ++r) {
+            const int idx = tid + r * NT;
+            if (!A_KMAJOR) {  // BM rows x 16 k: 4 float4 per row
                 const int row = idx / 4, kq = (idx % 4) * 4;
                 const int gm = m0 + row, gk = k0 + kq;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (gm < a.M && gk < k_end) v = *reinterpret_cast<const float4*>(a.A + (size_t)gm * a.lda + gk);
-                if (gk + 3 >= k_end) {  // zero lanes past the reduction end
-                    if (gk + 0 >= k_end) v.x = 0.f;
-                    if (gk + 1 >= k_end) v.y = 0.f;
-                    if (gk + 2 >= k_end) v.z = 0.f;
-                    if (gk + 3 >= k_end) v.w = 0.f;
-                }
+                zero_tail(v, gk);
                 ra[r] = v;
-            } else {
-                // A stored [K x lda] (rows = reduction): 16 rows x 128 m -> 32 float4 per row
-                const int kr = idx / 32, mq = (idx % 32) * 4;
+            } else {  // 16 k-rows x BM m: BM/4 float4 per row
+                const int kr = idx / (BM / 4), mq = (idx % (BM / 4)) * 4;
                 const int gk = k0 + kr, gm = m0 + mq;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (gk < k_end && gm < a.M) v = *reinterpret_cast<const float4*>(a.A + (size_t)gk * a.lda + gm);
                 ra[r] = v;
             }
         }
-        {
-            if (B_KN) {
-                // B [K x ldb]: 16 rows x 64 n -> 16 float4 per row
-                const int kr = tid / 16, nq = (tid % 16) * 4;
-                const int gk = k0 + kr, gn = n0 + nq;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (gk < k_end && gn < a.N) v = *reinterpret_cast<const float4*>(a.B + (size_t)gk * a.ldb + gn);
-                rb = v;
-            } else {
-                // B [N x ldb] row-major: 64 rows x 16 k -> 4 float4 per row
-                const int row = tid / 4, kq = (tid % 4) * 4;
-                const int gn = n0 + row, gk = k0 + kq;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (gn < a.N && gk < k_end) v = *reinterpret_cast<const float4*>(a.B + (size_t)gn * a.ldb + gk);
-                if (gk + 3 >= k_end) {
-                    if (gk + 0 >= k_end) v.x = 0.f;
-                    if (gk + 1 >= k_end) v.y = 0.f;
-                    if (gk + 2 >= k_end) v.z = 0.f;
-                    if (gk + 3 >= k_end) v.w = 0.f;
-                }
-                rb = v;
-            }
+        if (B_KN) {  // 16 k-rows x 64 n
+            const int kr = tid / 16, nq = (tid % 16) * 4;
+            const int gk = k0 + kr, gn = n0 + nq;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gk < k_end && gn < a.N) v = *reinterpret_cast<const float4*>(a.B + (size_t)gk * a.ldb + gn);
+            rb = v;
+        } else {  // 64 n-rows x 16 k
+            const int row = tid / 4, kq = (tid % 4) * 4;
+            const int gn = n0 + row, gk = k0 + kq;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gn < a.N && gk < k_end) v = *reinterpret_cast<const float4*>(a.B + (size_t)gn * a.ldb + gk);
+            zero_tail(v, gk);
+            rb = v;
         }
     };
     auto store_tiles = [&](int buf) {
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < AV; ++r) {
             const int idx = tid + r * NT;
             if (!A_KMAJOR) {
                 const int row = idx / 4, kq = (idx % 4) * 4;
@@ -140,7 +132,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
                 As[buf][kq + 2][row] = ra[r].z;
                 As[buf][kq + 3][row] = ra[r].w;
             } else {
-                const int kr = idx / 32, mq = (idx % 32) * 4;
+                const int kr = idx / (BM / 4), mq = (idx % (BM / 4)) * 4;
                 *reinterpret_cast<float4*>(&As[buf][kr][mq]) = ra[r];
             }
         }
@@ -166,10 +158,13 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
             if (more) load_tiles(k0 + BK);
 #pragma unroll
             for (int kk = 0; kk < BK; ++kk) {
-                const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8]);
-                const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8 + 4]);
+                float av[TM];
+#pragma unroll
+                for (int q = 0; q < TM; q += 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + q]);
+                    av[q] = t.x; av[q + 1] = t.y; av[q + 2] = t.z; av[q + 3] = t.w;
+                }
                 const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
-                const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                 const float bv[4] = {b0.x, b0.y, b0.z, b0.w};
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
@@ -184,11 +179,10 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
         }
     }
 
-    // epilogue
     const int Mlim = A_KMAJOR ? a.M : M;
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-        const int gm = m0 + ty * 8 + i;
+        const int gm = m0 + ty * TM + i;
         if (gm >= Mlim) continue;
 #pragma unroll
         for (int j = 0; j < TN; ++j) {
@@ -202,14 +196,15 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
             if (a.epi == EPI_RELU) v = fmaxf(v, 0.f);
             if (a.epi == EPI_MASK) v = a.mask[(size_t)gm * a.ldmask + gn] > 0.f ? v : 0.f;
             float* c = a.C + (size_t)gm * a.ldc + gn;
-            *c = a.beta != 0.f ? *c + v : v;
+            if (a.beta != 0.f) v += *c;
+            *c = v;
         }
     }
 }
 
 // Fixed-order reduction of split-K partials into C (deterministic).
 static __global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, int ldw,
-                              float* __restrict__ C, int ldc, float beta) {
+                                     float* __restrict__ C, int ldc, float beta) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)M * N) return;
     const int m = idx / N, n = idx % N;

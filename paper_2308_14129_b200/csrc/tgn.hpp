@@ -18,7 +18,10 @@
 namespace spd {
 
 inline int ld4(int cols) { return (cols + 3) / 4 * 4; }
-inline int ld_aug(int cols) { return (cols + 1 + 3) / 4 * 4; }  // [x | 1 | pad]
+// Row strides of every matrix a GEMM streams are whole 128-B lines (32 f32):
+// TMA boxes and FFMA tiles then touch each L2 line once.
+inline int ld32(int cols) { return (cols + 31) / 32 * 32; }
+inline int ld_aug(int cols) { return ld32(cols + 1); }  // [x | 1 | pad]
 
 // Flat parameter buffer: every linear layer is an augmented [W | b] matrix
 // (row stride ld_aug(K)); tensors start at 4-float boundaries.
@@ -127,6 +130,12 @@ private:
     void adam();
     void sync_shared();
     void timed(const char* name, const std::function<void()>& f);
+    // weight-gradient GEMMs run on a side stream forked from the main stream at
+    // the point their inputs exist, and joined back once per worker step
+    void side(const std::function<void(cudaStream_t)>& f);
+    void join_side();
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
 
     spd_tgn_config cfg_;
     ParamLayout lay_;

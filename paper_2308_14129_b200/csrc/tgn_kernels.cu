@@ -146,10 +146,12 @@ __global__ void k_embed_gather(WorkerDev w, Dims d, int R, const float* time_w,
     }
     const float* m = memx_row(w, mem_new, d.D, nbr_node[kr]);
     for (int c = lane; c < d.D; c += 32) o[c] = m[c];
-    const __nv_bfloat16* fr = w.feat + (std::size_t)nbr_ev[kr] * d.Fp;
-    for (int c = lane; c < d.F; c += 32) o[d.D + c] = __bfloat162float(fr[c]);
+    // column order [s_nbr | phi(dt) | e]: the gradient-carrying columns are a
+    // contiguous prefix, so the data-gradient GEMM computes only D + T columns
     const double dt = nbr_dt[kr];
-    for (int c = lane; c < d.T; c += 32) o[d.D + d.F + c] = time_cos(time_w[c], time_b[c], dt);
+    for (int c = lane; c < d.T; c += 32) o[d.D + c] = time_cos(time_w[c], time_b[c], dt);
+    const __nv_bfloat16* fr = w.feat + (std::size_t)nbr_ev[kr] * d.Fp;
+    for (int c = lane; c < d.F; c += 32) o[d.D + d.T + c] = __bfloat162float(fr[c]);
 }
 
 // Multi-head attention core over <= K neighbours (one warp per root).
@@ -168,10 +170,10 @@ __global__ void k_attn_fwd(Dims d, int R, const int* cnt, const float* Q, const 
         return;
     }
     const int dh = d.DQ / d.H;
-    const float* q = Q + (std::size_t)r * d.DQ;
+    const float* q = Q + (std::size_t)r * d.ld_Q;
     for (int h = 0; h < d.H; ++h) {
         for (int j = 0; j < c_n; ++j) {
-            const float* k = KV + ((std::size_t)r * d.K + j) * 2 * d.DQ + h * dh;
+            const float* k = KV + ((std::size_t)r * d.K + j) * d.ld_KV + h * dh;
             float p = 0.f;
             for (int c = lane; c < dh; c += 32) p += q[h * dh + c] * k[c];
             p = warp_sum(p);
@@ -200,10 +202,233 @@ __global__ void k_attn_fwd(Dims d, int R, const int* cnt, const float* Q, const 
         const int h = c / dh;
         float acc = 0.f;
         for (int j = 0; j < c_n; ++j)
-            acc += s[h * d.K + j] * KV[((std::size_t)r * d.K + j) * 2 * d.DQ + d.DQ + c];
+            acc += s[h * d.K + j] * KV[((std::size_t)r * d.K + j) * d.ld_KV + d.DQ + c];
         cr[c] = acc;
     }
 }
+
+// ---------------------------------------------------------------------------
+// Register-tiled attention core (DQ <= 256, K <= KMAX, head dim % 4 == 0,
+// H <= 4): one warp per root, lane l owns float4 chunks l and l+32 of every
+// row. All K (then V) rows of the root are loaded up front — 2*K independent
+// 128-bit loads in flight per lane — and each (key, head) dot product is an
+// xor-shuffle all-reduce, so every lane holds all scores and computes the
+// softmax redundantly without further communication.
+template <int KMAX, int HMAX>
+__global__ void __launch_bounds__(256) k_attn_fwd_reg(Dims d, int R, const int* cnt,
+                                                      const float* Q, const float* KV,
+                                                      float* alpha, float* ctx) {
+    const int r = warp_id_global(), lane = lane_id();
+    if (r >= R) return;
+    const int c_n = cnt[r];
+    const int nc = d.DQ / 4;  // chunks per row
+    const int dh4 = d.DQ / d.H / 4;
+    float4* cr = reinterpret_cast<float4*>(ctx + (std::size_t)r * d.ld_ctx);
+    const bool has0 = lane < nc, has1 = lane + 32 < nc;
+    const int h0 = lane / dh4, h1 = (lane + 32) / dh4;
+    if (c_n == 0) {
+        if (has0) cr[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (has1) cr[lane + 32] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    const float4* q4 = reinterpret_cast<const float4*>(Q + (std::size_t)r * d.ld_Q);
+    const float4 qa = has0 ? q4[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 qb = has1 ? q4[lane + 32] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* base = reinterpret_cast<const float4*>(KV + (std::size_t)r * d.K * d.ld_KV);
+    const int ld4 = d.ld_KV / 4;
+    float4 ka[KMAX], kb[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j < c_n) {
+            ka[j] = has0 ? base[j * ld4 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+            kb[j] = has1 ? base[j * ld4 + lane + 32] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    float s[HMAX][KMAX];
+    const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j >= c_n) break;
+        float p[HMAX];
+        const float da = qa.x * ka[j].x + qa.y * ka[j].y + qa.z * ka[j].z + qa.w * ka[j].w;
+        const float db = qb.x * kb[j].x + qb.y * kb[j].y + qb.z * kb[j].z + qb.w * kb[j].w;
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) p[h] = (h0 == h ? da : 0.f) + (h1 == h ? db : 0.f);
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) {
+            if (h >= d.H) break;
+            s[h][j] = warp_sum(p[h]) * inv;
+        }
+    }
+    // softmax per head (redundantly in every lane)
+#pragma unroll
+    for (int h = 0; h < HMAX; ++h) {
+        if (h >= d.H) break;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < c_n) mx = fmaxf(mx, s[h][j]);
+        float sum = 0.f;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < c_n) {
+                s[h][j] = expf(s[h][j] - mx);
+                sum += s[h][j];
+            }
+        const float is = 1.f / sum;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < c_n) s[h][j] *= is;
+    }
+    if (lane < d.K) {
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) {
+            if (h >= d.H) break;
+            float v = 0.f;
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j)
+                if (j == lane && j < c_n) v = s[h][j];
+            alpha[((std::size_t)r * d.H + h) * d.K + lane] = v;
+        }
+    }
+    // context = sum_j alpha_hj V_j  (V chunks follow the K chunks in the row)
+    const int voff = nc;  // V starts at column DQ = chunk nc
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j < c_n) {
+            ka[j] = has0 ? base[j * ld4 + voff + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+            kb[j] = has1 ? base[j * ld4 + voff + lane + 32] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    float4 oa = make_float4(0.f, 0.f, 0.f, 0.f), ob = oa;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j >= c_n) break;
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) {
+            if (h0 == h) a0 = s[h][j];
+            if (h1 == h) a1 = s[h][j];
+        }
+        oa.x += a0 * ka[j].x; oa.y += a0 * ka[j].y; oa.z += a0 * ka[j].z; oa.w += a0 * ka[j].w;
+        ob.x += a1 * kb[j].x; ob.y += a1 * kb[j].y; ob.z += a1 * kb[j].z; ob.w += a1 * kb[j].w;
+    }
+    if (has0) cr[lane] = oa;
+    if (has1) cr[lane + 32] = ob;
+}
+
+template <int KMAX, int HMAX>
+__global__ void __launch_bounds__(256) k_attn_bwd_reg(Dims d, int R, const int* cnt,
+                                                      const float* Q, const float* KV,
+                                                      const float* alpha, const float* dctx,
+                                                      int ld_dctx, float* dQ, float* dKV) {
+    const int r = warp_id_global(), lane = lane_id();
+    if (r >= R) return;
+    const int c_n = cnt[r];
+    const int nc = d.DQ / 4;
+    const int dh4 = d.DQ / d.H / 4;
+    const bool has0 = lane < nc, has1 = lane + 32 < nc;
+    const int h0 = lane / dh4, h1 = (lane + 32) / dh4;
+    const int ld4 = d.ld_KV / 4;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* base = reinterpret_cast<const float4*>(KV + (std::size_t)r * d.K * d.ld_KV);
+    float4* obase = reinterpret_cast<float4*>(dKV + (std::size_t)r * d.K * d.ld_KV);
+    float4* dq4 = reinterpret_cast<float4*>(dQ + (std::size_t)r * d.ld_Q);
+    // padded key rows get zero gradients
+    for (int j = c_n; j < d.K; ++j) {
+        if (has0) { obase[j * ld4 + lane] = z4; obase[j * ld4 + nc + lane] = z4; }
+        if (has1) { obase[j * ld4 + lane + 32] = z4; obase[j * ld4 + nc + lane + 32] = z4; }
+    }
+    if (c_n == 0) {
+        if (has0) dq4[lane] = z4;
+        if (has1) dq4[lane + 32] = z4;
+        return;
+    }
+    const float4* dc4 = reinterpret_cast<const float4*>(dctx + (std::size_t)r * ld_dctx);
+    const float4 ga = has0 ? dc4[lane] : z4, gb = has1 ? dc4[lane + 32] : z4;
+    float4 va[KMAX], vb[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+        if (j < c_n) {
+            va[j] = has0 ? base[j * ld4 + nc + lane] : z4;
+            vb[j] = has1 ? base[j * ld4 + nc + lane + 32] : z4;
+        }
+    float a[HMAX][KMAX], ds[HMAX][KMAX];
+    const float* al = alpha + (std::size_t)r * d.H * d.K;
+#pragma unroll
+    for (int h = 0; h < HMAX; ++h) {
+        if (h >= d.H) break;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < c_n) a[h][j] = al[h * d.K + j];
+    }
+    // d alpha_hj = <dctx_h, V_jh>; dV_j = alpha_hj dctx
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j >= c_n) break;
+        const float pa = ga.x * va[j].x + ga.y * va[j].y + ga.z * va[j].z + ga.w * va[j].w;
+        const float pb = gb.x * vb[j].x + gb.y * vb[j].y + gb.z * vb[j].z + gb.w * vb[j].w;
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) {
+            if (h >= d.H) break;
+            ds[h][j] = warp_sum((h0 == h ? pa : 0.f) + (h1 == h ? pb : 0.f));
+            if (h0 == h) a0 = a[h][j];
+            if (h1 == h) a1 = a[h][j];
+        }
+        if (has0) obase[j * ld4 + nc + lane] = make_float4(a0 * ga.x, a0 * ga.y, a0 * ga.z, a0 * ga.w);
+        if (has1)
+            obase[j * ld4 + nc + lane + 32] = make_float4(a1 * gb.x, a1 * gb.y, a1 * gb.z, a1 * gb.w);
+    }
+    // d score_hj = alpha_hj (dalpha_hj - sum_k alpha_hk dalpha_hk)
+#pragma unroll
+    for (int h = 0; h < HMAX; ++h) {
+        if (h >= d.H) break;
+        float dot = 0.f;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < c_n) dot += a[h][j] * ds[h][j];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+            if (j < c_n) ds[h][j] = a[h][j] * (ds[h][j] - dot);
+    }
+    const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
+    const float4* q4 = reinterpret_cast<const float4*>(Q + (std::size_t)r * d.ld_Q);
+    const float4 qa = has0 ? q4[lane] : z4, qb = has1 ? q4[lane + 32] : z4;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j)
+        if (j < c_n) {
+            va[j] = has0 ? base[j * ld4 + lane] : z4;  // reuse registers for K rows
+            vb[j] = has1 ? base[j * ld4 + lane + 32] : z4;
+        }
+    float4 oa = z4, ob = z4;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+        if (j >= c_n) break;
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) {
+            if (h0 == h) s0 = ds[h][j] * inv;
+            if (h1 == h) s1 = ds[h][j] * inv;
+        }
+        oa.x += s0 * va[j].x; oa.y += s0 * va[j].y; oa.z += s0 * va[j].z; oa.w += s0 * va[j].w;
+        ob.x += s1 * vb[j].x; ob.y += s1 * vb[j].y; ob.z += s1 * vb[j].z; ob.w += s1 * vb[j].w;
+        if (has0) obase[j * ld4 + lane] = make_float4(s0 * qa.x, s0 * qa.y, s0 * qa.z, s0 * qa.w);
+        if (has1) obase[j * ld4 + lane + 32] = make_float4(s1 * qb.x, s1 * qb.y, s1 * qb.z, s1 * qb.w);
+    }
+    if (has0) dq4[lane] = oa;
+    if (has1) dq4[lane + 32] = ob;
+}
+
+#define SPD_ATTN_INST(KM, HM)                                                                  \
+    template __global__ void k_attn_fwd_reg<KM, HM>(Dims, int, const int*, const float*,         \
+                                                    const float*, float*, float*);              \
+    template __global__ void k_attn_bwd_reg<KM, HM>(Dims, int, const int*, const float*,         \
+                                                    const float*, const float*, const float*, int, \
+                                                    float*, float*);
+SPD_ATTN_INST(10, 2)
+SPD_ATTN_INST(16, 4)
+#undef SPD_ATTN_INST
 
 // MergeLayer input [attn | s_root]; attn = 0 for a root without neighbours.
 __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
@@ -302,7 +527,7 @@ __global__ void k_attn_bwd(Dims d, int R, const int* cnt, const float* Q, const 
     if (c_n > 0) {
         for (int h = 0; h < d.H; ++h) {
             for (int j = 0; j < c_n; ++j) {
-                const float* v = KV + ((std::size_t)r * d.K + j) * 2 * d.DQ + d.DQ + h * dh;
+                const float* v = KV + ((std::size_t)r * d.K + j) * d.ld_KV + d.DQ + h * dh;
                 float p = 0.f;
                 for (int c = lane; c < dh; c += 32) p += dc[h * dh + c] * v[c];
                 p = warp_sum(p);
@@ -317,17 +542,17 @@ __global__ void k_attn_bwd(Dims d, int R, const int* cnt, const float* Q, const 
             __syncwarp();
         }
     }
-    float* dq = dQ + (std::size_t)r * d.DQ;
+    float* dq = dQ + (std::size_t)r * d.ld_Q;
     for (int c = lane; c < d.DQ; c += 32) {
         const int h = c / dh;
         float acc = 0.f;
         for (int j = 0; j < c_n; ++j)
-            acc += ds[h * d.K + j] * KV[((std::size_t)r * d.K + j) * 2 * d.DQ + c];
+            acc += ds[h * d.K + j] * KV[((std::size_t)r * d.K + j) * d.ld_KV + c];
         dq[c] = acc * inv;
     }
-    const float* q = Q + (std::size_t)r * d.DQ;
+    const float* q = Q + (std::size_t)r * d.ld_Q;
     for (int j = 0; j < d.K; ++j) {
-        float* o = dKV + ((std::size_t)r * d.K + j) * 2 * d.DQ;
+        float* o = dKV + ((std::size_t)r * d.K + j) * d.ld_KV;
         if (j >= c_n) {
             for (int c = lane; c < 2 * d.DQ; c += 32) o[c] = 0.f;
             continue;
@@ -389,7 +614,7 @@ __global__ void k_time_grad_partial(Dims d, int R, const int* cnt, const double*
                 const int r = kr / d.K, j = kr % d.K;
                 if (j >= cnt[r]) continue;
                 const double dt = nbr_dt[kr];
-                const double g = dkv_in[(std::size_t)kr * d.ld_kv + d.D + d.F + c];
+                const double g = dkv_in[(std::size_t)kr * d.ld_kv + d.D + c];
                 const double sn = (double)time_sin(wc, bc, dt);
                 gw -= sn * dt * g;
                 gb -= sn * g;
@@ -407,6 +632,87 @@ __global__ void k_time_grad_partial(Dims d, int R, const int* cnt, const double*
         }
         part[(std::size_t)blockIdx.x * 2 * d.T + c] = sw;
         part[(std::size_t)blockIdx.x * 2 * d.T + d.T + c] = sb;
+    }
+}
+
+// Fused single pass over the gradient-carrying input columns of every query
+// and key/value row: memory-row gradients (atomics into the GRU outputs of
+// pending nodes) and time-encoder gradients (f64, per-block fixed-order
+// partials). block (32, 8); rows_per_block rows; part[block][2T].
+__global__ void k_memtime_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                               const std::uint32_t* nbr_node, const int* cnt, const double* nbr_dt,
+                               const float* dq_in, const float* dm_in, const float* dkv_in,
+                               const float* time_w, const float* time_b, int rows_per_block,
+                               float* dH, double* part) {
+    constexpr int TC = 4;  // time columns per thread: T <= 128
+    __shared__ double red[2][8][32 * TC];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int total = R * (1 + d.K);
+    const int r0 = blockIdx.x * rows_per_block;
+    const int r1 = min(total, r0 + rows_per_block);
+    double gw[TC], gb[TC], sinb[TC];
+    float wc[TC], bc[TC];
+#pragma unroll
+    for (int i = 0; i < TC; ++i) {
+        gw[i] = gb[i] = 0.0;
+        const int c = tx + 32 * i;
+        wc[i] = c < d.T ? time_w[c] : 0.f;
+        bc[i] = c < d.T ? time_b[c] : 0.f;
+        sinb[i] = sin((double)bc[i]);
+    }
+    for (int row = r0 + ty; row < r1; row += blockDim.y) {
+        if (row < R) {
+            const float* q = dq_in + (std::size_t)row * d.ld_q;
+            const int s = w.slot[roots[row]];
+            if (s >= 0) {
+                const float* m = dm_in + (std::size_t)row * d.ld_m + d.DQ;
+                for (int c = tx; c < d.D; c += 32) atomicAdd(dH + (std::size_t)s * d.D + c, q[c] + m[c]);
+            }
+#pragma unroll
+            for (int i = 0; i < TC; ++i) {
+                const int c = tx + 32 * i;
+                if (c < d.T) gb[i] -= sinb[i] * (double)q[d.D + c];
+            }
+        } else {
+            const int kr = row - R;
+            const int r = kr / d.K, j = kr % d.K;
+            if (j >= cnt[r]) continue;
+            const float* g = dkv_in + (std::size_t)kr * d.ld_kv;
+            const int s = w.slot[nbr_node[kr]];
+            if (s >= 0)
+                for (int c = tx; c < d.D; c += 32) atomicAdd(dH + (std::size_t)s * d.D + c, g[c]);
+            const double dt = nbr_dt[kr];
+#pragma unroll
+            for (int i = 0; i < TC; ++i) {
+                const int c = tx + 32 * i;
+                if (c < d.T) {
+                    const double sn = (double)time_sin(wc[i], bc[i], dt);
+                    const double gv = g[d.D + c];
+                    gw[i] -= sn * dt * gv;
+                    gb[i] -= sn * gv;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < TC; ++i) {
+        red[0][ty][tx + 32 * i] = gw[i];
+        red[1][ty][tx + 32 * i] = gb[i];
+    }
+    __syncthreads();
+    if (ty == 0) {
+#pragma unroll
+        for (int i = 0; i < TC; ++i) {
+            const int c = tx + 32 * i;
+            if (c >= d.T) continue;
+            double sw = 0.0, sb = 0.0;
+            for (int y = 0; y < (int)blockDim.y; ++y) {
+                sw += red[0][y][c];
+                sb += red[1][y][c];
+            }
+            part[(std::size_t)blockIdx.x * 2 * d.T + c] = sw;
+            part[(std::size_t)blockIdx.x * 2 * d.T + d.T + c] = sb;
+        }
     }
 }
 

@@ -19,6 +19,7 @@ struct Dims {
     int D, T, F, Fp, DQ, DK, DM, H, K;
     int ld_x, ld_h, ld_q, ld_kv, ld_ctx, ld_m, ld_z, ld_din, ld_d1;  // aug strides
     int ld_g;  // 3D rounded
+    int ld_Q, ld_KV;  // row strides of Q/dQ/dctx (DQ) and KV/dKV (2 DQ), 128-B multiples
 };
 
 struct WorkerDev {
@@ -59,6 +60,17 @@ __global__ void k_embed_gather(WorkerDev w, Dims d, int R, const float* time_w,
                                float* q_in, float* kv_in);
 __global__ void k_attn_fwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
                            float* alpha, float* ctx);
+template <int KMAX, int HMAX>
+__global__ void k_attn_fwd_reg(Dims d, int R, const int* cnt, const float* Q, const float* KV,
+                               float* alpha, float* ctx);
+template <int KMAX, int HMAX>
+__global__ void k_attn_bwd_reg(Dims d, int R, const int* cnt, const float* Q, const float* KV,
+                               const float* alpha, const float* dctx, int ld_dctx, float* dQ,
+                               float* dKV);
+// the register-tiled attention kernels apply when these hold
+inline bool attn_reg_ok(const Dims& d) {
+    return d.DQ <= 256 && d.K <= 16 && d.H <= 4 && d.DQ % d.H == 0 && (d.DQ / d.H) % 4 == 0;
+}
 __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
                                const int* cnt, const float* O, const float* mem_new, float* m_in);
 __global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in);
@@ -76,6 +88,11 @@ __global__ void k_mem_grad(WorkerDev w, Dims d, int R, const std::uint32_t* root
 __global__ void k_time_grad_partial(Dims d, int R, const int* cnt, const double* nbr_dt,
                                     const float* dkv_in, const float* dq_in, const float* time_w,
                                     const float* time_b, int rows_per_block, double* part);
+__global__ void k_memtime_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                               const std::uint32_t* nbr_node, const int* cnt, const double* nbr_dt,
+                               const float* dq_in, const float* dm_in, const float* dkv_in,
+                               const float* time_w, const float* time_b, int rows_per_block,
+                               float* dH, double* part);
 __global__ void k_time_grad_final(int T, int nblocks, const double* part, double* acc);
 __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb);
 __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* save, const float* h,

@@ -103,6 +103,11 @@ void init_aug(DevBuf<float>& b, int rows, int cols, int ld, cudaStream_t s) {
 
 unsigned blocks_for(std::size_t n, int t = 256) { return unsigned((n + t - 1) / t); }
 
+// 64-row tiles when 128-row tiles would leave SMs idle (merge/decoder shapes).
+bool use_bm64(int M, int N) {
+    return long((M + 127) / 128) * ((N + gemm::BN - 1) / gemm::BN) < 2L * 148;
+}
+
 // C[M,N] (ldc) = A[M,K](lda) . B[N,K]^T(ldb), optional relu / mask epilogue.
 void gemm_fwd(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N,
               int K, const int* M_dev, cudaStream_t s, int epi = gemm::EPI_NONE,
@@ -111,9 +116,14 @@ void gemm_fwd(const float* A, int lda, const float* B, int ldb, float* C, int ld
     a.A = A; a.B = B; a.C = C; a.M = M; a.N = N; a.K = K;
     a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.M_dev = M_dev; a.beta = 0.f; a.epi = epi;
     a.mask = mask; a.ldmask = ldmask; a.k_split = 1;
-    dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + gemm::BM - 1) / gemm::BM, 1);
     if (!M || !N) return;
-    launch(gemm::gemm_kernel<false, false>, grid, gemm::NT, 0, s, a);
+    if (use_bm64(M, N)) {
+        dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + 63) / 64, 1);
+        launch(gemm::gemm_kernel<false, false, 64>, grid, gemm::NT, 0, s, a);
+    } else {
+        dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + 127) / 128, 1);
+        launch(gemm::gemm_kernel<false, false, 128>, grid, gemm::NT, 0, s, a);
+    }
     SPD_CUDA(cudaGetLastError());
 }
 
@@ -125,9 +135,14 @@ void gemm_dgrad(const float* A, int lda, const float* B, int ldb, float* C, int 
     a.A = A; a.B = B; a.C = C; a.M = M; a.N = N; a.K = K;
     a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.M_dev = M_dev; a.beta = 0.f; a.epi = epi;
     a.mask = mask; a.ldmask = ldmask; a.k_split = 1;
-    dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + gemm::BM - 1) / gemm::BM, 1);
     if (!M || !N) return;
-    launch(gemm::gemm_kernel<false, true>, grid, gemm::NT, 0, s, a);
+    if (use_bm64(M, N)) {
+        dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + 63) / 64, 1);
+        launch(gemm::gemm_kernel<false, true, 64>, grid, gemm::NT, 0, s, a);
+    } else {
+        dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + 127) / 128, 1);
+        launch(gemm::gemm_kernel<false, true, 128>, grid, gemm::NT, 0, s, a);
+    }
     SPD_CUDA(cudaGetLastError());
 }
 
@@ -137,7 +152,7 @@ void gemm_wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, in
                 int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
                 cudaStream_t s) {
     if (!rows || !N_out || !K_in) return;
-    const int tiles = ((N_out + gemm::BM - 1) / gemm::BM) * ((K_in + gemm::BN - 1) / gemm::BN);
+    const int tiles = ((N_out + 63) / 64) * ((K_in + gemm::BN - 1) / gemm::BN);
     int split = std::max(1, std::min(64, (2 * 148 + tiles - 1) / tiles));
     split = std::min(split, std::max(1, rows / 256));
     const int ldws = ld4(K_in);
@@ -146,8 +161,8 @@ void gemm_wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, in
     a.A = dY; a.B = X; a.C = dW; a.M = N_out; a.N = K_in; a.K = rows;
     a.lda = ldy; a.ldb = ldx; a.ldc = ldw; a.K_dev = rows_dev; a.beta = 1.f; a.epi = 0;
     a.k_split = split; a.workspace = ws; a.ldw = ldws;
-    dim3 grid((K_in + gemm::BN - 1) / gemm::BN, (N_out + gemm::BM - 1) / gemm::BM, split);
-    launch(gemm::gemm_kernel<true, true>, grid, gemm::NT, 0, s, a);
+    dim3 grid((K_in + gemm::BN - 1) / gemm::BN, (N_out + 63) / 64, split);
+    launch(gemm::gemm_kernel<true, true, 64>, grid, gemm::NT, 0, s, a);
     SPD_CUDA(cudaGetLastError());
     if (split > 1) {
         const std::size_t n = std::size_t(N_out) * K_in;
@@ -159,14 +174,16 @@ void gemm_wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, in
 // Tensor-core-eligible layers (GRU, attention projections) dispatch on
 // spd_tgn_config::gemm_mode: 0 = FP32 FFMA, 1 = tcgen05 TF32.
 void proj_fwd(bool tc, const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M,
-              int N, int K, const int* M_dev, cudaStream_t s) {
-    if (tc) umma::fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s);
-    else gemm_fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s);
+              int N, int K, const int* M_dev, cudaStream_t s, int epi = 0,
+              const float* mask = nullptr, int ldmask = 0) {
+    if (tc) umma::fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
+    else gemm_fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
 }
 void proj_dgrad(bool tc, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
-                int M, int N, int K, const int* M_dev, cudaStream_t s) {
-    if (tc) umma::dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s);
-    else gemm_dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s);
+                int M, int N, int K, const int* M_dev, cudaStream_t s, int epi = 0,
+                const float* mask = nullptr, int ldmask = 0) {
+    if (tc) umma::dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
+    else gemm_dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
 }
 void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw,
                 int N_out, int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
@@ -228,6 +245,9 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     require_device(device);
     DeviceGuard g(device);
     SPD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    SPD_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    SPD_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    SPD_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors);
     feat_seed_mixed_ = mix64(cfg.seed_feat);
     total_workers_ = static_cast<int>(subs.g.size());
@@ -346,7 +366,8 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     d.H = lay_.H; d.K = lay_.Kn;
     d.ld_x = ld_aug(d.DM); d.ld_h = ld_aug(D); d.ld_q = ld_aug(d.DQ); d.ld_kv = ld_aug(d.DK);
     d.ld_ctx = ld_aug(d.DQ); d.ld_m = ld_aug(d.DQ + D); d.ld_z = ld_aug(D); d.ld_din = ld_aug(2 * D);
-    d.ld_d1 = ld_aug(D); d.ld_g = ld4(3 * D);
+    d.ld_d1 = ld_aug(D); d.ld_g = ld32(3 * D);
+    d.ld_Q = ld32(d.DQ); d.ld_KV = ld32(2 * d.DQ);
     const int R = s.R, RK = s.RK, U = s.U;
     s.roots.alloc(R); s.root_t.alloc(R); s.cnt.alloc(R);
     s.nbr_node.alloc(RK); s.nbr_ev.alloc(RK); s.nbr_dt.alloc(RK);
@@ -358,7 +379,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.dGi.zero(stream_); s.dGh.zero(stream_); s.Gi.zero(stream_); s.Gh.zero(stream_);
     s.q_in.alloc(std::size_t(R) * d.ld_q); init_aug(s.q_in, R, d.DQ, d.ld_q, stream_);
     s.kv_in.alloc(std::size_t(RK) * d.ld_kv); init_aug(s.kv_in, RK, d.DK, d.ld_kv, stream_);
-    s.Q.alloc(std::size_t(R) * d.DQ); s.KV.alloc(std::size_t(RK) * 2 * d.DQ);
+    s.Q.alloc(std::size_t(R) * d.ld_Q); s.KV.alloc(std::size_t(RK) * d.ld_KV);
     s.alpha.alloc(std::size_t(R) * d.H * d.K);
     s.ctx.alloc(std::size_t(R) * d.ld_ctx); init_aug(s.ctx, R, d.DQ, d.ld_ctx, stream_);
     s.O.alloc(std::size_t(R) * d.DQ);
@@ -371,8 +392,8 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.dlogit.alloc(std::size_t(2 * B) * 4); s.dlogit.zero(stream_);
     s.dD1.alloc(std::size_t(2 * B) * D); s.dd_in.alloc(std::size_t(2 * B) * d.ld_din);
     s.d_emb.alloc(std::size_t(R) * D); s.dZ1.alloc(std::size_t(R) * D);
-    s.dm_in.alloc(std::size_t(R) * d.ld_m); s.dctx.alloc(std::size_t(R) * d.DQ);
-    s.dQ.alloc(std::size_t(R) * d.DQ); s.dKV.alloc(std::size_t(RK) * 2 * d.DQ);
+    s.dm_in.alloc(std::size_t(R) * d.ld_m); s.dctx.alloc(std::size_t(R) * d.ld_Q);
+    s.dQ.alloc(std::size_t(R) * d.ld_Q); s.dKV.alloc(std::size_t(RK) * d.ld_KV);
     s.dkv_in.alloc(std::size_t(RK) * d.ld_kv); s.dq_in.alloc(std::size_t(R) * d.ld_q);
     s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
     s.trows = 64;
@@ -393,8 +414,22 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
 
 int TGNTrainer::feat_stride() const { return s_->d.Fp; }
 
+void TGNTrainer::side(const std::function<void(cudaStream_t)>& f) {
+    SPD_CUDA(cudaEventRecord(ev_fork_, stream_));
+    SPD_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+    f(side_);
+}
+
+void TGNTrainer::join_side() {
+    SPD_CUDA(cudaEventRecord(ev_join_, side_));
+    SPD_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+}
+
 TGNTrainer::~TGNTrainer() {
     if (stage_) cudaFreeHost(stage_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (side_) cudaStreamDestroy(side_);
     if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
     if (stream_) cudaStreamDestroy(stream_);
 }
@@ -490,26 +525,35 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
             s.nbr_dt.p, s.cnt.p, s.mem_new.p, s.q_in.p, s.kv_in.p);
     });
     timed("gemm_q", [&] {
-        proj_fwd(tc, s.q_in.p, d.ld_q, P + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.DQ, R, d.DQ,
+        proj_fwd(tc, s.q_in.p, d.ld_q, P + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
                  d.DQ + 1, nullptr, st);
     });
     timed("gemm_kv", [&] {
-        proj_fwd(tc, s.kv_in.p, d.ld_kv, P + lay_.att_kv.off, lay_.att_kv.ld, s.KV.p, 2 * d.DQ, RK,
+        proj_fwd(tc, s.kv_in.p, d.ld_kv, P + lay_.att_kv.off, lay_.att_kv.ld, s.KV.p, d.ld_KV, RK,
                  2 * d.DQ, d.DK + 1, nullptr, st);
     });
     const std::size_t attn_smem = std::size_t(8) * d.H * d.K * sizeof(float);
+    const bool attn_reg = tgnk::attn_reg_ok(d);
+    const bool attn_small = d.K <= 10 && d.H <= 2;
     timed("attn_fwd", [&] {
-        launch(tgnk::k_attn_fwd, blocks_for(std::size_t(R) * 32), 256, attn_smem, st, 
-            d, R, s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
+        if (attn_reg && attn_small)
+            launch(tgnk::k_attn_fwd_reg<10, 2>, blocks_for(std::size_t(R) * 32), 256, 0, st, d, R,
+                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
+        else if (attn_reg)
+            launch(tgnk::k_attn_fwd_reg<16, 4>, blocks_for(std::size_t(R) * 32), 256, 0, st, d, R,
+                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
+        else
+            launch(tgnk::k_attn_fwd, blocks_for(std::size_t(R) * 32), 256, attn_smem, st, d, R,
+                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
     });
     timed("head_fwd", [&] {
         proj_fwd(tc, s.ctx.p, d.ld_ctx, P + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
                  d.DQ + 1, nullptr, st);
         launch(tgnk::k_merge_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, 
             wd, d, R, s.roots.p, s.cnt.p, s.O.p, s.mem_new.p, s.m_in.p);
-        gemm_fwd(s.m_in.p, d.ld_m, P + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
+        proj_fwd(tc, s.m_in.p, d.ld_m, P + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
                  d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU);
-        gemm_fwd(s.Z1.p, d.ld_z, P + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
+        proj_fwd(tc, s.Z1.p, d.ld_z, P + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
                  nullptr, st);
         launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, d, B, s.emb.p,
                                                                                  s.d_in.p);
@@ -527,51 +571,66 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
 
     // ------------------------------------------------------------ backward
     timed("head_bwd", [&] {
-        gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
-                   2 * B, nullptr, s.ws.p, s.ws.n, st);
-        gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
-                   2 * d.D + 1, 2 * B, nullptr, s.ws.p, s.ws.n, st);
+        side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
+                   2 * B, nullptr, s.ws.p, s.ws.n, sd); });
+        side([&](cudaStream_t sd) { gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
+                   2 * d.D + 1, 2 * B, nullptr, s.ws.p, s.ws.n, sd); });
         gemm_dgrad(s.dD1.p, d.D, P + lay_.dec1.off, lay_.dec1.ld, s.dd_in.p, d.ld_din, 2 * B,
                    2 * d.D, d.D, nullptr, st);
         launch(tgnk::k_dec_scatter, blocks_for(std::size_t(B) * 32), 256, 0, st, d, B, s.dd_in.p,
                                                                              s.d_emb.p);
         // merge layer 2 (relu mask from Z1), layer 1
-        gemm_wgrad(s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off, lay_.mrg2.ld, d.D, d.D + 1,
-                   R, nullptr, s.ws.p, s.ws.n, st);
-        gemm_dgrad(s.d_emb.p, d.D, P + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off, lay_.mrg2.ld, d.D, d.D + 1,
+                   R, nullptr, s.ws.p, s.ws.n, sd); });
+        proj_dgrad(tc, s.d_emb.p, d.D, P + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
                    nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z);
-        gemm_wgrad(s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off, lay_.mrg1.ld, d.D,
-                   d.DQ + d.D + 1, R, nullptr, s.ws.p, s.ws.n, st);
-        gemm_dgrad(s.dZ1.p, d.D, P + lay_.mrg1.off, lay_.mrg1.ld, s.dm_in.p, d.ld_m, R,
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off, lay_.mrg1.ld, d.D,
+                   d.DQ + d.D + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
+        proj_dgrad(tc, s.dZ1.p, d.D, P + lay_.mrg1.off, lay_.mrg1.ld, s.dm_in.p, d.ld_m, R,
                    d.DQ + d.D, d.D, nullptr, st);
         launch(tgnk::k_mask_rows, blocks_for(std::size_t(R) * 32), 256, 0, st, s.dm_in.p, R, d.DQ,
                                                                           d.ld_m, s.cnt.p);
         // output projection
-        proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
-                   d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, st);
-        proj_dgrad(tc, s.dm_in.p, d.ld_m, P + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.DQ, R, d.DQ,
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
+                   d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
+        proj_dgrad(tc, s.dm_in.p, d.ld_m, P + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R, d.DQ,
                    d.DQ, nullptr, st);
     });
     timed("attn_bwd", [&] {
-        launch(tgnk::k_attn_bwd, blocks_for(std::size_t(R) * 32), 256, attn_smem, st, 
-            d, R, s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.DQ, s.dQ.p, s.dKV.p);
+        if (attn_reg && attn_small)
+            launch(tgnk::k_attn_bwd_reg<10, 2>, blocks_for(std::size_t(R) * 32), 256, 0, st, d, R,
+                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.ld_Q, s.dQ.p, s.dKV.p);
+        else if (attn_reg)
+            launch(tgnk::k_attn_bwd_reg<16, 4>, blocks_for(std::size_t(R) * 32), 256, 0, st, d, R,
+                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.ld_Q, s.dQ.p, s.dKV.p);
+        else
+            launch(tgnk::k_attn_bwd, blocks_for(std::size_t(R) * 32), 256, attn_smem, st, d, R,
+                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.ld_Q, s.dQ.p, s.dKV.p);
     });
     timed("gemm_kv_wgrad", [&] {
-        proj_wgrad(tc, s.dKV.p, 2 * d.DQ, s.kv_in.p, d.ld_kv, G + lay_.att_kv.off, lay_.att_kv.ld,
-                   2 * d.DQ, d.DK + 1, RK, nullptr, s.ws.p, s.ws.n, st);
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dKV.p, d.ld_KV, s.kv_in.p, d.ld_kv, G + lay_.att_kv.off, lay_.att_kv.ld,
+                   2 * d.DQ, d.DK + 1, RK, nullptr, s.ws.p, s.ws.n, sd); });
     });
     timed("gemm_kv_dgrad", [&] {
-        proj_dgrad(tc, s.dKV.p, 2 * d.DQ, P + lay_.att_kv.off, lay_.att_kv.ld, s.dkv_in.p, d.ld_kv, RK,
-                   d.DK, 2 * d.DQ, nullptr, st);
+        proj_dgrad(tc, s.dKV.p, d.ld_KV, P + lay_.att_kv.off, lay_.att_kv.ld, s.dkv_in.p, d.ld_kv, RK,
+                   d.D + d.T, 2 * d.DQ, nullptr, st);  // only [s_nbr | phi] carry gradient
     });
     timed("q_bwd", [&] {
-        proj_wgrad(tc, s.dQ.p, d.DQ, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
-                   d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, st);
-        proj_dgrad(tc, s.dQ.p, d.DQ, P + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
+                   d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
+        proj_dgrad(tc, s.dQ.p, d.ld_Q, P + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
                    d.DQ, nullptr, st);
     });
     timed("mem_time_bwd", [&] {
         s.dH.zero(st);
+        if (d.T <= 128) {  // fused single pass
+            const int tb = (R * (1 + d.K) + s.trows - 1) / s.trows;
+            launch(tgnk::k_memtime_grad, tb, dim3(32, 8), 0, st, wd, d, R, s.roots.p, s.nbr_node.p,
+                   s.cnt.p, s.nbr_dt.p, s.dq_in.p, s.dm_in.p, s.dkv_in.p, P + lay_.time_w,
+                   P + lay_.time_b, s.trows, s.dH.p, s.tpart.p);
+            launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, st, d.T, tb, s.tpart.p, tgrad_.p);
+            return;
+        }
         launch(tgnk::k_mem_grad, blocks_for(std::size_t(R) * (1 + d.K) * 32), 256, 0, st, 
             wd, d, R, s.roots.p, s.nbr_node.p, s.cnt.p, s.dq_in.p, s.dm_in.p, s.dkv_in.p, s.dH.p);
         const int tb = (R * (1 + d.K) + s.trows - 1) / s.trows;
@@ -587,18 +646,20 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
         }
         launch(tgnk::k_gru_bwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, st, 
             wd, d, s.dH.p, s.gsave.p, s.h_gru.p, s.dGi.p, s.dGh.p);
-        proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
-                   3 * d.D, d.DM + 1, s.U, w.nU.p, s.ws.p, s.ws.n, st);
-        proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
-                   3 * d.D, d.D + 1, s.U, w.nU.p, s.ws.p, s.ws.n, st);
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
+                   3 * d.D, d.DM + 1, s.U, w.nU.p, s.ws.p, s.ws.n, sd); });
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
+                   3 * d.D, d.D + 1, s.U, w.nU.p, s.ws.p, s.ws.n, sd); });
     });
+    // side-stream weight grads read the pending set (nU, GRU inputs) that the
+    // post phase rewrites: join first
+    join_side();
     // persist this batch's memory update and store its last messages now,
     // while the scratch still holds this worker's rows (K11, K3)
     timed("post", [&] {
         launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
         launch(tgnk::k_pending, 1, 1024, 0, st, wd, lo, B);
     });
-    SPD_CUDA(cudaGetLastError());
 }
 
 void TGNTrainer::flush_pending(Worker& w) {
