@@ -282,13 +282,17 @@ spd_status spd_tgn_end_epoch(spd_tgn_trainer* t);
 /* Whole epoch (begin + steps + end). */
 spd_status spd_tgn_run_epoch(spd_tgn_trainer* t, int32_t epoch, double* mean_loss);
 
-/* Score edges (u,v,t) with eids for features against the current memory; no
- * training; memory is then updated with these events (TGN evaluation). Positive
- * edges are scored together with one sampled negative each (seed, stream).
- * Edges are in GLOBAL node ids; `worker` selects the local worker. */
-spd_status spd_tgn_evaluate(spd_tgn_trainer* t, int32_t worker, const spd_edge* e,
-                            const uint64_t* eids, uint64_t n, uint64_t neg_seed,
-                            float* pos_scores, float* neg_scores);
+/* Evaluation (TGN protocol; routing = spd_assign_eval_edges, partitioner.hpp:74-81).
+ * set: the worker's routed val edges followed by its routed test edges (GLOBAL
+ * ids, time-ordered, eids for features) are appended after its training events;
+ * the full-graph recent-k finder and the negative pool cover train + eval events.
+ * evaluate: eval events [lo, hi) are scored in batches against the current
+ * memory (logits of each positive and of one sampled negative, counter hash of
+ * (neg_seed, worker, position)); memory then advances through them. No gradients. */
+spd_status spd_tgn_set_eval_events(spd_tgn_trainer* t, int32_t worker, const spd_edge* e,
+                                   const uint64_t* eids, uint64_t n);
+spd_status spd_tgn_evaluate(spd_tgn_trainer* t, int32_t worker, uint64_t lo, uint64_t hi,
+                            uint64_t neg_seed, float* pos_scores, float* neg_scores);
 
 /* Introspection for parity tests. */
 spd_status spd_tgn_param_count(const spd_tgn_trainer* t, uint64_t* n);

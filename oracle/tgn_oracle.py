@@ -44,6 +44,10 @@ import torch
 
 M64 = (1 << 64) - 1
 
+# The oracle must be reproducible bit for bit run to run (CPU index_put
+# accumulation is otherwise thread-order dependent).
+torch.use_deterministic_algorithms(True, warn_only=True)
+
 
 # ------------------------------------------------------------- hashing
 def mix(x: int) -> int:
@@ -256,8 +260,8 @@ class TGNOracle:
         n = torch.tanh(gi[:, 2 * D:] + r * gh[:, 2 * D:])
         return (1 - z) * n + z * h
 
-    def _messages(self, w, P, U):
-        wd = self.W[w]
+    def _messages(self, w, P, U, data=None):
+        wd = self.W[w] if data is None else data
         mem = self.mem[w]
         pend = self.pend[w]
         other = [pend[u][0] for u in U]
@@ -268,8 +272,8 @@ class TGNOracle:
         x = torch.cat([mem[U], mem[other], wd.feat[ev], phi], 1).detach()
         return x, mem[U].detach(), ts
 
-    def _embed(self, w, P, memx, roots, t_roots):
-        c, wd = self.c, self.W[w]
+    def _embed(self, w, P, memx, roots, t_roots, data=None):
+        c, wd = self.c, (self.W[w] if data is None else data)
         D, T, K, H = c.d_mem, c.d_time, c.n_neighbors, c.n_heads
         R = len(roots)
         nb_node = np.zeros((R, K), np.int64)
@@ -461,7 +465,42 @@ class TGNOracle:
         return losses
 
     # --------------------------------------------------------- evaluation
-    def evaluate(self, w, wd_eval: WorkerData, src_l, dst_l, ts, ev_rows, neg_l):
-        """Score positives and negatives in batches against memory, updating
-        memory like training (no gradient, no parameter update)."""
-        raise NotImplementedError
+    def set_eval(self, w, edges_global, eids):
+        """Routed val then test edges of worker w appended after its training
+        events: the evaluation view (full-graph neighbours, features, pool)."""
+        wd = self.W[w]
+        tr = np.zeros(wd.E, dtype=edges_global.dtype)
+        tr["src"], tr["dst"], tr["ts"] = wd.nodes[wd.src], wd.nodes[wd.dst], wd.ts
+        comb = np.concatenate([tr, np.asarray(edges_global)])
+        ids = np.concatenate([wd.eids, np.asarray(eids, np.uint64)])
+        if not hasattr(self, "X"):
+            self.X = {}
+        self.X[w] = WorkerData(wd.nodes, comb, ids, self.c.d_edge, self.c.seed_feat)
+
+    def evaluate(self, w, lo, hi, neg_seed=5):
+        """TGN evaluation over eval events [lo, hi): per batch apply pending
+        messages, embed src/dst/negative, score, persist, store messages."""
+        X, E, B = self.X[w], self.W[w].E, self.c.batch_size
+        P = self.views(self.flat)
+        pos, neg = [], []
+        with torch.no_grad():
+            for b0 in range(lo, hi, B):
+                b1 = min(hi, b0 + B)
+                k0, n = E + b0, b1 - b0
+                src, dst, ts = X.src[k0:k0 + n], X.dst[k0:k0 + n], X.ts[k0:k0 + n]
+                ng = negatives(neg_seed, 0xE7A1, w, b0, n, X.pool)
+                U = np.array(sorted(self.pend[w].keys()), np.int64)
+                memx = self.mem[w].clone()
+                if len(U):
+                    x, h, mts = self._messages(w, P, U, X)
+                    hn = self._gru(P, x, h)
+                    memx[U] = hn
+                emb, _, _ = self._embed(w, P, memx, np.concatenate([src, dst, ng]),
+                                        np.concatenate([ts, ts, ts]), X)
+                pos.append(self._decode(P, emb[:n], emb[n:2 * n]).numpy())
+                neg.append(self._decode(P, emb[:n], emb[2 * n:]).numpy())
+                if len(U):
+                    self.mem[w][U] = hn
+                    self.lu[w][U] = mts
+                self._store_pending(w, src, dst, ts, np.arange(k0, k0 + n))
+        return np.concatenate(pos), np.concatenate(neg)

@@ -785,6 +785,19 @@ class TGNTrainer:
                     nbr=nbr[: 3 * n * cfg.n_neighbors].reshape(3 * n, cfg.n_neighbors),
                     loss=loss.value)
 
+    def set_eval_events(self, w: int, edges, eids):
+        """Routed val then test edges of worker w (global ids, time order)."""
+        e = _edges(edges)
+        ids = np.ascontiguousarray(eids, np.uint64)
+        _check(lib.spd_tgn_set_eval_events(self._h, w, ptr(e), ptr(ids, u64), len(e)))
+
+    def evaluate(self, w: int, lo: int, hi: int, neg_seed: int = 5):
+        """Logits of eval events [lo, hi) and of one sampled negative each."""
+        pos = np.zeros(max(1, hi - lo), np.float32)
+        neg = np.zeros(max(1, hi - lo), np.float32)
+        _check(lib.spd_tgn_evaluate(self._h, w, lo, hi, neg_seed, ptr(pos, f32), ptr(neg, f32)))
+        return pos[: hi - lo], neg[: hi - lo]
+
     def run_steps(self, n: int) -> float:
         """n lockstep steps timed on the trainer's stream (device ms)."""
         ms = f32()

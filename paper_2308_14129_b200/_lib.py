@@ -108,7 +108,8 @@ _SIGS = {
     "spd_tgn_step": (i32, [P, pf32]),
     "spd_tgn_end_epoch": (i32, [P]),
     "spd_tgn_run_epoch": (i32, [P, i32, pf64]),
-    "spd_tgn_evaluate": (i32, [P, i32, P, pu64, u64, u64, pf32, pf32]),
+    "spd_tgn_set_eval_events": (i32, [P, i32, P, pu64, u64]),
+    "spd_tgn_evaluate": (i32, [P, i32, u64, u64, u64, pf32, pf32]),
     "spd_tgn_param_count": (i32, [P, pu64]),
     "spd_tgn_get_params": (i32, [P, pf32]),
     "spd_tgn_set_params": (i32, [P, pf32]),

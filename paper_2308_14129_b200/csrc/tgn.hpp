@@ -14,6 +14,7 @@
 
 #include "cuda_util.hpp"
 #include "host.hpp"
+#include "tgn_kernels.cuh"
 
 namespace spd {
 
@@ -70,6 +71,13 @@ struct Worker {
     bool done = false;
     double last_loss = 0.0;
     std::uint64_t last_b = 0;
+    // evaluation view: train + eval events, their features and full-graph CSR
+    std::uint64_t E_eval = 0;
+    DevBuf<std::uint32_t> x_src, x_dst, x_adj_nbr, x_adj_ev, x_pool;
+    DevBuf<double> x_ts, x_adj_ts;
+    DevBuf<__nv_bfloat16> x_feat;
+    DevBuf<std::uint64_t> x_adj_off;
+    std::uint32_t x_n_pool = 0;
     // debug taps of the last step (filled only when TGNTrainer::debug_ is set)
     std::vector<float> tap_emb;
     std::vector<std::uint32_t> tap_roots, tap_nbr;
@@ -95,8 +103,15 @@ public:
     void step(float* loss_out);
     void end_epoch();
     void run_epoch(int epoch, double* mean_loss);
-    void evaluate(int worker, const spd_edge* e, const std::uint64_t* eids, std::uint64_t n,
-                  std::uint64_t neg_seed, float* pos, float* neg);
+    // Evaluation events (routed val then test edges, global ids, time-ordered)
+    // appended after the worker's training events: the full-graph neighbour
+    // finder and feature rows cover train + eval events.
+    void set_eval_events(int worker, const spd_edge* e, const std::uint64_t* eids,
+                         std::uint64_t n);
+    // Score eval events [lo, hi) in batches (positives + one sampled negative
+    // each) and advance the memory through them; no gradients.
+    void evaluate(int worker, std::uint64_t lo, std::uint64_t hi, std::uint64_t neg_seed,
+                  float* pos, float* neg);
 
     std::size_t param_count() const { return lay_.total; }
     void get_params(float* out) const;
@@ -122,10 +137,12 @@ public:
     cudaStream_t stream() const { return stream_; }
 
 private:
-    void worker_step(Worker& w, std::uint64_t step_in_epoch);
+    void worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t lo, int B,
+                     std::uint64_t nb, bool train, int slot_idx);
+    void backward(Worker& w, const tgnk::WorkerDev& wd, int B);
     void worker_post(Worker& w);
     void flush_pending(Worker& w);
-    void gru_forward(Worker& w, bool train);
+    void gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train);
     void allreduce_grads();
     void adam();
     void sync_shared();
@@ -149,6 +166,8 @@ private:
     int epoch_ = 0;
     std::vector<NodeId> shared_;
     DevBuf<float> params_, grads_, adam_m_, adam_v_;
+    DevBuf<float> params_tc_;  // tf32-rounded copy read by the tensor-core GEMMs
+    void refresh_tc_weights();
     DevBuf<double> tgrad_;  // f64 accumulators for the time encoder grads (2T)
     std::unique_ptr<Scratch> s_;
     StepTimes times_;

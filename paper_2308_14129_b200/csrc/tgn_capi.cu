@@ -52,10 +52,13 @@ spd_status spd_tgn_end_epoch(spd_tgn_trainer* t) { GUARD({ t->t->end_epoch(); })
 spd_status spd_tgn_run_epoch(spd_tgn_trainer* t, int32_t epoch, double* mean_loss) {
     GUARD({ t->t->run_epoch(epoch, mean_loss); });
 }
-spd_status spd_tgn_evaluate(spd_tgn_trainer* t, int32_t worker, const spd_edge* e,
-                            const uint64_t* eids, uint64_t n, uint64_t neg_seed,
-                            float* pos_scores, float* neg_scores) {
-    GUARD({ t->t->evaluate(worker, e, eids, n, neg_seed, pos_scores, neg_scores); });
+spd_status spd_tgn_set_eval_events(spd_tgn_trainer* t, int32_t worker, const spd_edge* e,
+                                   const uint64_t* eids, uint64_t n) {
+    GUARD({ t->t->set_eval_events(worker, e, eids, n); });
+}
+spd_status spd_tgn_evaluate(spd_tgn_trainer* t, int32_t worker, uint64_t lo, uint64_t hi,
+                            uint64_t neg_seed, float* pos_scores, float* neg_scores) {
+    GUARD({ t->t->evaluate(worker, lo, hi, neg_seed, pos_scores, neg_scores); });
 }
 spd_status spd_tgn_param_count(const spd_tgn_trainer* t, uint64_t* n) {
     GUARD({ *n = t->t->param_count(); });

@@ -32,6 +32,16 @@ __host__ __device__ __forceinline__ std::uint64_t neg_base(std::uint64_t seed, s
     return mix64(mix64(mix64(mix64(seed) ^ epoch) ^ worker) ^ step);
 }
 
+// fp32 -> nearest tf32 (ties away; low 13 mantissa bits cleared). tcgen05
+// kind::tf32 ignores those bits (truncation, a biased error that adds up
+// coherently over a dot product); operands rounded here first are read exactly.
+__device__ __forceinline__ float tf32r(float x) {
+    std::uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ float rnd_if(float x, int rnd) { return rnd ? tf32r(x) : x; }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

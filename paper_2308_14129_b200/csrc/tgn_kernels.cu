@@ -21,6 +21,9 @@ __device__ __forceinline__ const float* memx_row(const WorkerDev& w, const float
 }
 
 __device__ __forceinline__ float softplusf(float x) { return x > 20.f ? x : log1pf(expf(x)); }
+__device__ __forceinline__ float4 r4(float4 v, int rnd) {
+    return rnd ? make_float4(tf32r(v.x), tf32r(v.y), tf32r(v.z), tf32r(v.w)) : v;
+}
 }  // namespace
 
 __global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
@@ -87,14 +90,15 @@ __global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const flo
     const float* mn = w.mem + (std::size_t)node * d.D;
     const float* mo = w.mem + (std::size_t)other * d.D;
     for (int c = lane; c < d.D; c += 32) {
-        const float v = mn[c];
+        const float v = rnd_if(mn[c], d.rnd);
         xr[c] = v;
         hr[c] = v;
-        xr[d.D + c] = mo[c];
+        xr[d.D + c] = rnd_if(mo[c], d.rnd);
     }
     const __nv_bfloat16* fr = w.feat + (std::size_t)ev * d.Fp;
     for (int c = lane; c < d.F; c += 32) xr[2 * d.D + c] = __bfloat162float(fr[c]);
-    for (int c = lane; c < d.T; c += 32) xr[2 * d.D + d.F + c] = time_cos(time_w[c], time_b[c], dt);
+    for (int c = lane; c < d.T; c += 32)
+        xr[2 * d.D + d.F + c] = rnd_if(time_cos(time_w[c], time_b[c], dt), d.rnd);
 }
 
 // GRUCell (PyTorch gate order r, z, n) on G_i = W_ih x + b_ih, G_h = W_hh h + b_hh.
@@ -110,7 +114,7 @@ __global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh,
     const float z = sigmoidf_(gi[d.D + c] + gh[d.D + c]);
     const float ghn = gh[2 * d.D + c];
     const float n = tanhf(gi[2 * d.D + c] + r * ghn);
-    const float hv = h[(std::size_t)u * d.ld_h + c];
+    const float hv = w.mem[(std::size_t)w.pU[u] * d.D + c];  // exact h (h_gru may be tf32-rounded)
     mem_new[(std::size_t)u * d.D + c] = (1.f - z) * n + z * hv;
     if (save) {
         float* s = save + (std::size_t)u * 4 * d.D;
@@ -133,8 +137,8 @@ __global__ void k_embed_gather(WorkerDev w, Dims d, int R, const float* time_w,
     if (row < R) {
         const float* m = memx_row(w, mem_new, d.D, roots[row]);
         float* q = q_in + (std::size_t)row * d.ld_q;
-        for (int c = lane; c < d.D; c += 32) q[c] = m[c];
-        for (int c = lane; c < d.T; c += 32) q[d.D + c] = time_cos(time_w[c], time_b[c], 0.0);
+        for (int c = lane; c < d.D; c += 32) q[c] = rnd_if(m[c], d.rnd);
+        for (int c = lane; c < d.T; c += 32) q[d.D + c] = rnd_if(time_cos(time_w[c], time_b[c], 0.0), d.rnd);
         return;
     }
     const int kr = row - R;  // r * K + j
@@ -145,11 +149,11 @@ __global__ void k_embed_gather(WorkerDev w, Dims d, int R, const float* time_w,
         return;
     }
     const float* m = memx_row(w, mem_new, d.D, nbr_node[kr]);
-    for (int c = lane; c < d.D; c += 32) o[c] = m[c];
+    for (int c = lane; c < d.D; c += 32) o[c] = rnd_if(m[c], d.rnd);
     // column order [s_nbr | phi(dt) | e]: the gradient-carrying columns are a
     // contiguous prefix, so the data-gradient GEMM computes only D + T columns
     const double dt = nbr_dt[kr];
-    for (int c = lane; c < d.T; c += 32) o[d.D + c] = time_cos(time_w[c], time_b[c], dt);
+    for (int c = lane; c < d.T; c += 32) o[d.D + c] = rnd_if(time_cos(time_w[c], time_b[c], dt), d.rnd);
     const __nv_bfloat16* fr = w.feat + (std::size_t)nbr_ev[kr] * d.Fp;
     for (int c = lane; c < d.F; c += 32) o[d.D + d.T + c] = __bfloat162float(fr[c]);
 }
@@ -203,7 +207,7 @@ __global__ void k_attn_fwd(Dims d, int R, const int* cnt, const float* Q, const 
         float acc = 0.f;
         for (int j = 0; j < c_n; ++j)
             acc += s[h * d.K + j] * KV[((std::size_t)r * d.K + j) * d.ld_KV + d.DQ + c];
-        cr[c] = acc;
+        cr[c] = rnd_if(acc, d.rnd);
     }
 }
 
@@ -313,6 +317,10 @@ __global__ void __launch_bounds__(256) k_attn_fwd_reg(Dims d, int R, const int* 
         oa.x += a0 * ka[j].x; oa.y += a0 * ka[j].y; oa.z += a0 * ka[j].z; oa.w += a0 * ka[j].w;
         ob.x += a1 * kb[j].x; ob.y += a1 * kb[j].y; ob.z += a1 * kb[j].z; ob.w += a1 * kb[j].w;
     }
+    if (d.rnd) {
+        oa = make_float4(tf32r(oa.x), tf32r(oa.y), tf32r(oa.z), tf32r(oa.w));
+        ob = make_float4(tf32r(ob.x), tf32r(ob.y), tf32r(ob.z), tf32r(ob.w));
+    }
     if (has0) cr[lane] = oa;
     if (has1) cr[lane + 32] = ob;
 }
@@ -376,9 +384,9 @@ __global__ void __launch_bounds__(256) k_attn_bwd_reg(Dims d, int R, const int* 
             if (h0 == h) a0 = a[h][j];
             if (h1 == h) a1 = a[h][j];
         }
-        if (has0) obase[j * ld4 + nc + lane] = make_float4(a0 * ga.x, a0 * ga.y, a0 * ga.z, a0 * ga.w);
+        if (has0) obase[j * ld4 + nc + lane] = r4(make_float4(a0 * ga.x, a0 * ga.y, a0 * ga.z, a0 * ga.w), d.rnd);
         if (has1)
-            obase[j * ld4 + nc + lane + 32] = make_float4(a1 * gb.x, a1 * gb.y, a1 * gb.z, a1 * gb.w);
+            obase[j * ld4 + nc + lane + 32] = r4(make_float4(a1 * gb.x, a1 * gb.y, a1 * gb.z, a1 * gb.w), d.rnd);
     }
     // d score_hj = alpha_hj (dalpha_hj - sum_k alpha_hk dalpha_hk)
 #pragma unroll
@@ -413,11 +421,11 @@ __global__ void __launch_bounds__(256) k_attn_bwd_reg(Dims d, int R, const int* 
         }
         oa.x += s0 * va[j].x; oa.y += s0 * va[j].y; oa.z += s0 * va[j].z; oa.w += s0 * va[j].w;
         ob.x += s1 * vb[j].x; ob.y += s1 * vb[j].y; ob.z += s1 * vb[j].z; ob.w += s1 * vb[j].w;
-        if (has0) obase[j * ld4 + lane] = make_float4(s0 * qa.x, s0 * qa.y, s0 * qa.z, s0 * qa.w);
-        if (has1) obase[j * ld4 + lane + 32] = make_float4(s1 * qb.x, s1 * qb.y, s1 * qb.z, s1 * qb.w);
+        if (has0) obase[j * ld4 + lane] = r4(make_float4(s0 * qa.x, s0 * qa.y, s0 * qa.z, s0 * qa.w), d.rnd);
+        if (has1) obase[j * ld4 + lane + 32] = r4(make_float4(s1 * qb.x, s1 * qb.y, s1 * qb.z, s1 * qb.w), d.rnd);
     }
-    if (has0) dq4[lane] = oa;
-    if (has1) dq4[lane + 32] = ob;
+    if (has0) dq4[lane] = r4(oa, d.rnd);
+    if (has1) dq4[lane + 32] = r4(ob, d.rnd);
 }
 
 #define SPD_ATTN_INST(KM, HM)                                                                  \
@@ -437,9 +445,9 @@ __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* 
     if (r >= R) return;
     float* o = m_in + (std::size_t)r * d.ld_m;
     const bool has = cnt[r] > 0;
-    for (int c = lane; c < d.DQ; c += 32) o[c] = has ? O[(std::size_t)r * d.DQ + c] : 0.f;
+    for (int c = lane; c < d.DQ; c += 32) o[c] = has ? rnd_if(O[(std::size_t)r * d.DQ + c], d.rnd) : 0.f;
     const float* m = memx_row(w, mem_new, d.D, roots[r]);
-    for (int c = lane; c < d.D; c += 32) o[d.DQ + c] = m[c];
+    for (int c = lane; c < d.D; c += 32) o[d.DQ + c] = rnd_if(m[c], d.rnd);
 }
 
 // Decoder input rows: p < B -> [z_src | z_dst], p >= B -> [z_src | z_neg].
@@ -498,9 +506,9 @@ __global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb) {
     const float* a = dd_in + (std::size_t)i * d.ld_din;
     const float* b = dd_in + (std::size_t)(B + i) * d.ld_din;
     for (int c = lane; c < d.D; c += 32) {
-        d_emb[(std::size_t)i * d.D + c] = a[c] + b[c];
-        d_emb[(std::size_t)(B + i) * d.D + c] = a[d.D + c];
-        d_emb[(std::size_t)(2 * B + i) * d.D + c] = b[d.D + c];
+        d_emb[(std::size_t)i * d.D + c] = rnd_if(a[c] + b[c], d.rnd);
+        d_emb[(std::size_t)(B + i) * d.D + c] = rnd_if(a[d.D + c], d.rnd);
+        d_emb[(std::size_t)(2 * B + i) * d.D + c] = rnd_if(b[d.D + c], d.rnd);
     }
 }
 
@@ -548,7 +556,7 @@ __global__ void k_attn_bwd(Dims d, int R, const int* cnt, const float* Q, const 
         float acc = 0.f;
         for (int j = 0; j < c_n; ++j)
             acc += ds[h * d.K + j] * KV[((std::size_t)r * d.K + j) * d.ld_KV + c];
-        dq[c] = acc * inv;
+        dq[c] = rnd_if(acc * inv, d.rnd);
     }
     const float* q = Q + (std::size_t)r * d.ld_Q;
     for (int j = 0; j < d.K; ++j) {
@@ -559,8 +567,8 @@ __global__ void k_attn_bwd(Dims d, int R, const int* cnt, const float* Q, const 
         }
         for (int c = lane; c < d.DQ; c += 32) {
             const int h = c / dh;
-            o[c] = ds[h * d.K + j] * q[c] * inv;
-            o[d.DQ + c] = a[h * d.K + j] * dc[c];
+            o[c] = rnd_if(ds[h * d.K + j] * q[c] * inv, d.rnd);
+            o[d.DQ + c] = rnd_if(a[h * d.K + j] * dc[c], d.rnd);
         }
     }
 }
@@ -748,7 +756,7 @@ __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* sav
     const float* s = save + (std::size_t)u * 4 * d.D;
     const float r = s[c], z = s[d.D + c], n = s[2 * d.D + c], ghn = s[3 * d.D + c];
     const float g = dH[(std::size_t)u * d.D + c];
-    const float hv = h[(std::size_t)u * d.ld_h + c];
+    const float hv = w.mem[(std::size_t)w.pU[u] * d.D + c];  // exact h
     const float dn = g * (1.f - z);
     const float dz = g * (hv - n);
     const float dpn = dn * (1.f - n * n);
@@ -756,17 +764,17 @@ __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* sav
     const float dpz = dz * z * (1.f - z);
     float* gi = dGi + (std::size_t)u * d.ld_g;
     float* gh = dGh + (std::size_t)u * d.ld_g;
-    gi[c] = dpr;
-    gi[d.D + c] = dpz;
-    gi[2 * d.D + c] = dpn;
-    gh[c] = dpr;
-    gh[d.D + c] = dpz;
-    gh[2 * d.D + c] = dpn * r;
+    gi[c] = rnd_if(dpr, d.rnd);
+    gi[d.D + c] = rnd_if(dpz, d.rnd);
+    gi[2 * d.D + c] = rnd_if(dpn, d.rnd);
+    gh[c] = rnd_if(dpr, d.rnd);
+    gh[d.D + c] = rnd_if(dpz, d.rnd);
+    gh[2 * d.D + c] = rnd_if(dpn * r, d.rnd);
 }
 
 __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
                        float lr, float b1, float one_m_b1, float b2, float one_m_b2, float bc1,
-                       float bc2, float eps) {
+                       float bc2, float eps, float* p_tc) {
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float gi = g[i] / scale;
@@ -776,7 +784,14 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t
     v[i] = vi;
     const float mh = mi / bc1;
     const float vh = vi / bc2;
-    p[i] = p[i] - lr * mh / (sqrtf(vh) + eps);
+    const float pn = p[i] - lr * mh / (sqrtf(vh) + eps);
+    p[i] = pn;
+    if (p_tc) p_tc[i] = tf32r(pn);
+}
+
+__global__ void k_round_tf32(const float* src, float* dst, std::size_t n) {
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = tf32r(src[i]);
 }
 
 // Persist the GRU rows of pending nodes (K11) and clear their slots.

@@ -20,6 +20,7 @@ struct Dims {
     int ld_x, ld_h, ld_q, ld_kv, ld_ctx, ld_m, ld_z, ld_din, ld_d1;  // aug strides
     int ld_g;  // 3D rounded
     int ld_Q, ld_KV;  // row strides of Q/dQ/dctx (DQ) and KV/dKV (2 DQ), 128-B multiples
+    int rnd;          // round tensor-core operands to tf32 (round-to-nearest) at production
 };
 
 struct WorkerDev {
@@ -99,7 +100,8 @@ __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* sav
                           float* dGi, float* dGh);
 __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
                        float lr, float b1, float one_m_b1, float b2, float one_m_b2, float bc1,
-                       float bc2, float eps);
+                       float bc2, float eps, float* p_tc);
+__global__ void k_round_tf32(const float* src, float* dst, std::size_t n);
 __global__ void k_persist(WorkerDev w, int D, const float* mem_new);
 __global__ void k_pending(WorkerDev w, std::uint64_t lo, int B);
 __global__ void k_gen_features(__nv_bfloat16* feat, const std::uint64_t* eids, std::uint64_t E,

@@ -175,14 +175,14 @@ void gemm_wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, in
 // spd_tgn_config::gemm_mode: 0 = FP32 FFMA, 1 = tcgen05 TF32.
 void proj_fwd(bool tc, const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M,
               int N, int K, const int* M_dev, cudaStream_t s, int epi = 0,
-              const float* mask = nullptr, int ldmask = 0) {
-    if (tc) umma::fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
+              const float* mask = nullptr, int ldmask = 0, int rnd = 0) {
+    if (tc) umma::fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask, rnd);
     else gemm_fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
 }
 void proj_dgrad(bool tc, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
                 int M, int N, int K, const int* M_dev, cudaStream_t s, int epi = 0,
-                const float* mask = nullptr, int ldmask = 0) {
-    if (tc) umma::dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
+                const float* mask = nullptr, int ldmask = 0, int rnd = 0) {
+    if (tc) umma::dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask, rnd);
     else gemm_dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
 }
 void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw,
@@ -352,6 +352,8 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     std::vector<float> flat;
     init_params_host(lay_, cfg.seed_init, flat);
     params_.alloc(lay_.total); params_.upload(flat.data(), lay_.total, stream_);
+    params_tc_.alloc(lay_.total);
+    refresh_tc_weights();
     grads_.alloc(lay_.total); grads_.zero(stream_);
     adam_m_.alloc(lay_.total); adam_m_.zero(stream_);
     adam_v_.alloc(lay_.total); adam_v_.zero(stream_);
@@ -368,6 +370,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     d.ld_ctx = ld_aug(d.DQ); d.ld_m = ld_aug(d.DQ + D); d.ld_z = ld_aug(D); d.ld_din = ld_aug(2 * D);
     d.ld_d1 = ld_aug(D); d.ld_g = ld32(3 * D);
     d.ld_Q = ld32(d.DQ); d.ld_KV = ld32(2 * d.DQ);
+    d.rnd = cfg.gemm_mode == 1 ? 1 : 0;
     const int R = s.R, RK = s.RK, U = s.U;
     s.roots.alloc(R); s.root_t.alloc(R); s.cnt.alloc(R);
     s.nbr_node.alloc(RK); s.nbr_ev.alloc(RK); s.nbr_dt.alloc(RK);
@@ -477,59 +480,59 @@ void TGNTrainer::begin_epoch(int epoch) {
     }
 }
 
-void TGNTrainer::gru_forward(Worker& w, bool train) {
+void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train) {
     Scratch& s = *s_;
     const auto& d = s.d;
-    const auto wd = devview(w);
     const float* P = params_.p;
     const bool tc = cfg_.gemm_mode == 1;
+    const float* PW = tc ? params_tc_.p : params_.p;  // tf32-rounded weights for tensor cores
     launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
         wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
     SPD_CUDA(cudaGetLastError());
-    proj_fwd(tc, s.x_gru.p, d.ld_x, P + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, 3 * d.D,
+    proj_fwd(tc, s.x_gru.p, d.ld_x, PW + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, 3 * d.D,
              d.DM + 1, w.nU.p, stream_);
-    proj_fwd(tc, s.h_gru.p, d.ld_h, P + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, 3 * d.D,
+    proj_fwd(tc, s.h_gru.p, d.ld_h, PW + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, 3 * d.D,
              d.D + 1, w.nU.p, stream_);
     launch(tgnk::k_gru_fwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, stream_, 
         wd, d, s.Gi.p, s.Gh.p, s.h_gru.p, train ? s.gsave.p : nullptr, s.mem_new.p);
     SPD_CUDA(cudaGetLastError());
 }
 
-void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
+// One batch of one worker: events [lo, lo+B) of the view's event list.
+// train: forward + backward (weight grads accumulate into grads_) + post;
+// eval (train = false): forward + post (scores in s.logits), no gradients.
+void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t lo, int B,
+                             std::uint64_t nb, bool train, int slot_idx) {
     Scratch& s = *s_;
     const auto& d = s.d;
-    const std::uint64_t lo = w.pos * cfg_.batch_size;
-    const int B = static_cast<int>(std::min<std::uint64_t>(w.E, lo + cfg_.batch_size) - lo);
     w.last_b = B;
     const int R = 3 * B, RK = R * d.K;
-    const auto wd = devview(w);
     float* P = params_.p;
     float* G = grads_.p;
     cudaStream_t st = stream_;
     const bool tc = cfg_.gemm_mode == 1;  // tensor cores for GRU + attention projections only
-    if (w.pos == 0) {  // loop_start: reset (pac_sim.cpp:238)
+    const float* PW = tc ? params_tc_.p : params_.p;
+    if (train && w.pos == 0) {  // loop_start: reset (pac_sim.cpp:238)
         w.mem.zero(st);
         w.lu.zero(st);
         w.nU.zero(st);
     }
-    const std::uint64_t nb = neg_base(cfg_.seed_neg, std::uint64_t(epoch_), std::uint64_t(w.gid),
-                                      step_in_epoch);
     timed("roots_nbrs", [&] {
         launch(tgnk::k_roots_nbrs, blocks_for(R, 128), 128, 0, st, wd, lo, B, nb, d.K, s.roots.p,
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     });
-    timed("gru_fwd", [&] { gru_forward(w, true); });
+    timed("gru_fwd", [&] { gru_forward(w, wd, train); });
     timed("embed_gather", [&] {
         launch(tgnk::k_embed_gather, blocks_for(std::size_t(R) * (1 + d.K) * 32), 256, 0, st, 
             wd, d, R, P + lay_.time_w, P + lay_.time_b, s.roots.p, s.nbr_node.p, s.nbr_ev.p,
             s.nbr_dt.p, s.cnt.p, s.mem_new.p, s.q_in.p, s.kv_in.p);
     });
     timed("gemm_q", [&] {
-        proj_fwd(tc, s.q_in.p, d.ld_q, P + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
+        proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
                  d.DQ + 1, nullptr, st);
     });
     timed("gemm_kv", [&] {
-        proj_fwd(tc, s.kv_in.p, d.ld_kv, P + lay_.att_kv.off, lay_.att_kv.ld, s.KV.p, d.ld_KV, RK,
+        proj_fwd(tc, s.kv_in.p, d.ld_kv, PW + lay_.att_kv.off, lay_.att_kv.ld, s.KV.p, d.ld_KV, RK,
                  2 * d.DQ, d.DK + 1, nullptr, st);
     });
     const std::size_t attn_smem = std::size_t(8) * d.H * d.K * sizeof(float);
@@ -547,13 +550,13 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
                    s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
     });
     timed("head_fwd", [&] {
-        proj_fwd(tc, s.ctx.p, d.ld_ctx, P + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
+        proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
                  d.DQ + 1, nullptr, st);
         launch(tgnk::k_merge_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, 
             wd, d, R, s.roots.p, s.cnt.p, s.O.p, s.mem_new.p, s.m_in.p);
-        proj_fwd(tc, s.m_in.p, d.ld_m, P + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
-                 d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU);
-        proj_fwd(tc, s.Z1.p, d.ld_z, P + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
+        proj_fwd(tc, s.m_in.p, d.ld_m, PW + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
+                 d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU, nullptr, 0, tc);
+        proj_fwd(tc, s.Z1.p, d.ld_z, PW + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
                  nullptr, st);
         launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, d, B, s.emb.p,
                                                                                  s.d_in.p);
@@ -562,14 +565,30 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
         launch(tgnk::k_dec_head, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, 
             d, B, s.D1.p, P + lay_.dec2.off, s.dlogit.p, s.lossv.p, s.dD1.p, s.logits.p);
     });
-    // per-worker loss slot
-    int slot_idx = 0;
-    for (std::size_t k = 0; k < workers_.size(); ++k)
-        if (workers_[k].get() == &w) slot_idx = static_cast<int>(k);
     launch(tgnk::k_sum_loss, 1, 1024, 0, st, s.lossv.p, 2 * B, s.loss.p + slot_idx);
-    SPD_CUDA(cudaGetLastError());
+    if (train) backward(w, wd, B);
+    // persist this batch's memory update and store its last messages now,
+    // while the scratch still holds this worker's rows (K11, K3)
+    timed("post", [&] {
+        launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
+        launch(tgnk::k_pending, 1, 1024, 0, st, wd, lo, B);
+    });
+}
 
-    // ------------------------------------------------------------ backward
+// Hand-written backward of one worker's batch; weight-gradient GEMMs go to the
+// side stream and are joined before the post phase rewrites their inputs.
+void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
+    Scratch& s = *s_;
+    const auto& d = s.d;
+    const int R = 3 * B, RK = R * d.K;
+    float* P = params_.p;
+    float* G = grads_.p;
+    cudaStream_t st = stream_;
+    const bool tc = cfg_.gemm_mode == 1;
+    const float* PW = tc ? params_tc_.p : params_.p;
+    const std::size_t attn_smem = std::size_t(8) * d.H * d.K * sizeof(float);
+    const bool attn_reg = tgnk::attn_reg_ok(d);
+    const bool attn_small = d.K <= 10 && d.H <= 2;
     timed("head_bwd", [&] {
         side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
                    2 * B, nullptr, s.ws.p, s.ws.n, sd); });
@@ -582,18 +601,18 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
         // merge layer 2 (relu mask from Z1), layer 1
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off, lay_.mrg2.ld, d.D, d.D + 1,
                    R, nullptr, s.ws.p, s.ws.n, sd); });
-        proj_dgrad(tc, s.d_emb.p, d.D, P + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
-                   nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z);
+        proj_dgrad(tc, s.d_emb.p, d.D, PW + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
+                   nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z, tc);
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off, lay_.mrg1.ld, d.D,
                    d.DQ + d.D + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
-        proj_dgrad(tc, s.dZ1.p, d.D, P + lay_.mrg1.off, lay_.mrg1.ld, s.dm_in.p, d.ld_m, R,
-                   d.DQ + d.D, d.D, nullptr, st);
+        proj_dgrad(tc, s.dZ1.p, d.D, PW + lay_.mrg1.off, lay_.mrg1.ld, s.dm_in.p, d.ld_m, R,
+                   d.DQ + d.D, d.D, nullptr, st, 0, nullptr, 0, tc);
         launch(tgnk::k_mask_rows, blocks_for(std::size_t(R) * 32), 256, 0, st, s.dm_in.p, R, d.DQ,
                                                                           d.ld_m, s.cnt.p);
         // output projection
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
                    d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
-        proj_dgrad(tc, s.dm_in.p, d.ld_m, P + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R, d.DQ,
+        proj_dgrad(tc, s.dm_in.p, d.ld_m, PW + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R, d.DQ,
                    d.DQ, nullptr, st);
     });
     timed("attn_bwd", [&] {
@@ -612,13 +631,13 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
                    2 * d.DQ, d.DK + 1, RK, nullptr, s.ws.p, s.ws.n, sd); });
     });
     timed("gemm_kv_dgrad", [&] {
-        proj_dgrad(tc, s.dKV.p, d.ld_KV, P + lay_.att_kv.off, lay_.att_kv.ld, s.dkv_in.p, d.ld_kv, RK,
+        proj_dgrad(tc, s.dKV.p, d.ld_KV, PW + lay_.att_kv.off, lay_.att_kv.ld, s.dkv_in.p, d.ld_kv, RK,
                    d.D + d.T, 2 * d.DQ, nullptr, st);  // only [s_nbr | phi] carry gradient
     });
     timed("q_bwd", [&] {
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
                    d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
-        proj_dgrad(tc, s.dQ.p, d.ld_Q, P + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
+        proj_dgrad(tc, s.dQ.p, d.ld_Q, PW + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
                    d.DQ, nullptr, st);
     });
     timed("mem_time_bwd", [&] {
@@ -654,18 +673,12 @@ void TGNTrainer::worker_step(Worker& w, std::uint64_t step_in_epoch) {
     // side-stream weight grads read the pending set (nU, GRU inputs) that the
     // post phase rewrites: join first
     join_side();
-    // persist this batch's memory update and store its last messages now,
-    // while the scratch still holds this worker's rows (K11, K3)
-    timed("post", [&] {
-        launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
-        launch(tgnk::k_pending, 1, 1024, 0, st, wd, lo, B);
-    });
 }
 
 void TGNTrainer::flush_pending(Worker& w) {
     // loop end: apply the pending messages without gradient, persist
-    gru_forward(w, false);
     const auto wd = devview(w);
+    gru_forward(w, wd, false);
     launch(tgnk::k_persist, blocks_for(std::size_t(s_->U) * 32), 256, 0, stream_, wd, lay_.D,
            s_->mem_new.p);
     w.nU.zero(stream_);
@@ -785,7 +798,7 @@ void TGNTrainer::adam() {
     launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, stream_, 
         params_.p, grads_.p, adam_m_.p, adam_v_.p, lay_.total, float(total_workers_), cfg_.lr,
         cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2), bc1,
-        bc2, cfg_.adam_eps);
+        bc2, cfg_.adam_eps, cfg_.gemm_mode == 1 ? params_tc_.p : nullptr);
     SPD_CUDA(cudaGetLastError());
 }
 
@@ -798,7 +811,11 @@ void TGNTrainer::step(float* loss_out) {
     for (std::size_t k = 0; k < workers_.size(); ++k) {
         Worker& w = *workers_[k];
         if (w.batches == 0) continue;
-        worker_step(w, step_in_epoch_);
+        const std::uint64_t lo = w.pos * cfg_.batch_size;
+        const int B = static_cast<int>(std::min<std::uint64_t>(w.E, lo + cfg_.batch_size) - lo);
+        const std::uint64_t nb = neg_base(cfg_.seed_neg, std::uint64_t(epoch_), std::uint64_t(w.gid),
+                                          step_in_epoch_);
+        worker_step(w, devview(w), lo, B, nb, true, static_cast<int>(k));
         if (debug_) {  // taps before the next worker reuses the scratch
             const std::uint64_t B = w.last_b;
             const int D = lay_.D, K = lay_.Kn;
@@ -863,9 +880,15 @@ void TGNTrainer::get_params(float* out) const {
     params_.download(out, lay_.total, stream_);
     SPD_CUDA(cudaStreamSynchronize(stream_));
 }
+void TGNTrainer::refresh_tc_weights() {
+    launch(tgnk::k_round_tf32, blocks_for(lay_.total), 256, 0, stream_, params_.p, params_tc_.p,
+           lay_.total);
+}
+
 void TGNTrainer::set_params(const float* in) {
     DeviceGuard g(device_);
     params_.upload(in, lay_.total, stream_);
+    refresh_tc_weights();
     SPD_CUDA(cudaStreamSynchronize(stream_));
 }
 void TGNTrainer::get_grads(float* out) const {
@@ -1053,9 +1076,116 @@ void TGNTrainer::sync_shared() {
     SPD_CUDA(cudaStreamSynchronize(st));
 }
 
-void TGNTrainer::evaluate(int, const spd_edge*, const std::uint64_t*, std::uint64_t, std::uint64_t,
-                          float*, float*) {
-    internal_error("NotImplemented", "evaluation lands with the eval-routing row (SURVEY 8f #2)");
+namespace {
+// per-node time-sorted CSR over both directions of a time-ordered event list
+// (ties keep event order, src side first: the oracle's (ts, event, role) order)
+void build_adj(const std::vector<std::uint32_t>& src, const std::vector<std::uint32_t>& dst,
+               const std::vector<double>& ts, NodeId N, std::vector<std::uint64_t>& off,
+               std::vector<std::uint32_t>& nbr, std::vector<std::uint32_t>& ev,
+               std::vector<double>& ats) {
+    const std::uint64_t E = src.size();
+    off.assign(std::size_t(N) + 1, 0);
+    for (std::uint64_t k = 0; k < E; ++k) {
+        ++off[src[k] + 1];
+        ++off[dst[k] + 1];
+    }
+    for (NodeId i = 0; i < N; ++i) off[i + 1] += off[i];
+    std::vector<std::uint64_t> fill(off.begin(), off.end() - 1);
+    nbr.resize(2 * E);
+    ev.resize(2 * E);
+    ats.resize(2 * E);
+    for (std::uint64_t k = 0; k < E; ++k) {
+        std::uint64_t q = fill[src[k]]++;
+        nbr[q] = dst[k]; ev[q] = static_cast<std::uint32_t>(k); ats[q] = ts[k];
+        q = fill[dst[k]]++;
+        nbr[q] = src[k]; ev[q] = static_cast<std::uint32_t>(k); ats[q] = ts[k];
+    }
+}
+}  // namespace
+
+void TGNTrainer::set_eval_events(int wid, const spd_edge* e, const std::uint64_t* eids,
+                                 std::uint64_t n) {
+    Worker& w = worker(wid);
+    DeviceGuard g(device_);
+    const std::uint64_t E = w.E, Et = E + n;
+    if (Et > 0xFFFFFFFFull) data_error("InvalidParams", "partition exceeds 2^32 events");
+    std::vector<std::uint32_t> src(Et), dst(Et);
+    std::vector<double> ts(Et);
+    for (std::uint64_t k = 0; k < E; ++k) {
+        src[k] = w.ev_host[k].src;
+        dst[k] = w.ev_host[k].dst;
+        ts[k] = w.ev_host[k].ts;
+    }
+    auto loc = [&](NodeId gid) -> std::uint32_t {
+        auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), gid);
+        if (it == w.nodes.end() || *it != gid)
+            data_error("InvalidPartition", "eval edge endpoint outside the partition (route with "
+                                           "assign_eval_edges)");
+        return static_cast<std::uint32_t>(it - w.nodes.begin());
+    };
+    for (std::uint64_t k = 0; k < n; ++k) {
+        src[E + k] = loc(e[k].src);
+        dst[E + k] = loc(e[k].dst);
+        ts[E + k] = e[k].ts;
+        if (ts[E + k] < ts[E + k - (E + k > 0 ? 1 : 0)])
+            data_error("NonChronological", "eval edges must follow the training events in time");
+    }
+    std::vector<std::uint64_t> off;
+    std::vector<std::uint32_t> nbr, ev;
+    std::vector<double> ats;
+    build_adj(src, dst, ts, w.N, off, nbr, ev, ats);
+    std::vector<std::uint32_t> pool(dst);
+    std::sort(pool.begin(), pool.end());
+    pool.erase(std::unique(pool.begin(), pool.end()), pool.end());
+    if (pool.empty()) pool.push_back(0);
+    w.x_n_pool = static_cast<std::uint32_t>(pool.size());
+    w.x_src.alloc(Et); w.x_src.upload(src.data(), Et, stream_);
+    w.x_dst.alloc(Et); w.x_dst.upload(dst.data(), Et, stream_);
+    w.x_ts.alloc(Et); w.x_ts.upload(ts.data(), Et, stream_);
+    w.x_adj_off.alloc(off.size()); w.x_adj_off.upload(off.data(), off.size(), stream_);
+    w.x_adj_nbr.alloc(2 * Et); w.x_adj_nbr.upload(nbr.data(), 2 * Et, stream_);
+    w.x_adj_ev.alloc(2 * Et); w.x_adj_ev.upload(ev.data(), 2 * Et, stream_);
+    w.x_adj_ts.alloc(2 * Et); w.x_adj_ts.upload(ats.data(), 2 * Et, stream_);
+    w.x_pool.alloc(pool.size()); w.x_pool.upload(pool.data(), pool.size(), stream_);
+    const int Fp = s_->d.Fp, F = lay_.F;
+    w.x_feat.alloc(std::max<std::uint64_t>(1, Et) * std::max(1, Fp));
+    if (Fp && E)
+        SPD_CUDA(cudaMemcpyAsync(w.x_feat.p, w.feat.p, E * Fp * sizeof(__nv_bfloat16),
+                                 cudaMemcpyDeviceToDevice, stream_));
+    if (Fp && n) {
+        DevBuf<std::uint64_t> de(n);
+        de.upload(eids, n, stream_);
+        launch(tgnk::k_gen_features, blocks_for(n * Fp), 256, 0, stream_, w.x_feat.p + E * Fp, de.p,
+               n, F, Fp, feat_seed_mixed_);
+        SPD_CUDA(cudaStreamSynchronize(stream_));
+    }
+    w.E_eval = n;
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void TGNTrainer::evaluate(int wid, std::uint64_t lo, std::uint64_t hi, std::uint64_t neg_seed,
+                          float* pos, float* neg) {
+    Worker& w = worker(wid);
+    if (hi > w.E_eval || lo > hi) usage_error("eval range outside the eval events");
+    DeviceGuard g(device_);
+    tgnk::WorkerDev v = devview(w);
+    v.ev_src = w.x_src.p; v.ev_dst = w.x_dst.p; v.ev_ts = w.x_ts.p; v.feat = w.x_feat.p;
+    v.adj_off = w.x_adj_off.p; v.adj_nbr = w.x_adj_nbr.p; v.adj_ev = w.x_adj_ev.p;
+    v.adj_ts = w.x_adj_ts.p; v.pool = w.x_pool.p; v.n_pool = w.x_n_pool;
+    int slot_idx = 0;
+    for (std::size_t k = 0; k < workers_.size(); ++k)
+        if (workers_[k].get() == &w) slot_idx = static_cast<int>(k);
+    std::vector<float> lg;
+    for (std::uint64_t b0 = lo; b0 < hi; b0 += cfg_.batch_size) {
+        const int B = static_cast<int>(std::min<std::uint64_t>(hi, b0 + cfg_.batch_size) - b0);
+        const std::uint64_t nb = neg_base(neg_seed, 0xE7A1ull, std::uint64_t(w.gid), b0);
+        worker_step(w, v, w.E + b0, B, nb, false, slot_idx);
+        lg.resize(2 * B);
+        s_->logits.download(lg.data(), 2 * B, stream_);
+        SPD_CUDA(cudaStreamSynchronize(stream_));
+        std::copy(lg.begin(), lg.begin() + B, pos + (b0 - lo));
+        std::copy(lg.begin() + B, lg.end(), neg + (b0 - lo));
+    }
 }
 
 }  // namespace spd

@@ -50,7 +50,14 @@ struct Args {
     int ldmask;
     float* ws;  // PARTIAL: [k_split][M][ldws]
     int ldws;
+    int rnd;    // STORE: round outputs to tf32 (they feed another tensor-core GEMM)
 };
+
+__device__ __forceinline__ float tf32_rn(float x) {
+    std::uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
 
 __device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
@@ -105,26 +112,58 @@ __host__ __device__ constexpr std::uint32_t make_idesc(bool a_mn, bool b_mn, int
            (static_cast<std::uint32_t>(BM >> 4) << 24);
 }
 
-template <bool A_MN, bool B_MN, int BN>
+__device__ __forceinline__ std::uint32_t cluster_rank() {
+    std::uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+// TMA 2D load delivered to the same smem offset of every CTA in `mask`; each
+// destination's mbarrier (same offset) receives the complete_tx.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, std::uint64_t* bar,
+                                               int c0, int c1, std::uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
+
+// BN: N of one MMA (tile sub-width); NSUB sub-tiles side by side in TMEM, so a
+// CTA owns a 128 x (NSUB*BN) output tile and reads its A tile once. CL CTAs
+// along M form a cluster and split the B tile's TMA boxes between them, each
+// box multicast to all CL CTAs (B streamed from L2 once per cluster).
+template <bool A_MN, bool B_MN, int BN, int NSUB, int CL>
 struct Cfg {
+    static constexpr int NT = BN * NSUB;
     static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
-    static constexpr int B_BYTES = BN * BK * 4;
+    static constexpr int B_BYTES = NT * BK * 4;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    static constexpr int BUDGET = 227 * 1024 - 1024 - 256;
+    static constexpr int STAGES_ = BUDGET / STAGE_BYTES >= STAGES ? STAGES : BUDGET / STAGE_BYTES;
+    static constexpr int SMEM = STAGES_ * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int TMEM_COLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : NT <= 256 ? 256 : 512;
+    static constexpr int B_BOXES = B_MN ? NT / 32 : NSUB;  // TMA boxes per stage for B
+    static_assert(STAGES_ >= 2, "tile too large for the smem budget");
+    static_assert(!B_MN || BN % 32 == 0, "MN-major B needs whole 32-column boxes");
+    static_assert(NT <= 512, "accumulator exceeds TMEM");
 };
 
-template <bool A_MN, bool B_MN, int BN>
+template <bool A_MN, bool B_MN, int BN, int NSUB, int CL>
 __global__ void __launch_bounds__(THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB, Args args) {
-    using C_ = Cfg<A_MN, B_MN, BN>;
+    using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;
+    constexpr int NST = C_::STAGES_;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B alignment (SWIZZLE_128B atoms) by offset, keeping shared-space provenance
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
-    std::uint64_t* empty = full + STAGES;
-    std::uint64_t* tmem_full = empty + STAGES;
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + NST * C_::STAGE_BYTES);
+    std::uint64_t* empty = full + NST;
+    std::uint64_t* tmem_full = empty + NST;
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tmem_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -132,8 +171,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (args.M_dev) M = min(M, *args.M_dev);
     int K = args.K;
     if (args.K_dev) K = min(K, *args.K_dev);
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-    if (m0 >= M) return;  // uniform across the CTA
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * C_::NT;
+    // a lone CTA past the rows can leave; cluster members must stay to serve
+    // their share of the multicast B tiles
+    if (CL == 1 && m0 >= M) return;
+    const std::uint32_t crank = CL > 1 ? cluster_rank() : 0;
     int k_begin = 0, k_end = K;
     if (args.k_split > 1) {
         const int per = ((K + args.k_split - 1) / args.k_split + BK - 1) / BK * BK;
@@ -143,9 +185,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int n_k = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
+            mbar_init(empty + s, CL);  // every cluster CTA's MMA releases the stage
         }
         mbar_init(tmem_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -158,14 +200,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if (CL > 1) cluster_sync_all();  // peers' barriers exist before any multicast lands
     asm volatile("tcgen05.fence::after_thread_sync;");
     const std::uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
             for (int kb = 0; kb < n_k; ++kb) {
-                const int s = kb % STAGES;
-                if (kb >= STAGES) mbar_wait(empty + s, ((kb / STAGES) - 1) & 1);
+                const int s = kb % NST;
+                if (kb >= NST) mbar_wait(empty + s, ((kb / NST) - 1) & 1);
                 unsigned char* a_s = smem + s * C_::STAGE_BYTES;
                 unsigned char* b_s = a_s + C_::A_BYTES;
                 mbar_expect_tx(full + s, C_::STAGE_BYTES);
@@ -176,11 +219,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < BM / 32; ++j) tma_load_2d(a_s + j * 32 * 128, &tmA, full + s, m0 + 32 * j, kc);
                 }
-                if (!B_MN) {
-                    tma_load_2d(b_s, &tmB, full + s, kc, n0);
-                } else {
 #pragma unroll
-                    for (int j = 0; j < BN / 32; ++j) tma_load_2d(b_s + j * 32 * 128, &tmB, full + s, n0 + 32 * j, kc);
+                for (int j = 0; j < C_::B_BOXES; ++j) {
+                    if (CL > 1 && (j % CL) != (int)crank) continue;
+                    unsigned char* dst = B_MN ? b_s + j * 32 * 128 : b_s + j * BN * 128;
+                    const int c0 = B_MN ? n0 + 32 * j : kc;
+                    const int c1 = B_MN ? kc : n0 + j * BN;
+                    if (CL > 1) tma_load_2d_mc(dst, &tmB, full + s, c0, c1, (1u << CL) - 1);
+                    else tma_load_2d(dst, &tmB, full + s, c0, c1);
                 }
             }
         }
@@ -188,8 +234,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             constexpr std::uint32_t idesc = make_idesc(A_MN, B_MN, BN);
             for (int kb = 0; kb < n_k; ++kb) {
-                const int s = kb % STAGES;
-                mbar_wait(full + s, (kb / STAGES) & 1);
+                const int s = kb % NST;
+                mbar_wait(full + s, (kb / NST) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const std::uint32_t a_base = smem_u32(smem + s * C_::STAGE_BYTES);
                 const std::uint32_t b_base = a_base + C_::A_BYTES;
@@ -200,19 +246,32 @@ __global__ void __launch_bounds__(THREADS, 1)
                     // BK*128 B apart (LBO), K=8 step = 8 rows = 1024 B.
                     const std::uint64_t ad = A_MN ? make_desc(a_base + kk * 1024, BK * 128, 512, 1)
                                                   : make_desc(a_base + kk * 32, 16, 1024, 2);
-                    const std::uint64_t bd = B_MN ? make_desc(b_base + kk * 1024, BK * 128, 512, 1)
-                                                  : make_desc(b_base + kk * 32, 16, 1024, 2);
                     const std::uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\t"
-                        "setp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-                        "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+#pragma unroll
+                    for (int t = 0; t < NSUB; ++t) {
+                        const std::uint32_t bt = B_MN ? b_base + t * (BN / 32) * (BK * 128)
+                                                      : b_base + t * BN * 128;
+                        const std::uint64_t bd = B_MN ? make_desc(bt + kk * 1024, BK * 128, 512, 1)
+                                                      : make_desc(bt + kk * 32, 16, 1024, 2);
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\t"
+                            "setp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+                                tmem + t * BN),
+                            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                    }
                 }
-                asm volatile(
-                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                        smem_u32(empty + s))
-                    : "memory");
+                if (CL > 1)
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster"
+                        ".multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(empty + s)),
+                        "h"(static_cast<std::uint16_t>((1u << CL) - 1))
+                        : "memory");
+                else
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                            smem_u32(empty + s))
+                        : "memory");
             }
             asm volatile(
                 "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -235,7 +294,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         float* out_base = partial ? args.ws + (std::size_t)blockIdx.z * args.M * args.ldws : args.C;
         const int ldo = partial ? args.ldws : args.ldc;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = 0; c0 < C_::NT; c0 += 32) {
+            if (n0 + c0 >= args.N) break;
             std::uint32_t v[32];
             if (n_k > 0) {
                 const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(quad * 32) << 16) + c0;
@@ -264,22 +324,37 @@ __global__ void __launch_bounds__(THREADS, 1)
                 float* c = out_base + (std::size_t)row0 * ldo + col;
                 // mode/epilogue are CTA-uniform: branch once, keep the plain
                 // store path free of loads
-                if (partial || (args.mode == STORE && args.epi == EPI_NONE)) {
+                if (partial || (args.mode == STORE && args.epi == EPI_NONE && !args.rnd)) {
 #pragma unroll 8
                     for (int r = 0; r < rows; ++r) c[(std::size_t)r * ldo] = stage[r * 33 + lane];
-                } else if (args.mode == ACCUM) {
+                } else if (args.mode == STORE && args.epi == EPI_NONE) {
 #pragma unroll 8
-                    for (int r = 0; r < rows; ++r) c[(std::size_t)r * ldo] += stage[r * 33 + lane];
+                    for (int r = 0; r < rows; ++r) c[(std::size_t)r * ldo] = tf32_rn(stage[r * 33 + lane]);
+                } else if (args.mode == ACCUM) {
+                    // all 32 read-modify-write loads in flight before any use
+                    float cv[32];
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) cv[r] = r < rows ? c[(std::size_t)r * ldo] : 0.f;
+#pragma unroll
+                    for (int r = 0; r < 32; ++r)
+                        if (r < rows) c[(std::size_t)r * ldo] = cv[r] + stage[r * 33 + lane];
                 } else if (args.epi == EPI_RELU) {
 #pragma unroll 8
-                    for (int r = 0; r < rows; ++r)
-                        c[(std::size_t)r * ldo] = fmaxf(stage[r * 33 + lane], 0.f);
-                } else {  // EPI_MASK
+                    for (int r = 0; r < rows; ++r) {
+                        const float x = fmaxf(stage[r * 33 + lane], 0.f);
+                        c[(std::size_t)r * ldo] = args.rnd ? tf32_rn(x) : x;
+                    }
+                } else {  // EPI_MASK: prefetch the 32 mask values, then store
                     const float* mk = args.mask + (std::size_t)row0 * args.ldmask + col;
-#pragma unroll 8
-                    for (int r = 0; r < rows; ++r)
-                        c[(std::size_t)r * ldo] =
-                            mk[(std::size_t)r * args.ldmask] > 0.f ? stage[r * 33 + lane] : 0.f;
+                    float mv[32];
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) mv[r] = r < rows ? mk[(std::size_t)r * args.ldmask] : 0.f;
+#pragma unroll
+                    for (int r = 0; r < 32; ++r)
+                        if (r < rows) {
+                            const float x = mv[r] > 0.f ? stage[r * 33 + lane] : 0.f;
+                            c[(std::size_t)r * ldo] = args.rnd ? tf32_rn(x) : x;
+                        }
                 }
             }
             __syncwarp();
@@ -287,6 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
+    if (CL > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
     asm volatile("tcgen05.fence::after_thread_sync;");
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),

@@ -54,15 +54,31 @@ CUtensorMap make_map(const float* base, std::uint64_t inner, std::uint64_t rows,
     return m;
 }
 
-template <bool A_MN, bool B_MN, int BN>
+template <bool A_MN, bool B_MN, int BN, int NSUB = 1, int CL = 1>
 void run(const CUtensorMap& a, const CUtensorMap& b, const Args& args, dim3 grid, cudaStream_t s) {
-    using C_ = Cfg<A_MN, B_MN, BN>;
+    using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;
+    auto kern = umma_gemm_kernel<A_MN, B_MN, BN, NSUB, CL>;
     static std::once_flag once;
-    std::call_once(once, [] {
-        SPD_CUDA(cudaFuncSetAttribute(umma_gemm_kernel<A_MN, B_MN, BN>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
+    std::call_once(once, [&] {
+        SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
     });
-    umma_gemm_kernel<A_MN, B_MN, BN><<<grid, THREADS, C_::SMEM, s>>>(a, b, args);
+    if (CL == 1) {
+        kern<<<grid, THREADS, C_::SMEM, s>>>(a, b, args);
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(THREADS);
+        cfg.dynamicSmemBytes = C_::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = CL;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, args));
+    }
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
 }
@@ -100,33 +116,71 @@ int pick_bn(int N) {
 std::uint64_t launches() { return g_launch_counter.load(); }
 
 void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N, int K,
-         const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask) {
+         const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask, int rnd) {
     if (!M || !N) return;
+    Args a{};
+    a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
+    a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask; a.rnd = rnd;
+    const int mt = (M + BM - 1) / BM;
+    if (mt >= 64 && N > 256 && N <= 416 && !M_dev) {
+        // one CTA covers all N (2 x 208 in TMEM): A streamed once; W multicast
+        // to CTA pairs: W streamed from L2 once per 256 rows
+        const CUtensorMap ta = make_map(A, K, M, lda, BM);
+        const CUtensorMap tb = make_map(W, K, N, ldw, 208);
+        run<false, false, 208, 2, 2>(ta, tb, a, dim3(1, (mt + 1) / 2 * 2, 1), s);
+        return;
+    }
     const int bn = pick_bn(N);
     const CUtensorMap ta = make_map(A, K, M, lda, BM);
     const CUtensorMap tb = make_map(W, K, N, ldw, bn);
-    Args a{};
-    a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
-    a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask;
-    dispatch<false, false>(bn, ta, tb, a, dim3((N + bn - 1) / bn, (M + BM - 1) / BM, 1), s);
+    dispatch<false, false>(bn, ta, tb, a, dim3((N + bn - 1) / bn, mt, 1), s);
 }
 
 void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N,
-           int K, const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask) {
+           int K, const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask, int rnd) {
     if (!M || !N) return;
-    const int bn = pick_bn(N);  // multiple of 32: whole MN-major column blocks
     const CUtensorMap ta = make_map(A, K, M, lda, BM);
     const CUtensorMap tb = make_map(W, N, K, ldw, BK, true);  // W [K x N], N contiguous
     Args a{};
     a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
-    a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask;
-    dispatch<false, true>(bn, ta, tb, a, dim3((N + bn - 1) / bn, (M + BM - 1) / BM, 1), s);
+    a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask; a.rnd = rnd;
+    const int mt = (M + BM - 1) / BM;
+    if (mt >= 64 && N <= 224 && !M_dev) {  // big: W multicast to CTA pairs
+        run<false, true, 224, 1, 2>(ta, tb, a, dim3(1, (mt + 1) / 2 * 2, 1), s);
+        return;
+    }
+    const int bn = pick_bn(N);  // multiple of 32: whole MN-major column blocks
+    dispatch<false, true>(bn, ta, tb, a, dim3((N + bn - 1) / bn, mt, 1), s);
 }
 
 void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
            int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
            cudaStream_t s) {
     if (!rows || !N_out || !K_in) return;
+    const int mt = (N_out + BM - 1) / BM;
+    if (rows >= 16384 && K_in > 224 && K_in <= 448 && mt >= 2 && mt <= 4 && !rows_dev) {
+        // all M tiles of dW in one cluster: X (the B operand) streamed once,
+        // each 128-row slice of dY^T once; K_in covered by 2 x 224 in TMEM
+        const int ldws = (K_in + 3) / 4 * 4;
+        int split = std::max(1, std::min(rows / (8 * BK), 148 / 4));
+        while (split > 1 && std::size_t(split) * N_out * ldws > ws_cap) --split;
+        const CUtensorMap ta = make_map(dY, N_out, rows, ldy, BK, true);
+        const CUtensorMap tb = make_map(X, K_in, rows, ldx, BK, true);
+        Args a{};
+        a.C = dW; a.ldc = ldw; a.M = N_out; a.N = K_in; a.K = rows; a.K_dev = rows_dev;
+        a.k_split = split; a.mode = split > 1 ? PARTIAL : ACCUM; a.epi = EPI_NONE;
+        a.ws = ws; a.ldws = ldws;
+        if (mt <= 2) run<true, true, 224, 2, 2>(ta, tb, a, dim3(1, 2, split), s);
+        else run<true, true, 224, 2, 4>(ta, tb, a, dim3(1, 4, split), s);
+        if (split > 1) {
+            const std::size_t n = std::size_t(N_out) * K_in;
+            gemm::splitk_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(ws, split, N_out, K_in,
+                                                                          ldws, dW, ldw, 1.f);
+            g_launch_counter.fetch_add(1, std::memory_order_relaxed);
+            SPD_CUDA(cudaGetLastError());
+        }
+        return;
+    }
     const int bn = K_in <= 64 ? 64 : (K_in <= 128 ? 128 : 224);
     const int tiles = ((N_out + BM - 1) / BM) * ((K_in + bn - 1) / bn);
     const int ldws = (K_in + 3) / 4 * 4;

@@ -28,7 +28,7 @@ def padded(rows, cols, gen):
     return t
 
 
-SHAPES = [(60000, 400, 387), (6000, 200, 201), (4000, 300, 487), (130, 17, 5), (128, 64, 32),
+SHAPES = [(60000, 400, 387), (60000, 200, 400), (30001, 416, 388), (6000, 200, 201), (4000, 300, 487), (130, 17, 5), (128, 64, 32),
           (257, 130, 70), (6000, 100, 301)]
 
 
@@ -59,7 +59,7 @@ def test_dgrad(impl, tol, M, N, K):
 
 
 @pytest.mark.parametrize("impl,tol", [(0, 1e-5), (1, 3e-3)])
-@pytest.mark.parametrize("M,N,K", [(400, 387, 60000), (300, 487, 4000), (200, 201, 6000),
+@pytest.mark.parametrize("M,N,K", [(400, 387, 60000), (256, 300, 20000), (400, 448, 33000), (300, 487, 4000), (200, 201, 6000),
                                    (17, 5, 130), (1, 101, 4000), (100, 301, 6000)])
 def test_wgrad_accumulates(impl, tol, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M + N + K)

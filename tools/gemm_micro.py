@@ -27,5 +27,5 @@ def run(impl, which, M, N, K, lda_pad=0, iters=10):
 
 for args in [(1,0,60000,400,387,0),(1,0,60000,400,387,28),(1,0,60000,400,32,0),(1,0,60000,400,128,0),(1,0,60000,448,384,0),
              (1,0,6000,200,201,0),(1,0,6000,200,32,0),(1,0,128,224,32,0),(1,0,128,224,384,0),
-             (0,0,60000,400,387,0),(1,1,60000,386,400,0),(1,2,400,387,60000,0)]:
+             (0,0,60000,400,387,0),(1,1,60000,200,400,0),(1,1,60000,386,400,0),(1,2,400,387,60000,0)]:
     print(args, f"{run(*args):.1f} us")
