@@ -146,7 +146,13 @@ struct Cfg {
     static constexpr int STAGES_ = BUDGET / STAGE_BYTES >= STAGES ? STAGES : BUDGET / STAGE_BYTES;
     static constexpr int SMEM = STAGES_ * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int TMEM_COLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : NT <= 256 ? 256 : 512;
-    static constexpr int B_BOXES = B_MN ? NT / 32 : NSUB;  // TMA boxes per stage for B
+    // TMA boxes per stage for B: 32-column blocks (MN-major) or row slabs of
+    // KROWS rows (K-major; at least one per cluster CTA so the multicast load
+    // is spread evenly)
+    static constexpr int KBOXES = NSUB >= CL ? NSUB : CL;
+    static constexpr int KROWS = NT / KBOXES;
+    static constexpr int B_BOXES = B_MN ? NT / 32 : KBOXES;
+    static_assert(B_MN || (NT % KBOXES == 0 && KROWS % 8 == 0), "K-major B slabs of 8-row atoms");
     static_assert(STAGES_ >= 2, "tile too large for the smem budget");
     static_assert(!B_MN || BN % 32 == 0, "MN-major B needs whole 32-column boxes");
     static_assert(NT <= 512, "accumulator exceeds TMEM");
@@ -222,9 +228,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < C_::B_BOXES; ++j) {
                     if (CL > 1 && (j % CL) != (int)crank) continue;
-                    unsigned char* dst = B_MN ? b_s + j * 32 * 128 : b_s + j * BN * 128;
+                    unsigned char* dst = B_MN ? b_s + j * 32 * 128 : b_s + j * C_::KROWS * 128;
                     const int c0 = B_MN ? n0 + 32 * j : kc;
-                    const int c1 = B_MN ? kc : n0 + j * BN;
+                    const int c1 = B_MN ? kc : n0 + j * C_::KROWS;
                     if (CL > 1) tma_load_2d_mc(dst, &tmB, full + s, c0, c1, (1u << CL) - 1);
                     else tma_load_2d(dst, &tmB, full + s, c0, c1);
                 }

@@ -126,8 +126,8 @@ void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, in
         // one CTA covers all N (2 x 208 in TMEM): A streamed once; W multicast
         // to CTA pairs: W streamed from L2 once per 256 rows
         const CUtensorMap ta = make_map(A, K, M, lda, BM);
-        const CUtensorMap tb = make_map(W, K, N, ldw, 208);
-        run<false, false, 208, 2, 2>(ta, tb, a, dim3(1, (mt + 1) / 2 * 2, 1), s);
+        const CUtensorMap tb = make_map(W, K, N, ldw, 104);
+        run<false, false, 208, 2, 4>(ta, tb, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
         return;
     }
     const int bn = pick_bn(N);
@@ -146,7 +146,7 @@ void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, 
     a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask; a.rnd = rnd;
     const int mt = (M + BM - 1) / BM;
     if (mt >= 64 && N <= 224 && !M_dev) {  // big: W multicast to CTA pairs
-        run<false, true, 224, 1, 2>(ta, tb, a, dim3(1, (mt + 1) / 2 * 2, 1), s);
+        run<false, true, 224, 1, 4>(ta, tb, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
         return;
     }
     const int bn = pick_bn(N);  // multiple of 32: whole MN-major column blocks
