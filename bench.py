@@ -318,8 +318,7 @@ def main():
     dom = max(phases, key=lambda x: x[1]) if phases else ("none", 0.0)
     RK = 3 * B * K
     DQ, DK = D + T, D + F + T
-    flops = {"gemm_kv": 2.0 * RK * (DK + 1) * 2 * DQ, "gemm_kv_wgrad": 2.0 * RK * (DK + 1) * 2 * DQ,
-             "gemm_kv_dgrad": 2.0 * RK * 2 * DQ * DK}
+    flops = {}
     bpe = bytes_per_edge(D, T, F, K)
     if dom[0] in flops:
         ach = flops[dom[0]] / (dom[1] / 1e3) / 1e12

@@ -21,9 +21,6 @@ __device__ __forceinline__ const float* memx_row(const WorkerDev& w, const float
 }
 
 __device__ __forceinline__ float softplusf(float x) { return x > 20.f ? x : log1pf(expf(x)); }
-__device__ __forceinline__ float4 r4(float4 v, int rnd) {
-    return rnd ? make_float4(tf32r(v.x), tf32r(v.y), tf32r(v.z), tf32r(v.w)) : v;
-}
 }  // namespace
 
 __global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
@@ -125,318 +122,19 @@ __global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh,
     }
 }
 
-// K1 + K2 for attention: q_in = [s_root | phi(0)], kv_in = [s_nbr | e | phi(dt)]
-// (one warp per row; padded neighbour rows are zero).
-__global__ void k_embed_gather(WorkerDev w, Dims d, int R, const float* time_w,
+// K1 + K2 for the attention query: q_in = [s_root | phi(0)] (one warp per
+// root). The key/value rows are gathered inside the attention kernels
+// (tgn_attn.cu) and never stored.
+__global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* roots,
-                               const std::uint32_t* nbr_node, const std::uint32_t* nbr_ev,
-                               const double* nbr_dt, const int* cnt, const float* mem_new,
-                               float* q_in, float* kv_in) {
+                               const float* mem_new, float* q_in) {
     const int row = warp_id_global(), lane = lane_id();
-    if (row >= R * (1 + d.K)) return;
-    if (row < R) {
-        const float* m = memx_row(w, mem_new, d.D, roots[row]);
-        float* q = q_in + (std::size_t)row * d.ld_q;
-        for (int c = lane; c < d.D; c += 32) q[c] = rnd_if(m[c], d.rnd);
-        for (int c = lane; c < d.T; c += 32) q[d.D + c] = rnd_if(time_cos(time_w[c], time_b[c], 0.0), d.rnd);
-        return;
-    }
-    const int kr = row - R;  // r * K + j
-    const int r = kr / d.K, j = kr % d.K;
-    float* o = kv_in + (std::size_t)kr * d.ld_kv;
-    if (j >= cnt[r]) {
-        for (int c = lane; c < d.DK; c += 32) o[c] = 0.f;
-        return;
-    }
-    const float* m = memx_row(w, mem_new, d.D, nbr_node[kr]);
-    for (int c = lane; c < d.D; c += 32) o[c] = rnd_if(m[c], d.rnd);
-    // column order [s_nbr | phi(dt) | e]: the gradient-carrying columns are a
-    // contiguous prefix, so the data-gradient GEMM computes only D + T columns
-    const double dt = nbr_dt[kr];
-    for (int c = lane; c < d.T; c += 32) o[d.D + c] = rnd_if(time_cos(time_w[c], time_b[c], dt), d.rnd);
-    const __nv_bfloat16* fr = w.feat + (std::size_t)nbr_ev[kr] * d.Fp;
-    for (int c = lane; c < d.F; c += 32) o[d.D + d.T + c] = __bfloat162float(fr[c]);
+    if (row >= R) return;
+    const float* m = memx_row(w, mem_new, d.D, roots[row]);
+    float* q = q_in + (std::size_t)row * d.ld_q;
+    for (int c = lane; c < d.D; c += 32) q[c] = rnd_if(m[c], d.rnd);
+    for (int c = lane; c < d.T; c += 32) q[d.D + c] = rnd_if(time_cos(time_w[c], time_b[c], 0.0), d.rnd);
 }
-
-// Multi-head attention core over <= K neighbours (one warp per root).
-// KV rows: [K (DQ) | V (DQ)], row stride 2DQ. alpha: [R][H][K].
-__global__ void k_attn_fwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
-                           float* alpha, float* ctx) {
-    extern __shared__ float sm[];
-    const int warp_in_block = threadIdx.x >> 5, lane = lane_id();
-    const int r = warp_id_global();
-    if (r >= R) return;
-    float* s = sm + warp_in_block * d.H * d.K;
-    const int c_n = cnt[r];
-    float* cr = ctx + (std::size_t)r * d.ld_ctx;
-    if (c_n == 0) {
-        for (int c = lane; c < d.DQ; c += 32) cr[c] = 0.f;
-        return;
-    }
-    const int dh = d.DQ / d.H;
-    const float* q = Q + (std::size_t)r * d.ld_Q;
-    for (int h = 0; h < d.H; ++h) {
-        for (int j = 0; j < c_n; ++j) {
-            const float* k = KV + ((std::size_t)r * d.K + j) * d.ld_KV + h * dh;
-            float p = 0.f;
-            for (int c = lane; c < dh; c += 32) p += q[h * dh + c] * k[c];
-            p = warp_sum(p);
-            if (lane == 0) s[h * d.K + j] = p / sqrtf((float)dh);
-        }
-    }
-    __syncwarp();
-    // softmax per head over valid j (lane = j, K <= 32)
-    for (int h = 0; h < d.H; ++h) {
-        float v = lane < c_n ? s[h * d.K + lane] : -INFINITY;
-        float mx = v;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const float e = lane < c_n ? expf(v - mx) : 0.f;
-        const float sum = warp_sum(e);
-        const float a = e / sum;
-        __syncwarp();
-        if (lane < d.K) {
-            const float av = lane < c_n ? a : 0.f;
-            s[h * d.K + lane] = av;
-            alpha[((std::size_t)r * d.H + h) * d.K + lane] = av;
-        }
-    }
-    __syncwarp();
-    for (int c = lane; c < d.DQ; c += 32) {
-        const int h = c / dh;
-        float acc = 0.f;
-        for (int j = 0; j < c_n; ++j)
-            acc += s[h * d.K + j] * KV[((std::size_t)r * d.K + j) * d.ld_KV + d.DQ + c];
-        cr[c] = rnd_if(acc, d.rnd);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Register-tiled attention core (DQ <= 256, K <= KMAX, head dim % 4 == 0,
-// H <= 4): one warp per root, lane l owns float4 chunks l and l+32 of every
-// row. All K (then V) rows of the root are loaded up front — 2*K independent
-// 128-bit loads in flight per lane — and each (key, head) dot product is an
-// xor-shuffle all-reduce, so every lane holds all scores and computes the
-// softmax redundantly without further communication.
-template <int KMAX, int HMAX>
-__global__ void __launch_bounds__(256) k_attn_fwd_reg(Dims d, int R, const int* cnt,
-                                                      const float* Q, const float* KV,
-                                                      float* alpha, float* ctx) {
-    const int r = warp_id_global(), lane = lane_id();
-    if (r >= R) return;
-    const int c_n = cnt[r];
-    const int nc = d.DQ / 4;  // chunks per row
-    const int dh4 = d.DQ / d.H / 4;
-    float4* cr = reinterpret_cast<float4*>(ctx + (std::size_t)r * d.ld_ctx);
-    const bool has0 = lane < nc, has1 = lane + 32 < nc;
-    const int h0 = lane / dh4, h1 = (lane + 32) / dh4;
-    if (c_n == 0) {
-        if (has0) cr[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (has1) cr[lane + 32] = make_float4(0.f, 0.f, 0.f, 0.f);
-        return;
-    }
-    const float4* q4 = reinterpret_cast<const float4*>(Q + (std::size_t)r * d.ld_Q);
-    const float4 qa = has0 ? q4[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 qb = has1 ? q4[lane + 32] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4* base = reinterpret_cast<const float4*>(KV + (std::size_t)r * d.K * d.ld_KV);
-    const int ld4 = d.ld_KV / 4;
-    float4 ka[KMAX], kb[KMAX];
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        if (j < c_n) {
-            ka[j] = has0 ? base[j * ld4 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-            kb[j] = has1 ? base[j * ld4 + lane + 32] : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    }
-    float s[HMAX][KMAX];
-    const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        if (j >= c_n) break;
-        float p[HMAX];
-        const float da = qa.x * ka[j].x + qa.y * ka[j].y + qa.z * ka[j].z + qa.w * ka[j].w;
-        const float db = qb.x * kb[j].x + qb.y * kb[j].y + qb.z * kb[j].z + qb.w * kb[j].w;
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) p[h] = (h0 == h ? da : 0.f) + (h1 == h ? db : 0.f);
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) {
-            if (h >= d.H) break;
-            s[h][j] = warp_sum(p[h]) * inv;
-        }
-    }
-    // softmax per head (redundantly in every lane)
-#pragma unroll
-    for (int h = 0; h < HMAX; ++h) {
-        if (h >= d.H) break;
-        float mx = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j)
-            if (j < c_n) mx = fmaxf(mx, s[h][j]);
-        float sum = 0.f;
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j)
-            if (j < c_n) {
-                s[h][j] = expf(s[h][j] - mx);
-                sum += s[h][j];
-            }
-        const float is = 1.f / sum;
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j)
-            if (j < c_n) s[h][j] *= is;
-    }
-    if (lane < d.K) {
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) {
-            if (h >= d.H) break;
-            float v = 0.f;
-#pragma unroll
-            for (int j = 0; j < KMAX; ++j)
-                if (j == lane && j < c_n) v = s[h][j];
-            alpha[((std::size_t)r * d.H + h) * d.K + lane] = v;
-        }
-    }
-    // context = sum_j alpha_hj V_j  (V chunks follow the K chunks in the row)
-    const int voff = nc;  // V starts at column DQ = chunk nc
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        if (j < c_n) {
-            ka[j] = has0 ? base[j * ld4 + voff + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-            kb[j] = has1 ? base[j * ld4 + voff + lane + 32] : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    }
-    float4 oa = make_float4(0.f, 0.f, 0.f, 0.f), ob = oa;
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        if (j >= c_n) break;
-        float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) {
-            if (h0 == h) a0 = s[h][j];
-            if (h1 == h) a1 = s[h][j];
-        }
-        oa.x += a0 * ka[j].x; oa.y += a0 * ka[j].y; oa.z += a0 * ka[j].z; oa.w += a0 * ka[j].w;
-        ob.x += a1 * kb[j].x; ob.y += a1 * kb[j].y; ob.z += a1 * kb[j].z; ob.w += a1 * kb[j].w;
-    }
-    if (d.rnd) {
-        oa = make_float4(tf32r(oa.x), tf32r(oa.y), tf32r(oa.z), tf32r(oa.w));
-        ob = make_float4(tf32r(ob.x), tf32r(ob.y), tf32r(ob.z), tf32r(ob.w));
-    }
-    if (has0) cr[lane] = oa;
-    if (has1) cr[lane + 32] = ob;
-}
-
-template <int KMAX, int HMAX>
-__global__ void __launch_bounds__(256) k_attn_bwd_reg(Dims d, int R, const int* cnt,
-                                                      const float* Q, const float* KV,
-                                                      const float* alpha, const float* dctx,
-                                                      int ld_dctx, float* dQ, float* dKV) {
-    const int r = warp_id_global(), lane = lane_id();
-    if (r >= R) return;
-    const int c_n = cnt[r];
-    const int nc = d.DQ / 4;
-    const int dh4 = d.DQ / d.H / 4;
-    const bool has0 = lane < nc, has1 = lane + 32 < nc;
-    const int h0 = lane / dh4, h1 = (lane + 32) / dh4;
-    const int ld4 = d.ld_KV / 4;
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4* base = reinterpret_cast<const float4*>(KV + (std::size_t)r * d.K * d.ld_KV);
-    float4* obase = reinterpret_cast<float4*>(dKV + (std::size_t)r * d.K * d.ld_KV);
-    float4* dq4 = reinterpret_cast<float4*>(dQ + (std::size_t)r * d.ld_Q);
-    // padded key rows get zero gradients
-    for (int j = c_n; j < d.K; ++j) {
-        if (has0) { obase[j * ld4 + lane] = z4; obase[j * ld4 + nc + lane] = z4; }
-        if (has1) { obase[j * ld4 + lane + 32] = z4; obase[j * ld4 + nc + lane + 32] = z4; }
-    }
-    if (c_n == 0) {
-        if (has0) dq4[lane] = z4;
-        if (has1) dq4[lane + 32] = z4;
-        return;
-    }
-    const float4* dc4 = reinterpret_cast<const float4*>(dctx + (std::size_t)r * ld_dctx);
-    const float4 ga = has0 ? dc4[lane] : z4, gb = has1 ? dc4[lane + 32] : z4;
-    float4 va[KMAX], vb[KMAX];
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j)
-        if (j < c_n) {
-            va[j] = has0 ? base[j * ld4 + nc + lane] : z4;
-            vb[j] = has1 ? base[j * ld4 + nc + lane + 32] : z4;
-        }
-    float a[HMAX][KMAX], ds[HMAX][KMAX];
-    const float* al = alpha + (std::size_t)r * d.H * d.K;
-#pragma unroll
-    for (int h = 0; h < HMAX; ++h) {
-        if (h >= d.H) break;
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j)
-            if (j < c_n) a[h][j] = al[h * d.K + j];
-    }
-    // d alpha_hj = <dctx_h, V_jh>; dV_j = alpha_hj dctx
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        if (j >= c_n) break;
-        const float pa = ga.x * va[j].x + ga.y * va[j].y + ga.z * va[j].z + ga.w * va[j].w;
-        const float pb = gb.x * vb[j].x + gb.y * vb[j].y + gb.z * vb[j].z + gb.w * vb[j].w;
-        float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) {
-            if (h >= d.H) break;
-            ds[h][j] = warp_sum((h0 == h ? pa : 0.f) + (h1 == h ? pb : 0.f));
-            if (h0 == h) a0 = a[h][j];
-            if (h1 == h) a1 = a[h][j];
-        }
-        if (has0) obase[j * ld4 + nc + lane] = r4(make_float4(a0 * ga.x, a0 * ga.y, a0 * ga.z, a0 * ga.w), d.rnd);
-        if (has1)
-            obase[j * ld4 + nc + lane + 32] = r4(make_float4(a1 * gb.x, a1 * gb.y, a1 * gb.z, a1 * gb.w), d.rnd);
-    }
-    // d score_hj = alpha_hj (dalpha_hj - sum_k alpha_hk dalpha_hk)
-#pragma unroll
-    for (int h = 0; h < HMAX; ++h) {
-        if (h >= d.H) break;
-        float dot = 0.f;
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j)
-            if (j < c_n) dot += a[h][j] * ds[h][j];
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j)
-            if (j < c_n) ds[h][j] = a[h][j] * (ds[h][j] - dot);
-    }
-    const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
-    const float4* q4 = reinterpret_cast<const float4*>(Q + (std::size_t)r * d.ld_Q);
-    const float4 qa = has0 ? q4[lane] : z4, qb = has1 ? q4[lane + 32] : z4;
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j)
-        if (j < c_n) {
-            va[j] = has0 ? base[j * ld4 + lane] : z4;  // reuse registers for K rows
-            vb[j] = has1 ? base[j * ld4 + lane + 32] : z4;
-        }
-    float4 oa = z4, ob = z4;
-#pragma unroll
-    for (int j = 0; j < KMAX; ++j) {
-        if (j >= c_n) break;
-        float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) {
-            if (h0 == h) s0 = ds[h][j] * inv;
-            if (h1 == h) s1 = ds[h][j] * inv;
-        }
-        oa.x += s0 * va[j].x; oa.y += s0 * va[j].y; oa.z += s0 * va[j].z; oa.w += s0 * va[j].w;
-        ob.x += s1 * vb[j].x; ob.y += s1 * vb[j].y; ob.z += s1 * vb[j].z; ob.w += s1 * vb[j].w;
-        if (has0) obase[j * ld4 + lane] = r4(make_float4(s0 * qa.x, s0 * qa.y, s0 * qa.z, s0 * qa.w), d.rnd);
-        if (has1) obase[j * ld4 + lane + 32] = r4(make_float4(s1 * qb.x, s1 * qb.y, s1 * qb.z, s1 * qb.w), d.rnd);
-    }
-    if (has0) dq4[lane] = r4(oa, d.rnd);
-    if (has1) dq4[lane + 32] = r4(ob, d.rnd);
-}
-
-#define SPD_ATTN_INST(KM, HM)                                                                  \
-    template __global__ void k_attn_fwd_reg<KM, HM>(Dims, int, const int*, const float*,         \
-                                                    const float*, float*, float*);              \
-    template __global__ void k_attn_bwd_reg<KM, HM>(Dims, int, const int*, const float*,         \
-                                                    const float*, const float*, const float*, int, \
-                                                    float*, float*);
-SPD_ATTN_INST(10, 2)
-SPD_ATTN_INST(16, 4)
-#undef SPD_ATTN_INST
 
 // MergeLayer input [attn | s_root]; attn = 0 for a root without neighbours.
 __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
@@ -518,209 +216,45 @@ __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt)
     for (int c = lane; c < cols; c += 32) buf[(std::size_t)r * ld + c] = 0.f;
 }
 
-// Attention core backward (one warp per root).
-__global__ void k_attn_bwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
-                           const float* alpha, const float* dctx, int ld_dctx, float* dQ,
-                           float* dKV) {
-    extern __shared__ float sm[];
-    const int warp_in_block = threadIdx.x >> 5, lane = lane_id();
-    const int r = warp_id_global();
-    if (r >= R) return;
-    float* ds = sm + warp_in_block * d.H * d.K;
-    const int c_n = cnt[r];
-    const int dh = d.DQ / d.H;
-    const float inv = 1.f / sqrtf((float)dh);
-    const float* dc = dctx + (std::size_t)r * ld_dctx;
-    const float* a = alpha + (std::size_t)r * d.H * d.K;
-    if (c_n > 0) {
-        for (int h = 0; h < d.H; ++h) {
-            for (int j = 0; j < c_n; ++j) {
-                const float* v = KV + ((std::size_t)r * d.K + j) * d.ld_KV + d.DQ + h * dh;
-                float p = 0.f;
-                for (int c = lane; c < dh; c += 32) p += dc[h * dh + c] * v[c];
-                p = warp_sum(p);
-                if (lane == 0) ds[h * d.K + j] = p;  // d alpha_j
-            }
-            __syncwarp();
-            float da = lane < c_n ? ds[h * d.K + lane] : 0.f;
-            const float aj = lane < c_n ? a[h * d.K + lane] : 0.f;
-            const float dot = warp_sum(aj * da);
-            __syncwarp();
-            if (lane < c_n) ds[h * d.K + lane] = aj * (da - dot);  // d score_j
-            __syncwarp();
-        }
-    }
-    float* dq = dQ + (std::size_t)r * d.ld_Q;
-    for (int c = lane; c < d.DQ; c += 32) {
-        const int h = c / dh;
-        float acc = 0.f;
-        for (int j = 0; j < c_n; ++j)
-            acc += ds[h * d.K + j] * KV[((std::size_t)r * d.K + j) * d.ld_KV + c];
-        dq[c] = rnd_if(acc * inv, d.rnd);
-    }
-    const float* q = Q + (std::size_t)r * d.ld_Q;
-    for (int j = 0; j < d.K; ++j) {
-        float* o = dKV + ((std::size_t)r * d.K + j) * d.ld_KV;
-        if (j >= c_n) {
-            for (int c = lane; c < 2 * d.DQ; c += 32) o[c] = 0.f;
-            continue;
-        }
-        for (int c = lane; c < d.DQ; c += 32) {
-            const int h = c / dh;
-            o[c] = rnd_if(ds[h * d.K + j] * q[c] * inv, d.rnd);
-            o[d.DQ + c] = rnd_if(a[h * d.K + j] * dc[c], d.rnd);
-        }
-    }
-}
-
-// Memory-row gradients into the GRU output rows of pending nodes: roots
-// (query + merge inputs) and neighbours (key/value inputs).
-__global__ void k_mem_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
-                           const std::uint32_t* nbr_node, const int* cnt, const float* dq_in,
-                           const float* dm_in, const float* dkv_in, float* dH) {
-    const int row = warp_id_global(), lane = lane_id();
-    if (row >= R * (1 + d.K)) return;
-    if (row < R) {
-        const int s = w.slot[roots[row]];
-        if (s < 0) return;
-        const float* a = dq_in + (std::size_t)row * d.ld_q;
-        const float* b = dm_in + (std::size_t)row * d.ld_m + d.DQ;
-        for (int c = lane; c < d.D; c += 32) atomicAdd(dH + (std::size_t)s * d.D + c, a[c] + b[c]);
-        return;
-    }
-    const int kr = row - R;
-    const int r = kr / d.K, j = kr % d.K;
-    if (j >= cnt[r]) return;
-    const int s = w.slot[nbr_node[kr]];
-    if (s < 0) return;
-    const float* a = dkv_in + (std::size_t)kr * d.ld_kv;
-    for (int c = lane; c < d.D; c += 32) atomicAdd(dH + (std::size_t)s * d.D + c, a[c]);
-}
-
-// Time-encoder gradients: per block, f64 column partials over a chunk of rows
-// (kv rows: d/dw = -sin(ph) dt g, d/db = -sin(ph) g; query rows: phi(0)=cos(b)).
-// part: [nblocks][2T] (w then b).
-// blockDim = (32 columns, 8 row lanes); block covers 32 columns x rows_per_block
-// rows; f64 accumulation, fixed-order in-block reduction -> part[block][2T].
-__global__ void k_time_grad_partial(Dims d, int R, const int* cnt, const double* nbr_dt,
-                                    const float* dkv_in, const float* dq_in, const float* time_w,
-                                    const float* time_b, int rows_per_block, double* part) {
-    __shared__ double red[2][8][33];
-    const int total = R * (1 + d.K);
-    const int c = blockIdx.y * 32 + threadIdx.x;
-    const int r0 = blockIdx.x * rows_per_block;
-    const int r1 = min(total, r0 + rows_per_block);
-    double gw = 0.0, gb = 0.0;
-    if (c < d.T) {
-        const float wc = time_w[c], bc = time_b[c];
-        const double sin_b = sin((double)bc);
-        for (int row = r0 + threadIdx.y; row < r1; row += blockDim.y) {
-            if (row < R) {
-                gb -= sin_b * (double)dq_in[(std::size_t)row * d.ld_q + d.D + c];
-            } else {
-                const int kr = row - R;
-                const int r = kr / d.K, j = kr % d.K;
-                if (j >= cnt[r]) continue;
-                const double dt = nbr_dt[kr];
-                const double g = dkv_in[(std::size_t)kr * d.ld_kv + d.D + c];
-                const double sn = (double)time_sin(wc, bc, dt);
-                gw -= sn * dt * g;
-                gb -= sn * g;
-            }
-        }
-    }
-    red[0][threadIdx.y][threadIdx.x] = gw;
-    red[1][threadIdx.y][threadIdx.x] = gb;
-    __syncthreads();
-    if (threadIdx.y == 0 && c < d.T) {
-        double sw = 0.0, sb = 0.0;
-        for (int y = 0; y < (int)blockDim.y; ++y) {
-            sw += red[0][y][threadIdx.x];
-            sb += red[1][y][threadIdx.x];
-        }
-        part[(std::size_t)blockIdx.x * 2 * d.T + c] = sw;
-        part[(std::size_t)blockIdx.x * 2 * d.T + d.T + c] = sb;
-    }
-}
-
-// Fused single pass over the gradient-carrying input columns of every query
-// and key/value row: memory-row gradients (atomics into the GRU outputs of
-// pending nodes) and time-encoder gradients (f64, per-block fixed-order
-// partials). block (32, 8); rows_per_block rows; part[block][2T].
-__global__ void k_memtime_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
-                               const std::uint32_t* nbr_node, const int* cnt, const double* nbr_dt,
-                               const float* dq_in, const float* dm_in, const float* dkv_in,
-                               const float* time_w, const float* time_b, int rows_per_block,
-                               float* dH, double* part) {
-    constexpr int TC = 4;  // time columns per thread: T <= 128
-    __shared__ double red[2][8][32 * TC];
+// Root-side input gradients (query [s_root | phi(0)] and merge-layer s_root
+// columns): memory rows into the GRU outputs of pending nodes (float4
+// atomics) and d/db of phi(0) = cos(b) (f64 per-block fixed-order partials;
+// d/dw is 0 at dt = 0). block (32, 8); rows_per_block roots; part[block][2T].
+__global__ void k_root_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                            const float* dq_in, const float* dm_in, const float* time_b,
+                            int rows_per_block, float* dH, double* part) {
+    __shared__ double red[8][32];
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const int total = R * (1 + d.K);
     const int r0 = blockIdx.x * rows_per_block;
-    const int r1 = min(total, r0 + rows_per_block);
-    double gw[TC], gb[TC], sinb[TC];
-    float wc[TC], bc[TC];
-#pragma unroll
-    for (int i = 0; i < TC; ++i) {
-        gw[i] = gb[i] = 0.0;
-        const int c = tx + 32 * i;
-        wc[i] = c < d.T ? time_w[c] : 0.f;
-        bc[i] = c < d.T ? time_b[c] : 0.f;
-        sinb[i] = sin((double)bc[i]);
-    }
+    const int r1 = min(R, r0 + rows_per_block);
     for (int row = r0 + ty; row < r1; row += blockDim.y) {
-        if (row < R) {
-            const float* q = dq_in + (std::size_t)row * d.ld_q;
-            const int s = w.slot[roots[row]];
-            if (s >= 0) {
-                const float* m = dm_in + (std::size_t)row * d.ld_m + d.DQ;
-                for (int c = tx; c < d.D; c += 32) atomicAdd(dH + (std::size_t)s * d.D + c, q[c] + m[c]);
-            }
-#pragma unroll
-            for (int i = 0; i < TC; ++i) {
-                const int c = tx + 32 * i;
-                if (c < d.T) gb[i] -= sinb[i] * (double)q[d.D + c];
-            }
-        } else {
-            const int kr = row - R;
-            const int r = kr / d.K, j = kr % d.K;
-            if (j >= cnt[r]) continue;
-            const float* g = dkv_in + (std::size_t)kr * d.ld_kv;
-            const int s = w.slot[nbr_node[kr]];
-            if (s >= 0)
-                for (int c = tx; c < d.D; c += 32) atomicAdd(dH + (std::size_t)s * d.D + c, g[c]);
-            const double dt = nbr_dt[kr];
-#pragma unroll
-            for (int i = 0; i < TC; ++i) {
-                const int c = tx + 32 * i;
-                if (c < d.T) {
-                    const double sn = (double)time_sin(wc[i], bc[i], dt);
-                    const double gv = g[d.D + c];
-                    gw[i] -= sn * dt * gv;
-                    gb[i] -= sn * gv;
-                }
-            }
+        const int s = w.slot[roots[row]];
+        if (s < 0) continue;
+        const float4* q = reinterpret_cast<const float4*>(dq_in + (std::size_t)row * d.ld_q);
+        const float4* m = reinterpret_cast<const float4*>(dm_in + (std::size_t)row * d.ld_m + d.DQ);
+        float4* o = reinterpret_cast<float4*>(dH + (std::size_t)s * d.D);
+        for (int c = tx; c < d.D / 4; c += 32) {
+            const float4 a = q[c], b = m[c];
+            atomicAdd(o + c, make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
         }
     }
-#pragma unroll
-    for (int i = 0; i < TC; ++i) {
-        red[0][ty][tx + 32 * i] = gw[i];
-        red[1][ty][tx + 32 * i] = gb[i];
-    }
-    __syncthreads();
-    if (ty == 0) {
-#pragma unroll
-        for (int i = 0; i < TC; ++i) {
-            const int c = tx + 32 * i;
-            if (c >= d.T) continue;
-            double sw = 0.0, sb = 0.0;
-            for (int y = 0; y < (int)blockDim.y; ++y) {
-                sw += red[0][y][c];
-                sb += red[1][y][c];
-            }
-            part[(std::size_t)blockIdx.x * 2 * d.T + c] = sw;
+    for (int c0 = 0; c0 < d.T; c0 += 32) {
+        const int c = c0 + tx;
+        double gb = 0.0;
+        if (c < d.T) {
+            const double sinb = sin((double)time_b[c]);
+            for (int row = r0 + ty; row < r1; row += blockDim.y)
+                gb -= sinb * (double)dq_in[(std::size_t)row * d.ld_q + d.D + c];
+        }
+        red[ty][tx] = gb;
+        __syncthreads();
+        if (ty == 0 && c < d.T) {
+            double sb = 0.0;
+            for (int y = 0; y < (int)blockDim.y; ++y) sb += red[y][tx];
+            part[(std::size_t)blockIdx.x * 2 * d.T + c] = 0.0;
             part[(std::size_t)blockIdx.x * 2 * d.T + d.T + c] = sb;
         }
+        __syncthreads();
     }
 }
 

@@ -19,7 +19,8 @@ struct Dims {
     int D, T, F, Fp, DQ, DK, DM, H, K;
     int ld_x, ld_h, ld_q, ld_kv, ld_ctx, ld_m, ld_z, ld_din, ld_d1;  // aug strides
     int ld_g;  // 3D rounded
-    int ld_Q, ld_KV;  // row strides of Q/dQ/dctx (DQ) and KV/dKV (2 DQ), 128-B multiples
+    int ld_Q;   // row stride of Q/dQ/dctx (DQ), a 128-B multiple
+    int ld_p;   // per-head row width of Qp/xbar/dxbar/dQp: ld_aug(DK) (tgn_attn.cu)
     int rnd;          // round tensor-core operands to tf32 (round-to-nearest) at production
 };
 
@@ -54,24 +55,25 @@ __global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const flo
                              float* x, float* h, int set_slot);
 __global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh, const float* h,
                           float* save, float* mem_new);
-__global__ void k_embed_gather(WorkerDev w, Dims d, int R, const float* time_w,
+__global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* roots,
-                               const std::uint32_t* nbr_node, const std::uint32_t* nbr_ev,
-                               const double* nbr_dt, const int* cnt, const float* mem_new,
-                               float* q_in, float* kv_in);
-__global__ void k_attn_fwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
-                           float* alpha, float* ctx);
-template <int KMAX, int HMAX>
-__global__ void k_attn_fwd_reg(Dims d, int R, const int* cnt, const float* Q, const float* KV,
-                               float* alpha, float* ctx);
-template <int KMAX, int HMAX>
-__global__ void k_attn_bwd_reg(Dims d, int R, const int* cnt, const float* Q, const float* KV,
-                               const float* alpha, const float* dctx, int ld_dctx, float* dQ,
-                               float* dKV);
-// the register-tiled attention kernels apply when these hold
-inline bool attn_reg_ok(const Dims& d) {
-    return d.DQ <= 256 && d.K <= 16 && d.H <= 4 && d.DQ % d.H == 0 && (d.DQ / d.H) % 4 == 0;
-}
+                               const float* mem_new, float* q_in);
+// absorbed-projection attention (tgn_attn.cu): 4 roots per 128-thread block,
+// dynamic shared memory attn_smem_bytes(d); NCH = ceil(ld_p / 128),
+// NCX = ceil((D + T) / 128), HMAX >= H, K <= 16
+__host__ __device__ std::size_t attn_smem_bytes(const Dims& d);
+int attn_roots_per_block();
+template <int NCH, int HMAX>
+__global__ void k_attn_abs_fwd(WorkerDev w, Dims d, int R, const float* time_w,
+                               const float* time_b, const std::uint32_t* nbr_node,
+                               const std::uint32_t* nbr_ev, const double* nbr_dt, const int* cnt,
+                               const float* mem_new, const float* Qp, float* alpha, float* xbar);
+template <int NCH, int NCX, int HMAX>
+__global__ void k_attn_abs_bwd(WorkerDev w, Dims d, int R, const float* time_w,
+                               const float* time_b, const std::uint32_t* nbr_node,
+                               const std::uint32_t* nbr_ev, const double* nbr_dt, const int* cnt,
+                               const float* mem_new, const float* Qp, const float* alpha,
+                               const float* dxbar, float* dQp, float* dH, double* part);
 __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
                                const int* cnt, const float* O, const float* mem_new, float* m_in);
 __global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in);
@@ -80,20 +82,9 @@ __global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, floa
 __global__ void k_sum_loss(const float* lossv, int n, float* out);
 __global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb);
 __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt);
-__global__ void k_attn_bwd(Dims d, int R, const int* cnt, const float* Q, const float* KV,
-                           const float* alpha, const float* dctx, int ld_dctx, float* dQ,
-                           float* dKV);
-__global__ void k_mem_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
-                           const std::uint32_t* nbr_node, const int* cnt, const float* dq_in,
-                           const float* dm_in, const float* dkv_in, float* dH);
-__global__ void k_time_grad_partial(Dims d, int R, const int* cnt, const double* nbr_dt,
-                                    const float* dkv_in, const float* dq_in, const float* time_w,
-                                    const float* time_b, int rows_per_block, double* part);
-__global__ void k_memtime_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
-                               const std::uint32_t* nbr_node, const int* cnt, const double* nbr_dt,
-                               const float* dq_in, const float* dm_in, const float* dkv_in,
-                               const float* time_w, const float* time_b, int rows_per_block,
-                               float* dH, double* part);
+__global__ void k_root_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                            const float* dq_in, const float* dm_in, const float* time_b,
+                            int rows_per_block, float* dH, double* part);
 __global__ void k_time_grad_final(int T, int nblocks, const double* part, double* acc);
 __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb);
 __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* save, const float* h,

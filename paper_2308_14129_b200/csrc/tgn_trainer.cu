@@ -13,6 +13,7 @@
 #include <cstring>
 #include <functional>
 #include <numeric>
+#include <type_traits>
 
 #include "gemm_simt.cuh"
 #include "nccl_dyn.hpp"
@@ -84,12 +85,12 @@ struct Scratch {
     DevBuf<double> root_t, nbr_dt;
     DevBuf<int> cnt;
     DevBuf<float> x_gru, h_gru, Gi, Gh, gsave, mem_new, dH, dGi, dGh;
-    DevBuf<float> q_in, kv_in, Q, KV, alpha, ctx, O, m_in, Z1, emb, d_in, D1, logits, lossv, dlogit;
-    DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dQ, dKV, dkv_in, dq_in;
+    DevBuf<float> q_in, Q, Qp, xbar, alpha, ctx, O, m_in, Z1, emb, d_in, D1, logits, lossv, dlogit;
+    DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dxbar, dQp, dQ, dq_in;
     DevBuf<float> ws;
     DevBuf<double> tpart;
     DevBuf<float> loss;  // per local worker
-    int tblocks = 0, trows = 0;
+    int trows = 0, troot_blocks = 0, tattn_blocks = 0;  // time-grad partial blocks
 };
 
 namespace {
@@ -192,6 +193,71 @@ void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, floa
     else gemm_wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s);
 }
 
+// Absorbed-projection attention kernels (tgn_attn.cu), instantiated for
+// chunk counts NCH = ceil(ld_p / 128), NCX = ceil((D + T) / 128) and H <= 2 or 4.
+template <class Kern>
+void attn_launch(Kern k, unsigned grid, std::size_t smem, cudaStream_t st,
+                 const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
+                 const float* tb, const Scratch& s, const float* rows_in, float* out,
+                 double* part) {
+    static std::size_t set = 0;  // per instantiation: opt in to > 48 KB shared memory
+    if (smem > set) {
+        SPD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        set = smem;
+    }
+    if constexpr (std::is_same_v<Kern, decltype(&tgnk::k_attn_abs_fwd<1, 2>)>)
+        launch(k, grid, 128, smem, st, wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p,
+               s.cnt.p, s.mem_new.p, rows_in, s.alpha.p, out);
+    else
+        launch(k, grid, 128, smem, st, wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p,
+               s.cnt.p, s.mem_new.p, s.Qp.p, s.alpha.p, rows_in, out, s.dH.p, part);
+}
+
+void attn_abs_fwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
+                  const float* tb, const Scratch& s, cudaStream_t st) {
+    const int nch = (d.ld_p / 4 + 31) / 32;
+    const int rpb = tgnk::attn_roots_per_block();
+    const unsigned grid = unsigned((R + rpb - 1) / rpb);
+    const std::size_t smem = tgnk::attn_smem_bytes(d);
+#define SPD_F(NCH, HM) attn_launch(&tgnk::k_attn_abs_fwd<NCH, HM>, grid, smem, st, wd, d, R, tw, tb, s, \
+                                   s.Qp.p, s.xbar.p, nullptr)
+#define SPD_FK(NCH) if (d.H <= 2) SPD_F(NCH, 2); else SPD_F(NCH, 4)
+    switch (nch) {
+        case 1: SPD_FK(1); break;
+        case 2: SPD_FK(2); break;
+        case 3: SPD_FK(3); break;
+        case 4: SPD_FK(4); break;
+        default: internal_error("InvalidParams", "attention row too wide");
+    }
+#undef SPD_FK
+#undef SPD_F
+}
+
+void attn_abs_bwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
+                  const float* tb, const Scratch& s, double* part, cudaStream_t st) {
+    const int nch = (d.ld_p / 4 + 31) / 32;
+    const int ncx = ((d.D + d.T) / 4 + 31) / 32;
+    // every block of the partial region writes (zeros past R): the final
+    // reduction covers the region sized for the largest batch
+    const unsigned grid = unsigned(s.tattn_blocks);
+    const std::size_t smem = tgnk::attn_smem_bytes(d);
+#define SPD_B(NCH, NCX, HM) attn_launch(&tgnk::k_attn_abs_bwd<NCH, NCX, HM>, grid, smem, st, wd, d, R, \
+                                        tw, tb, s, s.dxbar.p, s.dQp.p, part)
+#define SPD_BK(NCH, NCX) if (d.H <= 2) SPD_B(NCH, NCX, 2); else SPD_B(NCH, NCX, 4)
+    switch (nch * 4 + ncx) {
+        case 1 * 4 + 1: SPD_BK(1, 1); break;
+        case 2 * 4 + 1: SPD_BK(2, 1); break;
+        case 2 * 4 + 2: SPD_BK(2, 2); break;
+        case 3 * 4 + 1: SPD_BK(3, 1); break;
+        case 3 * 4 + 2: SPD_BK(3, 2); break;
+        case 4 * 4 + 1: SPD_BK(4, 1); break;
+        case 4 * 4 + 2: SPD_BK(4, 2); break;
+        default: internal_error("InvalidParams", "attention row too wide");
+    }
+#undef SPD_BK
+#undef SPD_B
+}
+
 tgnk::WorkerDev devview(Worker& w) {
     tgnk::WorkerDev v{};
     v.ev_src = w.ev_src.p; v.ev_dst = w.ev_dst.p; v.ev_ts = w.ev_ts.p; v.feat = w.feat.p;
@@ -238,8 +304,12 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         data_error("InvalidParams", "d_mem and d_time must be positive multiples of 4, d_edge >= 0");
     if (cfg.n_heads < 1 || (cfg.d_mem + cfg.d_time) % cfg.n_heads)
         data_error("InvalidParams", "n_heads must divide d_mem + d_time");
-    if (cfg.n_neighbors < 1 || cfg.n_neighbors > 32)
-        data_error("InvalidParams", "n_neighbors must lie in [1, 32]");
+    if (cfg.n_neighbors < 1 || cfg.n_neighbors > 16)
+        data_error("InvalidParams", "n_neighbors must lie in [1, 16]");
+    if (cfg.n_heads > 4 || ((cfg.d_mem + cfg.d_time) / cfg.n_heads) % 4)
+        data_error("InvalidParams", "n_heads must be <= 4 with a head width that is a multiple of 4");
+    if (cfg.d_mem + cfg.d_time > 256 || ld_aug(cfg.d_mem + cfg.d_time + cfg.d_edge) > 512)
+        data_error("InvalidParams", "need d_mem + d_time <= 256 and d_mem + d_time + d_edge < 512");
     if (cfg.batch_size < 1) data_error("InvalidParams", "need batch_size >= 1");
     if (world < 1 || rank < 0 || rank >= world) data_error("InvalidParams", "bad rank/world");
     require_device(device);
@@ -366,10 +436,10 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     auto& d = s.d;
     d.D = D; d.T = lay_.T; d.F = F; d.Fp = Fp; d.DQ = lay_.DQ; d.DK = lay_.DK; d.DM = lay_.DM;
     d.H = lay_.H; d.K = lay_.Kn;
-    d.ld_x = ld_aug(d.DM); d.ld_h = ld_aug(D); d.ld_q = ld_aug(d.DQ); d.ld_kv = ld_aug(d.DK);
+    d.ld_x = ld_aug(d.DM); d.ld_h = ld_aug(D); d.ld_q = ld_aug(d.DQ);
     d.ld_ctx = ld_aug(d.DQ); d.ld_m = ld_aug(d.DQ + D); d.ld_z = ld_aug(D); d.ld_din = ld_aug(2 * D);
     d.ld_d1 = ld_aug(D); d.ld_g = ld32(3 * D);
-    d.ld_Q = ld32(d.DQ); d.ld_KV = ld32(2 * d.DQ);
+    d.ld_Q = ld32(d.DQ); d.ld_p = ld_aug(d.DK);
     d.rnd = cfg.gemm_mode == 1 ? 1 : 0;
     const int R = s.R, RK = s.RK, U = s.U;
     s.roots.alloc(R); s.root_t.alloc(R); s.cnt.alloc(R);
@@ -381,8 +451,9 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.dH.alloc(std::size_t(U) * D); s.dGi.alloc(std::size_t(U) * d.ld_g); s.dGh.alloc(std::size_t(U) * d.ld_g);
     s.dGi.zero(stream_); s.dGh.zero(stream_); s.Gi.zero(stream_); s.Gh.zero(stream_);
     s.q_in.alloc(std::size_t(R) * d.ld_q); init_aug(s.q_in, R, d.DQ, d.ld_q, stream_);
-    s.kv_in.alloc(std::size_t(RK) * d.ld_kv); init_aug(s.kv_in, RK, d.DK, d.ld_kv, stream_);
-    s.Q.alloc(std::size_t(R) * d.ld_Q); s.KV.alloc(std::size_t(RK) * d.ld_KV);
+    s.Q.alloc(std::size_t(R) * d.ld_Q);
+    const std::size_t hp = std::size_t(R) * d.H * d.ld_p;  // per-root, per-head rows
+    s.Qp.alloc(hp); s.xbar.alloc(hp); s.dxbar.alloc(hp); s.dQp.alloc(hp);
     s.alpha.alloc(std::size_t(R) * d.H * d.K);
     s.ctx.alloc(std::size_t(R) * d.ld_ctx); init_aug(s.ctx, R, d.DQ, d.ld_ctx, stream_);
     s.O.alloc(std::size_t(R) * d.DQ);
@@ -396,12 +467,12 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.dD1.alloc(std::size_t(2 * B) * D); s.dd_in.alloc(std::size_t(2 * B) * d.ld_din);
     s.d_emb.alloc(std::size_t(R) * D); s.dZ1.alloc(std::size_t(R) * D);
     s.dm_in.alloc(std::size_t(R) * d.ld_m); s.dctx.alloc(std::size_t(R) * d.ld_Q);
-    s.dQ.alloc(std::size_t(R) * d.ld_Q); s.dKV.alloc(std::size_t(RK) * d.ld_KV);
-    s.dkv_in.alloc(std::size_t(RK) * d.ld_kv); s.dq_in.alloc(std::size_t(R) * d.ld_q);
+    s.dQ.alloc(std::size_t(R) * d.ld_Q); s.dq_in.alloc(std::size_t(R) * d.ld_q);
     s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
     s.trows = 64;
-    s.tblocks = (R * (1 + d.K) + s.trows - 1) / s.trows;
-    s.tpart.alloc(std::size_t(s.tblocks) * 2 * d.T);
+    s.troot_blocks = (R + s.trows - 1) / s.trows;
+    s.tattn_blocks = (R + tgnk::attn_roots_per_block() - 1) / tgnk::attn_roots_per_block();
+    s.tpart.alloc(std::size_t(s.troot_blocks + s.tattn_blocks) * 2 * d.T);
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
     SPD_CUDA(cudaStreamSynchronize(stream_));
 
@@ -506,7 +577,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t
     Scratch& s = *s_;
     const auto& d = s.d;
     w.last_b = B;
-    const int R = 3 * B, RK = R * d.K;
+    const int R = 3 * B;
     float* P = params_.p;
     float* G = grads_.p;
     cudaStream_t st = stream_;
@@ -522,32 +593,28 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     });
     timed("gru_fwd", [&] { gru_forward(w, wd, train); });
-    timed("embed_gather", [&] {
-        launch(tgnk::k_embed_gather, blocks_for(std::size_t(R) * (1 + d.K) * 32), 256, 0, st, 
-            wd, d, R, P + lay_.time_w, P + lay_.time_b, s.roots.p, s.nbr_node.p, s.nbr_ev.p,
-            s.nbr_dt.p, s.cnt.p, s.mem_new.p, s.q_in.p, s.kv_in.p);
+    timed("query_gather", [&] {
+        launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
+               P + lay_.time_w, P + lay_.time_b, s.roots.p, s.mem_new.p, s.q_in.p);
     });
     timed("gemm_q", [&] {
         proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
-                 d.DQ + 1, nullptr, st);
+                 d.DQ + 1, nullptr, st, 0, nullptr, 0, tc);
     });
-    timed("gemm_kv", [&] {
-        proj_fwd(tc, s.kv_in.p, d.ld_kv, PW + lay_.att_kv.off, lay_.att_kv.ld, s.KV.p, d.ld_KV, RK,
-                 2 * d.DQ, d.DK + 1, nullptr, st);
-    });
-    const std::size_t attn_smem = std::size_t(8) * d.H * d.K * sizeof(float);
-    const bool attn_reg = tgnk::attn_reg_ok(d);
-    const bool attn_small = d.K <= 10 && d.H <= 2;
+    // attention with absorbed key/value projections (tgn_attn.cu):
+    //   Qp_h = Q_h [W_K,h | b_K,h]; kernel -> alpha, xbar_h; ctx_h = xbar_h [W_V,h | b_V,h]^T
+    const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
+    const float* WK = PW + lay_.att_kv.off;
+    const float* WV = WK + std::size_t(d.DQ) * lay_.att_kv.ld;
+    const int ldw = lay_.att_kv.ld;
     timed("attn_fwd", [&] {
-        if (attn_reg && attn_small)
-            launch(tgnk::k_attn_fwd_reg<10, 2>, blocks_for(std::size_t(R) * 32), 256, 0, st, d, R,
-                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
-        else if (attn_reg)
-            launch(tgnk::k_attn_fwd_reg<16, 4>, blocks_for(std::size_t(R) * 32), 256, 0, st, d, R,
-                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
-        else
-            launch(tgnk::k_attn_fwd, blocks_for(std::size_t(R) * 32), 256, attn_smem, st, d, R,
-                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.ctx.p);
+        for (int h = 0; h < d.H; ++h)
+            proj_dgrad(tc, s.Q.p + h * dh, d.ld_Q, WK + std::size_t(h) * dh * ldw, ldw,
+                       s.Qp.p + std::size_t(h) * d.ld_p, ldhp, R, d.DK + 1, dh, nullptr, st);
+        attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st);
+        for (int h = 0; h < d.H; ++h)
+            proj_fwd(tc, s.xbar.p + std::size_t(h) * d.ld_p, ldhp, WV + std::size_t(h) * dh * ldw, ldw,
+                     s.ctx.p + h * dh, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0, nullptr, 0, tc);
     });
     timed("head_fwd", [&] {
         proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
@@ -580,15 +647,12 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t
 void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     Scratch& s = *s_;
     const auto& d = s.d;
-    const int R = 3 * B, RK = R * d.K;
+    const int R = 3 * B;
     float* P = params_.p;
     float* G = grads_.p;
     cudaStream_t st = stream_;
     const bool tc = cfg_.gemm_mode == 1;
     const float* PW = tc ? params_tc_.p : params_.p;
-    const std::size_t attn_smem = std::size_t(8) * d.H * d.K * sizeof(float);
-    const bool attn_reg = tgnk::attn_reg_ok(d);
-    const bool attn_small = d.K <= 10 && d.H <= 2;
     timed("head_bwd", [&] {
         side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
                    2 * B, nullptr, s.ws.p, s.ws.n, sd); });
@@ -613,26 +677,38 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
                    d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
         proj_dgrad(tc, s.dm_in.p, d.ld_m, PW + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R, d.DQ,
-                   d.DQ, nullptr, st);
+                   d.DQ, nullptr, st, 0, nullptr, 0, tc);
     });
+    const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
+    const float* WK = PW + lay_.att_kv.off;
+    const float* WV = WK + std::size_t(d.DQ) * lay_.att_kv.ld;
+    const int ldw = lay_.att_kv.ld;
+    float* GK = G + lay_.att_kv.off;
+    float* GV = GK + std::size_t(d.DQ) * ldw;
+    s.dH.zero(st);
     timed("attn_bwd", [&] {
-        if (attn_reg && attn_small)
-            launch(tgnk::k_attn_bwd_reg<10, 2>, blocks_for(std::size_t(R) * 32), 256, 0, st, d, R,
-                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.ld_Q, s.dQ.p, s.dKV.p);
-        else if (attn_reg)
-            launch(tgnk::k_attn_bwd_reg<16, 4>, blocks_for(std::size_t(R) * 32), 256, 0, st, d, R,
-                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.ld_Q, s.dQ.p, s.dKV.p);
-        else
-            launch(tgnk::k_attn_bwd, blocks_for(std::size_t(R) * 32), 256, attn_smem, st, d, R,
-                   s.cnt.p, s.Q.p, s.KV.p, s.alpha.p, s.dctx.p, d.ld_Q, s.dQ.p, s.dKV.p);
-    });
-    timed("gemm_kv_wgrad", [&] {
-        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dKV.p, d.ld_KV, s.kv_in.p, d.ld_kv, G + lay_.att_kv.off, lay_.att_kv.ld,
-                   2 * d.DQ, d.DK + 1, RK, nullptr, s.ws.p, s.ws.n, sd); });
-    });
-    timed("gemm_kv_dgrad", [&] {
-        proj_dgrad(tc, s.dKV.p, d.ld_KV, PW + lay_.att_kv.off, lay_.att_kv.ld, s.dkv_in.p, d.ld_kv, RK,
-                   d.D + d.T, 2 * d.DQ, nullptr, st);  // only [s_nbr | phi] carry gradient
+        for (int h = 0; h < d.H; ++h) {
+            // dW_V,h += dctx_h^T xbar_h ; dxbar_h = dctx_h [W_V,h | b_V,h]
+            side([&](cudaStream_t sd) {
+                proj_wgrad(tc, s.dctx.p + h * dh, d.ld_Q, s.xbar.p + std::size_t(h) * d.ld_p, ldhp,
+                           GV + std::size_t(h) * dh * ldw, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
+                           s.ws.n, sd);
+            });
+            proj_dgrad(tc, s.dctx.p + h * dh, d.ld_Q, WV + std::size_t(h) * dh * ldw, ldw,
+                       s.dxbar.p + std::size_t(h) * d.ld_p, ldhp, R, d.DK + 1, dh, nullptr, st);
+        }
+        attn_abs_bwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s,
+                     s.tpart.p + std::size_t(s.troot_blocks) * 2 * d.T, st);
+        for (int h = 0; h < d.H; ++h) {
+            // dW_K,h += Q_h^T dQp_h ; dQ_h = dQp_h [W_K,h | b_K,h]^T
+            side([&](cudaStream_t sd) {
+                proj_wgrad(tc, s.Q.p + h * dh, d.ld_Q, s.dQp.p + std::size_t(h) * d.ld_p, ldhp,
+                           GK + std::size_t(h) * dh * ldw, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
+                           s.ws.n, sd);
+            });
+            proj_fwd(tc, s.dQp.p + std::size_t(h) * d.ld_p, ldhp, WK + std::size_t(h) * dh * ldw, ldw,
+                     s.dQ.p + h * dh, d.ld_Q, R, dh, d.DK + 1, nullptr, st, 0, nullptr, 0, tc);
+        }
     });
     timed("q_bwd", [&] {
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
@@ -640,23 +716,11 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         proj_dgrad(tc, s.dQ.p, d.ld_Q, PW + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
                    d.DQ, nullptr, st);
     });
-    timed("mem_time_bwd", [&] {
-        s.dH.zero(st);
-        if (d.T <= 128) {  // fused single pass
-            const int tb = (R * (1 + d.K) + s.trows - 1) / s.trows;
-            launch(tgnk::k_memtime_grad, tb, dim3(32, 8), 0, st, wd, d, R, s.roots.p, s.nbr_node.p,
-                   s.cnt.p, s.nbr_dt.p, s.dq_in.p, s.dm_in.p, s.dkv_in.p, P + lay_.time_w,
-                   P + lay_.time_b, s.trows, s.dH.p, s.tpart.p);
-            launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, st, d.T, tb, s.tpart.p, tgrad_.p);
-            return;
-        }
-        launch(tgnk::k_mem_grad, blocks_for(std::size_t(R) * (1 + d.K) * 32), 256, 0, st, 
-            wd, d, R, s.roots.p, s.nbr_node.p, s.cnt.p, s.dq_in.p, s.dm_in.p, s.dkv_in.p, s.dH.p);
-        const int tb = (R * (1 + d.K) + s.trows - 1) / s.trows;
-        launch(tgnk::k_time_grad_partial, dim3(tb, (d.T + 31) / 32), dim3(32, 8), 0, st, d, R,
-               s.cnt.p, s.nbr_dt.p, s.dkv_in.p, s.dq_in.p, P + lay_.time_w, P + lay_.time_b,
-               s.trows, s.tpart.p);
-        launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, st, d.T, tb, s.tpart.p, tgrad_.p);
+    timed("root_time_bwd", [&] {
+        launch(tgnk::k_root_grad, s.troot_blocks, dim3(32, 8), 0, st, wd, d, R, s.roots.p, s.dq_in.p,
+               s.dm_in.p, P + lay_.time_b, s.trows, s.dH.p, s.tpart.p);
+        launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, st, d.T, s.troot_blocks + s.tattn_blocks,
+               s.tpart.p, tgrad_.p);
     });
     timed("gru_bwd", [&] {
         if (tc) {  // the TC weight-grad reads whole K blocks: rows >= |pending| must be 0

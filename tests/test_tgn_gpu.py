@@ -167,3 +167,34 @@ def test_no_cpu_fallback_without_device(monkeypatch):
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert "LOUD CudaError" in out.stdout, out.stdout + out.stderr
+
+
+# model shapes covering every attention-kernel instantiation class: GDELT dims
+# (4 column chunks per lane, 2 gradient-carrying), no edge features (LastFM),
+# one head, and the (K <= 16, H <= 4) variant
+@pytest.mark.parametrize("dims", [
+    dict(d_mem=100, d_time=100, d_edge=186, n_neighbors=10, n_heads=2, batch_size=48),
+    dict(d_mem=32, d_time=16, d_edge=0, n_neighbors=5, n_heads=1),
+    dict(d_mem=64, d_time=32, d_edge=60, n_neighbors=16, n_heads=4, batch_size=48),
+    dict(d_mem=128, d_time=96, d_edge=20, n_neighbors=12, n_heads=2, batch_size=40),
+])
+def test_model_shapes_match_oracle(dims):
+    _, _, pa, subs = partitioned(parts=1, nodes=150, edges=2000)
+    cfg = small_cfg(**dims)
+    tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+    tr.set_debug(True)
+    o = oracle_for(cfg, subs, pa.shared)
+    tr.begin_epoch(0)
+    o.begin_epoch(0)
+    for step in range(4):
+        gl = tr.step()
+        ol = o.step()
+        t = tr.last_step(0)
+        ref = o.last[0]
+        assert np.array_equal(t["nbr"], glob(o, 0, ref["nbr_ids"]))
+        tol = TOL_STEP if step == 0 else TOL_TRAJ
+        assert rel_err(t["emb"], ref["emb"]) < tol, (step, rel_err(t["emb"], ref["emb"]))
+        assert abs(gl[0] - ol[0]) <= tol * max(1.0, abs(ol[0]))
+        if step == 0:
+            assert rel_err(tr.grads(), o.grad.numpy()) < TOL_GRAD
+    assert rel_err(tr.params(), o.flat.numpy()) < TOL_TRAJ
