@@ -217,7 +217,8 @@ def main():
     cfg_desc = {"workload": f"{args.config}-shape synthetic TIG ({N} nodes, {E} edges, d_e={F}), "
                             f"TGN d_mem=d_time=100 k={K} heads={H}, B={B}, SEP P={world}",
                 "nodes": N, "edges": E, "d_edge": F, "batch": B, "partitions": world,
-                "parallelism": f"sep{world}", "l2": "inputs larger than L2 (50-100 GB feature "
+                "parallelism": f"sep{world}", "timed_from": "mid-epoch (spd_tgn_seek to epoch_steps/2)",
+                "l2": "inputs larger than L2 (50-100 GB feature "
                 "table gathers + >126 MB activations per step)"}
 
     if args.impl == "reference":
@@ -255,6 +256,10 @@ def main():
                        rank=rank, world=world, nccl_id=nccl_id, device=local)
     log(f"trainer ready: {time.time() - t0:.1f}s, params={tr.n_params}, epoch_steps={tr.epoch_steps()}")
     tr.begin_epoch(0)
+    # steady state: time steps from the middle of the epoch (full recent-k
+    # neighbour lists), not the epoch's sparse first batches
+    seek = tr.epoch_steps() // 2
+    tr.seek(seek)
     tr.run_steps(args.warmup)
     barrier(pg)
     launches0 = sp.kernel_launches()

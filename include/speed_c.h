@@ -273,6 +273,11 @@ spd_status spd_nccl_unique_id(void* out128);
 spd_status spd_tgn_epoch_steps(const spd_tgn_trainer* t, uint64_t* steps);
 /* Begin an epoch: positions to loop start (memory reset, pac_sim.cpp:238). */
 spd_status spd_tgn_begin_epoch(spd_tgn_trainer* t, int32_t epoch);
+/* Position the lockstep schedule at global step `step` of the current epoch:
+ * each worker at batch (step mod its batch count), memory, clocks and pending
+ * messages cleared. Benchmarks use it to time steady-state steps mid-epoch
+ * (full recent-k neighbour lists) instead of an epoch's sparse first batches. */
+spd_status spd_tgn_seek(spd_tgn_trainer* t, uint64_t step);
 /* One global step: every local worker trains one batch, gradients are
  * all-reduced (mean over all workers), Adam updates. loss_out: per local
  * worker mean BCE of the batch (device->host read), may be NULL. */

@@ -715,6 +715,10 @@ class TGNTrainer:
     def begin_epoch(self, epoch: int):
         _check(lib.spd_tgn_begin_epoch(self._h, epoch))
 
+    def seek(self, step: int):
+        """Position the schedule at global step `step` of this epoch (spd_tgn_seek)."""
+        _check(lib.spd_tgn_seek(self._h, step))
+
     def step(self, want_loss: bool = True):
         if not want_loss:
             _check(lib.spd_tgn_step(self._h, None))

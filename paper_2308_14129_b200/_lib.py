@@ -105,6 +105,7 @@ _SIGS = {
     "spd_nccl_unique_id": (i32, [P]),
     "spd_tgn_epoch_steps": (i32, [P, pu64]),
     "spd_tgn_begin_epoch": (i32, [P, i32]),
+    "spd_tgn_seek": (i32, [P, u64]),
     "spd_tgn_step": (i32, [P, pf32]),
     "spd_tgn_end_epoch": (i32, [P]),
     "spd_tgn_run_epoch": (i32, [P, i32, pf64]),

@@ -100,6 +100,7 @@ public:
     std::uint64_t epoch_steps() const { return epoch_steps_; }
     std::uint64_t batch_size() const { return cfg_.batch_size; }
     void begin_epoch(int epoch);
+    void seek(std::uint64_t step);
     void step(float* loss_out);
     void end_epoch();
     void run_epoch(int epoch, double* mean_loss);

@@ -13,13 +13,15 @@
 // summation order differs.
 //
 // Execution: 4 warps per block, one root per warp. Each warp first stages its
-// root's k neighbour rows in shared memory with cp.async — memory row (f32,
-// from the GRU output when the neighbour was just updated), raw bf16 feature
-// row — and evaluates phi(dt) (f64 phase) into the same row, so every gather
-// of the root is in flight at once; both passes then read shared memory.
-// Lane l owns the float4 column chunks l, l+32, .. of the ld_p-wide augmented
-// row (D, T multiples of 4: a chunk lies wholly in the memory, time or
-// feature|1|pad region).
+// root's k neighbour rows in shared memory — memory row (f32, the GRU output
+// when the neighbour was just updated) and raw bf16 feature row by cp.async,
+// so every gather of the root is in flight at once, and cos (backward: also
+// sin) of the f64 time phase — and both passes then read shared memory.
+//
+// Lane slots are region-uniform: slot i < NM covers memory columns
+// 4(lane + 32i), the next NT slots time columns, the last NF slots feature
+// columns including the constant-1 bias column at F. Every slot of a warp is
+// in one region, so the inner loops are branch-free (compile-time region).
 #include "tgn_common.cuh"
 #include "tgn_kernels.cuh"
 
@@ -30,8 +32,8 @@ namespace {
 
 constexpr int kRootsPerBlock = 4;
 
-__device__ __forceinline__ float dot4(const float4& a, const float4& b) {
-    return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
+__device__ __forceinline__ float dot4acc(const float4& a, const float4& b, float acc) {
+    return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, fmaf(a.x, b.x, acc))));
 }
 __device__ __forceinline__ void axpy4(float4& acc, float s, const float4& x) {
     acc.x += s * x.x; acc.y += s * x.y; acc.z += s * x.z; acc.w += s * x.w;
@@ -53,35 +55,123 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-// bytes of one staged neighbour row: [mem f32 D | phi f32 T | feat bf16 Fp]
-__host__ __device__ __forceinline__ int row_bytes(const Dims& d) {
-    return 4 * (d.D + d.T) + 2 * d.Fp;
+// One staged neighbour row: [mem f32 D | cos f32 T | feat bf16 Fp | sin f32 T (bwd)]
+__host__ __device__ __forceinline__ int row_bytes(const Dims& d, bool with_sin) {
+    return 4 * (d.D + d.T) + 2 * d.Fp + (with_sin ? 4 * d.T : 0);
+}
+
+// Slot geometry (compile-time region per slot).
+template <int NM, int NT, int NF>
+struct Slots {
+    static constexpr int N = NM + NT + NF;
+    // region of slot i: 0 memory, 1 time, 2 feature|bias
+    static constexpr __host__ __device__ int region(int i) { return i < NM ? 0 : (i < NM + NT ? 1 : 2); }
+    static constexpr __host__ __device__ int local(int i) {
+        return i < NM ? i : (i < NM + NT ? i - NM : i - NM - NT);
+    }
+    // first column of slot i for this lane, and whether it holds data
+    static __device__ __forceinline__ int col(const Dims& d, int i, int lane) {
+        const int o = 4 * (lane + 32 * local(i));
+        return region(i) == 0 ? o : (region(i) == 1 ? d.D + o : d.D + d.T + o);
+    }
+    static __device__ __forceinline__ bool valid(const Dims& d, int i, int lane) {
+        const int o = 4 * (lane + 32 * local(i));
+        return region(i) == 0 ? o < d.D : (region(i) == 1 ? o < d.T : o <= d.F);
+    }
+};
+
+// Slot i of a staged row: columns col(i)..+3 of [s_nbr | phi | e], the
+// constant-1 bias column excluded. Its terms drop out of the kernels exactly:
+// <q'_h, e_bias> = <q_h, b_K,h> is the same for every neighbour, so softmax
+// (shift invariant) ignores it and its gradient sum_j ds_hj is 0; in xbar it
+// is sum_j a_hj = 1, set directly (set_bias).
+template <class S>
+__device__ __forceinline__ float4 x_slot(const Dims& d, int i, int lane, const unsigned char* row) {
+    const int o = 4 * (lane + 32 * S::local(i));
+    if (S::region(i) == 0) return o < d.D ? *reinterpret_cast<const float4*>(row + 4 * o) : z4();
+    if (S::region(i) == 1) return o < d.T ? *reinterpret_cast<const float4*>(row + 4 * (d.D + o)) : z4();
+    if (o >= d.Fp) return z4();  // Fp % 8 == 0: 4 bf16 never straddle the row end; pad is 0
+    const uint2 raw = *reinterpret_cast<const uint2*>(row + 4 * (d.D + d.T) + 2 * o);
+    return make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
+                       __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u));
+}
+
+// Put value c into the bias column (feature index F) of every head's slots.
+template <class S, int HMAX>
+__device__ __forceinline__ void set_bias(float4 (&v)[HMAX][S::N], const Dims& d, int lane, float c) {
+#pragma unroll
+    for (int i = 0; i < S::N; ++i) {
+        if (S::region(i) != 2) continue;
+        const int b = d.F - 4 * (lane + 32 * S::local(i));
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) {
+            if (b == 0) v[h][i].x = c;
+            else if (b == 1) v[h][i].y = c;
+            else if (b == 2) v[h][i].z = c;
+            else if (b == 3) v[h][i].w = c;
+        }
+    }
+}
+
+// Sum each of V values over the warp (V a power of two <= 32) with V - 1 +
+// (5 - log2 V) shuffles instead of 5 V: every stage halves the values a lane
+// carries. On return the lane holds the total of value index vidx<V>(lane).
+template <int V>
+__device__ __forceinline__ float warp_reduce_multi(float (&v)[V], int lane) {
+    constexpr int LOG = V == 1 ? 0 : V == 2 ? 1 : V == 4 ? 2 : V == 8 ? 3 : V == 16 ? 4 : 5;
+#pragma unroll
+    for (int st = 0; st < LOG; ++st) {
+        const int o = 16 >> st;
+        const bool up = lane & o;
+#pragma unroll
+        for (int k = 0; k < (V >> (st + 1)); ++k) {
+            const int half = V >> (st + 1);
+            const float send = up ? v[k] : v[k + half];
+            const float keep = up ? v[k + half] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    float r = v[0];
+#pragma unroll
+    for (int o = 16 >> LOG; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r;
+}
+template <int V>
+__device__ __forceinline__ int vidx(int lane) {
+    constexpr int LOG = V == 1 ? 0 : V == 2 ? 1 : V == 4 ? 2 : V == 8 ? 3 : V == 16 ? 4 : 5;
+    int idx = 0;
+#pragma unroll
+    for (int st = 0; st < LOG; ++st)
+        if (lane & (16 >> st)) idx += V >> (st + 1);
+    return idx;
 }
 
 // Stage root r's neighbour rows (warp-cooperative). Lane j < c_n holds
-// neighbour j's (node, dt, slot) on return, for the caller's scatters.
+// neighbour j's (dt, slot) on return, for the caller's scatters. TPL >= T/32.
+template <int TPL>
 __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, int r, int c_n,
                                            int lane, const float* time_w, const float* time_b,
                                            const std::uint32_t* nbr_node,
                                            const std::uint32_t* nbr_ev, const double* nbr_dt,
-                                           const float* mem_new, unsigned char* xs,
-                                           std::uint32_t& m_node, double& m_dt, int& m_slot) {
-    std::uint32_t ev = 0;
-    m_node = 0; m_dt = 0.0; m_slot = -1;
+                                           const float* mem_new, unsigned char* xs, bool with_sin,
+                                           double& m_dt, int& m_slot) {
+    std::uint32_t ev = 0, node = 0;
+    m_dt = 0.0;
+    m_slot = -1;
     if (lane < c_n) {
         const std::size_t o = (std::size_t)r * d.K + lane;
-        m_node = nbr_node[o];
+        node = nbr_node[o];
         ev = nbr_ev[o];
         m_dt = nbr_dt[o];
-        m_slot = w.slot[m_node];
+        m_slot = w.slot[node];
     }
-    const int RB = row_bytes(d);
+    const int RB = row_bytes(d, with_sin);
     const int mch = d.D / 4, fch = d.Fp / 8;  // 16-B chunks of the memory / feature rows
     for (int j = 0; j < c_n; ++j) {
-        const std::uint32_t node = __shfl_sync(0xffffffffu, m_node, j);
+        const std::uint32_t nj = __shfl_sync(0xffffffffu, node, j);
         const std::uint32_t e = __shfl_sync(0xffffffffu, ev, j);
         const int slot = __shfl_sync(0xffffffffu, m_slot, j);
-        const float* mrow = slot >= 0 ? mem_new + (std::size_t)slot * d.D : w.mem + (std::size_t)node * d.D;
+        const float* mrow = slot >= 0 ? mem_new + (std::size_t)slot * d.D : w.mem + (std::size_t)nj * d.D;
         const __nv_bfloat16* frow = w.feat + (std::size_t)e * d.Fp;
         unsigned char* dst = xs + (std::size_t)j * RB;
         for (int c = lane; c < mch + fch; c += 32) {
@@ -89,55 +179,114 @@ __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, in
             else cp_async16_cg(dst + 4 * (d.D + d.T) + 16 * (c - mch), frow + 8 * (c - mch));
         }
     }
-    // phi(dt) = cos(w dt + b), phase in f64
+    // phi(dt) = cos(w dt + b) (and sin for the backward), phase in f64;
+    // this lane's time columns t = lane + 32k (k < TPL) and their parameters
+    double tw[TPL], tb[TPL];
+#pragma unroll
+    for (int k = 0; k < TPL; ++k) {
+        const int t = lane + 32 * k;
+        tw[k] = t < d.T ? static_cast<double>(time_w[t]) : 0.0;
+        tb[k] = t < d.T ? static_cast<double>(time_b[t]) : 0.0;
+    }
+#pragma unroll 1
     for (int j = 0; j < c_n; ++j) {
         const double dt = __shfl_sync(0xffffffffu, m_dt, j);
-        float* ph = reinterpret_cast<float*>(xs + (std::size_t)j * RB) + d.D;
-        for (int t = lane; t < d.T; t += 32) ph[t] = time_cos(time_w[t], time_b[t], dt);
+        float* cs = reinterpret_cast<float*>(xs + (std::size_t)j * RB) + d.D;
+        float* sn = reinterpret_cast<float*>(xs + (std::size_t)j * RB + 4 * (d.D + d.T) + 2 * d.Fp);
+#pragma unroll
+        for (int k = 0; k < TPL; ++k) {
+            const int t = lane + 32 * k;
+            if (t < d.T) {
+                const float2 sc2 = with_sin ? phase_sincos<true>(tw[k], tb[k], dt)
+                                            : phase_sincos<false>(tw[k], tb[k], dt);
+                cs[t] = sc2.y;
+                if (with_sin) sn[t] = sc2.x;
+            }
+        }
     }
     cp_async_wait_all();
     __syncwarp();
 }
 
-// Chunk ch (columns 4ch..4ch+3) of the staged augmented row.
-__device__ __forceinline__ float4 x_chunk(const Dims& d, int ch, const unsigned char* row) {
-    const int c = 4 * ch;
-    if (c < d.D + d.T) return *reinterpret_cast<const float4*>(row + 4 * c);
-    const int f = c - d.D - d.T;
-    float4 v = z4();
-    if (f < d.Fp) {  // Fp % 8 == 0: 4 bf16 never straddle the row end; pad columns are 0
-        const uint2 raw = *reinterpret_cast<const uint2*>(row + 4 * (d.D + d.T) + 2 * f);
-        const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
-        const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
-        v = make_float4(__low2float(lo), __high2float(lo), __low2float(hi), __high2float(hi));
-    }
-    // augmented constant-1 column (bias) at feature index F
-    const int b = d.F - f;
-    if (b == 0) v.x = 1.f;
-    else if (b == 1) v.y = 1.f;
-    else if (b == 2) v.z = 1.f;
-    else if (b == 3) v.w = 1.f;
-    return v;
-}
-
-template <int NCH, int HMAX>
-__device__ __forceinline__ void load_rows(float4 (&v)[HMAX][NCH], const float* base, const Dims& d,
-                                          int lane, int nch) {
+template <class S, int HMAX>
+__device__ __forceinline__ void load_slots(float4 (&v)[HMAX][S::N], const float* base, const Dims& d,
+                                           int lane) {
 #pragma unroll
     for (int h = 0; h < HMAX; ++h)
 #pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-            const int ch = lane + 32 * i;
-            v[h][i] = (h < d.H && ch < nch)
-                          ? reinterpret_cast<const float4*>(base + (std::size_t)h * d.ld_p)[ch]
+        for (int i = 0; i < S::N; ++i)
+            v[h][i] = (h < d.H && S::valid(d, i, lane))
+                          ? *reinterpret_cast<const float4*>(base + (std::size_t)h * d.ld_p + S::col(d, i, lane))
                           : z4();
+}
+
+template <class S, int HMAX>
+__device__ __forceinline__ void store_slots(const float4 (&v)[HMAX][S::N], float* base, const Dims& d,
+                                            int lane, int rnd) {
+#pragma unroll
+    for (int h = 0; h < HMAX; ++h) {
+        if (h >= d.H) break;
+#pragma unroll
+        for (int i = 0; i < S::N; ++i)
+            if (S::valid(d, i, lane))
+                *reinterpret_cast<float4*>(base + (std::size_t)h * d.ld_p + S::col(d, i, lane)) = rnd4(v[h][i], rnd);
+    }
+}
+
+// sc[h*K + j] = scale * <v[h], x~_j> for every valid neighbour j, in groups
+// of 8 neighbours whose 8*HMAX partial dot products share one multi-value
+// warp reduction.
+template <class S, int HMAX>
+__device__ __forceinline__ void dots(const float4 (&v)[HMAX][S::N], const Dims& d, int lane, const unsigned char* xs, int RB,
+                                     int c_n, float* sc, float scale) {
+    constexpr int G = 8, V = G * HMAX;
+    const int vi = vidx<V>(lane);
+    const int hv = vi / G, gv = vi % G;
+    const bool writer = (lane & ((32 / V) - 1)) == 0;
+#pragma unroll 1
+    for (int j0 = 0; j0 < c_n; j0 += G) {
+        float p[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) p[k] = 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            if (j0 + g < c_n) {
+                const unsigned char* row = xs + (std::size_t)(j0 + g) * RB;
+#pragma unroll
+                for (int i = 0; i < S::N; ++i) {
+                    const float4 x = x_slot<S>(d, i, lane, row);
+#pragma unroll
+                    for (int h = 0; h < HMAX; ++h) p[h * G + g] = dot4acc(v[h][i], x, p[h * G + g]);
+                }
+            }
         }
+        const float r = warp_reduce_multi<V>(p, lane);
+        if (writer && hv < d.H && j0 + gv < c_n) sc[hv * d.K + j0 + gv] = r * scale;
+    }
+}
+
+template <class S, int HMAX>
+__device__ __forceinline__ void axpys(float4 (&v)[HMAX][S::N], const Dims& d, int lane, const unsigned char* xs, int RB,
+                                      int c_n, const float* coef) {
+#pragma unroll 2
+    for (int j = 0; j < c_n; ++j) {
+        const unsigned char* row = xs + (std::size_t)j * RB;
+        float a[HMAX];
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) a[h] = h < d.H ? coef[h * d.K + j] : 0.f;
+#pragma unroll
+        for (int i = 0; i < S::N; ++i) {
+            const float4 x = x_slot<S>(d, i, lane, row);
+#pragma unroll
+            for (int h = 0; h < HMAX; ++h) axpy4(v[h][i], a[h], x);
+        }
+    }
 }
 
 }  // namespace
 
-__host__ __device__ std::size_t attn_smem_bytes(const Dims& d) {
-    const std::size_t stage = std::size_t(kRootsPerBlock) * d.K * row_bytes(d);
+__host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd) {
+    const std::size_t stage = std::size_t(kRootsPerBlock) * d.K * row_bytes(d, bwd);
     const std::size_t tpart = std::size_t(kRootsPerBlock) * 2 * d.T * sizeof(float);
     return (stage > tpart ? stage : tpart) + kRootsPerBlock * 2 * sizeof(float) * d.H * d.K;
 }
@@ -146,7 +295,7 @@ int attn_roots_per_block() { return kRootsPerBlock; }
 // Forward: scores from q'_h (Qp), softmax, alpha [R][H][K], xbar_h [R][H][ld_p]
 // (tf32-rounded when it feeds a tensor-core GEMM). Roots without neighbours
 // get xbar = 0 (bias slot 0 too: ctx = 0; the oracle masks them).
-template <int NCH, int HMAX>
+template <int NM, int NT, int NF, int HMAX>
 __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R,
                                                       const float* time_w, const float* time_b,
                                                       const std::uint32_t* nbr_node,
@@ -154,55 +303,35 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
                                                       const double* nbr_dt, const int* cnt,
                                                       const float* mem_new, const float* Qp,
                                                       float* alpha, float* xbar) {
+    using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = blockIdx.x * kRootsPerBlock + warp;
     if (r >= R) return;
-    const int RB = row_bytes(d);
+    const int RB = row_bytes(d, false);
     unsigned char* xs = smem + (std::size_t)warp * d.K * RB;
-    float* sc = reinterpret_cast<float*>(smem + attn_smem_bytes(d)) - kRootsPerBlock * 2 * d.H * d.K +
-                warp * 2 * d.H * d.K;
+    float* sc = reinterpret_cast<float*>(smem + attn_smem_bytes(d, false)) -
+                kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
     const int c_n = cnt[r];
-    const int nch = d.ld_p / 4;
     const std::size_t row0 = (std::size_t)r * d.H * d.ld_p;
+    float4 v[HMAX][S::N];  // q'_h, then the xbar accumulators
     if (c_n == 0) {
-        for (int h = 0; h < d.H; ++h)
-            for (int ch = lane; ch < nch; ch += 32)
-                reinterpret_cast<float4*>(xbar + row0 + (std::size_t)h * d.ld_p)[ch] = z4();
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h)
+#pragma unroll
+            for (int i = 0; i < S::N; ++i) v[h][i] = z4();
+        store_slots<S, HMAX>(v, xbar + row0, d, lane, 0);
         if (lane < d.K)
             for (int h = 0; h < d.H; ++h) alpha[((std::size_t)r * d.H + h) * d.K + lane] = 0.f;
         return;
     }
-    std::uint32_t m_node;
     double m_dt;
     int m_slot;
-    stage_rows(w, d, r, c_n, lane, time_w, time_b, nbr_node, nbr_ev, nbr_dt, mem_new, xs, m_node,
-               m_dt, m_slot);
-    float4 v[HMAX][NCH];  // q'_h, then the xbar accumulators
-    load_rows<NCH, HMAX>(v, Qp + row0, d, lane, nch);
+    stage_rows<4 * NT>(w, d, r, c_n, lane, time_w, time_b, nbr_node, nbr_ev, nbr_dt, mem_new, xs,
+                       false, m_dt, m_slot);
+    load_slots<S, HMAX>(v, Qp + row0, d, lane);
     const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
-#pragma unroll 1
-    for (int j = 0; j < c_n; ++j) {
-        const unsigned char* row = xs + (std::size_t)j * RB;
-        float p[HMAX];
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) p[h] = 0.f;
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-            const int ch = lane + 32 * i;
-            if (ch < nch) {
-                const float4 x = x_chunk(d, ch, row);
-#pragma unroll
-                for (int h = 0; h < HMAX; ++h) p[h] += dot4(v[h][i], x);
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h)
-            if (h < d.H) {
-                const float s = warp_sum(p[h]);
-                if (lane == 0) sc[h * d.K + j] = s * inv;
-            }
-    }
+    dots<S, HMAX>(v, d, lane, xs, RB, c_n, sc, inv);
     __syncwarp();
     // softmax per head over the c_n valid neighbours (lane = neighbour)
     for (int h = 0; h < d.H; ++h) {
@@ -223,33 +352,10 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
 #pragma unroll
     for (int h = 0; h < HMAX; ++h)
 #pragma unroll
-        for (int i = 0; i < NCH; ++i) v[h][i] = z4();
-#pragma unroll 1
-    for (int j = 0; j < c_n; ++j) {
-        const unsigned char* row = xs + (std::size_t)j * RB;
-        float a[HMAX];
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) a[h] = h < d.H ? sc[h * d.K + j] : 0.f;
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-            const int ch = lane + 32 * i;
-            if (ch < nch) {
-                const float4 x = x_chunk(d, ch, row);
-#pragma unroll
-                for (int h = 0; h < HMAX; ++h) axpy4(v[h][i], a[h], x);
-            }
-        }
-    }
-#pragma unroll
-    for (int h = 0; h < HMAX; ++h) {
-        if (h >= d.H) break;
-        float4* o = reinterpret_cast<float4*>(xbar + row0 + (std::size_t)h * d.ld_p);
-#pragma unroll
-        for (int i = 0; i < NCH; ++i) {
-            const int ch = lane + 32 * i;
-            if (ch < nch) o[ch] = rnd4(v[h][i], d.rnd);
-        }
-    }
+        for (int i = 0; i < S::N; ++i) v[h][i] = z4();
+    axpys<S, HMAX>(v, d, lane, xs, RB, c_n, sc);
+    set_bias<S, HMAX>(v, d, lane, 1.f);  // sum_j a_hj
+    store_slots<S, HMAX>(v, xbar + row0, d, lane, d.rnd);
 }
 
 // Backward, given dxbar_h = [W_V,h|b_V,h]^T dctx_h (GEMM) per root:
@@ -259,7 +365,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
 //           memory part -> dH rows of pending nodes (float4 atomics), time part
 //           -> d/dw, d/db of cos(w dt + b) (per-block partials, fixed order).
 // part: [gridDim.x][2T] (w then b), f64; every block writes its row.
-template <int NCH, int NCX, int HMAX>
+template <int NM, int NT, int NF, int HMAX>
 __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R,
                                                       const float* time_w, const float* time_b,
                                                       const std::uint32_t* nbr_node,
@@ -268,61 +374,39 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
                                                       const float* mem_new, const float* Qp,
                                                       const float* alpha, const float* dxbar,
                                                       float* dQp, float* dH, double* part) {
+    using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = blockIdx.x * kRootsPerBlock + warp;
-    const int RB = row_bytes(d);
+    const int RB = row_bytes(d, true);
     unsigned char* xs = smem + (std::size_t)warp * d.K * RB;
-    float* sc = reinterpret_cast<float*>(smem + attn_smem_bytes(d)) - kRootsPerBlock * 2 * d.H * d.K +
-                warp * 2 * d.H * d.K;
+    float* sc = reinterpret_cast<float*>(smem + attn_smem_bytes(d, true)) -
+                kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
     float* aa = sc + d.H * d.K;  // alpha of this root
-    // time-encoder partials of this warp's root reuse the staging area at the end
-    const int nch = d.ld_p / 4;
-    const int nchx = (d.D + d.T) / 4;
     const int c_n = r < R ? cnt[r] : 0;
     const std::size_t row0 = (std::size_t)r * d.H * d.ld_p;
-    float4 gw[NCX], gb[NCX];
+    float4 gw[NT], gb[NT];  // time-encoder gradient partials of this lane's time slots
 #pragma unroll
-    for (int i = 0; i < NCX; ++i) gw[i] = gb[i] = z4();
+    for (int i = 0; i < NT; ++i) gw[i] = gb[i] = z4();
+    float4 v[HMAX][S::N];  // dxbar_h, then the dq'_h accumulators
     if (r < R && c_n == 0) {
-        for (int h = 0; h < d.H; ++h)
-            for (int ch = lane; ch < nch; ch += 32)
-                reinterpret_cast<float4*>(dQp + row0 + (std::size_t)h * d.ld_p)[ch] = z4();
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h)
+#pragma unroll
+            for (int i = 0; i < S::N; ++i) v[h][i] = z4();
+        store_slots<S, HMAX>(v, dQp + row0, d, lane, 0);
     }
     if (c_n > 0) {
-        std::uint32_t m_node;
         double m_dt;
         int m_slot;
-        stage_rows(w, d, r, c_n, lane, time_w, time_b, nbr_node, nbr_ev, nbr_dt, mem_new, xs,
-                   m_node, m_dt, m_slot);
+        stage_rows<4 * NT>(w, d, r, c_n, lane, time_w, time_b, nbr_node, nbr_ev, nbr_dt, mem_new, xs,
+                           true, m_dt, m_slot);
         if (lane < d.K)
             for (int h = 0; h < d.H; ++h)
                 aa[h * d.K + lane] = lane < c_n ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
-        float4 v[HMAX][NCH];  // dxbar_h, then the dq'_h accumulators
-        load_rows<NCH, HMAX>(v, dxbar + row0, d, lane, nch);
+        load_slots<S, HMAX>(v, dxbar + row0, d, lane);
         // pass 1: da_hj
-#pragma unroll 1
-        for (int j = 0; j < c_n; ++j) {
-            const unsigned char* row = xs + (std::size_t)j * RB;
-            float p[HMAX];
-#pragma unroll
-            for (int h = 0; h < HMAX; ++h) p[h] = 0.f;
-#pragma unroll
-            for (int i = 0; i < NCH; ++i) {
-                const int ch = lane + 32 * i;
-                if (ch < nch) {
-                    const float4 x = x_chunk(d, ch, row);
-#pragma unroll
-                    for (int h = 0; h < HMAX; ++h) p[h] += dot4(v[h][i], x);
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < HMAX; ++h)
-                if (h < d.H) {
-                    const float s = warp_sum(p[h]);
-                    if (lane == 0) sc[h * d.K + j] = s;
-                }
-        }
+        dots<S, HMAX>(v, d, lane, xs, RB, c_n, sc, 1.f);
         __syncwarp();
         // softmax backward (lane = neighbour): ds = a (da - <a, da>) / sqrt(dh)
         const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
@@ -338,48 +422,26 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
 #pragma unroll
         for (int h = 0; h < HMAX; ++h)
 #pragma unroll
-            for (int i = 0; i < NCH; ++i) v[h][i] = z4();
-#pragma unroll 1
-        for (int j = 0; j < c_n; ++j) {
-            const unsigned char* row = xs + (std::size_t)j * RB;
-            float s[HMAX];
-#pragma unroll
-            for (int h = 0; h < HMAX; ++h) s[h] = h < d.H ? sc[h * d.K + j] : 0.f;
-#pragma unroll
-            for (int i = 0; i < NCH; ++i) {
-                const int ch = lane + 32 * i;
-                if (ch < nch) {
-                    const float4 x = x_chunk(d, ch, row);
-#pragma unroll
-                    for (int h = 0; h < HMAX; ++h) axpy4(v[h][i], s[h], x);
-                }
-            }
-        }
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h) {
-            if (h >= d.H) break;
-            float4* o = reinterpret_cast<float4*>(dQp + row0 + (std::size_t)h * d.ld_p);
-#pragma unroll
-            for (int i = 0; i < NCH; ++i) {
-                const int ch = lane + 32 * i;
-                if (ch < nch) o[ch] = rnd4(v[h][i], d.rnd);
-            }
-        }
-        // pass 2b: input gradients on [s_nbr | phi] (no gather needed)
-        float4 g[HMAX][NCX], q[HMAX][NCX];
+            for (int i = 0; i < S::N; ++i) v[h][i] = z4();
+        axpys<S, HMAX>(v, d, lane, xs, RB, c_n, sc);
+        store_slots<S, HMAX>(v, dQp + row0, d, lane, d.rnd);
+        // pass 2b: input gradients on [s_nbr | phi] (memory and time slots)
+        constexpr int NX = NM + NT;
+        float4 g[HMAX][NX], q[HMAX][NX];
 #pragma unroll
         for (int h = 0; h < HMAX; ++h)
 #pragma unroll
-            for (int i = 0; i < NCX; ++i) {
-                const int ch = lane + 32 * i;
-                const bool ok = h < d.H && ch < nchx;
-                g[h][i] = ok ? reinterpret_cast<const float4*>(dxbar + row0 + (std::size_t)h * d.ld_p)[ch] : z4();
-                q[h][i] = ok ? reinterpret_cast<const float4*>(Qp + row0 + (std::size_t)h * d.ld_p)[ch] : z4();
+            for (int i = 0; i < NX; ++i) {
+                const bool ok = h < d.H && S::valid(d, i, lane);
+                const int c = S::col(d, i, lane);
+                g[h][i] = ok ? *reinterpret_cast<const float4*>(dxbar + row0 + (std::size_t)h * d.ld_p + c) : z4();
+                q[h][i] = ok ? *reinterpret_cast<const float4*>(Qp + row0 + (std::size_t)h * d.ld_p + c) : z4();
             }
 #pragma unroll 1
         for (int j = 0; j < c_n; ++j) {
             const int slot = __shfl_sync(0xffffffffu, m_slot, j);
-            const double dt = __shfl_sync(0xffffffffu, m_dt, j);
+            const float fdt = (float)__shfl_sync(0xffffffffu, m_dt, j);
+            const float* sn = reinterpret_cast<const float*>(xs + (std::size_t)j * RB + 4 * (d.D + d.T) + 2 * d.Fp);
             float a[HMAX], s[HMAX];
 #pragma unroll
             for (int h = 0; h < HMAX; ++h) {
@@ -387,28 +449,24 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
                 s[h] = h < d.H ? sc[h * d.K + j] : 0.f;
             }
 #pragma unroll
-            for (int i = 0; i < NCX; ++i) {
-                const int ch = lane + 32 * i;
-                if (ch >= nchx) continue;
+            for (int i = 0; i < NX; ++i) {
+                if (!S::valid(d, i, lane)) continue;
                 float4 gx = z4();
 #pragma unroll
                 for (int h = 0; h < HMAX; ++h) {
                     axpy4(gx, a[h], g[h][i]);
                     axpy4(gx, s[h], q[h][i]);
                 }
-                const int c = 4 * ch;
-                if (c < d.D) {
-                    if (slot >= 0) atomicAdd(reinterpret_cast<float4*>(dH + (std::size_t)slot * d.D + c), gx);
+                const int o = 4 * (lane + 32 * S::local(i));
+                if (S::region(i) == 0) {
+                    if (slot >= 0) atomicAdd(reinterpret_cast<float4*>(dH + (std::size_t)slot * d.D + o), gx);
                 } else {
-                    const int t = c - d.D;
-                    const float4 wv = *reinterpret_cast<const float4*>(time_w + t);
-                    const float4 bv = *reinterpret_cast<const float4*>(time_b + t);
-                    const float s0 = time_sin(wv.x, bv.x, dt), s1 = time_sin(wv.y, bv.y, dt);
-                    const float s2 = time_sin(wv.z, bv.z, dt), s3 = time_sin(wv.w, bv.w, dt);
-                    const float fdt = (float)dt;
-                    gb[i].x -= s0 * gx.x; gb[i].y -= s1 * gx.y; gb[i].z -= s2 * gx.z; gb[i].w -= s3 * gx.w;
-                    gw[i].x -= s0 * gx.x * fdt; gw[i].y -= s1 * gx.y * fdt;
-                    gw[i].z -= s2 * gx.z * fdt; gw[i].w -= s3 * gx.w * fdt;
+                    const float4 sv = *reinterpret_cast<const float4*>(sn + o);
+                    float4& bw = gw[S::local(i)];
+                    float4& bb = gb[S::local(i)];
+                    bb.x -= sv.x * gx.x; bb.y -= sv.y * gx.y; bb.z -= sv.z * gx.z; bb.w -= sv.w * gx.w;
+                    bw.x -= sv.x * gx.x * fdt; bw.y -= sv.y * gx.y * fdt;
+                    bw.z -= sv.z * gx.z * fdt; bw.w -= sv.w * gx.w * fdt;
                 }
             }
         }
@@ -420,14 +478,11 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     for (int c = lane; c < 2 * d.T; c += 32) tw[c] = 0.f;
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < NCX; ++i) {
-        const int ch = lane + 32 * i;
-        const int c = 4 * ch;
-        if (ch < nchx && c >= d.D) {
-            const int t = c - d.D;
-            tw[t] = gw[i].x; tw[t + 1] = gw[i].y; tw[t + 2] = gw[i].z; tw[t + 3] = gw[i].w;
-            tw[d.T + t] = gb[i].x; tw[d.T + t + 1] = gb[i].y;
-            tw[d.T + t + 2] = gb[i].z; tw[d.T + t + 3] = gb[i].w;
+    for (int i = 0; i < NT; ++i) {
+        const int t = 4 * (lane + 32 * i);
+        if (t < d.T) {
+            *reinterpret_cast<float4*>(tw + t) = gw[i];
+            *reinterpret_cast<float4*>(tw + d.T + t) = gb[i];
         }
     }
     __syncthreads();
@@ -439,27 +494,23 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     }
 }
 
-#define SPD_ABS_FWD_INST(NCH, HM)                                                               \
-    template __global__ void k_attn_abs_fwd<NCH, HM>(                                            \
+#define SPD_ABS_INST(NM, NT, NF, HM)                                                            \
+    template __global__ void k_attn_abs_fwd<NM, NT, NF, HM>(                                     \
         WorkerDev, Dims, int, const float*, const float*, const std::uint32_t*,                  \
         const std::uint32_t*, const double*, const int*, const float*, const float*, float*,     \
-        float*);
-#define SPD_ABS_BWD_INST(NCH, NCX, HM)                                                          \
-    template __global__ void k_attn_abs_bwd<NCH, NCX, HM>(                                       \
+        float*);                                                                                \
+    template __global__ void k_attn_abs_bwd<NM, NT, NF, HM>(                                     \
         WorkerDev, Dims, int, const float*, const float*, const std::uint32_t*,                  \
         const std::uint32_t*, const double*, const int*, const float*, const float*,             \
         const float*, const float*, float*, float*, double*);
-#define SPD_ABS_ALL(HM)                                                                         \
-    SPD_ABS_FWD_INST(1, HM) SPD_ABS_FWD_INST(2, HM) SPD_ABS_FWD_INST(3, HM)                      \
-    SPD_ABS_FWD_INST(4, HM)                                                                     \
-    SPD_ABS_BWD_INST(1, 1, HM) SPD_ABS_BWD_INST(2, 1, HM) SPD_ABS_BWD_INST(2, 2, HM)             \
-    SPD_ABS_BWD_INST(3, 1, HM) SPD_ABS_BWD_INST(3, 2, HM) SPD_ABS_BWD_INST(4, 1, HM)             \
-    SPD_ABS_BWD_INST(4, 2, HM)
-SPD_ABS_ALL(2)
-SPD_ABS_ALL(4)
-#undef SPD_ABS_ALL
-#undef SPD_ABS_BWD_INST
-#undef SPD_ABS_FWD_INST
+#define SPD_ABS_NF(NM, NT, HM) \
+    SPD_ABS_INST(NM, NT, 1, HM) SPD_ABS_INST(NM, NT, 2, HM) SPD_ABS_INST(NM, NT, 3, HM)
+#define SPD_ABS_H(HM) SPD_ABS_NF(1, 1, HM) SPD_ABS_NF(1, 2, HM) SPD_ABS_NF(2, 1, HM)
+SPD_ABS_H(2)
+SPD_ABS_H(4)
+#undef SPD_ABS_H
+#undef SPD_ABS_NF
+#undef SPD_ABS_INST
 
 }  // namespace tgnk
 }  // namespace spd

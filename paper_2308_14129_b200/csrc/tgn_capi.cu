@@ -47,6 +47,7 @@ spd_status spd_tgn_epoch_steps(const spd_tgn_trainer* t, uint64_t* steps) {
 spd_status spd_tgn_begin_epoch(spd_tgn_trainer* t, int32_t epoch) {
     GUARD({ t->t->begin_epoch(epoch); });
 }
+spd_status spd_tgn_seek(spd_tgn_trainer* t, uint64_t step) { GUARD({ t->t->seek(step); }); }
 spd_status spd_tgn_step(spd_tgn_trainer* t, float* loss_out) { GUARD({ t->t->step(loss_out); }); }
 spd_status spd_tgn_end_epoch(spd_tgn_trainer* t) { GUARD({ t->t->end_epoch(); }); }
 spd_status spd_tgn_run_epoch(spd_tgn_trainer* t, int32_t epoch, double* mean_loss) {

@@ -50,23 +50,45 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
 
-// Time-encoder phase w*dt + b formed in f64 (dt reaches ~2e8 at GDELT shape,
-// beyond f32's 2^24) with explicitly rounded multiply-add (the oracle's f64
-// math), reduced modulo 2*pi in f64 (k*2pi error ~k*2.4e-16 <= 1e-8 rad), then
-// evaluated with f32 cos/sin on |r| <= pi: within ~2e-7 of the oracle's
-// f64 cos rounded to f32.
-__device__ __forceinline__ float reduced_phase(float w, float b, double dt) {
-    const double ph = __dadd_rn(__dmul_rn(static_cast<double>(w), dt), static_cast<double>(b));
-    constexpr double kTwoPi = 6.283185307179586476925286766559;
-    constexpr double kInvTwoPi = 0.15915494309189533576888376337251;
-    const double k = rint(ph * kInvTwoPi);
-    return static_cast<float>(fma(-k, kTwoPi, ph));
+// Time encoder cos/sin(w*dt + b). The phase is formed in f64 (dt reaches
+// ~2e8 at GDELT shape, beyond f32's 2^24) with explicitly rounded multiply and
+// add (the oracle's f64 math), reduced to |r| <= pi/4 by the nearest multiple
+// of pi/2 in f64 (two-term Cody-Waite, error ~q * 1e-32), and evaluated by
+// f64 Taylor polynomials on [-pi/4, pi/4] (truncation < 4e-13) with the
+// quadrant's sign/swap, then rounded to f32: the oracle's f64 cos rounded to
+// f32 except in rare near-tie cases, without a libm call. Returns (sin, cos).
+template <bool WANT_SIN = true>
+__device__ __forceinline__ float2 phase_sincos(double w, double b, double dt) {
+    const double ph = __dadd_rn(__dmul_rn(w, dt), b);
+    constexpr double kTwoOverPi = 0.63661977236758134307553505349006;
+    constexpr double kPiO2Hi = 1.5707963267948965580e+00;  // f64(pi/2)
+    constexpr double kPiO2Lo = 6.1232339957367658e-17;      // pi/2 - kPiO2Hi
+    const double q = rint(ph * kTwoOverPi);
+    const double x = fma(-q, kPiO2Lo, fma(-q, kPiO2Hi, ph));
+    const int quad = static_cast<int>(static_cast<long long>(q) & 3);
+    const double z = x * x;
+    // cos x = 1 - z/2! + z^2/4! - ... - z^7/14! ; sin x = x (1 - z/3! + ... + z^6/13!)
+    const double c = fma(fma(fma(fma(fma(fma(fma(-1.1470745597729725e-11, z, 2.08767569878681e-09), z,
+                                                 -2.755731922398589e-07), z, 2.48015873015873e-05), z,
+                                         -1.388888888888889e-03), z, 4.1666666666666664e-02), z, -0.5), z, 1.0);
+    double sn = 0.0;
+    if (WANT_SIN || (quad & 1))
+        sn = x * fma(fma(fma(fma(fma(fma(1.6059043836821613e-10, z, -2.505210838544172e-08), z,
+                                     2.7557319223985893e-06), z, -1.984126984126984e-04), z,
+                             8.333333333333333e-03), z, -1.6666666666666666e-01), z, 1.0);
+    const float fs = static_cast<float>(sn), fc = static_cast<float>(c);
+    switch (quad) {
+        case 0: return make_float2(fs, fc);
+        case 1: return make_float2(fc, -fs);
+        case 2: return make_float2(-fs, -fc);
+        default: return make_float2(-fc, fs);
+    }
 }
 __device__ __forceinline__ float time_cos(float w, float b, double dt) {
-    return cosf(reduced_phase(w, b, dt));
+    return phase_sincos<false>(static_cast<double>(w), static_cast<double>(b), dt).y;
 }
 __device__ __forceinline__ float time_sin(float w, float b, double dt) {
-    return sinf(reduced_phase(w, b, dt));
+    return phase_sincos(static_cast<double>(w), static_cast<double>(b), dt).x;
 }
 
 }  // namespace spd

@@ -59,16 +59,16 @@ __global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* roots,
                                const float* mem_new, float* q_in);
 // absorbed-projection attention (tgn_attn.cu): 4 roots per 128-thread block,
-// dynamic shared memory attn_smem_bytes(d); NCH = ceil(ld_p / 128),
-// NCX = ceil((D + T) / 128), HMAX >= H, K <= 16
-__host__ __device__ std::size_t attn_smem_bytes(const Dims& d);
+// dynamic shared memory attn_smem_bytes(d, bwd); lane slots per region
+// NM = ceil(D / 128), NT = ceil(T / 128), NF = ceil((F + 1) / 128); HMAX >= H
+__host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd);
 int attn_roots_per_block();
-template <int NCH, int HMAX>
+template <int NM, int NT, int NF, int HMAX>
 __global__ void k_attn_abs_fwd(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* nbr_node,
                                const std::uint32_t* nbr_ev, const double* nbr_dt, const int* cnt,
                                const float* mem_new, const float* Qp, float* alpha, float* xbar);
-template <int NCH, int NCX, int HMAX>
+template <int NM, int NT, int NF, int HMAX>
 __global__ void k_attn_abs_bwd(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* nbr_node,
                                const std::uint32_t* nbr_ev, const double* nbr_dt, const int* cnt,

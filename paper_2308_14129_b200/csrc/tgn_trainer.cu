@@ -193,69 +193,65 @@ void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, floa
     else gemm_wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s);
 }
 
-// Absorbed-projection attention kernels (tgn_attn.cu), instantiated for
-// chunk counts NCH = ceil(ld_p / 128), NCX = ceil((D + T) / 128) and H <= 2 or 4.
-template <class Kern>
-void attn_launch(Kern k, unsigned grid, std::size_t smem, cudaStream_t st,
-                 const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
-                 const float* tb, const Scratch& s, const float* rows_in, float* out,
-                 double* part) {
-    static std::size_t set = 0;  // per instantiation: opt in to > 48 KB shared memory
-    if (smem > set) {
+// Absorbed-projection attention kernels (tgn_attn.cu), instantiated for lane
+// slots NM, NT in {1, 2} (NM + NT <= 3), NF in {1, 2, 3} and H <= 2 or 4.
+template <class Kern, class... Args>
+void attn_launch(Kern k, std::size_t& set, unsigned grid, std::size_t smem, cudaStream_t st,
+                 Args&&... args) {
+    if (smem > set) {  // opt in to > 48 KB shared memory (once per kernel and size)
         SPD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        SPD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      int(cudaSharedmemCarveoutMaxShared)));
         set = smem;
     }
-    if constexpr (std::is_same_v<Kern, decltype(&tgnk::k_attn_abs_fwd<1, 2>)>)
-        launch(k, grid, 128, smem, st, wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p,
-               s.cnt.p, s.mem_new.p, rows_in, s.alpha.p, out);
+    launch(k, grid, 128, smem, st, std::forward<Args>(args)...);
+}
+
+template <int NM, int NT, int NF, int HM>
+void attn_pick(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& wd,
+               const tgnk::Dims& d, int R, const float* tw, const float* tb, const Scratch& s,
+               double* part) {
+    static std::size_t set_fwd = 0, set_bwd = 0;  // per kernel instantiation
+    if (!bwd)
+        attn_launch(&tgnk::k_attn_abs_fwd<NM, NT, NF, HM>, set_fwd, grid, tgnk::attn_smem_bytes(d, false), st,
+                    wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
+                    s.Qp.p, s.alpha.p, s.xbar.p);
     else
-        launch(k, grid, 128, smem, st, wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p,
-               s.cnt.p, s.mem_new.p, s.Qp.p, s.alpha.p, rows_in, out, s.dH.p, part);
+        attn_launch(&tgnk::k_attn_abs_bwd<NM, NT, NF, HM>, set_bwd, grid, tgnk::attn_smem_bytes(d, true), st,
+                    wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
+                    s.Qp.p, s.alpha.p, s.dxbar.p, s.dQp.p, s.dH.p, part);
+}
+
+void attn_dispatch(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& wd,
+                   const tgnk::Dims& d, int R, const float* tw, const float* tb, const Scratch& s,
+                   double* part) {
+    const int nm = (d.D + 127) / 128, nt = (d.T + 127) / 128, nf = (d.F + 1 + 127) / 128;
+    const int key = (nm * 3 + nt) * 4 + nf;
+#define SPD_A(NM, NT, NF)                                                                       \
+    case (NM * 3 + NT) * 4 + NF:                                                                \
+        if (d.H <= 2) attn_pick<NM, NT, NF, 2>(bwd, grid, st, wd, d, R, tw, tb, s, part);        \
+        else attn_pick<NM, NT, NF, 4>(bwd, grid, st, wd, d, R, tw, tb, s, part);                 \
+        break;
+    switch (key) {
+        SPD_A(1, 1, 1) SPD_A(1, 1, 2) SPD_A(1, 1, 3)
+        SPD_A(1, 2, 1) SPD_A(1, 2, 2) SPD_A(1, 2, 3)
+        SPD_A(2, 1, 1) SPD_A(2, 1, 2) SPD_A(2, 1, 3)
+        default: internal_error("InvalidParams", "attention row outside the instantiated shapes");
+    }
+#undef SPD_A
 }
 
 void attn_abs_fwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
                   const float* tb, const Scratch& s, cudaStream_t st) {
-    const int nch = (d.ld_p / 4 + 31) / 32;
     const int rpb = tgnk::attn_roots_per_block();
-    const unsigned grid = unsigned((R + rpb - 1) / rpb);
-    const std::size_t smem = tgnk::attn_smem_bytes(d);
-#define SPD_F(NCH, HM) attn_launch(&tgnk::k_attn_abs_fwd<NCH, HM>, grid, smem, st, wd, d, R, tw, tb, s, \
-                                   s.Qp.p, s.xbar.p, nullptr)
-#define SPD_FK(NCH) if (d.H <= 2) SPD_F(NCH, 2); else SPD_F(NCH, 4)
-    switch (nch) {
-        case 1: SPD_FK(1); break;
-        case 2: SPD_FK(2); break;
-        case 3: SPD_FK(3); break;
-        case 4: SPD_FK(4); break;
-        default: internal_error("InvalidParams", "attention row too wide");
-    }
-#undef SPD_FK
-#undef SPD_F
+    attn_dispatch(false, unsigned((R + rpb - 1) / rpb), st, wd, d, R, tw, tb, s, nullptr);
 }
 
 void attn_abs_bwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
                   const float* tb, const Scratch& s, double* part, cudaStream_t st) {
-    const int nch = (d.ld_p / 4 + 31) / 32;
-    const int ncx = ((d.D + d.T) / 4 + 31) / 32;
     // every block of the partial region writes (zeros past R): the final
     // reduction covers the region sized for the largest batch
-    const unsigned grid = unsigned(s.tattn_blocks);
-    const std::size_t smem = tgnk::attn_smem_bytes(d);
-#define SPD_B(NCH, NCX, HM) attn_launch(&tgnk::k_attn_abs_bwd<NCH, NCX, HM>, grid, smem, st, wd, d, R, \
-                                        tw, tb, s, s.dxbar.p, s.dQp.p, part)
-#define SPD_BK(NCH, NCX) if (d.H <= 2) SPD_B(NCH, NCX, 2); else SPD_B(NCH, NCX, 4)
-    switch (nch * 4 + ncx) {
-        case 1 * 4 + 1: SPD_BK(1, 1); break;
-        case 2 * 4 + 1: SPD_BK(2, 1); break;
-        case 2 * 4 + 2: SPD_BK(2, 2); break;
-        case 3 * 4 + 1: SPD_BK(3, 1); break;
-        case 3 * 4 + 2: SPD_BK(3, 2); break;
-        case 4 * 4 + 1: SPD_BK(4, 1); break;
-        case 4 * 4 + 2: SPD_BK(4, 2); break;
-        default: internal_error("InvalidParams", "attention row too wide");
-    }
-#undef SPD_BK
-#undef SPD_B
+    attn_dispatch(true, unsigned(s.tattn_blocks), st, wd, d, R, tw, tb, s, part);
 }
 
 tgnk::WorkerDev devview(Worker& w) {
@@ -308,8 +304,8 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         data_error("InvalidParams", "n_neighbors must lie in [1, 16]");
     if (cfg.n_heads > 4 || ((cfg.d_mem + cfg.d_time) / cfg.n_heads) % 4)
         data_error("InvalidParams", "n_heads must be <= 4 with a head width that is a multiple of 4");
-    if (cfg.d_mem + cfg.d_time > 256 || ld_aug(cfg.d_mem + cfg.d_time + cfg.d_edge) > 512)
-        data_error("InvalidParams", "need d_mem + d_time <= 256 and d_mem + d_time + d_edge < 512");
+    if (cfg.d_mem + cfg.d_time > 256 || cfg.d_edge + 1 > 384)
+        data_error("InvalidParams", "need d_mem + d_time <= 256 and d_edge < 384");
     if (cfg.batch_size < 1) data_error("InvalidParams", "need batch_size >= 1");
     if (world < 1 || rank < 0 || rank >= world) data_error("InvalidParams", "bad rank/world");
     require_device(device);
@@ -454,6 +450,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.Q.alloc(std::size_t(R) * d.ld_Q);
     const std::size_t hp = std::size_t(R) * d.H * d.ld_p;  // per-root, per-head rows
     s.Qp.alloc(hp); s.xbar.alloc(hp); s.dxbar.alloc(hp); s.dQp.alloc(hp);
+    s.Qp.zero(stream_); s.xbar.zero(stream_); s.dxbar.zero(stream_); s.dQp.zero(stream_);
     s.alpha.alloc(std::size_t(R) * d.H * d.K);
     s.ctx.alloc(std::size_t(R) * d.ld_ctx); init_aug(s.ctx, R, d.DQ, d.ld_ctx, stream_);
     s.O.alloc(std::size_t(R) * d.DQ);
@@ -549,6 +546,23 @@ void TGNTrainer::begin_epoch(int epoch) {
             w.loops = 1;
         }
     }
+}
+
+void TGNTrainer::seek(std::uint64_t step) {
+    DeviceGuard g(device_);
+    if (step >= epoch_steps_) usage_error("seek past the end of the epoch");
+    step_in_epoch_ = step;
+    for (auto& wp : workers_) {
+        Worker& w = *wp;
+        if (w.batches == 0) continue;
+        w.pos = step % w.batches;
+        w.loops = step / w.batches;
+        w.done = w.loops > 0;
+        w.mem.zero(stream_);
+        w.lu.zero(stream_);
+        w.nU.zero(stream_);
+    }
+    SPD_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train) {

@@ -69,7 +69,7 @@ def test_tgn_config_validation_is_data_error():
     assert ei.value.code == "InvalidParams"
     # shapes outside the attention kernels' register tiling are rejected up front
     for bad in (dict(n_neighbors=17), dict(n_heads=8, d_mem=16, d_time=16),
-                dict(d_mem=200, d_time=100), dict(d_mem=100, d_time=100, d_edge=400)):
+                dict(d_mem=200, d_time=100), dict(d_mem=100, d_time=100, d_edge=384)):
         kw = dict(d_mem=8, d_time=8, d_edge=4, batch_size=16)
         kw.update(bad)
         with pytest.raises(sp.DataError) as ei:

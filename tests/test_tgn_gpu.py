@@ -198,3 +198,19 @@ def test_model_shapes_match_oracle(dims):
         if step == 0:
             assert rel_err(tr.grads(), o.grad.numpy()) < TOL_GRAD
     assert rel_err(tr.params(), o.flat.numpy()) < TOL_TRAJ
+
+
+def test_seek_positions_schedule_mid_epoch():
+    _, _, pa, subs = partitioned(parts=2)
+    cfg = small_cfg()
+    tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+    tr.begin_epoch(0)
+    mid = tr.epoch_steps() // 2
+    tr.seek(mid)
+    for w in range(2):
+        nb = -(-len(subs[w].edges) // cfg.batch_size)
+        assert tr.next_batch(w)[0] == (mid % nb) * cfg.batch_size
+    loss = tr.step()
+    assert np.all(np.isfinite(loss))
+    with pytest.raises(sp.UsageError):
+        tr.seek(tr.epoch_steps())

@@ -3,7 +3,7 @@
 K=${1:-k_attn_abs}
 N=${2:-2}
 OUT=${3:-gpurun_out/full}
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:$K -c $N -o /tmp/ncu_full \
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:$K -c $N -f -o /tmp/ncu_full \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 ${BENCH_ARGS} \
   > gpurun_out/ncu_full_bench.json 2> gpurun_out/ncu_full_bench.err
 ncu -i /tmp/ncu_full.ncu-rep --page details > ${OUT}_details.txt
