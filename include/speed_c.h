@@ -319,6 +319,9 @@ spd_status spd_tgn_last_step(const spd_tgn_trainer* t, int32_t worker, uint64_t*
  * (spd_tgn_kernel_times); both add synchronisation, off by default. */
 spd_status spd_tgn_set_debug(spd_tgn_trainer* t, int32_t on);
 spd_status spd_tgn_set_profile(spd_tgn_trainer* t, int32_t on);
+/* Regular steps (every local worker on a full batch) replay a captured CUDA
+ * graph of the step; on by default, off = launch every kernel eagerly. */
+spd_status spd_tgn_set_graph(spd_tgn_trainer* t, int32_t on);
 /* Per-phase times (ms, CUDA events on the trainer's stream) of the last step. */
 spd_status spd_tgn_kernel_times(const spd_tgn_trainer* t, float* ms, int32_t* n_kernels,
                                 char* names, int32_t name_stride, int32_t cap);

@@ -771,6 +771,10 @@ class TGNTrainer:
     def set_debug(self, on: bool = True):
         _check(lib.spd_tgn_set_debug(self._h, int(on)))
 
+    def set_graph(self, on: bool):
+        """Replay regular steps as a captured CUDA graph (default on)."""
+        _check(lib.spd_tgn_set_graph(self._h, int(on)))
+
     def set_profile(self, on: bool = True):
         _check(lib.spd_tgn_set_profile(self._h, int(on)))
 

@@ -65,6 +65,8 @@ struct Worker {
     DevBuf<std::uint32_t> pU, pOther, pEv;  // pending set (<= 2B)
     DevBuf<double> pTs;
     DevBuf<std::int32_t> nU;         // device-resident |pending|
+    DevBuf<std::uint64_t> ctl;       // per-step control: batch start, negative base
+    std::uint64_t ctl_host[2] = {0, 0};
     std::vector<std::uint32_t> shared_local;  // local row of each shared node (or UINT32_MAX)
     // schedule
     std::uint64_t batches = 0, pos = 0, loops = 0;
@@ -134,12 +136,17 @@ public:
     int feat_stride() const;
     void set_debug(bool on) { debug_ = on; }
     void set_profile(bool on) { profile_ = on; }
+    void set_graph(bool on) { use_graph_ = on; }
     int device() const { return device_; }
     cudaStream_t stream() const { return stream_; }
 
 private:
-    void worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t lo, int B,
-                     std::uint64_t nb, bool train, int slot_idx);
+    void worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx);
+    // host -> device per-step control words (pageable async copy: staged at
+    // call time, applied in stream order, so graph replays see fresh values)
+    void set_ctl(Worker& w, std::uint64_t lo, std::uint64_t nb);
+    void step_body(const std::vector<int>& Bs);  // worker steps + all-reduce + Adam (capturable)
+    void adam_prepare();
     void backward(Worker& w, const tgnk::WorkerDev& wd, int B);
     void worker_post(Worker& w);
     void flush_pending(Worker& w);
@@ -168,6 +175,13 @@ private:
     std::vector<NodeId> shared_;
     DevBuf<float> params_, grads_, adam_m_, adam_v_;
     DevBuf<float> params_tc_;  // tf32-rounded copy read by the tensor-core GEMMs
+    DevBuf<float> adam_bc_;    // Adam bias corrections of the current step (device)
+    float adam_bc_host_[2] = {1.f, 1.f};
+    // CUDA graph of the regular step (every local worker on a full batch)
+    cudaGraphExec_t graph_exec_ = nullptr;
+    std::uint64_t graph_kernels_ = 0;
+    bool use_graph_ = true;
+    std::uint64_t eager_full_steps_ = 0;
     void refresh_tc_weights();
     DevBuf<double> tgrad_;  // f64 accumulators for the time encoder grads (2T)
     std::unique_ptr<Scratch> s_;

@@ -90,6 +90,7 @@ spd_status spd_tgn_set_memory(spd_tgn_trainer* t, int32_t worker, const float* m
     GUARD({ t->t->set_memory(worker, mem, last_update); });
 }
 spd_status spd_tgn_set_debug(spd_tgn_trainer* t, int32_t on) { GUARD({ t->t->set_debug(on != 0); }); }
+spd_status spd_tgn_set_graph(spd_tgn_trainer* t, int32_t on) { GUARD({ t->t->set_graph(on != 0); }); }
 spd_status spd_tgn_set_profile(spd_tgn_trainer* t, int32_t on) {
     GUARD({ t->t->set_profile(on != 0); });
 }

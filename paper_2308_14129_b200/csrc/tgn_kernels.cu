@@ -33,11 +33,12 @@ __global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
 
 // K5 + K8: roots (src | dst | neg) and the recent-k neighbours strictly
 // before t: lower_bound on the node's time-sorted adjacency, last K entries.
-__global__ void k_roots_nbrs(WorkerDev w, std::uint64_t lo, int B, std::uint64_t neg_base, int K,
+__global__ void k_roots_nbrs(WorkerDev w, int B, int K,
                              std::uint32_t* roots, double* root_t, std::uint32_t* nbr_node,
                              std::uint32_t* nbr_ev, double* nbr_dt, int* cnt) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= 3 * B) return;
+    const std::uint64_t lo = w.ctl[0], neg_base = w.ctl[1];
     const int which = r / B, i = r % B;
     const std::uint64_t e = lo + i;
     const double t = w.ev_ts[e];
@@ -307,10 +308,11 @@ __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* sav
 }
 
 __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
-                       float lr, float b1, float one_m_b1, float b2, float one_m_b2, float bc1,
-                       float bc2, float eps, float* p_tc) {
+                       float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
+                       float eps, float* p_tc) {
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    const float bc1 = bc[0], bc2 = bc[1];  // bias corrections of this step (host-written)
     const float gi = g[i] / scale;
     const float mi = b1 * m[i] + one_m_b1 * gi;
     const float vi = b2 * v[i] + one_m_b2 * gi * gi;
@@ -343,7 +345,8 @@ __global__ void k_persist(WorkerDev w, int D, const float* mem_new) {
 // K3 last-message selection: endpoint slots q = 2k (src), 2k+1 (dst) of the
 // batch's events; per node the max slot wins (max (ts, stream index)),
 // compacted in slot order. Single block; lastpos starts and ends at -1.
-__global__ void k_pending(WorkerDev w, std::uint64_t lo, int B) {
+__global__ void k_pending(WorkerDev w, int B) {
+    const std::uint64_t lo = w.ctl[0];
     __shared__ int warp_tot[32];
     __shared__ int base;
     const int nslots = 2 * B;

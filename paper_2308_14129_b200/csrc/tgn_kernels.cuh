@@ -44,11 +44,15 @@ struct WorkerDev {
     std::uint32_t* pEv;
     double* pTs;
     std::int32_t* nU;
+    // per-step control written by the host before each step (stream-ordered,
+    // so a captured CUDA graph replays with fresh values): [0] first event of
+    // the batch, [1] negative-sampling base (oracle: negatives())
+    const std::uint64_t* ctl;
 };
 
 // --- kernels (definitions in tgn_kernels.cu) -------------------------------
 __global__ void k_init_aug(float* buf, int rows, int cols, int ld);
-__global__ void k_roots_nbrs(WorkerDev w, std::uint64_t lo, int B, std::uint64_t neg_base, int K,
+__global__ void k_roots_nbrs(WorkerDev w, int B, int K,
                              std::uint32_t* roots, double* root_t, std::uint32_t* nbr_node,
                              std::uint32_t* nbr_ev, double* nbr_dt, int* cnt);
 __global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const float* time_b,
@@ -90,11 +94,11 @@ __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb
 __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* save, const float* h,
                           float* dGi, float* dGh);
 __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
-                       float lr, float b1, float one_m_b1, float b2, float one_m_b2, float bc1,
-                       float bc2, float eps, float* p_tc);
+                       float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
+                       float eps, float* p_tc);
 __global__ void k_round_tf32(const float* src, float* dst, std::size_t n);
 __global__ void k_persist(WorkerDev w, int D, const float* mem_new);
-__global__ void k_pending(WorkerDev w, std::uint64_t lo, int B);
+__global__ void k_pending(WorkerDev w, int B);
 __global__ void k_gen_features(__nv_bfloat16* feat, const std::uint64_t* eids, std::uint64_t E,
                                int F, int Fp, std::uint64_t seed_mixed);
 __global__ void k_gather_rows(const float* src, int ld, const std::uint32_t* idx,

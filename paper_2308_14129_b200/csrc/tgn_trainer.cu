@@ -261,6 +261,7 @@ tgnk::WorkerDev devview(Worker& w) {
     v.pool = w.pool.p; v.n_pool = w.n_pool; v.mem = w.mem.p; v.lu = w.lu.p; v.slot = w.slot.p;
     v.lastpos = w.lastpos.p; v.pU = w.pU.p; v.pOther = w.pOther.p; v.pEv = w.pEv.p; v.pTs = w.pTs.p;
     v.nU = w.nU.p;
+    v.ctl = w.ctl.p;
     return v;
 }
 
@@ -403,6 +404,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
         w.pU.alloc(2 * B); w.pOther.alloc(2 * B); w.pEv.alloc(2 * B); w.pTs.alloc(2 * B);
         w.nU.alloc(1); w.nU.zero(stream_);
+        w.ctl.alloc(2); w.ctl.zero(stream_);
         for (NodeId sidx : shared_) {
             auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), sidx);
             w.shared_local.push_back(it != w.nodes.end() && *it == sidx
@@ -419,6 +421,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     init_params_host(lay_, cfg.seed_init, flat);
     params_.alloc(lay_.total); params_.upload(flat.data(), lay_.total, stream_);
     params_tc_.alloc(lay_.total);
+    adam_bc_.alloc(2);
     refresh_tc_weights();
     grads_.alloc(lay_.total); grads_.zero(stream_);
     adam_m_.alloc(lay_.total); adam_m_.zero(stream_);
@@ -497,6 +500,7 @@ void TGNTrainer::join_side() {
 }
 
 TGNTrainer::~TGNTrainer() {
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     if (stage_) cudaFreeHost(stage_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
@@ -586,8 +590,8 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train) {
 // One batch of one worker: events [lo, lo+B) of the view's event list.
 // train: forward + backward (weight grads accumulate into grads_) + post;
 // eval (train = false): forward + post (scores in s.logits), no gradients.
-void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t lo, int B,
-                             std::uint64_t nb, bool train, int slot_idx) {
+void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train,
+                             int slot_idx) {
     Scratch& s = *s_;
     const auto& d = s.d;
     w.last_b = B;
@@ -597,13 +601,8 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t
     cudaStream_t st = stream_;
     const bool tc = cfg_.gemm_mode == 1;  // tensor cores for GRU + attention projections only
     const float* PW = tc ? params_tc_.p : params_.p;
-    if (train && w.pos == 0) {  // loop_start: reset (pac_sim.cpp:238)
-        w.mem.zero(st);
-        w.lu.zero(st);
-        w.nU.zero(st);
-    }
     timed("roots_nbrs", [&] {
-        launch(tgnk::k_roots_nbrs, blocks_for(R, 128), 128, 0, st, wd, lo, B, nb, d.K, s.roots.p,
+        launch(tgnk::k_roots_nbrs, blocks_for(R, 128), 128, 0, st, wd, B, d.K, s.roots.p,
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     });
     timed("gru_fwd", [&] { gru_forward(w, wd, train); });
@@ -652,7 +651,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, std::uint64_t
     // while the scratch still holds this worker's rows (K11, K3)
     timed("post", [&] {
         launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
-        launch(tgnk::k_pending, 1, 1024, 0, st, wd, lo, B);
+        launch(tgnk::k_pending, 1, 1024, 0, st, wd, B);
     });
 }
 
@@ -868,32 +867,40 @@ void TGNTrainer::allreduce_grads() {
     }
 }
 
-void TGNTrainer::adam() {
+void TGNTrainer::adam_prepare() {
     ++adam_t_;
+    adam_bc_host_[0] = static_cast<float>(1.0 - std::pow(double(cfg_.beta1), double(adam_t_)));
+    adam_bc_host_[1] = static_cast<float>(1.0 - std::pow(double(cfg_.beta2), double(adam_t_)));
+    SPD_CUDA(cudaMemcpyAsync(adam_bc_.p, adam_bc_host_, sizeof(adam_bc_host_), cudaMemcpyHostToDevice,
+                             stream_));
+}
+
+void TGNTrainer::adam() {
     const double b1 = cfg_.beta1, b2 = cfg_.beta2;
-    const float bc1 = static_cast<float>(1.0 - std::pow(b1, double(adam_t_)));
-    const float bc2 = static_cast<float>(1.0 - std::pow(b2, double(adam_t_)));
-    launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, stream_, 
+    launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, stream_,
         params_.p, grads_.p, adam_m_.p, adam_v_.p, lay_.total, float(total_workers_), cfg_.lr,
-        cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2), bc1,
-        bc2, cfg_.adam_eps, cfg_.gemm_mode == 1 ? params_tc_.p : nullptr);
+        cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2),
+        static_cast<const float*>(adam_bc_.p), cfg_.adam_eps,
+        cfg_.gemm_mode == 1 ? params_tc_.p : nullptr);
     SPD_CUDA(cudaGetLastError());
 }
 
-void TGNTrainer::step(float* loss_out) {
-    DeviceGuard g(device_);
-    ++step_in_epoch_;
-    times_.ms.clear();
+void TGNTrainer::set_ctl(Worker& w, std::uint64_t lo, std::uint64_t nb) {
+    w.ctl_host[0] = lo;
+    w.ctl_host[1] = nb;
+    SPD_CUDA(cudaMemcpyAsync(w.ctl.p, w.ctl_host, sizeof(w.ctl_host), cudaMemcpyHostToDevice, stream_));
+}
+
+// Everything a global step launches once the per-step control words are on
+// the device: the local workers' batches, the gradient all-reduce and Adam.
+// Bs[k] = batch size of local worker k (0: idle). Capturable as a CUDA graph.
+void TGNTrainer::step_body(const std::vector<int>& Bs) {
     grads_.zero(stream_);
     tgrad_.zero(stream_);
     for (std::size_t k = 0; k < workers_.size(); ++k) {
         Worker& w = *workers_[k];
-        if (w.batches == 0) continue;
-        const std::uint64_t lo = w.pos * cfg_.batch_size;
-        const int B = static_cast<int>(std::min<std::uint64_t>(w.E, lo + cfg_.batch_size) - lo);
-        const std::uint64_t nb = neg_base(cfg_.seed_neg, std::uint64_t(epoch_), std::uint64_t(w.gid),
-                                          step_in_epoch_);
-        worker_step(w, devview(w), lo, B, nb, true, static_cast<int>(k));
+        if (Bs[k] == 0) continue;
+        worker_step(w, devview(w), Bs[k], true, static_cast<int>(k));
         if (debug_) {  // taps before the next worker reuses the scratch
             const std::uint64_t B = w.last_b;
             const int D = lay_.D, K = lay_.Kn;
@@ -910,6 +917,51 @@ void TGNTrainer::step(float* loss_out) {
     }
     timed("allreduce", [&] { allreduce_grads(); });
     timed("adam", [&] { adam(); });
+}
+
+void TGNTrainer::step(float* loss_out) {
+    DeviceGuard g(device_);
+    ++step_in_epoch_;
+    times_.ms.clear();
+    std::vector<int> Bs(workers_.size(), 0);
+    bool full = true;
+    for (std::size_t k = 0; k < workers_.size(); ++k) {
+        Worker& w = *workers_[k];
+        if (w.batches == 0) continue;
+        const std::uint64_t lo = w.pos * cfg_.batch_size;
+        Bs[k] = static_cast<int>(std::min<std::uint64_t>(w.E, lo + cfg_.batch_size) - lo);
+        full = full && Bs[k] == static_cast<int>(cfg_.batch_size);
+        if (w.pos == 0) {  // loop_start: reset (pac_sim.cpp:238)
+            w.mem.zero(stream_);
+            w.lu.zero(stream_);
+            w.nU.zero(stream_);
+        }
+        set_ctl(w, lo, neg_base(cfg_.seed_neg, std::uint64_t(epoch_), std::uint64_t(w.gid),
+                                step_in_epoch_));
+    }
+    adam_prepare();
+    // capture only after one eager full step (lazy attribute setup done)
+    const bool graph_ok = use_graph_ && full && !profile_ && !debug_ && eager_full_steps_ > 0;
+    if (!graph_ok && full) ++eager_full_steps_;
+    if (graph_ok) {
+        // regular step: replay the captured graph (launch-free, fork/join of
+        // the side stream preserved); capture it on first use
+        if (!graph_exec_) {
+            const std::uint64_t k0 = kernel_launches();
+            cudaGraph_t graph;
+            SPD_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+            step_body(Bs);
+            SPD_CUDA(cudaStreamEndCapture(stream_, &graph));
+            SPD_CUDA(cudaGraphInstantiate(&graph_exec_, graph, 0));
+            SPD_CUDA(cudaGraphDestroy(graph));
+            graph_kernels_ = kernel_launches() - k0;
+            g_kernel_launches.fetch_sub(graph_kernels_, std::memory_order_relaxed);
+        }
+        SPD_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+        g_kernel_launches.fetch_add(graph_kernels_, std::memory_order_relaxed);
+    } else {
+        step_body(Bs);
+    }
     for (auto& wp : workers_)
         if (wp->batches > 0) worker_post(*wp);
     if (loss_out) {
@@ -1256,8 +1308,8 @@ void TGNTrainer::evaluate(int wid, std::uint64_t lo, std::uint64_t hi, std::uint
     std::vector<float> lg;
     for (std::uint64_t b0 = lo; b0 < hi; b0 += cfg_.batch_size) {
         const int B = static_cast<int>(std::min<std::uint64_t>(hi, b0 + cfg_.batch_size) - b0);
-        const std::uint64_t nb = neg_base(neg_seed, 0xE7A1ull, std::uint64_t(w.gid), b0);
-        worker_step(w, v, w.E + b0, B, nb, false, slot_idx);
+        set_ctl(w, w.E + b0, neg_base(neg_seed, 0xE7A1ull, std::uint64_t(w.gid), b0));
+        worker_step(w, v, B, false, slot_idx);
         lg.resize(2 * B);
         s_->logits.download(lg.data(), 2 * B, stream_);
         SPD_CUDA(cudaStreamSynchronize(stream_));

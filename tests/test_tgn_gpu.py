@@ -214,3 +214,23 @@ def test_seek_positions_schedule_mid_epoch():
     assert np.all(np.isfinite(loss))
     with pytest.raises(sp.UsageError):
         tr.seek(tr.epoch_steps())
+
+
+@pytest.mark.parametrize("gemm_mode", [0, 1])
+def test_graph_replay_matches_eager(gemm_mode):
+    """Regular steps replay a captured CUDA graph; the per-step control words
+    (batch start, negative base, Adam corrections) live on the device, so the
+    replayed trajectory equals the eagerly launched one (up to float-atomic
+    ordering in the memory-gradient scatter)."""
+    _, _, pa, subs = partitioned(parts=2, nodes=200, edges=3000)
+    cfg = small_cfg(batch_size=50, gemm_mode=gemm_mode)
+    out = []
+    for graph in (False, True):
+        tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+        tr.set_graph(graph)
+        losses = [tr.run_epoch(ep) for ep in range(2)]
+        out.append((np.array(losses), tr.params(), tr.memory(0)[0], tr.memory(1)[1]))
+    (l0, p0, m0, u0), (l1, p1, m1, u1) = out
+    assert np.allclose(l0, l1, rtol=1e-3), (l0, l1)
+    assert rel_err(p1, p0) < TOL_TRAJ and rel_err(m1, m0) < TOL_TRAJ
+    assert np.array_equal(u0, u1)
