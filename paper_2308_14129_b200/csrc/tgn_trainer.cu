@@ -173,24 +173,31 @@ void gemm_wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, in
 }
 
 // Tensor-core-eligible layers (GRU, attention projections) dispatch on
-// spd_tgn_config::gemm_mode: 0 = FP32 FFMA, 1 = tcgen05 TF32.
+// spd_tgn_config::gemm_mode: 0 = FP32 FFMA, 1 = tcgen05 TF32. A Batch runs
+// per-head GEMMs as one launch on the tensor-core path (FFMA: one per head).
 void proj_fwd(bool tc, const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M,
               int N, int K, const int* M_dev, cudaStream_t s, int epi = 0,
-              const float* mask = nullptr, int ldmask = 0, int rnd = 0) {
-    if (tc) umma::fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask, rnd);
-    else gemm_fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
+              const float* mask = nullptr, int ldmask = 0, int rnd = 0, const umma::Batch& bt = {}) {
+    if (tc) return umma::fwd(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask, rnd, bt);
+    for (int z = 0; z < bt.n; ++z)
+        gemm_fwd(A + z * bt.a, lda, B + z * bt.b, ldb, C + z * bt.c, ldc, M, N, K, M_dev, s, epi, mask,
+                 ldmask);
 }
 void proj_dgrad(bool tc, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
                 int M, int N, int K, const int* M_dev, cudaStream_t s, int epi = 0,
-                const float* mask = nullptr, int ldmask = 0, int rnd = 0) {
-    if (tc) umma::dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask, rnd);
-    else gemm_dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask);
+                const float* mask = nullptr, int ldmask = 0, int rnd = 0, const umma::Batch& bt = {}) {
+    if (tc) return umma::dgrad(A, lda, B, ldb, C, ldc, M, N, K, M_dev, s, epi, mask, ldmask, rnd, bt);
+    for (int z = 0; z < bt.n; ++z)
+        gemm_dgrad(A + z * bt.a, lda, B + z * bt.b, ldb, C + z * bt.c, ldc, M, N, K, M_dev, s, epi,
+                   mask, ldmask);
 }
 void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw,
                 int N_out, int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
-                cudaStream_t s) {
-    if (tc) umma::wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s);
-    else gemm_wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s);
+                cudaStream_t s, const umma::Batch& bt = {}) {
+    if (tc) return umma::wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s, bt);
+    for (int z = 0; z < bt.n; ++z)
+        gemm_wgrad(dY + z * bt.a, ldy, X + z * bt.b, ldx, dW + z * bt.c, ldw, N_out, K_in, rows,
+                   rows_dev, ws, ws_cap, s);
 }
 
 // Absorbed-projection attention kernels (tgn_attn.cu), instantiated for lane
@@ -620,14 +627,15 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     const float* WK = PW + lay_.att_kv.off;
     const float* WV = WK + std::size_t(d.DQ) * lay_.att_kv.ld;
     const int ldw = lay_.att_kv.ld;
-    timed("attn_fwd", [&] {
-        for (int h = 0; h < d.H; ++h)
-            proj_dgrad(tc, s.Q.p + h * dh, d.ld_Q, WK + std::size_t(h) * dh * ldw, ldw,
-                       s.Qp.p + std::size_t(h) * d.ld_p, ldhp, R, d.DK + 1, dh, nullptr, st);
-        attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st);
-        for (int h = 0; h < d.H; ++h)
-            proj_fwd(tc, s.xbar.p + std::size_t(h) * d.ld_p, ldhp, WV + std::size_t(h) * dh * ldw, ldw,
-                     s.ctx.p + h * dh, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0, nullptr, 0, tc);
+    const std::ptrdiff_t wst = std::ptrdiff_t(dh) * ldw;  // per-head weight slab
+    timed("gemm_qp", [&] {
+        proj_dgrad(tc, s.Q.p, d.ld_Q, WK, ldw, s.Qp.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0, nullptr,
+                   0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
+    });
+    timed("k_attn_abs_fwd", [&] { attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st); });
+    timed("gemm_ctx", [&] {
+        proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
+                 nullptr, 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
     });
     timed("head_fwd", [&] {
         proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
@@ -699,29 +707,28 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     float* GK = G + lay_.att_kv.off;
     float* GV = GK + std::size_t(d.DQ) * ldw;
     s.dH.zero(st);
-    timed("attn_bwd", [&] {
-        for (int h = 0; h < d.H; ++h) {
-            // dW_V,h += dctx_h^T xbar_h ; dxbar_h = dctx_h [W_V,h | b_V,h]
-            side([&](cudaStream_t sd) {
-                proj_wgrad(tc, s.dctx.p + h * dh, d.ld_Q, s.xbar.p + std::size_t(h) * d.ld_p, ldhp,
-                           GV + std::size_t(h) * dh * ldw, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
-                           s.ws.n, sd);
-            });
-            proj_dgrad(tc, s.dctx.p + h * dh, d.ld_Q, WV + std::size_t(h) * dh * ldw, ldw,
-                       s.dxbar.p + std::size_t(h) * d.ld_p, ldhp, R, d.DK + 1, dh, nullptr, st);
-        }
+    const std::ptrdiff_t wst = std::ptrdiff_t(dh) * ldw;  // per-head weight slab
+    timed("gemm_dxbar", [&] {
+        // dW_V,h += dctx_h^T xbar_h ; dxbar_h = dctx_h [W_V,h | b_V,h]
+        side([&](cudaStream_t sd) {
+            proj_wgrad(tc, s.dctx.p, d.ld_Q, s.xbar.p, ldhp, GV, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
+                       s.ws.n, sd, umma::Batch{d.H, dh, d.ld_p, wst});
+        });
+        proj_dgrad(tc, s.dctx.p, d.ld_Q, WV, ldw, s.dxbar.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0,
+                   nullptr, 0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
+    });
+    timed("k_attn_abs_bwd", [&] {
         attn_abs_bwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s,
                      s.tpart.p + std::size_t(s.troot_blocks) * 2 * d.T, st);
-        for (int h = 0; h < d.H; ++h) {
-            // dW_K,h += Q_h^T dQp_h ; dQ_h = dQp_h [W_K,h | b_K,h]^T
-            side([&](cudaStream_t sd) {
-                proj_wgrad(tc, s.Q.p + h * dh, d.ld_Q, s.dQp.p + std::size_t(h) * d.ld_p, ldhp,
-                           GK + std::size_t(h) * dh * ldw, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
-                           s.ws.n, sd);
-            });
-            proj_fwd(tc, s.dQp.p + std::size_t(h) * d.ld_p, ldhp, WK + std::size_t(h) * dh * ldw, ldw,
-                     s.dQ.p + h * dh, d.ld_Q, R, dh, d.DK + 1, nullptr, st, 0, nullptr, 0, tc);
-        }
+    });
+    timed("gemm_dq", [&] {
+        // dW_K,h += Q_h^T dQp_h ; dQ_h = dQp_h [W_K,h | b_K,h]^T
+        side([&](cudaStream_t sd) {
+            proj_wgrad(tc, s.Q.p, d.ld_Q, s.dQp.p, ldhp, GK, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
+                       s.ws.n, sd, umma::Batch{d.H, dh, d.ld_p, wst});
+        });
+        proj_fwd(tc, s.dQp.p, ldhp, WK, ldw, s.dQ.p, d.ld_Q, R, dh, d.DK + 1, nullptr, st, 0, nullptr,
+                 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
     });
     timed("q_bwd", [&] {
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,

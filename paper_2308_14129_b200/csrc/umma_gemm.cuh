@@ -48,9 +48,19 @@ struct Args {
     int epi;
     const float* mask;
     int ldmask;
-    float* ws;  // PARTIAL: [k_split][M][ldws]
+    float* ws;  // PARTIAL: [batch][k_split][M][ldws]
     int ldws;
     int rnd;    // STORE: round outputs to tf32 (they feed another tensor-core GEMM)
+    // batched GEMMs (blockIdx.z = batch * k_split + split): C of batch b at
+    // C + b * c_bstride; operands through maps.a[b] / maps.b[b]
+    int batch;
+    long long c_bstride;
+};
+
+constexpr int kMaxBatch = 4;
+struct Maps {
+    CUtensorMap a[kMaxBatch];
+    CUtensorMap b[kMaxBatch];
 };
 
 __device__ __forceinline__ float tf32_rn(float x) {
@@ -160,8 +170,7 @@ struct Cfg {
 
 template <bool A_MN, bool B_MN, int BN, int NSUB, int CL>
 __global__ void __launch_bounds__(THREADS, 1)
-    umma_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                     const __grid_constant__ CUtensorMap tmB, Args args) {
+    umma_gemm_kernel(const __grid_constant__ Maps maps, Args args) {
     using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;
     constexpr int NST = C_::STAGES_;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -178,6 +187,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     int K = args.K;
     if (args.K_dev) K = min(K, *args.K_dev);
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * C_::NT;
+    const int bz = args.k_split > 1 ? blockIdx.z / args.k_split : blockIdx.z;  // batch index
+    const int sz = args.k_split > 1 ? blockIdx.z % args.k_split : 0;          // split index
+    const CUtensorMap* tmA = &maps.a[bz];
+    const CUtensorMap* tmB = &maps.b[bz];
     // a lone CTA past the rows can leave; cluster members must stay to serve
     // their share of the multicast B tiles
     if (CL == 1 && m0 >= M) return;
@@ -185,7 +198,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int k_begin = 0, k_end = K;
     if (args.k_split > 1) {
         const int per = ((K + args.k_split - 1) / args.k_split + BK - 1) / BK * BK;
-        k_begin = blockIdx.z * per;
+        k_begin = sz * per;
         k_end = min(K, k_begin + per);
     }
     const int n_k = k_end > k_begin ? (k_end - k_begin + BK - 1) / BK : 0;
@@ -220,10 +233,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_expect_tx(full + s, C_::STAGE_BYTES);
                 const int kc = k_begin + kb * BK;
                 if (!A_MN) {
-                    tma_load_2d(a_s, &tmA, full + s, kc, m0);
+                    tma_load_2d(a_s, tmA, full + s, kc, m0);
                 } else {
 #pragma unroll
-                    for (int j = 0; j < BM / 32; ++j) tma_load_2d(a_s + j * 32 * 128, &tmA, full + s, m0 + 32 * j, kc);
+                    for (int j = 0; j < BM / 32; ++j) tma_load_2d(a_s + j * 32 * 128, tmA, full + s, m0 + 32 * j, kc);
                 }
 #pragma unroll
                 for (int j = 0; j < C_::B_BOXES; ++j) {
@@ -231,8 +244,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                     unsigned char* dst = B_MN ? b_s + j * 32 * 128 : b_s + j * C_::KROWS * 128;
                     const int c0 = B_MN ? n0 + 32 * j : kc;
                     const int c1 = B_MN ? kc : n0 + j * C_::KROWS;
-                    if (CL > 1) tma_load_2d_mc(dst, &tmB, full + s, c0, c1, (1u << CL) - 1);
-                    else tma_load_2d(dst, &tmB, full + s, c0, c1);
+                    if (CL > 1) tma_load_2d_mc(dst, tmB, full + s, c0, c1, (1u << CL) - 1);
+                    else tma_load_2d(dst, tmB, full + s, c0, c1);
                 }
             }
         }
@@ -297,7 +310,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             asm volatile("tcgen05.fence::after_thread_sync;");
         }
         const bool partial = args.mode == PARTIAL;
-        float* out_base = partial ? args.ws + (std::size_t)blockIdx.z * args.M * args.ldws : args.C;
+        float* const C = args.C + bz * args.c_bstride;
+        float* const ws_b = partial ? args.ws + (std::size_t)bz * args.k_split * args.M * args.ldws : nullptr;
+        float* out_base = partial ? ws_b + (std::size_t)sz * args.M * args.ldws : C;
         const int ldo = partial ? args.ldws : args.ldc;
 #pragma unroll 1
         for (int c0 = 0; c0 < C_::NT; c0 += 32) {

@@ -54,8 +54,33 @@ CUtensorMap make_map(const float* base, std::uint64_t inner, std::uint64_t rows,
     return m;
 }
 
+// Fixed-order sum of the split-K partials [batch][split][M][ldws] into the
+// batch's dW (accumulate): deterministic, one launch for every batch.
+__global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, int ldws,
+                                float* __restrict__ C, int ldc, long long c_bstride, int batch) {
+    const std::size_t idx = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (std::size_t)batch * M * N) return;
+    const int b = static_cast<int>(idx / ((std::size_t)M * N));
+    const int e = static_cast<int>(idx % ((std::size_t)M * N));
+    const int m = e / N, n = e % N;
+    const float* w = ws + (std::size_t)b * splits * M * ldws + (std::size_t)m * ldws + n;
+    float acc = 0.f;
+#pragma unroll 8
+    for (int z = 0; z < splits; ++z) acc += w[(std::size_t)z * M * ldws];
+    float* c = C + b * c_bstride + (std::size_t)m * ldc + n;
+    *c = *c + acc;
+}
+
+void reduce(const float* ws, int split, int M, int N, int ldws, float* C, int ldc, const Batch& bt,
+            cudaStream_t s) {
+    const std::size_t n = std::size_t(bt.n) * M * N;
+    k_splitk_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(ws, split, M, N, ldws, C, ldc, bt.c, bt.n);
+    g_launch_counter.fetch_add(1, std::memory_order_relaxed);
+    SPD_CUDA(cudaGetLastError());
+}
+
 template <bool A_MN, bool B_MN, int BN, int NSUB = 1, int CL = 1>
-void run(const CUtensorMap& a, const CUtensorMap& b, const Args& args, dim3 grid, cudaStream_t s) {
+void run(const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
     using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;
     auto kern = umma_gemm_kernel<A_MN, B_MN, BN, NSUB, CL>;
     static std::once_flag once;
@@ -63,7 +88,7 @@ void run(const CUtensorMap& a, const CUtensorMap& b, const Args& args, dim3 grid
         SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
     });
     if (CL == 1) {
-        kern<<<grid, THREADS, C_::SMEM, s>>>(a, b, args);
+        kern<<<grid, THREADS, C_::SMEM, s>>>(maps, args);
     } else {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = grid;
@@ -77,20 +102,19 @@ void run(const CUtensorMap& a, const CUtensorMap& b, const Args& args, dim3 grid
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, a, b, args));
+        SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, args));
     }
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
 }
 
 template <bool A_MN, bool B_MN>
-void dispatch(int bn, const CUtensorMap& a, const CUtensorMap& b, const Args& args, dim3 grid,
-              cudaStream_t s) {
+void dispatch(int bn, const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
     switch (bn) {
-        case 64: run<A_MN, B_MN, 64>(a, b, args, grid, s); break;
-        case 128: run<A_MN, B_MN, 128>(a, b, args, grid, s); break;
-        case 224: run<A_MN, B_MN, 224>(a, b, args, grid, s); break;
-        case 256: run<A_MN, B_MN, 256>(a, b, args, grid, s); break;
+        case 64: run<A_MN, B_MN, 64>(maps, args, grid, s); break;
+        case 128: run<A_MN, B_MN, 128>(maps, args, grid, s); break;
+        case 224: run<A_MN, B_MN, 224>(maps, args, grid, s); break;
+        case 256: run<A_MN, B_MN, 256>(maps, args, grid, s); break;
         default: internal_error("InvalidParams", "unsupported tile width");
     }
 }
@@ -111,95 +135,103 @@ int pick_bn(int N) {
     return best;
 }
 
+void check_batch(const Batch& b) {
+    if (b.n < 1 || b.n > kMaxBatch) internal_error("InvalidParams", "GEMM batch outside [1, 4]");
+}
+
 }  // namespace
 
 std::uint64_t launches() { return g_launch_counter.load(); }
 
 void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N, int K,
-         const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask, int rnd) {
+         const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask, int rnd,
+         const Batch& bt) {
     if (!M || !N) return;
+    check_batch(bt);
     Args a{};
     a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
     a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask; a.rnd = rnd;
+    a.batch = bt.n; a.c_bstride = bt.c;
     const int mt = (M + BM - 1) / BM;
-    if (mt >= 64 && N > 256 && N <= 416 && !M_dev) {
+    Maps maps{};
+    if (mt >= 64 && N > 256 && N <= 416 && !M_dev && bt.n == 1) {
         // one CTA covers all N (2 x 208 in TMEM): A streamed once; W multicast
         // to CTA pairs: W streamed from L2 once per 256 rows
-        const CUtensorMap ta = make_map(A, K, M, lda, BM);
-        const CUtensorMap tb = make_map(W, K, N, ldw, 104);
-        run<false, false, 208, 2, 4>(ta, tb, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
+        maps.a[0] = make_map(A, K, M, lda, BM);
+        maps.b[0] = make_map(W, K, N, ldw, 104);
+        run<false, false, 208, 2, 4>(maps, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
         return;
     }
     const int bn = pick_bn(N);
-    const CUtensorMap ta = make_map(A, K, M, lda, BM);
-    const CUtensorMap tb = make_map(W, K, N, ldw, bn);
-    dispatch<false, false>(bn, ta, tb, a, dim3((N + bn - 1) / bn, mt, 1), s);
+    for (int z = 0; z < bt.n; ++z) {
+        maps.a[z] = make_map(A + z * bt.a, K, M, lda, BM);
+        maps.b[z] = make_map(W + z * bt.b, K, N, ldw, bn);
+    }
+    dispatch<false, false>(bn, maps, a, dim3((N + bn - 1) / bn, mt, bt.n), s);
 }
 
 void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N,
-           int K, const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask, int rnd) {
+           int K, const int* M_dev, cudaStream_t s, int epi, const float* mask, int ldmask, int rnd,
+           const Batch& bt) {
     if (!M || !N) return;
-    const CUtensorMap ta = make_map(A, K, M, lda, BM);
-    const CUtensorMap tb = make_map(W, N, K, ldw, BK, true);  // W [K x N], N contiguous
+    check_batch(bt);
+    Maps maps{};
     Args a{};
     a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
     a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask; a.rnd = rnd;
+    a.batch = bt.n; a.c_bstride = bt.c;
     const int mt = (M + BM - 1) / BM;
-    if (mt >= 64 && N <= 224 && !M_dev) {  // big: W multicast to CTA pairs
-        run<false, true, 224, 1, 4>(ta, tb, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
+    if (mt >= 64 && N <= 224 && !M_dev && bt.n == 1) {  // big: W multicast to CTA pairs
+        maps.a[0] = make_map(A, K, M, lda, BM);
+        maps.b[0] = make_map(W, N, K, ldw, BK, true);
+        run<false, true, 224, 1, 4>(maps, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
         return;
     }
     const int bn = pick_bn(N);  // multiple of 32: whole MN-major column blocks
-    dispatch<false, true>(bn, ta, tb, a, dim3((N + bn - 1) / bn, mt, 1), s);
+    for (int z = 0; z < bt.n; ++z) {
+        maps.a[z] = make_map(A + z * bt.a, K, M, lda, BM);
+        maps.b[z] = make_map(W + z * bt.b, N, K, ldw, BK, true);  // W [K x N], N contiguous
+    }
+    dispatch<false, true>(bn, maps, a, dim3((N + bn - 1) / bn, mt, bt.n), s);
 }
 
 void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
            int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
-           cudaStream_t s) {
+           cudaStream_t s, const Batch& bt) {
     if (!rows || !N_out || !K_in) return;
+    check_batch(bt);
     const int mt = (N_out + BM - 1) / BM;
-    if (rows >= 16384 && K_in > 224 && K_in <= 448 && mt >= 2 && mt <= 4 && !rows_dev) {
+    const int ldws = (K_in + 3) / 4 * 4;
+    Maps maps{};
+    Args a{};
+    a.C = dW; a.ldc = ldw; a.M = N_out; a.N = K_in; a.K = rows; a.K_dev = rows_dev;
+    a.epi = EPI_NONE; a.ws = ws; a.ldws = ldws; a.batch = bt.n; a.c_bstride = bt.c;
+    if (rows >= 16384 && K_in > 224 && K_in <= 448 && mt >= 2 && mt <= 4 && !rows_dev && bt.n == 1) {
         // all M tiles of dW in one cluster: X (the B operand) streamed once,
         // each 128-row slice of dY^T once; K_in covered by 2 x 224 in TMEM
-        const int ldws = (K_in + 3) / 4 * 4;
         int split = std::max(1, std::min(rows / (8 * BK), 148 / 4));
         while (split > 1 && std::size_t(split) * N_out * ldws > ws_cap) --split;
-        const CUtensorMap ta = make_map(dY, N_out, rows, ldy, BK, true);
-        const CUtensorMap tb = make_map(X, K_in, rows, ldx, BK, true);
-        Args a{};
-        a.C = dW; a.ldc = ldw; a.M = N_out; a.N = K_in; a.K = rows; a.K_dev = rows_dev;
-        a.k_split = split; a.mode = split > 1 ? PARTIAL : ACCUM; a.epi = EPI_NONE;
-        a.ws = ws; a.ldws = ldws;
-        if (mt <= 2) run<true, true, 224, 2, 2>(ta, tb, a, dim3(1, 2, split), s);
-        else run<true, true, 224, 2, 4>(ta, tb, a, dim3(1, 4, split), s);
-        if (split > 1) {
-            const std::size_t n = std::size_t(N_out) * K_in;
-            gemm::splitk_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(ws, split, N_out, K_in,
-                                                                          ldws, dW, ldw, 1.f);
-            g_launch_counter.fetch_add(1, std::memory_order_relaxed);
-            SPD_CUDA(cudaGetLastError());
-        }
+        maps.a[0] = make_map(dY, N_out, rows, ldy, BK, true);
+        maps.b[0] = make_map(X, K_in, rows, ldx, BK, true);
+        a.k_split = split; a.mode = split > 1 ? PARTIAL : ACCUM;
+        const int cl = mt <= 2 ? 2 : 4;
+        if (cl == 2) run<true, true, 224, 2, 2>(maps, a, dim3(1, 2, split), s);
+        else run<true, true, 224, 2, 4>(maps, a, dim3(1, 4, split), s);
+        if (split > 1) reduce(ws, split, N_out, K_in, ldws, dW, ldw, bt, s);
         return;
     }
     const int bn = K_in <= 64 ? 64 : (K_in <= 128 ? 128 : 224);
-    const int tiles = ((N_out + BM - 1) / BM) * ((K_in + bn - 1) / bn);
-    const int ldws = (K_in + 3) / 4 * 4;
+    const int tiles = ((N_out + BM - 1) / BM) * ((K_in + bn - 1) / bn) * bt.n;
     int split = std::max(1, std::min(rows / (4 * BK), (148 + tiles - 1) / tiles));
-    while (split > 1 && std::size_t(split) * N_out * ldws > ws_cap) --split;
-    const CUtensorMap ta = make_map(dY, N_out, rows, ldy, BK, true);  // dY [rows x N_out]
-    const CUtensorMap tb = make_map(X, K_in, rows, ldx, BK, true);    // X  [rows x K_in]
-    Args a{};
-    a.C = dW; a.ldc = ldw; a.M = N_out; a.N = K_in; a.K = rows; a.K_dev = rows_dev;
-    a.k_split = split; a.mode = split > 1 ? PARTIAL : ACCUM; a.epi = EPI_NONE;
-    a.ws = ws; a.ldws = ldws;
-    dispatch<true, true>(bn, ta, tb, a, dim3((K_in + bn - 1) / bn, (N_out + BM - 1) / BM, split), s);
-    if (split > 1) {
-        const std::size_t n = std::size_t(N_out) * K_in;
-        gemm::splitk_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(ws, split, N_out, K_in, ldws,
-                                                                      dW, ldw, 1.f);
-        g_launch_counter.fetch_add(1, std::memory_order_relaxed);
-        SPD_CUDA(cudaGetLastError());
+    while (split > 1 && std::size_t(split) * bt.n * N_out * ldws > ws_cap) --split;
+    for (int z = 0; z < bt.n; ++z) {
+        maps.a[z] = make_map(dY + z * bt.a, N_out, rows, ldy, BK, true);  // dY [rows x N_out]
+        maps.b[z] = make_map(X + z * bt.b, K_in, rows, ldx, BK, true);    // X  [rows x K_in]
     }
+    a.k_split = split; a.mode = split > 1 ? PARTIAL : ACCUM;
+    dispatch<true, true>(bn, maps, a,
+                         dim3((K_in + bn - 1) / bn, (N_out + BM - 1) / BM, split * bt.n), s);
+    if (split > 1) reduce(ws, split, N_out, K_in, ldws, dW, ldw, bt, s);
 }
 
 }  // namespace umma

@@ -11,14 +11,22 @@
 namespace spd {
 namespace umma {
 
+// Batched launch over heads: operand z at A + z*a, W + z*b, output at C + z*c
+// (elements); n <= 4. Weight-gradient batches offset dY, X and dW the same way.
+struct Batch {
+    int n = 1;
+    std::ptrdiff_t a = 0, b = 0, c = 0;
+};
+
 void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N, int K,
          const int* M_dev, cudaStream_t s, int epi = 0, const float* mask = nullptr,
-         int ldmask = 0, int rnd = 0);
+         int ldmask = 0, int rnd = 0, const Batch& bt = {});
 void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N,
            int K, const int* M_dev, cudaStream_t s, int epi = 0, const float* mask = nullptr,
-           int ldmask = 0, int rnd = 0);
+           int ldmask = 0, int rnd = 0, const Batch& bt = {});
 void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
-           int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap, cudaStream_t s);
+           int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap, cudaStream_t s,
+           const Batch& bt = {});
 std::uint64_t launches();
 
 }  // namespace umma
