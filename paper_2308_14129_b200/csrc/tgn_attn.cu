@@ -148,13 +148,17 @@ __device__ __forceinline__ int vidx(int lane) {
 
 // Stage root r's neighbour rows (warp-cooperative). Lane j < c_n holds
 // neighbour j's (dt, slot) on return, for the caller's scatters. TPL >= T/32.
+// Time encoding: the forward evaluates cos and sin of the f64 phase once per
+// occurrence and also stores them to phi[r][j] = [cos T | sin T] (f32); the
+// backward (with_sin) stages them from there by cp.async instead of
+// re-evaluating (the kernels are instruction-bound, HBM is not).
 template <int TPL>
 __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, int r, int c_n,
                                            int lane, const float* time_w, const float* time_b,
                                            const std::uint32_t* nbr_node,
                                            const std::uint32_t* nbr_ev, const double* nbr_dt,
                                            const float* mem_new, unsigned char* xs, bool with_sin,
-                                           double& m_dt, int& m_slot) {
+                                           float* phi, double& m_dt, int& m_slot) {
     std::uint32_t ev = 0, node = 0;
     m_dt = 0.0;
     m_slot = -1;
@@ -166,41 +170,48 @@ __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, in
         m_slot = w.slot[node];
     }
     const int RB = row_bytes(d, with_sin);
-    const int mch = d.D / 4, fch = d.Fp / 8;  // 16-B chunks of the memory / feature rows
+    const int mch = d.D / 4, fch = d.Fp / 8, tch = with_sin ? d.T / 4 : 0;  // 16-B chunks
+    float* phir = phi + (std::size_t)r * d.K * 2 * d.T;
     for (int j = 0; j < c_n; ++j) {
         const std::uint32_t nj = __shfl_sync(0xffffffffu, node, j);
         const std::uint32_t e = __shfl_sync(0xffffffffu, ev, j);
         const int slot = __shfl_sync(0xffffffffu, m_slot, j);
         const float* mrow = slot >= 0 ? mem_new + (std::size_t)slot * d.D : w.mem + (std::size_t)nj * d.D;
         const __nv_bfloat16* frow = w.feat + (std::size_t)e * d.Fp;
+        const float* prow = phir + (std::size_t)j * 2 * d.T;
         unsigned char* dst = xs + (std::size_t)j * RB;
-        for (int c = lane; c < mch + fch; c += 32) {
+        for (int c = lane; c < mch + fch + 2 * tch; c += 32) {
             if (c < mch) cp_async16_ca(dst + 16 * c, mrow + 4 * c);
-            else cp_async16_cg(dst + 4 * (d.D + d.T) + 16 * (c - mch), frow + 8 * (c - mch));
+            else if (c < mch + fch) cp_async16_cg(dst + 4 * (d.D + d.T) + 16 * (c - mch), frow + 8 * (c - mch));
+            else if (c < mch + fch + tch) cp_async16_cg(dst + 4 * d.D + 16 * (c - mch - fch), prow + 4 * (c - mch - fch));
+            else cp_async16_cg(dst + 4 * (d.D + d.T) + 2 * d.Fp + 16 * (c - mch - fch - tch),
+                               prow + d.T + 4 * (c - mch - fch - tch));
         }
     }
-    // phi(dt) = cos(w dt + b) (and sin for the backward), phase in f64;
-    // this lane's time columns t = lane + 32k (k < TPL) and their parameters
-    double tw[TPL], tb[TPL];
-#pragma unroll
-    for (int k = 0; k < TPL; ++k) {
-        const int t = lane + 32 * k;
-        tw[k] = t < d.T ? static_cast<double>(time_w[t]) : 0.0;
-        tb[k] = t < d.T ? static_cast<double>(time_b[t]) : 0.0;
-    }
-#pragma unroll 1
-    for (int j = 0; j < c_n; ++j) {
-        const double dt = __shfl_sync(0xffffffffu, m_dt, j);
-        float* cs = reinterpret_cast<float*>(xs + (std::size_t)j * RB) + d.D;
-        float* sn = reinterpret_cast<float*>(xs + (std::size_t)j * RB + 4 * (d.D + d.T) + 2 * d.Fp);
+    if (!with_sin) {
+        // phi(dt) = cos(w dt + b), phase in f64; this lane's time columns
+        // t = lane + 32k (k < TPL) and their parameters
+        double tw[TPL], tb[TPL];
 #pragma unroll
         for (int k = 0; k < TPL; ++k) {
             const int t = lane + 32 * k;
-            if (t < d.T) {
-                const float2 sc2 = with_sin ? phase_sincos<true>(tw[k], tb[k], dt)
-                                            : phase_sincos<false>(tw[k], tb[k], dt);
-                cs[t] = sc2.y;
-                if (with_sin) sn[t] = sc2.x;
+            tw[k] = t < d.T ? static_cast<double>(time_w[t]) : 0.0;
+            tb[k] = t < d.T ? static_cast<double>(time_b[t]) : 0.0;
+        }
+#pragma unroll 1
+        for (int j = 0; j < c_n; ++j) {
+            const double dt = __shfl_sync(0xffffffffu, m_dt, j);
+            float* cs = reinterpret_cast<float*>(xs + (std::size_t)j * RB) + d.D;
+            float* pg = phir + (std::size_t)j * 2 * d.T;
+#pragma unroll
+            for (int k = 0; k < TPL; ++k) {
+                const int t = lane + 32 * k;
+                if (t < d.T) {
+                    const float2 sc2 = phase_sincos<true>(tw[k], tb[k], dt);
+                    cs[t] = sc2.y;
+                    pg[t] = sc2.y;
+                    pg[d.T + t] = sc2.x;
+                }
             }
         }
     }
@@ -302,7 +313,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
                                                       const std::uint32_t* nbr_ev,
                                                       const double* nbr_dt, const int* cnt,
                                                       const float* mem_new, const float* Qp,
-                                                      float* alpha, float* xbar) {
+                                                      float* alpha, float* xbar, float* phi) {
     using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -328,7 +339,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     double m_dt;
     int m_slot;
     stage_rows<4 * NT>(w, d, r, c_n, lane, time_w, time_b, nbr_node, nbr_ev, nbr_dt, mem_new, xs,
-                       false, m_dt, m_slot);
+                       false, phi, m_dt, m_slot);
     load_slots<S, HMAX>(v, Qp + row0, d, lane);
     const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
     dots<S, HMAX>(v, d, lane, xs, RB, c_n, sc, inv);
@@ -373,7 +384,8 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
                                                       const double* nbr_dt, const int* cnt,
                                                       const float* mem_new, const float* Qp,
                                                       const float* alpha, const float* dxbar,
-                                                      float* dQp, float* dH, double* part) {
+                                                      const float* phi, float* dQp, float* dH,
+                                                      double* part) {
     using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -400,7 +412,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
         double m_dt;
         int m_slot;
         stage_rows<4 * NT>(w, d, r, c_n, lane, time_w, time_b, nbr_node, nbr_ev, nbr_dt, mem_new, xs,
-                           true, m_dt, m_slot);
+                           true, const_cast<float*>(phi), m_dt, m_slot);
         if (lane < d.K)
             for (int h = 0; h < d.H; ++h)
                 aa[h * d.K + lane] = lane < c_n ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
@@ -498,11 +510,11 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     template __global__ void k_attn_abs_fwd<NM, NT, NF, HM>(                                     \
         WorkerDev, Dims, int, const float*, const float*, const std::uint32_t*,                  \
         const std::uint32_t*, const double*, const int*, const float*, const float*, float*,     \
-        float*);                                                                                \
+        float*, float*);                                                                        \
     template __global__ void k_attn_abs_bwd<NM, NT, NF, HM>(                                     \
         WorkerDev, Dims, int, const float*, const float*, const std::uint32_t*,                  \
         const std::uint32_t*, const double*, const int*, const float*, const float*,             \
-        const float*, const float*, float*, float*, double*);
+        const float*, const float*, const float*, float*, float*, double*);
 #define SPD_ABS_NF(NM, NT, HM) \
     SPD_ABS_INST(NM, NT, 1, HM) SPD_ABS_INST(NM, NT, 2, HM) SPD_ABS_INST(NM, NT, 3, HM)
 #define SPD_ABS_H(HM) SPD_ABS_NF(1, 1, HM) SPD_ABS_NF(1, 2, HM) SPD_ABS_NF(2, 1, HM)

@@ -32,11 +32,14 @@ __global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
 }
 
 // K5 + K8: roots (src | dst | neg) and the recent-k neighbours strictly
-// before t: lower_bound on the node's time-sorted adjacency, last K entries.
+// before t: lower_bound of t in the node's time-sorted adjacency, last K
+// entries. One warp per root: a 33-ary search (32 lanes probe, a ballot
+// narrows the range 33x per round: 4 dependent rounds for a 10^6-entry hub
+// instead of 20 for a binary search), then lanes copy the K neighbours.
 __global__ void k_roots_nbrs(WorkerDev w, int B, int K,
                              std::uint32_t* roots, double* root_t, std::uint32_t* nbr_node,
                              std::uint32_t* nbr_ev, double* nbr_dt, int* cnt) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = warp_id_global(), lane = lane_id();
     if (r >= 3 * B) return;
     const std::uint64_t lo = w.ctl[0], neg_base = w.ctl[1];
     const int which = r / B, i = r % B;
@@ -46,23 +49,32 @@ __global__ void k_roots_nbrs(WorkerDev w, int B, int K,
     if (which == 0) node = w.ev_src[e];
     else if (which == 1) node = w.ev_dst[e];
     else node = w.pool[mix64(neg_base ^ (std::uint64_t)i) % w.n_pool];
-    roots[r] = node;
-    root_t[r] = t;
     const std::uint64_t a = w.adj_off[node], b = w.adj_off[node + 1];
-    std::uint64_t l = a, h = b;
-    while (l < h) {
-        const std::uint64_t mid = (l + h) >> 1;
-        if (w.adj_ts[mid] < t) l = mid + 1;
-        else h = mid;
+    std::uint64_t l = a, h = b;  // answer (first index with ts >= t) lies in [l, h]
+    while (h - l > 32) {
+        const std::uint64_t step = (h - l + 32) / 33;
+        const std::uint64_t p = l + (std::uint64_t)(lane + 1) * step;
+        const bool below = p < h && w.adj_ts[p] < t;
+        const int c = __popc(__ballot_sync(0xffffffffu, below));  // probes below t: a prefix
+        const std::uint64_t nl = l + (std::uint64_t)c * step + (c > 0 ? 1 : 0);
+        h = min(h, l + (std::uint64_t)(c + 1) * step);
+        l = nl;
     }
-    const std::uint64_t avail = l - a;
+    const std::uint64_t p = l + lane;
+    const bool below = p < h && w.adj_ts[p] < t;
+    const std::uint64_t pos = l + __popc(__ballot_sync(0xffffffffu, below));
+    const std::uint64_t avail = pos - a;
     const int c = avail < (std::uint64_t)K ? (int)avail : K;
-    const std::uint64_t start = l - c;
-    cnt[r] = c;
-    for (int j = 0; j < K; ++j) {
-        const std::size_t o = (std::size_t)r * K + j;
-        if (j < c) {
-            const std::uint64_t idx = start + j;
+    const std::uint64_t start = pos - c;
+    if (lane == 0) {
+        roots[r] = node;
+        root_t[r] = t;
+        cnt[r] = c;
+    }
+    if (lane < K) {
+        const std::size_t o = (std::size_t)r * K + lane;
+        if (lane < c) {
+            const std::uint64_t idx = start + lane;
             nbr_node[o] = w.adj_nbr[idx];
             nbr_ev[o] = w.adj_ev[idx];
             nbr_dt[o] = t - w.adj_ts[idx];
@@ -351,10 +363,17 @@ __global__ void k_pending(WorkerDev w, int B) {
     __shared__ int base;
     const int nslots = 2 * B;
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int q = tid; q < nslots; q += nt) {
-        const std::uint64_t e = lo + (q >> 1);
-        const std::uint32_t node = (q & 1) ? w.ev_dst[e] : w.ev_src[e];
-        atomicMax(w.lastpos + node, q);
+    for (int q0 = 0; q0 < nslots; q0 += nt) {
+        const int q = q0 + tid;
+        std::uint32_t node = 0xFFFFFFFFu;
+        if (q < nslots) {
+            const std::uint64_t e = lo + (q >> 1);
+            node = (q & 1) ? w.ev_dst[e] : w.ev_src[e];
+        }
+        // hubs repeat within a warp's 16 events: only the highest lane of each
+        // equal-node group touches the contended counter
+        const unsigned grp = __match_any_sync(0xffffffffu, node);
+        if (q < nslots && (tid & 31) == 31 - __clz(grp)) atomicMax(w.lastpos + node, q);
     }
     if (tid == 0) base = 0;
     __syncthreads();

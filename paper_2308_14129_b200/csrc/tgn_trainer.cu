@@ -89,6 +89,7 @@ struct Scratch {
     DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dxbar, dQp, dQ, dq_in;
     DevBuf<float> ws;
     DevBuf<double> tpart;
+    DevBuf<float> phi;  // [R][K][cos T | sin T] of the neighbour occurrences (fwd -> bwd)
     DevBuf<float> loss;  // per local worker
     int trows = 0, troot_blocks = 0, tattn_blocks = 0;  // time-grad partial blocks
 };
@@ -222,11 +223,12 @@ void attn_pick(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& 
     if (!bwd)
         attn_launch(&tgnk::k_attn_abs_fwd<NM, NT, NF, HM>, set_fwd, grid, tgnk::attn_smem_bytes(d, false), st,
                     wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
-                    s.Qp.p, s.alpha.p, s.xbar.p);
+                    s.Qp.p, s.alpha.p, s.xbar.p, s.phi.p);
     else
         attn_launch(&tgnk::k_attn_abs_bwd<NM, NT, NF, HM>, set_bwd, grid, tgnk::attn_smem_bytes(d, true), st,
                     wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
-                    s.Qp.p, s.alpha.p, s.dxbar.p, s.dQp.p, s.dH.p, part);
+                    s.Qp.p, s.alpha.p, s.dxbar.p, static_cast<const float*>(s.phi.p), s.dQp.p, s.dH.p,
+                    part);
 }
 
 void attn_dispatch(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& wd,
@@ -450,6 +452,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     const int R = s.R, RK = s.RK, U = s.U;
     s.roots.alloc(R); s.root_t.alloc(R); s.cnt.alloc(R);
     s.nbr_node.alloc(RK); s.nbr_ev.alloc(RK); s.nbr_dt.alloc(RK);
+    s.phi.alloc(std::size_t(RK) * 2 * d.T);
     s.x_gru.alloc(std::size_t(U) * d.ld_x); init_aug(s.x_gru, U, d.DM, d.ld_x, stream_);
     s.h_gru.alloc(std::size_t(U) * d.ld_h); init_aug(s.h_gru, U, D, d.ld_h, stream_);
     s.Gi.alloc(std::size_t(U) * d.ld_g); s.Gh.alloc(std::size_t(U) * d.ld_g);
@@ -476,7 +479,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.dm_in.alloc(std::size_t(R) * d.ld_m); s.dctx.alloc(std::size_t(R) * d.ld_Q);
     s.dQ.alloc(std::size_t(R) * d.ld_Q); s.dq_in.alloc(std::size_t(R) * d.ld_q);
     s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
-    s.trows = 64;
+    s.trows = 16;
     s.troot_blocks = (R + s.trows - 1) / s.trows;
     s.tattn_blocks = (R + tgnk::attn_roots_per_block() - 1) / tgnk::attn_roots_per_block();
     s.tpart.alloc(std::size_t(s.troot_blocks + s.tattn_blocks) * 2 * d.T);
@@ -609,7 +612,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     const bool tc = cfg_.gemm_mode == 1;  // tensor cores for GRU + attention projections only
     const float* PW = tc ? params_tc_.p : params_.p;
     timed("roots_nbrs", [&] {
-        launch(tgnk::k_roots_nbrs, blocks_for(R, 128), 128, 0, st, wd, B, d.K, s.roots.p,
+        launch(tgnk::k_roots_nbrs, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, B, d.K, s.roots.p,
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     });
     timed("gru_fwd", [&] { gru_forward(w, wd, train); });
