@@ -222,7 +222,9 @@ void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw
     }
     const int bn = K_in <= 64 ? 64 : (K_in <= 128 ? 128 : 224);
     const int tiles = ((N_out + BM - 1) / BM) * ((K_in + bn - 1) / bn) * bt.n;
-    int split = std::max(1, std::min(rows / (4 * BK), (148 + tiles - 1) / tiles));
+    // ~64 CTAs: enough K-parallelism for these small outputs without a split-K
+    // partial traffic (split x |dW|) that the reduce then has to stream back
+    int split = std::max(1, std::min(rows / (4 * BK), (64 + tiles - 1) / tiles));
     while (split > 1 && std::size_t(split) * bt.n * N_out * ldws > ws_cap) --split;
     for (int z = 0; z < bt.n; ++z) {
         maps.a[z] = make_map(dY + z * bt.a, N_out, rows, ldy, BK, true);  // dY [rows x N_out]
