@@ -51,6 +51,24 @@ def bytes_per_edge(D, T, F, K):
     return fwd + 12 * K * (D + F)
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes per launch) of `kernel`
+    from the newest committed ncu --set full raw export under profiles/."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{kernel}_raw.csv")))
+    if not files:
+        return None, None
+    rows = list(csv.reader(open(files[-1])))
+    h, units = rows[0], rows[1]
+    total = 0.0
+    for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = h.index(name)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1)
+        total += float(rows[2][i].replace(",", "")) * scale
+    return total, os.path.relpath(files[-1], ROOT)
+
+
 def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -344,6 +362,8 @@ def main():
     if dom[1] > 0:
         roof["achieved"] = (occ_bytes + root_bytes) / (dom[1] / 1e3) / 1e9
         roof["frac"] = roof["achieved"] / hbm_peak
+    # measured DRAM traffic of the same kernel: the committed ncu --set full capture
+    roof["traffic"], roof["traffic_source"] = ncu_traffic("k_attn_abs_bwd")
     bpe = bytes_per_edge(D, T, F, K)
     step_roof = {"bytes_per_edge": bpe, "achieved_gbs_per_gpu": value / world * bpe / 1e9,
                  "frac_of_hbm": value / world * bpe / 1e9 / hbm_peak,
