@@ -19,6 +19,7 @@
 // register-staged double buffering through shared memory.
 #pragma once
 
+#include "pdl.cuh"
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -51,6 +52,7 @@ struct Args {
 // A_KMAJOR: A stored [K x M] (weight-grad orientation). B_KN: B stored [K x N].
 template <bool A_KMAJOR, bool B_KN, int BM>
 __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
+    pdl_entry();
     constexpr int TM = BM / 16;       // rows per thread
     constexpr int AV = BM * BK / 4 / NT;  // float4 A loads per thread (2 or 1)
     __shared__ __align__(16) float As[2][BK][BM + 4];
@@ -205,6 +207,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
 // Fixed-order reduction of split-K partials into C (deterministic).
 static __global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, int ldw,
                                      float* __restrict__ C, int ldc, float beta) {
+    pdl_entry();
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)M * N) return;
     const int m = idx / N, n = idx % N;

@@ -22,6 +22,7 @@
 // 4(lane + 32i), the next NT slots time columns, the last NF slots feature
 // columns including the constant-1 bias column at F. Every slot of a warp is
 // in one region, so the inner loops are branch-free (compile-time region).
+#include "pdl.cuh"
 #include "tgn_common.cuh"
 #include "tgn_kernels.cuh"
 
@@ -314,6 +315,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
                                                       const double* nbr_dt, const int* cnt,
                                                       const float* mem_new, const float* Qp,
                                                       float* alpha, float* xbar, float* phi) {
+    pdl_entry();
     using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -386,6 +388,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
                                                       const float* alpha, const float* dxbar,
                                                       const float* phi, float* dQp, float* dH,
                                                       double* part) {
+    pdl_entry();
     using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

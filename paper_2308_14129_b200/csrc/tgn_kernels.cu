@@ -1,5 +1,6 @@
 // Non-GEMM kernels of the TGN training step; see tgn_kernels.cuh. Semantics
 // follow oracle/tgn_oracle.py line for line (which states the model choices).
+#include "pdl.cuh"
 #include "tgn_common.cuh"
 #include "tgn_kernels.cuh"
 
@@ -24,6 +25,7 @@ __device__ __forceinline__ float softplusf(float x) { return x > 20.f ? x : log1
 }  // namespace
 
 __global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
+    pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (std::size_t)rows * ld) return;
     const int c = i % ld;
@@ -39,6 +41,7 @@ __global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
 __global__ void k_roots_nbrs(WorkerDev w, int B, int K,
                              std::uint32_t* roots, double* root_t, std::uint32_t* nbr_node,
                              std::uint32_t* nbr_ev, double* nbr_dt, int* cnt) {
+    pdl_entry();
     const int r = warp_id_global(), lane = lane_id();
     if (r >= 3 * B) return;
     const std::uint64_t lo = w.ctl[0], neg_base = w.ctl[1];
@@ -90,6 +93,7 @@ __global__ void k_roots_nbrs(WorkerDev w, int B, int K,
 // and hidden s_i for every pending node (one warp per node).
 __global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const float* time_b,
                              float* x, float* h, int set_slot) {
+    pdl_entry();
     const int u = warp_id_global(), lane = lane_id();
     if (u >= *w.nU) return;
     const std::uint32_t node = w.pU[u], other = w.pOther[u], ev = w.pEv[u];
@@ -114,6 +118,7 @@ __global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const flo
 // GRUCell (PyTorch gate order r, z, n) on G_i = W_ih x + b_ih, G_h = W_hh h + b_hh.
 __global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh, const float* h,
                           float* save, float* mem_new) {
+    pdl_entry();
     const int nU = *w.nU;
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (std::size_t)nU * d.D) return;
@@ -141,6 +146,7 @@ __global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh,
 __global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* roots,
                                const float* mem_new, float* q_in) {
+    pdl_entry();
     const int row = warp_id_global(), lane = lane_id();
     if (row >= R) return;
     const float* m = memx_row(w, mem_new, d.D, roots[row]);
@@ -152,6 +158,7 @@ __global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
 // MergeLayer input [attn | s_root]; attn = 0 for a root without neighbours.
 __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
                                const int* cnt, const float* O, const float* mem_new, float* m_in) {
+    pdl_entry();
     const int r = warp_id_global(), lane = lane_id();
     if (r >= R) return;
     float* o = m_in + (std::size_t)r * d.ld_m;
@@ -163,6 +170,7 @@ __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* 
 
 // Decoder input rows: p < B -> [z_src | z_dst], p >= B -> [z_src | z_neg].
 __global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in) {
+    pdl_entry();
     const int p = warp_id_global(), lane = lane_id();
     if (p >= 2 * B) return;
     const int i = p < B ? p : p - B;
@@ -178,6 +186,7 @@ __global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in) {
 // w2 = augmented [w | b] row of dec2.
 __global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, float* dlogit,
                            float* lossv, float* dD1, float* logits) {
+    pdl_entry();
     const int p = warp_id_global(), lane = lane_id();
     if (p >= 2 * B) return;
     const float* x = D1 + (std::size_t)p * d.ld_d1;
@@ -198,6 +207,7 @@ __global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, floa
 
 // Fixed-order single-block sum (deterministic loss).
 __global__ void k_sum_loss(const float* lossv, int n, float* out) {
+    pdl_entry();
     __shared__ float sh[32];
     float s = 0.f;
     for (int i = threadIdx.x; i < n; i += blockDim.x) s += lossv[i];
@@ -212,6 +222,7 @@ __global__ void k_sum_loss(const float* lossv, int n, float* out) {
 }
 
 __global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb) {
+    pdl_entry();
     const int i = warp_id_global(), lane = lane_id();
     if (i >= B) return;
     const float* a = dd_in + (std::size_t)i * d.ld_din;
@@ -224,6 +235,7 @@ __global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb) {
 }
 
 __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt) {
+    pdl_entry();
     const int r = warp_id_global(), lane = lane_id();
     if (r >= R || cnt[r] > 0) return;
     for (int c = lane; c < cols; c += 32) buf[(std::size_t)r * ld + c] = 0.f;
@@ -236,6 +248,7 @@ __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt)
 __global__ void k_root_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
                             const float* dq_in, const float* dm_in, const float* time_b,
                             int rows_per_block, float* dH, double* part) {
+    pdl_entry();
     __shared__ double red[8][32];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int r0 = blockIdx.x * rows_per_block;
@@ -273,6 +286,7 @@ __global__ void k_root_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roo
 
 // one block per output (2T): fixed-order strided sums + tree -> deterministic.
 __global__ void k_time_grad_final(int T, int nblocks, const double* part, double* acc) {
+    pdl_entry();
     __shared__ double red[256];
     const int c = blockIdx.x;
     double s = 0.0;
@@ -287,6 +301,7 @@ __global__ void k_time_grad_final(int T, int nblocks, const double* part, double
 }
 
 __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb) {
+    pdl_entry();
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= T) return;
     gw[c] += (float)acc[c];
@@ -296,6 +311,7 @@ __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb
 // GRUCell backward to the gate pre-activations (inputs x, h are constants).
 __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* save, const float* h,
                           float* dGi, float* dGh) {
+    pdl_entry();
     const int nU = *w.nU;
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (std::size_t)nU * d.D) return;
@@ -322,6 +338,7 @@ __global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* sav
 __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
                        float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
                        float eps, float* p_tc) {
+    pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float bc1 = bc[0], bc2 = bc[1];  // bias corrections of this step (host-written)
@@ -338,12 +355,14 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t
 }
 
 __global__ void k_round_tf32(const float* src, float* dst, std::size_t n) {
+    pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = tf32r(src[i]);
 }
 
 // Persist the GRU rows of pending nodes (K11) and clear their slots.
 __global__ void k_persist(WorkerDev w, int D, const float* mem_new) {
+    pdl_entry();
     const int u = warp_id_global(), lane = lane_id();
     if (u >= *w.nU) return;
     const std::uint32_t node = w.pU[u];
@@ -358,6 +377,7 @@ __global__ void k_persist(WorkerDev w, int D, const float* mem_new) {
 // batch's events; per node the max slot wins (max (ts, stream index)),
 // compacted in slot order. Single block; lastpos starts and ends at -1.
 __global__ void k_pending(WorkerDev w, int B) {
+    pdl_entry();
     const std::uint64_t lo = w.ctl[0];
     __shared__ int warp_tot[32];
     __shared__ int base;
@@ -428,6 +448,7 @@ __global__ void k_pending(WorkerDev w, int B) {
 // Synthetic BF16-exact edge features for the partition's events (E x Fp, pad 0).
 __global__ void k_gen_features(__nv_bfloat16* feat, const std::uint64_t* eids, std::uint64_t E,
                                int F, int Fp, std::uint64_t seed_mixed) {
+    pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E * (std::size_t)Fp) return;
     const std::uint64_t e = i / Fp;
@@ -438,6 +459,7 @@ __global__ void k_gen_features(__nv_bfloat16* feat, const std::uint64_t* eids, s
 
 __global__ void k_gather_rows(const float* src, int ld, const std::uint32_t* idx, std::uint32_t n,
                               int cols, float* out) {
+    pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (std::size_t)n * cols) return;
     const std::uint32_t r = i / cols, c = i % cols;

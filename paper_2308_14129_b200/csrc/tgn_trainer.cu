@@ -7,6 +7,7 @@
 //   Q, [K;V] GEMMs -> attention -> W_o GEMM -> merge gather -> W_m1, W_m2 ->
 //   decoder gather -> W_d1 -> head/loss ; backward mirrors it with
 //   weight-gradient GEMMs accumulating straight into the flat gradient.
+#include "pdl.cuh"
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -29,12 +30,22 @@ std::atomic<std::uint64_t> g_kernel_launches{0};
 
 // Every kernel of the TGN path goes through here: counted (bench.py reports
 // the launches inside the timed region) and checked.
+// Optionally launched with programmatic stream serialization (pdl.cuh).
 template <class... KArgs, class... Args>
 void launch(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
             Args&&... args) {
-    k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    SPD_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(std::forward<Args>(args))...));
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    SPD_CUDA(cudaGetLastError());
 }
 
 #define ncclCommInitRank NcclApi::get().CommInitRank
@@ -1077,6 +1088,7 @@ void TGNTrainer::last_step(int wid, std::uint64_t* b, float* emb, std::uint32_t*
 namespace {
 __global__ void k_sync_pack(const float* mem, const double* lu, const std::uint32_t* rows, int S,
                             int D, int first, float* sum, float* mn, float* mx, double* ts_max) {
+    pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (std::size_t)S * (D + 1)) return;
     const int sidx = i / (D + 1), c = i % (D + 1);
@@ -1101,6 +1113,7 @@ __global__ void k_sync_pack(const float* mem, const double* lu, const std::uint3
 }
 __global__ void k_sync_ts_minmax(const double* lu, const std::uint32_t* rows, int S, int first,
                                  double* tmin, double* tmax) {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= S) return;
     const double t = rows[i] == 0xFFFFFFFFu ? 0.0 : lu[rows[i]];
@@ -1110,6 +1123,7 @@ __global__ void k_sync_ts_minmax(const double* lu, const std::uint32_t* rows, in
 __global__ void k_sync_apply_avg(float* mem, double* lu, const std::uint32_t* rows, int S, int D,
                                  const float* sum, const float* mn, const float* mx,
                                  const double* tmin, const double* tmax, float inv_w) {
+    pdl_entry();
     const int sidx = blockIdx.x;
     if (sidx >= S) return;
     const std::uint32_t r = rows[sidx];
@@ -1127,6 +1141,7 @@ __global__ void k_sync_apply_avg(float* mem, double* lu, const std::uint32_t* ro
 }
 __global__ void k_sync_owner(const double* lu, const std::uint32_t* rows, int S, const double* tmax,
                              int gid, int* owner) {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= S) return;
     const double t = rows[i] == 0xFFFFFFFFu ? 0.0 : lu[rows[i]];
@@ -1134,6 +1149,7 @@ __global__ void k_sync_owner(const double* lu, const std::uint32_t* rows, int S,
 }
 __global__ void k_sync_owner_pack(const float* mem, const std::uint32_t* rows, int S, int D,
                                   const int* owner, int gid, float* sum) {
+    pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (std::size_t)S * D) return;
     const int sidx = i / D, c = i % D;
@@ -1143,6 +1159,7 @@ __global__ void k_sync_owner_pack(const float* mem, const std::uint32_t* rows, i
 }
 __global__ void k_sync_apply_max(float* mem, double* lu, const std::uint32_t* rows, int S, int D,
                                  const float* rowv, const double* tmax) {
+    pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= (std::size_t)S * D) return;
     const int sidx = i / D, c = i % D;

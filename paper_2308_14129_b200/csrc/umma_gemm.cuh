@@ -21,6 +21,7 @@
 //                   (SBO = 1024 B), 32-column blocks LBO = BK*128 B apart.
 #pragma once
 
+#include "pdl.cuh"
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -171,6 +172,7 @@ struct Cfg {
 template <bool A_MN, bool B_MN, int BN, int NSUB, int CL>
 __global__ void __launch_bounds__(THREADS, 1)
     umma_gemm_kernel(const __grid_constant__ Maps maps, Args args) {
+    pdl_entry();
     using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;
     constexpr int NST = C_::STAGES_;
     extern __shared__ __align__(1024) unsigned char smem_raw[];

@@ -1,6 +1,7 @@
 // Host side of the tcgen05 TF32 GEMM: TMA tensor-map encoding (driver entry
 // point, no libcuda link), tile-width selection, split-K and the three
 // orientations used by the TGN step.
+#include "pdl.cuh"
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -58,6 +59,7 @@ CUtensorMap make_map(const float* base, std::uint64_t inner, std::uint64_t rows,
 // batch's dW (accumulate): deterministic, one launch for every batch.
 __global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, int ldws,
                                 float* __restrict__ C, int ldc, long long c_bstride, int batch) {
+    pdl_entry();
     const std::size_t idx = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (std::size_t)batch * M * N) return;
     const int b = static_cast<int>(idx / ((std::size_t)M * N));
@@ -74,7 +76,17 @@ __global__ void k_splitk_reduce(const float* __restrict__ ws, int splits, int M,
 void reduce(const float* ws, int split, int M, int N, int ldws, float* C, int ldc, const Batch& bt,
             cudaStream_t s) {
     const std::size_t n = std::size_t(bt.n) * M * N;
-    k_splitk_reduce<<<unsigned((n + 255) / 256), 256, 0, s>>>(ws, split, M, N, ldws, C, ldc, bt.c, bt.n);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned((n + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    SPD_CUDA(cudaLaunchKernelEx(&cfg, k_splitk_reduce, ws, split, M, N, ldws, C, ldc,
+                                static_cast<long long>(bt.c), bt.n));
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
 }
@@ -87,23 +99,22 @@ void run(const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
     std::call_once(once, [&] {
         SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
     });
-    if (CL == 1) {
-        kern<<<grid, THREADS, C_::SMEM, s>>>(maps, args);
-    } else {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = grid;
-        cfg.blockDim = dim3(THREADS);
-        cfg.dynamicSmemBytes = C_::SMEM;
-        cfg.stream = s;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 1;
-        attr[0].val.clusterDim.y = CL;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, args));
-    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = CL;
+    attr[1].val.clusterDim.z = 1;
+    const bool pdl = pdl_enabled();
+    cfg.attrs = pdl ? attr : attr + 1;
+    cfg.numAttrs = (pdl ? 1 : 0) + (CL > 1 ? 1 : 0);
+    SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, args));
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
 }
