@@ -60,11 +60,19 @@ def test_eval_scores_match_oracle(gemm_mode):
     o = oracle_for(cfg, subs, pa.shared)
     tr.run_epoch(0)
     o.run_epoch(0)
+    # Evaluation from identical state: after a 94-step lr=1e-3 Adam epoch two
+    # FP32 implementations that differ only in summation order drift apart by
+    # a few % (Adam normalises gradient noise; e.g. the split decoder sums move
+    # the scores 3% vs 0.1% for a single 201-long dot), which would test the
+    # chaos of training rather than the eval path. The trajectories themselves
+    # are pinned by test_tgn_gpu.py; the AP/AUC bar by the Wikipedia-shape run.
+    tr.set_params(o.flat.numpy())
+    for w in range(len(subs)):
+        tr.set_memory(w, o.mem[w].numpy(), o.lu[w])
     g = scores(tr, ev, False)
     c = scores(o, ev, True)
-    # FP32: summation-order drift only. TF32 (10-bit operand mantissas): a
-    # 94-step lr=1e-3 trajectory drifts a few %; the AP/AUC bar below is the contract.
-    tol = 2e-3 if gemm_mode == 0 else 1.5e-1
+    # FP32: summation order only; TF32 (10-bit operand mantissas) projections
+    tol = 2e-4 if gemm_mode == 0 else 2e-2
     for a, b in zip(g, c):
         assert rel_err(a, b) < tol, rel_err(a, b)
     # (the AP/AUC bar is asserted on the Wikipedia-shaped run below: with ~900
