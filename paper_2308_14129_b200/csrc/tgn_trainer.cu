@@ -599,10 +599,14 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train) {
     launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
         wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
     SPD_CUDA(cudaGetLastError());
+    // the two gate GEMMs are independent: hidden-side one on the side stream
+    side([&](cudaStream_t sd) {
+        proj_fwd(tc, s.h_gru.p, d.ld_h, PW + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U,
+                 3 * d.D, d.D + 1, w.nU.p, sd);
+    });
     proj_fwd(tc, s.x_gru.p, d.ld_x, PW + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, 3 * d.D,
              d.DM + 1, w.nU.p, stream_);
-    proj_fwd(tc, s.h_gru.p, d.ld_h, PW + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, 3 * d.D,
-             d.D + 1, w.nU.p, stream_);
+    join_side();
     launch(tgnk::k_gru_fwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, stream_, 
         wd, d, s.Gi.p, s.Gh.p, s.h_gru.p, train ? s.gsave.p : nullptr, s.mem_new.p);
     SPD_CUDA(cudaGetLastError());
@@ -622,10 +626,15 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     cudaStream_t st = stream_;
     const bool tc = cfg_.gemm_mode == 1;  // tensor cores for GRU + attention projections only
     const float* PW = tc ? params_tc_.p : params_.p;
-    timed("roots_nbrs", [&] {
-        launch(tgnk::k_roots_nbrs, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, B, d.K, s.roots.p,
+    // the recent-k search depends only on the batch and the static CSR: it runs
+    // on the side stream beside the GRU update (joined inside gru_forward);
+    // profiled runs keep it on the main stream so its phase time is its own
+    auto roots = [&](cudaStream_t sx) {
+        launch(tgnk::k_roots_nbrs, blocks_for(std::size_t(R) * 32), 256, 0, sx, wd, B, d.K, s.roots.p,
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
-    });
+    };
+    if (profile_) timed("roots_nbrs", [&] { roots(st); });
+    else side(roots);
     timed("gru_fwd", [&] { gru_forward(w, wd, train); });
     timed("query_gather", [&] {
         launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
