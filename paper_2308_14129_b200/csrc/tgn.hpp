@@ -161,6 +161,11 @@ private:
     void join_side();
     cudaStream_t side_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    // a second fork for the GRU's hidden-side gate GEMM, and the points of the
+    // side stream the main stream waits for (neighbours found, phases evaluated)
+    cudaStream_t aux_ = nullptr;
+    cudaEvent_t ev_aux_fork_ = nullptr, ev_aux_join_ = nullptr, ev_roots_ = nullptr,
+                ev_phi_ = nullptr;
 
     spd_tgn_config cfg_;
     ParamLayout lay_;

@@ -148,18 +148,15 @@ __device__ __forceinline__ int vidx(int lane) {
 }
 
 // Stage root r's neighbour rows (warp-cooperative). Lane j < c_n holds
-// neighbour j's (dt, slot) on return, for the caller's scatters. TPL >= T/32.
-// Time encoding: the forward evaluates cos and sin of the f64 phase once per
-// occurrence and also stores them to phi[r][j] = [cos T | sin T] (f32); the
-// backward (with_sin) stages them from there by cp.async instead of
-// re-evaluating (the kernels are instruction-bound, HBM is not).
-template <int TPL>
+// neighbour j's (dt, slot) on return, for the caller's scatters. The time
+// encoding of the occurrences comes from phi[r][j] = [cos T | sin T] (k_phi,
+// evaluated beside the GRU update): cos into the row, and sin too for the
+// backward (with_sin).
 __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, int r, int c_n,
-                                           int lane, const float* time_w, const float* time_b,
-                                           const std::uint32_t* nbr_node,
+                                           int lane, const std::uint32_t* nbr_node,
                                            const std::uint32_t* nbr_ev, const double* nbr_dt,
                                            const float* mem_new, unsigned char* xs, bool with_sin,
-                                           float* phi, double& m_dt, int& m_slot) {
+                                           const float* phi, double& m_dt, int& m_slot) {
     std::uint32_t ev = 0, node = 0;
     m_dt = 0.0;
     m_slot = -1;
@@ -171,8 +168,8 @@ __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, in
         m_slot = w.slot[node];
     }
     const int RB = row_bytes(d, with_sin);
-    const int mch = d.D / 4, fch = d.Fp / 8, tch = with_sin ? d.T / 4 : 0;  // 16-B chunks
-    float* phir = phi + (std::size_t)r * d.K * 2 * d.T;
+    const int mch = d.D / 4, fch = d.Fp / 8, tch = d.T / 4, sch = with_sin ? d.T / 4 : 0;  // 16-B chunks
+    const float* phir = phi + (std::size_t)r * d.K * 2 * d.T;
     for (int j = 0; j < c_n; ++j) {
         const std::uint32_t nj = __shfl_sync(0xffffffffu, node, j);
         const std::uint32_t e = __shfl_sync(0xffffffffu, ev, j);
@@ -181,39 +178,12 @@ __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, in
         const __nv_bfloat16* frow = w.feat + (std::size_t)e * d.Fp;
         const float* prow = phir + (std::size_t)j * 2 * d.T;
         unsigned char* dst = xs + (std::size_t)j * RB;
-        for (int c = lane; c < mch + fch + 2 * tch; c += 32) {
+        for (int c = lane; c < mch + fch + tch + sch; c += 32) {
             if (c < mch) cp_async16_ca(dst + 16 * c, mrow + 4 * c);
             else if (c < mch + fch) cp_async16_cg(dst + 4 * (d.D + d.T) + 16 * (c - mch), frow + 8 * (c - mch));
             else if (c < mch + fch + tch) cp_async16_cg(dst + 4 * d.D + 16 * (c - mch - fch), prow + 4 * (c - mch - fch));
             else cp_async16_cg(dst + 4 * (d.D + d.T) + 2 * d.Fp + 16 * (c - mch - fch - tch),
                                prow + d.T + 4 * (c - mch - fch - tch));
-        }
-    }
-    if (!with_sin) {
-        // phi(dt) = cos(w dt + b), phase in f64; this lane's time columns
-        // t = lane + 32k (k < TPL) and their parameters
-        double tw[TPL], tb[TPL];
-#pragma unroll
-        for (int k = 0; k < TPL; ++k) {
-            const int t = lane + 32 * k;
-            tw[k] = t < d.T ? static_cast<double>(time_w[t]) : 0.0;
-            tb[k] = t < d.T ? static_cast<double>(time_b[t]) : 0.0;
-        }
-#pragma unroll 1
-        for (int j = 0; j < c_n; ++j) {
-            const double dt = __shfl_sync(0xffffffffu, m_dt, j);
-            float* cs = reinterpret_cast<float*>(xs + (std::size_t)j * RB) + d.D;
-            float* pg = phir + (std::size_t)j * 2 * d.T;
-#pragma unroll
-            for (int k = 0; k < TPL; ++k) {
-                const int t = lane + 32 * k;
-                if (t < d.T) {
-                    const float2 sc2 = phase_sincos<true>(tw[k], tb[k], dt);
-                    cs[t] = sc2.y;
-                    pg[t] = sc2.y;
-                    pg[d.T + t] = sc2.x;
-                }
-            }
         }
     }
     cp_async_wait_all();
@@ -297,6 +267,30 @@ __device__ __forceinline__ void axpys(float4 (&v)[HMAX][S::N], const Dims& d, in
 
 }  // namespace
 
+// Time encoding of every valid neighbour occurrence, phi[r][j] = [cos T | sin T]
+// of w dt + b (f64 phase, tgn_common.cuh phase_sincos); one thread per
+// (occurrence, 4 consecutive time columns): float4 parameter loads and
+// stores, four independent f64 chains in flight.
+__global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, const double* nbr_dt,
+                      const int* cnt, float* phi) {
+    pdl_entry();
+    const int T4 = d.T / 4;
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)R * d.K * T4) return;
+    const std::size_t occ = i / T4;
+    const int t = 4 * static_cast<int>(i % T4);
+    const int r = static_cast<int>(occ / d.K), j = static_cast<int>(occ % d.K);
+    if (j >= cnt[r]) return;
+    const double dt = nbr_dt[occ];
+    const float4 w = *reinterpret_cast<const float4*>(time_w + t);
+    const float4 b = *reinterpret_cast<const float4*>(time_b + t);
+    const float2 s0 = phase_sincos<true>(w.x, b.x, dt), s1 = phase_sincos<true>(w.y, b.y, dt);
+    const float2 s2 = phase_sincos<true>(w.z, b.z, dt), s3 = phase_sincos<true>(w.w, b.w, dt);
+    float* p = phi + occ * 2 * d.T;
+    *reinterpret_cast<float4*>(p + t) = make_float4(s0.y, s1.y, s2.y, s3.y);
+    *reinterpret_cast<float4*>(p + d.T + t) = make_float4(s0.x, s1.x, s2.x, s3.x);
+}
+
 __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd) {
     const std::size_t stage = std::size_t(kRootsPerBlock) * d.K * row_bytes(d, bwd);
     const std::size_t tpart = std::size_t(kRootsPerBlock) * 2 * d.T * sizeof(float);
@@ -340,8 +334,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     }
     double m_dt;
     int m_slot;
-    stage_rows<4 * NT>(w, d, r, c_n, lane, time_w, time_b, nbr_node, nbr_ev, nbr_dt, mem_new, xs,
-                       false, phi, m_dt, m_slot);
+    stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, false, phi, m_dt, m_slot);
     load_slots<S, HMAX>(v, Qp + row0, d, lane);
     const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
     dots<S, HMAX>(v, d, lane, xs, RB, c_n, sc, inv);
@@ -414,8 +407,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     if (c_n > 0) {
         double m_dt;
         int m_slot;
-        stage_rows<4 * NT>(w, d, r, c_n, lane, time_w, time_b, nbr_node, nbr_ev, nbr_dt, mem_new, xs,
-                           true, const_cast<float*>(phi), m_dt, m_slot);
+        stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, true, phi, m_dt, m_slot);
         if (lane < d.K)
             for (int h = 0; h < d.H; ++h)
                 aa[h * d.K + lane] = lane < c_n ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;

@@ -66,6 +66,8 @@ __global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
 // dynamic shared memory attn_smem_bytes(d, bwd); lane slots per region
 // NM = ceil(D / 128), NT = ceil(T / 128), NF = ceil((F + 1) / 128); HMAX >= H
 __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd);
+__global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, const double* nbr_dt,
+                      const int* cnt, float* phi);
 int attn_roots_per_block();
 template <int NM, int NT, int NF, int HMAX>
 __global__ void k_attn_abs_fwd(WorkerDev w, Dims d, int R, const float* time_w,

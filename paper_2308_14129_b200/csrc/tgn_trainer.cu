@@ -331,10 +331,18 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     if (world < 1 || rank < 0 || rank >= world) data_error("InvalidParams", "bad rank/world");
     require_device(device);
     DeviceGuard g(device);
-    SPD_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-    SPD_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+    // the main stream carries the step's critical path: highest priority, so
+    // its CTAs are scheduled ahead of the side streams' (weight gradients,
+    // neighbour search, time encoding) whenever both have work queued
+    int prio_lo = 0, prio_hi = 0;
+    SPD_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SPD_CUDA(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
+    SPD_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, prio_lo));
     SPD_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     SPD_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
+    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_phi_})
+        SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors);
     feat_seed_mixed_ = mix64(cfg.seed_feat);
     total_workers_ = static_cast<int>(subs.g.size());
@@ -526,6 +534,9 @@ TGNTrainer::~TGNTrainer() {
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (side_) cudaStreamDestroy(side_);
+    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_phi_})
+        if (e) cudaEventDestroy(e);
+    if (aux_) cudaStreamDestroy(aux_);
     if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
     if (stream_) cudaStreamDestroy(stream_);
 }
@@ -599,14 +610,15 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train) {
     launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
         wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
     SPD_CUDA(cudaGetLastError());
-    // the two gate GEMMs are independent: hidden-side one on the side stream
-    side([&](cudaStream_t sd) {
-        proj_fwd(tc, s.h_gru.p, d.ld_h, PW + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U,
-                 3 * d.D, d.D + 1, w.nU.p, sd);
-    });
+    // the two gate GEMMs are independent: the hidden-side one on the aux stream
+    SPD_CUDA(cudaEventRecord(ev_aux_fork_, stream_));
+    SPD_CUDA(cudaStreamWaitEvent(aux_, ev_aux_fork_, 0));
+    proj_fwd(tc, s.h_gru.p, d.ld_h, PW + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, 3 * d.D,
+             d.D + 1, w.nU.p, aux_);
     proj_fwd(tc, s.x_gru.p, d.ld_x, PW + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, 3 * d.D,
              d.DM + 1, w.nU.p, stream_);
-    join_side();
+    SPD_CUDA(cudaEventRecord(ev_aux_join_, aux_));
+    SPD_CUDA(cudaStreamWaitEvent(stream_, ev_aux_join_, 0));
     launch(tgnk::k_gru_fwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, stream_, 
         wd, d, s.Gi.p, s.Gh.p, s.h_gru.p, train ? s.gsave.p : nullptr, s.mem_new.p);
     SPD_CUDA(cudaGetLastError());
@@ -626,16 +638,33 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     cudaStream_t st = stream_;
     const bool tc = cfg_.gemm_mode == 1;  // tensor cores for GRU + attention projections only
     const float* PW = tc ? params_tc_.p : params_.p;
-    // the recent-k search depends only on the batch and the static CSR: it runs
-    // on the side stream beside the GRU update (joined inside gru_forward);
-    // profiled runs keep it on the main stream so its phase time is its own
+    // The recent-k search and the time encoding of every neighbour occurrence
+    // depend only on the batch, the static CSR and the time parameters: they
+    // run on the side stream beside the GRU update and the query GEMMs; the
+    // main stream waits for each result where it is first read. Profiled runs
+    // keep them on the main stream so their phase times are their own.
     auto roots = [&](cudaStream_t sx) {
         launch(tgnk::k_roots_nbrs, blocks_for(std::size_t(R) * 32), 256, 0, sx, wd, B, d.K, s.roots.p,
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     };
-    if (profile_) timed("roots_nbrs", [&] { roots(st); });
-    else side(roots);
+    auto phi = [&](cudaStream_t sx) {
+        launch(tgnk::k_phi, blocks_for(std::size_t(R) * d.K * (d.T / 4)), 256, 0, sx, d, R,
+               P + lay_.time_w, P + lay_.time_b, static_cast<const double*>(s.nbr_dt.p),
+               static_cast<const int*>(s.cnt.p), s.phi.p);
+    };
+    if (profile_) {
+        timed("roots_nbrs", [&] { roots(st); });
+        timed("phi", [&] { phi(st); });
+    } else {
+        side([&](cudaStream_t sd) {
+            roots(sd);
+            SPD_CUDA(cudaEventRecord(ev_roots_, sd));
+            phi(sd);
+            SPD_CUDA(cudaEventRecord(ev_phi_, sd));
+        });
+    }
     timed("gru_fwd", [&] { gru_forward(w, wd, train); });
+    if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_roots_, 0));
     timed("query_gather", [&] {
         launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
                P + lay_.time_w, P + lay_.time_b, s.roots.p, s.mem_new.p, s.q_in.p);
@@ -655,6 +684,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         proj_dgrad(tc, s.Q.p, d.ld_Q, WK, ldw, s.Qp.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0, nullptr,
                    0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
     });
+    if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_phi_, 0));
     timed("k_attn_abs_fwd", [&] { attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st); });
     timed("gemm_ctx", [&] {
         proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
