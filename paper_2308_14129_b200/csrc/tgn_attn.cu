@@ -44,21 +44,46 @@ __device__ __forceinline__ float4 rnd4(float4 v, int rnd) {
     return rnd ? make_float4(tf32r(v.x), tf32r(v.y), tf32r(v.z), tf32r(v.w)) : v;
 }
 
-__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+// one-instruction bulk copy global -> shared (TMA engine), completion counted
+// in bytes on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         std::uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+__device__ __forceinline__ void bar_init(std::uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_expect(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(std::uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n"
+        "DONE_%=:\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
 }
 
-// One staged neighbour row: [mem f32 D | cos f32 T | feat bf16 Fp | sin f32 T (bwd)]
+// One staged neighbour row: [mem f32 D | cos f32 T | sin f32 T (bwd) | feat bf16 Fp]
+// (each part one bulk copy: the memory row, the phi row, the feature row)
 __host__ __device__ __forceinline__ int row_bytes(const Dims& d, bool with_sin) {
-    return 4 * (d.D + d.T) + 2 * d.Fp + (with_sin ? 4 * d.T : 0);
+    return 4 * (d.D + d.T) + (with_sin ? 4 * d.T : 0) + 2 * d.Fp;
+}
+__host__ __device__ __forceinline__ int feat_off(const Dims& d, bool with_sin) {
+    return 4 * (d.D + d.T) + (with_sin ? 4 * d.T : 0);
 }
 
 // Slot geometry (compile-time region per slot).
@@ -87,12 +112,13 @@ struct Slots {
 // (shift invariant) ignores it and its gradient sum_j ds_hj is 0; in xbar it
 // is sum_j a_hj = 1, set directly (set_bias).
 template <class S>
-__device__ __forceinline__ float4 x_slot(const Dims& d, int i, int lane, const unsigned char* row) {
+__device__ __forceinline__ float4 x_slot(const Dims& d, int i, int lane, const unsigned char* row,
+                                         int foff) {
     const int o = 4 * (lane + 32 * S::local(i));
     if (S::region(i) == 0) return o < d.D ? *reinterpret_cast<const float4*>(row + 4 * o) : z4();
     if (S::region(i) == 1) return o < d.T ? *reinterpret_cast<const float4*>(row + 4 * (d.D + o)) : z4();
     if (o >= d.Fp) return z4();  // Fp % 8 == 0: 4 bf16 never straddle the row end; pad is 0
-    const uint2 raw = *reinterpret_cast<const uint2*>(row + 4 * (d.D + d.T) + 2 * o);
+    const uint2 raw = *reinterpret_cast<const uint2*>(row + foff + 2 * o);
     return make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
                        __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u));
 }
@@ -147,47 +173,36 @@ __device__ __forceinline__ int vidx(int lane) {
     return idx;
 }
 
-// Stage root r's neighbour rows (warp-cooperative). Lane j < c_n holds
-// neighbour j's (dt, slot) on return, for the caller's scatters. The time
-// encoding of the occurrences comes from phi[r][j] = [cos T | sin T] (k_phi,
-// evaluated beside the GRU update): cos into the row, and sin too for the
-// backward (with_sin).
+// Stage root r's neighbour rows (warp-cooperative): lane j < c_n issues the
+// three bulk copies of neighbour j's row — memory row (GRU output when just
+// updated), phi row (cos, and sin for the backward; k_phi), bf16 feature row
+// — all completing on the warp's mbarrier, so every gather of the root is in
+// flight at once for ~3 instructions per neighbour. Lane j < c_n holds
+// neighbour j's (dt, slot) on return, for the caller's scatters.
 __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, int r, int c_n,
                                            int lane, const std::uint32_t* nbr_node,
                                            const std::uint32_t* nbr_ev, const double* nbr_dt,
                                            const float* mem_new, unsigned char* xs, bool with_sin,
-                                           const float* phi, double& m_dt, int& m_slot) {
-    std::uint32_t ev = 0, node = 0;
+                                           const float* phi, std::uint64_t* bar, double& m_dt,
+                                           int& m_slot) {
     m_dt = 0.0;
     m_slot = -1;
+    const unsigned pbytes = 4u * d.T * (with_sin ? 2u : 1u);
+    const unsigned per = 4u * d.D + pbytes + 2u * d.Fp;
+    if (lane == 0) bar_expect(bar, per * c_n);
+    __syncwarp();
     if (lane < c_n) {
         const std::size_t o = (std::size_t)r * d.K + lane;
-        node = nbr_node[o];
-        ev = nbr_ev[o];
+        const std::uint32_t node = nbr_node[o], ev = nbr_ev[o];
         m_dt = nbr_dt[o];
         m_slot = w.slot[node];
+        const float* mrow = m_slot >= 0 ? mem_new + (std::size_t)m_slot * d.D : w.mem + (std::size_t)node * d.D;
+        unsigned char* dst = xs + (std::size_t)lane * row_bytes(d, with_sin);
+        bulk_g2s(dst, mrow, 4u * d.D, bar);
+        bulk_g2s(dst + 4 * d.D, phi + o * 2 * d.T, pbytes, bar);
+        if (d.Fp) bulk_g2s(dst + feat_off(d, with_sin), w.feat + (std::size_t)ev * d.Fp, 2u * d.Fp, bar);
     }
-    const int RB = row_bytes(d, with_sin);
-    const int mch = d.D / 4, fch = d.Fp / 8, tch = d.T / 4, sch = with_sin ? d.T / 4 : 0;  // 16-B chunks
-    const float* phir = phi + (std::size_t)r * d.K * 2 * d.T;
-    for (int j = 0; j < c_n; ++j) {
-        const std::uint32_t nj = __shfl_sync(0xffffffffu, node, j);
-        const std::uint32_t e = __shfl_sync(0xffffffffu, ev, j);
-        const int slot = __shfl_sync(0xffffffffu, m_slot, j);
-        const float* mrow = slot >= 0 ? mem_new + (std::size_t)slot * d.D : w.mem + (std::size_t)nj * d.D;
-        const __nv_bfloat16* frow = w.feat + (std::size_t)e * d.Fp;
-        const float* prow = phir + (std::size_t)j * 2 * d.T;
-        unsigned char* dst = xs + (std::size_t)j * RB;
-        for (int c = lane; c < mch + fch + tch + sch; c += 32) {
-            if (c < mch) cp_async16_ca(dst + 16 * c, mrow + 4 * c);
-            else if (c < mch + fch) cp_async16_cg(dst + 4 * (d.D + d.T) + 16 * (c - mch), frow + 8 * (c - mch));
-            else if (c < mch + fch + tch) cp_async16_cg(dst + 4 * d.D + 16 * (c - mch - fch), prow + 4 * (c - mch - fch));
-            else cp_async16_cg(dst + 4 * (d.D + d.T) + 2 * d.Fp + 16 * (c - mch - fch - tch),
-                               prow + d.T + 4 * (c - mch - fch - tch));
-        }
-    }
-    cp_async_wait_all();
-    __syncwarp();
+    bar_wait(bar, 0);
 }
 
 template <class S, int HMAX>
@@ -219,8 +234,9 @@ __device__ __forceinline__ void store_slots(const float4 (&v)[HMAX][S::N], float
 // of 8 neighbours whose 8*HMAX partial dot products share one multi-value
 // warp reduction.
 template <class S, int HMAX>
-__device__ __forceinline__ void dots(const float4 (&v)[HMAX][S::N], const Dims& d, int lane, const unsigned char* xs, int RB,
-                                     int c_n, float* sc, float scale) {
+__device__ __forceinline__ void dots(const float4 (&v)[HMAX][S::N], const Dims& d, int lane,
+                                     const unsigned char* xs, int RB, int foff, int c_n, float* sc,
+                                     float scale) {
     constexpr int G = 8, V = G * HMAX;
     const int vi = vidx<V>(lane);
     const int hv = vi / G, gv = vi % G;
@@ -236,7 +252,7 @@ __device__ __forceinline__ void dots(const float4 (&v)[HMAX][S::N], const Dims& 
                 const unsigned char* row = xs + (std::size_t)(j0 + g) * RB;
 #pragma unroll
                 for (int i = 0; i < S::N; ++i) {
-                    const float4 x = x_slot<S>(d, i, lane, row);
+                    const float4 x = x_slot<S>(d, i, lane, row, foff);
 #pragma unroll
                     for (int h = 0; h < HMAX; ++h) p[h * G + g] = dot4acc(v[h][i], x, p[h * G + g]);
                 }
@@ -248,8 +264,9 @@ __device__ __forceinline__ void dots(const float4 (&v)[HMAX][S::N], const Dims& 
 }
 
 template <class S, int HMAX>
-__device__ __forceinline__ void axpys(float4 (&v)[HMAX][S::N], const Dims& d, int lane, const unsigned char* xs, int RB,
-                                      int c_n, const float* coef) {
+__device__ __forceinline__ void axpys(float4 (&v)[HMAX][S::N], const Dims& d, int lane,
+                                      const unsigned char* xs, int RB, int foff, int c_n,
+                                      const float* coef) {
 #pragma unroll 2
     for (int j = 0; j < c_n; ++j) {
         const unsigned char* row = xs + (std::size_t)j * RB;
@@ -258,7 +275,7 @@ __device__ __forceinline__ void axpys(float4 (&v)[HMAX][S::N], const Dims& d, in
         for (int h = 0; h < HMAX; ++h) a[h] = h < d.H ? coef[h * d.K + j] : 0.f;
 #pragma unroll
         for (int i = 0; i < S::N; ++i) {
-            const float4 x = x_slot<S>(d, i, lane, row);
+            const float4 x = x_slot<S>(d, i, lane, row, foff);
 #pragma unroll
             for (int h = 0; h < HMAX; ++h) axpy4(v[h][i], a[h], x);
         }
@@ -294,7 +311,8 @@ __global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, c
 __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd) {
     const std::size_t stage = std::size_t(kRootsPerBlock) * d.K * row_bytes(d, bwd);
     const std::size_t tpart = std::size_t(kRootsPerBlock) * 2 * d.T * sizeof(float);
-    return (stage > tpart ? stage : tpart) + kRootsPerBlock * 2 * sizeof(float) * d.H * d.K;
+    return (stage > tpart ? stage : tpart) + kRootsPerBlock * 2 * sizeof(float) * d.H * d.K +
+           kRootsPerBlock * sizeof(std::uint64_t);
 }
 int attn_roots_per_block() { return kRootsPerBlock; }
 
@@ -315,10 +333,13 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = blockIdx.x * kRootsPerBlock + warp;
     if (r >= R) return;
-    const int RB = row_bytes(d, false);
+    constexpr bool BWD = false;
+    const int RB = row_bytes(d, BWD);
     unsigned char* xs = smem + (std::size_t)warp * d.K * RB;
-    float* sc = reinterpret_cast<float*>(smem + attn_smem_bytes(d, false)) -
-                kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(smem + attn_smem_bytes(d, BWD)) - kRootsPerBlock + warp;
+    float* sc = reinterpret_cast<float*>(bar - warp) - kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
+    if (lane == 0) bar_init(bar);
+    __syncwarp();
     const int c_n = cnt[r];
     const std::size_t row0 = (std::size_t)r * d.H * d.ld_p;
     float4 v[HMAX][S::N];  // q'_h, then the xbar accumulators
@@ -334,10 +355,10 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     }
     double m_dt;
     int m_slot;
-    stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, false, phi, m_dt, m_slot);
+    stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, BWD, phi, bar, m_dt, m_slot);
     load_slots<S, HMAX>(v, Qp + row0, d, lane);
     const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
-    dots<S, HMAX>(v, d, lane, xs, RB, c_n, sc, inv);
+    dots<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc, inv);
     __syncwarp();
     // softmax per head over the c_n valid neighbours (lane = neighbour)
     for (int h = 0; h < d.H; ++h) {
@@ -359,7 +380,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     for (int h = 0; h < HMAX; ++h)
 #pragma unroll
         for (int i = 0; i < S::N; ++i) v[h][i] = z4();
-    axpys<S, HMAX>(v, d, lane, xs, RB, c_n, sc);
+    axpys<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc);
     set_bias<S, HMAX>(v, d, lane, 1.f);  // sum_j a_hj
     store_slots<S, HMAX>(v, xbar + row0, d, lane, d.rnd);
 }
@@ -386,10 +407,13 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = blockIdx.x * kRootsPerBlock + warp;
-    const int RB = row_bytes(d, true);
+    constexpr bool BWD = true;
+    const int RB = row_bytes(d, BWD);
     unsigned char* xs = smem + (std::size_t)warp * d.K * RB;
-    float* sc = reinterpret_cast<float*>(smem + attn_smem_bytes(d, true)) -
-                kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(smem + attn_smem_bytes(d, BWD)) - kRootsPerBlock + warp;
+    float* sc = reinterpret_cast<float*>(bar - warp) - kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
+    if (lane == 0) bar_init(bar);
+    __syncwarp();
     float* aa = sc + d.H * d.K;  // alpha of this root
     const int c_n = r < R ? cnt[r] : 0;
     const std::size_t row0 = (std::size_t)r * d.H * d.ld_p;
@@ -407,13 +431,13 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     if (c_n > 0) {
         double m_dt;
         int m_slot;
-        stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, true, phi, m_dt, m_slot);
+        stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, BWD, phi, bar, m_dt, m_slot);
         if (lane < d.K)
             for (int h = 0; h < d.H; ++h)
                 aa[h * d.K + lane] = lane < c_n ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
         load_slots<S, HMAX>(v, dxbar + row0, d, lane);
         // pass 1: da_hj
-        dots<S, HMAX>(v, d, lane, xs, RB, c_n, sc, 1.f);
+        dots<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc, 1.f);
         __syncwarp();
         // softmax backward (lane = neighbour): ds = a (da - <a, da>) / sqrt(dh)
         const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
@@ -430,7 +454,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
         for (int h = 0; h < HMAX; ++h)
 #pragma unroll
             for (int i = 0; i < S::N; ++i) v[h][i] = z4();
-        axpys<S, HMAX>(v, d, lane, xs, RB, c_n, sc);
+        axpys<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc);
         store_slots<S, HMAX>(v, dQp + row0, d, lane, d.rnd);
         // pass 2b: input gradients on [s_nbr | phi] (memory and time slots)
         constexpr int NX = NM + NT;
@@ -448,7 +472,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
         for (int j = 0; j < c_n; ++j) {
             const int slot = __shfl_sync(0xffffffffu, m_slot, j);
             const float fdt = (float)__shfl_sync(0xffffffffu, m_dt, j);
-            const float* sn = reinterpret_cast<const float*>(xs + (std::size_t)j * RB + 4 * (d.D + d.T) + 2 * d.Fp);
+            const float* sn = reinterpret_cast<const float*>(xs + (std::size_t)j * RB + 4 * (d.D + d.T));
             float a[HMAX], s[HMAX];
 #pragma unroll
             for (int h = 0; h < HMAX; ++h) {
