@@ -177,7 +177,8 @@ __device__ __forceinline__ int vidx(int lane) {
 // three bulk copies of neighbour j's row — memory row (GRU output when just
 // updated), phi row (cos, and sin for the backward; k_phi), bf16 feature row
 // — all completing on the warp's mbarrier, so every gather of the root is in
-// flight at once for ~3 instructions per neighbour. Lane j < c_n holds
+// flight at once for ~3 instructions per neighbour; the caller overlaps its
+// per-root loads with them before bar_wait. Lane j < c_n holds
 // neighbour j's (dt, slot) on return, for the caller's scatters.
 __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, int r, int c_n,
                                            int lane, const std::uint32_t* nbr_node,
@@ -202,7 +203,7 @@ __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, in
         bulk_g2s(dst + 4 * d.D, phi + o * 2 * d.T, pbytes, bar);
         if (d.Fp) bulk_g2s(dst + feat_off(d, with_sin), w.feat + (std::size_t)ev * d.Fp, 2u * d.Fp, bar);
     }
-    bar_wait(bar, 0);
+    // the caller issues its own per-root loads, then waits (bar_wait(bar, 0))
 }
 
 template <class S, int HMAX>
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     int m_slot;
     stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, BWD, phi, bar, m_dt, m_slot);
     load_slots<S, HMAX>(v, Qp + row0, d, lane);
+    bar_wait(bar, 0);
     const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
     dots<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc, inv);
     __syncwarp();
@@ -436,6 +438,8 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
             for (int h = 0; h < d.H; ++h)
                 aa[h * d.K + lane] = lane < c_n ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
         load_slots<S, HMAX>(v, dxbar + row0, d, lane);
+        bar_wait(bar, 0);
+        __syncwarp();
         // pass 1: da_hj
         dots<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc, 1.f);
         __syncwarp();
