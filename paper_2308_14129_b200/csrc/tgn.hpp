@@ -141,7 +141,9 @@ public:
     cudaStream_t stream() const { return stream_; }
 
 private:
-    void worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx);
+    void worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx,
+                     bool post = true);
+    void worker_post_kernels(Worker& w);
     // host -> device per-step control words (pageable async copy: staged at
     // call time, applied in stream order, so graph replays see fresh values)
     void set_ctl(Worker& w, std::uint64_t lo, std::uint64_t nb);
@@ -151,8 +153,8 @@ private:
     void worker_post(Worker& w);
     void flush_pending(Worker& w);
     void gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train);
-    void allreduce_grads();
-    void adam();
+    void allreduce_grads(cudaStream_t st);
+    void adam(cudaStream_t st);
     void sync_shared();
     void timed(const char* name, const std::function<void()>& f);
     // weight-gradient GEMMs run on a side stream forked from the main stream at

@@ -627,8 +627,18 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train) {
 // One batch of one worker: events [lo, lo+B) of the view's event list.
 // train: forward + backward (weight grads accumulate into grads_) + post;
 // eval (train = false): forward + post (scores in s.logits), no gradients.
+void TGNTrainer::worker_post_kernels(Worker& w) {
+    Scratch& s = *s_;
+    const tgnk::WorkerDev wd = devview(w);
+    timed("post", [&] {
+        launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, wd, s.d.D,
+               s.mem_new.p);
+        launch(tgnk::k_pending, 1, 1024, 0, stream_, wd, w.last_b);
+    });
+}
+
 void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train,
-                             int slot_idx) {
+                             int slot_idx, bool post) {
     Scratch& s = *s_;
     const auto& d = s.d;
     w.last_b = B;
@@ -706,10 +716,17 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         launch(tgnk::k_dec_head, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, 
             d, B, s.D1.p, P + lay_.dec2.off, s.dlogit.p, s.lossv.p, s.dD1.p, s.logits.p);
     });
-    launch(tgnk::k_sum_loss, 1, 1024, 0, st, s.lossv.p, 2 * B, s.loss.p + slot_idx);
+    // the batch loss is only read by the host after the step: off the critical path
+    auto sum_loss = [&](cudaStream_t sx) {
+        launch(tgnk::k_sum_loss, 1, 1024, 0, sx, s.lossv.p, 2 * B, s.loss.p + slot_idx);
+    };
+    if (train) side(sum_loss);
+    else sum_loss(st);
     if (train) backward(w, wd, B);
     // persist this batch's memory update and store its last messages now,
-    // while the scratch still holds this worker's rows (K11, K3)
+    // while the scratch still holds this worker's rows (K11, K3); the last
+    // worker of a training step defers it to step_body (beside the optimizer)
+    if (!post) return;
     timed("post", [&] {
         launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
         launch(tgnk::k_pending, 1, 1024, 0, st, wd, B);
@@ -792,8 +809,11 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     timed("root_time_bwd", [&] {
         launch(tgnk::k_root_grad, s.troot_blocks, dim3(32, 8), 0, st, wd, d, R, s.roots.p, s.dq_in.p,
                s.dm_in.p, P + lay_.time_b, s.trows, s.dH.p, s.tpart.p);
-        launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, st, d.T, s.troot_blocks + s.tattn_blocks,
-               s.tpart.p, tgrad_.p);
+        // the time-encoder gradient is next read by the all-reduce: side stream
+        side([&](cudaStream_t sd) {
+            launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, sd, d.T, s.troot_blocks + s.tattn_blocks,
+                   s.tpart.p, tgrad_.p);
+        });
     });
     timed("gru_bwd", [&] {
         if (tc) {  // the TC weight-grad reads whole K blocks: rows >= |pending| must be 0
@@ -916,14 +936,14 @@ void TGNTrainer::worker_post(Worker& w) {
     }
 }
 
-void TGNTrainer::allreduce_grads() {
+void TGNTrainer::allreduce_grads(cudaStream_t st) {
     // time-encoder grads (f64 accumulators) into the flat buffer first
-    launch(tgnk::k_time_grad_apply, blocks_for(lay_.T), 256, 0, stream_, 
+    launch(tgnk::k_time_grad_apply, blocks_for(lay_.T), 256, 0, st, 
         lay_.T, tgrad_.p, grads_.p + lay_.time_w, grads_.p + lay_.time_b);
     SPD_CUDA(cudaGetLastError());
     if (world_ > 1) {
         SPD_NCCL(ncclAllReduce(grads_.p, grads_.p, lay_.total, ncclFloat, ncclSum,
-                               static_cast<ncclComm_t>(nccl_), stream_));
+                               static_cast<ncclComm_t>(nccl_), st));
     }
 }
 
@@ -935,9 +955,9 @@ void TGNTrainer::adam_prepare() {
                              stream_));
 }
 
-void TGNTrainer::adam() {
+void TGNTrainer::adam(cudaStream_t st) {
     const double b1 = cfg_.beta1, b2 = cfg_.beta2;
-    launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, stream_,
+    launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, st,
         params_.p, grads_.p, adam_m_.p, adam_v_.p, lay_.total, float(total_workers_), cfg_.lr,
         cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2),
         static_cast<const float*>(adam_bc_.p), cfg_.adam_eps,
@@ -957,10 +977,13 @@ void TGNTrainer::set_ctl(Worker& w, std::uint64_t lo, std::uint64_t nb) {
 void TGNTrainer::step_body(const std::vector<int>& Bs) {
     grads_.zero(stream_);
     tgrad_.zero(stream_);
+    std::size_t last = workers_.size();
+    for (std::size_t k = 0; k < workers_.size(); ++k)
+        if (Bs[k] > 0) last = k;
     for (std::size_t k = 0; k < workers_.size(); ++k) {
         Worker& w = *workers_[k];
         if (Bs[k] == 0) continue;
-        worker_step(w, devview(w), Bs[k], true, static_cast<int>(k));
+        worker_step(w, devview(w), Bs[k], true, static_cast<int>(k), k != last);
         if (debug_) {  // taps before the next worker reuses the scratch
             const std::uint64_t B = w.last_b;
             const int D = lay_.D, K = lay_.Kn;
@@ -975,8 +998,20 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
             SPD_CUDA(cudaStreamSynchronize(stream_));
         }
     }
-    timed("allreduce", [&] { allreduce_grads(); });
-    timed("adam", [&] { adam(); });
+    // the last worker's post phase (memory persist, last messages) and the
+    // gradient all-reduce + Adam touch disjoint state: run them side by side
+    if (profile_ || last == workers_.size()) {
+        if (last != workers_.size()) worker_post_kernels(*workers_[last]);
+        timed("allreduce", [&] { allreduce_grads(stream_); });
+        timed("adam", [&] { adam(stream_); });
+        return;
+    }
+    side([&](cudaStream_t sd) {
+        allreduce_grads(sd);
+        adam(sd);
+    });
+    worker_post_kernels(*workers_[last]);
+    join_side();
 }
 
 void TGNTrainer::step(float* loss_out) {
