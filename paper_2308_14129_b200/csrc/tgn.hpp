@@ -65,8 +65,8 @@ struct Worker {
     DevBuf<std::uint32_t> pU, pOther, pEv;  // pending set (<= 2B)
     DevBuf<double> pTs;
     DevBuf<std::int32_t> nU;         // device-resident |pending|
-    DevBuf<std::uint64_t> ctl;       // per-step control: batch start, negative base
-    std::uint64_t ctl_host[2] = {0, 0};
+    const std::uint64_t* ctl = nullptr;  // per-step control words in the trainer's block
+    int ctl_index = 0;                   // its position in that block
     std::vector<std::uint32_t> shared_local;  // local row of each shared node (or UINT32_MAX)
     // schedule
     std::uint64_t batches = 0, pos = 0, loops = 0;
@@ -144,25 +144,40 @@ private:
     void worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx,
                      bool post = true);
     void worker_post_kernels(Worker& w);
-    // host -> device per-step control words (pageable async copy: staged at
-    // call time, applied in stream order, so graph replays see fresh values)
+    // Per-step control words (every worker's batch start and negative base,
+    // Adam's bias corrections) are staged host-side by set_ctl / adam_prepare
+    // and shipped as one block by commit_ctl from a ring of pinned slots
+    // (asynchronous, stream-ordered: graph replays see fresh values and the
+    // host never waits for the device).
     void set_ctl(Worker& w, std::uint64_t lo, std::uint64_t nb);
+    void commit_ctl();
     void step_body(const std::vector<int>& Bs);  // worker steps + all-reduce + Adam (capturable)
     void adam_prepare();
     void backward(Worker& w, const tgnk::WorkerDev& wd, int B);
     void worker_post(Worker& w);
     void flush_pending(Worker& w);
-    void gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train);
+    void gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
+                     const std::function<void()>& after_gather = {});
     void allreduce_grads(cudaStream_t st);
     void adam(cudaStream_t st);
     void sync_shared();
     void timed(const char* name, const std::function<void()>& f);
     // weight-gradient GEMMs run on a side stream forked from the main stream at
     // the point their inputs exist, and joined back once per worker step
-    void side(const std::function<void(cudaStream_t)>& f);
+    void side(const std::function<void(cudaStream_t)>& f, int which = -1);
     void join_side();
-    cudaStream_t side_ = nullptr;
-    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    // Side streams: independent off-critical-path work (weight gradients, the
+    // neighbour search, Adam) is spread round-robin over kSide streams, each
+    // with its own slice of the split-K workspace, and joined where needed.
+    static constexpr int kSide = 4;
+    cudaStream_t sides_[kSide] = {};
+    cudaEvent_t ev_join_[kSide] = {};
+    bool side_used_[kSide] = {};
+    int side_next_ = 0;
+    cudaStream_t side_ = nullptr;  // == sides_[0]: the neighbour-search / time-encoding stream
+    cudaEvent_t ev_fork_ = nullptr;
+    float* ws_cur_ = nullptr;      // workspace slice of the side task being issued
+    std::size_t wsn_cur_ = 0;
     // a second fork for the GRU's hidden-side gate GEMM, and the points of the
     // side stream the main stream waits for (neighbours found, phases evaluated)
     cudaStream_t aux_ = nullptr;
@@ -182,8 +197,14 @@ private:
     std::vector<NodeId> shared_;
     DevBuf<float> params_, grads_, adam_m_, adam_v_;
     DevBuf<float> params_tc_;  // tf32-rounded copy read by the tensor-core GEMMs
-    DevBuf<float> adam_bc_;    // Adam bias corrections of the current step (device)
-    float adam_bc_host_[2] = {1.f, 1.f};
+    DevBuf<std::uint64_t> ctl_dev_;  // [2 per worker | Adam bias corrections (2 x f32)]
+    std::vector<std::uint64_t> ctl_stage_;
+    static constexpr int kCtlSlots = 64;
+    std::uint64_t* ctl_ring_ = nullptr;  // pinned [kCtlSlots][ctl words]
+    cudaEvent_t ctl_ev_[kCtlSlots] = {};
+    bool ctl_used_[kCtlSlots] = {};
+    std::uint64_t ctl_next_ = 0;
+    const float* adam_bc_ = nullptr;
     // CUDA graph of the regular step (every local worker on a full batch)
     cudaGraphExec_t graph_exec_ = nullptr;
     std::uint64_t graph_kernels_ = 0;

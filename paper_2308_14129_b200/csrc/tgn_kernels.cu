@@ -33,6 +33,13 @@ __global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
     else buf[i] = 0.f;
 }
 
+__global__ void k_zero2(float* a, std::size_t na, double* b, std::size_t nb) {
+    pdl_entry();
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < na) a[i] = 0.f;
+    if (i < nb) b[i] = 0.0;
+}
+
 // K5 + K8: roots (src | dst | neg) and the recent-k neighbours strictly
 // before t: lower_bound of t in the node's time-sorted adjacency, last K
 // entries. One warp per root: a 33-ary search (32 lanes probe, a ballot

@@ -39,11 +39,17 @@ void launch(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaSt
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    // the stream's priority, explicit on the launch so graph kernel nodes keep
+    // it: side-stream work yields SMs to the critical path
+    int prio = 0;
+    SPD_CUDA(cudaStreamGetPriority(s, &prio));
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = prio;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     SPD_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(std::forward<Args>(args))...));
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -281,7 +287,7 @@ tgnk::WorkerDev devview(Worker& w) {
     v.pool = w.pool.p; v.n_pool = w.n_pool; v.mem = w.mem.p; v.lu = w.lu.p; v.slot = w.slot.p;
     v.lastpos = w.lastpos.p; v.pU = w.pU.p; v.pOther = w.pOther.p; v.pEv = w.pEv.p; v.pTs = w.pTs.p;
     v.nU = w.nU.p;
-    v.ctl = w.ctl.p;
+    v.ctl = w.ctl;
     return v;
 }
 
@@ -337,9 +343,13 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     int prio_lo = 0, prio_hi = 0;
     SPD_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SPD_CUDA(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, prio_hi));
-    SPD_CUDA(cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, prio_lo));
+    for (int k = 0; k < kSide; ++k) {
+        SPD_CUDA(cudaStreamCreateWithPriority(&sides_[k], cudaStreamNonBlocking, prio_lo));
+        SPD_CUDA(cudaEventCreateWithFlags(&ev_join_[k], cudaEventDisableTiming));
+    }
+    side_ = sides_[0];
     SPD_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
-    SPD_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+
     SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
     for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_phi_})
         SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -432,7 +442,6 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
         w.pU.alloc(2 * B); w.pOther.alloc(2 * B); w.pEv.alloc(2 * B); w.pTs.alloc(2 * B);
         w.nU.alloc(1); w.nU.zero(stream_);
-        w.ctl.alloc(2); w.ctl.zero(stream_);
         for (NodeId sidx : shared_) {
             auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), sidx);
             w.shared_local.push_back(it != w.nodes.end() && *it == sidx
@@ -449,7 +458,21 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     init_params_host(lay_, cfg.seed_init, flat);
     params_.alloc(lay_.total); params_.upload(flat.data(), lay_.total, stream_);
     params_tc_.alloc(lay_.total);
-    adam_bc_.alloc(2);
+    // per-step control block (see commit_ctl)
+    {
+        const std::size_t words = 2 * workers_.size() + 1;
+        ctl_dev_.alloc(words);
+        ctl_dev_.zero(stream_);
+        ctl_stage_.assign(words, 0);
+        for (std::size_t k = 0; k < workers_.size(); ++k) {
+            workers_[k]->ctl = ctl_dev_.p + 2 * k;
+            workers_[k]->ctl_index = static_cast<int>(k);
+        }
+        adam_bc_ = reinterpret_cast<const float*>(ctl_dev_.p + 2 * workers_.size());
+        SPD_CUDA(cudaHostAlloc(&ctl_ring_, std::size_t(kCtlSlots) * words * sizeof(std::uint64_t),
+                               cudaHostAllocDefault));
+        for (auto& e : ctl_ev_) SPD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     refresh_tc_weights();
     grads_.alloc(lay_.total); grads_.zero(stream_);
     adam_m_.alloc(lay_.total); adam_m_.zero(stream_);
@@ -517,23 +540,40 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
 
 int TGNTrainer::feat_stride() const { return s_->d.Fp; }
 
-void TGNTrainer::side(const std::function<void(cudaStream_t)>& f) {
+// Fork f onto a side stream (round-robin unless `which` pins one) at the
+// current point of the main stream; f's split-K GEMMs use ws_cur_/wsn_cur_.
+void TGNTrainer::side(const std::function<void(cudaStream_t)>& f, int which) {
+    const int k = which >= 0 ? which : (side_next_++ % kSide);
     SPD_CUDA(cudaEventRecord(ev_fork_, stream_));
-    SPD_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
-    f(side_);
+    SPD_CUDA(cudaStreamWaitEvent(sides_[k], ev_fork_, 0));
+    const std::size_t slice = s_->ws.n / kSide;
+    ws_cur_ = s_->ws.p + slice * k;
+    wsn_cur_ = slice;
+    side_used_[k] = true;
+    f(sides_[k]);
 }
 
 void TGNTrainer::join_side() {
-    SPD_CUDA(cudaEventRecord(ev_join_, side_));
-    SPD_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+    for (int k = 0; k < kSide; ++k) {
+        if (!side_used_[k]) continue;
+        SPD_CUDA(cudaEventRecord(ev_join_[k], sides_[k]));
+        SPD_CUDA(cudaStreamWaitEvent(stream_, ev_join_[k], 0));
+        side_used_[k] = false;
+    }
 }
 
 TGNTrainer::~TGNTrainer() {
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (auto e : ctl_ev_)
+        if (e) cudaEventDestroy(e);
+    if (ctl_ring_) cudaFreeHost(ctl_ring_);
     if (stage_) cudaFreeHost(stage_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
-    if (ev_join_) cudaEventDestroy(ev_join_);
-    if (side_) cudaStreamDestroy(side_);
+    for (int k = 0; k < kSide; ++k) {
+        if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
+        if (sides_[k]) cudaStreamDestroy(sides_[k]);
+    }
     for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_phi_})
         if (e) cudaEventDestroy(e);
     if (aux_) cudaStreamDestroy(aux_);
@@ -601,7 +641,8 @@ void TGNTrainer::seek(std::uint64_t step) {
     SPD_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train) {
+void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
+                             const std::function<void()>& after_gather) {
     Scratch& s = *s_;
     const auto& d = s.d;
     const float* P = params_.p;
@@ -609,7 +650,7 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train) {
     const float* PW = tc ? params_tc_.p : params_.p;  // tf32-rounded weights for tensor cores
     launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
         wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
-    SPD_CUDA(cudaGetLastError());
+    if (after_gather) after_gather();
     // the two gate GEMMs are independent: the hidden-side one on the aux stream
     SPD_CUDA(cudaEventRecord(ev_aux_fork_, stream_));
     SPD_CUDA(cudaStreamWaitEvent(aux_, ev_aux_fork_, 0));
@@ -665,15 +706,20 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     if (profile_) {
         timed("roots_nbrs", [&] { roots(st); });
         timed("phi", [&] { phi(st); });
-    } else {
-        side([&](cudaStream_t sd) {
-            roots(sd);
-            SPD_CUDA(cudaEventRecord(ev_roots_, sd));
-            phi(sd);
-            SPD_CUDA(cudaEventRecord(ev_phi_, sd));
-        });
     }
-    timed("gru_fwd", [&] { gru_forward(w, wd, train); });
+    // (the side-stream branch is forked after the GRU's first kernel is
+    // enqueued: graph replays submit independent branches in creation order)
+    timed("gru_fwd", [&] {
+        gru_forward(w, wd, train, [&] {
+            if (profile_) return;
+            side([&](cudaStream_t sd) {
+                roots(sd);
+                SPD_CUDA(cudaEventRecord(ev_roots_, sd));
+                phi(sd);
+                SPD_CUDA(cudaEventRecord(ev_phi_, sd));
+            }, 0);
+        });
+    });
     if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_roots_, 0));
     timed("query_gather", [&] {
         launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
@@ -746,27 +792,27 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     const float* PW = tc ? params_tc_.p : params_.p;
     timed("head_bwd", [&] {
         side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
-                   2 * B, nullptr, s.ws.p, s.ws.n, sd); });
+                   2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
         side([&](cudaStream_t sd) { gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
-                   2 * d.D + 1, 2 * B, nullptr, s.ws.p, s.ws.n, sd); });
+                   2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
         gemm_dgrad(s.dD1.p, d.D, P + lay_.dec1.off, lay_.dec1.ld, s.dd_in.p, d.ld_din, 2 * B,
                    2 * d.D, d.D, nullptr, st);
         launch(tgnk::k_dec_scatter, blocks_for(std::size_t(B) * 32), 256, 0, st, d, B, s.dd_in.p,
                                                                              s.d_emb.p);
         // merge layer 2 (relu mask from Z1), layer 1
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off, lay_.mrg2.ld, d.D, d.D + 1,
-                   R, nullptr, s.ws.p, s.ws.n, sd); });
+                   R, nullptr, ws_cur_, wsn_cur_, sd); });
         proj_dgrad(tc, s.d_emb.p, d.D, PW + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
                    nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z, tc);
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off, lay_.mrg1.ld, d.D,
-                   d.DQ + d.D + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
+                   d.DQ + d.D + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
         proj_dgrad(tc, s.dZ1.p, d.D, PW + lay_.mrg1.off, lay_.mrg1.ld, s.dm_in.p, d.ld_m, R,
                    d.DQ + d.D, d.D, nullptr, st, 0, nullptr, 0, tc);
         launch(tgnk::k_mask_rows, blocks_for(std::size_t(R) * 32), 256, 0, st, s.dm_in.p, R, d.DQ,
                                                                           d.ld_m, s.cnt.p);
         // output projection
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
-                   d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
+                   d.DQ + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
         proj_dgrad(tc, s.dm_in.p, d.ld_m, PW + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R, d.DQ,
                    d.DQ, nullptr, st, 0, nullptr, 0, tc);
     });
@@ -802,7 +848,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     });
     timed("q_bwd", [&] {
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
-                   d.DQ + 1, R, nullptr, s.ws.p, s.ws.n, sd); });
+                   d.DQ + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
         proj_dgrad(tc, s.dQ.p, d.ld_Q, PW + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
                    d.DQ, nullptr, st);
     });
@@ -823,9 +869,9 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         launch(tgnk::k_gru_bwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, st, 
             wd, d, s.dH.p, s.gsave.p, s.h_gru.p, s.dGi.p, s.dGh.p);
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
-                   3 * d.D, d.DM + 1, s.U, w.nU.p, s.ws.p, s.ws.n, sd); });
+                   3 * d.D, d.DM + 1, s.U, w.nU.p, ws_cur_, wsn_cur_, sd); });
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
-                   3 * d.D, d.D + 1, s.U, w.nU.p, s.ws.p, s.ws.n, sd); });
+                   3 * d.D, d.D + 1, s.U, w.nU.p, ws_cur_, wsn_cur_, sd); });
     });
     // side-stream weight grads read the pending set (nU, GRU inputs) that the
     // post phase rewrites: join first
@@ -949,10 +995,20 @@ void TGNTrainer::allreduce_grads(cudaStream_t st) {
 
 void TGNTrainer::adam_prepare() {
     ++adam_t_;
-    adam_bc_host_[0] = static_cast<float>(1.0 - std::pow(double(cfg_.beta1), double(adam_t_)));
-    adam_bc_host_[1] = static_cast<float>(1.0 - std::pow(double(cfg_.beta2), double(adam_t_)));
-    SPD_CUDA(cudaMemcpyAsync(adam_bc_.p, adam_bc_host_, sizeof(adam_bc_host_), cudaMemcpyHostToDevice,
-                             stream_));
+    const float bc[2] = {static_cast<float>(1.0 - std::pow(double(cfg_.beta1), double(adam_t_))),
+                         static_cast<float>(1.0 - std::pow(double(cfg_.beta2), double(adam_t_)))};
+    std::memcpy(&ctl_stage_.back(), bc, sizeof(bc));
+}
+
+void TGNTrainer::commit_ctl() {
+    const int slot = static_cast<int>(ctl_next_++ % kCtlSlots);
+    if (ctl_used_[slot]) SPD_CUDA(cudaEventSynchronize(ctl_ev_[slot]));  // its copy ran ~64 steps ago
+    std::uint64_t* h = ctl_ring_ + std::size_t(slot) * ctl_stage_.size();
+    std::memcpy(h, ctl_stage_.data(), ctl_stage_.size() * sizeof(std::uint64_t));
+    SPD_CUDA(cudaMemcpyAsync(ctl_dev_.p, h, ctl_stage_.size() * sizeof(std::uint64_t),
+                             cudaMemcpyHostToDevice, stream_));
+    SPD_CUDA(cudaEventRecord(ctl_ev_[slot], stream_));
+    ctl_used_[slot] = true;
 }
 
 void TGNTrainer::adam(cudaStream_t st) {
@@ -960,23 +1016,24 @@ void TGNTrainer::adam(cudaStream_t st) {
     launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, st,
         params_.p, grads_.p, adam_m_.p, adam_v_.p, lay_.total, float(total_workers_), cfg_.lr,
         cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2),
-        static_cast<const float*>(adam_bc_.p), cfg_.adam_eps,
+        adam_bc_, cfg_.adam_eps,
         cfg_.gemm_mode == 1 ? params_tc_.p : nullptr);
     SPD_CUDA(cudaGetLastError());
 }
 
 void TGNTrainer::set_ctl(Worker& w, std::uint64_t lo, std::uint64_t nb) {
-    w.ctl_host[0] = lo;
-    w.ctl_host[1] = nb;
-    SPD_CUDA(cudaMemcpyAsync(w.ctl.p, w.ctl_host, sizeof(w.ctl_host), cudaMemcpyHostToDevice, stream_));
+    ctl_stage_[2 * w.ctl_index] = lo;
+    ctl_stage_[2 * w.ctl_index + 1] = nb;
 }
 
 // Everything a global step launches once the per-step control words are on
 // the device: the local workers' batches, the gradient all-reduce and Adam.
 // Bs[k] = batch size of local worker k (0: idle). Capturable as a CUDA graph.
 void TGNTrainer::step_body(const std::vector<int>& Bs) {
-    grads_.zero(stream_);
-    tgrad_.zero(stream_);
+    // gradient buffers cleared by a kernel, not memset nodes: in a graph
+    // replay a memset node costs a copy-engine hand-off before the first kernel
+    launch(tgnk::k_zero2, blocks_for(lay_.total), 256, 0, stream_, grads_.p, lay_.total, tgrad_.p,
+           std::size_t(2) * ld4(lay_.T));
     std::size_t last = workers_.size();
     for (std::size_t k = 0; k < workers_.size(); ++k)
         if (Bs[k] > 0) last = k;
@@ -1035,6 +1092,7 @@ void TGNTrainer::step(float* loss_out) {
                                 step_in_epoch_));
     }
     adam_prepare();
+    commit_ctl();
     // capture only after one eager full step (lazy attribute setup done)
     const bool graph_ok = use_graph_ && full && !profile_ && !debug_ && eager_full_steps_ > 0;
     if (!graph_ok && full) ++eager_full_steps_;
@@ -1410,6 +1468,7 @@ void TGNTrainer::evaluate(int wid, std::uint64_t lo, std::uint64_t hi, std::uint
     for (std::uint64_t b0 = lo; b0 < hi; b0 += cfg_.batch_size) {
         const int B = static_cast<int>(std::min<std::uint64_t>(hi, b0 + cfg_.batch_size) - b0);
         set_ctl(w, w.E + b0, neg_base(neg_seed, 0xE7A1ull, std::uint64_t(w.gid), b0));
+        commit_ctl();
         worker_step(w, v, B, false, slot_idx);
         lg.resize(2 * B);
         s_->logits.download(lg.data(), 2 * B, stream_);

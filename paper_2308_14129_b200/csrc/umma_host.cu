@@ -80,11 +80,15 @@ void reduce(const float* ws, int split, int M, int N, int ldws, float* C, int ld
     cfg.gridDim = dim3(unsigned((n + 255) / 256));
     cfg.blockDim = dim3(256);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int prio = 0;
+    SPD_CUDA(cudaStreamGetPriority(s, &prio));
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = prio;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     SPD_CUDA(cudaLaunchKernelEx(&cfg, k_splitk_reduce, ws, split, M, N, ldws, C, ldc,
                                 static_cast<long long>(bt.c), bt.n));
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
@@ -104,16 +108,22 @@ void run(const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = C_::SMEM;
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[3];
+    int prio = 0;  // the stream's priority, explicit so graph kernel nodes keep it
+    SPD_CUDA(cudaStreamGetPriority(s, &prio));
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = prio;
     attr[1].id = cudaLaunchAttributeClusterDimension;
     attr[1].val.clusterDim.x = 1;
     attr[1].val.clusterDim.y = CL;
     attr[1].val.clusterDim.z = 1;
-    const bool pdl = pdl_enabled();
-    cfg.attrs = pdl ? attr : attr + 1;
-    cfg.numAttrs = (pdl ? 1 : 0) + (CL > 1 ? 1 : 0);
+    attr[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
+    attr[2].val.programmaticStreamSerializationAllowed = 1;
+    int na = 1;
+    if (CL > 1) attr[na++] = attr[1];
+    if (pdl_enabled()) attr[na++] = attr[2];
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, args));
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
