@@ -62,9 +62,16 @@ struct Worker {
     DevBuf<double> lu, lu_snap;      // N
     DevBuf<std::int32_t> slot;       // N: node -> row of the pending set, -1
     DevBuf<std::int32_t> lastpos;    // N: scratch for last-message selection
-    DevBuf<std::uint32_t> pU, pOther, pEv;  // pending set (<= 2B)
-    DevBuf<double> pTs;
-    DevBuf<std::int32_t> nU;         // device-resident |pending|
+    // pending last-message sets (<= 2B each), double-buffered: a step's GRU
+    // reads pend[cur] (the previous batch's messages) while k_pending writes
+    // this batch's into pend[cur ^ 1]; cur flips after the step
+    struct PendingSet {
+        DevBuf<std::uint32_t> pU, pOther, pEv;
+        DevBuf<double> pTs;
+        DevBuf<std::int32_t> nU;  // device-resident |pending|
+    } pend[2];
+    int cur = 0;
+    std::int32_t* nU() { return pend[cur].nU.p; }
     const std::uint64_t* ctl = nullptr;  // per-step control words in the trainer's block
     int ctl_index = 0;                   // its position in that block
     std::vector<std::uint32_t> shared_local;  // local row of each shared node (or UINT32_MAX)
@@ -206,7 +213,7 @@ private:
     std::uint64_t ctl_next_ = 0;
     const float* adam_bc_ = nullptr;
     // CUDA graph of the regular step (every local worker on a full batch)
-    cudaGraphExec_t graph_exec_ = nullptr;
+    cudaGraphExec_t graph_exec_[2] = {};  // one per pending-set parity
     std::uint64_t graph_kernels_ = 0;
     bool use_graph_ = true;
     std::uint64_t eager_full_steps_ = 0;

@@ -382,7 +382,8 @@ __global__ void k_persist(WorkerDev w, int D, const float* mem_new) {
 
 // K3 last-message selection: endpoint slots q = 2k (src), 2k+1 (dst) of the
 // batch's events; per node the max slot wins (max (ts, stream index)),
-// compacted in slot order. Single block; lastpos starts and ends at -1.
+// compacted in slot order into the worker's other pending set (nx*).
+// Single block; lastpos starts and ends at -1.
 __global__ void k_pending(WorkerDev w, int B) {
     pdl_entry();
     const std::uint64_t lo = w.ctl[0];
@@ -435,16 +436,16 @@ __global__ void k_pending(WorkerDev w, int B) {
         __syncthreads();
         const int pos = base + warp_tot[wid] + pre;
         if (win) {
-            w.pU[pos] = node;
-            w.pOther[pos] = other;
-            w.pEv[pos] = (std::uint32_t)e;
-            w.pTs[pos] = w.ev_ts[e];
+            w.nxU[pos] = node;
+            w.nxOther[pos] = other;
+            w.nxEv[pos] = (std::uint32_t)e;
+            w.nxTs[pos] = w.ev_ts[e];
         }
         __syncthreads();
         if (tid == nt - 1) base = pos + win;
         __syncthreads();
     }
-    if (tid == 0) *w.nU = base;
+    if (tid == 0) *w.nxN = base;
     for (int q = tid; q < nslots; q += nt) {
         const std::uint64_t e = lo + (q >> 1);
         const std::uint32_t node = (q & 1) ? w.ev_dst[e] : w.ev_src[e];

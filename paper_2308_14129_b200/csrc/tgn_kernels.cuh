@@ -44,6 +44,12 @@ struct WorkerDev {
     std::uint32_t* pEv;
     double* pTs;
     std::int32_t* nU;
+    // the other pending set, written by k_pending with this batch's messages
+    std::uint32_t* nxU;
+    std::uint32_t* nxOther;
+    std::uint32_t* nxEv;
+    double* nxTs;
+    std::int32_t* nxN;
     // per-step control written by the host before each step (stream-ordered,
     // so a captured CUDA graph replays with fresh values): [0] first event of
     // the batch, [1] negative-sampling base (oracle: negatives())

@@ -285,8 +285,11 @@ tgnk::WorkerDev devview(Worker& w) {
     v.ev_src = w.ev_src.p; v.ev_dst = w.ev_dst.p; v.ev_ts = w.ev_ts.p; v.feat = w.feat.p;
     v.adj_off = w.adj_off.p; v.adj_nbr = w.adj_nbr.p; v.adj_ev = w.adj_ev.p; v.adj_ts = w.adj_ts.p;
     v.pool = w.pool.p; v.n_pool = w.n_pool; v.mem = w.mem.p; v.lu = w.lu.p; v.slot = w.slot.p;
-    v.lastpos = w.lastpos.p; v.pU = w.pU.p; v.pOther = w.pOther.p; v.pEv = w.pEv.p; v.pTs = w.pTs.p;
-    v.nU = w.nU.p;
+    const Worker::PendingSet& c = w.pend[w.cur];
+    const Worker::PendingSet& n = w.pend[w.cur ^ 1];
+    v.lastpos = w.lastpos.p; v.pU = c.pU.p; v.pOther = c.pOther.p; v.pEv = c.pEv.p; v.pTs = c.pTs.p;
+    v.nU = c.nU.p;
+    v.nxU = n.pU.p; v.nxOther = n.pOther.p; v.nxEv = n.pEv.p; v.nxTs = n.pTs.p; v.nxN = n.nU.p;
     v.ctl = w.ctl;
     return v;
 }
@@ -440,8 +443,10 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         SPD_CUDA(cudaMemsetAsync(w.slot.p, 0xFF, w.slot.bytes(), stream_));
         w.lastpos.alloc(N);
         SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
-        w.pU.alloc(2 * B); w.pOther.alloc(2 * B); w.pEv.alloc(2 * B); w.pTs.alloc(2 * B);
-        w.nU.alloc(1); w.nU.zero(stream_);
+        for (auto& ps : w.pend) {
+            ps.pU.alloc(2 * B); ps.pOther.alloc(2 * B); ps.pEv.alloc(2 * B); ps.pTs.alloc(2 * B);
+            ps.nU.alloc(1); ps.nU.zero(stream_);
+        }
         for (NodeId sidx : shared_) {
             auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), sidx);
             w.shared_local.push_back(it != w.nodes.end() && *it == sidx
@@ -563,7 +568,8 @@ void TGNTrainer::join_side() {
 }
 
 TGNTrainer::~TGNTrainer() {
-    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    for (auto g : graph_exec_)
+        if (g) cudaGraphExecDestroy(g);
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto e : ctl_ev_)
         if (e) cudaEventDestroy(e);
@@ -636,7 +642,7 @@ void TGNTrainer::seek(std::uint64_t step) {
         w.done = w.loops > 0;
         w.mem.zero(stream_);
         w.lu.zero(stream_);
-        w.nU.zero(stream_);
+        for (auto& ps : w.pend) ps.nU.zero(stream_);
     }
     SPD_CUDA(cudaStreamSynchronize(stream_));
 }
@@ -655,9 +661,9 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
     SPD_CUDA(cudaEventRecord(ev_aux_fork_, stream_));
     SPD_CUDA(cudaStreamWaitEvent(aux_, ev_aux_fork_, 0));
     proj_fwd(tc, s.h_gru.p, d.ld_h, PW + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, 3 * d.D,
-             d.D + 1, w.nU.p, aux_);
+             d.D + 1, w.nU(), aux_);
     proj_fwd(tc, s.x_gru.p, d.ld_x, PW + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, 3 * d.D,
-             d.DM + 1, w.nU.p, stream_);
+             d.DM + 1, w.nU(), stream_);
     SPD_CUDA(cudaEventRecord(ev_aux_join_, aux_));
     SPD_CUDA(cudaStreamWaitEvent(stream_, ev_aux_join_, 0));
     launch(tgnk::k_gru_fwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, stream_, 
@@ -674,7 +680,6 @@ void TGNTrainer::worker_post_kernels(Worker& w) {
     timed("post", [&] {
         launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, wd, s.d.D,
                s.mem_new.p);
-        launch(tgnk::k_pending, 1, 1024, 0, stream_, wd, w.last_b);
     });
 }
 
@@ -707,6 +712,11 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         timed("roots_nbrs", [&] { roots(st); });
         timed("phi", [&] { phi(st); });
     }
+    // this batch's last messages into the other pending set (K3): depends only
+    // on the batch's events, off the critical path (the GRU below reads the
+    // current set); eval steps run it in their post phase
+    if (train)
+        side([&](cudaStream_t sd) { launch(tgnk::k_pending, 1, 1024, 0, sd, wd, B); });
     // (the side-stream branch is forked after the GRU's first kernel is
     // enqueued: graph replays submit independent branches in creation order)
     timed("gru_fwd", [&] {
@@ -775,7 +785,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     if (!post) return;
     timed("post", [&] {
         launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
-        launch(tgnk::k_pending, 1, 1024, 0, st, wd, B);
+        if (!train) launch(tgnk::k_pending, 1, 1024, 0, st, wd, B);
     });
 }
 
@@ -869,9 +879,9 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         launch(tgnk::k_gru_bwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, st, 
             wd, d, s.dH.p, s.gsave.p, s.h_gru.p, s.dGi.p, s.dGh.p);
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
-                   3 * d.D, d.DM + 1, s.U, w.nU.p, ws_cur_, wsn_cur_, sd); });
+                   3 * d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
-                   3 * d.D, d.D + 1, s.U, w.nU.p, ws_cur_, wsn_cur_, sd); });
+                   3 * d.D, d.D + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
     });
     // side-stream weight grads read the pending set (nU, GRU inputs) that the
     // post phase rewrites: join first
@@ -884,7 +894,7 @@ void TGNTrainer::flush_pending(Worker& w) {
     gru_forward(w, wd, false);
     launch(tgnk::k_persist, blocks_for(std::size_t(s_->U) * 32), 256, 0, stream_, wd, lay_.D,
            s_->mem_new.p);
-    w.nU.zero(stream_);
+    w.pend[w.cur].nU.zero(stream_);
 }
 
 // GEMM kernels on caller-owned device buffers, for numerics tests against a
@@ -971,6 +981,7 @@ void TGNTrainer::step_host(const spd_edge* const* events, const std::uint16_t* c
 }
 
 void TGNTrainer::worker_post(Worker& w) {
+    w.cur ^= 1;  // the set k_pending just filled holds the messages to apply next
     ++w.pos;
     if (w.pos == w.batches) {  // loop_end: flush (new params) + snapshot (pac_sim.cpp:248-255)
         flush_pending(w);
@@ -1086,31 +1097,42 @@ void TGNTrainer::step(float* loss_out) {
         if (w.pos == 0) {  // loop_start: reset (pac_sim.cpp:238)
             w.mem.zero(stream_);
             w.lu.zero(stream_);
-            w.nU.zero(stream_);
+            for (auto& ps : w.pend) ps.nU.zero(stream_);
         }
         set_ctl(w, lo, neg_base(cfg_.seed_neg, std::uint64_t(epoch_), std::uint64_t(w.gid),
                                 step_in_epoch_));
     }
     adam_prepare();
     commit_ctl();
+    // one graph per pending-set parity (the sets' pointers are baked in); all
+    // active workers flip together on full-batch steps
+    int par = -1;
+    bool same_par = true;
+    for (std::size_t k = 0; k < workers_.size(); ++k)
+        if (Bs[k] > 0) {
+            if (par < 0) par = workers_[k]->cur;
+            same_par = same_par && workers_[k]->cur == par;
+        }
     // capture only after one eager full step (lazy attribute setup done)
-    const bool graph_ok = use_graph_ && full && !profile_ && !debug_ && eager_full_steps_ > 0;
+    const bool graph_ok = use_graph_ && full && same_par && par >= 0 && !profile_ && !debug_ &&
+                          eager_full_steps_ > 0;
     if (!graph_ok && full) ++eager_full_steps_;
     if (graph_ok) {
         // regular step: replay the captured graph (launch-free, fork/join of
         // the side stream preserved); capture it on first use
-        if (!graph_exec_) {
+        cudaGraphExec_t& graph_exec = graph_exec_[par];
+        if (!graph_exec) {
             const std::uint64_t k0 = kernel_launches();
             cudaGraph_t graph;
             SPD_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
             step_body(Bs);
             SPD_CUDA(cudaStreamEndCapture(stream_, &graph));
-            SPD_CUDA(cudaGraphInstantiate(&graph_exec_, graph, 0));
+            SPD_CUDA(cudaGraphInstantiate(&graph_exec, graph, 0));
             SPD_CUDA(cudaGraphDestroy(graph));
             graph_kernels_ = kernel_launches() - k0;
             g_kernel_launches.fetch_sub(graph_kernels_, std::memory_order_relaxed);
         }
-        SPD_CUDA(cudaGraphLaunch(graph_exec_, stream_));
+        SPD_CUDA(cudaGraphLaunch(graph_exec, stream_));
         g_kernel_launches.fetch_add(graph_kernels_, std::memory_order_relaxed);
     } else {
         step_body(Bs);
@@ -1132,7 +1154,7 @@ void TGNTrainer::end_epoch() {
         Worker& w = *wp;
         SPD_CUDA(cudaMemcpyAsync(w.mem.p, w.mem_snap.p, w.mem.bytes(), cudaMemcpyDeviceToDevice, stream_));
         SPD_CUDA(cudaMemcpyAsync(w.lu.p, w.lu_snap.p, w.lu.bytes(), cudaMemcpyDeviceToDevice, stream_));
-        w.nU.zero(stream_);
+        for (auto& ps : w.pend) ps.nU.zero(stream_);
     }
     sync_shared();
     SPD_CUDA(cudaStreamSynchronize(stream_));
@@ -1457,10 +1479,13 @@ void TGNTrainer::evaluate(int wid, std::uint64_t lo, std::uint64_t hi, std::uint
     Worker& w = worker(wid);
     if (hi > w.E_eval || lo > hi) usage_error("eval range outside the eval events");
     DeviceGuard g(device_);
-    tgnk::WorkerDev v = devview(w);
-    v.ev_src = w.x_src.p; v.ev_dst = w.x_dst.p; v.ev_ts = w.x_ts.p; v.feat = w.x_feat.p;
-    v.adj_off = w.x_adj_off.p; v.adj_nbr = w.x_adj_nbr.p; v.adj_ev = w.x_adj_ev.p;
-    v.adj_ts = w.x_adj_ts.p; v.pool = w.x_pool.p; v.n_pool = w.x_n_pool;
+    auto eval_view = [&] {
+        tgnk::WorkerDev v = devview(w);
+        v.ev_src = w.x_src.p; v.ev_dst = w.x_dst.p; v.ev_ts = w.x_ts.p; v.feat = w.x_feat.p;
+        v.adj_off = w.x_adj_off.p; v.adj_nbr = w.x_adj_nbr.p; v.adj_ev = w.x_adj_ev.p;
+        v.adj_ts = w.x_adj_ts.p; v.pool = w.x_pool.p; v.n_pool = w.x_n_pool;
+        return v;
+    };
     int slot_idx = 0;
     for (std::size_t k = 0; k < workers_.size(); ++k)
         if (workers_[k].get() == &w) slot_idx = static_cast<int>(k);
@@ -1469,7 +1494,8 @@ void TGNTrainer::evaluate(int wid, std::uint64_t lo, std::uint64_t hi, std::uint
         const int B = static_cast<int>(std::min<std::uint64_t>(hi, b0 + cfg_.batch_size) - b0);
         set_ctl(w, w.E + b0, neg_base(neg_seed, 0xE7A1ull, std::uint64_t(w.gid), b0));
         commit_ctl();
-        worker_step(w, v, B, false, slot_idx);
+        worker_step(w, eval_view(), B, false, slot_idx);
+        w.cur ^= 1;
         lg.resize(2 * B);
         s_->logits.download(lg.data(), 2 * B, stream_);
         SPD_CUDA(cudaStreamSynchronize(stream_));
