@@ -293,12 +293,14 @@ __global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, c
                       const int* cnt, float* phi) {
     pdl_entry();
     const int T4 = d.T / 4;
-    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (std::size_t)R * d.K * T4) return;
+    // grid-stride over (occurrence, 4 columns): launched with a small grid so
+    // it shares the SMs with the critical path's kernels instead of flooding them
+    for (std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+         i < (std::size_t)R * d.K * T4; i += (std::size_t)gridDim.x * blockDim.x) {
     const std::size_t occ = i / T4;
     const int t = 4 * static_cast<int>(i % T4);
     const int r = static_cast<int>(occ / d.K), j = static_cast<int>(occ % d.K);
-    if (j >= cnt[r]) return;
+    if (j >= cnt[r]) continue;
     const double dt = nbr_dt[occ];
     const float4 w = *reinterpret_cast<const float4*>(time_w + t);
     const float4 b = *reinterpret_cast<const float4*>(time_b + t);
@@ -307,6 +309,7 @@ __global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, c
     float* p = phi + occ * 2 * d.T;
     *reinterpret_cast<float4*>(p + t) = make_float4(s0.y, s1.y, s2.y, s3.y);
     *reinterpret_cast<float4*>(p + d.T + t) = make_float4(s0.x, s1.x, s2.x, s3.x);
+    }
 }
 
 __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd) {

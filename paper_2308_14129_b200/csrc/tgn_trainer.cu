@@ -704,7 +704,8 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     };
     auto phi = [&](cudaStream_t sx) {
-        launch(tgnk::k_phi, blocks_for(std::size_t(R) * d.K * (d.T / 4)), 256, 0, sx, d, R,
+        launch(tgnk::k_phi, std::min<unsigned>(blocks_for(std::size_t(R) * d.K * (d.T / 4)), 2 * 148),
+               256, 0, sx, d, R,
                P + lay_.time_w, P + lay_.time_b, static_cast<const double*>(s.nbr_dt.p),
                static_cast<const int*>(s.cnt.p), s.phi.p);
     };
