@@ -61,11 +61,14 @@ def ncu_traffic(kernel):
         return None, None
     rows = list(csv.reader(open(files[-1])))
     h, units = rows[0], rows[1]
+    row = next((r for r in rows[2:] if kernel in r[h.index("Kernel Name")]), None)
+    if row is None:
+        return None, None
     total = 0.0
     for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         i = h.index(name)
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units[i], 1)
-        total += float(rows[2][i].replace(",", "")) * scale
+        total += float(row[i].replace(",", "")) * scale
     return total, os.path.relpath(files[-1], ROOT)
 
 
