@@ -111,6 +111,33 @@ spd_status spd_assignment_edge_part(const spd_assignment* a, int32_t* out);
 spd_status spd_assignment_node_parts(const spd_assignment* a, uint64_t* off, int32_t* parts);
 spd_status spd_assignment_shared(const spd_assignment* a, uint32_t* out);
 
+/* ------------------------------------------------------ on-disk formats (f3)
+ * load_edges / write_edges (graph_io.hpp; graph_io.cpp:106-154): CSV
+ * "src,dst,ts", same acceptance rules, error codes and texts (ParseError
+ * "row N: ...", FileNotFound); rows stable-sorted by ts unless assume_sorted.
+ * *out is malloc'ed: release with spd_free. */
+void spd_free(void* p);
+spd_status spd_load_edges_csv(const char* path, int32_t assume_sorted, spd_edge** out, uint64_t* n,
+                              uint32_t* node_count, double* t_max);
+spd_status spd_write_edges_csv(const char* path, const spd_edge* e, uint64_t n);
+/* Binary event file: 32-B header {"SPDEDGE1", u64 n, u32 node_count, u32 0,
+ * f64 t_max} + n TemporalEdge records (types.hpp:15-20) verbatim. The reader
+ * fills caller memory (e.g. pinned buffers) and validates ids < node_count
+ * (ParseError) and time order (UnsortedStream). */
+spd_status spd_write_edges_bin(const char* path, const spd_edge* e, uint64_t n,
+                               uint32_t node_count, double t_max);
+spd_status spd_edges_bin_info(const char* path, uint64_t* n, uint32_t* node_count, double* t_max);
+spd_status spd_load_edges_bin(const char* path, spd_edge* out, uint64_t cap);
+/* Assignment JSON of the CLI's partition subcommand (speedpart_main.cpp:110-119)
+ * — {"config":<config_json>,"edge_part":[..],"node_parts":{"0":[..],..},
+ * "shared":[..],"discards":n}, compact — and its reader (load_assignment,
+ * speedpart_main.cpp:129-166: missing keys -> ParseError "assignment is
+ * missing '<key>'"; num_parts / k_eff from config.parts / config.topk).
+ * config_out (optional) receives the raw config object text (spd_free). */
+spd_status spd_assignment_write_json(const spd_assignment* a, const char* config_json,
+                                     const char* path);
+spd_status spd_assignment_read_json(const char* path, spd_assignment** out, char** config_out);
+
 /* assign_eval_edges (partitioner.hpp:74-81). */
 typedef struct spd_eval_routing spd_eval_routing;
 spd_status spd_assign_eval_edges(const spd_edge* val, uint64_t n_val, const spd_edge* test,

@@ -35,7 +35,8 @@ def lib():
                   "ref_select_hubs", "ref_score", "ref_partition", "ref_assign_eval_edges",
                   "ref_induce_subgraphs", "ref_shuffle_combine", "ref_model_seeded",
                   "ref_model_update_run", "ref_model_update_threads", "ref_sync_shared",
-                  "ref_digest", "ref_run_epoch", "ref_simulate", "ref_quality"):
+                  "ref_digest", "ref_run_epoch", "ref_simulate", "ref_quality",
+                  "ref_load_edges", "ref_write_edges"):
             getattr(_lib, n).restype = C.c_int
     return _lib
 
@@ -261,3 +262,44 @@ def simulate(edges, node_count, t_max, num_parts, node_parts, shared, num_worker
                         digests=[dg.raw[17 * (ep * W + w):17 * (ep * W + w) + 16].decode()
                                  for w in range(W)]))
     return dict(epochs=eps, sync_events=tot.value)
+
+
+def load_edges(path, assume_sorted=False):
+    """graph_io.cpp:106-140 -> (edges EDGE_DTYPE array, node_count, t_max)."""
+    L = lib()
+    out = C.c_void_p()
+    n, nc, tm = u64(), u32(), f64()
+    _chk(L.ref_load_edges(str(path).encode(), int(assume_sorted), C.byref(out), C.byref(n),
+                          C.byref(nc), C.byref(tm)))
+    arr = np.empty(n.value, dtype=EDGE_DTYPE)
+    if n.value:
+        C.memmove(arr.ctypes.data, out.value, n.value * EDGE_DTYPE.itemsize)
+    L.ref_free(out)
+    return arr, nc.value, tm.value
+
+
+_WRITE_SCRIPT = """
+import ctypes as C, sys
+L = C.CDLL(sys.argv[1])
+raw = open(sys.argv[2], 'rb').read()
+buf = C.create_string_buffer(raw, max(1, len(raw)))
+L.ref_write_edges.argtypes = [C.c_char_p, C.c_void_p, C.c_uint64]
+L.ref_last_error_detail.restype = C.c_char_p
+st = L.ref_write_edges(sys.argv[3].encode(), C.cast(buf, C.c_void_p), len(raw) // 16)
+if st:
+    sys.exit(f"ref_write_edges: {st} {L.ref_last_error_detail().decode()}")
+"""
+
+
+def write_edges(edges, path):
+    """graph_io.cpp:142-154, run in a fresh interpreter: the reference's
+    ostream number formatting (a libstdc++ linked into _ref) crashes once
+    numpy's own C++ runtime is loaded in the same process."""
+    import subprocess
+    import sys
+    import tempfile
+    e = np.ascontiguousarray(edges, dtype=EDGE_DTYPE)
+    with tempfile.NamedTemporaryFile(suffix=".bin") as f:
+        f.write(e.tobytes())
+        f.flush()
+        subprocess.run([sys.executable, "-c", _WRITE_SCRIPT, REF_SO, f.name, str(path)], check=True)

@@ -474,6 +474,23 @@ int ref_simulate(const TemporalEdge* e, std::uint64_t n, std::uint32_t node_coun
     });
 }
 
+// graph_io.cpp:106-140 load_edges(path, assume_sorted); *out malloc'ed (ref_free)
+int ref_load_edges(const char* path, int assume_sorted, TemporalEdge** out, std::uint64_t* n,
+                   std::uint32_t* node_count, double* t_max) {
+    return guarded([&] {
+        EdgeStream s = load_edges(std::string(path), assume_sorted != 0);
+        *out = dup(s.edges);
+        *n = s.edges.size();
+        *node_count = s.node_count;
+        *t_max = s.t_max;
+    });
+}
+
+// graph_io.cpp:142-154 write_edges(stream, path)
+int ref_write_edges(const char* path, const TemporalEdge* e, std::uint64_t n) {
+    return guarded([&] { write_edges(make_stream(e, n, 0, 0.0), std::string(path)); });
+}
+
 // metrics.cpp:33-68 (reporting only)
 int ref_quality(const TemporalEdge* e, std::uint64_t n, std::uint32_t node_count, int num_parts,
                 const std::int32_t* edge_part, const std::uint64_t* np_off,

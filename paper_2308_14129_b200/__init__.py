@@ -305,6 +305,69 @@ def assignment_handle(pa: PartitionAssignment, n_edges: int | None = None):
     return h
 
 
+# ------------------------------------------------------- on-disk formats
+def load_edges(path: str, assume_sorted: bool = False) -> EdgeStream:
+    """graph_io.hpp load_edges (graph_io.cpp:106-140): CSV src,dst,ts."""
+    out = C.c_void_p()
+    n, nc, tm = u64(), u32(), f64()
+    _check(lib.spd_load_edges_csv(str(path).encode(), int(assume_sorted), C.byref(out), C.byref(n),
+                                  C.byref(nc), C.byref(tm)))
+    try:
+        arr = np.empty(n.value, dtype=EDGE_DTYPE)
+        if n.value:
+            C.memmove(arr.ctypes.data, out.value, n.value * EDGE_DTYPE.itemsize)
+    finally:
+        lib.spd_free(out)
+    return EdgeStream(arr, nc.value, tm.value)
+
+
+def write_edges(s: EdgeStream, path: str) -> None:
+    """graph_io.hpp write_edges (graph_io.cpp:142-154): %.17g timestamps."""
+    e = _edges(s)
+    _check(lib.spd_write_edges_csv(str(path).encode(), ptr(e) if len(e) else None, len(e)))
+
+
+def write_edges_bin(s: EdgeStream, path: str) -> None:
+    """Binary event file (header + TemporalEdge records); see speed_c.h."""
+    e = _edges(s)
+    _check(lib.spd_write_edges_bin(str(path).encode(), ptr(e) if len(e) else None, len(e),
+                                   s.node_count, s.t_max))
+
+
+def load_edges_bin(path: str, out: np.ndarray | None = None) -> EdgeStream:
+    """Reads a binary event file into ``out`` (e.g. a pinned buffer) or a new array."""
+    n, nc, tm = u64(), u32(), f64()
+    _check(lib.spd_edges_bin_info(str(path).encode(), C.byref(n), C.byref(nc), C.byref(tm)))
+    arr = np.empty(n.value, dtype=EDGE_DTYPE) if out is None else out[: n.value]
+    if arr.dtype != EDGE_DTYPE or len(arr) < n.value or not arr.flags.c_contiguous:
+        raise UsageError("Usage", "output buffer must be a contiguous EDGE_DTYPE array of n records")
+    _check(lib.spd_load_edges_bin(str(path).encode(), ptr(arr) if n.value else None, n.value))
+    return EdgeStream(arr, nc.value, tm.value)
+
+
+def write_assignment_json(pa: PartitionAssignment, path: str, config: dict | None = None) -> None:
+    """The CLI partition subcommand's output document (speedpart_main.cpp:110-119)."""
+    import json
+    h = assignment_handle(pa)
+    try:
+        cfg = json.dumps(config if config is not None else {}, separators=(",", ":"))
+        _check(lib.spd_assignment_write_json(h, cfg.encode(), str(path).encode()))
+    finally:
+        lib.spd_assignment_destroy(h)
+
+
+def load_assignment_json(path: str):
+    """load_assignment (speedpart_main.cpp:129-166) -> (PartitionAssignment, config dict)."""
+    import json
+    h, cfg = C.c_void_p(), C.c_void_p()
+    _check(lib.spd_assignment_read_json(str(path).encode(), C.byref(h), C.byref(cfg)))
+    try:
+        text = C.string_at(cfg.value).decode()
+    finally:
+        lib.spd_free(cfg)
+    return _assignment_from_handle(h), json.loads(text)
+
+
 @dataclass
 class EvalRouting:  # partitioner.hpp:74-79
     val_edges: list

@@ -71,6 +71,14 @@ _SIGS = {
     "spd_assignment_edge_part": (i32, [P, pi32]),
     "spd_assignment_node_parts": (i32, [P, pu64, pi32]),
     "spd_assignment_shared": (i32, [P, pu32]),
+    "spd_free": (None, [P]),
+    "spd_load_edges_csv": (i32, [pchar, i32, PP, pu64, pu32, pf64]),
+    "spd_write_edges_csv": (i32, [pchar, P, u64]),
+    "spd_write_edges_bin": (i32, [pchar, P, u64, u32, f64]),
+    "spd_edges_bin_info": (i32, [pchar, pu64, pu32, pf64]),
+    "spd_load_edges_bin": (i32, [pchar, P, u64]),
+    "spd_assignment_write_json": (i32, [P, pchar, pchar]),
+    "spd_assignment_read_json": (i32, [pchar, PP, PP]),
     "spd_assign_eval_edges": (i32, [P, u64, P, u64, P, PP]),
     "spd_eval_routing_counts": (i32, [P, i32, pu64, pu64]),
     "spd_eval_routing_edges": (i32, [P, i32, pu64]),
