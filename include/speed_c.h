@@ -305,6 +305,13 @@ spd_status spd_tgn_begin_epoch(spd_tgn_trainer* t, int32_t epoch);
  * messages cleared. Benchmarks use it to time steady-state steps mid-epoch
  * (full recent-k neighbour lists) instead of an epoch's sparse first batches. */
 spd_status spd_tgn_seek(spd_tgn_trainer* t, uint64_t step);
+/* Shuffle-combine (simulate with SimConfig::shuffle, pac_sim.cpp:280-329):
+ * before an epoch, rebind the trainer to that epoch's regrouped subgraphs
+ * (spd_shuffle_combine + spd_induce_groups; one per worker, same count).
+ * Parameters and Adam state carry over; memory, clocks and pending messages
+ * start from zero (reset at every loop start, pac_sim.cpp:238); evaluation
+ * views must be set again. ConfigMismatch if the worker count differs. */
+spd_status spd_tgn_rebind(spd_tgn_trainer* t, const spd_subgraphs* subs);
 /* One global step: every local worker trains one batch, gradients are
  * all-reduced (mean over all workers), Adam updates. loss_out: per local
  * worker mean BCE of the batch (device->host read), may be NULL. */

@@ -223,6 +223,20 @@ class TGNOracle:
         self.snap = [None] * len(workers)
         self.last = {}
 
+    def rebind(self, workers: list[WorkerData]):
+        """Shuffle-combine (pac_sim.cpp:280-329): the next epoch's regrouped
+        workers; parameters and Adam state carry over, per-worker state restarts."""
+        if len(workers) != len(self.W):
+            raise ValueError("rebind needs the same number of workers")
+        D = self.c.d_mem
+        self.W = workers
+        self.mem = [torch.zeros(w.N, D) for w in workers]
+        self.lu = [np.zeros(w.N) for w in workers]
+        self.pend = [dict() for _ in workers]
+        self.pos = [0] * len(workers)
+        self.snap = [None] * len(workers)
+        self.last = {}
+
     # views into a differentiable copy of the flat params
     def views(self, flat: torch.Tensor):
         c = self.c

@@ -24,7 +24,7 @@ __all__ = [
     "compute_centrality", "compute_degree_centrality", "select_hubs", "PartitionerConfig",
     "PartitionState", "PartitionAssignment", "score", "partition_stream",
     "partition_unrestricted", "EvalRouting", "assign_eval_edges", "SubGraph",
-    "induce_subgraphs", "shuffle_combine", "ModelParams", "MemoryStore", "model_update",
+    "induce_subgraphs", "induce_groups", "shuffle_combine", "ModelParams", "MemoryStore", "model_update",
     "SyncStrategy", "sync_shared", "StepLog", "EpochReport", "run_epoch", "SimConfig",
     "SimReport", "simulate", "kDiscarded",
 ]
@@ -444,6 +444,31 @@ def induce_subgraphs(s: EdgeStream, node_parts, num_parts: int) -> list:
         lib.spd_subgraphs_destroy(h)
 
 
+def induce_groups(s: EdgeStream, groups: Sequence[Sequence[int]],
+                  small: Sequence[Sequence[int]]):
+    """One epoch of simulate's shuffle branch (pac_sim.cpp:306-326): the
+    subgraph induced by each combined group, and the `recovered` count (edges
+    some group induces that no small part does)."""
+    e = _edges(s)
+
+    def csr(lists):
+        off = np.zeros(len(lists) + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([len(v) for v in lists])
+        flat = np.array([x for v in lists for x in v] or [0], dtype=np.uint32)
+        return off, flat
+    go, gn = csr(groups)
+    so, sn = csr(small)
+    h = C.c_void_p()
+    rec = u64()
+    _check(lib.spd_induce_groups(ptr(e), len(e), s.node_count, ptr(go, u64), ptr(gn, u32),
+                                 len(groups), ptr(so, u64), ptr(sn, u32), len(small), C.byref(h),
+                                 C.byref(rec)))
+    try:
+        return _subgraphs_from_handle(h), rec.value
+    finally:
+        lib.spd_subgraphs_destroy(h)
+
+
 def subgraphs_handle(subs: Sequence[SubGraph]):
     """Opaque spd_subgraphs* for a list of SubGraph (caller destroys)."""
     n = len(subs)
@@ -777,6 +802,16 @@ class TGNTrainer:
 
     def begin_epoch(self, epoch: int):
         _check(lib.spd_tgn_begin_epoch(self._h, epoch))
+
+    def rebind(self, subgraphs: Sequence[SubGraph]):
+        """Shuffle-combine: train the next epoch on regrouped subgraphs
+        (spd_tgn_rebind; parameters and Adam state carry over)."""
+        sh = subgraphs_handle(subgraphs)
+        try:
+            _check(lib.spd_tgn_rebind(self._h, sh))
+        finally:
+            lib.spd_subgraphs_destroy(sh)
+        self._events_per_worker = {w: len(subgraphs[w].edges) for w in self.workers}
 
     def seek(self, step: int):
         """Position the schedule at global step `step` of this epoch (spd_tgn_seek)."""

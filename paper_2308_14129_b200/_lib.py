@@ -137,6 +137,7 @@ _SIGS = {
     "spd_edge_features_bf16": (i32, [u64, pu64, u64, i32, i32, P]),
     "spd_debug_gemm": (i32, [i32, i32, P, i32, P, i32, P, i32, i32, i32, i32, P, u64]),
     "spd_tgn_set_debug": (i32, [P, i32]),
+    "spd_tgn_rebind": (i32, [P, P]),
     "spd_tgn_set_graph": (i32, [P, i32]),
     "spd_tgn_set_profile": (i32, [P, i32]),
     "spd_edge_feature": (f32, [u64, u64, u32]),

@@ -110,6 +110,7 @@ public:
     std::uint64_t batch_size() const { return cfg_.batch_size; }
     void begin_epoch(int epoch);
     void seek(std::uint64_t step);
+    void rebind(const SubGraphs& subs);  // shuffle-combine: next epoch's regrouped subgraphs
     void step(float* loss_out);
     void end_epoch();
     void run_epoch(int epoch, double* mean_loss);
@@ -148,6 +149,7 @@ public:
     cudaStream_t stream() const { return stream_; }
 
 private:
+    void build_workers(const SubGraphs& subs, const std::vector<int>& ids);
     void worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx,
                      bool post = true);
     void worker_post_kernels(Worker& w);
@@ -190,6 +192,10 @@ private:
     cudaStream_t aux_ = nullptr;
     cudaEvent_t ev_aux_fork_ = nullptr, ev_aux_join_ = nullptr, ev_roots_ = nullptr,
                 ev_phi_ = nullptr;
+    // gradient zeroing forked at step start beside the forward; the backward
+    // (first gradient writer) joins it
+    cudaStream_t zs_ = nullptr;
+    cudaEvent_t ev_zfork_ = nullptr, ev_zero_ = nullptr;
 
     spd_tgn_config cfg_;
     ParamLayout lay_;

@@ -48,6 +48,12 @@ spd_status spd_tgn_begin_epoch(spd_tgn_trainer* t, int32_t epoch) {
     GUARD({ t->t->begin_epoch(epoch); });
 }
 spd_status spd_tgn_seek(spd_tgn_trainer* t, uint64_t step) { GUARD({ t->t->seek(step); }); }
+spd_status spd_tgn_rebind(spd_tgn_trainer* t, const spd_subgraphs* subs) {
+    GUARD({
+        if (!t || !subs) usage_error("null argument");
+        t->t->rebind(subs->s);
+    });
+}
 spd_status spd_tgn_step(spd_tgn_trainer* t, float* loss_out) { GUARD({ t->t->step(loss_out); }); }
 spd_status spd_tgn_end_epoch(spd_tgn_trainer* t) { GUARD({ t->t->end_epoch(); }); }
 spd_status spd_tgn_run_epoch(spd_tgn_trainer* t, int32_t epoch, double* mean_loss) {

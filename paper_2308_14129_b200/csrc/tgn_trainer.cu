@@ -9,6 +9,7 @@
 //   weight-gradient GEMMs accumulating straight into the flat gradient.
 #include "pdl.cuh"
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -354,109 +355,15 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     SPD_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
 
     SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
-    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_phi_})
+    SPD_CUDA(cudaStreamCreateWithPriority(&zs_, cudaStreamNonBlocking, prio_lo));
+    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_phi_, &ev_zfork_, &ev_zero_})
         SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors);
     feat_seed_mixed_ = mix64(cfg.seed_feat);
-    total_workers_ = static_cast<int>(subs.g.size());
-    for (const auto& sg : subs.g)
-        all_batches_.push_back((sg.edges.size() + cfg.batch_size - 1) / cfg.batch_size);
-    epoch_steps_ = all_batches_.empty() ? 0 : *std::max_element(all_batches_.begin(), all_batches_.end());
-
     const int D = lay_.D, F = lay_.F;
     const int Fp = F ? (F + 7) / 8 * 8 : 0;
     const int B = static_cast<int>(cfg.batch_size);
-    for (int wid : workers) {
-        if (wid < 0 || wid >= total_workers_) data_error("InvalidParams", "worker id out of range");
-        const SubGraph& sg = subs.g[wid];
-        auto W = std::make_unique<Worker>();
-        Worker& w = *W;
-        w.gid = wid;
-        w.nodes = sg.nodes;
-        w.N = static_cast<NodeId>(sg.nodes.size());
-        w.E = sg.edges.size();
-        w.batches = all_batches_[wid];
-        // local ids
-        std::vector<std::uint32_t> src(w.E), dst(w.E);
-        std::vector<double> ts(w.E);
-        auto loc = [&](NodeId gid) -> std::uint32_t {
-            auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), gid);
-            if (it == w.nodes.end() || *it != gid)
-                data_error("InvalidPartition", "edge endpoint outside the subgraph's node set");
-            return static_cast<std::uint32_t>(it - w.nodes.begin());
-        };
-        for (std::uint64_t k = 0; k < w.E; ++k) {
-            src[k] = loc(sg.edges[k].src);
-            dst[k] = loc(sg.edges[k].dst);
-            ts[k] = sg.edges[k].ts;
-            if (k && ts[k] < ts[k - 1])
-                data_error("NonChronological", "subgraph edges must be time-ordered");
-        }
-        // per-node time-sorted adjacency (both directions; ties keep event
-        // order, src side first — the oracle's (ts, event, role) order)
-        std::vector<std::uint64_t> off(std::size_t(w.N) + 1, 0);
-        for (std::uint64_t k = 0; k < w.E; ++k) {
-            ++off[src[k] + 1];
-            ++off[dst[k] + 1];
-        }
-        for (NodeId i = 0; i < w.N; ++i) off[i + 1] += off[i];
-        std::vector<std::uint64_t> fill(off.begin(), off.end() - 1);
-        std::vector<std::uint32_t> anbr(2 * w.E), aev(2 * w.E);
-        std::vector<double> ats(2 * w.E);
-        for (std::uint64_t k = 0; k < w.E; ++k) {  // events are time-ordered: append keeps order
-            std::uint64_t p = fill[src[k]]++;
-            anbr[p] = dst[k]; aev[p] = static_cast<std::uint32_t>(k); ats[p] = ts[k];
-            p = fill[dst[k]]++;
-            anbr[p] = src[k]; aev[p] = static_cast<std::uint32_t>(k); ats[p] = ts[k];
-        }
-        std::vector<std::uint32_t> pool(dst);
-        std::sort(pool.begin(), pool.end());
-        pool.erase(std::unique(pool.begin(), pool.end()), pool.end());
-        if (pool.empty()) pool.push_back(0);
-        w.n_pool = static_cast<std::uint32_t>(pool.size());
-        if (w.E > 0xFFFFFFFFull) data_error("InvalidParams", "partition exceeds 2^32 events");
-
-        w.ev_src.alloc(w.E); w.ev_src.upload(src.data(), w.E, stream_);
-        w.ev_dst.alloc(w.E); w.ev_dst.upload(dst.data(), w.E, stream_);
-        w.ev_ts.alloc(w.E); w.ev_ts.upload(ts.data(), w.E, stream_);
-        w.adj_off.alloc(off.size()); w.adj_off.upload(off.data(), off.size(), stream_);
-        w.adj_nbr.alloc(2 * w.E); w.adj_nbr.upload(anbr.data(), 2 * w.E, stream_);
-        w.adj_ev.alloc(2 * w.E); w.adj_ev.upload(aev.data(), 2 * w.E, stream_);
-        w.adj_ts.alloc(2 * w.E); w.adj_ts.upload(ats.data(), 2 * w.E, stream_);
-        w.pool.alloc(pool.size()); w.pool.upload(pool.data(), pool.size(), stream_);
-        // synthetic features, generated on the device from the global edge ids
-        w.feat.alloc(std::max<std::uint64_t>(1, w.E) * std::max(1, Fp));
-        if (Fp && w.E) {
-            DevBuf<std::uint64_t> eids(w.E);
-            eids.upload(sg.eids.data(), w.E, stream_);
-            launch(tgnk::k_gen_features, blocks_for(w.E * Fp), 256, 0, stream_, 
-                w.feat.p, eids.p, w.E, F, Fp, feat_seed_mixed_);
-            SPD_CUDA(cudaGetLastError());
-            SPD_CUDA(cudaStreamSynchronize(stream_));
-        }
-        const std::size_t N = std::max<std::size_t>(1, w.N);
-        w.mem.alloc(N * D); w.mem.zero(stream_);
-        w.mem_snap.alloc(N * D); w.mem_snap.zero(stream_);
-        w.lu.alloc(N); w.lu.zero(stream_);
-        w.lu_snap.alloc(N); w.lu_snap.zero(stream_);
-        w.slot.alloc(N);
-        SPD_CUDA(cudaMemsetAsync(w.slot.p, 0xFF, w.slot.bytes(), stream_));
-        w.lastpos.alloc(N);
-        SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
-        for (auto& ps : w.pend) {
-            ps.pU.alloc(2 * B); ps.pOther.alloc(2 * B); ps.pEv.alloc(2 * B); ps.pTs.alloc(2 * B);
-            ps.nU.alloc(1); ps.nU.zero(stream_);
-        }
-        for (NodeId sidx : shared_) {
-            auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), sidx);
-            w.shared_local.push_back(it != w.nodes.end() && *it == sidx
-                                         ? static_cast<std::uint32_t>(it - w.nodes.begin())
-                                         : 0xFFFFFFFFu);
-        }
-        w.ev_host.resize(w.E);
-        for (std::uint64_t k = 0; k < w.E; ++k) w.ev_host[k] = spd_edge{src[k], dst[k], ts[k]};
-        workers_.push_back(std::move(W));
-    }
+    build_workers(subs, workers);
 
     // parameters + optimiser state
     std::vector<float> flat;
@@ -580,11 +487,146 @@ TGNTrainer::~TGNTrainer() {
         if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
         if (sides_[k]) cudaStreamDestroy(sides_[k]);
     }
-    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_phi_})
+    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_phi_, ev_zfork_, ev_zero_})
         if (e) cudaEventDestroy(e);
     if (aux_) cudaStreamDestroy(aux_);
+    if (zs_) cudaStreamDestroy(zs_);
     if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
     if (stream_) cudaStreamDestroy(stream_);
+}
+
+// Per-worker device state from the subgraphs: local ids, time-sorted CSR,
+// destination pool, features (generated on device), memory and pending sets.
+void TGNTrainer::build_workers(const SubGraphs& subs, const std::vector<int>& ids) {
+    const int D = lay_.D, F = lay_.F;
+    const int Fp = F ? (F + 7) / 8 * 8 : 0;
+    const int B = static_cast<int>(cfg_.batch_size);
+    const spd_tgn_config& cfg = cfg_;
+    total_workers_ = static_cast<int>(subs.g.size());
+    all_batches_.clear();
+    for (const auto& sg : subs.g)
+        all_batches_.push_back((sg.edges.size() + cfg.batch_size - 1) / cfg.batch_size);
+    epoch_steps_ = all_batches_.empty() ? 0 : *std::max_element(all_batches_.begin(), all_batches_.end());
+
+    for (int wid : ids) {
+        if (wid < 0 || wid >= total_workers_) data_error("InvalidParams", "worker id out of range");
+        const SubGraph& sg = subs.g[wid];
+        auto W = std::make_unique<Worker>();
+        Worker& w = *W;
+        w.gid = wid;
+        w.nodes = sg.nodes;
+        w.N = static_cast<NodeId>(sg.nodes.size());
+        w.E = sg.edges.size();
+        w.batches = all_batches_[wid];
+        // local ids
+        std::vector<std::uint32_t> src(w.E), dst(w.E);
+        std::vector<double> ts(w.E);
+        auto loc = [&](NodeId gid) -> std::uint32_t {
+            auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), gid);
+            if (it == w.nodes.end() || *it != gid)
+                data_error("InvalidPartition", "edge endpoint outside the subgraph's node set");
+            return static_cast<std::uint32_t>(it - w.nodes.begin());
+        };
+        for (std::uint64_t k = 0; k < w.E; ++k) {
+            src[k] = loc(sg.edges[k].src);
+            dst[k] = loc(sg.edges[k].dst);
+            ts[k] = sg.edges[k].ts;
+            if (k && ts[k] < ts[k - 1])
+                data_error("NonChronological", "subgraph edges must be time-ordered");
+        }
+        // per-node time-sorted adjacency (both directions; ties keep event
+        // order, src side first — the oracle's (ts, event, role) order)
+        std::vector<std::uint64_t> off(std::size_t(w.N) + 1, 0);
+        for (std::uint64_t k = 0; k < w.E; ++k) {
+            ++off[src[k] + 1];
+            ++off[dst[k] + 1];
+        }
+        for (NodeId i = 0; i < w.N; ++i) off[i + 1] += off[i];
+        std::vector<std::uint64_t> fill(off.begin(), off.end() - 1);
+        std::vector<std::uint32_t> anbr(2 * w.E), aev(2 * w.E);
+        std::vector<double> ats(2 * w.E);
+        for (std::uint64_t k = 0; k < w.E; ++k) {  // events are time-ordered: append keeps order
+            std::uint64_t p = fill[src[k]]++;
+            anbr[p] = dst[k]; aev[p] = static_cast<std::uint32_t>(k); ats[p] = ts[k];
+            p = fill[dst[k]]++;
+            anbr[p] = src[k]; aev[p] = static_cast<std::uint32_t>(k); ats[p] = ts[k];
+        }
+        std::vector<std::uint32_t> pool(dst);
+        std::sort(pool.begin(), pool.end());
+        pool.erase(std::unique(pool.begin(), pool.end()), pool.end());
+        if (pool.empty()) pool.push_back(0);
+        w.n_pool = static_cast<std::uint32_t>(pool.size());
+        if (w.E > 0xFFFFFFFFull) data_error("InvalidParams", "partition exceeds 2^32 events");
+
+        w.ev_src.alloc(w.E); w.ev_src.upload(src.data(), w.E, stream_);
+        w.ev_dst.alloc(w.E); w.ev_dst.upload(dst.data(), w.E, stream_);
+        w.ev_ts.alloc(w.E); w.ev_ts.upload(ts.data(), w.E, stream_);
+        w.adj_off.alloc(off.size()); w.adj_off.upload(off.data(), off.size(), stream_);
+        w.adj_nbr.alloc(2 * w.E); w.adj_nbr.upload(anbr.data(), 2 * w.E, stream_);
+        w.adj_ev.alloc(2 * w.E); w.adj_ev.upload(aev.data(), 2 * w.E, stream_);
+        w.adj_ts.alloc(2 * w.E); w.adj_ts.upload(ats.data(), 2 * w.E, stream_);
+        w.pool.alloc(pool.size()); w.pool.upload(pool.data(), pool.size(), stream_);
+        // synthetic features, generated on the device from the global edge ids
+        w.feat.alloc(std::max<std::uint64_t>(1, w.E) * std::max(1, Fp));
+        if (Fp && w.E) {
+            DevBuf<std::uint64_t> eids(w.E);
+            eids.upload(sg.eids.data(), w.E, stream_);
+            launch(tgnk::k_gen_features, blocks_for(w.E * Fp), 256, 0, stream_, 
+                w.feat.p, eids.p, w.E, F, Fp, feat_seed_mixed_);
+            SPD_CUDA(cudaGetLastError());
+            SPD_CUDA(cudaStreamSynchronize(stream_));
+        }
+        const std::size_t N = std::max<std::size_t>(1, w.N);
+        w.mem.alloc(N * D); w.mem.zero(stream_);
+        w.mem_snap.alloc(N * D); w.mem_snap.zero(stream_);
+        w.lu.alloc(N); w.lu.zero(stream_);
+        w.lu_snap.alloc(N); w.lu_snap.zero(stream_);
+        w.slot.alloc(N);
+        SPD_CUDA(cudaMemsetAsync(w.slot.p, 0xFF, w.slot.bytes(), stream_));
+        w.lastpos.alloc(N);
+        SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
+        for (auto& ps : w.pend) {
+            ps.pU.alloc(2 * B); ps.pOther.alloc(2 * B); ps.pEv.alloc(2 * B); ps.pTs.alloc(2 * B);
+            ps.nU.alloc(1); ps.nU.zero(stream_);
+        }
+        for (NodeId sidx : shared_) {
+            auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), sidx);
+            w.shared_local.push_back(it != w.nodes.end() && *it == sidx
+                                         ? static_cast<std::uint32_t>(it - w.nodes.begin())
+                                         : 0xFFFFFFFFu);
+        }
+        w.ev_host.resize(w.E);
+        for (std::uint64_t k = 0; k < w.E; ++k) w.ev_host[k] = spd_edge{src[k], dst[k], ts[k]};
+        workers_.push_back(std::move(W));
+    }
+}
+
+// Shuffle-combine (pac_sim.cpp:280-329): the next epoch trains on regrouped
+// subgraphs. Parameters and optimiser state carry over; memory starts from
+// zero (every loop start resets it, pac_sim.cpp:238), captured graphs and
+// evaluation views are rebuilt.
+void TGNTrainer::rebind(const SubGraphs& subs) {
+    DeviceGuard g(device_);
+    if (static_cast<int>(subs.g.size()) != total_workers_)
+        data_error("ConfigMismatch", "rebind needs one subgraph per worker (" +
+                                         std::to_string(total_workers_) + ")");
+    SPD_CUDA(cudaDeviceSynchronize());
+    std::vector<int> ids;
+    for (const auto& w : workers_) ids.push_back(w->gid);
+    for (auto& ge : graph_exec_)
+        if (ge) {
+            SPD_CUDA(cudaGraphExecDestroy(ge));
+            ge = nullptr;
+        }
+    eager_full_steps_ = 0;
+    workers_.clear();
+    build_workers(subs, ids);
+    for (std::size_t k = 0; k < workers_.size(); ++k) {
+        workers_[k]->ctl = ctl_dev_.p + 2 * k;
+        workers_[k]->ctl_index = static_cast<int>(k);
+    }
+    step_in_epoch_ = 0;
+    SPD_CUDA(cudaStreamSynchronize(stream_));
 }
 
 Worker& TGNTrainer::worker(int w) {
@@ -704,7 +746,11 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     };
     auto phi = [&](cudaStream_t sx) {
-        launch(tgnk::k_phi, std::min<unsigned>(blocks_for(std::size_t(R) * d.K * (d.T / 4)), 2 * 148),
+        static const unsigned phi_cap = [] {
+            const char* e = std::getenv("SPD_PHI_BLOCKS");
+            return e ? unsigned(std::atoi(e)) : 2u * 148u;
+        }();
+        launch(tgnk::k_phi, std::min<unsigned>(blocks_for(std::size_t(R) * d.K * (d.T / 4)), phi_cap),
                256, 0, sx, d, R,
                P + lay_.time_w, P + lay_.time_b, static_cast<const double*>(s.nbr_dt.p),
                static_cast<const int*>(s.cnt.p), s.phi.p);
@@ -720,15 +766,23 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         side([&](cudaStream_t sd) { launch(tgnk::k_pending, 1, 1024, 0, sd, wd, B); });
     // (the side-stream branch is forked after the GRU's first kernel is
     // enqueued: graph replays submit independent branches in creation order)
+    auto fork_roots = [&] {
+        side([&](cudaStream_t sd) {
+            roots(sd);
+            SPD_CUDA(cudaEventRecord(ev_roots_, sd));
+            phi(sd);
+            SPD_CUDA(cudaEventRecord(ev_phi_, sd));
+        }, 0);
+    };
+    static const bool roots_early = [] {
+        const char* e = std::getenv("SPD_ROOTS_EARLY");
+        return e && *e == '1';
+    }();
+    if (!profile_ && roots_early) fork_roots();
     timed("gru_fwd", [&] {
         gru_forward(w, wd, train, [&] {
-            if (profile_) return;
-            side([&](cudaStream_t sd) {
-                roots(sd);
-                SPD_CUDA(cudaEventRecord(ev_roots_, sd));
-                phi(sd);
-                SPD_CUDA(cudaEventRecord(ev_phi_, sd));
-            }, 0);
+            if (profile_ || roots_early) return;
+            fork_roots();
         });
     });
     if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_roots_, 0));
@@ -801,6 +855,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     cudaStream_t st = stream_;
     const bool tc = cfg_.gemm_mode == 1;
     const float* PW = tc ? params_tc_.p : params_.p;
+    SPD_CUDA(cudaStreamWaitEvent(st, ev_zero_, 0));  // gradients cleared (step_body)
     timed("head_bwd", [&] {
         side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
                    2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
@@ -1043,9 +1098,14 @@ void TGNTrainer::set_ctl(Worker& w, std::uint64_t lo, std::uint64_t nb) {
 // Bs[k] = batch size of local worker k (0: idle). Capturable as a CUDA graph.
 void TGNTrainer::step_body(const std::vector<int>& Bs) {
     // gradient buffers cleared by a kernel, not memset nodes: in a graph
-    // replay a memset node costs a copy-engine hand-off before the first kernel
-    launch(tgnk::k_zero2, blocks_for(lay_.total), 256, 0, stream_, grads_.p, lay_.total, tgrad_.p,
+    // replay a memset node costs a copy-engine hand-off before the first
+    // kernel. It runs on its own stream beside the forward (nothing reads or
+    // writes the gradients before the backward, which joins it).
+    SPD_CUDA(cudaEventRecord(ev_zfork_, stream_));
+    SPD_CUDA(cudaStreamWaitEvent(zs_, ev_zfork_, 0));
+    launch(tgnk::k_zero2, blocks_for(lay_.total), 256, 0, zs_, grads_.p, lay_.total, tgrad_.p,
            std::size_t(2) * ld4(lay_.T));
+    SPD_CUDA(cudaEventRecord(ev_zero_, zs_));
     std::size_t last = workers_.size();
     for (std::size_t k = 0; k < workers_.size(); ++k)
         if (Bs[k] > 0) last = k;

@@ -170,7 +170,7 @@ struct Cfg {
 };
 
 template <bool A_MN, bool B_MN, int BN, int NSUB, int CL>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, 2)
     umma_gemm_kernel(const __grid_constant__ Maps maps, Args args) {
     pdl_entry();
     using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 
@@ -140,12 +141,22 @@ void dispatch(int bn, const Maps& maps, const Args& args, dim3 grid, cudaStream_
     }
 }
 
+// SPD_UMMA_MAXBN caps the tile width (tuning experiments; default 256)
+int max_bn() {
+    static const int v = [] {
+        const char* e = std::getenv("SPD_UMMA_MAXBN");
+        return e ? std::atoi(e) : 256;
+    }();
+    return v;
+}
+
 // widest tile with the least padding of N (ties -> wider)
 int pick_bn(int N) {
     const int cands[] = {256, 224, 128, 64};
     int best = 64;
     long best_pad = 1L << 40;
     for (int c : cands) {
+        if (c > max_bn() && c != 64) continue;
         const long tiles = (N + c - 1) / c;
         const long pad = tiles * c - N + tiles * 8;  // small per-tile overhead term
         if (pad < best_pad) {

@@ -234,3 +234,43 @@ def test_graph_replay_matches_eager(gemm_mode):
     assert np.allclose(l0, l1, rtol=1e-3), (l0, l1)
     assert rel_err(p1, p0) < TOL_TRAJ and rel_err(m1, m0) < TOL_TRAJ
     assert np.array_equal(u0, u1)
+
+
+def test_shuffle_combine_rebind_matches_oracle():
+    """simulate's shuffle branch (pac_sim.cpp:280-329) for the TGN trainer:
+    4 small SEP parts regrouped into 2 workers per epoch (seeded), the trainer
+    rebound each epoch; parameters and Adam state carry across epochs."""
+    from oracle import tgn_oracle as T
+    s, split, pa, small_subs = partitioned(nodes=200, edges=2400, parts=4)
+    small = [g.nodes for g in small_subs]
+    cfg = small_cfg()
+    tr = o = None
+    for epoch in range(2):
+        groups = sp.shuffle_combine(small, 2, 11 + epoch)
+        subs, recovered = sp.induce_groups(split.train, groups, small)
+        assert recovered >= 0
+        if tr is None:
+            tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+            o = oracle_for(cfg, subs, pa.shared)
+        else:
+            tr.rebind(subs)
+            o.rebind([T.WorkerData(g.nodes, g.edges, g.eids, o.c.d_edge, o.c.seed_feat) for g in subs])
+        assert tr.epoch_steps() == o.epoch_steps()
+        tr.begin_epoch(epoch)
+        o.begin_epoch(epoch)
+        for _ in range(o.epoch_steps()):
+            gl = tr.step()
+            ol = o.step()
+            for w in range(2):
+                if not np.isnan(ol[w]):
+                    assert abs(gl[w] - ol[w]) <= TOL_TRAJ * max(1.0, abs(ol[w])), (epoch, gl, ol)
+        tr.end_epoch()
+        o.end_epoch()
+        assert rel_err(tr.params(), o.flat.numpy()) < TOL_TRAJ, epoch
+        for w in range(2):
+            m, lu = tr.memory(w)
+            assert np.array_equal(lu, o.lu[w]), (epoch, w)
+            assert rel_err(m, o.mem[w].numpy()) < TOL_TRAJ, (epoch, w)
+    with pytest.raises(sp.DataError) as ei:
+        tr.rebind(subs[:1])
+    assert ei.value.code == "ConfigMismatch"
