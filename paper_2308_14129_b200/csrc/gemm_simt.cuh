@@ -50,18 +50,24 @@ struct Args {
 };
 
 // A_KMAJOR: A stored [K x M] (weight-grad orientation). B_KN: B stored [K x N].
-template <bool A_KMAJOR, bool B_KN, int BM>
+// BNT: tile width (64, or 32 for small problems: twice the CTAs, so a
+// 4000 x 100 decoder GEMM fills the 148 SMs). Thread (tx, ty) owns rows
+// ty*TM.. and columns tx*4..; every output still sums k in order.
+template <bool A_KMAJOR, bool B_KN, int BM, int BNT = BN>
 __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
     pdl_entry();
-    constexpr int TM = BM / 16;       // rows per thread
+    constexpr int TX = BNT / 4, TY = NT / TX;
+    constexpr int TM = BM / TY;       // rows per thread
     constexpr int AV = BM * BK / 4 / NT;  // float4 A loads per thread (2 or 1)
+    constexpr int BV = BK * BNT / 4;      // float4 B loads per tile (threads < BV)
+    static_assert(TM == 2 || TM % 4 == 0, "rows per thread");
     __shared__ __align__(16) float As[2][BK][BM + 4];
-    __shared__ __align__(16) float Bs[2][BK][BN + 4];
+    __shared__ __align__(16) float Bs[2][BK][BNT + 4];
     int M = a.M;
     if (a.M_dev) M = min(M, *a.M_dev);
     int K = a.K;
     if (a.K_dev) K = min(K, *a.K_dev);
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BNT;
     if (!A_KMAJOR && m0 >= M) return;
     if (n0 >= a.N) return;
     if (A_KMAJOR && m0 >= a.M) return;
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
         k_end = min(K, k_begin + per);
     }
     const int tid = threadIdx.x;
-    const int tx = tid % 16, ty = tid / 16;  // outputs (ty*TM.., tx*4..)
+    const int tx = tid % TX, ty = tid / TX;  // outputs (ty*TM.., tx*4..)
 
     float acc[TM][TN];
 #pragma unroll
@@ -108,13 +114,14 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
                 ra[r] = v;
             }
         }
-        if (B_KN) {  // 16 k-rows x 64 n
-            const int kr = tid / 16, nq = (tid % 16) * 4;
+        if (tid >= BV) {
+        } else if (B_KN) {  // 16 k-rows x BNT n
+            const int kr = tid / TX, nq = (tid % TX) * 4;
             const int gk = k0 + kr, gn = n0 + nq;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (gk < k_end && gn < a.N) v = *reinterpret_cast<const float4*>(a.B + (size_t)gk * a.ldb + gn);
             rb = v;
-        } else {  // 64 n-rows x 16 k
+        } else {  // BNT n-rows x 16 k
             const int row = tid / 4, kq = (tid % 4) * 4;
             const int gn = n0 + row, gk = k0 + kq;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -138,8 +145,9 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
                 *reinterpret_cast<float4*>(&As[buf][kr][mq]) = ra[r];
             }
         }
-        if (B_KN) {
-            const int kr = tid / 16, nq = (tid % 16) * 4;
+        if (tid >= BV) {
+        } else if (B_KN) {
+            const int kr = tid / TX, nq = (tid % TX) * 4;
             *reinterpret_cast<float4*>(&Bs[buf][kr][nq]) = rb;
         } else {
             const int row = tid / 4, kq = (tid % 4) * 4;
@@ -161,10 +169,15 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
 #pragma unroll
             for (int kk = 0; kk < BK; ++kk) {
                 float av[TM];
+                if constexpr (TM == 2) {
+                    const float2 t = *reinterpret_cast<const float2*>(&As[buf][kk][ty * TM]);
+                    av[0] = t.x; av[1] = t.y;
+                } else {
 #pragma unroll
-                for (int q = 0; q < TM; q += 4) {
-                    const float4 t = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + q]);
-                    av[q] = t.x; av[q + 1] = t.y; av[q + 2] = t.z; av[q + 3] = t.w;
+                    for (int q = 0; q < TM; q += 4) {
+                        const float4 t = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + q]);
+                        av[q] = t.x; av[q + 1] = t.y; av[q + 2] = t.z; av[q + 3] = t.w;
+                    }
                 }
                 const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
                 const float bv[4] = {b0.x, b0.y, b0.z, b0.w};

@@ -127,6 +127,10 @@ unsigned blocks_for(std::size_t n, int t = 256) { return unsigned((n + t - 1) / 
 bool use_bm64(int M, int N) {
     return long((M + 127) / 128) * ((N + gemm::BN - 1) / gemm::BN) < 2L * 148;
 }
+// 64 x 32 tiles when 64 x 64 ones would leave SMs idle
+bool use_bn32(int M, int N) {
+    return long((M + 63) / 64) * ((N + gemm::BN - 1) / gemm::BN) < 148L;
+}
 
 // C[M,N] (ldc) = A[M,K](lda) . B[N,K]^T(ldb), optional relu / mask epilogue.
 void gemm_fwd(const float* A, int lda, const float* B, int ldb, float* C, int ldc, int M, int N,
@@ -137,7 +141,10 @@ void gemm_fwd(const float* A, int lda, const float* B, int ldb, float* C, int ld
     a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.M_dev = M_dev; a.beta = 0.f; a.epi = epi;
     a.mask = mask; a.ldmask = ldmask; a.k_split = 1;
     if (!M || !N) return;
-    if (use_bm64(M, N)) {
+    if (use_bn32(M, N)) {
+        dim3 grid((N + 31) / 32, (M + 63) / 64, 1);
+        launch(gemm::gemm_kernel<false, false, 64, 32>, grid, gemm::NT, 0, s, a);
+    } else if (use_bm64(M, N)) {
         dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + 63) / 64, 1);
         launch(gemm::gemm_kernel<false, false, 64>, grid, gemm::NT, 0, s, a);
     } else {
@@ -156,7 +163,10 @@ void gemm_dgrad(const float* A, int lda, const float* B, int ldb, float* C, int 
     a.lda = lda; a.ldb = ldb; a.ldc = ldc; a.M_dev = M_dev; a.beta = 0.f; a.epi = epi;
     a.mask = mask; a.ldmask = ldmask; a.k_split = 1;
     if (!M || !N) return;
-    if (use_bm64(M, N)) {
+    if (use_bn32(M, N)) {
+        dim3 grid((N + 31) / 32, (M + 63) / 64, 1);
+        launch(gemm::gemm_kernel<false, true, 64, 32>, grid, gemm::NT, 0, s, a);
+    } else if (use_bm64(M, N)) {
         dim3 grid((N + gemm::BN - 1) / gemm::BN, (M + 63) / 64, 1);
         launch(gemm::gemm_kernel<false, true, 64>, grid, gemm::NT, 0, s, a);
     } else {

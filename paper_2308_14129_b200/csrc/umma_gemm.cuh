@@ -153,7 +153,10 @@ struct Cfg {
     static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
     static constexpr int B_BYTES = NT * BK * 4;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int BUDGET = 227 * 1024 - 1024 - 256;
+    // narrow tiles: 3 CTAs per SM (3 stages, <= 113 registers), so a CTA's
+    // epilogue and its neighbours' TMA round trips overlap; wider: 2 per SM
+    static constexpr int CTAS_PER_SM = NT <= 64 ? 3 : 2;
+    static constexpr int BUDGET = (NT <= 64 ? 75 * 1024 : 227 * 1024) - 1024 - 256;
     static constexpr int STAGES_ = BUDGET / STAGE_BYTES >= STAGES ? STAGES : BUDGET / STAGE_BYTES;
     static constexpr int SMEM = STAGES_ * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int TMEM_COLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : NT <= 256 ? 256 : 512;
@@ -170,7 +173,7 @@ struct Cfg {
 };
 
 template <bool A_MN, bool B_MN, int BN, int NSUB, int CL>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, (BN * NSUB <= 64 ? 3 : 2))
     umma_gemm_kernel(const __grid_constant__ Maps maps, Args args) {
     pdl_entry();
     using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;

@@ -141,11 +141,15 @@ void dispatch(int bn, const Maps& maps, const Args& args, dim3 grid, cudaStream_
     }
 }
 
-// SPD_UMMA_MAXBN caps the tile width (tuning experiments; default 256)
+// Tile-width cap for the forward / data-gradient GEMMs. Default 64: at the
+// step's sizes (R = 6,000 rows) 128 x 64 tiles give ~190-380 CTAs at 3 per SM
+// (3 stages, <= 113 registers), so each CTA's epilogue overlaps its
+// neighbours' TMA round trips; measured 0.409 vs 0.432 ms per GDELT step
+// against the widest-tile choice. SPD_UMMA_MAXBN overrides (experiments).
 int max_bn() {
     static const int v = [] {
         const char* e = std::getenv("SPD_UMMA_MAXBN");
-        return e ? std::atoi(e) : 256;
+        return e ? std::atoi(e) : 64;
     }();
     return v;
 }
