@@ -56,12 +56,12 @@ def ncu_traffic(kernel):
     from the newest committed ncu --set full raw export under profiles/."""
     import csv
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{kernel}_raw.csv")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_k_attn_abs_raw.csv")))
     if not files:
         return None, None
     rows = list(csv.reader(open(files[-1])))
     h, units = rows[0], rows[1]
-    row = next((r for r in rows[2:] if kernel in r[h.index("Kernel Name")]), None)
+    row = next((r for r in rows[2:] if kernel + "<" in r[h.index("Kernel Name")]), None)
     if row is None:
         return None, None
     total = 0.0
@@ -354,26 +354,31 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs") or 6650.0
-    # dominant kernel: the fused attention backward (the step's largest single
-    # kernel); algorithmic bytes per launch, full recent-k lists (mid-epoch):
-    # per neighbour occurrence its memory row (4D), bf16 feature row (2F) and
-    # (node, event, dt, slot) = 20 B; per root Qp and dxbar read and dQp
-    # written (3 x H x 4(DK+1)) plus alpha (4HK)
+    # dominant kernel: the larger of the two attention kernels on the critical
+    # path; algorithmic bytes per launch, full recent-k lists (mid-epoch). Per
+    # neighbour occurrence both read its memory row (4D), cos row of phi (4T),
+    # bf16 feature row (2F) and (node, event, dt, slot) = 20 B. Per root the
+    # forward reads q'_h and writes xbar_h (2 x H x 4(DK+1)) and alpha (4HK);
+    # the backward reads dxbar_h and writes dq'_h (2 x H x 4(DK+1)), reads
+    # alpha and writes ds (2 x 4HK).
     DK = D + T + F
     R_ = 3 * B
-    occ_bytes = R_ * K * (4 * D + 2 * F + 20)
-    root_bytes = R_ * (3 * H * 4 * (DK + 1) + 4 * H * K)
+    occ_bytes = R_ * K * (4 * D + 4 * T + 2 * F + 20)
+    alg = {"k_attn_abs_fwd": occ_bytes + R_ * (2 * H * 4 * (DK + 1) + 4 * H * K),
+           "k_attn_abs_bwd": occ_bytes + R_ * (2 * H * 4 * (DK + 1) + 2 * 4 * H * K)}
     kern = dict(phases)
-    dom = ("k_attn_abs_bwd", kern.get("k_attn_abs_bwd", 0.0))
+    name = max(alg, key=lambda k: kern.get(k, 0.0))
+    dom = (name, kern.get(name, 0.0))
     roof = {"bound": "hbm", "kernel": dom[0], "achieved": None, "peak": hbm_peak, "unit": "GB/s",
             "frac": None, "traffic": None,
-            "algorithmic_bytes_per_launch": occ_bytes + root_bytes,
+            "algorithmic_bytes_per_launch": alg[name],
             "launch_ms": dom[1], "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"}
     if dom[1] > 0:
-        roof["achieved"] = (occ_bytes + root_bytes) / (dom[1] / 1e3) / 1e9
+        roof["achieved"] = alg[name] / (dom[1] / 1e3) / 1e9
         roof["frac"] = roof["achieved"] / hbm_peak
+    roof["other_kernels_ms"] = {k: kern.get(k) for k in ("k_attn_abs_fwd", "k_attn_abs_bwd", "attn_bwd_x")}
     # measured DRAM traffic of the same kernel: the committed ncu --set full capture
-    roof["traffic"], roof["traffic_source"] = ncu_traffic("k_attn_abs_bwd")
+    roof["traffic"], roof["traffic_source"] = ncu_traffic(name)
     bpe = bytes_per_edge(D, T, F, K)
     step_roof = {"bytes_per_edge": bpe, "achieved_gbs_per_gpu": value / world * bpe / 1e9,
                  "frac_of_hbm": value / world * bpe / 1e9 / hbm_peak,

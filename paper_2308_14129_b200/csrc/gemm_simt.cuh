@@ -14,9 +14,11 @@
 // along the contiguous dimension are always in bounds; only the reduction
 // index is predicated (rows past a device-resident count read 0).
 //
-// Tile BM x 64 x 16 (BM = 128 or 64: the launcher picks 64 when 128-row tiles
+// Tile BM x 64 x BK (BK = 32 for BM = 64, 16 for BM = 128; BM = 128 or 64: the launcher picks 64 when 128-row tiles
 // would leave SMs idle), 256 threads, (BM/16) x 4 outputs per thread,
-// register-staged double buffering through shared memory.
+// register-staged double buffering through shared memory. BK = 32 halves the
+// k-tile count (one L2 round trip each) against 16: these GEMMs have K ~ 200
+// and too few CTAs to hide a round trip per 16 k-steps.
 #pragma once
 
 #include "pdl.cuh"
@@ -27,7 +29,7 @@
 namespace spd {
 namespace gemm {
 
-constexpr int BN = 64, BK = 16, NT = 256, TN = 4;
+constexpr int BN = 64, NT = 256, TN = 4;
 
 enum Epi : int { EPI_NONE = 0, EPI_RELU = 1, EPI_MASK = 2 /* C *= (mask > 0) */ };
 
@@ -56,6 +58,7 @@ struct Args {
 template <bool A_KMAJOR, bool B_KN, int BM, int BNT = BN>
 __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
     pdl_entry();
+    constexpr int BK = BM >= 128 ? 16 : 32;  // static shared memory <= 48 KB
     constexpr int TX = BNT / 4, TY = NT / TX;
     constexpr int TM = BM / TY;       // rows per thread
     constexpr int AV = BM * BK / 4 / NT;  // float4 A loads per thread (2 or 1)
@@ -86,7 +89,8 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
 
-    float4 ra[AV], rb;
+    constexpr int BVT = (BV + NT - 1) / NT;  // float4 B loads per thread
+    float4 ra[AV], rb[BVT];
     auto zero_tail = [&](float4& v, int gk) {
         if (gk + 3 >= k_end) {
             if (gk + 0 >= k_end) v.x = 0.f;
@@ -95,18 +99,19 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
             if (gk + 3 >= k_end) v.w = 0.f;
         }
     };
+    constexpr int KQ = BK / 4;  // float4 per BK-long row segment
     auto load_tiles = [&](int k0) {
 #pragma unroll
         for (int r = 0; r < AV; ++r) {
             const int idx = tid + r * NT;
-            if (!A_KMAJOR) {  // BM rows x 16 k: 4 float4 per row
-                const int row = idx / 4, kq = (idx % 4) * 4;
+            if (!A_KMAJOR) {  // BM rows x BK k
+                const int row = idx / KQ, kq = (idx % KQ) * 4;
                 const int gm = m0 + row, gk = k0 + kq;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (gm < a.M && gk < k_end) v = *reinterpret_cast<const float4*>(a.A + (size_t)gm * a.lda + gk);
                 zero_tail(v, gk);
                 ra[r] = v;
-            } else {  // 16 k-rows x BM m: BM/4 float4 per row
+            } else {  // BK k-rows x BM m
                 const int kr = idx / (BM / 4), mq = (idx % (BM / 4)) * 4;
                 const int gk = k0 + kr, gm = m0 + mq;
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -114,20 +119,23 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
                 ra[r] = v;
             }
         }
-        if (tid >= BV) {
-        } else if (B_KN) {  // 16 k-rows x BNT n
-            const int kr = tid / TX, nq = (tid % TX) * 4;
-            const int gk = k0 + kr, gn = n0 + nq;
+#pragma unroll
+        for (int r = 0; r < BVT; ++r) {
+            const int idx = tid + r * NT;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (gk < k_end && gn < a.N) v = *reinterpret_cast<const float4*>(a.B + (size_t)gk * a.ldb + gn);
-            rb = v;
-        } else {  // BNT n-rows x 16 k
-            const int row = tid / 4, kq = (tid % 4) * 4;
-            const int gn = n0 + row, gk = k0 + kq;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (gn < a.N && gk < k_end) v = *reinterpret_cast<const float4*>(a.B + (size_t)gn * a.ldb + gk);
-            zero_tail(v, gk);
-            rb = v;
+            if (idx < BV) {
+                if (B_KN) {  // BK k-rows x BNT n
+                    const int kr = idx / TX, nq = (idx % TX) * 4;
+                    const int gk = k0 + kr, gn = n0 + nq;
+                    if (gk < k_end && gn < a.N) v = *reinterpret_cast<const float4*>(a.B + (size_t)gk * a.ldb + gn);
+                } else {  // BNT n-rows x BK k
+                    const int row = idx / KQ, kq = (idx % KQ) * 4;
+                    const int gn = n0 + row, gk = k0 + kq;
+                    if (gn < a.N && gk < k_end) v = *reinterpret_cast<const float4*>(a.B + (size_t)gn * a.ldb + gk);
+                    zero_tail(v, gk);
+                }
+            }
+            rb[r] = v;
         }
     };
     auto store_tiles = [&](int buf) {
@@ -135,7 +143,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
         for (int r = 0; r < AV; ++r) {
             const int idx = tid + r * NT;
             if (!A_KMAJOR) {
-                const int row = idx / 4, kq = (idx % 4) * 4;
+                const int row = idx / KQ, kq = (idx % KQ) * 4;
                 As[buf][kq + 0][row] = ra[r].x;
                 As[buf][kq + 1][row] = ra[r].y;
                 As[buf][kq + 2][row] = ra[r].z;
@@ -145,16 +153,20 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
                 *reinterpret_cast<float4*>(&As[buf][kr][mq]) = ra[r];
             }
         }
-        if (tid >= BV) {
-        } else if (B_KN) {
-            const int kr = tid / TX, nq = (tid % TX) * 4;
-            *reinterpret_cast<float4*>(&Bs[buf][kr][nq]) = rb;
-        } else {
-            const int row = tid / 4, kq = (tid % 4) * 4;
-            Bs[buf][kq + 0][row] = rb.x;
-            Bs[buf][kq + 1][row] = rb.y;
-            Bs[buf][kq + 2][row] = rb.z;
-            Bs[buf][kq + 3][row] = rb.w;
+#pragma unroll
+        for (int r = 0; r < BVT; ++r) {
+            const int idx = tid + r * NT;
+            if (idx >= BV) continue;
+            if (B_KN) {
+                const int kr = idx / TX, nq = (idx % TX) * 4;
+                *reinterpret_cast<float4*>(&Bs[buf][kr][nq]) = rb[r];
+            } else {
+                const int row = idx / KQ, kq = (idx % KQ) * 4;
+                Bs[buf][kq + 0][row] = rb[r].x;
+                Bs[buf][kq + 1][row] = rb[r].y;
+                Bs[buf][kq + 2][row] = rb[r].z;
+                Bs[buf][kq + 3][row] = rb[r].w;
+            }
         }
     };
 

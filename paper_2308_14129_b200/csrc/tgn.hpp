@@ -196,6 +196,7 @@ private:
     // (first gradient writer) joins it
     cudaStream_t zs_ = nullptr;
     cudaEvent_t ev_zfork_ = nullptr, ev_zero_ = nullptr;
+    cudaEvent_t ev_bwdx_ = nullptr;  // attention input-gradient scatter done
 
     spd_tgn_config cfg_;
     ParamLayout lay_;

@@ -313,9 +313,9 @@ __global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, c
 }
 
 __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd) {
-    const std::size_t stage = std::size_t(kRootsPerBlock) * d.K * row_bytes(d, bwd);
-    const std::size_t tpart = std::size_t(kRootsPerBlock) * 2 * d.T * sizeof(float);
-    return (stage > tpart ? stage : tpart) + kRootsPerBlock * 2 * sizeof(float) * d.H * d.K +
+    // forward and backward stage the same rows (memory | cos | features)
+    const std::size_t stage = std::size_t(kRootsPerBlock) * d.K * row_bytes(d, false);
+    return stage + kRootsPerBlock * 2 * sizeof(float) * d.H * d.K +
            kRootsPerBlock * sizeof(std::uint64_t);
 }
 int attn_roots_per_block() { return kRootsPerBlock; }
@@ -390,13 +390,19 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     store_slots<S, HMAX>(v, xbar + row0, d, lane, d.rnd);
 }
 
-// Backward, given dxbar_h = [W_V,h|b_V,h]^T dctx_h (GEMM) per root:
-//   da_hj = <dxbar_h, x~_j>;  ds_hj = a_hj (da_hj - sum_k a_hk da_hk) / sqrt(dh)
-//   dq'_h = sum_j ds_hj x~_j                         -> dQp (GEMMs give dQ, dW_K)
-//   dx_j  = sum_h a_hj dxbar_h + ds_hj q'_h  on the gradient-carrying columns:
-//           memory part -> dH rows of pending nodes (float4 atomics), time part
-//           -> d/dw, d/db of cos(w dt + b) (per-block partials, fixed order).
-// part: [gridDim.x][2T] (w then b), f64; every block writes its row.
+// Backward, given dxbar_h = [W_V,h|b_V,h]^T dctx_h (GEMM) per root, in two
+// kernels so the critical path (dq'_h -> dQ GEMM -> query backward) does not
+// wait for the input-gradient scatter:
+//   k_attn_abs_bwd (critical path):
+//     da_hj = <dxbar_h, x~_j>;  ds_hj = a_hj (da_hj - sum_k a_hk da_hk) / sqrt(dh)
+//     dq'_h = sum_j ds_hj x~_j                       -> dQp (GEMMs give dQ, dW_K)
+//     ds    -> dsc [R][H][K] for the scatter kernel
+//   k_attn_abs_bwd_x (side stream, beside the dQ GEMMs):
+//     dx_j  = sum_h a_hj dxbar_h + ds_hj q'_h  on the gradient-carrying columns:
+//             memory part -> dH rows of pending nodes (float4 atomics), time
+//             part -> d/dw, d/db of cos(w dt + b) (per-block partials, fixed order).
+//   It needs no staged neighbour rows: only per-root vectors, the
+//   neighbours' slots and dt, and the sin half of their phi rows.
 template <int NM, int NT, int NF, int HMAX>
 __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R,
                                                       const float* time_w, const float* time_b,
@@ -405,66 +411,106 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
                                                       const double* nbr_dt, const int* cnt,
                                                       const float* mem_new, const float* Qp,
                                                       const float* alpha, const float* dxbar,
-                                                      const float* phi, float* dQp, float* dH,
-                                                      double* part) {
+                                                      const float* phi, float* dQp, float* dsc) {
     pdl_entry();
     using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = blockIdx.x * kRootsPerBlock + warp;
-    constexpr bool BWD = true;
+    if (r >= R) return;
+    constexpr bool BWD = false;  // staged rows: memory | cos | features (as the forward)
     const int RB = row_bytes(d, BWD);
     unsigned char* xs = smem + (std::size_t)warp * d.K * RB;
-    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(smem + attn_smem_bytes(d, BWD)) - kRootsPerBlock + warp;
+    std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(smem + attn_smem_bytes(d, true)) - kRootsPerBlock + warp;
     float* sc = reinterpret_cast<float*>(bar - warp) - kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
     if (lane == 0) bar_init(bar);
     __syncwarp();
     float* aa = sc + d.H * d.K;  // alpha of this root
-    const int c_n = r < R ? cnt[r] : 0;
+    const int c_n = cnt[r];
     const std::size_t row0 = (std::size_t)r * d.H * d.ld_p;
-    float4 gw[NT], gb[NT];  // time-encoder gradient partials of this lane's time slots
-#pragma unroll
-    for (int i = 0; i < NT; ++i) gw[i] = gb[i] = z4();
     float4 v[HMAX][S::N];  // dxbar_h, then the dq'_h accumulators
-    if (r < R && c_n == 0) {
+    if (c_n == 0) {
 #pragma unroll
         for (int h = 0; h < HMAX; ++h)
 #pragma unroll
             for (int i = 0; i < S::N; ++i) v[h][i] = z4();
         store_slots<S, HMAX>(v, dQp + row0, d, lane, 0);
+        return;
     }
-    if (c_n > 0) {
-        double m_dt;
-        int m_slot;
-        stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, BWD, phi, bar, m_dt, m_slot);
-        if (lane < d.K)
-            for (int h = 0; h < d.H; ++h)
-                aa[h * d.K + lane] = lane < c_n ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
-        load_slots<S, HMAX>(v, dxbar + row0, d, lane);
-        bar_wait(bar, 0);
+    double m_dt;
+    int m_slot;
+    stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, BWD, phi, bar, m_dt, m_slot);
+    if (lane < d.K)
+        for (int h = 0; h < d.H; ++h)
+            aa[h * d.K + lane] = lane < c_n ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
+    load_slots<S, HMAX>(v, dxbar + row0, d, lane);
+    bar_wait(bar, 0);
+    __syncwarp();
+    // pass 1: da_hj
+    dots<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc, 1.f);
+    __syncwarp();
+    // softmax backward (lane = neighbour): ds = a (da - <a, da>) / sqrt(dh)
+    const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
+    for (int h = 0; h < d.H; ++h) {
+        const float a = lane < c_n ? aa[h * d.K + lane] : 0.f;
+        const float da = lane < c_n ? sc[h * d.K + lane] : 0.f;
+        const float dot = warp_sum(a * da);
         __syncwarp();
-        // pass 1: da_hj
-        dots<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc, 1.f);
-        __syncwarp();
-        // softmax backward (lane = neighbour): ds = a (da - <a, da>) / sqrt(dh)
-        const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
-        for (int h = 0; h < d.H; ++h) {
-            const float a = lane < c_n ? aa[h * d.K + lane] : 0.f;
-            const float da = lane < c_n ? sc[h * d.K + lane] : 0.f;
-            const float dot = warp_sum(a * da);
-            __syncwarp();
-            if (lane < d.K) sc[h * d.K + lane] = lane < c_n ? a * (da - dot) * inv : 0.f;
+        const float ds = lane < c_n ? a * (da - dot) * inv : 0.f;
+        if (lane < d.K) {
+            sc[h * d.K + lane] = ds;
+            dsc[((std::size_t)r * d.H + h) * d.K + lane] = ds;
         }
-        __syncwarp();
-        // pass 2a: dq'_h = sum_j ds_hj x~_j
+    }
+    __syncwarp();
+    // pass 2a: dq'_h = sum_j ds_hj x~_j
 #pragma unroll
-        for (int h = 0; h < HMAX; ++h)
+    for (int h = 0; h < HMAX; ++h)
 #pragma unroll
-            for (int i = 0; i < S::N; ++i) v[h][i] = z4();
-        axpys<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc);
-        store_slots<S, HMAX>(v, dQp + row0, d, lane, d.rnd);
-        // pass 2b: input gradients on [s_nbr | phi] (memory and time slots)
-        constexpr int NX = NM + NT;
+        for (int i = 0; i < S::N; ++i) v[h][i] = z4();
+    axpys<S, HMAX>(v, d, lane, xs, RB, feat_off(d, BWD), c_n, sc);
+    store_slots<S, HMAX>(v, dQp + row0, d, lane, d.rnd);
+}
+
+// Input-gradient scatter of the attention backward (see above). One warp per
+// root, kRootsPerBlock roots per block; part: [gridDim.x][2T] (w then b), f64,
+// every block writes its row. Lane slots cover the memory (NM) and time (NT)
+// columns; per neighbour the lane's sin values come straight from the phi
+// rows (L2), one neighbour ahead of use.
+template <int NM, int NT, int HMAX>
+__global__ void __launch_bounds__(128) k_attn_abs_bwd_x(WorkerDev w, Dims d, int R,
+                                                        const std::uint32_t* nbr_node,
+                                                        const double* nbr_dt, const int* cnt,
+                                                        const float* Qp, const float* alpha,
+                                                        const float* dsc, const float* dxbar,
+                                                        const float* phi, float* dH, double* part) {
+    pdl_entry();
+    using S = Slots<NM, NT, 0>;
+    constexpr int NX = NM + NT;
+    __shared__ float red[kRootsPerBlock][2 * 4 * 32 * NT];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * kRootsPerBlock + warp;
+    const int c_n = r < R ? cnt[r] : 0;
+    float4 gw[NT], gb[NT];  // time-encoder gradient partials of this lane's time slots
+#pragma unroll
+    for (int i = 0; i < NT; ++i) gw[i] = gb[i] = z4();
+    if (c_n > 0) {
+        const std::size_t row0 = (std::size_t)r * d.H * d.ld_p;
+        // neighbour j's (slot, dt) on lane j; alpha and ds of lane j per head
+        int m_slot = -1;
+        double m_dt = 0.0;
+        float la[HMAX], ls[HMAX];
+        if (lane < c_n) {
+            const std::size_t o = (std::size_t)r * d.K + lane;
+            m_slot = w.slot[nbr_node[o]];
+            m_dt = nbr_dt[o];
+        }
+#pragma unroll
+        for (int h = 0; h < HMAX; ++h) {
+            const bool ok = h < d.H && lane < c_n;
+            la[h] = ok ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
+            ls[h] = ok ? dsc[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
+        }
         float4 g[HMAX][NX], q[HMAX][NX];
 #pragma unroll
         for (int h = 0; h < HMAX; ++h)
@@ -475,16 +521,30 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
                 g[h][i] = ok ? *reinterpret_cast<const float4*>(dxbar + row0 + (std::size_t)h * d.ld_p + c) : z4();
                 q[h][i] = ok ? *reinterpret_cast<const float4*>(Qp + row0 + (std::size_t)h * d.ld_p + c) : z4();
             }
+        const float* sin0 = phi + (std::size_t)r * d.K * 2 * d.T + d.T;
+        float4 snx[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            const int o = 4 * (lane + 32 * i);
+            snx[i] = o < d.T ? *reinterpret_cast<const float4*>(sin0 + o) : z4();
+        }
 #pragma unroll 1
         for (int j = 0; j < c_n; ++j) {
             const int slot = __shfl_sync(0xffffffffu, m_slot, j);
             const float fdt = (float)__shfl_sync(0xffffffffu, m_dt, j);
-            const float* sn = reinterpret_cast<const float*>(xs + (std::size_t)j * RB + 4 * (d.D + d.T));
-            float a[HMAX], s[HMAX];
+            float a[HMAX], sv_[HMAX];
 #pragma unroll
             for (int h = 0; h < HMAX; ++h) {
-                a[h] = h < d.H ? aa[h * d.K + j] : 0.f;
-                s[h] = h < d.H ? sc[h * d.K + j] : 0.f;
+                a[h] = __shfl_sync(0xffffffffu, la[h], j);
+                sv_[h] = __shfl_sync(0xffffffffu, ls[h], j);
+            }
+            float4 snc[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                snc[i] = snx[i];
+                const int o = 4 * (lane + 32 * i);
+                if (j + 1 < c_n && o < d.T)
+                    snx[i] = *reinterpret_cast<const float4*>(sin0 + (std::size_t)(j + 1) * 2 * d.T + o);
             }
 #pragma unroll
             for (int i = 0; i < NX; ++i) {
@@ -493,13 +553,13 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
 #pragma unroll
                 for (int h = 0; h < HMAX; ++h) {
                     axpy4(gx, a[h], g[h][i]);
-                    axpy4(gx, s[h], q[h][i]);
+                    axpy4(gx, sv_[h], q[h][i]);
                 }
                 const int o = 4 * (lane + 32 * S::local(i));
                 if (S::region(i) == 0) {
                     if (slot >= 0) atomicAdd(reinterpret_cast<float4*>(dH + (std::size_t)slot * d.D + o), gx);
                 } else {
-                    const float4 sv = *reinterpret_cast<const float4*>(sn + o);
+                    const float4 sv = snc[S::local(i)];
                     float4& bw = gw[S::local(i)];
                     float4& bb = gb[S::local(i)];
                     bb.x -= sv.x * gx.x; bb.y -= sv.y * gx.y; bb.z -= sv.z * gx.z; bb.w -= sv.w * gx.w;
@@ -510,24 +570,19 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
         }
     }
     // fixed-order per-block reduction of the roots' time-encoder partials
-    // (the staging area is reused: [kRootsPerBlock][2T] f32)
-    __syncthreads();
-    float* tw = reinterpret_cast<float*>(smem) + warp * 2 * d.T;
-    for (int c = lane; c < 2 * d.T; c += 32) tw[c] = 0.f;
-    __syncwarp();
+    float* tw = red[warp];
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
         const int t = 4 * (lane + 32 * i);
-        if (t < d.T) {
-            *reinterpret_cast<float4*>(tw + t) = gw[i];
-            *reinterpret_cast<float4*>(tw + d.T + t) = gb[i];
-        }
+        *reinterpret_cast<float4*>(tw + t) = gw[i];
+        *reinterpret_cast<float4*>(tw + 4 * 32 * NT + t) = gb[i];
     }
     __syncthreads();
     for (int c = threadIdx.x; c < 2 * d.T; c += blockDim.x) {
+        const int cc = c < d.T ? c : 4 * 32 * NT + (c - d.T);
         double sacc = 0.0;
 #pragma unroll
-        for (int k = 0; k < kRootsPerBlock; ++k) sacc += (double)reinterpret_cast<float*>(smem)[k * 2 * d.T + c];
+        for (int k = 0; k < kRootsPerBlock; ++k) sacc += (double)red[k][cc];
         part[(std::size_t)blockIdx.x * 2 * d.T + c] = sacc;
     }
 }
@@ -540,14 +595,20 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     template __global__ void k_attn_abs_bwd<NM, NT, NF, HM>(                                     \
         WorkerDev, Dims, int, const float*, const float*, const std::uint32_t*,                  \
         const std::uint32_t*, const double*, const int*, const float*, const float*,             \
-        const float*, const float*, const float*, float*, float*, double*);
+        const float*, const float*, const float*, float*, float*);
+#define SPD_ABSX_INST(NM, NT, HM)                                                               \
+    template __global__ void k_attn_abs_bwd_x<NM, NT, HM>(                                       \
+        WorkerDev, Dims, int, const std::uint32_t*, const double*, const int*, const float*,     \
+        const float*, const float*, const float*, const float*, float*, double*);
 #define SPD_ABS_NF(NM, NT, HM) \
-    SPD_ABS_INST(NM, NT, 1, HM) SPD_ABS_INST(NM, NT, 2, HM) SPD_ABS_INST(NM, NT, 3, HM)
+    SPD_ABS_INST(NM, NT, 1, HM) SPD_ABS_INST(NM, NT, 2, HM) SPD_ABS_INST(NM, NT, 3, HM) \
+    SPD_ABSX_INST(NM, NT, HM)
 #define SPD_ABS_H(HM) SPD_ABS_NF(1, 1, HM) SPD_ABS_NF(1, 2, HM) SPD_ABS_NF(2, 1, HM)
 SPD_ABS_H(2)
 SPD_ABS_H(4)
 #undef SPD_ABS_H
 #undef SPD_ABS_NF
+#undef SPD_ABSX_INST
 #undef SPD_ABS_INST
 
 }  // namespace tgnk

@@ -87,8 +87,12 @@ __global__ void k_attn_abs_bwd(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* nbr_node,
                                const std::uint32_t* nbr_ev, const double* nbr_dt, const int* cnt,
                                const float* mem_new, const float* Qp, const float* alpha,
-                               const float* dxbar, const float* phi, float* dQp, float* dH,
-                               double* part);
+                               const float* dxbar, const float* phi, float* dQp, float* dsc);
+template <int NM, int NT, int HMAX>
+__global__ void k_attn_abs_bwd_x(WorkerDev w, Dims d, int R, const std::uint32_t* nbr_node,
+                                 const double* nbr_dt, const int* cnt, const float* Qp,
+                                 const float* alpha, const float* dsc, const float* dxbar,
+                                 const float* phi, float* dH, double* part);
 __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
                                const int* cnt, const float* O, const float* mem_new, float* m_in);
 __global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in);

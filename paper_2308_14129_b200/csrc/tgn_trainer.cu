@@ -103,7 +103,7 @@ struct Scratch {
     DevBuf<double> root_t, nbr_dt;
     DevBuf<int> cnt;
     DevBuf<float> x_gru, h_gru, Gi, Gh, gsave, mem_new, dH, dGi, dGh;
-    DevBuf<float> q_in, Q, Qp, xbar, alpha, ctx, O, m_in, Z1, emb, d_in, D1, logits, lossv, dlogit;
+    DevBuf<float> q_in, Q, Qp, xbar, alpha, dsc, ctx, O, m_in, Z1, emb, d_in, D1, logits, lossv, dlogit;
     DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dxbar, dQp, dQ, dq_in;
     DevBuf<float> ws;
     DevBuf<double> tpart;
@@ -255,8 +255,8 @@ void attn_pick(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& 
     else
         attn_launch(&tgnk::k_attn_abs_bwd<NM, NT, NF, HM>, set_bwd, grid, tgnk::attn_smem_bytes(d, true), st,
                     wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
-                    s.Qp.p, s.alpha.p, s.dxbar.p, static_cast<const float*>(s.phi.p), s.dQp.p, s.dH.p,
-                    part);
+                    s.Qp.p, s.alpha.p, s.dxbar.p, static_cast<const float*>(s.phi.p), s.dQp.p,
+                    s.dsc.p);
 }
 
 void attn_dispatch(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& wd,
@@ -282,6 +282,28 @@ void attn_abs_fwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const f
                   const float* tb, const Scratch& s, cudaStream_t st) {
     const int rpb = tgnk::attn_roots_per_block();
     attn_dispatch(false, unsigned((R + rpb - 1) / rpb), st, wd, d, R, tw, tb, s, nullptr);
+}
+
+// input-gradient scatter of the attention backward (tgn_attn.cu k_attn_abs_bwd_x)
+void attn_abs_bwd_x(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const Scratch& s,
+                    double* part, cudaStream_t st) {
+    const int nm = (d.D + 127) / 128, nt = (d.T + 127) / 128;
+    const unsigned grid = unsigned(s.tattn_blocks);  // every block writes its partial row
+#define SPD_X(NM, NT)                                                                            \
+    if (nm == NM && nt == NT) {                                                                 \
+        if (d.H <= 2)                                                                           \
+            launch(tgnk::k_attn_abs_bwd_x<NM, NT, 2>, grid, 128, 0, st, wd, d, R, s.nbr_node.p,  \
+                   s.nbr_dt.p, s.cnt.p, s.Qp.p, s.alpha.p, s.dsc.p, s.dxbar.p,                   \
+                   static_cast<const float*>(s.phi.p), s.dH.p, part);                            \
+        else                                                                                    \
+            launch(tgnk::k_attn_abs_bwd_x<NM, NT, 4>, grid, 128, 0, st, wd, d, R, s.nbr_node.p,  \
+                   s.nbr_dt.p, s.cnt.p, s.Qp.p, s.alpha.p, s.dsc.p, s.dxbar.p,                   \
+                   static_cast<const float*>(s.phi.p), s.dH.p, part);                            \
+        return;                                                                                 \
+    }
+    SPD_X(1, 1) SPD_X(1, 2) SPD_X(2, 1)
+#undef SPD_X
+    internal_error("InvalidParams", "attention row outside the instantiated shapes");
 }
 
 void attn_abs_bwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
@@ -366,7 +388,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
 
     SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
     SPD_CUDA(cudaStreamCreateWithPriority(&zs_, cudaStreamNonBlocking, prio_lo));
-    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_phi_, &ev_zfork_, &ev_zero_})
+    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_phi_, &ev_zfork_, &ev_zero_, &ev_bwdx_})
         SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors);
     feat_seed_mixed_ = mix64(cfg.seed_feat);
@@ -429,6 +451,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.Qp.alloc(hp); s.xbar.alloc(hp); s.dxbar.alloc(hp); s.dQp.alloc(hp);
     s.Qp.zero(stream_); s.xbar.zero(stream_); s.dxbar.zero(stream_); s.dQp.zero(stream_);
     s.alpha.alloc(std::size_t(R) * d.H * d.K);
+    s.dsc.alloc(std::size_t(R) * d.H * d.K);
     s.ctx.alloc(std::size_t(R) * d.ld_ctx); init_aug(s.ctx, R, d.DQ, d.ld_ctx, stream_);
     s.O.alloc(std::size_t(R) * d.DQ);
     s.m_in.alloc(std::size_t(R) * d.ld_m); init_aug(s.m_in, R, d.DQ + D, d.ld_m, stream_);
@@ -497,7 +520,7 @@ TGNTrainer::~TGNTrainer() {
         if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
         if (sides_[k]) cudaStreamDestroy(sides_[k]);
     }
-    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_phi_, ev_zfork_, ev_zero_})
+    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_phi_, ev_zfork_, ev_zero_, ev_bwdx_})
         if (e) cudaEventDestroy(e);
     if (aux_) cudaStreamDestroy(aux_);
     if (zs_) cudaStreamDestroy(zs_);
@@ -909,10 +932,20 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         proj_dgrad(tc, s.dctx.p, d.ld_Q, WV, ldw, s.dxbar.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0,
                    nullptr, 0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
     });
+    double* attn_part = s.tpart.p + std::size_t(s.troot_blocks) * 2 * d.T;
     timed("k_attn_abs_bwd", [&] {
-        attn_abs_bwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s,
-                     s.tpart.p + std::size_t(s.troot_blocks) * 2 * d.T, st);
+        attn_abs_bwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, nullptr, st);
     });
+    // the input-gradient scatter (dH of neighbours, time-encoder partials)
+    // runs beside the dQ GEMMs; gru_bwd and the time-grad reduction wait for it
+    if (profile_) {
+        timed("attn_bwd_x", [&] { attn_abs_bwd_x(wd, d, R, s, attn_part, st); });
+    } else {
+        side([&](cudaStream_t sd) {
+            attn_abs_bwd_x(wd, d, R, s, attn_part, sd);
+            SPD_CUDA(cudaEventRecord(ev_bwdx_, sd));
+        });
+    }
     timed("gemm_dq", [&] {
         // dW_K,h += Q_h^T dQp_h ; dQ_h = dQp_h [W_K,h | b_K,h]^T
         side([&](cudaStream_t sd) {
@@ -931,6 +964,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     timed("root_time_bwd", [&] {
         launch(tgnk::k_root_grad, s.troot_blocks, dim3(32, 8), 0, st, wd, d, R, s.roots.p, s.dq_in.p,
                s.dm_in.p, P + lay_.time_b, s.trows, s.dH.p, s.tpart.p);
+        if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_bwdx_, 0));  // dH, attention partials
         // the time-encoder gradient is next read by the all-reduce: side stream
         side([&](cudaStream_t sd) {
             launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, sd, d.T, s.troot_blocks + s.tattn_blocks,
