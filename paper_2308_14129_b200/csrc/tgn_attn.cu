@@ -31,7 +31,14 @@ namespace tgnk {
 
 namespace {
 
-constexpr int kRootsPerBlock = 4;
+// roots (warps) per block of the staging kernels: the staged rows (~11.8 KB
+// per root at GDELT dims) bound residency, and 3-root blocks pack 18 warps
+// per SM where 4-root blocks fit 16
+#ifndef SPD_ATTN_ROOTS
+#define SPD_ATTN_ROOTS 3
+#endif
+constexpr int kRootsPerBlock = SPD_ATTN_ROOTS;
+constexpr int kRootsX = 4;  // roots per 128-thread block of the scatter kernel
 
 __device__ __forceinline__ float dot4acc(const float4& a, const float4& b, float acc) {
     return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, fmaf(a.x, b.x, acc))));
@@ -319,6 +326,7 @@ __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd) {
            kRootsPerBlock * sizeof(std::uint64_t);
 }
 int attn_roots_per_block() { return kRootsPerBlock; }
+int attn_x_roots_per_block() { return kRootsX; }
 
 // Forward: scores from q'_h (Qp), softmax, alpha [R][H][K], xbar_h [R][H][ld_p]
 // (tf32-rounded when it feeds a tensor-core GEMM). Roots without neighbours
@@ -487,9 +495,9 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd_x(WorkerDev w, Dims d, int
     pdl_entry();
     using S = Slots<NM, NT, 0>;
     constexpr int NX = NM + NT;
-    __shared__ float red[kRootsPerBlock][2 * 4 * 32 * NT];
+    __shared__ float red[kRootsX][2 * 4 * 32 * NT];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = blockIdx.x * kRootsPerBlock + warp;
+    const int r = blockIdx.x * kRootsX + warp;
     const int c_n = r < R ? cnt[r] : 0;
     float4 gw[NT], gb[NT];  // time-encoder gradient partials of this lane's time slots
 #pragma unroll
@@ -582,7 +590,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd_x(WorkerDev w, Dims d, int
         const int cc = c < d.T ? c : 4 * 32 * NT + (c - d.T);
         double sacc = 0.0;
 #pragma unroll
-        for (int k = 0; k < kRootsPerBlock; ++k) sacc += (double)red[k][cc];
+        for (int k = 0; k < kRootsX; ++k) sacc += (double)red[k][cc];
         part[(std::size_t)blockIdx.x * 2 * d.T + c] = sacc;
     }
 }

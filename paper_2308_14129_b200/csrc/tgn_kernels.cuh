@@ -76,6 +76,7 @@ __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd);
 __global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, const double* nbr_dt,
                       const int* cnt, float* phi);
 int attn_roots_per_block();
+int attn_x_roots_per_block();
 template <int NM, int NT, int NF, int HMAX>
 __global__ void k_attn_abs_fwd(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* nbr_node,

@@ -9,6 +9,7 @@
 //   weight-gradient GEMMs accumulating straight into the flat gradient.
 #include "pdl.cuh"
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 #include <atomic>
 #include <cmath>
@@ -32,9 +33,33 @@ std::atomic<std::uint64_t> g_kernel_launches{0};
 // Every kernel of the TGN path goes through here: counted (bench.py reports
 // the launches inside the timed region) and checked.
 // Optionally launched with programmatic stream serialization (pdl.cuh).
+// Every kernel prefers the maximum shared-memory carveout. An SM's L1/shared
+// split is fixed while blocks are resident, so a side-stream kernel launched
+// with a small-shared carveout (k_phi, k_roots_nbrs: no shared memory) would
+// keep the critical path's GEMM and attention CTAs (72-190 KB) off every SM it
+// occupies until it drains (CUPTI: a 20 us hole before the query GEMM).
+// SPD_CARVEOUT=0 restores the driver default (experiments).
+bool carveout_max() {
+    static const bool v = [] {
+        const char* e = std::getenv("SPD_CARVEOUT");
+        return !(e && *e == '0');
+    }();
+    return v;
+}
+template <class K>
+void prefer_max_shared(K k) {
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        if (carveout_max())
+            SPD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          int(cudaSharedmemCarveoutMaxShared)));
+    });
+}
+
 template <class... KArgs, class... Args>
 void launch(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
             Args&&... args) {
+    prefer_max_shared(k);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -240,7 +265,7 @@ void attn_launch(Kern k, std::size_t& set, unsigned grid, std::size_t smem, cuda
                                       int(cudaSharedmemCarveoutMaxShared)));
         set = smem;
     }
-    launch(k, grid, 128, smem, st, std::forward<Args>(args)...);
+    launch(k, grid, 32 * tgnk::attn_roots_per_block(), smem, st, std::forward<Args>(args)...);
 }
 
 template <int NM, int NT, int NF, int HM>
@@ -308,9 +333,8 @@ void attn_abs_bwd_x(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const
 
 void attn_abs_bwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
                   const float* tb, const Scratch& s, double* part, cudaStream_t st) {
-    // every block of the partial region writes (zeros past R): the final
-    // reduction covers the region sized for the largest batch
-    attn_dispatch(true, unsigned(s.tattn_blocks), st, wd, d, R, tw, tb, s, part);
+    const int rpb = tgnk::attn_roots_per_block();
+    attn_dispatch(true, unsigned((R + rpb - 1) / rpb), st, wd, d, R, tw, tb, s, part);
 }
 
 tgnk::WorkerDev devview(Worker& w) {
@@ -468,7 +492,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
     s.trows = 16;
     s.troot_blocks = (R + s.trows - 1) / s.trows;
-    s.tattn_blocks = (R + tgnk::attn_roots_per_block() - 1) / tgnk::attn_roots_per_block();
+    s.tattn_blocks = (R + tgnk::attn_x_roots_per_block() - 1) / tgnk::attn_x_roots_per_block();
     s.tpart.alloc(std::size_t(s.troot_blocks + s.tattn_blocks) * 2 * d.T);
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
     SPD_CUDA(cudaStreamSynchronize(stream_));
