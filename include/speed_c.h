@@ -368,6 +368,14 @@ spd_status spd_tgn_run_steps(spd_tgn_trainer* t, uint64_t n, float* device_ms);
  * feature rows of stride feat_stride) — copied H2D, trained, losses copied back. */
 spd_status spd_tgn_step_host(spd_tgn_trainer* t, const spd_edge* const* events,
                              const uint16_t* const* feats, float* loss_out);
+/* Pipelined form of spd_tgn_step_host: same inputs (pin them), but host
+ * staging of this batch overlaps the device's previous step (pinned staging
+ * ring, copies on a copy stream the step waits on) and the per-worker losses
+ * land in the caller's pinned loss_pinned asynchronously. spd_tgn_sync waits
+ * for all queued steps; read loss_pinned after it. */
+spd_status spd_tgn_step_host_async(spd_tgn_trainer* t, const spd_edge* const* events,
+                                   const uint16_t* const* feats, float* loss_pinned);
+spd_status spd_tgn_sync(spd_tgn_trainer* t);
 /* Event range [lo, hi) of worker's next batch in its local stream. */
 spd_status spd_tgn_next_batch(const spd_tgn_trainer* t, int32_t worker, uint64_t* lo,
                               uint64_t* hi, int32_t* feat_stride);

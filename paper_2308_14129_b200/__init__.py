@@ -937,6 +937,19 @@ class TGNTrainer:
         _check(lib.spd_tgn_step_host(self._h, ev, ft, ptr(out, f32)))
         return out[: len(self.workers)]
 
+    def step_host_async(self, events: list, feats: list | None, loss_pinned: np.ndarray):
+        """Pipelined end-to-end step (spd_tgn_step_host_async): inputs as
+        step_host (pinned), losses land in `loss_pinned` (float32[workers],
+        pinned) once `sync()` returns. Keep the inputs alive until then."""
+        ev = (C.c_void_p * len(events))(*[e.ctypes.data for e in events])
+        ft = (C.c_void_p * len(events))(*[f.ctypes.data for f in feats]) if feats else None
+        if loss_pinned.dtype != np.float32 or len(loss_pinned) < len(self.workers):
+            raise UsageError("Usage", "loss_pinned must be float32[n_workers]")
+        _check(lib.spd_tgn_step_host_async(self._h, ev, ft, loss_pinned.ctypes.data))
+
+    def sync(self):
+        _check(lib.spd_tgn_sync(self._h))
+
     def io_bytes(self):
         a, b = u64(), u64()
         _check(lib.spd_tgn_io_bytes(self._h, C.byref(a), C.byref(b)))

@@ -110,7 +110,10 @@ public:
     std::uint64_t batch_size() const { return cfg_.batch_size; }
     void begin_epoch(int epoch);
     void seek(std::uint64_t step);
-    void rebind(const SubGraphs& subs);  // shuffle-combine: next epoch's regrouped subgraphs
+    void rebind(const SubGraphs& subs);
+    void step_host_async(const spd_edge* const* events, const std::uint16_t* const* feats,
+                         float* loss_pinned);
+    void sync();  // shuffle-combine: next epoch's regrouped subgraphs
     void step(float* loss_out);
     void end_epoch();
     void run_epoch(int epoch, double* mean_loss);
@@ -232,6 +235,15 @@ private:
     bool debug_ = false;
     unsigned char* stage_ = nullptr;  // pinned
     std::size_t stage_bytes_ = 0;
+    // pipelined end-to-end steps (step_host_async): a ring of pinned SoA
+    // staging slots, their copies on their own stream, one event per slot
+    static constexpr int kStageSlots = 3;
+    unsigned char* aring_[kStageSlots] = {};
+    std::size_t aring_bytes_ = 0;
+    cudaEvent_t aring_ev_[kStageSlots] = {};
+    bool aring_used_[kStageSlots] = {};
+    int aring_next_ = 0;
+    cudaStream_t copy_ = nullptr;
     std::uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
     std::uint64_t feat_seed_mixed_ = 0;
 };

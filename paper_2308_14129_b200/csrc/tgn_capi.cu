@@ -131,6 +131,11 @@ spd_status spd_tgn_step_host(spd_tgn_trainer* t, const spd_edge* const* events,
                              const uint16_t* const* feats, float* loss_out) {
     GUARD({ t->t->step_host(events, feats, loss_out); });
 }
+spd_status spd_tgn_step_host_async(spd_tgn_trainer* t, const spd_edge* const* events,
+                                   const uint16_t* const* feats, float* loss_pinned) {
+    GUARD({ t->t->step_host_async(events, feats, loss_pinned); });
+}
+spd_status spd_tgn_sync(spd_tgn_trainer* t) { GUARD({ t->t->sync(); }); }
 spd_status spd_tgn_next_batch(const spd_tgn_trainer* t, int32_t worker, uint64_t* lo,
                               uint64_t* hi, int32_t* feat_stride) {
     GUARD({

@@ -33,33 +33,9 @@ std::atomic<std::uint64_t> g_kernel_launches{0};
 // Every kernel of the TGN path goes through here: counted (bench.py reports
 // the launches inside the timed region) and checked.
 // Optionally launched with programmatic stream serialization (pdl.cuh).
-// Every kernel prefers the maximum shared-memory carveout. An SM's L1/shared
-// split is fixed while blocks are resident, so a side-stream kernel launched
-// with a small-shared carveout (k_phi, k_roots_nbrs: no shared memory) would
-// keep the critical path's GEMM and attention CTAs (72-190 KB) off every SM it
-// occupies until it drains (CUPTI: a 20 us hole before the query GEMM).
-// SPD_CARVEOUT=0 restores the driver default (experiments).
-bool carveout_max() {
-    static const bool v = [] {
-        const char* e = std::getenv("SPD_CARVEOUT");
-        return !(e && *e == '0');
-    }();
-    return v;
-}
-template <class K>
-void prefer_max_shared(K k) {
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        if (carveout_max())
-            SPD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                          int(cudaSharedmemCarveoutMaxShared)));
-    });
-}
-
 template <class... KArgs, class... Args>
 void launch(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
             Args&&... args) {
-    prefer_max_shared(k);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -547,6 +523,11 @@ TGNTrainer::~TGNTrainer() {
     for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_phi_, ev_zfork_, ev_zero_, ev_bwdx_})
         if (e) cudaEventDestroy(e);
     if (aux_) cudaStreamDestroy(aux_);
+    for (auto& p : aring_)
+        if (p) cudaFreeHost(p);
+    for (auto& e : aring_ev_)
+        if (e) cudaEventDestroy(e);
+    if (copy_) cudaStreamDestroy(copy_);
     if (zs_) cudaStreamDestroy(zs_);
     if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
     if (stream_) cudaStreamDestroy(stream_);
@@ -1102,6 +1083,76 @@ void TGNTrainer::step_host(const spd_edge* const* events, const std::uint16_t* c
     }
     step(loss_out);
     d2h_bytes_ += workers_.size() * sizeof(float);
+}
+
+// Pipelined end-to-end step: the same inputs and outputs as step_host, but
+// host staging of this batch overlaps the device's previous step. Events are
+// scattered into a ring of pinned SoA slots (the host waits only for the copy
+// issued kStageSlots steps ago), copied on the copy stream together with the
+// caller's pinned feature rows; the step's graph waits on that copy. The
+// per-worker losses are copied into the caller's pinned loss_pinned without a
+// host wait (NaN for idle workers is the caller's to apply); sync() waits.
+void TGNTrainer::step_host_async(const spd_edge* const* events, const std::uint16_t* const* feats,
+                                 float* loss_pinned) {
+    DeviceGuard g(device_);
+    if (step_in_epoch_ >= epoch_steps_) {
+        end_epoch();
+        begin_epoch(epoch_ + 1);
+    }
+    if (!copy_) {
+        SPD_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+        for (auto& e : aring_ev_) SPD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const std::size_t need = workers_.size() * cfg_.batch_size * 16;
+    if (aring_bytes_ < need) {
+        SPD_CUDA(cudaDeviceSynchronize());
+        for (auto& p : aring_) {
+            if (p) cudaFreeHost(p);
+            SPD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), need, cudaHostAllocDefault));
+        }
+        aring_bytes_ = need;
+        for (auto& u : aring_used_) u = false;
+    }
+    const int slot = aring_next_;
+    aring_next_ = (aring_next_ + 1) % kStageSlots;
+    if (aring_used_[slot]) SPD_CUDA(cudaEventSynchronize(aring_ev_[slot]));
+    const int Fp = s_->d.Fp;
+    for (std::size_t k = 0; k < workers_.size(); ++k) {
+        Worker& w = *workers_[k];
+        if (w.batches == 0) continue;
+        const std::uint64_t lo = w.pos * cfg_.batch_size;
+        const std::uint64_t B = std::min<std::uint64_t>(w.E, lo + cfg_.batch_size) - lo;
+        std::uint32_t* hs = reinterpret_cast<std::uint32_t*>(aring_[slot] + k * cfg_.batch_size * 16);
+        std::uint32_t* hd = hs + B;
+        double* ht = reinterpret_cast<double*>(hd + B);
+        const spd_edge* e = events[k];
+        for (std::uint64_t i = 0; i < B; ++i) {
+            hs[i] = e[i].src;
+            hd[i] = e[i].dst;
+            ht[i] = e[i].ts;
+        }
+        SPD_CUDA(cudaMemcpyAsync(w.ev_src.p + lo, hs, B * 4, cudaMemcpyHostToDevice, copy_));
+        SPD_CUDA(cudaMemcpyAsync(w.ev_dst.p + lo, hd, B * 4, cudaMemcpyHostToDevice, copy_));
+        SPD_CUDA(cudaMemcpyAsync(w.ev_ts.p + lo, ht, B * 8, cudaMemcpyHostToDevice, copy_));
+        if (Fp && feats && feats[k])
+            SPD_CUDA(cudaMemcpyAsync(w.feat.p + lo * Fp, feats[k], B * Fp * 2,
+                                     cudaMemcpyHostToDevice, copy_));
+        h2d_bytes_ += B * 16 + (Fp ? B * Fp * 2 : 0);
+    }
+    SPD_CUDA(cudaEventRecord(aring_ev_[slot], copy_));
+    aring_used_[slot] = true;
+    SPD_CUDA(cudaStreamWaitEvent(stream_, aring_ev_[slot], 0));
+    step(nullptr);
+    if (loss_pinned)
+        SPD_CUDA(cudaMemcpyAsync(loss_pinned, s_->loss.p, workers_.size() * sizeof(float),
+                                 cudaMemcpyDeviceToHost, stream_));
+    d2h_bytes_ += workers_.size() * sizeof(float);
+}
+
+void TGNTrainer::sync() {
+    DeviceGuard g(device_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+    if (copy_) SPD_CUDA(cudaStreamSynchronize(copy_));
 }
 
 void TGNTrainer::worker_post(Worker& w) {

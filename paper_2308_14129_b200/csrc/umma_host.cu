@@ -90,11 +90,6 @@ void reduce(const float* ws, int split, int M, int N, int ldws, float* C, int ld
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    static std::once_flag once;  // max shared carveout (see tgn_trainer.cu launch)
-    std::call_once(once, [] {
-        SPD_CUDA(cudaFuncSetAttribute(k_splitk_reduce, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      int(cudaSharedmemCarveoutMaxShared)));
-    });
     SPD_CUDA(cudaLaunchKernelEx(&cfg, k_splitk_reduce, ws, split, M, N, ldws, C, ldc,
                                 static_cast<long long>(bt.c), bt.n));
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
@@ -108,8 +103,6 @@ void run(const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
     static std::once_flag once;
     std::call_once(once, [&] {
         SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
-        SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      int(cudaSharedmemCarveoutMaxShared)));
     });
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;

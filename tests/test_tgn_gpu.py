@@ -274,3 +274,51 @@ def test_shuffle_combine_rebind_matches_oracle():
     with pytest.raises(sp.DataError) as ei:
         tr.rebind(subs[:1])
     assert ei.value.code == "ConfigMismatch"
+
+
+def test_host_fed_steps_match_resident_steps():
+    """End-to-end API (spd_tgn_step_host and its pipelined form
+    spd_tgn_step_host_async + spd_tgn_sync): the same batches fed from host
+    memory train like the device-resident stream (FP32 trajectory bar)."""
+    import torch
+    _, _, pa, subs = partitioned(parts=1)
+    cfg = small_cfg()
+    runs = {}
+    for mode in ("resident", "host", "async"):
+        tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+        tr.begin_epoch(0)
+        ev_all = tr.worker_events(0)
+        Fp = tr.next_batch(0)[2]
+        n = min(8, tr.epoch_steps())
+        losses = []
+        loss_pin = torch.empty(n, dtype=torch.float32, pin_memory=True).numpy()
+        keep = []
+        for k in range(n):
+            lo, hi, _ = tr.next_batch(0)
+            if mode == "resident":
+                losses.append(float(tr.step()[0]))
+                continue
+            ev = torch.empty((hi - lo) * 16, dtype=torch.uint8, pin_memory=True).numpy().view(sp.EDGE_DTYPE)
+            ev[:] = ev_all[lo:hi]
+            ft = torch.empty((hi - lo) * Fp, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16)
+            ft = sp.edge_features_bf16(cfg.seed_feat, subs[0].eids[lo:hi], cfg.d_edge, Fp,
+                                       out=ft.reshape(hi - lo, Fp))
+            keep.append((ev, ft))
+            if mode == "host":
+                losses.append(float(tr.step_host([ev], [ft])[0]))
+            else:
+                tr.step_host_async([ev], [ft], loss_pin[k:k + 1])
+        if mode == "async":
+            tr.sync()
+            losses = loss_pin.tolist()
+        h2d, d2h = tr.io_bytes()
+        if mode != "resident":
+            assert h2d > 0 and d2h == 4 * n
+        runs[mode] = (np.array(losses), tr.params())
+        tr.close()
+    ref_l, ref_p = runs["resident"]
+    for mode in ("host", "async"):
+        l, p = runs[mode]
+        assert np.all(np.isfinite(l))
+        assert np.max(np.abs(l - ref_l)) <= TOL_TRAJ * max(1.0, float(np.max(np.abs(ref_l)))), (mode, l, ref_l)
+        assert rel_err(p, ref_p) < TOL_TRAJ, mode
