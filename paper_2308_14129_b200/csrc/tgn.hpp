@@ -200,6 +200,7 @@ private:
     cudaStream_t zs_ = nullptr;
     cudaEvent_t ev_zfork_ = nullptr, ev_zero_ = nullptr;
     cudaEvent_t ev_bwdx_ = nullptr;  // attention input-gradient scatter done
+    bool scratch_zeroed_ = false;    // dH/dGi/dGh cleared by this step's k_zero_list
 
     spd_tgn_config cfg_;
     ParamLayout lay_;

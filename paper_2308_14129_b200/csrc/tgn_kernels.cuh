@@ -59,6 +59,14 @@ struct WorkerDev {
 // --- kernels (definitions in tgn_kernels.cu) -------------------------------
 __global__ void k_init_aug(float* buf, int rows, int cols, int ld);
 __global__ void k_zero2(float* a, std::size_t na, double* b, std::size_t nb);
+struct ZeroList {
+    static constexpr int kMax = 4;
+    float* p[kMax];
+    std::size_t n[kMax];
+    double* d;
+    std::size_t nd;
+};
+__global__ void k_zero_list(ZeroList z);
 __global__ void k_roots_nbrs(WorkerDev w, int B, int K,
                              std::uint32_t* roots, double* root_t, std::uint32_t* nbr_node,
                              std::uint32_t* nbr_ev, double* nbr_dt, int* cnt);

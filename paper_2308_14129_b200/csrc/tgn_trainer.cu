@@ -804,12 +804,20 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         side([&](cudaStream_t sd) { launch(tgnk::k_pending, 1, 1024, 0, sd, wd, B); });
     // (the side-stream branch is forked after the GRU's first kernel is
     // enqueued: graph replays submit independent branches in creation order)
+    // SPD_PHI_LATE=1 (experiment): the time encoding forks after the query
+    // GEMM instead of right after the neighbour search
+    static const bool phi_late = [] {
+        const char* e = std::getenv("SPD_PHI_LATE");
+        return e && *e == '1';
+    }();
     auto fork_roots = [&] {
         side([&](cudaStream_t sd) {
             roots(sd);
             SPD_CUDA(cudaEventRecord(ev_roots_, sd));
-            phi(sd);
-            SPD_CUDA(cudaEventRecord(ev_phi_, sd));
+            if (!phi_late) {
+                phi(sd);
+                SPD_CUDA(cudaEventRecord(ev_phi_, sd));
+            }
         }, 0);
     };
     static const bool roots_early = [] {
@@ -832,6 +840,11 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
                  d.DQ + 1, nullptr, st, 0, nullptr, 0, tc);
     });
+    if (!profile_ && phi_late)  // after the neighbour search (query_gather waited on it)
+        side([&](cudaStream_t sd) {
+            phi(sd);
+            SPD_CUDA(cudaEventRecord(ev_phi_, sd));
+        });
     // attention with absorbed key/value projections (tgn_attn.cu):
     //   Qp_h = Q_h [W_K,h | b_K,h]; kernel -> alpha, xbar_h; ctx_h = xbar_h [W_V,h | b_V,h]^T
     const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
@@ -894,6 +907,10 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     const bool tc = cfg_.gemm_mode == 1;
     const float* PW = tc ? params_tc_.p : params_.p;
     SPD_CUDA(cudaStreamWaitEvent(st, ev_zero_, 0));  // gradients cleared (step_body)
+    // dH / dGi / dGh: cleared at step start for the step's first backward;
+    // later local workers reuse the scratch and clear it themselves
+    const bool fresh = scratch_zeroed_;
+    scratch_zeroed_ = false;
     timed("head_bwd", [&] {
         side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
                    2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
@@ -926,7 +943,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     const int ldw = lay_.att_kv.ld;
     float* GK = G + lay_.att_kv.off;
     float* GV = GK + std::size_t(d.DQ) * ldw;
-    s.dH.zero(st);
+    if (!fresh) s.dH.zero(st);
     const std::ptrdiff_t wst = std::ptrdiff_t(dh) * ldw;  // per-head weight slab
     timed("gemm_dxbar", [&] {
         // dW_V,h += dctx_h^T xbar_h ; dxbar_h = dctx_h [W_V,h | b_V,h]
@@ -943,23 +960,40 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     });
     // the input-gradient scatter (dH of neighbours, time-encoder partials)
     // runs beside the dQ GEMMs; gru_bwd and the time-grad reduction wait for it
-    if (profile_) {
-        timed("attn_bwd_x", [&] { attn_abs_bwd_x(wd, d, R, s, attn_part, st); });
-    } else {
-        side([&](cudaStream_t sd) {
-            attn_abs_bwd_x(wd, d, R, s, attn_part, sd);
-            SPD_CUDA(cudaEventRecord(ev_bwdx_, sd));
-        });
-    }
-    timed("gemm_dq", [&] {
-        // dW_K,h += Q_h^T dQp_h ; dQ_h = dQp_h [W_K,h | b_K,h]^T
+    // SPD_BWDX_LATE=1 (experiment): fork the scatter and the dW_K GEMM after
+    // the dQ GEMM, so its CTAs claim the SMs first
+    static const bool late = [] {
+        const char* e = std::getenv("SPD_BWDX_LATE");
+        return e && *e == '1';
+    }();
+    auto fork_x = [&] {
+        if (profile_) {
+            timed("attn_bwd_x", [&] { attn_abs_bwd_x(wd, d, R, s, attn_part, st); });
+        } else {
+            side([&](cudaStream_t sd) {
+                attn_abs_bwd_x(wd, d, R, s, attn_part, sd);
+                SPD_CUDA(cudaEventRecord(ev_bwdx_, sd));
+            });
+        }
+    };
+    auto fork_wk = [&] {
+        // dW_K,h += Q_h^T dQp_h
         side([&](cudaStream_t sd) {
             proj_wgrad(tc, s.Q.p, d.ld_Q, s.dQp.p, ldhp, GK, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
                        s.ws.n, sd, umma::Batch{d.H, dh, d.ld_p, wst});
         });
+    };
+    if (!late) fork_x();
+    timed("gemm_dq", [&] {
+        // dQ_h = dQp_h [W_K,h | b_K,h]^T
+        if (!late) fork_wk();
         proj_fwd(tc, s.dQp.p, ldhp, WK, ldw, s.dQ.p, d.ld_Q, R, dh, d.DK + 1, nullptr, st, 0, nullptr,
                  0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
     });
+    if (late) {
+        fork_x();
+        fork_wk();
+    }
     timed("q_bwd", [&] {
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
                    d.DQ + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
@@ -977,7 +1011,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         });
     });
     timed("gru_bwd", [&] {
-        if (tc) {  // the TC weight-grad reads whole K blocks: rows >= |pending| must be 0
+        if (tc && !fresh) {  // the TC weight-grad reads whole K blocks: rows >= |pending| must be 0
             s.dGi.zero(st);
             s.dGh.zero(st);
         }
@@ -1222,8 +1256,21 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
     // writes the gradients before the backward, which joins it).
     SPD_CUDA(cudaEventRecord(ev_zfork_, stream_));
     SPD_CUDA(cudaStreamWaitEvent(zs_, ev_zfork_, 0));
-    launch(tgnk::k_zero2, blocks_for(lay_.total), 256, 0, zs_, grads_.p, lay_.total, tgrad_.p,
-           std::size_t(2) * ld4(lay_.T));
+    {
+        Scratch& s = *s_;
+        tgnk::ZeroList z{};
+        z.p[0] = grads_.p; z.n[0] = lay_.total;
+        z.p[1] = s.dH.p; z.n[1] = s.dH.n;
+        if (cfg_.gemm_mode == 1) {  // TC weight grads read whole K blocks of dGi/dGh
+            z.p[2] = s.dGi.p; z.n[2] = s.dGi.n;
+            z.p[3] = s.dGh.p; z.n[3] = s.dGh.n;
+        }
+        z.d = tgrad_.p; z.nd = std::size_t(2) * ld4(lay_.T);
+        std::size_t mx = z.nd;
+        for (int k = 0; k < tgnk::ZeroList::kMax; ++k) mx = std::max(mx, z.n[k]);
+        launch(tgnk::k_zero_list, blocks_for(mx), 256, 0, zs_, z);
+        scratch_zeroed_ = true;  // the first backward of this step skips its own zeroing
+    }
     SPD_CUDA(cudaEventRecord(ev_zero_, zs_));
     std::size_t last = workers_.size();
     for (std::size_t k = 0; k < workers_.size(); ++k)
