@@ -804,20 +804,12 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         side([&](cudaStream_t sd) { launch(tgnk::k_pending, 1, 1024, 0, sd, wd, B); });
     // (the side-stream branch is forked after the GRU's first kernel is
     // enqueued: graph replays submit independent branches in creation order)
-    // SPD_PHI_LATE=1 (experiment): the time encoding forks after the query
-    // GEMM instead of right after the neighbour search
-    static const bool phi_late = [] {
-        const char* e = std::getenv("SPD_PHI_LATE");
-        return e && *e == '1';
-    }();
     auto fork_roots = [&] {
         side([&](cudaStream_t sd) {
             roots(sd);
             SPD_CUDA(cudaEventRecord(ev_roots_, sd));
-            if (!phi_late) {
-                phi(sd);
-                SPD_CUDA(cudaEventRecord(ev_phi_, sd));
-            }
+            phi(sd);
+            SPD_CUDA(cudaEventRecord(ev_phi_, sd));
         }, 0);
     };
     static const bool roots_early = [] {
@@ -840,11 +832,6 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
                  d.DQ + 1, nullptr, st, 0, nullptr, 0, tc);
     });
-    if (!profile_ && phi_late)  // after the neighbour search (query_gather waited on it)
-        side([&](cudaStream_t sd) {
-            phi(sd);
-            SPD_CUDA(cudaEventRecord(ev_phi_, sd));
-        });
     // attention with absorbed key/value projections (tgn_attn.cu):
     //   Qp_h = Q_h [W_K,h | b_K,h]; kernel -> alpha, xbar_h; ctx_h = xbar_h [W_V,h | b_V,h]^T
     const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
@@ -960,12 +947,6 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     });
     // the input-gradient scatter (dH of neighbours, time-encoder partials)
     // runs beside the dQ GEMMs; gru_bwd and the time-grad reduction wait for it
-    // SPD_BWDX_LATE=1 (experiment): fork the scatter and the dW_K GEMM after
-    // the dQ GEMM, so its CTAs claim the SMs first
-    static const bool late = [] {
-        const char* e = std::getenv("SPD_BWDX_LATE");
-        return e && *e == '1';
-    }();
     auto fork_x = [&] {
         if (profile_) {
             timed("attn_bwd_x", [&] { attn_abs_bwd_x(wd, d, R, s, attn_part, st); });
@@ -983,17 +964,13 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
                        s.ws.n, sd, umma::Batch{d.H, dh, d.ld_p, wst});
         });
     };
-    if (!late) fork_x();
+    fork_x();
     timed("gemm_dq", [&] {
         // dQ_h = dQp_h [W_K,h | b_K,h]^T
-        if (!late) fork_wk();
+        fork_wk();
         proj_fwd(tc, s.dQp.p, ldhp, WK, ldw, s.dQ.p, d.ld_Q, R, dh, d.DK + 1, nullptr, st, 0, nullptr,
                  0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
     });
-    if (late) {
-        fork_x();
-        fork_wk();
-    }
     timed("q_bwd", [&] {
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
                    d.DQ + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
