@@ -224,6 +224,42 @@ __global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, floa
     for (int c = lane; c < d.D; c += 32) dx[c] = x[c] > 0.f ? g * w2[c] : 0.f;
 }
 
+// Decoder layer 1 without the gathered [z_u | z_v] rows: the src half of the
+// weight is applied once per event (Ya = z_src W_a^T), the other half to the
+// dst and negative embeddings (Yb = z_{dst|neg} W_b^T), so
+//   D1_pos[i] = relu(Ya[i] + Yb[i] + b1),  D1_neg[i] = relu(Ya[i] + Yb[B+i] + b1)
+// (the MergeLayer's W [z_u | z_v] + b split by columns), then the head as
+// k_dec_head. W1 = augmented dec1 rows [w(2D) | b], row stride ld1.
+__global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, const float* W1,
+                            int ld1, const float* w2, float* D1, float* dlogit, float* lossv,
+                            float* dD1, float* logits) {
+    pdl_entry();
+    const int p = warp_id_global(), lane = lane_id();
+    if (p >= 2 * B) return;
+    const int i = p < B ? p : p - B;
+    const float* a = Ya + (std::size_t)i * d.D;
+    const float* b = Yb + (std::size_t)p * d.D;  // dst rows [0, B), negative rows [B, 2B)
+    float* x = D1 + (std::size_t)p * d.ld_d1;
+    float acc = 0.f;
+    for (int c = lane; c < d.D; c += 32) {
+        const float z = fmaxf(a[c] + b[c] + W1[(std::size_t)c * ld1 + 2 * d.D], 0.f);
+        x[c] = z;
+        acc += z * w2[c];
+    }
+    acc = warp_sum(acc) + w2[d.D];
+    const bool pos = p < B;
+    const float sig = sigmoidf_(acc);
+    const float g = (sig - (pos ? 1.f : 0.f)) / (float)B;
+    if (lane == 0) {
+        dlogit[(std::size_t)p * 4] = g;
+        lossv[p] = (pos ? softplusf(-acc) : softplusf(acc)) / (float)B;
+        if (logits) logits[p] = acc;
+    }
+    __syncwarp();
+    float* dx = dD1 + (std::size_t)p * d.D;
+    for (int c = lane; c < d.D; c += 32) dx[c] = x[c] > 0.f ? g * w2[c] : 0.f;
+}
+
 // Fixed-order single-block sum (deterministic loss).
 __global__ void k_sum_loss(const float* lossv, int n, float* out) {
     pdl_entry();

@@ -107,6 +107,9 @@ __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* 
 __global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in);
 __global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, float* dlogit,
                            float* lossv, float* dD1, float* logits);
+__global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, const float* W1,
+                            int ld1, const float* w2, float* D1, float* dlogit, float* lossv,
+                            float* dD1, float* logits);
 __global__ void k_sum_loss(const float* lossv, int n, float* out);
 __global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb);
 __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt);

@@ -104,6 +104,7 @@ struct Scratch {
     DevBuf<double> root_t, nbr_dt;
     DevBuf<int> cnt;
     DevBuf<float> x_gru, h_gru, Gi, Gh, gsave, mem_new, dH, dGi, dGh;
+    DevBuf<float> Ya, Yb;  // decoder layer-1 halves (k_dec_head2)
     DevBuf<float> q_in, Q, Qp, xbar, alpha, dsc, ctx, O, m_in, Z1, emb, d_in, D1, logits, lossv, dlogit;
     DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dxbar, dQp, dQ, dq_in;
     DevBuf<float> ws;
@@ -457,6 +458,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.m_in.alloc(std::size_t(R) * d.ld_m); init_aug(s.m_in, R, d.DQ + D, d.ld_m, stream_);
     s.Z1.alloc(std::size_t(R) * d.ld_z); init_aug(s.Z1, R, D, d.ld_z, stream_);
     s.emb.alloc(std::size_t(R) * D);
+    s.Ya.alloc(std::size_t(B) * D); s.Yb.alloc(std::size_t(2 * B) * D);
     s.d_in.alloc(std::size_t(2 * B) * d.ld_din); init_aug(s.d_in, 2 * B, 2 * D, d.ld_din, stream_);
     s.D1.alloc(std::size_t(2 * B) * d.ld_d1); init_aug(s.D1, 2 * B, D, d.ld_d1, stream_);
     s.logits.alloc(2 * B); s.lossv.alloc(2 * B);
@@ -858,12 +860,19 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
                  d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU, nullptr, 0, tc);
         proj_fwd(tc, s.Z1.p, d.ld_z, PW + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
                  nullptr, st);
-        launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, d, B, s.emb.p,
-                                                                                 s.d_in.p);
-        gemm_fwd(s.d_in.p, d.ld_din, P + lay_.dec1.off, lay_.dec1.ld, s.D1.p, d.ld_d1, 2 * B, d.D,
-                 2 * d.D + 1, nullptr, st, gemm::EPI_RELU);
-        launch(tgnk::k_dec_head, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, 
-            d, B, s.D1.p, P + lay_.dec2.off, s.dlogit.p, s.lossv.p, s.dD1.p, s.logits.p);
+        // decoder layer 1 split by input halves (k_dec_head2): the src half on
+        // the aux stream, the dst/negative half on the main stream
+        const float* W1 = P + lay_.dec1.off;
+        SPD_CUDA(cudaEventRecord(ev_aux_fork_, st));
+        SPD_CUDA(cudaStreamWaitEvent(aux_, ev_aux_fork_, 0));
+        gemm_fwd(s.emb.p, d.D, W1, lay_.dec1.ld, s.Ya.p, d.D, B, d.D, d.D, nullptr, aux_);
+        gemm_fwd(s.emb.p + std::size_t(B) * d.D, d.D, W1 + d.D, lay_.dec1.ld, s.Yb.p, d.D, 2 * B, d.D,
+                 d.D, nullptr, st);
+        SPD_CUDA(cudaEventRecord(ev_aux_join_, aux_));
+        SPD_CUDA(cudaStreamWaitEvent(st, ev_aux_join_, 0));
+        launch(tgnk::k_dec_head2, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, d, B,
+               static_cast<const float*>(s.Ya.p), static_cast<const float*>(s.Yb.p), W1,
+               lay_.dec1.ld, P + lay_.dec2.off, s.D1.p, s.dlogit.p, s.lossv.p, s.dD1.p, s.logits.p);
     });
     // the batch loss is only read by the host after the step: off the critical path
     auto sum_loss = [&](cudaStream_t sx) {
@@ -901,7 +910,11 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     timed("head_bwd", [&] {
         side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
                    2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
-        side([&](cudaStream_t sd) { gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
+        side([&](cudaStream_t sd) {
+            // the gathered decoder input [z_u | z_v | 1] is only needed here
+            launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, sd, d, B,
+                   s.emb.p, s.d_in.p);
+            gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
                    2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
         gemm_dgrad(s.dD1.p, d.D, P + lay_.dec1.off, lay_.dec1.ld, s.dd_in.p, d.ld_din, 2 * B,
                    2 * d.D, d.D, nullptr, st);
