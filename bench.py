@@ -283,6 +283,15 @@ def main():
     tr = sp.TGNTrainer(cfg, wl["subs"], workers=[rank], shared=wl["shared"], node_count=N,
                        rank=rank, world=world, nccl_id=nccl_id, device=local)
     log(f"trainer ready: {time.time() - t0:.1f}s, params={tr.n_params}, epoch_steps={tr.epoch_steps()}")
+    # per-GPU device memory held after the trainer is built (events, CSR,
+    # feature rows, memory, parameters, scratch): SURVEY §8 ML25M footprint
+    mem_gb = None
+    try:
+        import torch
+        free_b, total_b = torch.cuda.mem_get_info(local)
+        mem_gb = {"used_gb": round((total_b - free_b) / 1e9, 2), "total_gb": round(total_b / 1e9, 2)}
+    except Exception:
+        pass
     tr.begin_epoch(0)
     # steady state: time steps from the middle of the epoch (full recent-k
     # neighbour lists), not the epoch's sparse first batches
@@ -412,6 +421,7 @@ def main():
             "config": cfg_desc, "e2e": e2e, "roofline": roof, "step_roofline": step_roof,
             "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk.summary(),
             "effective_edges_per_s": wl["train_edges"] / (tr.epoch_steps() * ms_per_step / 1e3),
+            "device_memory_per_gpu": mem_gb,
             "epoch_steps": tr.epoch_steps(), "train_edges": wl["train_edges"],
             "phases_ms": {n: round(t, 4) for n, t in phases},
         }
