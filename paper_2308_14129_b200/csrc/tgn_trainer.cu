@@ -374,6 +374,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     if (world < 1 || rank < 0 || rank >= world) data_error("InvalidParams", "bad rank/world");
     require_device(device);
     DeviceGuard g(device);
+    pdl_auto() = cfg.batch_size <= 512;  // launch-latency-bound steps (pdl.cuh)
     // the main stream carries the step's critical path: highest priority, so
     // its CTAs are scheduled ahead of the side streams' (weight gradients,
     // neighbour search, time encoding) whenever both have work queued

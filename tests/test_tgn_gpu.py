@@ -231,8 +231,13 @@ def test_graph_replay_matches_eager(gemm_mode):
         losses = [tr.run_epoch(ep) for ep in range(2)]
         out.append((np.array(losses), tr.params(), tr.memory(0)[0], tr.memory(1)[1]))
     (l0, p0, m0, u0), (l1, p1, m1, u1) = out
+    # two runs differ only by float-atomic ordering; in TF32 mode the tf32
+    # rounding of intermediate activations turns that into ~3e-3 of drift
+    # over 2 epochs, so each mode gets its own trajectory bar (a replay bug —
+    # wrong batch, stale control words — moves everything by O(1))
+    tol = TOL_TRAJ if gemm_mode == 0 else TOL_TF32
     assert np.allclose(l0, l1, rtol=1e-3), (l0, l1)
-    assert rel_err(p1, p0) < TOL_TRAJ and rel_err(m1, m0) < TOL_TRAJ
+    assert rel_err(p1, p0) < tol and rel_err(m1, m0) < tol, (rel_err(p1, p0), rel_err(m1, m0))
     assert np.array_equal(u0, u1)
 
 
