@@ -36,13 +36,20 @@ __global__ void k_init_aug(float* buf, int rows, int cols, int ld) {
 // Step-start zeroing of the gradient buffers and the backward's accumulation
 // scratch (dH, and the GRU gate gradients whose unused rows the tensor-core
 // weight-gradient GEMM reads), one launch beside the forward.
+// Grid-stride over a small grid: a full-size grid would fill every SM for
+// its few microseconds and hold the step's first critical-path kernels back.
 __global__ void k_zero_list(ZeroList z) {
     pdl_entry();
-    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    std::size_t mx = z.nd;
 #pragma unroll
-    for (int k = 0; k < ZeroList::kMax; ++k)
-        if (i < z.n[k]) z.p[k][i] = 0.f;
-    if (i < z.nd) z.d[i] = 0.0;
+    for (int k = 0; k < ZeroList::kMax; ++k) mx = z.n[k] > mx ? z.n[k] : mx;
+    for (std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x; i < mx;
+         i += (std::size_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < ZeroList::kMax; ++k)
+            if (i < z.n[k]) z.p[k][i] = 0.f;
+        if (i < z.nd) z.d[i] = 0.0;
+    }
 }
 
 __global__ void k_zero2(float* a, std::size_t na, double* b, std::size_t nb) {

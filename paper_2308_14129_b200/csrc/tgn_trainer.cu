@@ -1259,7 +1259,7 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
         z.d = tgrad_.p; z.nd = std::size_t(2) * ld4(lay_.T);
         std::size_t mx = z.nd;
         for (int k = 0; k < tgnk::ZeroList::kMax; ++k) mx = std::max(mx, z.n[k]);
-        launch(tgnk::k_zero_list, blocks_for(mx), 256, 0, zs_, z);
+        launch(tgnk::k_zero_list, std::min<unsigned>(blocks_for(mx), 148), 256, 0, zs_, z);
         scratch_zeroed_ = true;  // the first backward of this step skips its own zeroing
     }
     SPD_CUDA(cudaEventRecord(ev_zero_, zs_));
