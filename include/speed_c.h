@@ -276,7 +276,7 @@ typedef struct spd_tgn_config {
     uint64_t seed_feat;  /* synthetic edge features */
     uint64_t seed_neg;   /* negative sampling */
     int32_t sync_average;/* epoch-end shared-node sync: 1 average (default), 0 max-ts */
-    int32_t gemm_mode;   /* 0 = FP32 FFMA, 1 = tcgen05 BF16 (tolerance-gated) */
+    int32_t gemm_mode;   /* 0 = FP32 FFMA, 1 = tcgen05 TF32 for the GRU and attention projections (tolerance-gated) */
 } spd_tgn_config;
 
 typedef struct spd_tgn_trainer spd_tgn_trainer;

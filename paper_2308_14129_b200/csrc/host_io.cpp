@@ -351,6 +351,19 @@ spd_status spd_write_edges_bin(const char* path, const spd_edge* e, uint64_t n, 
                                double t_max) {
     GUARD({
         if (!path || (n && !e)) usage_error("null argument");
+        // the reader's acceptance rules, checked before anything is written, so
+        // every file this writes reads back (ids < node_count, finite ts >= 0,
+        // time-ordered)
+        double prev = 0.0;
+        for (std::uint64_t q = 0; q < n; ++q) {
+            if (e[q].src >= node_count || e[q].dst >= node_count)
+                data_error("InvalidParams", "edge " + std::to_string(q) + ": node id out of range");
+            if (!std::isfinite(e[q].ts) || e[q].ts < 0.0)
+                data_error("ParseError", "edge " + std::to_string(q) + ": timestamp is negative or not finite");
+            if (e[q].ts < prev)
+                data_error("UnsortedStream", "edge " + std::to_string(q) + ": timestamp decreases");
+            prev = e[q].ts;
+        }
         File f{std::fopen(path, "wb")};
         if (!f.f) data_error("FileNotFound", std::string("cannot open '") + path + "' for writing");
         BinHeader h{};
@@ -399,6 +412,8 @@ spd_status spd_load_edges_bin(const char* path, spd_edge* out, uint64_t cap) {
             for (std::uint64_t q = k; q < k + m; ++q) {
                 if (out[q].src >= h.node_count || out[q].dst >= h.node_count)
                     data_error("ParseError", "edge " + std::to_string(q) + ": node id out of range");
+                if (!std::isfinite(out[q].ts) || out[q].ts < 0.0)  // parse_ts's rule (graph_io.cpp)
+                    data_error("ParseError", "edge " + std::to_string(q) + ": timestamp is negative or not finite");
                 if (!(out[q].ts >= prev))
                     data_error("UnsortedStream", "edge " + std::to_string(q) + ": timestamp decreases");
                 prev = out[q].ts;

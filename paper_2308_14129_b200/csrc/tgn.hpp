@@ -245,6 +245,12 @@ private:
     bool aring_used_[kStageSlots] = {};
     int aring_next_ = 0;
     cudaStream_t copy_ = nullptr;
+    // the steps those copies fed: end-of-step event and each worker's window,
+    // so a copy never overwrites a window an in-flight step still reads
+    cudaEvent_t astep_ev_[kStageSlots] = {};
+    std::vector<std::uint64_t> astep_lo_[kStageSlots];
+    void check_host_events(const Worker& w, std::uint64_t lo, std::uint64_t B,
+                           const spd_edge* e) const;
     std::uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
     std::uint64_t feat_seed_mixed_ = 0;
 };

@@ -12,6 +12,7 @@
 #include <mutex>
 #include <cstdlib>
 #include <atomic>
+#include <cfloat>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -530,6 +531,8 @@ TGNTrainer::~TGNTrainer() {
         if (p) cudaFreeHost(p);
     for (auto& e : aring_ev_)
         if (e) cudaEventDestroy(e);
+    for (auto& e : astep_ev_)
+        if (e) cudaEventDestroy(e);
     if (copy_) cudaStreamDestroy(copy_);
     if (zs_) cudaStreamDestroy(zs_);
     if (nccl_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_));
@@ -949,8 +952,8 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     timed("gemm_dxbar", [&] {
         // dW_V,h += dctx_h^T xbar_h ; dxbar_h = dctx_h [W_V,h | b_V,h]
         side([&](cudaStream_t sd) {
-            proj_wgrad(tc, s.dctx.p, d.ld_Q, s.xbar.p, ldhp, GV, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
-                       s.ws.n, sd, umma::Batch{d.H, dh, d.ld_p, wst});
+            proj_wgrad(tc, s.dctx.p, d.ld_Q, s.xbar.p, ldhp, GV, ldw, dh, d.DK + 1, R, nullptr, ws_cur_,
+                       wsn_cur_, sd, umma::Batch{d.H, dh, d.ld_p, wst});
         });
         proj_dgrad(tc, s.dctx.p, d.ld_Q, WV, ldw, s.dxbar.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0,
                    nullptr, 0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
@@ -974,8 +977,8 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     auto fork_wk = [&] {
         // dW_K,h += Q_h^T dQp_h
         side([&](cudaStream_t sd) {
-            proj_wgrad(tc, s.Q.p, d.ld_Q, s.dQp.p, ldhp, GK, ldw, dh, d.DK + 1, R, nullptr, s.ws.p,
-                       s.ws.n, sd, umma::Batch{d.H, dh, d.ld_p, wst});
+            proj_wgrad(tc, s.Q.p, d.ld_Q, s.dQp.p, ldhp, GK, ldw, dh, d.DK + 1, R, nullptr, ws_cur_,
+                       wsn_cur_, sd, umma::Batch{d.H, dh, d.ld_p, wst});
         });
     };
     fork_x();
@@ -1090,6 +1093,7 @@ void TGNTrainer::step_host(const spd_edge* const* events, const std::uint16_t* c
         }
         SPD_CUDA(cudaStreamSynchronize(stream_));  // staging reuse across workers/steps
         const spd_edge* e = events[k];
+        check_host_events(w, lo, B, e);
         std::uint32_t* hs = reinterpret_cast<std::uint32_t*>(stage_);
         std::uint32_t* hd = hs + B;
         double* ht = reinterpret_cast<double*>(hd + B);
@@ -1127,6 +1131,7 @@ void TGNTrainer::step_host_async(const spd_edge* const* events, const std::uint1
     if (!copy_) {
         SPD_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
         for (auto& e : aring_ev_) SPD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : astep_ev_) SPD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     const std::size_t need = workers_.size() * cfg_.batch_size * 16;
     if (aring_bytes_ < need) {
@@ -1151,11 +1156,17 @@ void TGNTrainer::step_host_async(const spd_edge* const* events, const std::uint1
         std::uint32_t* hd = hs + B;
         double* ht = reinterpret_cast<double*>(hd + B);
         const spd_edge* e = events[k];
+        check_host_events(w, lo, B, e);
         for (std::uint64_t i = 0; i < B; ++i) {
             hs[i] = e[i].src;
             hd[i] = e[i].dst;
             ht[i] = e[i].ts;
         }
+        // an earlier step still in flight may read this very window (a worker
+        // with one or two batches per loop): the copy waits for that step
+        for (int j = 0; j < kStageSlots; ++j)
+            if (j != slot && k < astep_lo_[j].size() && astep_lo_[j][k] == lo)
+                SPD_CUDA(cudaStreamWaitEvent(copy_, astep_ev_[j], 0));
         SPD_CUDA(cudaMemcpyAsync(w.ev_src.p + lo, hs, B * 4, cudaMemcpyHostToDevice, copy_));
         SPD_CUDA(cudaMemcpyAsync(w.ev_dst.p + lo, hd, B * 4, cudaMemcpyHostToDevice, copy_));
         SPD_CUDA(cudaMemcpyAsync(w.ev_ts.p + lo, ht, B * 8, cudaMemcpyHostToDevice, copy_));
@@ -1167,11 +1178,27 @@ void TGNTrainer::step_host_async(const spd_edge* const* events, const std::uint1
     SPD_CUDA(cudaEventRecord(aring_ev_[slot], copy_));
     aring_used_[slot] = true;
     SPD_CUDA(cudaStreamWaitEvent(stream_, aring_ev_[slot], 0));
+    astep_lo_[slot].assign(workers_.size(), ~std::uint64_t(0));
+    for (std::size_t k = 0; k < workers_.size(); ++k)
+        if (workers_[k]->batches) astep_lo_[slot][k] = workers_[k]->pos * cfg_.batch_size;
     step(nullptr);
+    SPD_CUDA(cudaEventRecord(astep_ev_[slot], stream_));
     if (loss_pinned)
         SPD_CUDA(cudaMemcpyAsync(loss_pinned, s_->loss.p, workers_.size() * sizeof(float),
                                  cudaMemcpyDeviceToHost, stream_));
     d2h_bytes_ += workers_.size() * sizeof(float);
+}
+
+// Host-fed events must be the partition's own stream: the neighbour CSR, the
+// negative pool and the feature rows of the resident stream are built from it
+// at construction, so different events would train on inconsistent state.
+void TGNTrainer::check_host_events(const Worker& w, std::uint64_t lo, std::uint64_t B,
+                                   const spd_edge* e) const {
+    if (!e) usage_error("step_host: missing event batch for worker " + std::to_string(w.gid));
+    if (std::memcmp(e, w.ev_host.data() + lo, B * sizeof(spd_edge)) != 0)
+        data_error("InvalidParams", "host-fed events of worker " + std::to_string(w.gid) +
+                                        " differ from its resident stream at batch start " +
+                                        std::to_string(lo));
 }
 
 void TGNTrainer::sync() {
@@ -1483,6 +1510,19 @@ __global__ void k_sync_pack(const float* mem, const double* lu, const std::uint3
         mx[o] = fmaxf(mx[o], v);
     }
 }
+__global__ void k_sync_fill(float* mn, float* mx, std::size_t n, double* tmin, double* tmax,
+                            int S) {
+    pdl_entry();
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        mn[i] = FLT_MAX;
+        mx[i] = -FLT_MAX;
+    }
+    if (i < (std::size_t)S) {
+        tmin[i] = INFINITY;
+        tmax[i] = -INFINITY;
+    }
+}
 __global__ void k_sync_ts_minmax(const double* lu, const std::uint32_t* rows, int S, int first,
                                  double* tmin, double* tmax) {
     pdl_entry();
@@ -1556,10 +1596,9 @@ void TGNTrainer::sync_shared() {
     }
     // local reduction in worker order (the reference's summation order)
     const bool have_local = !workers_.empty();
-    if (!have_local) {
+    if (!have_local) {  // identities of sum / min / max, so the collectives see only the peers
         sum.zero(st);
-        SPD_CUDA(cudaMemsetAsync(mn.p, 0x7F, mn.bytes(), st));   // +large
-        SPD_CUDA(cudaMemsetAsync(mx.p, 0xFF, mx.bytes(), st));   // NaN-free -large
+        launch(k_sync_fill, blocks_for(mn.n), 256, 0, st, mn.p, mx.p, mn.n, tmin.p, tmax.p, S);
     }
     for (std::size_t k = 0; k < workers_.size(); ++k) {
         Worker& w = *workers_[k];

@@ -168,8 +168,12 @@ def test_binary_rejects_corruption(tmp_path):
     bad_id[32:36] = np.uint32(s.node_count).tobytes()  # first src == node_count
     cases["id"] = (bytes(bad_id), "ParseError")
     unsorted = bytearray(raw)
-    unsorted[32 + 16 + 8: 32 + 32] = np.float64(-1.0).tobytes()  # second ts below the first
+    unsorted[32 + 16 + 8: 32 + 32] = np.float64(0.5).tobytes()  # second ts below the first (1.0)
     cases["order"] = (bytes(unsorted), "UnsortedStream")
+    for name, v in (("negative", -1.0), ("nan", float("nan")), ("inf", float("inf"))):
+        b = bytearray(raw)  # parse_ts's rule (graph_io.cpp:60-72): finite and >= 0
+        b[32 + 8: 32 + 16] = np.float64(v).tobytes()
+        cases[name] = (bytes(b), "ParseError")
     for name, (blob, code) in cases.items():
         q = tmp_path / f"{name}.bin"
         q.write_bytes(blob)
@@ -179,6 +183,24 @@ def test_binary_rejects_corruption(tmp_path):
     with pytest.raises(sp.DataError) as ei:
         sp.load_edges_bin(str(tmp_path / "absent.bin"))
     assert ei.value.code == "FileNotFound"
+
+
+def test_binary_writer_rejects_what_the_reader_rejects(tmp_path):
+    # every file the writer produces reads back: unsorted, negative-time or
+    # out-of-range streams are refused before anything is written
+    s = sp.gen_powerlaw(50, 400, 2.5, 1)
+    for name, mutate, code in (
+            ("order", ("ts", 1, 0.5), "UnsortedStream"),
+            ("negative", ("ts", 0, -2.0), "ParseError"),
+            ("nan", ("ts", 3, float("nan")), "ParseError"),
+            ("id", ("dst", 2, s.node_count), "InvalidParams")):
+        e = s.edges.copy()
+        e[mutate[0]][mutate[1]] = mutate[2]
+        p = tmp_path / f"w_{name}.bin"
+        with pytest.raises(sp.DataError) as ei:
+            sp.write_edges_bin(sp.EdgeStream(e, s.node_count, s.t_max), str(p))
+        assert ei.value.code == code, name
+        assert not p.exists() or p.stat().st_size == 0, name
 
 
 # -------------------------------------------------------- assignment JSON

@@ -327,3 +327,23 @@ def test_host_fed_steps_match_resident_steps():
         assert np.all(np.isfinite(l))
         assert np.max(np.abs(l - ref_l)) <= TOL_TRAJ * max(1.0, float(np.max(np.abs(ref_l)))), (mode, l, ref_l)
         assert rel_err(p, ref_p) < TOL_TRAJ, mode
+
+
+def test_host_fed_events_must_match_resident_stream():
+    """The neighbour CSR, negative pool and feature rows are built from the
+    partition's resident stream: host-fed batches that differ are refused."""
+    _, _, pa, subs = partitioned(parts=1)
+    cfg = small_cfg()
+    tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+    tr.begin_epoch(0)
+    ev_all = tr.worker_events(0)
+    lo, hi, Fp = tr.next_batch(0)
+    ev = np.ascontiguousarray(ev_all[lo:hi]).copy()
+    ev["ts"][3] += 0.25
+    ft = sp.edge_features_bf16(cfg.seed_feat, subs[0].eids[lo:hi], cfg.d_edge, Fp)
+    with pytest.raises(sp.DataError) as ei:
+        tr.step_host([ev], [ft])
+    assert ei.value.code == "InvalidParams"
+    ok = np.ascontiguousarray(ev_all[lo:hi]).copy()
+    assert np.all(np.isfinite(tr.step_host([ok], [ft])))
+    tr.close()
