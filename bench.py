@@ -188,6 +188,74 @@ def build_workload(name, P, rank, log):
     return dict(N=N, E=E, F=F, B=B, train_edges=len(tr), subs=subs, shared=pa.shared, split=split)
 
 
+def build_workload_ref(name, P, log):
+    """The same workload built by the REFERENCE library itself (oracle/_ref:
+    gen_powerlaw graph_io.cpp:175-250, chrono_split :156-173, centrality +
+    hubs centrality.cpp:27-88, partition_stream partitioner.cpp:152,
+    induce_subgraphs pac_sim.cpp:106-132) — bit-identical to the product's
+    (tests/test_host_parity.py), and the product library is never loaded."""
+    from oracle import ref as R
+    N, E, F, B = CONFIGS[name]
+    t0 = time.time()
+    edges, nc, _ = R.gen_powerlaw(N, E, 2.5, 1)
+    log(f"reference gen_powerlaw {N}x{E}: {time.time() - t0:.1f}s")
+    n_tr, _, _ = R.chrono_split_sizes(len(edges), 0.70, 0.15)
+    tr = np.ascontiguousarray(edges[:n_tr])
+    del edges
+    t_max = float(tr["ts"].max()) if n_tr else 0.0
+    t0 = time.time()
+    cent, _ = R.compute_centrality(tr, nc, t_max, 0.5)
+    hubs = R.select_hubs(cent, 0.05)
+    t1 = time.time()
+    pa = R.partition(tr, nc, t_max, P, cent, hubs, 0.05)
+    t_part = time.time() - t1
+    log(f"reference centrality+hubs {t1 - t0:.1f}s, partition_stream P={P}: {t_part:.1f}s "
+        f"({n_tr / max(t_part, 1e-9) / 1e6:.1f} M edges/s), shared={len(pa['shared'])}")
+    subs = R.induce_subgraphs(tr, nc, pa["node_parts"], P)
+    return dict(N=N, E=E, F=F, B=B, train_edges=n_tr, subs=subs, shared=pa["shared"],
+                partition_s=t_part, hubs_s=t1 - t0)
+
+
+def cpu_partition_baseline(wl):
+    """the reference partition_stream over the full train
+    stream, single thread as written."""
+    return {"what": "reference partition_stream (partitioner.cpp:152) over the full train stream",
+            "value": wl["train_edges"] / wl["partition_s"], "unit": "edges/s", "cores": 1,
+            "kind": "reference", "seconds": wl["partition_s"],
+            "sample": f"{wl['train_edges']} train edges, P={len(wl['subs'])}, k=0.05"}
+
+
+def cpu_tgn_oracle_rate(nodes, edges, eids, cfg, log, window=200_000, steps=3):
+    """the CPU TGN oracle (oracle/tgn_oracle.py, torch fp32 on
+    all host threads) — the same model as the GPU step — on a bounded window
+    of the partition stream: history from the window's first half, `steps`
+    batches timed from its middle (memory zero there, as the trainer's seek)."""
+    import torch
+    from oracle import tgn_oracle as T
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    E = len(edges)
+    lo = max(0, E // 2 - window // 2)
+    hi = min(E, lo + window)
+    oc = T.TGNConfig(d_mem=cfg["D"], d_time=cfg["T"], d_edge=cfg["F"], n_neighbors=cfg["K"],
+                     n_heads=cfg["H"], batch_size=cfg["B"], lr=1e-4)
+    wd = T.WorkerData(nodes, edges[lo:hi], eids[lo:hi], oc.d_edge, oc.seed_feat)
+    o = T.TGNOracle(oc, [wd])
+    o.begin_epoch(0)
+    o.seek((hi - lo) // 2 // oc.batch_size)
+    o.step()  # warm-up (allocator, thread pool)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.step()
+    secs = time.perf_counter() - t0
+    rate = steps * oc.batch_size / secs
+    log(f"CPU TGN oracle: {steps} steps x B={oc.batch_size} in {secs:.1f}s on {threads} threads")
+    return {"what": "CPU TGN oracle step (oracle/tgn_oracle.py: same model, torch fp32 + autograd)",
+            "value": rate, "unit": "edges/s", "cores": threads, "kind": "port",
+            "sample": f"{steps} steps of B={oc.batch_size} from the middle of a {hi - lo}-event "
+                      f"window of partition 0"}
+
+
 def cpu_reference_rate(sub_edges, node_count_local, d, seconds, log, threads=None):
     """The reference's own model_update (oracle/_ref) on host cores: T threads,
     each its own MemoryStore over a disjoint slice of the partition stream."""
@@ -206,13 +274,31 @@ def cpu_reference_rate(sub_edges, node_count_local, d, seconds, log, threads=Non
     return per * threads / secs, threads, per
 
 
-def localize(sub):
+def localize(nodes, edges):
     """Partition events in local ids (the reference MemoryStore is dense over ids)."""
-    from paper_2308_14129_b200 import EDGE_DTYPE
-    loc = np.searchsorted(sub.nodes, sub.edges["src"]), np.searchsorted(sub.nodes, sub.edges["dst"])
-    e = np.empty(len(sub.edges), EDGE_DTYPE)
-    e["src"], e["dst"], e["ts"] = loc[0], loc[1], sub.edges["ts"]
+    from oracle.ref import EDGE_DTYPE
+    loc = np.searchsorted(nodes, edges["src"]), np.searchsorted(nodes, edges["dst"])
+    e = np.empty(len(edges), EDGE_DTYPE)
+    e["src"], e["dst"], e["ts"] = loc[0], loc[1], edges["ts"]
     return e
+
+
+def loaded_native_libs():
+    """Shared objects of this repo mapped into the process (evidence of which
+    implementation ran)."""
+    try:
+        maps = open("/proc/self/maps").read().split("\n")
+    except OSError:
+        return None
+    libs = sorted({ln.split()[-1] for ln in maps if ln.endswith(".so") and ROOT in ln})
+    return [os.path.relpath(x, ROOT) for x in libs]
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 
 
 def main():
@@ -225,13 +311,23 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--fp32-steps", type=int, default=100,
+                    help="also time this many steps with gemm_mode 0 (FP32 FFMA) for comparison")
     ap.add_argument("--gemm-mode", type=int, default=1,
                     help="0 = FP32 FFMA everywhere; 1 = tcgen05 TF32 for the GRU and attention "
                          "projection GEMMs (merge/decoder stay FP32 FFMA)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
 
     rank, world, local, pg = dist_init()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     verbose = rank == 0
 
     def log(msg):
@@ -252,9 +348,12 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        wl = build_workload(args.config, world, rank, log)
-        sub = wl["subs"][0]
-        rate, cores, per = cpu_reference_rate(localize(sub), len(sub.nodes), D, args.cpu_seconds, log)
+        # everything on this arm runs the reference library (oracle/_ref);
+        # the product library is never imported or loaded
+        wl = build_workload_ref(args.config, world, log)
+        nodes, edges = wl["subs"][0]
+        rate, cores, per = cpu_reference_rate(localize(nodes, edges), len(nodes), D,
+                                              args.cpu_seconds, log)
         sample = f"{cores} threads x {per} consecutive partition-0 events, d={D}, surrogate model_update"
         print(json.dumps({
             "impl": "reference", "metric": metric, "value": rate, "unit": "edges/s",
@@ -263,8 +362,11 @@ def main():
             "cpu_baseline": {"value": rate, "unit": "edges/s", "cores": cores, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": rate, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "partition_baseline": cpu_partition_baseline(wl),
+            "native_libs": loaded_native_libs(),
             "note": "speedpart has no TGN: its training path is the fixed surrogate model_update "
-                    "(pac_sim.cpp:68-104), timed here via oracle/_ref on all host threads"}))
+                    "(pac_sim.cpp:68-104), timed here via oracle/_ref on all host threads; the "
+                    "workload (generator, split, SEP, induction) is built by oracle/_ref as well"}))
         return
 
     import paper_2308_14129_b200 as sp
@@ -398,17 +500,51 @@ def main():
                  "frac_of_hbm": value / world * bpe / 1e9 / hbm_peak,
                  "roofline_edges_per_s_per_gpu": hbm_peak * 1e9 / bpe}
 
+    # the same workload in FP32 FFMA (gemm_mode 0): the evidence behind the
+    # TF32 tensor-core choice for the GRU / attention projections
+    fp32 = None
+    if args.gemm_mode == 1 and args.fp32_steps > 0:
+        tr.set_gemm_mode(0)
+        tr.seek(seek)
+        tr.run_steps(args.warmup)
+        barrier(pg)
+        ms0 = allreduce_max(pg, tr.run_steps(args.fp32_steps))
+        e0 = allreduce_sum(pg, float(sum(min(B, len(sub_mine.edges)) for _ in range(args.fp32_steps))))
+        fp32 = {"gemm_mode": 0, "value": e0 / (ms0 / 1e3), "unit": "edges/s",
+                "ms_per_step": ms0 / args.fp32_steps, "steps": args.fp32_steps,
+                "what": "same trainer and workload with every GEMM in FP32 FFMA"}
+        tr.set_gemm_mode(1)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        extra = []
         try:
-            rate, cores, per = cpu_reference_rate(localize(sub_mine), len(sub_mine.nodes), D,
-                                                  args.cpu_seconds, log)
+            rate, cores, per = cpu_reference_rate(localize(sub_mine.nodes, sub_mine.edges),
+                                                  len(sub_mine.nodes), D, args.cpu_seconds, log)
             cpu = {"value": rate, "unit": "edges/s", "cores": cores, "kind": "reference",
                    "sample": f"{cores} threads x {per} consecutive partition events, d={D}, "
                              "speedpart model_update (surrogate: the reference has no TGN)"}
         except Exception as ex:  # the reference .so must travel; report, do not fail the bench
             cpu = {"value": None, "unit": "edges/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
+        try:  # reference partition_stream on the full train stream
+            from oracle import ref as R
+            tre = wl["split"].train.edges
+            t_max = float(tre["ts"].max()) if len(tre) else 0.0
+            cent, _ = R.compute_centrality(tre, N, t_max, 0.5)
+            hubs = R.select_hubs(cent, 0.05)
+            t0 = time.time()
+            R.partition(tre, N, t_max, world, cent, hubs, 0.05)
+            extra.append(cpu_partition_baseline({"train_edges": len(tre), "partition_s": time.time() - t0,
+                                                 "subs": [None] * world}))
+        except Exception as ex:
+            extra.append({"what": "reference partition_stream", "value": None, "sample": f"unavailable: {ex}"})
+        try:  # the CPU TGN oracle (same model) on all host cores
+            extra.append(cpu_tgn_oracle_rate(sub_mine.nodes, sub_mine.edges, sub_mine.eids,
+                                             dict(D=D, T=T, F=F, K=K, H=H, B=B), log))
+        except Exception as ex:
+            extra.append({"what": "CPU TGN oracle", "value": None, "sample": f"unavailable: {ex}"})
+        cpu["also"] = extra
 
     if rank == 0:
         out = {
@@ -419,7 +555,7 @@ def main():
             "data": "synthetic (gen_powerlaw topology seed 1, hashed bf16-exact edge features seed 2, "
                     "random-init TGN seed 3)",
             "config": cfg_desc, "e2e": e2e, "roofline": roof, "step_roofline": step_roof,
-            "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk.summary(),
+            "cpu_baseline": cpu, "fp32_ffma": fp32, "gpu_launches": launches, "clocks": clk.summary(),
             "effective_edges_per_s": wl["train_edges"] / (tr.epoch_steps() * ms_per_step / 1e3),
             "device_memory_per_gpu": mem_gb,
             "epoch_steps": tr.epoch_steps(), "train_edges": wl["train_edges"],

@@ -356,6 +356,10 @@ spd_status spd_tgn_set_profile(spd_tgn_trainer* t, int32_t on);
 /* Regular steps (every local worker on a full batch) replay a captured CUDA
  * graph of the step; on by default, off = launch every kernel eagerly. */
 spd_status spd_tgn_set_graph(spd_tgn_trainer* t, int32_t on);
+/* Switch spd_tgn_config::gemm_mode between steps (0 FP32 FFMA, 1 tcgen05 TF32
+ * projections): parameters, optimiser state and memory carry over; captured
+ * step graphs are rebuilt. */
+spd_status spd_tgn_set_gemm_mode(spd_tgn_trainer* t, int32_t mode);
 /* Per-phase times (ms, CUDA events on the trainer's stream) of the last step. */
 spd_status spd_tgn_kernel_times(const spd_tgn_trainer* t, float* ms, int32_t* n_kernels,
                                 char* names, int32_t name_stride, int32_t cap);

@@ -367,6 +367,23 @@ class TGNOracle:
             if self.batches(w) == 0:
                 self.snap[w] = (self.mem[w].clone(), self.lu[w].copy())
 
+    def seek(self, step):
+        """Position the schedule at global step `step` of the current epoch
+        with memory, clocks and pending messages cleared (the trainer's
+        spd_tgn_seek: a timed region starts mid-epoch from a reset state)."""
+        if step >= self.epoch_steps():
+            raise ValueError("seek past the end of the epoch")
+        self.step_in_epoch = step
+        for w in range(len(self.W)):
+            nb = self.batches(w)
+            if nb == 0:
+                continue
+            self.pos[w] = step % nb
+            self.done[w] = step // nb > 0
+            self.mem[w].zero_()
+            self.lu[w][:] = 0
+            self.pend[w] = {}
+
     def step(self):
         """One lockstep global step over all workers; returns per-worker loss."""
         c = self.c
@@ -403,9 +420,9 @@ class TGNOracle:
             g, = torch.autograd.grad(loss, flat)
             grads += g
             n_active += 1
-            losses.append(float(loss))
+            losses.append(float(loss.detach()))
             self.last[w] = dict(emb=emb.detach().numpy(), neg=neg, nbr_ids=ids, cnt=cnt,
-                                loss=float(loss), U=U, memx=memx.detach().numpy(),
+                                loss=float(loss.detach()), U=U, memx=memx.detach().numpy(),
                                 post=(U, hn.detach() if len(U) else None,
                                       mts if len(U) else None, src, dst, ts, lo, hi))
         # gradient mean over ALL workers (an idle worker contributes zeros)

@@ -739,18 +739,9 @@ class TGNConfig:
                           self.gemm_mode)
 
 
-def _prefer_loaded_nccl():
-    """Load torch's bundled libnccl first when torch is present, so the
-    library's dlopen(RTLD_NOLOAD) reuses it instead of a second copy."""
-    try:
-        import torch  # noqa: F401
-        import torch.distributed  # noqa: F401
-    except Exception:
-        pass
-
-
 def nccl_unique_id() -> bytes:
-    _prefer_loaded_nccl()
+    """ncclGetUniqueId of the libnccl the library binds at run time (one
+    already loaded into the process, else $SPD_NCCL_LIB, else the system's)."""
     buf = C.create_string_buffer(128)
     _check(lib.spd_nccl_unique_id(buf))
     return buf.raw
@@ -764,8 +755,6 @@ class TGNTrainer:
                  node_count: int | None = None, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, device: int = 0):
         self.cfg = cfg
-        if world > 1:
-            _prefer_loaded_nccl()
         self.workers = list(range(len(subgraphs))) if workers is None else list(workers)
         if node_count is None:
             node_count = int(max([int(g.nodes.max()) + 1 for g in subgraphs if len(g.nodes)] + [0]))
@@ -868,6 +857,11 @@ class TGNTrainer:
 
     def set_debug(self, on: bool = True):
         _check(lib.spd_tgn_set_debug(self._h, int(on)))
+
+    def set_gemm_mode(self, mode: int):
+        """0 = FP32 FFMA everywhere, 1 = tcgen05 TF32 GRU/attention projections."""
+        _check(lib.spd_tgn_set_gemm_mode(self._h, int(mode)))
+        self.cfg.gemm_mode = int(mode)
 
     def set_graph(self, on: bool):
         """Replay regular steps as a captured CUDA graph (default on)."""

@@ -141,6 +141,7 @@ _SIGS = {
     "spd_tgn_step_host_async": (i32, [P, PP, PP, P]),
     "spd_tgn_sync": (i32, [P]),
     "spd_tgn_set_graph": (i32, [P, i32]),
+    "spd_tgn_set_gemm_mode": (i32, [P, i32]),
     "spd_tgn_set_profile": (i32, [P, i32]),
     "spd_edge_feature": (f32, [u64, u64, u32]),
 }

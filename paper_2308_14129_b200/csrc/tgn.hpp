@@ -148,6 +148,7 @@ public:
     void set_debug(bool on) { debug_ = on; }
     void set_profile(bool on) { profile_ = on; }
     void set_graph(bool on) { use_graph_ = on; }
+    void set_gemm_mode(int mode);
     int device() const { return device_; }
     cudaStream_t stream() const { return stream_; }
 

@@ -1435,6 +1435,24 @@ void TGNTrainer::refresh_tc_weights() {
            lay_.total);
 }
 
+void TGNTrainer::set_gemm_mode(int mode) {
+    DeviceGuard g(device_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+    for (auto& ge : graph_exec_)
+        if (ge) {
+            SPD_CUDA(cudaGraphExecDestroy(ge));
+            ge = nullptr;
+        }
+    eager_full_steps_ = 0;
+    cfg_.gemm_mode = mode;
+    s_->d.rnd = mode == 1 ? 1 : 0;
+    refresh_tc_weights();
+    // the TC weight-gradient GEMMs read whole K blocks of the gate gradients
+    s_->dGi.zero(stream_);
+    s_->dGh.zero(stream_);
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+
 void TGNTrainer::set_params(const float* in) {
     DeviceGuard g(device_);
     params_.upload(in, lay_.total, stream_);
