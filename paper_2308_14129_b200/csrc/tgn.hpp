@@ -192,15 +192,16 @@ private:
     float* ws_cur_ = nullptr;      // workspace slice of the side task being issued
     std::size_t wsn_cur_ = 0;
     // a second fork for the GRU's hidden-side gate GEMM, and the points of the
-    // side stream the main stream waits for (neighbours found, phases evaluated)
+    // side stream the main stream waits for (neighbours found, dH index built)
     cudaStream_t aux_ = nullptr;
     cudaEvent_t ev_aux_fork_ = nullptr, ev_aux_join_ = nullptr, ev_roots_ = nullptr,
-                ev_phi_ = nullptr;
+                ev_dhidx_ = nullptr;
     // gradient zeroing forked at step start beside the forward; the backward
     // (first gradient writer) joins it
     cudaStream_t zs_ = nullptr;
     cudaEvent_t ev_zfork_ = nullptr, ev_zero_ = nullptr;
-    cudaEvent_t ev_bwdx_ = nullptr;  // attention input-gradient scatter done
+    cudaEvent_t ev_bwdx_ = nullptr;  // attention time-encoder partials done
+    cudaEvent_t ev_pull_ = nullptr;  // dH chunk partials done (tgn_dh.cu)
     bool scratch_zeroed_ = false;    // dH/dGi/dGh cleared by this step's k_zero_list
 
     spd_tgn_config cfg_;

@@ -12,11 +12,14 @@
 // here and never written to HBM. Same algebra as the oracle; only the FP32
 // summation order differs.
 //
-// Execution: 4 warps per block, one root per warp. Each warp first stages its
+// Execution: 3 warps per block, one root per warp. Each warp first stages its
 // root's k neighbour rows in shared memory — memory row (f32, the GRU output
-// when the neighbour was just updated) and raw bf16 feature row by cp.async,
-// so every gather of the root is in flight at once, and cos (backward: also
-// sin) of the f64 time phase — and both passes then read shared memory.
+// when the neighbour was just updated) and raw bf16 feature row by TMA bulk
+// copies, so every gather of the root is in flight at once — and, while those
+// copies fly, each lane evaluates the time encoding cos(w dt + b) of its own
+// time columns for every neighbour (f64 phase, tgn_common.cuh phase_sincos)
+// into the same staged rows; both passes then read shared memory. Nothing of
+// the time encoding is materialised in HBM.
 //
 // Lane slots are region-uniform: slot i < NM covers memory columns
 // 4(lane + 32i), the next NT slots time columns, the last NF slots feature
@@ -181,22 +184,20 @@ __device__ __forceinline__ int vidx(int lane) {
 }
 
 // Stage root r's neighbour rows (warp-cooperative): lane j < c_n issues the
-// three bulk copies of neighbour j's row — memory row (GRU output when just
-// updated), phi row (cos, and sin for the backward; k_phi), bf16 feature row
-// — all completing on the warp's mbarrier, so every gather of the root is in
-// flight at once for ~3 instructions per neighbour; the caller overlaps its
-// per-root loads with them before bar_wait. Lane j < c_n holds
-// neighbour j's (dt, slot) on return, for the caller's scatters.
+// two bulk copies of neighbour j's row — memory row (GRU output when just
+// updated) and bf16 feature row — both completing on the warp's mbarrier, so
+// every gather of the root is in flight at once for ~2 instructions per
+// neighbour; the caller fills the time columns (fill_cos) and issues its
+// per-root loads meanwhile, then waits. Lane j < c_n holds neighbour j's
+// (dt, slot) on return.
 __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, int r, int c_n,
                                            int lane, const std::uint32_t* nbr_node,
                                            const std::uint32_t* nbr_ev, const double* nbr_dt,
-                                           const float* mem_new, unsigned char* xs, bool with_sin,
-                                           const float* phi, std::uint64_t* bar, double& m_dt,
-                                           int& m_slot) {
+                                           const float* mem_new, unsigned char* xs,
+                                           std::uint64_t* bar, double& m_dt, int& m_slot) {
     m_dt = 0.0;
     m_slot = -1;
-    const unsigned pbytes = 4u * d.T * (with_sin ? 2u : 1u);
-    const unsigned per = 4u * d.D + pbytes + 2u * d.Fp;
+    const unsigned per = 4u * d.D + 2u * d.Fp;
     if (lane == 0) bar_expect(bar, per * c_n);
     __syncwarp();
     if (lane < c_n) {
@@ -205,12 +206,42 @@ __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, in
         m_dt = nbr_dt[o];
         m_slot = w.slot[node];
         const float* mrow = m_slot >= 0 ? mem_new + (std::size_t)m_slot * d.D : w.mem + (std::size_t)node * d.D;
-        unsigned char* dst = xs + (std::size_t)lane * row_bytes(d, with_sin);
+        unsigned char* dst = xs + (std::size_t)lane * row_bytes(d, false);
         bulk_g2s(dst, mrow, 4u * d.D, bar);
-        bulk_g2s(dst + 4 * d.D, phi + o * 2 * d.T, pbytes, bar);
-        if (d.Fp) bulk_g2s(dst + feat_off(d, with_sin), w.feat + (std::size_t)ev * d.Fp, 2u * d.Fp, bar);
+        if (d.Fp) bulk_g2s(dst + feat_off(d, false), w.feat + (std::size_t)ev * d.Fp, 2u * d.Fp, bar);
     }
-    // the caller issues its own per-root loads, then waits (bar_wait(bar, 0))
+    // the caller fills the time columns, issues its own per-root loads, then
+    // waits (bar_wait(bar, 0))
+}
+
+// Time columns of the staged rows: each lane writes cos(w dt_j + b) of its own
+// time slots (the columns its x_slot reads) for every neighbour j < c_n.
+template <class S>
+__device__ __forceinline__ void fill_cos(const Dims& d, int lane, int c_n, double m_dt,
+                                         const float* time_w, const float* time_b,
+                                         unsigned char* xs, int RB) {
+    float4 tw[S::N], tb[S::N];
+#pragma unroll
+    for (int i = 0; i < S::N; ++i) {
+        const int o = 4 * (lane + 32 * S::local(i));
+        const bool ok = S::region(i) == 1 && o < d.T;
+        tw[i] = ok ? *reinterpret_cast<const float4*>(time_w + o) : z4();
+        tb[i] = ok ? *reinterpret_cast<const float4*>(time_b + o) : z4();
+    }
+#pragma unroll 1
+    for (int j = 0; j < c_n; ++j) {
+        const double dt = __shfl_sync(0xffffffffu, m_dt, j);
+        unsigned char* row = xs + (std::size_t)j * RB;
+#pragma unroll
+        for (int i = 0; i < S::N; ++i) {
+            if (S::region(i) != 1) continue;
+            const int o = 4 * (lane + 32 * S::local(i));
+            if (o >= d.T) continue;
+            const float c0 = time_cos(tw[i].x, tb[i].x, dt), c1 = time_cos(tw[i].y, tb[i].y, dt);
+            const float c2 = time_cos(tw[i].z, tb[i].z, dt), c3 = time_cos(tw[i].w, tb[i].w, dt);
+            *reinterpret_cast<float4*>(row + 4 * (d.D + o)) = make_float4(c0, c1, c2, c3);
+        }
+    }
 }
 
 template <class S, int HMAX>
@@ -292,33 +323,6 @@ __device__ __forceinline__ void axpys(float4 (&v)[HMAX][S::N], const Dims& d, in
 
 }  // namespace
 
-// Time encoding of every valid neighbour occurrence, phi[r][j] = [cos T | sin T]
-// of w dt + b (f64 phase, tgn_common.cuh phase_sincos); one thread per
-// (occurrence, 4 consecutive time columns): float4 parameter loads and
-// stores, four independent f64 chains in flight.
-__global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, const double* nbr_dt,
-                      const int* cnt, float* phi) {
-    pdl_entry();
-    const int T4 = d.T / 4;
-    // grid-stride over (occurrence, 4 columns): launched with a small grid so
-    // it shares the SMs with the critical path's kernels instead of flooding them
-    for (std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
-         i < (std::size_t)R * d.K * T4; i += (std::size_t)gridDim.x * blockDim.x) {
-    const std::size_t occ = i / T4;
-    const int t = 4 * static_cast<int>(i % T4);
-    const int r = static_cast<int>(occ / d.K), j = static_cast<int>(occ % d.K);
-    if (j >= cnt[r]) continue;
-    const double dt = nbr_dt[occ];
-    const float4 w = *reinterpret_cast<const float4*>(time_w + t);
-    const float4 b = *reinterpret_cast<const float4*>(time_b + t);
-    const float2 s0 = phase_sincos<true>(w.x, b.x, dt), s1 = phase_sincos<true>(w.y, b.y, dt);
-    const float2 s2 = phase_sincos<true>(w.z, b.z, dt), s3 = phase_sincos<true>(w.w, b.w, dt);
-    float* p = phi + occ * 2 * d.T;
-    *reinterpret_cast<float4*>(p + t) = make_float4(s0.y, s1.y, s2.y, s3.y);
-    *reinterpret_cast<float4*>(p + d.T + t) = make_float4(s0.x, s1.x, s2.x, s3.x);
-    }
-}
-
 __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd) {
     // forward and backward stage the same rows (memory | cos | features)
     const std::size_t stage = std::size_t(kRootsPerBlock) * d.K * row_bytes(d, false);
@@ -338,7 +342,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
                                                       const std::uint32_t* nbr_ev,
                                                       const double* nbr_dt, const int* cnt,
                                                       const float* mem_new, const float* Qp,
-                                                      float* alpha, float* xbar, float* phi) {
+                                                      float* alpha, float* xbar) {
     pdl_entry();
     using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -367,7 +371,8 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     }
     double m_dt;
     int m_slot;
-    stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, BWD, phi, bar, m_dt, m_slot);
+    stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, bar, m_dt, m_slot);
+    fill_cos<S>(d, lane, c_n, m_dt, time_w, time_b, xs, RB);
     load_slots<S, HMAX>(v, Qp + row0, d, lane);
     bar_wait(bar, 0);
     const float inv = 1.f / sqrtf((float)(d.DQ / d.H));
@@ -398,19 +403,20 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     store_slots<S, HMAX>(v, xbar + row0, d, lane, d.rnd);
 }
 
-// Backward, given dxbar_h = [W_V,h|b_V,h]^T dctx_h (GEMM) per root, in two
+// Backward, given dxbar_h = [W_V,h|b_V,h]^T dctx_h (GEMM) per root, in three
 // kernels so the critical path (dq'_h -> dQ GEMM -> query backward) does not
-// wait for the input-gradient scatter:
+// wait for the input-gradient work:
 //   k_attn_abs_bwd (critical path):
 //     da_hj = <dxbar_h, x~_j>;  ds_hj = a_hj (da_hj - sum_k a_hk da_hk) / sqrt(dh)
 //     dq'_h = sum_j ds_hj x~_j                       -> dQp (GEMMs give dQ, dW_K)
-//     ds    -> dsc [R][H][K] for the scatter kernel
-//   k_attn_abs_bwd_x (side stream, beside the dQ GEMMs):
-//     dx_j  = sum_h a_hj dxbar_h + ds_hj q'_h  on the gradient-carrying columns:
-//             memory part -> dH rows of pending nodes (float4 atomics), time
-//             part -> d/dw, d/db of cos(w dt + b) (per-block partials, fixed order).
-//   It needs no staged neighbour rows: only per-root vectors, the
-//   neighbours' slots and dt, and the sin half of their phi rows.
+//     ds    -> dsc [R][H][K]
+//   then, beside the dQ GEMMs, the input gradient of x~_j
+//     dx_j  = sum_h a_hj dxbar_h + ds_hj q'_h
+//   on its gradient-carrying columns: the memory part is summed per pending
+//   row in a fixed order by tgn_dh.cu (k_dh_pull, no atomics), the time part
+//   gives d/dw, d/db of cos(w dt + b) in k_attn_time_grad (per-block partials,
+//   fixed order). Neither needs staged rows: only per-root vectors, alpha,
+//   ds and the neighbours' dt.
 template <int NM, int NT, int NF, int HMAX>
 __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R,
                                                       const float* time_w, const float* time_b,
@@ -419,7 +425,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
                                                       const double* nbr_dt, const int* cnt,
                                                       const float* mem_new, const float* Qp,
                                                       const float* alpha, const float* dxbar,
-                                                      const float* phi, float* dQp, float* dsc) {
+                                                      float* dQp, float* dsc) {
     pdl_entry();
     using S = Slots<NM, NT, NF>;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -447,7 +453,8 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     }
     double m_dt;
     int m_slot;
-    stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, BWD, phi, bar, m_dt, m_slot);
+    stage_rows(w, d, r, c_n, lane, nbr_node, nbr_ev, nbr_dt, mem_new, xs, bar, m_dt, m_slot);
+    fill_cos<S>(d, lane, c_n, m_dt, time_w, time_b, xs, RB);
     if (lane < d.K)
         for (int h = 0; h < d.H; ++h)
             aa[h * d.K + lane] = lane < c_n ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
@@ -480,21 +487,17 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     store_slots<S, HMAX>(v, dQp + row0, d, lane, d.rnd);
 }
 
-// Input-gradient scatter of the attention backward (see above). One warp per
-// root, kRootsPerBlock roots per block; part: [gridDim.x][2T] (w then b), f64,
-// every block writes its row. Lane slots cover the memory (NM) and time (NT)
-// columns; per neighbour the lane's sin values come straight from the phi
-// rows (L2), one neighbour ahead of use.
-template <int NM, int NT, int HMAX>
-__global__ void __launch_bounds__(128) k_attn_abs_bwd_x(WorkerDev w, Dims d, int R,
-                                                        const std::uint32_t* nbr_node,
-                                                        const double* nbr_dt, const int* cnt,
-                                                        const float* Qp, const float* alpha,
-                                                        const float* dsc, const float* dxbar,
-                                                        const float* phi, float* dH, double* part) {
+// Time-encoder gradient of the attention backward (see above): one warp per
+// root, kRootsX roots per block; part: [gridDim.x][2T] (w then b), f64, every
+// block writes its row. Lane slot i covers time columns 4(lane + 32 i); the
+// sin of the phase is evaluated inline (f64 phase, phase_sincos).
+template <int NT, int HMAX>
+__global__ void __launch_bounds__(128) k_attn_time_grad(Dims d, int R, const float* time_w,
+                                                        const float* time_b, const double* nbr_dt,
+                                                        const int* cnt, const float* Qp,
+                                                        const float* alpha, const float* dsc,
+                                                        const float* dxbar, double* part) {
     pdl_entry();
-    using S = Slots<NM, NT, 0>;
-    constexpr int NX = NM + NT;
     __shared__ float red[kRootsX][2 * 4 * 32 * NT];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = blockIdx.x * kRootsX + warp;
@@ -504,86 +507,67 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd_x(WorkerDev w, Dims d, int
     for (int i = 0; i < NT; ++i) gw[i] = gb[i] = z4();
     if (c_n > 0) {
         const std::size_t row0 = (std::size_t)r * d.H * d.ld_p;
-        // neighbour j's (slot, dt) on lane j; alpha and ds of lane j per head
-        int m_slot = -1;
+        // neighbour j's dt on lane j; alpha and ds of lane j per head
         double m_dt = 0.0;
         float la[HMAX], ls[HMAX];
-        if (lane < c_n) {
-            const std::size_t o = (std::size_t)r * d.K + lane;
-            m_slot = w.slot[nbr_node[o]];
-            m_dt = nbr_dt[o];
-        }
+        if (lane < c_n) m_dt = nbr_dt[(std::size_t)r * d.K + lane];
 #pragma unroll
         for (int h = 0; h < HMAX; ++h) {
             const bool ok = h < d.H && lane < c_n;
             la[h] = ok ? alpha[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
             ls[h] = ok ? dsc[((std::size_t)r * d.H + h) * d.K + lane] : 0.f;
         }
-        float4 g[HMAX][NX], q[HMAX][NX];
-#pragma unroll
-        for (int h = 0; h < HMAX; ++h)
-#pragma unroll
-            for (int i = 0; i < NX; ++i) {
-                const bool ok = h < d.H && S::valid(d, i, lane);
-                const int c = S::col(d, i, lane);
-                g[h][i] = ok ? *reinterpret_cast<const float4*>(dxbar + row0 + (std::size_t)h * d.ld_p + c) : z4();
-                q[h][i] = ok ? *reinterpret_cast<const float4*>(Qp + row0 + (std::size_t)h * d.ld_p + c) : z4();
-            }
-        const float* sin0 = phi + (std::size_t)r * d.K * 2 * d.T + d.T;
-        float4 snx[NT];
+        float4 g[HMAX][NT], q[HMAX][NT], tw[NT], tb[NT];
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
             const int o = 4 * (lane + 32 * i);
-            snx[i] = o < d.T ? *reinterpret_cast<const float4*>(sin0 + o) : z4();
+            const bool okc = o < d.T;
+            tw[i] = okc ? *reinterpret_cast<const float4*>(time_w + o) : z4();
+            tb[i] = okc ? *reinterpret_cast<const float4*>(time_b + o) : z4();
+#pragma unroll
+            for (int h = 0; h < HMAX; ++h) {
+                const bool ok = h < d.H && okc;
+                const std::size_t c = row0 + (std::size_t)h * d.ld_p + d.D + o;
+                g[h][i] = ok ? *reinterpret_cast<const float4*>(dxbar + c) : z4();
+                q[h][i] = ok ? *reinterpret_cast<const float4*>(Qp + c) : z4();
+            }
         }
 #pragma unroll 1
         for (int j = 0; j < c_n; ++j) {
-            const int slot = __shfl_sync(0xffffffffu, m_slot, j);
-            const float fdt = (float)__shfl_sync(0xffffffffu, m_dt, j);
+            const double dt = __shfl_sync(0xffffffffu, m_dt, j);
+            const float fdt = (float)dt;
             float a[HMAX], sv_[HMAX];
 #pragma unroll
             for (int h = 0; h < HMAX; ++h) {
                 a[h] = __shfl_sync(0xffffffffu, la[h], j);
                 sv_[h] = __shfl_sync(0xffffffffu, ls[h], j);
             }
-            float4 snc[NT];
 #pragma unroll
             for (int i = 0; i < NT; ++i) {
-                snc[i] = snx[i];
-                const int o = 4 * (lane + 32 * i);
-                if (j + 1 < c_n && o < d.T)
-                    snx[i] = *reinterpret_cast<const float4*>(sin0 + (std::size_t)(j + 1) * 2 * d.T + o);
-            }
-#pragma unroll
-            for (int i = 0; i < NX; ++i) {
-                if (!S::valid(d, i, lane)) continue;
+                if (4 * (lane + 32 * i) >= d.T) continue;
                 float4 gx = z4();
 #pragma unroll
                 for (int h = 0; h < HMAX; ++h) {
                     axpy4(gx, a[h], g[h][i]);
                     axpy4(gx, sv_[h], q[h][i]);
                 }
-                const int o = 4 * (lane + 32 * S::local(i));
-                if (S::region(i) == 0) {
-                    if (slot >= 0) atomicAdd(reinterpret_cast<float4*>(dH + (std::size_t)slot * d.D + o), gx);
-                } else {
-                    const float4 sv = snc[S::local(i)];
-                    float4& bw = gw[S::local(i)];
-                    float4& bb = gb[S::local(i)];
-                    bb.x -= sv.x * gx.x; bb.y -= sv.y * gx.y; bb.z -= sv.z * gx.z; bb.w -= sv.w * gx.w;
-                    bw.x -= sv.x * gx.x * fdt; bw.y -= sv.y * gx.y * fdt;
-                    bw.z -= sv.z * gx.z * fdt; bw.w -= sv.w * gx.w * fdt;
-                }
+                const float4 sv = make_float4(time_sin(tw[i].x, tb[i].x, dt), time_sin(tw[i].y, tb[i].y, dt),
+                                              time_sin(tw[i].z, tb[i].z, dt), time_sin(tw[i].w, tb[i].w, dt));
+                float4& bw = gw[i];
+                float4& bb = gb[i];
+                bb.x -= sv.x * gx.x; bb.y -= sv.y * gx.y; bb.z -= sv.z * gx.z; bb.w -= sv.w * gx.w;
+                bw.x -= sv.x * gx.x * fdt; bw.y -= sv.y * gx.y * fdt;
+                bw.z -= sv.z * gx.z * fdt; bw.w -= sv.w * gx.w * fdt;
             }
         }
     }
     // fixed-order per-block reduction of the roots' time-encoder partials
-    float* tw = red[warp];
+    float* tws = red[warp];
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
         const int t = 4 * (lane + 32 * i);
-        *reinterpret_cast<float4*>(tw + t) = gw[i];
-        *reinterpret_cast<float4*>(tw + 4 * 32 * NT + t) = gb[i];
+        *reinterpret_cast<float4*>(tws + t) = gw[i];
+        *reinterpret_cast<float4*>(tws + 4 * 32 * NT + t) = gb[i];
     }
     __syncthreads();
     for (int c = threadIdx.x; c < 2 * d.T; c += blockDim.x) {
@@ -599,25 +583,31 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd_x(WorkerDev w, Dims d, int
     template __global__ void k_attn_abs_fwd<NM, NT, NF, HM>(                                     \
         WorkerDev, Dims, int, const float*, const float*, const std::uint32_t*,                  \
         const std::uint32_t*, const double*, const int*, const float*, const float*, float*,     \
-        float*, float*);                                                                        \
+        float*);                                                                                \
     template __global__ void k_attn_abs_bwd<NM, NT, NF, HM>(                                     \
         WorkerDev, Dims, int, const float*, const float*, const std::uint32_t*,                  \
         const std::uint32_t*, const double*, const int*, const float*, const float*,             \
-        const float*, const float*, const float*, float*, float*);
-#define SPD_ABSX_INST(NM, NT, HM)                                                               \
-    template __global__ void k_attn_abs_bwd_x<NM, NT, HM>(                                       \
-        WorkerDev, Dims, int, const std::uint32_t*, const double*, const int*, const float*,     \
-        const float*, const float*, const float*, const float*, float*, double*);
+        const float*, const float*, float*, float*);
 #define SPD_ABS_NF(NM, NT, HM) \
-    SPD_ABS_INST(NM, NT, 1, HM) SPD_ABS_INST(NM, NT, 2, HM) SPD_ABS_INST(NM, NT, 3, HM) \
-    SPD_ABSX_INST(NM, NT, HM)
+    SPD_ABS_INST(NM, NT, 1, HM) SPD_ABS_INST(NM, NT, 2, HM) SPD_ABS_INST(NM, NT, 3, HM)
 #define SPD_ABS_H(HM) SPD_ABS_NF(1, 1, HM) SPD_ABS_NF(1, 2, HM) SPD_ABS_NF(2, 1, HM)
 SPD_ABS_H(2)
 SPD_ABS_H(4)
 #undef SPD_ABS_H
 #undef SPD_ABS_NF
-#undef SPD_ABSX_INST
 #undef SPD_ABS_INST
+template __global__ void k_attn_time_grad<1, 2>(Dims, int, const float*, const float*, const double*,
+                                                const int*, const float*, const float*, const float*,
+                                                const float*, double*);
+template __global__ void k_attn_time_grad<1, 4>(Dims, int, const float*, const float*, const double*,
+                                                const int*, const float*, const float*, const float*,
+                                                const float*, double*);
+template __global__ void k_attn_time_grad<2, 2>(Dims, int, const float*, const float*, const double*,
+                                                const int*, const float*, const float*, const float*,
+                                                const float*, double*);
+template __global__ void k_attn_time_grad<2, 4>(Dims, int, const float*, const float*, const double*,
+                                                const int*, const float*, const float*, const float*,
+                                                const float*, double*);
 
 }  // namespace tgnk
 }  // namespace spd

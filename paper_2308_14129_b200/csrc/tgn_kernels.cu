@@ -303,29 +303,17 @@ __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt)
     for (int c = lane; c < cols; c += 32) buf[(std::size_t)r * ld + c] = 0.f;
 }
 
-// Root-side input gradients (query [s_root | phi(0)] and merge-layer s_root
-// columns): memory rows into the GRU outputs of pending nodes (float4
-// atomics) and d/db of phi(0) = cos(b) (f64 per-block fixed-order partials;
-// d/dw is 0 at dt = 0). block (32, 8); rows_per_block roots; part[block][2T].
-__global__ void k_root_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
-                            const float* dq_in, const float* dm_in, const float* time_b,
-                            int rows_per_block, float* dH, double* part) {
+// Root-side time-encoder gradient: d/db of the query's phi(0) = cos(b)
+// columns (f64 per-block fixed-order partials; d/dw is 0 at dt = 0). The
+// roots' memory-column gradients are summed per pending row by tgn_dh.cu.
+// block (32, 8); rows_per_block roots; part[block][2T].
+__global__ void k_root_grad(Dims d, int R, const float* dq_in, const float* time_b,
+                            int rows_per_block, double* part) {
     pdl_entry();
     __shared__ double red[8][32];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int r0 = blockIdx.x * rows_per_block;
     const int r1 = min(R, r0 + rows_per_block);
-    for (int row = r0 + ty; row < r1; row += blockDim.y) {
-        const int s = w.slot[roots[row]];
-        if (s < 0) continue;
-        const float4* q = reinterpret_cast<const float4*>(dq_in + (std::size_t)row * d.ld_q);
-        const float4* m = reinterpret_cast<const float4*>(dm_in + (std::size_t)row * d.ld_m + d.DQ);
-        float4* o = reinterpret_cast<float4*>(dH + (std::size_t)s * d.D);
-        for (int c = tx; c < d.D / 4; c += 32) {
-            const float4 a = q[c], b = m[c];
-            atomicAdd(o + c, make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
-        }
-    }
     for (int c0 = 0; c0 < d.T; c0 += 32) {
         const int c = c0 + tx;
         double gb = 0.0;
@@ -368,33 +356,6 @@ __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb
     if (c >= T) return;
     gw[c] += (float)acc[c];
     gb[c] += (float)acc[T + c];
-}
-
-// GRUCell backward to the gate pre-activations (inputs x, h are constants).
-__global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* save, const float* h,
-                          float* dGi, float* dGh) {
-    pdl_entry();
-    const int nU = *w.nU;
-    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (std::size_t)nU * d.D) return;
-    const int u = i / d.D, c = i % d.D;
-    const float* s = save + (std::size_t)u * 4 * d.D;
-    const float r = s[c], z = s[d.D + c], n = s[2 * d.D + c], ghn = s[3 * d.D + c];
-    const float g = dH[(std::size_t)u * d.D + c];
-    const float hv = w.mem[(std::size_t)w.pU[u] * d.D + c];  // exact h
-    const float dn = g * (1.f - z);
-    const float dz = g * (hv - n);
-    const float dpn = dn * (1.f - n * n);
-    const float dpr = dpn * ghn * r * (1.f - r);
-    const float dpz = dz * z * (1.f - z);
-    float* gi = dGi + (std::size_t)u * d.ld_g;
-    float* gh = dGh + (std::size_t)u * d.ld_g;
-    gi[c] = rnd_if(dpr, d.rnd);
-    gi[d.D + c] = rnd_if(dpz, d.rnd);
-    gi[2 * d.D + c] = rnd_if(dpn, d.rnd);
-    gh[c] = rnd_if(dpr, d.rnd);
-    gh[d.D + c] = rnd_if(dpz, d.rnd);
-    gh[2 * d.D + c] = rnd_if(dpn * r, d.rnd);
 }
 
 __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,

@@ -56,6 +56,36 @@ struct WorkerDev {
     const std::uint64_t* ctl;
 };
 
+// Index of the step's memory-row readers for the deterministic dH reduction
+// (tgn_dh.cu). Entries: occurrence e = r * K + j for e < RK, then (from block
+// nb_occ on) root r = e - nb_occ * kDhBlock.
+constexpr int kDhBlock = 1024;  // entries per histogram / scatter block
+constexpr int kDhChunk = 32;    // occurrences per k_dh_pull warp
+struct DhIndex {
+    int RK, K, R, nb_occ, nb_root, U_cap;
+    const std::uint32_t* nbr_node;
+    const int* cnt;
+    const std::uint32_t* roots;
+    int* hist;          // [nb_occ + nb_root][U_cap] -> per-block exclusive prefixes
+    int* off_occ;       // [U_cap + 1]
+    int* off_root;      // [U_cap + 1]
+    int* chunk_off;     // [U_cap + 1]
+    int* chunk_slot;    // [RK / kDhChunk + U_cap]
+    int* chunk_start;   // [RK / kDhChunk + U_cap]
+    int* list_occ;      // [RK]
+    int* list_root;     // [R]
+};
+__global__ void k_dh_hist(WorkerDev w, DhIndex x);
+__global__ void k_dh_scan(DhIndex x);
+__global__ void k_dh_scatter(WorkerDev w, DhIndex x);
+template <int NM, int HMAX>
+__global__ void k_dh_pull(DhIndex x, Dims d, const float* alpha, const float* dsc,
+                          const float* dxbar, const float* Qp, float* partial);
+template <int NM>
+__global__ void k_gru_bwd_dh(WorkerDev w, Dims d, DhIndex x, const float* partial,
+                             const float* dq_in, const float* dm_in, const float* save,
+                             float* dGi, float* dGh);
+
 // --- kernels (definitions in tgn_kernels.cu) -------------------------------
 __global__ void k_init_aug(float* buf, int rows, int cols, int ld);
 __global__ void k_zero2(float* a, std::size_t na, double* b, std::size_t nb);
@@ -81,27 +111,24 @@ __global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
 // dynamic shared memory attn_smem_bytes(d, bwd); lane slots per region
 // NM = ceil(D / 128), NT = ceil(T / 128), NF = ceil((F + 1) / 128); HMAX >= H
 __host__ __device__ std::size_t attn_smem_bytes(const Dims& d, bool bwd);
-__global__ void k_phi(Dims d, int R, const float* time_w, const float* time_b, const double* nbr_dt,
-                      const int* cnt, float* phi);
 int attn_roots_per_block();
 int attn_x_roots_per_block();
 template <int NM, int NT, int NF, int HMAX>
 __global__ void k_attn_abs_fwd(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* nbr_node,
                                const std::uint32_t* nbr_ev, const double* nbr_dt, const int* cnt,
-                               const float* mem_new, const float* Qp, float* alpha, float* xbar,
-                               float* phi);
+                               const float* mem_new, const float* Qp, float* alpha, float* xbar);
 template <int NM, int NT, int NF, int HMAX>
 __global__ void k_attn_abs_bwd(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* nbr_node,
                                const std::uint32_t* nbr_ev, const double* nbr_dt, const int* cnt,
                                const float* mem_new, const float* Qp, const float* alpha,
-                               const float* dxbar, const float* phi, float* dQp, float* dsc);
-template <int NM, int NT, int HMAX>
-__global__ void k_attn_abs_bwd_x(WorkerDev w, Dims d, int R, const std::uint32_t* nbr_node,
+                               const float* dxbar, float* dQp, float* dsc);
+template <int NT, int HMAX>
+__global__ void k_attn_time_grad(Dims d, int R, const float* time_w, const float* time_b,
                                  const double* nbr_dt, const int* cnt, const float* Qp,
                                  const float* alpha, const float* dsc, const float* dxbar,
-                                 const float* phi, float* dH, double* part);
+                                 double* part);
 __global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
                                const int* cnt, const float* O, const float* mem_new, float* m_in);
 __global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in);
@@ -113,13 +140,10 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
 __global__ void k_sum_loss(const float* lossv, int n, float* out);
 __global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb);
 __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt);
-__global__ void k_root_grad(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
-                            const float* dq_in, const float* dm_in, const float* time_b,
-                            int rows_per_block, float* dH, double* part);
+__global__ void k_root_grad(Dims d, int R, const float* dq_in, const float* time_b,
+                            int rows_per_block, double* part);
 __global__ void k_time_grad_final(int T, int nblocks, const double* part, double* acc);
 __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb);
-__global__ void k_gru_bwd(WorkerDev w, Dims d, const float* dH, const float* save, const float* h,
-                          float* dGi, float* dGh);
 __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
                        float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
                        float eps, float* p_tc);

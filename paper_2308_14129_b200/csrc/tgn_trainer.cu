@@ -104,13 +104,18 @@ struct Scratch {
     DevBuf<std::uint32_t> roots, nbr_node, nbr_ev;
     DevBuf<double> root_t, nbr_dt;
     DevBuf<int> cnt;
-    DevBuf<float> x_gru, h_gru, Gi, Gh, gsave, mem_new, dH, dGi, dGh;
+    DevBuf<float> x_gru, h_gru, Gi, Gh, gsave, mem_new, dGi, dGh;
     DevBuf<float> Ya, Yb;  // decoder layer-1 halves (k_dec_head2)
     DevBuf<float> q_in, Q, Qp, xbar, alpha, dsc, ctx, O, m_in, Z1, emb, d_in, D1, logits, lossv, dlogit;
     DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dxbar, dQp, dQ, dq_in;
     DevBuf<float> ws;
     DevBuf<double> tpart;
-    DevBuf<float> phi;  // [R][K][cos T | sin T] of the neighbour occurrences (fwd -> bwd)
+    // deterministic dH reduction (tgn_dh.cu): reader index + chunk partials
+    DevBuf<int> dh_hist, dh_off_occ, dh_off_root, dh_chunk_off, dh_chunk_slot, dh_chunk_start,
+        dh_list_occ, dh_list_root;
+    DevBuf<float> dh_partial;
+    tgnk::DhIndex dh{};
+    int dh_max_chunks = 0;
     DevBuf<float> loss;  // per local worker
     int trows = 0, troot_blocks = 0, tattn_blocks = 0;  // time-grad partial blocks
 };
@@ -254,12 +259,11 @@ void attn_pick(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& 
     if (!bwd)
         attn_launch(&tgnk::k_attn_abs_fwd<NM, NT, NF, HM>, set_fwd, grid, tgnk::attn_smem_bytes(d, false), st,
                     wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
-                    s.Qp.p, s.alpha.p, s.xbar.p, s.phi.p);
+                    s.Qp.p, s.alpha.p, s.xbar.p);
     else
         attn_launch(&tgnk::k_attn_abs_bwd<NM, NT, NF, HM>, set_bwd, grid, tgnk::attn_smem_bytes(d, true), st,
                     wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
-                    s.Qp.p, s.alpha.p, s.dxbar.p, static_cast<const float*>(s.phi.p), s.dQp.p,
-                    s.dsc.p);
+                    s.Qp.p, s.alpha.p, s.dxbar.p, s.dQp.p, s.dsc.p);
 }
 
 void attn_dispatch(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& wd,
@@ -287,26 +291,56 @@ void attn_abs_fwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const f
     attn_dispatch(false, unsigned((R + rpb - 1) / rpb), st, wd, d, R, tw, tb, s, nullptr);
 }
 
-// input-gradient scatter of the attention backward (tgn_attn.cu k_attn_abs_bwd_x)
-void attn_abs_bwd_x(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const Scratch& s,
+// time-encoder gradient of the attention backward (tgn_attn.cu k_attn_time_grad)
+void attn_time_grad(const tgnk::Dims& d, int R, const float* tw, const float* tb, const Scratch& s,
                     double* part, cudaStream_t st) {
-    const int nm = (d.D + 127) / 128, nt = (d.T + 127) / 128;
+    const int nt = (d.T + 127) / 128;
     const unsigned grid = unsigned(s.tattn_blocks);  // every block writes its partial row
-#define SPD_X(NM, NT)                                                                            \
-    if (nm == NM && nt == NT) {                                                                 \
-        if (d.H <= 2)                                                                           \
-            launch(tgnk::k_attn_abs_bwd_x<NM, NT, 2>, grid, 128, 0, st, wd, d, R, s.nbr_node.p,  \
-                   s.nbr_dt.p, s.cnt.p, s.Qp.p, s.alpha.p, s.dsc.p, s.dxbar.p,                   \
-                   static_cast<const float*>(s.phi.p), s.dH.p, part);                            \
-        else                                                                                    \
-            launch(tgnk::k_attn_abs_bwd_x<NM, NT, 4>, grid, 128, 0, st, wd, d, R, s.nbr_node.p,  \
-                   s.nbr_dt.p, s.cnt.p, s.Qp.p, s.alpha.p, s.dsc.p, s.dxbar.p,                   \
-                   static_cast<const float*>(s.phi.p), s.dH.p, part);                            \
-        return;                                                                                 \
+    auto go = [&](auto k) {
+        launch(k, grid, 128, 0, st, d, R, tw, tb, static_cast<const double*>(s.nbr_dt.p),
+               static_cast<const int*>(s.cnt.p), static_cast<const float*>(s.Qp.p),
+               static_cast<const float*>(s.alpha.p), static_cast<const float*>(s.dsc.p),
+               static_cast<const float*>(s.dxbar.p), part);
+    };
+    if (nt == 1) d.H <= 2 ? go(tgnk::k_attn_time_grad<1, 2>) : go(tgnk::k_attn_time_grad<1, 4>);
+    else if (nt == 2) d.H <= 2 ? go(tgnk::k_attn_time_grad<2, 2>) : go(tgnk::k_attn_time_grad<2, 4>);
+    else internal_error("InvalidParams", "time encoder wider than the instantiated shapes");
+}
+
+// memory-row gradients of the GRU outputs, deterministic (tgn_dh.cu)
+void dh_index(const tgnk::WorkerDev& wd, const Scratch& s, cudaStream_t st) {
+    const std::size_t sm = std::size_t(s.dh.U_cap) * sizeof(int);
+    static std::size_t set = 0;
+    if (sm > 48 * 1024 && sm > set) {
+        SPD_CUDA(cudaFuncSetAttribute(tgnk::k_dh_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        SPD_CUDA(cudaFuncSetAttribute(tgnk::k_dh_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+        set = sm;
     }
-    SPD_X(1, 1) SPD_X(1, 2) SPD_X(2, 1)
-#undef SPD_X
-    internal_error("InvalidParams", "attention row outside the instantiated shapes");
+    const unsigned nb = unsigned(s.dh.nb_occ + s.dh.nb_root);
+    launch(tgnk::k_dh_hist, nb, tgnk::kDhBlock, sm, st, wd, s.dh);
+    launch(tgnk::k_dh_scan, 1, 1024, 0, st, s.dh);
+    launch(tgnk::k_dh_scatter, nb, tgnk::kDhBlock, sm, st, wd, s.dh);
+}
+void dh_pull(const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
+    const unsigned grid = unsigned((std::size_t(s.dh_max_chunks) * 32 + 255) / 256);
+    auto go = [&](auto k) {
+        launch(k, grid, 256, 0, st, s.dh, d, static_cast<const float*>(s.alpha.p),
+               static_cast<const float*>(s.dsc.p), static_cast<const float*>(s.dxbar.p),
+               static_cast<const float*>(s.Qp.p), s.dh_partial.p);
+    };
+    const int nm = (d.D + 127) / 128;
+    if (nm == 1) d.H <= 2 ? go(tgnk::k_dh_pull<1, 2>) : go(tgnk::k_dh_pull<1, 4>);
+    else d.H <= 2 ? go(tgnk::k_dh_pull<2, 2>) : go(tgnk::k_dh_pull<2, 4>);
+}
+void gru_bwd_dh(const tgnk::WorkerDev& wd, const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
+    const unsigned grid = unsigned((std::size_t(s.U) * 32 + 255) / 256);
+    auto go = [&](auto k) {
+        launch(k, grid, 256, 0, st, wd, d, s.dh, static_cast<const float*>(s.dh_partial.p),
+               static_cast<const float*>(s.dq_in.p), static_cast<const float*>(s.dm_in.p),
+               static_cast<const float*>(s.gsave.p), s.dGi.p, s.dGh.p);
+    };
+    if ((d.D + 127) / 128 == 1) go(tgnk::k_gru_bwd_dh<1>);
+    else go(tgnk::k_gru_bwd_dh<2>);
 }
 
 void attn_abs_bwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
@@ -391,7 +425,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
 
     SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
     SPD_CUDA(cudaStreamCreateWithPriority(&zs_, cudaStreamNonBlocking, prio_lo));
-    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_phi_, &ev_zfork_, &ev_zero_, &ev_bwdx_})
+    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_dhidx_, &ev_zfork_, &ev_zero_, &ev_bwdx_, &ev_pull_})
         SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors);
     feat_seed_mixed_ = mix64(cfg.seed_feat);
@@ -441,12 +475,26 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     const int R = s.R, RK = s.RK, U = s.U;
     s.roots.alloc(R); s.root_t.alloc(R); s.cnt.alloc(R);
     s.nbr_node.alloc(RK); s.nbr_ev.alloc(RK); s.nbr_dt.alloc(RK);
-    s.phi.alloc(std::size_t(RK) * 2 * d.T);
+    {  // dH reader index (tgn_dh.cu)
+        auto& x = s.dh;
+        x.RK = RK; x.K = d.K; x.R = R; x.U_cap = U;
+        x.nb_occ = (RK + tgnk::kDhBlock - 1) / tgnk::kDhBlock;
+        x.nb_root = (R + tgnk::kDhBlock - 1) / tgnk::kDhBlock;
+        s.dh_max_chunks = RK / tgnk::kDhChunk + U + 1;
+        s.dh_hist.alloc(std::size_t(x.nb_occ + x.nb_root) * U);
+        s.dh_off_occ.alloc(U + 1); s.dh_off_root.alloc(U + 1); s.dh_chunk_off.alloc(U + 1);
+        s.dh_chunk_slot.alloc(s.dh_max_chunks); s.dh_chunk_start.alloc(s.dh_max_chunks);
+        s.dh_list_occ.alloc(RK); s.dh_list_root.alloc(R);
+        s.dh_partial.alloc(std::size_t(s.dh_max_chunks) * D);
+        x.hist = s.dh_hist.p; x.off_occ = s.dh_off_occ.p; x.off_root = s.dh_off_root.p;
+        x.chunk_off = s.dh_chunk_off.p; x.chunk_slot = s.dh_chunk_slot.p;
+        x.chunk_start = s.dh_chunk_start.p; x.list_occ = s.dh_list_occ.p; x.list_root = s.dh_list_root.p;
+    }
     s.x_gru.alloc(std::size_t(U) * d.ld_x); init_aug(s.x_gru, U, d.DM, d.ld_x, stream_);
     s.h_gru.alloc(std::size_t(U) * d.ld_h); init_aug(s.h_gru, U, D, d.ld_h, stream_);
     s.Gi.alloc(std::size_t(U) * d.ld_g); s.Gh.alloc(std::size_t(U) * d.ld_g);
     s.gsave.alloc(std::size_t(U) * 4 * D); s.mem_new.alloc(std::size_t(U) * D);
-    s.dH.alloc(std::size_t(U) * D); s.dGi.alloc(std::size_t(U) * d.ld_g); s.dGh.alloc(std::size_t(U) * d.ld_g);
+    s.dGi.alloc(std::size_t(U) * d.ld_g); s.dGh.alloc(std::size_t(U) * d.ld_g);
     s.dGi.zero(stream_); s.dGh.zero(stream_); s.Gi.zero(stream_); s.Gh.zero(stream_);
     s.q_in.alloc(std::size_t(R) * d.ld_q); init_aug(s.q_in, R, d.DQ, d.ld_q, stream_);
     s.Q.alloc(std::size_t(R) * d.ld_Q);
@@ -474,6 +522,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.troot_blocks = (R + s.trows - 1) / s.trows;
     s.tattn_blocks = (R + tgnk::attn_x_roots_per_block() - 1) / tgnk::attn_x_roots_per_block();
     s.tpart.alloc(std::size_t(s.troot_blocks + s.tattn_blocks) * 2 * d.T);
+    s.dh.nbr_node = s.nbr_node.p; s.dh.cnt = s.cnt.p; s.dh.roots = s.roots.p;
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
     SPD_CUDA(cudaStreamSynchronize(stream_));
 
@@ -524,7 +573,7 @@ TGNTrainer::~TGNTrainer() {
         if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
         if (sides_[k]) cudaStreamDestroy(sides_[k]);
     }
-    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_phi_, ev_zfork_, ev_zero_, ev_bwdx_})
+    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_dhidx_, ev_zfork_, ev_zero_, ev_bwdx_, ev_pull_})
         if (e) cudaEventDestroy(e);
     if (aux_) cudaStreamDestroy(aux_);
     for (auto& p : aring_)
@@ -780,29 +829,17 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     cudaStream_t st = stream_;
     const bool tc = cfg_.gemm_mode == 1;  // tensor cores for GRU + attention projections only
     const float* PW = tc ? params_tc_.p : params_.p;
-    // The recent-k search and the time encoding of every neighbour occurrence
-    // depend only on the batch, the static CSR and the time parameters: they
-    // run on the side stream beside the GRU update and the query GEMMs; the
-    // main stream waits for each result where it is first read. Profiled runs
-    // keep them on the main stream so their phase times are their own.
+    // The recent-k search depends only on the batch and the static CSR, the
+    // dH reader index (tgn_dh.cu) on the neighbour lists and the pending
+    // slots: both run on the side stream beside the GRU update and the query
+    // GEMMs; the main stream waits for the neighbours where they are first
+    // read, the backward for the index. Profiled runs keep them on the main
+    // stream so their phase times are their own.
     auto roots = [&](cudaStream_t sx) {
         launch(tgnk::k_roots_nbrs, blocks_for(std::size_t(R) * 32), 256, 0, sx, wd, B, d.K, s.roots.p,
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     };
-    auto phi = [&](cudaStream_t sx) {
-        static const unsigned phi_cap = [] {
-            const char* e = std::getenv("SPD_PHI_BLOCKS");
-            return e ? unsigned(std::atoi(e)) : 2u * 148u;
-        }();
-        launch(tgnk::k_phi, std::min<unsigned>(blocks_for(std::size_t(R) * d.K * (d.T / 4)), phi_cap),
-               256, 0, sx, d, R,
-               P + lay_.time_w, P + lay_.time_b, static_cast<const double*>(s.nbr_dt.p),
-               static_cast<const int*>(s.cnt.p), s.phi.p);
-    };
-    if (profile_) {
-        timed("roots_nbrs", [&] { roots(st); });
-        timed("phi", [&] { phi(st); });
-    }
+    if (profile_) timed("roots_nbrs", [&] { roots(st); });
     // this batch's last messages into the other pending set (K3): depends only
     // on the batch's events, off the critical path (the GRU below reads the
     // current set); eval steps run it in their post phase
@@ -814,21 +851,19 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         side([&](cudaStream_t sd) {
             roots(sd);
             SPD_CUDA(cudaEventRecord(ev_roots_, sd));
-            phi(sd);
-            SPD_CUDA(cudaEventRecord(ev_phi_, sd));
+            if (train) {
+                dh_index(wd, s, sd);
+                SPD_CUDA(cudaEventRecord(ev_dhidx_, sd));  // the dH index is ready
+            }
         }, 0);
     };
-    static const bool roots_early = [] {
-        const char* e = std::getenv("SPD_ROOTS_EARLY");
-        return e && *e == '1';
-    }();
-    if (!profile_ && roots_early) fork_roots();
     timed("gru_fwd", [&] {
         gru_forward(w, wd, train, [&] {
-            if (profile_ || roots_early) return;
+            if (profile_) return;  // (the index reads the slots the gather sets)
             fork_roots();
         });
     });
+    if (profile_ && train) timed("dh_index", [&] { dh_index(wd, s, st); });
     if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_roots_, 0));
     timed("query_gather", [&] {
         launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
@@ -849,7 +884,6 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         proj_dgrad(tc, s.Q.p, d.ld_Q, WK, ldw, s.Qp.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0, nullptr,
                    0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
     });
-    if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_phi_, 0));
     timed("k_attn_abs_fwd", [&] { attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st); });
     timed("gemm_ctx", [&] {
         proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
@@ -907,8 +941,8 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     const bool tc = cfg_.gemm_mode == 1;
     const float* PW = tc ? params_tc_.p : params_.p;
     SPD_CUDA(cudaStreamWaitEvent(st, ev_zero_, 0));  // gradients cleared (step_body)
-    // dH / dGi / dGh: cleared at step start for the step's first backward;
-    // later local workers reuse the scratch and clear it themselves
+    // dGi / dGh rows past |pending|: cleared at step start for the step's
+    // first backward; later local workers reuse the scratch and clear them
     const bool fresh = scratch_zeroed_;
     scratch_zeroed_ = false;
     timed("head_bwd", [&] {
@@ -947,7 +981,6 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     const int ldw = lay_.att_kv.ld;
     float* GK = G + lay_.att_kv.off;
     float* GV = GK + std::size_t(d.DQ) * ldw;
-    if (!fresh) s.dH.zero(st);
     const std::ptrdiff_t wst = std::ptrdiff_t(dh) * ldw;  // per-head weight slab
     timed("gemm_dxbar", [&] {
         // dW_V,h += dctx_h^T xbar_h ; dxbar_h = dctx_h [W_V,h | b_V,h]
@@ -962,17 +995,25 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     timed("k_attn_abs_bwd", [&] {
         attn_abs_bwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, nullptr, st);
     });
-    // the input-gradient scatter (dH of neighbours, time-encoder partials)
-    // runs beside the dQ GEMMs; gru_bwd and the time-grad reduction wait for it
+    // the attention input gradients — memory columns summed per pending row
+    // (k_dh_pull, deterministic, tgn_dh.cu) and the time-encoder partials —
+    // run beside the dQ GEMMs; the GRU backward and the time-grad reduction
+    // wait for them
     auto fork_x = [&] {
         if (profile_) {
-            timed("attn_bwd_x", [&] { attn_abs_bwd_x(wd, d, R, s, attn_part, st); });
-        } else {
-            side([&](cudaStream_t sd) {
-                attn_abs_bwd_x(wd, d, R, s, attn_part, sd);
-                SPD_CUDA(cudaEventRecord(ev_bwdx_, sd));
-            });
+            timed("dh_pull", [&] { dh_pull(d, s, st); });
+            timed("attn_time_grad", [&] { attn_time_grad(d, R, P + lay_.time_w, P + lay_.time_b, s, attn_part, st); });
+            return;
         }
+        side([&](cudaStream_t sd) {
+            SPD_CUDA(cudaStreamWaitEvent(sd, ev_dhidx_, 0));  // the dH reader index
+            dh_pull(d, s, sd);
+            SPD_CUDA(cudaEventRecord(ev_pull_, sd));
+        });
+        side([&](cudaStream_t sd) {
+            attn_time_grad(d, R, P + lay_.time_w, P + lay_.time_b, s, attn_part, sd);
+            SPD_CUDA(cudaEventRecord(ev_bwdx_, sd));
+        });
     };
     auto fork_wk = [&] {
         // dW_K,h += Q_h^T dQp_h
@@ -994,23 +1035,22 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         proj_dgrad(tc, s.dQ.p, d.ld_Q, PW + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
                    d.DQ, nullptr, st);
     });
-    timed("root_time_bwd", [&] {
-        launch(tgnk::k_root_grad, s.troot_blocks, dim3(32, 8), 0, st, wd, d, R, s.roots.p, s.dq_in.p,
-               s.dm_in.p, P + lay_.time_b, s.trows, s.dH.p, s.tpart.p);
-        if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_bwdx_, 0));  // dH, attention partials
-        // the time-encoder gradient is next read by the all-reduce: side stream
-        side([&](cudaStream_t sd) {
-            launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, sd, d.T, s.troot_blocks + s.tattn_blocks,
-                   s.tpart.p, tgrad_.p);
-        });
+    // root-side time-encoder partials and their reduction with the attention
+    // partials: only the all-reduce reads the result, so off the critical path
+    side([&](cudaStream_t sd) {
+        launch(tgnk::k_root_grad, s.troot_blocks, dim3(32, 8), 0, sd, d, R,
+               static_cast<const float*>(s.dq_in.p), P + lay_.time_b, s.trows, s.tpart.p);
+        if (!profile_) SPD_CUDA(cudaStreamWaitEvent(sd, ev_bwdx_, 0));
+        launch(tgnk::k_time_grad_final, 2 * d.T, 256, 0, sd, d.T, s.troot_blocks + s.tattn_blocks,
+               s.tpart.p, tgrad_.p);
     });
     timed("gru_bwd", [&] {
         if (tc && !fresh) {  // the TC weight-grad reads whole K blocks: rows >= |pending| must be 0
             s.dGi.zero(st);
             s.dGh.zero(st);
         }
-        launch(tgnk::k_gru_bwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, st, 
-            wd, d, s.dH.p, s.gsave.p, s.h_gru.p, s.dGi.p, s.dGh.p);
+        if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_pull_, 0));  // dH chunk partials
+        gru_bwd_dh(wd, d, s, st);
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
                    3 * d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
@@ -1278,10 +1318,9 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
         Scratch& s = *s_;
         tgnk::ZeroList z{};
         z.p[0] = grads_.p; z.n[0] = lay_.total;
-        z.p[1] = s.dH.p; z.n[1] = s.dH.n;
         if (cfg_.gemm_mode == 1) {  // TC weight grads read whole K blocks of dGi/dGh
-            z.p[2] = s.dGi.p; z.n[2] = s.dGi.n;
-            z.p[3] = s.dGh.p; z.n[3] = s.dGh.n;
+            z.p[1] = s.dGi.p; z.n[1] = s.dGi.n;
+            z.p[2] = s.dGh.p; z.n[2] = s.dGh.n;
         }
         z.d = tgrad_.p; z.nd = std::size_t(2) * ld4(lay_.T);
         std::size_t mx = z.nd;

@@ -220,8 +220,8 @@ def test_seek_positions_schedule_mid_epoch():
 def test_graph_replay_matches_eager(gemm_mode):
     """Regular steps replay a captured CUDA graph; the per-step control words
     (batch start, negative base, Adam corrections) live on the device, so the
-    replayed trajectory equals the eagerly launched one (up to float-atomic
-    ordering in the memory-gradient scatter)."""
+    replayed trajectory equals the eagerly launched one — bit for bit, since
+    every reduction of the step has a fixed order."""
     _, _, pa, subs = partitioned(parts=2, nodes=200, edges=3000)
     cfg = small_cfg(batch_size=50, gemm_mode=gemm_mode)
     out = []
@@ -229,16 +229,36 @@ def test_graph_replay_matches_eager(gemm_mode):
         tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
         tr.set_graph(graph)
         losses = [tr.run_epoch(ep) for ep in range(2)]
-        out.append((np.array(losses), tr.params(), tr.memory(0)[0], tr.memory(1)[1]))
+        out.append((np.array(losses), tr.params(), tr.memory(0), tr.memory(1)))
     (l0, p0, m0, u0), (l1, p1, m1, u1) = out
-    # two runs differ only by float-atomic ordering; in TF32 mode the tf32
-    # rounding of intermediate activations turns that into ~3e-3 of drift
-    # over 2 epochs, so each mode gets its own trajectory bar (a replay bug —
-    # wrong batch, stale control words — moves everything by O(1))
-    tol = TOL_TRAJ if gemm_mode == 0 else TOL_TF32
-    assert np.allclose(l0, l1, rtol=1e-3), (l0, l1)
-    assert rel_err(p1, p0) < tol and rel_err(m1, m0) < tol, (rel_err(p1, p0), rel_err(m1, m0))
-    assert np.array_equal(u0, u1)
+    assert np.array_equal(l0, l1), (l0, l1)
+    assert np.array_equal(p0, p1)
+    for a, b in ((m0, m1), (u0, u1)):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("gemm_mode", [0, 1])
+def test_training_is_deterministic(gemm_mode):
+    """Two trainings from the same inputs and seeds are bit-identical (the
+    memory-row gradient is a fixed-order reduction, tgn_dh.cu; every other
+    sum already was): the per-step losses, parameters, Adam-updated weights
+    and memory states. Hubs make many neighbour occurrences share a pending
+    row, the case float atomics made order-dependent."""
+    _, _, pa, subs = partitioned(parts=2, nodes=300, edges=12000)
+    cfg = small_cfg(batch_size=400, d_mem=100, d_time=100, d_edge=20, n_neighbors=10,
+                    gemm_mode=gemm_mode)
+    runs = []
+    for _ in range(2):
+        tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+        tr.begin_epoch(0)
+        losses = [tr.step() for _ in range(min(8, tr.epoch_steps()))]
+        runs.append((np.array(losses), tr.params(), tr.grads(), tr.memory(0), tr.memory(1)))
+        tr.close()
+    (l0, p0, g0, a0, b0), (l1, p1, g1, a1, b1) = runs
+    assert np.array_equal(l0, l1)
+    assert np.array_equal(p0, p1) and np.array_equal(g0, g1)
+    for x, y in ((a0, a1), (b0, b1)):
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
 
 
 def test_shuffle_combine_rebind_matches_oracle():
