@@ -858,14 +858,6 @@ class TGNTrainer:
     def set_debug(self, on: bool = True):
         _check(lib.spd_tgn_set_debug(self._h, int(on)))
 
-    def debug_scratch(self, name: str) -> np.ndarray:
-        """Copy of a per-step scratch buffer (x_gru, h_gru, Gi, Gh, mem_new, gsave)."""
-        n = u64()
-        _check(lib.spd_tgn_debug_scratch(self._h, name.encode(), None, 0, C.byref(n)))
-        out = np.zeros(n.value, np.float32)
-        _check(lib.spd_tgn_debug_scratch(self._h, name.encode(), ptr(out, f32), n.value, C.byref(n)))
-        return out
-
     def set_gemm_mode(self, mode: int):
         """0 = FP32 FFMA everywhere, 1 = tcgen05 TF32 GRU/attention projections."""
         _check(lib.spd_tgn_set_gemm_mode(self._h, int(mode)))

@@ -142,7 +142,6 @@ _SIGS = {
     "spd_tgn_sync": (i32, [P]),
     "spd_tgn_set_graph": (i32, [P, i32]),
     "spd_tgn_set_gemm_mode": (i32, [P, i32]),
-    "spd_tgn_debug_scratch": (i32, [P, C.c_char_p, pf32, u64, pu64]),
     "spd_tgn_set_profile": (i32, [P, i32]),
     "spd_edge_feature": (f32, [u64, u64, u32]),
 }

@@ -360,6 +360,10 @@ spd_status spd_tgn_set_graph(spd_tgn_trainer* t, int32_t on);
  * projections): parameters, optimiser state and memory carry over; captured
  * step graphs are rebuilt. */
 spd_status spd_tgn_set_gemm_mode(spd_tgn_trainer* t, int32_t mode);
+/* Debug: copy of the per-step scratch buffer `name` (x_gru, h_gru, Gi, Gh,
+ * mem_new, gsave) into out[0, cap); *n = its element count. */
+spd_status spd_tgn_debug_scratch(spd_tgn_trainer* t, const char* name, float* out, uint64_t cap,
+                                 uint64_t* n);
 /* Per-phase times (ms, CUDA events on the trainer's stream) of the last step. */
 spd_status spd_tgn_kernel_times(const spd_tgn_trainer* t, float* ms, int32_t* n_kernels,
                                 char* names, int32_t name_stride, int32_t cap);

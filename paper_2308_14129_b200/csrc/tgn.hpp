@@ -134,6 +134,9 @@ public:
     Worker& worker(int w);
     void get_memory(int w, float* mem, double* lu);
     void set_memory(int w, const float* mem, const double* lu);
+    // copy of a per-step scratch buffer (debugging / tests): names x_gru,
+    // h_gru, Gi, Gh, mem_new, gsave; returns the element count
+    std::size_t debug_scratch(const char* name, float* out, std::size_t cap);
     void last_step(int w, std::uint64_t* b, float* emb, std::uint32_t* negs, std::uint32_t* nbr,
                    float* loss);
     const StepTimes& times() const { return times_; }

@@ -228,18 +228,25 @@ __device__ __forceinline__ void fill_cos(const Dims& d, int lane, int c_n, doubl
         tw[i] = ok ? *reinterpret_cast<const float4*>(time_w + o) : z4();
         tb[i] = ok ? *reinterpret_cast<const float4*>(time_b + o) : z4();
     }
+    // two neighbours per pass: 8 independent phase chains per lane
 #pragma unroll 1
-    for (int j = 0; j < c_n; ++j) {
-        const double dt = __shfl_sync(0xffffffffu, m_dt, j);
-        unsigned char* row = xs + (std::size_t)j * RB;
+    for (int j0 = 0; j0 < c_n; j0 += 2) {
+        const int j1 = j0 + 1 < c_n ? j0 + 1 : j0;
+        const double dt0 = __shfl_sync(0xffffffffu, m_dt, j0);
+        const double dt1 = __shfl_sync(0xffffffffu, m_dt, j1);
+        unsigned char* row0 = xs + (std::size_t)j0 * RB;
+        unsigned char* row1 = xs + (std::size_t)j1 * RB;
 #pragma unroll
         for (int i = 0; i < S::N; ++i) {
             if (S::region(i) != 1) continue;
             const int o = 4 * (lane + 32 * S::local(i));
             if (o >= d.T) continue;
-            const float c0 = time_cos(tw[i].x, tb[i].x, dt), c1 = time_cos(tw[i].y, tb[i].y, dt);
-            const float c2 = time_cos(tw[i].z, tb[i].z, dt), c3 = time_cos(tw[i].w, tb[i].w, dt);
-            *reinterpret_cast<float4*>(row + 4 * (d.D + o)) = make_float4(c0, c1, c2, c3);
+            const float a0 = time_cos(tw[i].x, tb[i].x, dt0), a1 = time_cos(tw[i].y, tb[i].y, dt0);
+            const float a2 = time_cos(tw[i].z, tb[i].z, dt0), a3 = time_cos(tw[i].w, tb[i].w, dt0);
+            const float b0 = time_cos(tw[i].x, tb[i].x, dt1), b1 = time_cos(tw[i].y, tb[i].y, dt1);
+            const float b2 = time_cos(tw[i].z, tb[i].z, dt1), b3 = time_cos(tw[i].w, tb[i].w, dt1);
+            *reinterpret_cast<float4*>(row0 + 4 * (d.D + o)) = make_float4(a0, a1, a2, a3);
+            *reinterpret_cast<float4*>(row1 + 4 * (d.D + o)) = make_float4(b0, b1, b2, b3);
         }
     }
 }

@@ -97,6 +97,13 @@ spd_status spd_tgn_set_memory(spd_tgn_trainer* t, int32_t worker, const float* m
 }
 spd_status spd_tgn_set_debug(spd_tgn_trainer* t, int32_t on) { GUARD({ t->t->set_debug(on != 0); }); }
 spd_status spd_tgn_set_graph(spd_tgn_trainer* t, int32_t on) { GUARD({ t->t->set_graph(on != 0); }); }
+spd_status spd_tgn_debug_scratch(spd_tgn_trainer* t, const char* name, float* out, uint64_t cap,
+                                 uint64_t* n) {
+    GUARD({
+        const std::size_t m = t->t->debug_scratch(name, out, cap);
+        if (n) *n = m;
+    });
+}
 spd_status spd_tgn_set_gemm_mode(spd_tgn_trainer* t, int32_t mode) {
     GUARD({
         if (mode != 0 && mode != 1) usage_error("gemm_mode must be 0 or 1");

@@ -10,18 +10,22 @@
 //
 //   1. index (side stream, during the forward; needs only the neighbour lists
 //      and the slot map): a stable counting sort of the entries by slot, in
-//      three kernels — per-block slot histograms, a column scan over blocks +
-//      exclusive scans over slots, and a scatter whose per-block ranks are
-//      assigned warp by warp in entry order. Lists: occurrence entries
-//      (r * K + j) and root entries (r), each grouped by slot in ascending
-//      entry order; each slot's occurrence list cut into chunks of 32.
-//   2. k_dh_pull (backward, beside the dQ GEMMs): one warp per chunk sums its
-//      occurrences' memory-column gradients
+//      four kernels — per-block slot histograms, a per-slot prefix over the
+//      blocks, exclusive scans over the slots, and a scatter whose per-block
+//      ranks are assigned warp by warp in entry order. Lists: occurrence
+//      entries (r * K + j) and root entries (r), each grouped by slot in
+//      ascending entry order, each slot's lists cut into chunks of 16.
+//   2. k_dh_pull (backward, beside the dQ GEMMs): one warp per occurrence
+//      chunk sums its entries' memory-column gradients
 //        dx_j = sum_h a_hj dxbar_h + ds_hj q'_h          (tgn_attn.cu)
-//      in list order into a chunk partial row.
-//   3. k_gru_bwd_dh: one warp per pending row sums the row's chunk partials in
-//      chunk order, then its root entries' dq_in / dm_in memory columns in
-//      list order, and runs the GRUCell backward on the result.
+//      in list order into a chunk partial row; k_dh_pull_root (after the
+//      query data-gradient GEMM) does the same for the root chunks' query /
+//      merge memory columns (dq_in, dm_in).
+//   3. k_gru_bwd_dh: one warp per pending row sums the row's chunk partials
+//      in chunk order (occurrence chunks, then root chunks) and runs the
+//      GRUCell backward on the result.
+// Chunks bound every serial chain (a hub row read by thousands of entries is
+// summed 16 entries per warp, then ~entries/16 partials).
 // Semantics: oracle/tgn_oracle.py (autograd); only the summation order is the
 // kernel's own — and it is the same every run.
 #include "pdl.cuh"
@@ -66,42 +70,56 @@ __global__ void __launch_bounds__(kDhBlock) k_dh_hist(WorkerDev w, DhIndex x) {
     for (int u = threadIdx.x; u < x.U_cap; u += blockDim.x) out[u] = h_s[u];
 }
 
-// One block: hist[b][u] -> exclusive prefix over the blocks of its list
-// (occurrence blocks, then root blocks); per-slot totals -> exclusive scans
-// off_occ / off_root; occurrence chunks of 32 per slot -> chunk_off, and the
-// chunk -> (slot, first list position) map. Thread t owns the consecutive
+// Per slot u (one thread each): hist[b][u] -> exclusive prefix over the
+// blocks of its list (occurrence blocks, then root blocks), in place; the
+// two totals go to off_occ[u] / off_root[u] for k_dh_scan.
+__global__ void __launch_bounds__(128) k_dh_colscan(DhIndex x) {
+    pdl_entry();
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= x.U_cap) return;
+    constexpr int G = 16;  // loads in flight per thread
+    int tot[2];
+#pragma unroll
+    for (int list = 0; list < 2; ++list) {
+        const int b0 = list ? x.nb_occ : 0, b1 = list ? x.nb_occ + x.nb_root : x.nb_occ;
+        int run = 0;
+        for (int g = b0; g < b1; g += G) {
+            int v[G];
+#pragma unroll
+            for (int t = 0; t < G; ++t) v[t] = g + t < b1 ? x.hist[(std::size_t)(g + t) * x.U_cap + u] : 0;
+#pragma unroll
+            for (int t = 0; t < G; ++t) {
+                if (g + t < b1) x.hist[(std::size_t)(g + t) * x.U_cap + u] = run;
+                run += v[t];
+            }
+        }
+        tot[list] = run;
+    }
+    x.off_occ[u] = tot[0];
+    x.off_root[u] = tot[1];
+}
+
+// One block: per-slot totals -> exclusive scans off_occ / off_root and the
+// chunk offsets of both lists (chunks of kDhChunk per slot), plus the
+// chunk -> (slot, first list position) maps. Thread t owns the consecutive
 // slots [t * per, (t + 1) * per).
 __global__ void __launch_bounds__(1024) k_dh_scan(DhIndex x) {
     pdl_entry();
-    __shared__ int warp_sums[3][32];
+    __shared__ int warp_sums[4][32];
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int per = (x.U_cap + blockDim.x - 1) / blockDim.x;
     const int u0 = min(x.U_cap, t * per), u1 = min(x.U_cap, u0 + per);
-    int so = 0, sr = 0, sc = 0;
+    int v[4] = {0, 0, 0, 0};  // occurrences, roots, occurrence chunks, root chunks
     for (int u = u0; u < u1; ++u) {
-        int ro = 0, rr = 0;
-        for (int b = 0; b < x.nb_occ; ++b) {
-            int* p = x.hist + (std::size_t)b * x.U_cap + u;
-            const int v = *p;
-            *p = ro;
-            ro += v;
-        }
-        for (int b = x.nb_occ; b < x.nb_occ + x.nb_root; ++b) {
-            int* p = x.hist + (std::size_t)b * x.U_cap + u;
-            const int v = *p;
-            *p = rr;
-            rr += v;
-        }
-        x.off_occ[u] = ro;  // totals for now; offsets below
-        x.off_root[u] = rr;
-        so += ro;
-        sr += rr;
-        sc += (ro + kDhChunk - 1) / kDhChunk;
+        const int to = x.off_occ[u], tr = x.off_root[u];
+        v[0] += to;
+        v[1] += tr;
+        v[2] += (to + kDhChunk - 1) / kDhChunk;
+        v[3] += (tr + kDhChunk - 1) / kDhChunk;
     }
-    // block exclusive scans of the three per-thread sums
-    int v[3] = {so, sr, sc};
+    int ex[4];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < 4; ++q) {
         int incl = v[q];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -109,12 +127,12 @@ __global__ void __launch_bounds__(1024) k_dh_scan(DhIndex x) {
             if (lane >= o) incl += y;
         }
         if (lane == 31) warp_sums[q][wid] = incl;
-        v[q] = incl - v[q];  // exclusive within the warp
+        ex[q] = incl - v[q];  // exclusive within the warp
     }
     __syncthreads();
     if (wid == 0) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < 4; ++q) {
             const int a = lane < (int)(blockDim.x >> 5) ? warp_sums[q][lane] : 0;
             int incl = a;
 #pragma unroll
@@ -126,25 +144,33 @@ __global__ void __launch_bounds__(1024) k_dh_scan(DhIndex x) {
         }
     }
     __syncthreads();
-    int po = v[0] + warp_sums[0][wid], pr = v[1] + warp_sums[1][wid], pc = v[2] + warp_sums[2][wid];
+    int po = ex[0] + warp_sums[0][wid], pr = ex[1] + warp_sums[1][wid];
+    int pc = ex[2] + warp_sums[2][wid], prc = ex[3] + warp_sums[3][wid];
     for (int u = u0; u < u1; ++u) {
         const int to = x.off_occ[u], tr = x.off_root[u];
-        const int ch = (to + kDhChunk - 1) / kDhChunk;
+        const int co = (to + kDhChunk - 1) / kDhChunk, cr = (tr + kDhChunk - 1) / kDhChunk;
         x.off_occ[u] = po;
         x.off_root[u] = pr;
         x.chunk_off[u] = pc;
-        for (int c = 0; c < ch; ++c) {
+        x.rchunk_off[u] = prc;
+        for (int c = 0; c < co; ++c) {
             x.chunk_slot[pc + c] = u;
             x.chunk_start[pc + c] = po + c * kDhChunk;
         }
+        for (int c = 0; c < cr; ++c) {
+            x.rchunk_slot[prc + c] = u;
+            x.rchunk_start[prc + c] = pr + c * kDhChunk;
+        }
         po += to;
         pr += tr;
-        pc += ch;
+        pc += co;
+        prc += cr;
     }
     if (t == (int)blockDim.x - 1) {
         x.off_occ[x.U_cap] = po;
         x.off_root[x.U_cap] = pr;
         x.chunk_off[x.U_cap] = pc;
+        x.rchunk_off[x.U_cap] = prc;
     }
 }
 
@@ -178,7 +204,8 @@ __global__ void __launch_bounds__(kDhBlock) k_dh_scatter(WorkerDev w, DhIndex x)
 }
 
 // One warp per occurrence chunk: the chunk's memory-column gradients summed in
-// list order into partial[c] (D floats). NM = ceil(D / 128) float4 per lane.
+// list order into partial[c] (D floats). NM = ceil(D / 128) float4 per lane;
+// entries in groups of G whose loads are all issued before the first FMA.
 template <int NM, int HMAX>
 __global__ void __launch_bounds__(256) k_dh_pull(DhIndex x, Dims d, const float* alpha,
                                                  const float* dsc, const float* dxbar,
@@ -187,34 +214,46 @@ __global__ void __launch_bounds__(256) k_dh_pull(DhIndex x, Dims d, const float*
     const int c = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (c >= x.chunk_off[x.U_cap]) return;
     const int u = x.chunk_slot[c], p0 = x.chunk_start[c];
-    const int p1 = min(p0 + kDhChunk, x.off_occ[u + 1]);
+    const int n = min(kDhChunk, x.off_occ[u + 1] - p0);
     float4 acc[NM];
 #pragma unroll
     for (int i = 0; i < NM; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int ldr = d.H * d.ld_p;
-    // entry ids of the chunk, one per lane, broadcast in order
-    const int my_e = p0 + lane < p1 ? x.list_occ[p0 + lane] : 0;
-#pragma unroll 2
-    for (int p = 0; p < p1 - p0; ++p) {
-        const int e = __shfl_sync(0xffffffffu, my_e, p);
-        const int r = e / d.K, j = e - r * d.K;
-        float a[HMAX], s[HMAX];
+    const int my_e = lane < n ? x.list_occ[p0 + lane] : 0;  // entry ids, broadcast in order
+    constexpr int G = 8 / HMAX;
+    for (int g = 0; g < n; g += G) {
+        float a[G][HMAX], s[G][HMAX];
+        float4 gx[G][HMAX][NM], qx[G][HMAX][NM];
 #pragma unroll
-        for (int h = 0; h < HMAX; ++h) {
-            a[h] = h < d.H ? alpha[((std::size_t)r * d.H + h) * d.K + j] : 0.f;
-            s[h] = h < d.H ? dsc[((std::size_t)r * d.H + h) * d.K + j] : 0.f;
+        for (int t = 0; t < G; ++t) {
+            const int e = __shfl_sync(0xffffffffu, my_e, min(g + t, 31));
+            const bool ok = g + t < n;
+            const int r = e / d.K, j = e - r * d.K;
+#pragma unroll
+            for (int h = 0; h < HMAX; ++h) {
+                const bool okh = ok && h < d.H;
+                a[t][h] = okh ? alpha[((std::size_t)r * d.H + h) * d.K + j] : 0.f;
+                s[t][h] = okh ? dsc[((std::size_t)r * d.H + h) * d.K + j] : 0.f;
+#pragma unroll
+                for (int i = 0; i < NM; ++i) {
+                    const int col = 4 * (lane + 32 * i);
+                    const bool okc = okh && col < d.D;
+                    const std::size_t o = (std::size_t)r * ldr + (std::size_t)h * d.ld_p + col;
+                    gx[t][h][i] = okc ? f4(dxbar + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    qx[t][h][i] = okc ? f4(Qp + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
         }
-        const float* gx = dxbar + (std::size_t)r * ldr;
-        const float* qx = Qp + (std::size_t)r * ldr;
 #pragma unroll
-        for (int i = 0; i < NM; ++i) {
-            const int col = 4 * (lane + 32 * i);
-            if (col < d.D) {
+        for (int t = 0; t < G; ++t) {
+            if (g + t >= n) break;
 #pragma unroll
-                for (int h = 0; h < HMAX; ++h) {
-                    if (h >= d.H) break;
-                    fma4(acc[i], a[h], f4(gx + (std::size_t)h * d.ld_p + col));
-                    fma4(acc[i], s[h], f4(qx + (std::size_t)h * d.ld_p + col));
+            for (int h = 0; h < HMAX; ++h) {
+                if (h >= d.H) break;
+#pragma unroll
+                for (int i = 0; i < NM; ++i) {
+                    fma4(acc[i], a[t][h], gx[t][h][i]);
+                    fma4(acc[i], s[t][h], qx[t][h][i]);
                 }
             }
         }
@@ -227,42 +266,89 @@ __global__ void __launch_bounds__(256) k_dh_pull(DhIndex x, Dims d, const float*
     }
 }
 
-// One warp per pending row u: dH = chunk partials (chunk order) + root entries
-// (list order: query [s_root | phi(0)] and merge [attn | s_root] memory
-// columns), then the GRUCell backward (gate order r, z, n) to the gate
-// pre-activation gradients dGi (input side) and dGh (hidden side).
+// One warp per root chunk: the roots' query [s_root | phi(0)] and merge
+// [attn | s_root] memory-column gradients summed in list order into
+// rpartial[c].
+template <int NM>
+__global__ void __launch_bounds__(256) k_dh_pull_root(DhIndex x, Dims d, const float* dq_in,
+                                                      const float* dm_in, float* rpartial) {
+    pdl_entry();
+    const int c = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (c >= x.rchunk_off[x.U_cap]) return;
+    const int u = x.rchunk_slot[c], p0 = x.rchunk_start[c];
+    const int n = min(kDhChunk, x.off_root[u + 1] - p0);
+    float4 acc[NM];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int my_r = lane < n ? x.list_root[p0 + lane] : 0;
+    constexpr int G = 4;
+    for (int g = 0; g < n; g += G) {
+        float4 qa[G][NM], ma[G][NM];
+#pragma unroll
+        for (int t = 0; t < G; ++t) {
+            const int r = __shfl_sync(0xffffffffu, my_r, min(g + t, 31));
+#pragma unroll
+            for (int i = 0; i < NM; ++i) {
+                const int col = 4 * (lane + 32 * i);
+                const bool ok = g + t < n && col < d.D;
+                qa[t][i] = ok ? f4(dq_in + (std::size_t)r * d.ld_q + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+                ma[t][i] = ok ? f4(dm_in + (std::size_t)r * d.ld_m + d.DQ + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < G; ++t) {
+            if (g + t >= n) break;
+#pragma unroll
+            for (int i = 0; i < NM; ++i)
+                add4(acc[i], make_float4(qa[t][i].x + ma[t][i].x, qa[t][i].y + ma[t][i].y,
+                                         qa[t][i].z + ma[t][i].z, qa[t][i].w + ma[t][i].w));
+        }
+    }
+    float* o = rpartial + (std::size_t)c * d.D;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+        const int col = 4 * (lane + 32 * i);
+        if (col < d.D) *reinterpret_cast<float4*>(o + col) = acc[i];
+    }
+}
+
+// Sum of the chunk partials [c0, c1) in chunk order, 4 loads in flight.
+template <int NM>
+__device__ __forceinline__ void sum_chunks(float4 (&g)[NM], const float* part, int c0, int c1,
+                                           int D, int lane) {
+    for (int c = c0; c < c1; c += 4) {
+        float4 v[4][NM];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int i = 0; i < NM; ++i) {
+                const int col = 4 * (lane + 32 * i);
+                v[t][i] = c + t < c1 && col < D ? f4(part + (std::size_t)(c + t) * D + col)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (c + t < c1)
+#pragma unroll
+                for (int i = 0; i < NM; ++i) add4(g[i], v[t][i]);
+    }
+}
+
+// One warp per pending row u: dH = occurrence chunk partials then root chunk
+// partials (chunk order), then the GRUCell backward (gate order r, z, n) to
+// the gate pre-activation gradients dGi (input side) and dGh (hidden side).
 template <int NM>
 __global__ void __launch_bounds__(256) k_gru_bwd_dh(WorkerDev w, Dims d, DhIndex x,
-                                                    const float* partial, const float* dq_in,
-                                                    const float* dm_in, const float* save,
-                                                    float* dGi, float* dGh) {
+                                                    const float* partial, const float* rpartial,
+                                                    const float* save, float* dGi, float* dGh) {
     pdl_entry();
     const int u = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (u >= *w.nU) return;
     float4 g[NM];
 #pragma unroll
     for (int i = 0; i < NM; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int c0 = x.chunk_off[u], c1 = x.chunk_off[u + 1];
-    for (int c = c0; c < c1; ++c) {
-#pragma unroll
-        for (int i = 0; i < NM; ++i) {
-            const int col = 4 * (lane + 32 * i);
-            if (col < d.D) add4(g[i], f4(partial + (std::size_t)c * d.D + col));
-        }
-    }
-    const int q0 = x.off_root[u], q1 = x.off_root[u + 1];
-    for (int q = q0; q < q1; ++q) {
-        const int r = x.list_root[q];
-#pragma unroll
-        for (int i = 0; i < NM; ++i) {
-            const int col = 4 * (lane + 32 * i);
-            if (col < d.D) {
-                const float4 a = f4(dq_in + (std::size_t)r * d.ld_q + col);
-                const float4 b = f4(dm_in + (std::size_t)r * d.ld_m + d.DQ + col);
-                add4(g[i], make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
-            }
-        }
-    }
+    sum_chunks<NM>(g, partial, x.chunk_off[u], x.chunk_off[u + 1], d.D, lane);
+    sum_chunks<NM>(g, rpartial, x.rchunk_off[u], x.rchunk_off[u + 1], d.D, lane);
     const float* sv = save + (std::size_t)u * 4 * d.D;
     const float* hrow = w.mem + (std::size_t)w.pU[u] * d.D;  // exact h (h_gru may be tf32-rounded)
     float* gi = dGi + (std::size_t)u * d.ld_g;
@@ -305,10 +391,12 @@ template __global__ void k_dh_pull<2, 2>(DhIndex, Dims, const float*, const floa
                                          const float*, float*);
 template __global__ void k_dh_pull<2, 4>(DhIndex, Dims, const float*, const float*, const float*,
                                          const float*, float*);
+template __global__ void k_dh_pull_root<1>(DhIndex, Dims, const float*, const float*, float*);
+template __global__ void k_dh_pull_root<2>(DhIndex, Dims, const float*, const float*, float*);
 template __global__ void k_gru_bwd_dh<1>(WorkerDev, Dims, DhIndex, const float*, const float*,
-                                         const float*, const float*, float*, float*);
+                                         const float*, float*, float*);
 template __global__ void k_gru_bwd_dh<2>(WorkerDev, Dims, DhIndex, const float*, const float*,
-                                         const float*, const float*, float*, float*);
+                                         const float*, float*, float*);
 
 }  // namespace tgnk
 }  // namespace spd

@@ -60,31 +60,37 @@ struct WorkerDev {
 // (tgn_dh.cu). Entries: occurrence e = r * K + j for e < RK, then (from block
 // nb_occ on) root r = e - nb_occ * kDhBlock.
 constexpr int kDhBlock = 1024;  // entries per histogram / scatter block
-constexpr int kDhChunk = 32;    // occurrences per k_dh_pull warp
+constexpr int kDhChunk = 16;    // entries per pull warp
 struct DhIndex {
     int RK, K, R, nb_occ, nb_root, U_cap;
     const std::uint32_t* nbr_node;
     const int* cnt;
     const std::uint32_t* roots;
     int* hist;          // [nb_occ + nb_root][U_cap] -> per-block exclusive prefixes
-    int* off_occ;       // [U_cap + 1]
-    int* off_root;      // [U_cap + 1]
-    int* chunk_off;     // [U_cap + 1]
-    int* chunk_slot;    // [RK / kDhChunk + U_cap]
-    int* chunk_start;   // [RK / kDhChunk + U_cap]
+    int* off_occ;       // [U_cap + 1] occurrence list offsets per slot
+    int* off_root;      // [U_cap + 1] root list offsets per slot
+    int* chunk_off;     // [U_cap + 1] first occurrence chunk per slot
+    int* rchunk_off;    // [U_cap + 1] first root chunk per slot
+    int* chunk_slot;    // [max occurrence chunks] slot of the chunk
+    int* chunk_start;   //                         first list position
+    int* rchunk_slot;   // [max root chunks]
+    int* rchunk_start;
     int* list_occ;      // [RK]
     int* list_root;     // [R]
 };
 __global__ void k_dh_hist(WorkerDev w, DhIndex x);
+__global__ void k_dh_colscan(DhIndex x);
 __global__ void k_dh_scan(DhIndex x);
 __global__ void k_dh_scatter(WorkerDev w, DhIndex x);
 template <int NM, int HMAX>
 __global__ void k_dh_pull(DhIndex x, Dims d, const float* alpha, const float* dsc,
                           const float* dxbar, const float* Qp, float* partial);
 template <int NM>
+__global__ void k_dh_pull_root(DhIndex x, Dims d, const float* dq_in, const float* dm_in,
+                               float* rpartial);
+template <int NM>
 __global__ void k_gru_bwd_dh(WorkerDev w, Dims d, DhIndex x, const float* partial,
-                             const float* dq_in, const float* dm_in, const float* save,
-                             float* dGi, float* dGh);
+                             const float* rpartial, const float* save, float* dGi, float* dGh);
 
 // --- kernels (definitions in tgn_kernels.cu) -------------------------------
 __global__ void k_init_aug(float* buf, int rows, int cols, int ld);

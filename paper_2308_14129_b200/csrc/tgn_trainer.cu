@@ -111,11 +111,11 @@ struct Scratch {
     DevBuf<float> ws;
     DevBuf<double> tpart;
     // deterministic dH reduction (tgn_dh.cu): reader index + chunk partials
-    DevBuf<int> dh_hist, dh_off_occ, dh_off_root, dh_chunk_off, dh_chunk_slot, dh_chunk_start,
-        dh_list_occ, dh_list_root;
-    DevBuf<float> dh_partial;
+    DevBuf<int> dh_hist, dh_off_occ, dh_off_root, dh_chunk_off, dh_rchunk_off, dh_chunk_slot,
+        dh_chunk_start, dh_rchunk_slot, dh_rchunk_start, dh_list_occ, dh_list_root;
+    DevBuf<float> dh_partial, dh_rpartial;
     tgnk::DhIndex dh{};
-    int dh_max_chunks = 0;
+    int dh_max_chunks = 0, dh_max_rchunks = 0;
     DevBuf<float> loss;  // per local worker
     int trows = 0, troot_blocks = 0, tattn_blocks = 0;  // time-grad partial blocks
 };
@@ -318,6 +318,7 @@ void dh_index(const tgnk::WorkerDev& wd, const Scratch& s, cudaStream_t st) {
     }
     const unsigned nb = unsigned(s.dh.nb_occ + s.dh.nb_root);
     launch(tgnk::k_dh_hist, nb, tgnk::kDhBlock, sm, st, wd, s.dh);
+    launch(tgnk::k_dh_colscan, unsigned((s.dh.U_cap + 127) / 128), 128, 0, st, s.dh);
     launch(tgnk::k_dh_scan, 1, 1024, 0, st, s.dh);
     launch(tgnk::k_dh_scatter, nb, tgnk::kDhBlock, sm, st, wd, s.dh);
 }
@@ -332,12 +333,21 @@ void dh_pull(const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
     if (nm == 1) d.H <= 2 ? go(tgnk::k_dh_pull<1, 2>) : go(tgnk::k_dh_pull<1, 4>);
     else d.H <= 2 ? go(tgnk::k_dh_pull<2, 2>) : go(tgnk::k_dh_pull<2, 4>);
 }
+void dh_pull_root(const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
+    const unsigned grid = unsigned((std::size_t(s.dh_max_rchunks) * 32 + 255) / 256);
+    auto go = [&](auto k) {
+        launch(k, grid, 256, 0, st, s.dh, d, static_cast<const float*>(s.dq_in.p),
+               static_cast<const float*>(s.dm_in.p), s.dh_rpartial.p);
+    };
+    if ((d.D + 127) / 128 == 1) go(tgnk::k_dh_pull_root<1>);
+    else go(tgnk::k_dh_pull_root<2>);
+}
 void gru_bwd_dh(const tgnk::WorkerDev& wd, const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
     const unsigned grid = unsigned((std::size_t(s.U) * 32 + 255) / 256);
     auto go = [&](auto k) {
         launch(k, grid, 256, 0, st, wd, d, s.dh, static_cast<const float*>(s.dh_partial.p),
-               static_cast<const float*>(s.dq_in.p), static_cast<const float*>(s.dm_in.p),
-               static_cast<const float*>(s.gsave.p), s.dGi.p, s.dGh.p);
+               static_cast<const float*>(s.dh_rpartial.p), static_cast<const float*>(s.gsave.p),
+               s.dGi.p, s.dGh.p);
     };
     if ((d.D + 127) / 128 == 1) go(tgnk::k_gru_bwd_dh<1>);
     else go(tgnk::k_gru_bwd_dh<2>);
@@ -480,15 +490,22 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         x.RK = RK; x.K = d.K; x.R = R; x.U_cap = U;
         x.nb_occ = (RK + tgnk::kDhBlock - 1) / tgnk::kDhBlock;
         x.nb_root = (R + tgnk::kDhBlock - 1) / tgnk::kDhBlock;
+        // every slot adds at most one partly filled chunk per list
         s.dh_max_chunks = RK / tgnk::kDhChunk + U + 1;
+        s.dh_max_rchunks = R / tgnk::kDhChunk + U + 1;
         s.dh_hist.alloc(std::size_t(x.nb_occ + x.nb_root) * U);
-        s.dh_off_occ.alloc(U + 1); s.dh_off_root.alloc(U + 1); s.dh_chunk_off.alloc(U + 1);
+        s.dh_off_occ.alloc(U + 1); s.dh_off_root.alloc(U + 1);
+        s.dh_chunk_off.alloc(U + 1); s.dh_rchunk_off.alloc(U + 1);
         s.dh_chunk_slot.alloc(s.dh_max_chunks); s.dh_chunk_start.alloc(s.dh_max_chunks);
+        s.dh_rchunk_slot.alloc(s.dh_max_rchunks); s.dh_rchunk_start.alloc(s.dh_max_rchunks);
         s.dh_list_occ.alloc(RK); s.dh_list_root.alloc(R);
         s.dh_partial.alloc(std::size_t(s.dh_max_chunks) * D);
+        s.dh_rpartial.alloc(std::size_t(s.dh_max_rchunks) * D);
         x.hist = s.dh_hist.p; x.off_occ = s.dh_off_occ.p; x.off_root = s.dh_off_root.p;
-        x.chunk_off = s.dh_chunk_off.p; x.chunk_slot = s.dh_chunk_slot.p;
-        x.chunk_start = s.dh_chunk_start.p; x.list_occ = s.dh_list_occ.p; x.list_root = s.dh_list_root.p;
+        x.chunk_off = s.dh_chunk_off.p; x.rchunk_off = s.dh_rchunk_off.p;
+        x.chunk_slot = s.dh_chunk_slot.p; x.chunk_start = s.dh_chunk_start.p;
+        x.rchunk_slot = s.dh_rchunk_slot.p; x.rchunk_start = s.dh_rchunk_start.p;
+        x.list_occ = s.dh_list_occ.p; x.list_root = s.dh_list_root.p;
     }
     s.x_gru.alloc(std::size_t(U) * d.ld_x); init_aug(s.x_gru, U, d.DM, d.ld_x, stream_);
     s.h_gru.alloc(std::size_t(U) * d.ld_h); init_aug(s.h_gru, U, D, d.ld_h, stream_);
@@ -1049,7 +1066,8 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
             s.dGi.zero(st);
             s.dGh.zero(st);
         }
-        if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_pull_, 0));  // dH chunk partials
+        dh_pull_root(d, s, st);
+        if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_pull_, 0));  // occurrence chunk partials
         gru_bwd_dh(wd, d, s, st);
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
                    3 * d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
@@ -1521,6 +1539,22 @@ void TGNTrainer::set_memory(int wid, const float* mem, const double* lu) {
     if (lu) w.lu.upload(lu, w.N, stream_);
     SPD_CUDA(cudaStreamSynchronize(stream_));
 }
+std::size_t TGNTrainer::debug_scratch(const char* name, float* out, std::size_t cap) {
+    DeviceGuard g(device_);
+    Scratch& s = *s_;
+    const std::string n(name ? name : "");
+    const DevBuf<float>* b = n == "x_gru" ? &s.x_gru : n == "h_gru" ? &s.h_gru : n == "Gi" ? &s.Gi
+                             : n == "Gh" ? &s.Gh : n == "mem_new" ? &s.mem_new : n == "gsave" ? &s.gsave
+                             : nullptr;
+    if (!b) usage_error("unknown scratch buffer '" + n + "'");
+    if (out) {
+        SPD_CUDA(cudaDeviceSynchronize());
+        b->download(out, std::min(cap, b->n), stream_);
+        SPD_CUDA(cudaStreamSynchronize(stream_));
+    }
+    return b->n;
+}
+
 void TGNTrainer::last_step(int wid, std::uint64_t* b, float* emb, std::uint32_t* negs,
                            std::uint32_t* nbr, float* loss) {
     Worker& w = worker(wid);
