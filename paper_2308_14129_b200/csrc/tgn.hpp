@@ -169,7 +169,7 @@ private:
     void commit_ctl();
     void step_body(const std::vector<int>& Bs);  // worker steps + all-reduce + Adam (capturable)
     void adam_prepare();
-    void backward(Worker& w, const tgnk::WorkerDev& wd, int B);
+    void backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fused);
     void worker_post(Worker& w);
     void flush_pending(Worker& w);
     void gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
@@ -205,7 +205,8 @@ private:
     cudaEvent_t ev_zfork_ = nullptr, ev_zero_ = nullptr;
     cudaEvent_t ev_bwdx_ = nullptr;  // attention time-encoder partials done
     cudaEvent_t ev_pull_ = nullptr;  // dH chunk partials done (tgn_dh.cu)
-    bool scratch_zeroed_ = false;    // dH/dGi/dGh cleared by this step's k_zero_list
+    bool scratch_zeroed_ = false;    // dGi/dGh cleared by this step's k_zero_list
+    bool head_fits_ = false;         // the fused head (tgn_head.cu) supports these dims
 
     spd_tgn_config cfg_;
     ParamLayout lay_;

@@ -540,6 +540,11 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.tattn_blocks = (R + tgnk::attn_x_roots_per_block() - 1) / tgnk::attn_x_roots_per_block();
     s.tpart.alloc(std::size_t(s.troot_blocks + s.tattn_blocks) * 2 * d.T);
     s.dh.nbr_node = s.nbr_node.p; s.dh.cnt = s.cnt.p; s.dh.roots = s.roots.p;
+    {  // fused head (tgn_head.cu): one 227 KB CTA per 16 events; SPD_FUSED_HEAD=0 disables
+        const char* e = std::getenv("SPD_FUSED_HEAD");
+        head_fits_ = !(e && *e == '0') && d.DQ + d.D <= 320 &&
+                     tgnk::head_smem_bytes(d) <= std::size_t(227) * 1024;
+    }
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
     SPD_CUDA(cudaStreamSynchronize(stream_));
 
@@ -857,6 +862,8 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
                s.root_t.p, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p);
     };
     if (profile_) timed("roots_nbrs", [&] { roots(st); });
+    s.dh.R = R;  // this batch's roots and occurrences (a loop's last batch may be short)
+    s.dh.RK = R * d.K;
     // this batch's last messages into the other pending set (K3): depends only
     // on the batch's events, off the critical path (the GRU below reads the
     // current set); eval steps run it in their post phase
@@ -906,7 +913,29 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
                  nullptr, 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
     });
-    timed("head_fwd", [&] {
+    // gemm_mode 1 training steps: the fused head (tgn_head.cu), ctx -> loss -> dctx
+    const bool fused = train && tc && head_fits_;
+    if (fused) timed("head_fused", [&] {
+        tgnk::HeadArgs h{};
+        h.d = d; h.B = B; h.w = wd; h.ctx = s.ctx.p; h.cnt = s.cnt.p; h.roots = s.roots.p;
+        h.mem_new = s.mem_new.p;
+        h.Wo = PW + lay_.att_o.off; h.ldo = lay_.att_o.ld;
+        h.Wm1 = PW + lay_.mrg1.off; h.ldm1 = lay_.mrg1.ld;
+        h.Wm2 = PW + lay_.mrg2.off; h.ldm2 = lay_.mrg2.ld;
+        h.Wd1 = P + lay_.dec1.off; h.ldd1 = lay_.dec1.ld; h.wd2 = P + lay_.dec2.off;
+        h.m_in = s.m_in.p; h.Z1 = s.Z1.p; h.emb = s.emb.p; h.D1 = s.D1.p; h.dlogit = s.dlogit.p;
+        h.lossv = s.lossv.p; h.logits = s.logits.p; h.dD1 = s.dD1.p; h.d_emb = s.d_emb.p;
+        h.dZ1 = s.dZ1.p; h.dm_in = s.dm_in.p; h.dctx = s.dctx.p;
+        const std::size_t sm = tgnk::head_smem_bytes(d);
+        static std::size_t set = 0;
+        if (sm > set) {
+            SPD_CUDA(cudaFuncSetAttribute(tgnk::k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            set = sm;
+        }
+        const int eb = tgnk::head_events_per_block();
+        launch(tgnk::k_head, unsigned((B + eb - 1) / eb), 256, sm, st, h);
+    });
+    else timed("head_fwd", [&] {
         proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
                  d.DQ + 1, nullptr, st);
         launch(tgnk::k_merge_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, 
@@ -935,7 +964,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     };
     if (train) side(sum_loss);
     else sum_loss(st);
-    if (train) backward(w, wd, B);
+    if (train) backward(w, wd, B, fused);
     // persist this batch's memory update and store its last messages now,
     // while the scratch still holds this worker's rows (K11, K3); the last
     // worker of a training step defers it to step_body (beside the optimizer)
@@ -948,7 +977,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
 
 // Hand-written backward of one worker's batch; weight-gradient GEMMs go to the
 // side stream and are joined before the post phase rewrites their inputs.
-void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
+void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fused) {
     Scratch& s = *s_;
     const auto& d = s.d;
     const int R = 3 * B;
@@ -962,7 +991,24 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     // first backward; later local workers reuse the scratch and clear them
     const bool fresh = scratch_zeroed_;
     scratch_zeroed_ = false;
-    timed("head_bwd", [&] {
+    if (fused) {  // the head's data gradients are done (k_head): its weight gradients only
+        side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off,
+                                               lay_.dec2.ld, 1, d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
+        side([&](cudaStream_t sd) {
+            launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, sd, d, B,
+                   s.emb.p, s.d_in.p);
+            gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
+                       2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd);
+        });
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off,
+                                               lay_.mrg2.ld, d.D, d.D + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off,
+                                               lay_.mrg1.ld, d.D, d.DQ + d.D + 1, R, nullptr, ws_cur_,
+                                               wsn_cur_, sd); });
+        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off,
+                                               lay_.att_o.ld, d.DQ, d.DQ + 1, R, nullptr, ws_cur_,
+                                               wsn_cur_, sd); });
+    } else timed("head_bwd", [&] {
         side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
                    2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
         side([&](cudaStream_t sd) {
