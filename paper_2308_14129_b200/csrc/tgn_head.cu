@@ -165,6 +165,40 @@ __device__ __forceinline__ void zero_cols(float* A, int lda, int c0, int c1) {
 }
 
 __device__ __forceinline__ float softplusf_(float x) { return x > 20.f ? x : log1pf(expf(x)); }
+
+// FP32 FFMA over the 48 block rows, register-tiled: thread (rg, cg) of a
+// 16 x 16 layout owns rows 3 rg .. 3 rg + 2 and columns cg + 16 j (j < 7):
+//   Y[row][c] = sum_k X[row][k] * Wt(k, c, row)
+// X rows in shared memory (stride ldx), Wt read through `w(k, c, row)`;
+// 21 independent accumulators, k unrolled by 4.
+template <class WF, class OUT>
+__device__ __forceinline__ void ffma48(const float* X, int ldx, int K, int N, WF&& w, OUT&& out) {
+    const int rg = threadIdx.x >> 4, cg = threadIdx.x & 15;
+    float acc[3][7];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int j = 0; j < 7; ++j) acc[a][j] = 0.f;
+    const float* x0 = X + (std::size_t)(3 * rg) * ldx;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+        const float xa = x0[k], xb = x0[ldx + k], xc = x0[2 * ldx + k];
+#pragma unroll
+        for (int j = 0; j < 7; ++j) {
+            const int c = cg + 16 * j;
+            if (c < N) {
+                acc[0][j] = fmaf(xa, w(k, c, 3 * rg), acc[0][j]);
+                acc[1][j] = fmaf(xb, w(k, c, 3 * rg + 1), acc[1][j]);
+                acc[2][j] = fmaf(xc, w(k, c, 3 * rg + 2), acc[2][j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int j = 0; j < 7; ++j)
+            if (cg + 16 * j < N) out(3 * rg + a, cg + 16 * j, acc[a][j]);
+}
 }  // namespace
 
 std::size_t head_smem_bytes(const Dims& d) {
@@ -193,10 +227,27 @@ __global__ void __launch_bounds__(256, 1) k_head(HeadArgs h) {
     float* sD1 = sdZ + kRows * ldz;        // [32][D + 1]: D1 (pos rows 0..15, neg 16..31)
     float* sdD1 = sD1 + 2 * kEB * (D + 1); // [32][D + 1]: dD1
     float* sg = sdD1 + 2 * kEB * (D + 1);  // [32]: dlogit
+    __shared__ int s_has[kRows];           // root has neighbours (attention output kept)
+    __shared__ const float* s_mrow[kRows];  // the root's memory row (GRU output when pending)
     const int i0 = blockIdx.x * kEB;
     // local row lr -> event i0 + lr % 16, kind lr / 16 (src, dst, neg); global root row
     auto grow = [&](int lr) { return (lr / kEB) * B + i0 + lr % kEB; };
     auto valid = [&](int lr) { return i0 + lr % kEB < B; };
+    if (threadIdx.x < kRows) {
+        const int lr = threadIdx.x;
+        int has = 0;
+        const float* mr = nullptr;
+        if (valid(lr)) {
+            const int r = grow(lr);
+            const std::uint32_t n = h.roots[r];
+            const int sl = h.w.slot[n];
+            has = h.cnt[r] > 0;
+            mr = sl >= 0 ? h.mem_new + (std::size_t)sl * D : h.w.mem + (std::size_t)n * D;
+        }
+        s_has[lr] = has;
+        s_mrow[lr] = mr;
+    }
+    __syncthreads();
 
     // ---- F1: [ctx | 1] rows (tf32 already); pad columns zero
     const int Ko = DQ + 1, Kop = (Ko + 31) / 32 * 32;
@@ -210,9 +261,7 @@ __global__ void __launch_bounds__(256, 1) k_head(HeadArgs h) {
         const int lr = i / (Kmp - DQ), c = DQ + i % (Kmp - DQ);
         float v = 0.f;
         if (valid(lr) && c < DQ + D) {
-            const std::uint32_t n = h.roots[grow(lr)];
-            const int s = h.w.slot[n];
-            v = tf32r(s >= 0 ? h.mem_new[(std::size_t)s * D + (c - DQ)] : h.w.mem[(std::size_t)n * D + (c - DQ)]);
+            v = tf32r(s_mrow[lr][c - DQ]);
         } else if (c == DQ + D) {
             v = 1.f;
         }
@@ -223,8 +272,7 @@ __global__ void __launch_bounds__(256, 1) k_head(HeadArgs h) {
     // ---- F2: O = [ctx | 1] W_o^T -> m_in[:, :DQ] (0 for roots without neighbours)
     gemm48<true>(acc, sA, ldo, h.Wo, h.ldo, DQ, Ko);
     for_acc(acc, DQ, [&](int r, int c, float v) {
-        const bool has = valid(r) && h.cnt[grow(r)] > 0;
-        sM[(std::size_t)r * ldm + c] = has ? tf32r(v) : 0.f;
+        sM[(std::size_t)r * ldm + c] = s_has[r] ? tf32r(v) : 0.f;
     });
     __syncthreads();
     for (int i = threadIdx.x; i < kRows * (DQ + D); i += blockDim.x) {  // m_in for the W_m1 gradient
@@ -256,20 +304,17 @@ __global__ void __launch_bounds__(256, 1) k_head(HeadArgs h) {
         sW1[i] = h.Wd1[(std::size_t)n * h.ldd1 + c];  // [W_a | W_b | b1] row n (odd stride)
     }
     __syncthreads();
-    // ---- F5 (FFMA): D1[p] = relu(W_a z_src + W_b z_other + b1), p < 16 pos, >= 16 neg
+    // ---- F5 (FFMA): Y = [z_src W_a^T ; z_{dst|neg} W_b^T] (48 x D, into sdE), then
+    //      D1[p] = relu(Y_src[p % 16] + Y_other[p] + b1), p < 16 pos, >= 16 neg
     const int ld1 = 2 * D + 1;
+    ffma48(sE, D, D, D, [&](int k, int c, int row) { return sW1[(std::size_t)c * ld1 + (row < kEB ? 0 : D) + k]; },
+           [&](int row, int c, float v) { sdE[(std::size_t)row * ldz + c] = v; });
+    __syncthreads();
     for (int i = threadIdx.x; i < 2 * kEB * D; i += blockDim.x) {
         const int p = i / D, n = i % D;
-        const int e = p % kEB;
-        const float* zs = sE + (std::size_t)e * D;                            // src row
-        const float* zo = sE + (std::size_t)((p < kEB ? kEB : 2 * kEB) + e) * D;  // dst | neg row
-        const float* wr = sW1 + (std::size_t)n * ld1;
-        float a = 0.f, b = 0.f;
-        for (int k = 0; k < D; ++k) {
-            a = fmaf(zs[k], wr[k], a);
-            b = fmaf(zo[k], wr[D + k], b);
-        }
-        sD1[(std::size_t)p * (D + 1) + n] = fmaxf(a + b + wr[2 * D], 0.f);
+        const float v = sdE[(std::size_t)(p % kEB) * ldz + n] + sdE[(std::size_t)(kEB + p) * ldz + n] +
+                        sW1[(std::size_t)n * ld1 + 2 * D];
+        sD1[(std::size_t)p * (D + 1) + n] = fmaxf(v, 0.f);
     }
     __syncthreads();
     // ---- F6 (FFMA): logits, BCE terms, dlogit, dD1 = [D1 > 0] g w2 (one warp per pair row)
@@ -305,23 +350,20 @@ __global__ void __launch_bounds__(256, 1) k_head(HeadArgs h) {
         }
     }
     __syncthreads();
-    // ---- B1 (FFMA): d_emb = dD1 W_d1 by halves: src (pos + neg) W_a, dst pos W_b, neg neg W_b
+    // ---- B1 (FFMA): d_emb = dD1 W_d1 by halves: src (pos + neg) W_a, dst pos W_b,
+    //      neg neg W_b; the per-row dD1 combination staged in sdZ first
     for (int i = threadIdx.x; i < kRows * D; i += blockDim.x) {
-        const int lr = i / D, c = i % D;
-        const int kind = lr / kEB, e = lr % kEB;
-        float a = 0.f;
-        if (kind == 0) {
-            const float* gp = sdD1 + (std::size_t)e * (D + 1);
-            const float* gn = sdD1 + (std::size_t)(kEB + e) * (D + 1);
-            for (int n = 0; n < D; ++n) a = fmaf(gp[n] + gn[n], sW1[(std::size_t)n * ld1 + c], a);
-        } else {
-            const float* gq = sdD1 + (std::size_t)((kind == 1 ? 0 : kEB) + e) * (D + 1);
-            for (int n = 0; n < D; ++n) a = fmaf(gq[n], sW1[(std::size_t)n * ld1 + D + c], a);
-        }
-        a = valid(lr) ? tf32r(a) : 0.f;
-        sdE[(std::size_t)lr * ldz + c] = a;
-        if (valid(lr)) h.d_emb[(std::size_t)grow(lr) * D + c] = a;
+        const int lr = i / D, n = i % D, e = lr % kEB, kind = lr / kEB;
+        const float gp = sdD1[(std::size_t)e * (D + 1) + n], gn = sdD1[(std::size_t)(kEB + e) * (D + 1) + n];
+        sdZ[(std::size_t)lr * ldz + n] = kind == 0 ? gp + gn : kind == 1 ? gp : gn;
     }
+    __syncthreads();
+    ffma48(sdZ, ldz, D, D, [&](int n, int c, int row) { return sW1[(std::size_t)n * ld1 + (row < kEB ? 0 : D) + c]; },
+           [&](int lr, int c, float a) {
+               a = valid(lr) ? tf32r(a) : 0.f;
+               sdE[(std::size_t)lr * ldz + c] = a;
+               if (valid(lr)) h.d_emb[(std::size_t)grow(lr) * D + c] = a;
+           });
     zero_cols(sdE, ldz, D, (D + 31) / 32 * 32);
     __syncthreads();
     // ---- B2: dZ1 = (d_emb W_m2) * [Z1 > 0]
@@ -337,7 +379,7 @@ __global__ void __launch_bounds__(256, 1) k_head(HeadArgs h) {
     gemm48<false>(acc, sdZ, ldz, h.Wm1, h.ldm1, DQ + D, D);
     for_acc(acc, DQ + D, [&](int r, int c, float v) {
         const bool ok = valid(r);
-        const float x = (c < DQ && !(ok && h.cnt[grow(r)] > 0)) ? 0.f : tf32r(v);
+        const float x = (c < DQ && !s_has[r]) ? 0.f : tf32r(v);
         if (c < DQ) sA[(std::size_t)r * ldo + c] = x;
         if (ok) h.dm_in[(std::size_t)grow(r) * d.ld_m + c] = x;
     });
