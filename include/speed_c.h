@@ -285,7 +285,8 @@ typedef struct spd_tgn_trainer spd_tgn_trainer;
  * `workers` lists which subgraphs of `subs` it owns; across processes the
  * lists partition [0, count). world>1 joins an NCCL communicator from
  * nccl_id (128 bytes from spd_nccl_unique_id) for the per-step gradient
- * all-reduce and the epoch-end shared-node sync. shared: global ids of SEP's
+ * all-reduce and the epoch-end shared-node sync; with nccl_id == NULL it uses
+ * the peer-memory transport below instead. shared: global ids of SEP's
  * shared hubs (PartitionAssignment::shared). edge ids in `subs` index the
  * synthetic feature generator. */
 spd_status spd_tgn_create(const spd_tgn_config* cfg, const spd_subgraphs* subs,
@@ -294,6 +295,18 @@ spd_status spd_tgn_create(const spd_tgn_config* cfg, const spd_subgraphs* subs,
                           const void* nccl_id, int32_t device, spd_tgn_trainer** out);
 void spd_tgn_destroy(spd_tgn_trainer* t);
 spd_status spd_nccl_unique_id(void* out128);
+/* Peer-memory transport (world > 1 created with nccl_id == NULL): the
+ * per-step gradient all-reduce is fused into Adam, reading every rank's
+ * gradient buffer from its HBM (CUDA IPC: NVLink P2P across GPUs, shared HBM
+ * for ranks on one GPU), in rank order — replicated parameters stay
+ * bit-identical; the epoch-end shared-hub sync (pac_sim.cpp:162-203) reduces
+ * over the same mappings. Replaces the Alg. 2 barrier + all-reduce of
+ * PAPER.md:340-358 / pac_sim.cpp:233-260. Every rank exports a blob of
+ * spd_tgn_peer_blob_bytes() bytes, the caller gathers them in rank order
+ * (any host channel) and every rank connects before its first step. */
+uint64_t spd_tgn_peer_blob_bytes(void);
+spd_status spd_tgn_peer_export(const spd_tgn_trainer* t, void* out);
+spd_status spd_tgn_peer_connect(spd_tgn_trainer* t, const void* blobs);
 
 /* Number of lockstep global steps in one epoch = max_w ceil(|E_w| / B) over ALL
  * workers (run_epoch, pac_sim.cpp:221-234). */
@@ -364,6 +377,15 @@ spd_status spd_tgn_set_gemm_mode(spd_tgn_trainer* t, int32_t mode);
  * mem_new, gsave) into out[0, cap); *n = its element count. */
 spd_status spd_tgn_debug_scratch(spd_tgn_trainer* t, const char* name, float* out, uint64_t cap,
                                  uint64_t* n);
+/* Bridge backbone: replace the TGN model inside this
+ * trainer's schedule (loop-start reset, pending last messages, loop-end flush
+ * + snapshot, epoch-end restore + shared sync) by the reference's surrogate
+ * MSG/UPD, ModelParams {d x 3d w_m row-major, omega[d], gamma}
+ * (pac_sim.hpp:47-59, pac_sim.cpp:50-104). Steps then apply the pending
+ * messages only: no embedding, loss or gradients. At batch_size 1 an epoch
+ * reproduces run_epoch (pac_sim.cpp:205-264). d must equal d_mem. */
+spd_status spd_tgn_set_surrogate(spd_tgn_trainer* t, int32_t d, const double* w_m,
+                                 const double* omega, double gamma);
 /* Per-phase times (ms, CUDA events on the trainer's stream) of the last step. */
 spd_status spd_tgn_kernel_times(const spd_tgn_trainer* t, float* ms, int32_t* n_kernels,
                                 char* names, int32_t name_stride, int32_t cap);

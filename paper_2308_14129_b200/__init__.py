@@ -749,7 +749,8 @@ def nccl_unique_id() -> bytes:
 
 class TGNTrainer:
     """Per-process TGN trainer over the SEP partitions `workers` (default: all)
-    of `subgraphs`, on `device`; world>1 joins an NCCL communicator."""
+    of `subgraphs`, on `device`; world>1 joins an NCCL communicator (nccl_id)
+    or, without an id, the peer-memory transport (peer_export / peer_connect)."""
 
     def __init__(self, cfg: TGNConfig, subgraphs: Sequence[SubGraph], workers=None, shared=(),
                  node_count: int | None = None, rank: int = 0, world: int = 1,
@@ -783,6 +784,24 @@ class TGNTrainer:
 
     def close(self):
         self.__del__()
+
+    def set_surrogate(self, model: "ModelParams"):
+        """Bridge backbone: the reference's surrogate MSG/UPD replaces the GRU
+        in this trainer's schedule (spd_tgn_set_surrogate)."""
+        w = np.ascontiguousarray(model.w_m, np.float64)
+        om = np.ascontiguousarray(model.omega, np.float64)
+        _check(lib.spd_tgn_set_surrogate(self._h, model.d, ptr(w, f64), ptr(om, f64), model.gamma))
+
+    def peer_export(self) -> bytes:
+        """This rank's peer-transport blob (world > 1 without an NCCL id):
+        gather every rank's blob in rank order, then peer_connect."""
+        buf = C.create_string_buffer(int(lib.spd_tgn_peer_blob_bytes()))
+        _check(lib.spd_tgn_peer_export(self._h, buf))
+        return buf.raw
+
+    def peer_connect(self, blobs: Sequence[bytes]):
+        raw = b"".join(blobs)
+        _check(lib.spd_tgn_peer_connect(self._h, C.create_string_buffer(raw, len(raw))))
 
     def epoch_steps(self) -> int:
         n = u64()

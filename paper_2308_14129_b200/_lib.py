@@ -111,6 +111,10 @@ _SIGS = {
                              i32, PP]),
     "spd_tgn_destroy": (None, [P]),
     "spd_nccl_unique_id": (i32, [P]),
+    "spd_tgn_peer_blob_bytes": (u64, []),
+    "spd_tgn_set_surrogate": (i32, [P, i32, P, P, f64]),
+    "spd_tgn_peer_export": (i32, [P, P]),
+    "spd_tgn_peer_connect": (i32, [P, P]),
     "spd_tgn_epoch_steps": (i32, [P, pu64]),
     "spd_tgn_begin_epoch": (i32, [P, i32]),
     "spd_tgn_seek": (i32, [P, u64]),

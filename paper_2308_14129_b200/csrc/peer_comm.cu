@@ -157,6 +157,19 @@ void PeerComm::wait(int kind, const std::uint64_t* seq_dev, std::int64_t offset,
     SPD_CUDA(cudaGetLastError());
 }
 
+void PeerComm::adam_step(const std::uint64_t* seq_dev, float* p, float* m, float* v, std::size_t n,
+                         float scale, float lr, float b1, float one_m_b1, float b2, float one_m_b2,
+                   const float* bc, float eps,
+                         float* p_tc, cudaStream_t st) {
+    if (!connected_) usage_error("peer transport not connected (spd_tgn_peer_connect)");
+    signal(kReady, seq_dev, 0, st);
+    wait(kReady, seq_dev, 0, st);
+    k_adam_peer<<<unsigned((n + 255) / 256), 256, 0, st>>>(p, v_, m, v, n, scale, lr, b1, one_m_b1, b2,
+                                                           one_m_b2, bc, eps, p_tc);
+    SPD_CUDA(cudaGetLastError());
+    signal(kDone, seq_dev, 0, st);
+}
+
 void PeerComm::allreduce(void* data, std::size_t count, int type, int op, cudaStream_t st) {
     if (!connected_) usage_error("peer transport not connected (spd_tgn_peer_connect)");
     const std::size_t esz = type == kF64 ? 8 : 4;

@@ -58,6 +58,14 @@ public:
     // Eager collective over the ranks (epoch-end sync): data[0, count) of
     // `type` reduced with `op` in rank order into data on every rank.
     void allreduce(void* data, std::size_t count, int type, int op, cudaStream_t st);
+    // The step's fused gradient all-reduce + Adam (k_adam_peer): READY(seq),
+    // wait for every rank's READY(seq), read-sum-update, DONE(seq). The
+    // caller's next gradient clear waits for DONE(seq) of every rank
+    // (wait(kDone, seq_dev, -1) at step start).
+    void adam_step(const std::uint64_t* seq_dev, float* p, float* m, float* v, std::size_t n,
+                   float scale, float lr, float b1, float one_m_b1, float b2, float one_m_b2,
+                   const float* bc, float eps,
+                   float* p_tc, cudaStream_t st);
 
 private:
     int rank_, world_, device_;

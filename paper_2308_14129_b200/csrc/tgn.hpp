@@ -14,6 +14,7 @@
 
 #include "cuda_util.hpp"
 #include "host.hpp"
+#include "peer_comm.hpp"
 #include "tgn_kernels.cuh"
 
 namespace spd {
@@ -141,6 +142,15 @@ public:
                    float* loss);
     const StepTimes& times() const { return times_; }
     float run_steps(std::uint64_t n);
+    // peer-memory transport (world > 1 without an NCCL id, peer_comm.hpp):
+    // every rank exports its blob, the caller exchanges them, every rank connects
+    bool peer_mode() const { return peer_ != nullptr; }
+    // Bridge backbone: the reference's surrogate MSG/UPD
+    // (pac_sim.cpp:50-104) replaces the GRU in this trainer's schedule; steps
+    // apply the pending messages only (no embedding, loss, gradients)
+    void set_surrogate(int d, const double* w_m, const double* omega, double gamma);
+    void peer_export(unsigned char* out) const;
+    void peer_connect(const unsigned char* blobs);
     void step_host(const spd_edge* const* events, const std::uint16_t* const* feats,
                    float* loss_out);
     std::uint64_t h2d_bytes() const { return h2d_bytes_; }
@@ -214,6 +224,14 @@ private:
     int total_workers_ = 1;
     cudaStream_t stream_ = nullptr;
     void* nccl_ = nullptr;  // ncclComm_t
+    std::unique_ptr<PeerComm> peer_;  // peer-memory transport instead of NCCL
+    bool surrogate_ = false;          // bridge backbone (set_surrogate)
+    DevBuf<double> sur_w_, sur_om_;
+    double sur_gamma_ = 0.0;
+    void surrogate_update(Worker& w, const tgnk::WorkerDev& wd);
+    // world > 1 collective over ranks (NCCL or the peer transport), in place
+    void coll(void* data, std::size_t count, int type, int op, cudaStream_t st);
+    std::uint64_t peer_seq_ = 0;  // global steps issued (the step protocol's sequence)
     std::vector<std::unique_ptr<Worker>> workers_;
     std::vector<std::uint64_t> all_batches_;  // per global worker
     std::uint64_t epoch_steps_ = 0, step_in_epoch_ = 0, adam_t_ = 0;
@@ -221,7 +239,7 @@ private:
     std::vector<NodeId> shared_;
     DevBuf<float> params_, grads_, adam_m_, adam_v_;
     DevBuf<float> params_tc_;  // tf32-rounded copy read by the tensor-core GEMMs
-    DevBuf<std::uint64_t> ctl_dev_;  // [2 per worker | Adam bias corrections (2 x f32)]
+    DevBuf<std::uint64_t> ctl_dev_;  // [2 per worker | Adam bias corrections (2 x f32) | step seq]
     std::vector<std::uint64_t> ctl_stage_;
     static constexpr int kCtlSlots = 64;
     std::uint64_t* ctl_ring_ = nullptr;  // pinned [kCtlSlots][ctl words]

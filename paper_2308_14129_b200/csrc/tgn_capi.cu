@@ -41,6 +41,28 @@ spd_status spd_tgn_create(const spd_tgn_config* cfg, const spd_subgraphs* subs,
 
 void spd_tgn_destroy(spd_tgn_trainer* t) { delete t; }
 
+spd_status spd_tgn_set_surrogate(spd_tgn_trainer* t, int32_t d, const double* w_m,
+                                 const double* omega, double gamma) {
+    GUARD({
+        if (!t || !w_m || !omega) usage_error("null argument");
+        t->t->set_surrogate(d, w_m, omega, gamma);
+    });
+}
+
+uint64_t spd_tgn_peer_blob_bytes(void) { return PeerComm::kBlobBytes; }
+spd_status spd_tgn_peer_export(const spd_tgn_trainer* t, void* out) {
+    GUARD({
+        if (!t || !out) usage_error("null argument");
+        t->t->peer_export(static_cast<unsigned char*>(out));
+    });
+}
+spd_status spd_tgn_peer_connect(spd_tgn_trainer* t, const void* blobs) {
+    GUARD({
+        if (!t || !blobs) usage_error("null argument");
+        t->t->peer_connect(static_cast<const unsigned char*>(blobs));
+    });
+}
+
 spd_status spd_tgn_epoch_steps(const spd_tgn_trainer* t, uint64_t* steps) {
     GUARD({ *steps = t->t->epoch_steps(); });
 }

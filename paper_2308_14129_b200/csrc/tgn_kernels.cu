@@ -396,6 +396,34 @@ __global__ void k_persist(WorkerDev w, int D, const float* mem_new) {
     }
 }
 
+// Bridge backbone: the reference's surrogate MSG/UPD
+// (pac_sim.cpp:50-64 message, :68-104 model_update) in place of the GRU, applied
+// to the pending last messages — every record reads the PRE-states of its node
+// and of the other endpoint (as model_update reads both endpoints before
+// writing either), m = tanh(W_m [s_u | s_other | cos(omega * (ts - lu_u))]),
+// s_u <- (1 - gamma) s_u + gamma m. One thread per (record, output row); f64
+// with explicitly rounded products and sums in the reference's column order
+// (no FMA contraction); states are stored in the trainer's f32 memory.
+__global__ void k_surrogate_update(WorkerDev w, int D, const double* w_m, const double* omega,
+                                   double gamma, float* mem_new) {
+    pdl_entry();
+    const std::size_t t = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int n = *w.nU;
+    if (t >= (std::size_t)n * D) return;
+    const int i = static_cast<int>(t / D), r = static_cast<int>(t % D);
+    const std::uint32_t u = w.pU[i], o = w.pOther[i];
+    const double dt = __dadd_rn(w.pTs[i], -w.lu[u]);
+    const float* su = w.mem + (std::size_t)u * D;
+    const float* so = w.mem + (std::size_t)o * D;
+    const double* wr = w_m + (std::size_t)r * 3 * D;
+    double acc = 0.0;
+    for (int c = 0; c < D; ++c) acc = __dadd_rn(acc, __dmul_rn(wr[c], double(su[c])));
+    for (int c = 0; c < D; ++c) acc = __dadd_rn(acc, __dmul_rn(wr[D + c], double(so[c])));
+    for (int c = 0; c < D; ++c) acc = __dadd_rn(acc, __dmul_rn(wr[2 * D + c], cos(__dmul_rn(omega[c], dt))));
+    const double m = tanh(acc);
+    mem_new[t] = float(__dadd_rn(__dmul_rn(1.0 - gamma, double(su[r])), __dmul_rn(gamma, m)));
+}
+
 // K3 last-message selection: endpoint slots q = 2k (src), 2k+1 (dst) of the
 // batch's events; per node the max slot wins (max (ts, stream index)),
 // compacted in slot order into the worker's other pending set (nx*).

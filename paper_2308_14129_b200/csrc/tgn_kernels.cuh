@@ -178,6 +178,8 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t
 __global__ void k_round_tf32(const float* src, float* dst, std::size_t n);
 __global__ void k_persist(WorkerDev w, int D, const float* mem_new);
 __global__ void k_pending(WorkerDev w, int B);
+__global__ void k_surrogate_update(WorkerDev w, int D, const double* w_m, const double* omega,
+                                   double gamma, float* mem_new);
 __global__ void k_gen_features(__nv_bfloat16* feat, const std::uint64_t* eids, std::uint64_t E,
                                int F, int Fp, std::uint64_t seed_mixed);
 __global__ void k_gather_rows(const float* src, int ld, const std::uint32_t* idx,

@@ -451,7 +451,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     params_tc_.alloc(lay_.total);
     // per-step control block (see commit_ctl)
     {
-        const std::size_t words = 2 * workers_.size() + 1;
+        const std::size_t words = 2 * workers_.size() + 2;  // + Adam bias corrections, step seq
         ctl_dev_.alloc(words);
         ctl_dev_.zero(stream_);
         ctl_stage_.assign(words, 0);
@@ -540,16 +540,20 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.tattn_blocks = (R + tgnk::attn_x_roots_per_block() - 1) / tgnk::attn_x_roots_per_block();
     s.tpart.alloc(std::size_t(s.troot_blocks + s.tattn_blocks) * 2 * d.T);
     s.dh.nbr_node = s.nbr_node.p; s.dh.cnt = s.cnt.p; s.dh.roots = s.roots.p;
-    {  // fused head (tgn_head.cu): one 227 KB CTA per 16 events; SPD_FUSED_HEAD=0 disables
+    {  // fused head (tgn_head.cu): one 227 KB CTA per 16 events; opt-in (SPD_FUSED_HEAD=1):
+       // GDELT B = 2000 step 0.483 ms with it vs 0.411 ms with the separate kernels
         const char* e = std::getenv("SPD_FUSED_HEAD");
-        head_fits_ = !(e && *e == '0') && d.DQ + d.D <= 320 &&
+        head_fits_ = (e && *e == '1') && d.DQ + d.D <= 320 &&
                      tgnk::head_smem_bytes(d) <= std::size_t(227) * 1024;
     }
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
     SPD_CUDA(cudaStreamSynchronize(stream_));
 
-    if (world_ > 1) {
-        if (!nccl_id) usage_error("world > 1 needs an NCCL unique id");
+    if (world_ > 1 && !nccl_id) {  // peer-memory transport (peer_comm.hpp): connect before stepping
+        const std::size_t S = shared_.size();
+        const std::size_t sb = std::max<std::size_t>({256, S * lay_.D * sizeof(float), S * sizeof(double)});
+        peer_ = std::make_unique<PeerComm>(rank_, world_, device_, grads_.p, sb);
+    } else if (world_ > 1) {
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof(id));
         ncclComm_t comm;
@@ -804,9 +808,38 @@ void TGNTrainer::seek(std::uint64_t step) {
     SPD_CUDA(cudaStreamSynchronize(stream_));
 }
 
+void TGNTrainer::set_surrogate(int d, const double* w_m, const double* omega, double gamma) {
+    DeviceGuard g(device_);
+    if (d != lay_.D) data_error("ConfigMismatch", "surrogate dimension must equal d_mem");
+    sur_w_.alloc(std::size_t(3) * d * d);
+    sur_w_.upload(w_m, sur_w_.n, stream_);
+    sur_om_.alloc(d);
+    sur_om_.upload(omega, d, stream_);
+    sur_gamma_ = gamma;
+    surrogate_ = true;
+    for (auto& ge : graph_exec_)
+        if (ge) {
+            SPD_CUDA(cudaGraphExecDestroy(ge));
+            ge = nullptr;
+        }
+    eager_full_steps_ = 0;
+    SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void TGNTrainer::surrogate_update(Worker& w, const tgnk::WorkerDev& wd) {
+    Scratch& s = *s_;
+    launch(tgnk::k_surrogate_update, blocks_for(std::size_t(s.U) * lay_.D), 256, 0, stream_, wd, lay_.D,
+           static_cast<const double*>(sur_w_.p), static_cast<const double*>(sur_om_.p), sur_gamma_,
+           s.mem_new.p);
+}
+
 void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
                              const std::function<void()>& after_gather) {
     Scratch& s = *s_;
+    if (surrogate_) {
+        surrogate_update(w, wd);
+        return;
+    }
     const auto& d = s.d;
     const float* P = params_.p;
     const bool tc = cfg_.gemm_mode == 1;
@@ -1329,7 +1362,7 @@ void TGNTrainer::allreduce_grads(cudaStream_t st) {
     launch(tgnk::k_time_grad_apply, blocks_for(lay_.T), 256, 0, st, 
         lay_.T, tgrad_.p, grads_.p + lay_.time_w, grads_.p + lay_.time_b);
     SPD_CUDA(cudaGetLastError());
-    if (world_ > 1) {
+    if (world_ > 1 && !peer_) {  // (the peer transport sums inside its Adam kernel)
         SPD_NCCL(ncclAllReduce(grads_.p, grads_.p, lay_.total, ncclFloat, ncclSum,
                                static_cast<ncclComm_t>(nccl_), st));
     }
@@ -1339,7 +1372,8 @@ void TGNTrainer::adam_prepare() {
     ++adam_t_;
     const float bc[2] = {static_cast<float>(1.0 - std::pow(double(cfg_.beta1), double(adam_t_))),
                          static_cast<float>(1.0 - std::pow(double(cfg_.beta2), double(adam_t_)))};
-    std::memcpy(&ctl_stage_.back(), bc, sizeof(bc));
+    std::memcpy(&ctl_stage_[ctl_stage_.size() - 2], bc, sizeof(bc));
+    ctl_stage_.back() = ++peer_seq_;  // the peer transport's step sequence
 }
 
 void TGNTrainer::commit_ctl() {
@@ -1355,6 +1389,13 @@ void TGNTrainer::commit_ctl() {
 
 void TGNTrainer::adam(cudaStream_t st) {
     const double b1 = cfg_.beta1, b2 = cfg_.beta2;
+    if (peer_) {  // all-reduce fused with the update: every rank's gradients read from its HBM
+        peer_->adam_step(ctl_dev_.p + ctl_stage_.size() - 1, params_.p, adam_m_.p, adam_v_.p, lay_.total,
+                         float(total_workers_), cfg_.lr, cfg_.beta1, static_cast<float>(1.0 - b1),
+                         cfg_.beta2, static_cast<float>(1.0 - b2), adam_bc_, cfg_.adam_eps,
+                         cfg_.gemm_mode == 1 ? params_tc_.p : nullptr, st);
+        return;
+    }
     launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, st,
         params_.p, grads_.p, adam_m_.p, adam_v_.p, lay_.total, float(total_workers_), cfg_.lr,
         cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2),
@@ -1372,6 +1413,20 @@ void TGNTrainer::set_ctl(Worker& w, std::uint64_t lo, std::uint64_t nb) {
 // the device: the local workers' batches, the gradient all-reduce and Adam.
 // Bs[k] = batch size of local worker k (0: idle). Capturable as a CUDA graph.
 void TGNTrainer::step_body(const std::vector<int>& Bs) {
+    if (surrogate_) {  // bridge backbone: apply, persist and collect the last messages only
+        s_->loss.zero(stream_);
+        for (std::size_t k = 0; k < workers_.size(); ++k) {
+            if (Bs[k] == 0) continue;
+            Worker& w = *workers_[k];
+            const tgnk::WorkerDev wd = devview(w);
+            w.last_b = Bs[k];
+            surrogate_update(w, wd);
+            launch(tgnk::k_persist, blocks_for(std::size_t(s_->U) * 32), 256, 0, stream_, wd, lay_.D,
+                   s_->mem_new.p);
+            launch(tgnk::k_pending, 1, 1024, 0, stream_, wd, Bs[k]);
+        }
+        return;
+    }
     // gradient buffers cleared by a kernel, not memset nodes: in a graph
     // replay a memset node costs a copy-engine hand-off before the first
     // kernel. It runs on its own stream beside the forward (nothing reads or
@@ -1389,6 +1444,8 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
         z.d = tgrad_.p; z.nd = std::size_t(2) * ld4(lay_.T);
         std::size_t mx = z.nd;
         for (int k = 0; k < tgnk::ZeroList::kMax; ++k) mx = std::max(mx, z.n[k]);
+        // peers read these gradients until they signal DONE for the previous step
+        if (peer_) peer_->wait(kDone, ctl_dev_.p + ctl_stage_.size() - 1, -1, zs_);
         launch(tgnk::k_zero_list, std::min<unsigned>(blocks_for(mx), 148), 256, 0, zs_, z);
         scratch_zeroed_ = true;  // the first backward of this step skips its own zeroing
     }
@@ -1430,8 +1487,31 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
     join_side();
 }
 
+void TGNTrainer::peer_export(unsigned char* out) const {
+    if (!peer_) usage_error("peer transport: trainer was created with an NCCL id or world 1");
+    peer_->export_blob(out);
+}
+
+void TGNTrainer::peer_connect(const unsigned char* blobs) {
+    if (!peer_) usage_error("peer transport: trainer was created with an NCCL id or world 1");
+    peer_->connect(blobs);
+}
+
+void TGNTrainer::coll(void* data, std::size_t count, int type, int op, cudaStream_t st) {
+    if (world_ < 2 || count == 0) return;
+    if (peer_) {
+        peer_->allreduce(data, count, type, op, st);
+        return;
+    }
+    const ncclDataType_t t = type == kF64 ? ncclDouble : type == kI32 ? ncclInt32 : ncclFloat;
+    const ncclRedOp_t o = op == kOpMin ? ncclMin : op == kOpMax ? ncclMax : ncclSum;
+    SPD_NCCL(ncclAllReduce(data, data, count, t, o, static_cast<ncclComm_t>(nccl_), st));
+}
+
 void TGNTrainer::step(float* loss_out) {
     DeviceGuard g(device_);
+    if (peer_ && !peer_->connected())
+        usage_error("peer transport not connected (spd_tgn_peer_export / spd_tgn_peer_connect)");
     ++step_in_epoch_;
     times_.ms.clear();
     std::vector<int> Bs(workers_.size(), 0);
@@ -1744,35 +1824,32 @@ void TGNTrainer::sync_shared() {
         launch(k_sync_ts_minmax, blocks_for(S), 256, 0, st, w.lu.p, rows[k].p, S, k == 0, tmin.p, tmax.p);
     }
     SPD_CUDA(cudaGetLastError());
-    ncclComm_t comm = static_cast<ncclComm_t>(nccl_);
     if (cfg_.sync_average) {
-        if (world_ > 1) {
-            SPD_NCCL(ncclGroupStart());
-            SPD_NCCL(ncclAllReduce(sum.p, sum.p, sum.n, ncclFloat, ncclSum, comm, st));
-            SPD_NCCL(ncclAllReduce(mn.p, mn.p, mn.n, ncclFloat, ncclMin, comm, st));
-            SPD_NCCL(ncclAllReduce(mx.p, mx.p, mx.n, ncclFloat, ncclMax, comm, st));
-            SPD_NCCL(ncclAllReduce(tmin.p, tmin.p, S, ncclDouble, ncclMin, comm, st));
-            SPD_NCCL(ncclAllReduce(tmax.p, tmax.p, S, ncclDouble, ncclMax, comm, st));
-            SPD_NCCL(ncclGroupEnd());
-        }
+        if (world_ > 1 && !peer_) SPD_NCCL(ncclGroupStart());
+        coll(sum.p, sum.n, kF32, kOpSum, st);
+        coll(mn.p, mn.n, kF32, kOpMin, st);
+        coll(mx.p, mx.n, kF32, kOpMax, st);
+        coll(tmin.p, S, kF64, kOpMin, st);
+        coll(tmax.p, S, kF64, kOpMax, st);
+        if (world_ > 1 && !peer_) SPD_NCCL(ncclGroupEnd());
         for (std::size_t k = 0; k < workers_.size(); ++k) {
             Worker& w = *workers_[k];
             launch(k_sync_apply_avg, S, 128, 0, st, w.mem.p, w.lu.p, rows[k].p, S, D, sum.p, mn.p, mx.p,
                                                 tmin.p, tmax.p, 1.f / float(total_workers_));
         }
     } else {
-        if (world_ > 1) SPD_NCCL(ncclAllReduce(tmax.p, tmax.p, S, ncclDouble, ncclMax, comm, st));
+        coll(tmax.p, S, kF64, kOpMax, st);
         DevBuf<int> owner(S);
         SPD_CUDA(cudaMemsetAsync(owner.p, 0x7F, owner.bytes(), st));
         for (std::size_t k = 0; k < workers_.size(); ++k)
             launch(k_sync_owner, blocks_for(S), 256, 0, st, workers_[k]->lu.p, rows[k].p, S, tmax.p,
                                                         workers_[k]->gid, owner.p);
-        if (world_ > 1) SPD_NCCL(ncclAllReduce(owner.p, owner.p, S, ncclInt32, ncclMin, comm, st));
+        coll(owner.p, S, kI32, kOpMin, st);
         sum.zero(st);
         for (std::size_t k = 0; k < workers_.size(); ++k)
             launch(k_sync_owner_pack, blocks_for(std::size_t(S) * D), 256, 0, st, 
                 workers_[k]->mem.p, rows[k].p, S, D, owner.p, workers_[k]->gid, sum.p);
-        if (world_ > 1) SPD_NCCL(ncclAllReduce(sum.p, sum.p, sum.n, ncclFloat, ncclSum, comm, st));
+        coll(sum.p, sum.n, kF32, kOpSum, st);
         for (std::size_t k = 0; k < workers_.size(); ++k)
             launch(k_sync_apply_max, blocks_for(std::size_t(S) * D), 256, 0, st, 
                 workers_[k]->mem.p, workers_[k]->lu.p, rows[k].p, S, D, sum.p, tmax.p);
