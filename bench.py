@@ -169,7 +169,7 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def build_workload(name, P, rank, log):
+def build_workload(name, P, rank, log, hub_k=0.05):
     import paper_2308_14129_b200 as sp
     N, E, F, B = CONFIGS[name]
     t0 = time.time()
@@ -180,7 +180,7 @@ def build_workload(name, P, rank, log):
     tr = split.train
     t0 = time.time()
     c = sp.compute_centrality(tr, 0.5)
-    pa = sp.partition_stream(tr, sp.PartitionerConfig(P, 1.0, 1.0, sp.select_hubs(c, 0.05), c))
+    pa = sp.partition_stream(tr, sp.PartitionerConfig(P, 1.0, 1.0, sp.select_hubs(c, hub_k), c))
     log(f"SEP P={P}: {time.time() - t0:.1f}s, shared={len(pa.shared)}, discards={pa.discard_count}")
     t0 = time.time()
     subs = sp.induce_subgraphs(tr, pa.node_parts, P)
@@ -313,6 +313,13 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--fp32-steps", type=int, default=100,
                     help="also time this many steps with gemm_mode 0 (FP32 FFMA) for comparison")
+    ap.add_argument("--parts", type=int, default=0,
+                    help="SEP partitions (default: one per GPU); more than --gpus trains several "
+                         "partitions per GPU as local workers of one trainer")
+    ap.add_argument("--hub-k", type=float, default=0.05, help="SEP shared-hub fraction k")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1 gradient all-reduce: peer = fused into Adam over CUDA-IPC-mapped "
+                         "peer HBM (NVLink); nccl = ncclAllReduce then Adam")
     ap.add_argument("--gemm-mode", type=int, default=1,
                     help="0 = FP32 FFMA everywhere; 1 = tcgen05 TF32 for the GRU and attention "
                          "projection GEMMs (merge/decoder stay FP32 FFMA)")
@@ -336,12 +343,20 @@ def main():
 
     metric = "training edges/sec (TGN, SEP partitions = GPUs, processed events)"
     N, E, F, B = CONFIGS[args.config]
+    P = args.parts or world
+    if P % world:
+        raise SystemExit(f"--parts {P} is not a multiple of the {world} ranks")
+    mine = list(range(rank * (P // world), (rank + 1) * (P // world)))  # this rank's partitions
     D = T = 100
     K, H = 10, 2
     cfg_desc = {"workload": f"{args.config}-shape synthetic TIG ({N} nodes, {E} edges, d_e={F}), "
-                            f"TGN d_mem=d_time=100 k={K} heads={H}, B={B}, SEP P={world}",
-                "nodes": N, "edges": E, "d_edge": F, "batch": B, "partitions": world,
-                "parallelism": f"sep{world}", "timed_from": "mid-epoch (spd_tgn_seek to epoch_steps/2)",
+                            f"TGN d_mem=d_time=100 k={K} heads={H}, B={B}, SEP P={P}"
+                            + (f" k_hub={args.hub_k}" if args.hub_k != 0.05 else ""),
+                "nodes": N, "edges": E, "d_edge": F, "batch": B, "partitions": P,
+                "partitions_per_gpu": P // world, "hub_k": args.hub_k,
+                "parallelism": f"sep{P}" + (f" ({P // world} per GPU)" if P > world else ""),
+                "transport": (args.transport if world > 1 else None),
+                "timed_from": "mid-epoch (spd_tgn_seek to epoch_steps/2)",
                 "l2": "inputs larger than L2 (50-100 GB feature "
                 "table gathers + >126 MB activations per step)"}
 
@@ -350,7 +365,7 @@ def main():
             return
         # everything on this arm runs the reference library (oracle/_ref);
         # the product library is never imported or loaded
-        wl = build_workload_ref(args.config, world, log)
+        wl = build_workload_ref(args.config, P, log)
         nodes, edges = wl["subs"][0]
         rate, cores, per = cpu_reference_rate(localize(nodes, edges), len(nodes), D,
                                               args.cpu_seconds, log)
@@ -370,20 +385,25 @@ def main():
         return
 
     import paper_2308_14129_b200 as sp
-    wl = build_workload(args.config, world, rank, log)
-    sub_mine = wl["subs"][rank]
+    wl = build_workload(args.config, P, rank, log, args.hub_k)
+    subs_mine = [wl["subs"][w] for w in mine]
+    sub_mine = subs_mine[0]
     cfg = sp.TGNConfig(d_mem=D, d_time=T, d_edge=F, n_neighbors=K, n_heads=H, batch_size=B, lr=1e-4,
                        gemm_mode=args.gemm_mode)
     nccl_id = None
-    if world > 1:
+    if world > 1 and args.transport == "nccl":
         import torch
         nid = sp.nccl_unique_id() if rank == 0 else bytes(128)
         t = torch.tensor(list(nid), dtype=torch.uint8)
         pg.broadcast(t, 0)
         nccl_id = bytes(t.tolist())
     t0 = time.time()
-    tr = sp.TGNTrainer(cfg, wl["subs"], workers=[rank], shared=wl["shared"], node_count=N,
+    tr = sp.TGNTrainer(cfg, wl["subs"], workers=mine, shared=wl["shared"], node_count=N,
                        rank=rank, world=world, nccl_id=nccl_id, device=local)
+    if world > 1 and args.transport == "peer":  # exchange the peer-memory blobs over gloo
+        blobs = [None] * world
+        pg.all_gather_object(blobs, tr.peer_export())
+        tr.peer_connect(blobs)
     log(f"trainer ready: {time.time() - t0:.1f}s, params={tr.n_params}, epoch_steps={tr.epoch_steps()}")
     # per-GPU device memory held after the trainer is built (events, CSR,
     # feature rows, memory, parameters, scratch): SURVEY §8 ML25M footprint
@@ -408,7 +428,8 @@ def main():
         barrier(pg)
     launches = sp.kernel_launches() - launches0
     ms_max = allreduce_max(pg, ms)
-    edges_mine = sum(min(B, len(sub_mine.edges)) for _ in range(args.steps))
+    per_step = sum(min(B, len(g.edges)) for g in subs_mine)  # every worker steps (loop-within-epoch)
+    edges_mine = per_step * args.steps
     edges_all = allreduce_sum(pg, float(edges_mine))
     value = edges_all / (ms_max / 1e3)
     ms_per_step = ms_max / args.steps
@@ -425,44 +446,45 @@ def main():
     phases = list(acc.items())
     tr.set_profile(False)
 
-    # end-to-end through the public API from pinned host buffers
+    # end-to-end through the public API from pinned host buffers: every local
+    # worker's next e2e_steps batches (wrapping within its partition stream,
+    # loop-within-epoch) staged in pinned memory, fed through step_host_async
     import torch
-    ev_local = tr.worker_events(rank)
-    Fp = tr.next_batch(rank)[2]
     e2e_steps = args.e2e_steps
     pin = torch.cuda.is_available()
-    # stage the next e2e_steps batches (wrapping within the partition stream)
-    lo0 = tr.next_batch(rank)[0]
-    Bw = B
-    nE = len(ev_local)
-    ev_batches, ft_batches = [], []
-    pos = lo0
-    for k in range(e2e_steps):
-        hi = min(nE, pos + Bw)
-        idx = np.arange(pos, hi)
-        eb = torch.empty(len(idx) * 16, dtype=torch.uint8, pin_memory=pin).numpy().view(sp.EDGE_DTYPE)
-        eb[:] = ev_local[idx]
-        fb = torch.empty(len(idx) * max(Fp, 1), dtype=torch.int16, pin_memory=pin).numpy().view(np.uint16)
-        fb = fb.reshape(len(idx), max(Fp, 1))
-        if Fp:
-            sp.edge_features_bf16(cfg.seed_feat, sub_mine.eids[idx], F, Fp, out=fb)
-        ev_batches.append(eb)
-        ft_batches.append(fb)
-        pos = hi if hi < nE else 0
+    nw = len(mine)
+    ev_batches = [[None] * nw for _ in range(e2e_steps)]
+    ft_batches = [[None] * nw for _ in range(e2e_steps)]
+    for j, w in enumerate(mine):
+        ev_local = tr.worker_events(w)
+        pos, _, Fp = tr.next_batch(w)
+        nE = len(ev_local)
+        for k in range(e2e_steps):
+            hi = min(nE, pos + B)
+            idx = np.arange(pos, hi)
+            eb = torch.empty(len(idx) * 16, dtype=torch.uint8, pin_memory=pin).numpy().view(sp.EDGE_DTYPE)
+            eb[:] = ev_local[idx]
+            fb = torch.empty(len(idx) * max(Fp, 1), dtype=torch.int16, pin_memory=pin).numpy().view(np.uint16)
+            fb = fb.reshape(len(idx), max(Fp, 1))
+            if Fp:
+                sp.edge_features_bf16(cfg.seed_feat, subs_mine[j].eids[idx], F, Fp, out=fb)
+            ev_batches[k][j] = eb
+            ft_batches[k][j] = fb
+            pos = hi if hi < nE else 0
     h0, d0 = tr.io_bytes()
-    # one pinned loss slot per step: every step's loss is read back (D2H)
-    loss_pin = torch.empty(e2e_steps, dtype=torch.float32, pin_memory=pin).numpy()
+    # one pinned loss slot per worker and step: every step's losses are read back (D2H)
+    loss_pin = torch.empty(e2e_steps * nw, dtype=torch.float32, pin_memory=pin).numpy()
     barrier(pg)
     t0 = time.perf_counter()
     for k in range(e2e_steps):
-        tr.step_host_async([ev_batches[k]], [ft_batches[k]] if Fp else None, loss_pin[k:k + 1])
+        tr.step_host_async(ev_batches[k], ft_batches[k] if F else None, loss_pin[k * nw:(k + 1) * nw])
     tr.sync()
     t_e2e = time.perf_counter() - t0
     if not np.all(np.isfinite(loss_pin)):
         raise RuntimeError(f"non-finite e2e losses {loss_pin}")
     h1, d1 = tr.io_bytes()
     t_e2e = allreduce_max(pg, t_e2e)
-    e2e_edges = allreduce_sum(pg, float(sum(len(b) for b in ev_batches)))
+    e2e_edges = allreduce_sum(pg, float(sum(len(b) for bs in ev_batches for b in bs)))
     e2e = {"value": e2e_edges / t_e2e, "unit": "edges/s",
            "h2d_bytes_per_step": (h1 - h0) // e2e_steps, "d2h_bytes_per_step": (d1 - d0) // e2e_steps,
            "steps": e2e_steps, "api": "TGNTrainer.step_host_async + sync (spd_tgn_step_host_async)"}
@@ -509,7 +531,7 @@ def main():
         tr.run_steps(args.warmup)
         barrier(pg)
         ms0 = allreduce_max(pg, tr.run_steps(args.fp32_steps))
-        e0 = allreduce_sum(pg, float(sum(min(B, len(sub_mine.edges)) for _ in range(args.fp32_steps))))
+        e0 = allreduce_sum(pg, float(per_step * args.fp32_steps))
         fp32 = {"gemm_mode": 0, "value": e0 / (ms0 / 1e3), "unit": "edges/s",
                 "ms_per_step": ms0 / args.fp32_steps, "steps": args.fp32_steps,
                 "what": "same trainer and workload with every GEMM in FP32 FFMA"}
@@ -534,9 +556,9 @@ def main():
             cent, _ = R.compute_centrality(tre, N, t_max, 0.5)
             hubs = R.select_hubs(cent, 0.05)
             t0 = time.time()
-            R.partition(tre, N, t_max, world, cent, hubs, 0.05)
+            R.partition(tre, N, t_max, P, cent, hubs, args.hub_k)
             extra.append(cpu_partition_baseline({"train_edges": len(tre), "partition_s": time.time() - t0,
-                                                 "subs": [None] * world}))
+                                                 "subs": [None] * P}))
         except Exception as ex:
             extra.append({"what": "reference partition_stream", "value": None, "sample": f"unavailable: {ex}"})
         try:  # the CPU TGN oracle (same model) on all host cores

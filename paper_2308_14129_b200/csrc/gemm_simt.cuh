@@ -31,7 +31,12 @@ namespace gemm {
 
 constexpr int BN = 64, NT = 256, TN = 4;
 
-enum Epi : int { EPI_NONE = 0, EPI_RELU = 1, EPI_MASK = 2 /* C *= (mask > 0) */ };
+enum Epi : int {
+    EPI_NONE = 0,
+    EPI_RELU = 1,
+    EPI_MASK = 2,    // C *= (mask > 0)
+    EPI_ROWMASK = 3  // C = 0 in columns < ldmask of rows with ((const int*) mask)[row] == 0
+};
 
 struct Args {
     const float* A;
@@ -222,6 +227,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(Args a) {
             }
             if (a.epi == EPI_RELU) v = fmaxf(v, 0.f);
             if (a.epi == EPI_MASK) v = a.mask[(size_t)gm * a.ldmask + gn] > 0.f ? v : 0.f;
+            if (a.epi == EPI_ROWMASK && gn < a.ldmask && reinterpret_cast<const int*>(a.mask)[gm] == 0) v = 0.f;
             float* c = a.C + (size_t)gm * a.ldc + gn;
             if (a.beta != 0.f) v += *c;
             *c = v;

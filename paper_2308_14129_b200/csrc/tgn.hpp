@@ -191,6 +191,15 @@ private:
     // weight-gradient GEMMs run on a side stream forked from the main stream at
     // the point their inputs exist, and joined back once per worker step
     void side(const std::function<void(cudaStream_t)>& f, int which = -1);
+    // Critical-path-first issue order: mark() records a point of the main
+    // stream; side_from(mark, f) forks side work from that point AFTER the
+    // main stream's next kernels were created, so graph replays submit the
+    // critical-path kernel first and it claims SMs before the side work.
+    cudaEvent_t mark();
+    void side_from(cudaEvent_t at, const std::function<void(cudaStream_t)>& f);
+    static constexpr int kMarks = 32;
+    cudaEvent_t marks_[kMarks] = {};
+    int mark_next_ = 0;
     void join_side();
     // Side streams: independent off-critical-path work (weight gradients, the
     // neighbour search, Adam) is spread round-robin over kSide streams, each

@@ -54,39 +54,6 @@ __device__ __forceinline__ float4 rnd4(float4 v, int rnd) {
     return rnd ? make_float4(tf32r(v.x), tf32r(v.y), tf32r(v.z), tf32r(v.w)) : v;
 }
 
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-// one-instruction bulk copy global -> shared (TMA engine), completion counted
-// in bytes on an mbarrier
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         std::uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bar_init(std::uint64_t* bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void bar_expect(std::uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bar_wait(std::uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@p bra DONE_%=;\n\t"
-        "bra WAIT_%=;\n"
-        "DONE_%=:\n\t}" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 // One staged neighbour row: [mem f32 D | cos f32 T | sin f32 T (bwd) | feat bf16 Fp]
 // (each part one bulk copy: the memory row, the phi row, the feature row)
 __host__ __device__ __forceinline__ int row_bytes(const Dims& d, bool with_sin) {

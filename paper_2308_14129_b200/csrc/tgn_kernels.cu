@@ -116,7 +116,9 @@ __global__ void k_roots_nbrs(WorkerDev w, int B, int K,
 }
 
 // K1 + K2 for the memory updater: message [s_i | s_j | e | phi(t - t_i^-)]
-// and hidden s_i for every pending node (one warp per node).
+// and hidden s_i for every pending node (one warp per node). 128-bit access:
+// lane l moves memory columns 4l..4l+3 of both endpoint rows and 8 bf16
+// feature columns (one 16-B load), and evaluates 4 time columns.
 __global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const float* time_b,
                              float* x, float* h, int set_slot) {
     pdl_entry();
@@ -127,18 +129,45 @@ __global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const flo
     if (set_slot && lane == 0) w.slot[node] = u;
     float* xr = x + (std::size_t)u * d.ld_x;
     float* hr = h + (std::size_t)u * d.ld_h;
-    const float* mn = w.mem + (std::size_t)node * d.D;
-    const float* mo = w.mem + (std::size_t)other * d.D;
-    for (int c = lane; c < d.D; c += 32) {
-        const float v = rnd_if(mn[c], d.rnd);
-        xr[c] = v;
-        hr[c] = v;
-        xr[d.D + c] = rnd_if(mo[c], d.rnd);
+    const float4* mn = reinterpret_cast<const float4*>(w.mem + (std::size_t)node * d.D);
+    const float4* mo = reinterpret_cast<const float4*>(w.mem + (std::size_t)other * d.D);
+    for (int c4 = lane; c4 < d.D / 4; c4 += 32) {
+        const float4 v = rnd4_if(__ldg(mn + c4), d.rnd);
+        reinterpret_cast<float4*>(xr)[c4] = v;
+        reinterpret_cast<float4*>(hr)[c4] = v;
+        reinterpret_cast<float4*>(xr + d.D)[c4] = rnd4_if(__ldg(mo + c4), d.rnd);
     }
-    const __nv_bfloat16* fr = w.feat + (std::size_t)ev * d.Fp;
-    for (int c = lane; c < d.F; c += 32) xr[2 * d.D + c] = __bfloat162float(fr[c]);
-    for (int c = lane; c < d.T; c += 32)
-        xr[2 * d.D + d.F + c] = rnd_if(time_cos(time_w[c], time_b[c], dt), d.rnd);
+    const uint4* fr = reinterpret_cast<const uint4*>(w.feat + (std::size_t)ev * d.Fp);
+    float* xf = xr + 2 * d.D;
+    for (int c8 = lane; 8 * c8 < d.F; c8 += 32) {  // bf16 -> f32 is exact
+        const uint4 raw = __ldg(fr + c8);
+        const float f[8] = {__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
+                            __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u),
+                            __uint_as_float(raw.z << 16), __uint_as_float(raw.z & 0xFFFF0000u),
+                            __uint_as_float(raw.w << 16), __uint_as_float(raw.w & 0xFFFF0000u)};
+        if (8 * c8 + 8 <= d.F) {
+            reinterpret_cast<float4*>(xf)[2 * c8] = make_float4(f[0], f[1], f[2], f[3]);
+            reinterpret_cast<float4*>(xf)[2 * c8 + 1] = make_float4(f[4], f[5], f[6], f[7]);
+        } else {
+            for (int q = 0; q < 8 && 8 * c8 + q < d.F; ++q) xf[8 * c8 + q] = f[q];
+        }
+    }
+    // time columns start at 2D + F: 16-, 8- or 4-B aligned by F mod 4
+    float* xt = xr + 2 * d.D + d.F;
+    for (int c4 = lane; c4 < d.T / 4; c4 += 32) {
+        const float4 tw = __ldg(reinterpret_cast<const float4*>(time_w) + c4);
+        const float4 tb = __ldg(reinterpret_cast<const float4*>(time_b) + c4);
+        const float2 a = make_float2(rnd_if(time_cos(tw.x, tb.x, dt), d.rnd), rnd_if(time_cos(tw.y, tb.y, dt), d.rnd));
+        const float2 b = make_float2(rnd_if(time_cos(tw.z, tb.z, dt), d.rnd), rnd_if(time_cos(tw.w, tb.w, dt), d.rnd));
+        if (d.F % 4 == 0) {
+            reinterpret_cast<float4*>(xt)[c4] = make_float4(a.x, a.y, b.x, b.y);
+        } else if (d.F % 2 == 0) {
+            reinterpret_cast<float2*>(xt)[2 * c4] = a;
+            reinterpret_cast<float2*>(xt)[2 * c4 + 1] = b;
+        } else {
+            xt[4 * c4] = a.x; xt[4 * c4 + 1] = a.y; xt[4 * c4 + 2] = b.x; xt[4 * c4 + 3] = b.y;
+        }
+    }
 }
 
 // GRUCell (PyTorch gate order r, z, n) on G_i = W_ih x + b_ih, G_h = W_hh h + b_hh.
@@ -169,29 +198,31 @@ __global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh,
 // K1 + K2 for the attention query: q_in = [s_root | phi(0)] (one warp per
 // root). The key/value rows are gathered inside the attention kernels
 // (tgn_attn.cu) and never stored.
+// The roots' memory rows go to both of their readers: the query input
+// [s_root | phi(0)] and the MergeLayer input's s_root columns (m_in[:, DQ:];
+// its attention columns come from the output-projection GEMM's row-masked
+// epilogue), so m_in needs no gather of its own.
 __global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* roots,
-                               const float* mem_new, float* q_in) {
+                               const float* mem_new, float* q_in, float* m_in) {
     pdl_entry();
     const int row = warp_id_global(), lane = lane_id();
     if (row >= R) return;
-    const float* m = memx_row(w, mem_new, d.D, roots[row]);
+    const float4* m = reinterpret_cast<const float4*>(memx_row(w, mem_new, d.D, roots[row]));
     float* q = q_in + (std::size_t)row * d.ld_q;
-    for (int c = lane; c < d.D; c += 32) q[c] = rnd_if(m[c], d.rnd);
-    for (int c = lane; c < d.T; c += 32) q[d.D + c] = rnd_if(time_cos(time_w[c], time_b[c], 0.0), d.rnd);
-}
-
-// MergeLayer input [attn | s_root]; attn = 0 for a root without neighbours.
-__global__ void k_merge_gather(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
-                               const int* cnt, const float* O, const float* mem_new, float* m_in) {
-    pdl_entry();
-    const int r = warp_id_global(), lane = lane_id();
-    if (r >= R) return;
-    float* o = m_in + (std::size_t)r * d.ld_m;
-    const bool has = cnt[r] > 0;
-    for (int c = lane; c < d.DQ; c += 32) o[c] = has ? rnd_if(O[(std::size_t)r * d.DQ + c], d.rnd) : 0.f;
-    const float* m = memx_row(w, mem_new, d.D, roots[r]);
-    for (int c = lane; c < d.D; c += 32) o[d.DQ + c] = rnd_if(m[c], d.rnd);
+    float* mi = m_in ? m_in + (std::size_t)row * d.ld_m + d.DQ : nullptr;
+    for (int c4 = lane; c4 < d.D / 4; c4 += 32) {
+        const float4 v = rnd4_if(m[c4], d.rnd);
+        reinterpret_cast<float4*>(q)[c4] = v;
+        if (mi) reinterpret_cast<float4*>(mi)[c4] = v;
+    }
+    for (int c4 = lane; c4 < d.T / 4; c4 += 32) {
+        const float4 tw = __ldg(reinterpret_cast<const float4*>(time_w) + c4);
+        const float4 tb = __ldg(reinterpret_cast<const float4*>(time_b) + c4);
+        reinterpret_cast<float4*>(q + d.D)[c4] =
+            make_float4(rnd_if(time_cos(tw.x, tb.x, 0.0), d.rnd), rnd_if(time_cos(tw.y, tb.y, 0.0), d.rnd),
+                        rnd_if(time_cos(tw.z, tb.z, 0.0), d.rnd), rnd_if(time_cos(tw.w, tb.w, 0.0), d.rnd));
+    }
 }
 
 // Decoder input rows: p < B -> [z_src | z_dst], p >= B -> [z_src | z_neg].
@@ -201,10 +232,12 @@ __global__ void k_dec_gather(Dims d, int B, const float* emb, float* d_in) {
     if (p >= 2 * B) return;
     const int i = p < B ? p : p - B;
     const int other = p < B ? B + i : 2 * B + i;
-    float* o = d_in + (std::size_t)p * d.ld_din;
-    for (int c = lane; c < d.D; c += 32) {
-        o[c] = emb[(std::size_t)i * d.D + c];
-        o[d.D + c] = emb[(std::size_t)other * d.D + c];
+    float4* o = reinterpret_cast<float4*>(d_in + (std::size_t)p * d.ld_din);
+    const float4* a = reinterpret_cast<const float4*>(emb + (std::size_t)i * d.D);
+    const float4* b = reinterpret_cast<const float4*>(emb + (std::size_t)other * d.D);
+    for (int c4 = lane; c4 < d.D / 4; c4 += 32) {
+        o[c4] = a[c4];
+        o[d.D / 4 + c4] = b[c4];
     }
 }
 
@@ -265,6 +298,165 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
     __syncwarp();
     float* dx = dD1 + (std::size_t)p * d.D;
     for (int c = lane; c < d.D; c += 32) dx[c] = x[c] > 0.f ? g * w2[c] : 0.f;
+}
+
+// K7 fused decoder (FP32 FFMA, the north star's rule for the decoder): per
+// block of kDecEv events, from the embeddings of their src / dst / negative
+// roots to the data gradient of those embeddings, in one launch —
+//   Y_src = W_a z_src, Y_dst = W_b z_dst, Y_neg = W_b z_neg
+//   D1 = relu(Y_src + Y_{dst|neg} + b1); logit = D1 . w2 + b2; BCE terms
+//   dlogit = (sigmoid - y) / B; dD1 = [D1 > 0] dlogit w2
+//   d_src = (dD1_pos + dD1_neg) W_a, d_dst = dD1_pos W_b, d_neg = dD1_neg W_b
+// (the MergeLayer of oracle/tgn_oracle.py _decode applied to [z_u | z_v] by
+// input halves). W1 = [W_a | W_b | b1] rows (row stride ld1) are staged in
+// shared memory once per block; thread (kind, n) owns output column n of the
+// block's kDecEv rows of one kind (src, dst, neg) and reads its weight row /
+// column with 16-B loads while the activations broadcast. Writes D1, dlogit,
+// dD1 (the weight gradients' inputs), loss terms, logits and d_emb. bwd = 0
+// (evaluation): forward and logits only.
+__global__ void __launch_bounds__(768)
+    k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2, float* D1,
+              float* dlogit, float* lossv, float* dD1, float* logits, float* d_emb, int bwd) {
+    pdl_entry();
+    extern __shared__ __align__(16) float dsm[];
+    const int D = d.D, ldw = 2 * D + 4, ldz = D + 4;
+    float* sW = dsm;                                  // [D][ldw]: W_a | W_b | b1
+    float* sZ = sW + (std::size_t)D * ldw;            // [3 EV][ldz]: z rows; later dD1 [2 EV]
+    float* sY = sZ + 3 * kDecEv * ldz;                // [3 EV][ldz]
+    float* sD1 = sY + 3 * kDecEv * ldz;               // [2 EV][ldz]
+    float* sw2 = sD1 + 2 * kDecEv * ldz;              // [ldz]
+    float* sg = sw2 + ldz;                            // [2 EV]
+    float* sdD1 = sZ;
+    __shared__ __align__(8) std::uint64_t bar;
+    const int i0 = blockIdx.x * kDecEv;
+    const int nev = min(kDecEv, B - i0);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    // stage the weight rows (cols 0 .. 2D+3: W_a | W_b | b1 | pad) and the
+    // block's embedding rows with TMA bulk copies issued by warp 0 on one mbarrier
+    if (tid < 32) {
+        if (tid == 0) {
+            bar_init(&bar);
+            bar_expect(&bar, unsigned(D * ldw * 4 + 3 * nev * D * 4));
+        }
+        __syncwarp();
+        for (int n = tid; n < D; n += 32)
+            bulk_g2s(sW + (std::size_t)n * ldw, W1 + (std::size_t)n * ld1, unsigned(ldw * 4), &bar);
+        for (int r = tid; r < 3 * nev; r += 32) {
+            const int kind = r / nev, e = r % nev;
+            bulk_g2s(sZ + (std::size_t)(kind * kDecEv + e) * ldz, emb + ((std::size_t)kind * B + i0 + e) * D,
+                     unsigned(D * 4), &bar);
+        }
+    }
+    for (int i = tid; i < 3 * (kDecEv - nev) * D; i += nt) {  // rows past the batch: zero
+        const int r = i / D, kind = r / (kDecEv - nev), e = nev + r % (kDecEv - nev);
+        sZ[(std::size_t)(kind * kDecEv + e) * ldz + i % D] = 0.f;
+    }
+    for (int i = tid; i <= D; i += nt) sw2[i] = w2[i];
+    __syncthreads();  // (barrier initialised before anyone waits)
+    bar_wait(&bar, 0);
+    // forward projections: thread (kind, n)
+    if (tid < 3 * D) {
+        const int kind = tid / D, n = tid % D;
+        const float* wr = sW + (std::size_t)n * ldw + (kind ? D : 0);
+        const float* z = sZ + (std::size_t)kind * kDecEv * ldz;
+        float acc[kDecEv];
+#pragma unroll
+        for (int e = 0; e < kDecEv; ++e) acc[e] = 0.f;
+#pragma unroll 2
+        for (int k = 0; k < D; k += 4) {
+            const float4 w = *reinterpret_cast<const float4*>(wr + k);
+#pragma unroll
+            for (int e = 0; e < kDecEv; ++e) {
+                const float4 x = *reinterpret_cast<const float4*>(z + (std::size_t)e * ldz + k);
+                acc[e] = fmaf(x.x, w.x, acc[e]);
+                acc[e] = fmaf(x.y, w.y, acc[e]);
+                acc[e] = fmaf(x.z, w.z, acc[e]);
+                acc[e] = fmaf(x.w, w.w, acc[e]);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kDecEv; ++e) sY[(std::size_t)(kind * kDecEv + e) * ldz + n] = acc[e];
+    }
+    __syncthreads();
+    // D1 rows: p < EV positive (src, dst), p >= EV negative (src, neg)
+    for (int i = tid; i < 2 * kDecEv * D; i += nt) {
+        const int p = i / D, n = i % D, e = p % kDecEv;
+        const float v = sY[(std::size_t)e * ldz + n] + sY[(std::size_t)((p < kDecEv ? 1 : 2) * kDecEv + e) * ldz + n] +
+                        sW[(std::size_t)n * ldw + 2 * D];
+        const float x = fmaxf(v, 0.f);
+        sD1[(std::size_t)p * ldz + n] = x;
+        if (bwd && e < nev) D1[(std::size_t)((p < kDecEv ? 0 : B) + i0 + e) * d.ld_d1 + n] = x;
+    }
+    __syncthreads();
+    // logits and BCE terms: one warp per pair row
+    {
+        const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+        for (int p = warp; p < 2 * kDecEv; p += nw) {
+            const int e = p % kDecEv;
+            const float* x = sD1 + (std::size_t)p * ldz;
+            float acc = 0.f;
+            for (int c = lane; c < D; c += 32) acc += x[c] * sw2[c];
+            acc = warp_sum(acc) + sw2[D];
+            const bool pos = p < kDecEv;
+            const float g = (sigmoidf_(acc) - (pos ? 1.f : 0.f)) / (float)B;
+            if (lane == 0) {
+                sg[p] = g;
+                if (e < nev) {
+                    const std::size_t gp = (pos ? 0 : B) + i0 + e;
+                    if (bwd) dlogit[gp * 4] = g;
+                    lossv[gp] = (pos ? softplusf(-acc) : softplusf(acc)) / (float)B;
+                    if (logits) logits[gp] = acc;
+                }
+            }
+        }
+    }
+    if (!bwd) return;
+    __syncthreads();
+    for (int i = tid; i < 2 * kDecEv * D; i += nt) {  // dD1 -> global (the weight gradients' input)
+        const int p = i / D, n = i % D, e = p % kDecEv;
+        const float v = sD1[(std::size_t)p * ldz + n] > 0.f ? sg[p] * sw2[n] : 0.f;
+        sD1[(std::size_t)p * ldz + n] = v;  // (D1 itself is no longer read)
+        if (e < nev) dD1[(std::size_t)((p < kDecEv ? 0 : B) + i0 + e) * D + n] = v;
+    }
+    __syncthreads();
+    // per-row output gradients of the three embedding kinds (over the z rows,
+    // no longer read): src rows take both pairs of their event
+    for (int i = tid; i < 3 * kDecEv * D; i += nt) {
+        const int r = i / D, n = i % D, kind = r / kDecEv, e = r % kDecEv;
+        const float gp = sD1[(std::size_t)e * ldz + n], gn = sD1[(std::size_t)(kDecEv + e) * ldz + n];
+        sdD1[(std::size_t)r * ldz + n] = kind == 0 ? gp + gn : kind == 1 ? gp : gn;
+    }
+    __syncthreads();
+    // data gradients d_emb[kind][e][k] = sum_n G[kind][e][n] W_kind[n][k]: thread (kind, k)
+    if (tid < 3 * D) {
+        const int kind = tid / D, k = tid % D;
+        const float* wc = sW + (kind ? D : 0) + k;  // column k of W_a / W_b
+        const float* g = sdD1 + (std::size_t)kind * kDecEv * ldz;
+        float acc[kDecEv];
+#pragma unroll
+        for (int e = 0; e < kDecEv; ++e) acc[e] = 0.f;
+#pragma unroll 2
+        for (int n = 0; n < D; n += 4) {
+            const float w0 = wc[(std::size_t)n * ldw], w1 = wc[(std::size_t)(n + 1) * ldw],
+                        w2_ = wc[(std::size_t)(n + 2) * ldw], w3 = wc[(std::size_t)(n + 3) * ldw];
+#pragma unroll
+            for (int e = 0; e < kDecEv; ++e) {
+                const float4 x = *reinterpret_cast<const float4*>(g + (std::size_t)e * ldz + n);
+                acc[e] = fmaf(x.x, w0, acc[e]);
+                acc[e] = fmaf(x.y, w1, acc[e]);
+                acc[e] = fmaf(x.z, w2_, acc[e]);
+                acc[e] = fmaf(x.w, w3, acc[e]);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kDecEv; ++e)
+            if (e < nev) d_emb[((std::size_t)kind * B + i0 + e) * D + k] = rnd_if(acc[e], d.rnd);
+    }
+}
+
+std::size_t decoder_smem_bytes(const Dims& d) {
+    const std::size_t D = d.D, ldw = 2 * D + 4, ldz = D + 4;
+    return 4 * (D * ldw + 8 * kDecEv * ldz + ldz + 2 * kDecEv);
 }
 
 // Fixed-order single-block sum (deterministic loss).
@@ -389,7 +581,9 @@ __global__ void k_persist(WorkerDev w, int D, const float* mem_new) {
     const int u = warp_id_global(), lane = lane_id();
     if (u >= *w.nU) return;
     const std::uint32_t node = w.pU[u];
-    for (int c = lane; c < D; c += 32) w.mem[(std::size_t)node * D + c] = mem_new[(std::size_t)u * D + c];
+    for (int c4 = lane; c4 < D / 4; c4 += 32)  // 128-bit rows (D % 4 == 0)
+        reinterpret_cast<float4*>(w.mem + (std::size_t)node * D)[c4] =
+            reinterpret_cast<const float4*>(mem_new + (std::size_t)u * D)[c4];
     if (lane == 0) {
         w.lu[node] = w.pTs[u];
         w.slot[node] = -1;

@@ -134,7 +134,7 @@ __global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh,
                           float* save, float* mem_new);
 __global__ void k_query_gather(WorkerDev w, Dims d, int R, const float* time_w,
                                const float* time_b, const std::uint32_t* roots,
-                               const float* mem_new, float* q_in);
+                               const float* mem_new, float* q_in, float* m_in);
 // absorbed-projection attention (tgn_attn.cu): 4 roots per 128-thread block,
 // dynamic shared memory attn_smem_bytes(d, bwd); lane slots per region
 // NM = ceil(D / 128), NT = ceil(T / 128), NF = ceil((F + 1) / 128); HMAX >= H
@@ -165,6 +165,12 @@ __global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, floa
 __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, const float* W1,
                             int ld1, const float* w2, float* D1, float* dlogit, float* lossv,
                             float* dD1, float* logits);
+constexpr int kDecEv = 8;  // events per k_decoder block
+// k_decoder launches roundup(3 d_mem, 32) threads (<= 768)
+__global__ void k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2,
+                          float* D1, float* dlogit, float* lossv, float* dD1, float* logits,
+                          float* d_emb, int bwd);
+std::size_t decoder_smem_bytes(const Dims& d);
 __global__ void k_sum_loss(const float* lossv, int n, float* out);
 __global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb);
 __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt);

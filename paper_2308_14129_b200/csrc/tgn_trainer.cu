@@ -432,6 +432,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     }
     side_ = sides_[0];
     SPD_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    for (auto& e : marks_) SPD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 
     SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
     SPD_CUDA(cudaStreamCreateWithPriority(&zs_, cudaStreamNonBlocking, prio_lo));
@@ -577,6 +578,22 @@ void TGNTrainer::side(const std::function<void(cudaStream_t)>& f, int which) {
     f(sides_[k]);
 }
 
+cudaEvent_t TGNTrainer::mark() {
+    cudaEvent_t e = marks_[mark_next_++ % kMarks];
+    SPD_CUDA(cudaEventRecord(e, stream_));
+    return e;
+}
+
+void TGNTrainer::side_from(cudaEvent_t at, const std::function<void(cudaStream_t)>& f) {
+    const int k = side_next_++ % kSide;
+    SPD_CUDA(cudaStreamWaitEvent(sides_[k], at, 0));
+    const std::size_t slice = s_->ws.n / kSide;
+    ws_cur_ = s_->ws.p + slice * k;
+    wsn_cur_ = slice;
+    side_used_[k] = true;
+    f(sides_[k]);
+}
+
 void TGNTrainer::join_side() {
     for (int k = 0; k < kSide; ++k) {
         if (!side_used_[k]) continue;
@@ -595,6 +612,8 @@ TGNTrainer::~TGNTrainer() {
     if (ctl_ring_) cudaFreeHost(ctl_ring_);
     if (stage_) cudaFreeHost(stage_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
+    for (auto e : marks_)
+        if (e) cudaEventDestroy(e);
     for (int k = 0; k < kSide; ++k) {
         if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
         if (sides_[k]) cudaStreamDestroy(sides_[k]);
@@ -904,27 +923,32 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         side([&](cudaStream_t sd) { launch(tgnk::k_pending, 1, 1024, 0, sd, wd, B); });
     // (the side-stream branch is forked after the GRU's first kernel is
     // enqueued: graph replays submit independent branches in creation order)
+    cudaEvent_t at_gather = nullptr;
     auto fork_roots = [&] {
-        side([&](cudaStream_t sd) {
+        side_from(at_gather, [&](cudaStream_t sd) {
             roots(sd);
             SPD_CUDA(cudaEventRecord(ev_roots_, sd));
             if (train) {
                 dh_index(wd, s, sd);
                 SPD_CUDA(cudaEventRecord(ev_dhidx_, sd));  // the dH index is ready
             }
-        }, 0);
+        });
     };
     timed("gru_fwd", [&] {
         gru_forward(w, wd, train, [&] {
             if (profile_) return;  // (the index reads the slots the gather sets)
-            fork_roots();
+            at_gather = mark();
         });
     });
+    // forked from the gather's end, but created after the GRU's GEMMs and cell
+    // so replays hand those their SMs first
+    if (!profile_) fork_roots();
     if (profile_ && train) timed("dh_index", [&] { dh_index(wd, s, st); });
     if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_roots_, 0));
     timed("query_gather", [&] {
         launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
-               P + lay_.time_w, P + lay_.time_b, s.roots.p, s.mem_new.p, s.q_in.p);
+               P + lay_.time_w, P + lay_.time_b, s.roots.p, s.mem_new.p, s.q_in.p,
+               train && tc && head_fits_ ? nullptr : s.m_in.p);
     });
     timed("gemm_q", [&] {
         proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
@@ -969,27 +993,30 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         launch(tgnk::k_head, unsigned((B + eb - 1) / eb), 256, sm, st, h);
     });
     else timed("head_fwd", [&] {
-        proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.O.p, d.DQ, R, d.DQ,
-                 d.DQ + 1, nullptr, st);
-        launch(tgnk::k_merge_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, 
-            wd, d, R, s.roots.p, s.cnt.p, s.O.p, s.mem_new.p, s.m_in.p);
+        // O = [ctx | 1] W_o^T straight into the MergeLayer input's attention
+        // columns, 0 for roots without neighbours (the s_root columns came
+        // with the query gather)
+        proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.m_in.p, d.ld_m, R, d.DQ,
+                 d.DQ + 1, nullptr, st, gemm::EPI_ROWMASK, reinterpret_cast<const float*>(s.cnt.p), d.DQ, tc);
         proj_fwd(tc, s.m_in.p, d.ld_m, PW + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
                  d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU, nullptr, 0, tc);
         proj_fwd(tc, s.Z1.p, d.ld_z, PW + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
                  nullptr, st);
-        // decoder layer 1 split by input halves (k_dec_head2): the src half on
-        // the aux stream, the dst/negative half on the main stream
-        const float* W1 = P + lay_.dec1.off;
-        SPD_CUDA(cudaEventRecord(ev_aux_fork_, st));
-        SPD_CUDA(cudaStreamWaitEvent(aux_, ev_aux_fork_, 0));
-        gemm_fwd(s.emb.p, d.D, W1, lay_.dec1.ld, s.Ya.p, d.D, B, d.D, d.D, nullptr, aux_);
-        gemm_fwd(s.emb.p + std::size_t(B) * d.D, d.D, W1 + d.D, lay_.dec1.ld, s.Yb.p, d.D, 2 * B, d.D,
-                 d.D, nullptr, st);
-        SPD_CUDA(cudaEventRecord(ev_aux_join_, aux_));
-        SPD_CUDA(cudaStreamWaitEvent(st, ev_aux_join_, 0));
-        launch(tgnk::k_dec_head2, blocks_for(std::size_t(2 * B) * 32), 256, 0, st, d, B,
-               static_cast<const float*>(s.Ya.p), static_cast<const float*>(s.Yb.p), W1,
-               lay_.dec1.ld, P + lay_.dec2.off, s.D1.p, s.dlogit.p, s.lossv.p, s.dD1.p, s.logits.p);
+        // the decoder, its loss and its data gradient: one FFMA kernel (k_decoder;
+        // its TMA row copies need 16-B aligned weight rows)
+        if (lay_.dec1.off % 4 || lay_.dec1.ld % 4) internal_error("InvalidParams", "decoder rows unaligned");
+        static std::size_t dec_smem_set = 0;
+        const std::size_t dsm = tgnk::decoder_smem_bytes(d);
+        if (dsm > dec_smem_set) {
+            SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(dsm)));
+            dec_smem_set = dsm;
+        }
+        launch(tgnk::k_decoder, unsigned((B + tgnk::kDecEv - 1) / tgnk::kDecEv),
+               unsigned((3 * d.D + 31) / 32 * 32), dsm, st, d, B, static_cast<const float*>(s.emb.p),
+               static_cast<const float*>(P + lay_.dec1.off), lay_.dec1.ld,
+               static_cast<const float*>(P + lay_.dec2.off), s.D1.p, s.dlogit.p, s.lossv.p, s.dD1.p,
+               s.logits.p, s.d_emb.p, train ? 1 : 0);
     });
     // the batch loss is only read by the host after the step: off the critical path
     auto sum_loss = [&](cudaStream_t sx) {
@@ -1042,34 +1069,41 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fuse
                                                lay_.att_o.ld, d.DQ, d.DQ + 1, R, nullptr, ws_cur_,
                                                wsn_cur_, sd); });
     } else timed("head_bwd", [&] {
-        side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off, lay_.dec2.ld, 1, d.D + 1,
-                   2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
-        side([&](cudaStream_t sd) {
+        // (d_emb came with the forward: k_decoder). Each data-gradient GEMM is
+        // created before the weight-gradient side work forked from the same
+        // point, so replays hand the critical path its SMs first.
+        // merge layer 2 (relu mask from Z1)
+        cudaEvent_t at = mark();
+        proj_dgrad(tc, s.d_emb.p, d.D, PW + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
+                   nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z, tc);
+        side_from(at, [&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off,
+                                                        lay_.dec2.ld, 1, d.D + 1, 2 * B, nullptr, ws_cur_,
+                                                        wsn_cur_, sd); });
+        side_from(at, [&](cudaStream_t sd) {
             // the gathered decoder input [z_u | z_v | 1] is only needed here
             launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, sd, d, B,
                    s.emb.p, s.d_in.p);
             gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
                    2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
-        gemm_dgrad(s.dD1.p, d.D, P + lay_.dec1.off, lay_.dec1.ld, s.dd_in.p, d.ld_din, 2 * B,
-                   2 * d.D, d.D, nullptr, st);
-        launch(tgnk::k_dec_scatter, blocks_for(std::size_t(B) * 32), 256, 0, st, d, B, s.dd_in.p,
-                                                                             s.d_emb.p);
-        // merge layer 2 (relu mask from Z1), layer 1
-        side([&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off, lay_.mrg2.ld, d.D, d.D + 1,
-                   R, nullptr, ws_cur_, wsn_cur_, sd); });
-        proj_dgrad(tc, s.d_emb.p, d.D, PW + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
-                   nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z, tc);
-        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off, lay_.mrg1.ld, d.D,
-                   d.DQ + d.D + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
+        side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off,
+                                                        lay_.mrg2.ld, d.D, d.D + 1, R, nullptr, ws_cur_,
+                                                        wsn_cur_, sd); });
+        // merge layer 1
+        at = mark();
+        // (attention columns of roots without neighbours: 0)
         proj_dgrad(tc, s.dZ1.p, d.D, PW + lay_.mrg1.off, lay_.mrg1.ld, s.dm_in.p, d.ld_m, R,
-                   d.DQ + d.D, d.D, nullptr, st, 0, nullptr, 0, tc);
-        launch(tgnk::k_mask_rows, blocks_for(std::size_t(R) * 32), 256, 0, st, s.dm_in.p, R, d.DQ,
-                                                                          d.ld_m, s.cnt.p);
+                   d.DQ + d.D, d.D, nullptr, st, gemm::EPI_ROWMASK, reinterpret_cast<const float*>(s.cnt.p),
+                   d.DQ, tc);
+        side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off,
+                                                        lay_.mrg1.ld, d.D, d.DQ + d.D + 1, R, nullptr,
+                                                        ws_cur_, wsn_cur_, sd); });
         // output projection
-        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld, d.DQ,
-                   d.DQ + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
+        at = mark();
         proj_dgrad(tc, s.dm_in.p, d.ld_m, PW + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R, d.DQ,
                    d.DQ, nullptr, st, 0, nullptr, 0, tc);
+        side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx,
+                                                        G + lay_.att_o.off, lay_.att_o.ld, d.DQ, d.DQ + 1,
+                                                        R, nullptr, ws_cur_, wsn_cur_, sd); });
     });
     const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
     const float* WK = PW + lay_.att_kv.off;
@@ -1080,12 +1114,13 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fuse
     const std::ptrdiff_t wst = std::ptrdiff_t(dh) * ldw;  // per-head weight slab
     timed("gemm_dxbar", [&] {
         // dW_V,h += dctx_h^T xbar_h ; dxbar_h = dctx_h [W_V,h | b_V,h]
-        side([&](cudaStream_t sd) {
+        cudaEvent_t at = mark();
+        proj_dgrad(tc, s.dctx.p, d.ld_Q, WV, ldw, s.dxbar.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0,
+                   nullptr, 0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
+        side_from(at, [&](cudaStream_t sd) {
             proj_wgrad(tc, s.dctx.p, d.ld_Q, s.xbar.p, ldhp, GV, ldw, dh, d.DK + 1, R, nullptr, ws_cur_,
                        wsn_cur_, sd, umma::Batch{d.H, dh, d.ld_p, wst});
         });
-        proj_dgrad(tc, s.dctx.p, d.ld_Q, WV, ldw, s.dxbar.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0,
-                   nullptr, 0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
     });
     double* attn_part = s.tpart.p + std::size_t(s.troot_blocks) * 2 * d.T;
     timed("k_attn_abs_bwd", [&] {
@@ -1095,41 +1130,41 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fuse
     // (k_dh_pull, deterministic, tgn_dh.cu) and the time-encoder partials —
     // run beside the dQ GEMMs; the GRU backward and the time-grad reduction
     // wait for them
-    auto fork_x = [&] {
-        if (profile_) {
-            timed("dh_pull", [&] { dh_pull(d, s, st); });
-            timed("attn_time_grad", [&] { attn_time_grad(d, R, P + lay_.time_w, P + lay_.time_b, s, attn_part, st); });
-            return;
-        }
-        side([&](cudaStream_t sd) {
+    if (profile_) {
+        timed("dh_pull", [&] { dh_pull(d, s, st); });
+        timed("attn_time_grad", [&] { attn_time_grad(d, R, P + lay_.time_w, P + lay_.time_b, s, attn_part, st); });
+    }
+    cudaEvent_t at_bwd = mark();  // the attention backward is done
+    timed("gemm_dq", [&] {
+        // dQ_h = dQp_h [W_K,h | b_K,h]^T
+        proj_fwd(tc, s.dQp.p, ldhp, WK, ldw, s.dQ.p, d.ld_Q, R, dh, d.DK + 1, nullptr, st, 0, nullptr,
+                 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
+    });
+    if (!profile_) {
+        // the attention input gradients (dH pull, time-encoder partials) and
+        // dW_K beside the query backward: created after the dQ GEMM
+        side_from(at_bwd, [&](cudaStream_t sd) {
             SPD_CUDA(cudaStreamWaitEvent(sd, ev_dhidx_, 0));  // the dH reader index
             dh_pull(d, s, sd);
             SPD_CUDA(cudaEventRecord(ev_pull_, sd));
         });
-        side([&](cudaStream_t sd) {
+        side_from(at_bwd, [&](cudaStream_t sd) {
             attn_time_grad(d, R, P + lay_.time_w, P + lay_.time_b, s, attn_part, sd);
             SPD_CUDA(cudaEventRecord(ev_bwdx_, sd));
         });
-    };
-    auto fork_wk = [&] {
-        // dW_K,h += Q_h^T dQp_h
-        side([&](cudaStream_t sd) {
-            proj_wgrad(tc, s.Q.p, d.ld_Q, s.dQp.p, ldhp, GK, ldw, dh, d.DK + 1, R, nullptr, ws_cur_,
-                       wsn_cur_, sd, umma::Batch{d.H, dh, d.ld_p, wst});
-        });
-    };
-    fork_x();
-    timed("gemm_dq", [&] {
-        // dQ_h = dQp_h [W_K,h | b_K,h]^T
-        fork_wk();
-        proj_fwd(tc, s.dQp.p, ldhp, WK, ldw, s.dQ.p, d.ld_Q, R, dh, d.DK + 1, nullptr, st, 0, nullptr,
-                 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
+    }
+    // dW_K,h += Q_h^T dQp_h
+    side_from(at_bwd, [&](cudaStream_t sd) {
+        proj_wgrad(tc, s.Q.p, d.ld_Q, s.dQp.p, ldhp, GK, ldw, dh, d.DK + 1, R, nullptr, ws_cur_,
+                   wsn_cur_, sd, umma::Batch{d.H, dh, d.ld_p, wst});
     });
     timed("q_bwd", [&] {
-        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
-                   d.DQ + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
+        cudaEvent_t at = mark();
         proj_dgrad(tc, s.dQ.p, d.ld_Q, PW + lay_.att_q.off, lay_.att_q.ld, s.dq_in.p, d.ld_q, R, d.DQ,
                    d.DQ, nullptr, st);
+        side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off,
+                                                        lay_.att_q.ld, d.DQ, d.DQ + 1, R, nullptr, ws_cur_,
+                                                        wsn_cur_, sd); });
     });
     // root-side time-encoder partials and their reduction with the attention
     // partials: only the all-reduce reads the result, so off the critical path

@@ -36,7 +36,7 @@ constexpr int STAGES = 4;
 constexpr int THREADS = 192;
 
 enum Mode : int { STORE = 0, ACCUM = 1, PARTIAL = 2 };
-enum Epi : int { EPI_NONE = 0, EPI_RELU = 1, EPI_MASK = 2 };
+enum Epi : int { EPI_NONE = 0, EPI_RELU = 1, EPI_MASK = 2, EPI_ROWMASK = 3 /* gemm_simt.cuh */ };
 
 struct Args {
     float* C;
@@ -346,6 +346,10 @@ __global__ void __launch_bounds__(THREADS, (BN * NSUB <= 64 ? 3 : 2))
             __syncwarp();
             const int col = n0 + c0 + lane;
             const int rows = min(32, M - row0);
+            unsigned zero_rows = 0;  // EPI_ROWMASK: rows of this warp's slab with count 0
+            if (args.epi == EPI_ROWMASK)
+                zero_rows = __ballot_sync(0xffffffffu, lane < rows &&
+                                                           reinterpret_cast<const int*>(args.mask)[row0 + lane] == 0);
             if (col < args.N && rows > 0) {
                 float* c = out_base + (std::size_t)row0 * ldo + col;
                 // mode/epilogue are CTA-uniform: branch once, keep the plain
@@ -364,6 +368,15 @@ __global__ void __launch_bounds__(THREADS, (BN * NSUB <= 64 ? 3 : 2))
 #pragma unroll
                     for (int r = 0; r < 32; ++r)
                         if (r < rows) c[(std::size_t)r * ldo] = cv[r] + stage[r * 33 + lane];
+                } else if (args.epi == EPI_ROWMASK) {
+                    // rows whose count is 0 are zero in the columns < ldmask
+                    const bool masked_col = col < args.ldmask;
+#pragma unroll 8
+                    for (int r = 0; r < rows; ++r) {
+                        const bool z = masked_col && ((zero_rows >> r) & 1u);
+                        const float x = z ? 0.f : stage[r * 33 + lane];
+                        c[(std::size_t)r * ldo] = args.rnd ? tf32_rn(x) : x;
+                    }
                 } else if (args.epi == EPI_RELU) {
 #pragma unroll 8
                     for (int r = 0; r < rows; ++r) {
