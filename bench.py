@@ -445,6 +445,13 @@ def main():
             acc[n] = acc.get(n, 0.0) + t / n_prof
     phases = list(acc.items())
     tr.set_profile(False)
+    # epoch-end work (pac_sim.cpp:259-260): restore the loop-end snapshots and
+    # sync SEP's shared hubs across every worker (host wall clock around the
+    # synchronous call; outside the timed steps)
+    barrier(pg)
+    t0 = time.perf_counter()
+    tr.end_epoch()
+    epoch_end_ms = allreduce_max(pg, (time.perf_counter() - t0) * 1e3)
 
     # end-to-end through the public API from pinned host buffers: every local
     # worker's next e2e_steps batches (wrapping within its partition stream,
@@ -581,6 +588,7 @@ def main():
             "effective_edges_per_s": wl["train_edges"] / (tr.epoch_steps() * ms_per_step / 1e3),
             "device_memory_per_gpu": mem_gb,
             "epoch_steps": tr.epoch_steps(), "train_edges": wl["train_edges"],
+            "shared_hubs": len(wl["shared"]), "epoch_end_sync_ms": epoch_end_ms,
             "phases_ms": {n: round(t, 4) for n, t in phases},
         }
         print(json.dumps(out))

@@ -226,6 +226,7 @@ private:
     cudaEvent_t ev_pull_ = nullptr;  // dH chunk partials done (tgn_dh.cu)
     bool scratch_zeroed_ = false;    // dGi/dGh cleared by this step's k_zero_list
     bool head_fits_ = false;         // the fused head (tgn_head.cu) supports these dims
+    bool gru_fused_ = true;          // gemm_mode 1: fused tcgen05 GRU (SPD_GRU_FUSED=0: two GEMMs + cell)
 
     spd_tgn_config cfg_;
     ParamLayout lay_;

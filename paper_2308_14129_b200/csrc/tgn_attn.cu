@@ -472,9 +472,16 @@ __global__ void __launch_bounds__(128) k_attn_time_grad(Dims d, int R, const flo
                                                         const float* alpha, const float* dsc,
                                                         const float* dxbar, double* part) {
     pdl_entry();
-    __shared__ float red[kRootsX][2 * 4 * 32 * NT];
+    __shared__ double red[kRootsX][2 * 4 * 32 * NT];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = blockIdx.x * kRootsX + warp;
+    // grid-stride over root groups (a capped grid leaves SMs to the critical
+    // path beside it): per-root float partials, accumulated per lane in f64
+    double aw[NT][4], ab[NT][4];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) aw[i][k] = ab[i][k] = 0.0;
+    for (int r = blockIdx.x * kRootsX + warp; r - warp < R; r += gridDim.x * kRootsX) {
     const int c_n = r < R ? cnt[r] : 0;
     float4 gw[NT], gb[NT];  // time-encoder gradient partials of this lane's time slots
 #pragma unroll
@@ -535,20 +542,28 @@ __global__ void __launch_bounds__(128) k_attn_time_grad(Dims d, int R, const flo
             }
         }
     }
-    // fixed-order per-block reduction of the roots' time-encoder partials
-    float* tws = red[warp];
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
-        const int t = 4 * (lane + 32 * i);
-        *reinterpret_cast<float4*>(tws + t) = gw[i];
-        *reinterpret_cast<float4*>(tws + 4 * 32 * NT + t) = gb[i];
+        aw[i][0] += gw[i].x; aw[i][1] += gw[i].y; aw[i][2] += gw[i].z; aw[i][3] += gw[i].w;
+        ab[i][0] += gb[i].x; ab[i][1] += gb[i].y; ab[i][2] += gb[i].z; ab[i][3] += gb[i].w;
     }
+    }
+    // fixed-order per-block reduction of the warps' time-encoder partials
+    double* tws = red[warp];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int t = 4 * (lane + 32 * i) + k;
+            tws[t] = aw[i][k];
+            tws[4 * 32 * NT + t] = ab[i][k];
+        }
     __syncthreads();
     for (int c = threadIdx.x; c < 2 * d.T; c += blockDim.x) {
         const int cc = c < d.T ? c : 4 * 32 * NT + (c - d.T);
         double sacc = 0.0;
 #pragma unroll
-        for (int k = 0; k < kRootsX; ++k) sacc += (double)red[k][cc];
+        for (int k = 0; k < kRootsX; ++k) sacc += red[k][cc];
         part[(std::size_t)blockIdx.x * 2 * d.T + c] = sacc;
     }
 }

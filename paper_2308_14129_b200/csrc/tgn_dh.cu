@@ -211,8 +211,11 @@ __global__ void __launch_bounds__(256) k_dh_pull(DhIndex x, Dims d, const float*
                                                  const float* dsc, const float* dxbar,
                                                  const float* Qp, float* partial) {
     pdl_entry();
-    const int c = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-    if (c >= x.chunk_off[x.U_cap]) return;
+    const int lane = threadIdx.x & 31, nchunks = x.chunk_off[x.U_cap];
+    // grid-stride over the chunks (a capped grid leaves SMs to the query
+    // backward running beside it)
+    for (int c = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); c < nchunks;
+         c += (int)((gridDim.x * blockDim.x) >> 5)) {
     const int u = x.chunk_slot[c], p0 = x.chunk_start[c];
     const int n = min(kDhChunk, x.off_occ[u + 1] - p0);
     float4 acc[NM];
@@ -263,6 +266,7 @@ __global__ void __launch_bounds__(256) k_dh_pull(DhIndex x, Dims d, const float*
     for (int i = 0; i < NM; ++i) {
         const int col = 4 * (lane + 32 * i);
         if (col < d.D) *reinterpret_cast<float4*>(o + col) = acc[i];
+    }
     }
 }
 

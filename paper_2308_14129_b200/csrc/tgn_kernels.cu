@@ -306,7 +306,7 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
 //   Y_src = W_a z_src, Y_dst = W_b z_dst, Y_neg = W_b z_neg
 //   D1 = relu(Y_src + Y_{dst|neg} + b1); logit = D1 . w2 + b2; BCE terms
 //   dlogit = (sigmoid - y) / B; dD1 = [D1 > 0] dlogit w2
-//   d_src = (dD1_pos + dD1_neg) W_a, d_dst = dD1_pos W_b, d_neg = dD1_neg W_b
+//   d_src = dD1_pos W_a + dD1_neg W_a, d_dst = dD1_pos W_b, d_neg = dD1_neg W_b
 // (the MergeLayer of oracle/tgn_oracle.py _decode applied to [z_u | z_v] by
 // input halves). W1 = [W_a | W_b | b1] rows (row stride ld1) are staged in
 // shared memory once per block; thread (kind, n) owns output column n of the
@@ -419,20 +419,15 @@ __global__ void __launch_bounds__(768)
         if (e < nev) dD1[(std::size_t)((p < kDecEv ? 0 : B) + i0 + e) * D + n] = v;
     }
     __syncthreads();
-    // per-row output gradients of the three embedding kinds (over the z rows,
-    // no longer read): src rows take both pairs of their event
-    for (int i = tid; i < 3 * kDecEv * D; i += nt) {
-        const int r = i / D, n = i % D, kind = r / kDecEv, e = r % kDecEv;
-        const float gp = sD1[(std::size_t)e * ldz + n], gn = sD1[(std::size_t)(kDecEv + e) * ldz + n];
-        sdD1[(std::size_t)r * ldz + n] = kind == 0 ? gp + gn : kind == 1 ? gp : gn;
-    }
-    __syncthreads();
-    // data gradients d_emb[kind][e][k] = sum_n G[kind][e][n] W_kind[n][k]: thread (kind, k)
-    if (tid < 3 * D) {
-        const int kind = tid / D, k = tid % D;
-        const float* wc = sW + (kind ? D : 0) + k;  // column k of W_a / W_b
-        const float* g = sdD1 + (std::size_t)kind * kDecEv * ldz;
-        float acc[kDecEv];
+    // data gradients, as the oracle's autograd forms them (two decoder calls,
+    // pos and neg): thread (q, k), q = 0 dD1_pos W_a, 1 dD1_neg W_a, 2 dD1_pos W_b,
+    // 3 dD1_neg W_b; d_src = q0 + q1 (summed through shared memory over the
+    // z rows, no longer read), d_dst = q2, d_neg = q3
+    float acc[kDecEv];
+    const int q = tid / D, k = tid % D;
+    if (tid < 4 * D) {
+        const float* wc = sW + (q >= 2 ? D : 0) + k;  // column k of W_a / W_b
+        const float* g = sD1 + (std::size_t)(q & 1) * kDecEv * ldz;
 #pragma unroll
         for (int e = 0; e < kDecEv; ++e) acc[e] = 0.f;
 #pragma unroll 2
@@ -448,11 +443,124 @@ __global__ void __launch_bounds__(768)
                 acc[e] = fmaf(x.w, w3, acc[e]);
             }
         }
+        if (q == 1)
 #pragma unroll
-        for (int e = 0; e < kDecEv; ++e)
-            if (e < nev) d_emb[((std::size_t)kind * B + i0 + e) * D + k] = rnd_if(acc[e], d.rnd);
+            for (int e = 0; e < kDecEv; ++e) sdD1[(std::size_t)e * ldz + k] = acc[e];
+    }
+    __syncthreads();
+    if (tid < 4 * D && q != 1) {
+        const int kind = q == 0 ? 0 : q - 1;
+#pragma unroll
+        for (int e = 0; e < kDecEv; ++e) {
+            const float v = q == 0 ? acc[e] + sdD1[(std::size_t)e * ldz + k] : acc[e];
+            if (e < nev) d_emb[((std::size_t)kind * B + i0 + e) * D + k] = rnd_if(v, d.rnd);
+        }
     }
 }
+
+// Decoder weight gradients (FP32 FFMA), deterministic two-pass: block b sums
+// its chunk of kDecWgEv events into part[b] = [dW1 (D x (2D+1)) | dW2 (D+1)]:
+//   dW_a += dD1_pos^T z_src + dD1_neg^T z_src,  dW_b += dD1_pos^T z_dst + dD1_neg^T z_neg,
+//   db1 += sum dD1_pos + sum dD1_neg,            dw2 += dlogit^T [D1 | 1]
+// (the MergeLayer weight gradient of oracle/tgn_oracle.py by input halves);
+// k_dec_wgrad_reduce adds the partials in block order to the gradients.
+// Thread (tn, tk) of 16 x 16 owns rows tn + 16 i, columns tk + 16 j.
+__global__ void __launch_bounds__(256) k_dec_wgrad_part(Dims d, int B, const float* emb,
+                                                        const float* dD1, const float* dlogit,
+                                                        const float* D1, float* part) {
+    pdl_entry();
+    extern __shared__ __align__(16) float wsm[];
+    const int D = d.D, ld = D + 4;
+    float* sgp = wsm;                    // [EV][ld] dD1 of positive pairs
+    float* sgn = sgp + kDecWgEv * ld;    // [EV][ld] dD1 of negative pairs
+    float* sz = sgn + kDecWgEv * ld;     // [3][EV][ld] z_src | z_dst | z_neg
+    const int e0 = blockIdx.x * kDecWgEv, ne = min(kDecWgEv, B - e0);
+    const int tid = threadIdx.x, D4 = D / 4;
+    for (int i = tid; i < 5 * kDecWgEv * D4; i += blockDim.x) {
+        const int r = i / D4, c = 4 * (i % D4), which = r / kDecWgEv, e = r % kDecWgEv;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (e < ne) {
+            const float* src = which == 0 ? dD1 + (std::size_t)(e0 + e) * D
+                             : which == 1 ? dD1 + (std::size_t)(B + e0 + e) * D
+                                          : emb + ((std::size_t)(which - 2) * B + e0 + e) * D;
+            v = *reinterpret_cast<const float4*>(src + c);
+        }
+        *reinterpret_cast<float4*>(wsm + (std::size_t)r * ld + c) = v;
+    }
+    __syncthreads();
+    float* out = part + (std::size_t)blockIdx.x * (D * (2 * D + 1) + D + 1);
+    const int tn = tid >> 4, tk = tid & 15;
+    constexpr int TI = 7, TJ = 7;  // rows / columns per thread (D <= 112)
+    // the positive and the negative decoder call accumulate separately and
+    // are added at the end (the oracle's autograd sums the two calls' grads)
+    for (int half = 0; half < 2; ++half) {
+        float ap[TI][TJ], an[TI][TJ];
+#pragma unroll
+        for (int i = 0; i < TI; ++i)
+#pragma unroll
+            for (int j = 0; j < TJ; ++j) ap[i][j] = an[i][j] = 0.f;
+        for (int e = 0; e < ne; ++e) {
+            float gp[TI], gn[TI], zp[TJ], zn[TJ];
+#pragma unroll
+            for (int i = 0; i < TI; ++i) {
+                const int n = min(tn + 16 * i, D - 1);
+                gp[i] = sgp[e * ld + n];
+                gn[i] = sgn[e * ld + n];
+            }
+#pragma unroll
+            for (int j = 0; j < TJ; ++j) {
+                const int k = min(tk + 16 * j, D - 1);
+                zp[j] = sz[((half == 0 ? 0 : 1) * kDecWgEv + e) * ld + k];  // z_src | z_dst
+                zn[j] = sz[((half == 0 ? 0 : 2) * kDecWgEv + e) * ld + k];  // z_src | z_neg
+            }
+#pragma unroll
+            for (int i = 0; i < TI; ++i)
+#pragma unroll
+                for (int j = 0; j < TJ; ++j) {
+                    ap[i][j] = fmaf(gp[i], zp[j], ap[i][j]);
+                    an[i][j] = fmaf(gn[i], zn[j], an[i][j]);
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < TI; ++i)
+#pragma unroll
+            for (int j = 0; j < TJ; ++j) {
+                const int n = tn + 16 * i, k = tk + 16 * j;
+                if (n < D && k < D) out[(std::size_t)n * (2 * D + 1) + half * D + k] = ap[i][j] + an[i][j];
+            }
+    }
+    // bias columns: db1 (column 2D of dW1) and dw2 (incl. db2)
+    for (int n = tid; n < D; n += blockDim.x) {
+        float a = 0.f, b = 0.f;
+        for (int e = 0; e < ne; ++e) {
+            a += sgp[e * ld + n];
+            b += sgn[e * ld + n];
+        }
+        out[(std::size_t)n * (2 * D + 1) + 2 * D] = a + b;
+    }
+    for (int c = tid; c <= D; c += blockDim.x) {
+        float a = 0.f, b = 0.f;
+        for (int e = 0; e < ne; ++e) {
+            const std::size_t pp = e0 + e, pn = B + e0 + e;
+            a += dlogit[pp * 4] * (c < D ? D1[pp * d.ld_d1 + c] : 1.f);
+            b += dlogit[pn * 4] * (c < D ? D1[pn * d.ld_d1 + c] : 1.f);
+        }
+        out[(std::size_t)D * (2 * D + 1) + c] = a + b;
+    }
+}
+
+__global__ void k_dec_wgrad_reduce(Dims d, int nblk, const float* part, float* g1, int ld1, float* g2) {
+    pdl_entry();
+    const int D = d.D, n1 = D * (2 * D + 1), per = n1 + D + 1;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= per) return;
+    float a = 0.f;
+    for (int b = 0; b < nblk; ++b) a += part[(std::size_t)b * per + i];
+    if (i < n1) g1[(std::size_t)(i / (2 * D + 1)) * ld1 + i % (2 * D + 1)] += a;
+    else g2[i - n1] += a;
+}
+
+std::size_t dec_wgrad_smem_bytes(const Dims& d) { return 4 * std::size_t(5) * kDecWgEv * (d.D + 4); }
 
 std::size_t decoder_smem_bytes(const Dims& d) {
     const std::size_t D = d.D, ldw = 2 * D + 4, ldz = D + 4;

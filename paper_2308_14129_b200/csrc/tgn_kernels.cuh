@@ -166,11 +166,16 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
                             int ld1, const float* w2, float* D1, float* dlogit, float* lossv,
                             float* dD1, float* logits);
 constexpr int kDecEv = 8;  // events per k_decoder block
-// k_decoder launches roundup(3 d_mem, 32) threads (<= 768)
+// k_decoder launches roundup(4 d_mem, 32) threads (<= 768: d_mem <= 192)
 __global__ void k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2,
                           float* D1, float* dlogit, float* lossv, float* dD1, float* logits,
                           float* d_emb, int bwd);
 std::size_t decoder_smem_bytes(const Dims& d);
+constexpr int kDecWgEv = 32;  // events per k_dec_wgrad_part block
+__global__ void k_dec_wgrad_part(Dims d, int B, const float* emb, const float* dD1, const float* dlogit,
+                                 const float* D1, float* part);
+__global__ void k_dec_wgrad_reduce(Dims d, int nblk, const float* part, float* g1, int ld1, float* g2);
+std::size_t dec_wgrad_smem_bytes(const Dims& d);
 __global__ void k_sum_loss(const float* lossv, int n, float* out);
 __global__ void k_dec_scatter(Dims d, int B, const float* dd_in, float* d_emb);
 __global__ void k_mask_rows(float* buf, int R, int cols, int ld, const int* cnt);

@@ -109,6 +109,7 @@ struct Scratch {
     DevBuf<float> q_in, Q, Qp, xbar, alpha, dsc, ctx, O, m_in, Z1, emb, d_in, D1, logits, lossv, dlogit;
     DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dxbar, dQp, dQ, dq_in;
     DevBuf<float> ws;
+    DevBuf<float> decw;  // decoder weight-gradient chunk partials (k_dec_wgrad_part)
     DevBuf<double> tpart;
     // deterministic dH reduction (tgn_dh.cu): reader index + chunk partials
     DevBuf<int> dh_hist, dh_off_occ, dh_off_root, dh_chunk_off, dh_rchunk_off, dh_chunk_slot,
@@ -323,7 +324,8 @@ void dh_index(const tgnk::WorkerDev& wd, const Scratch& s, cudaStream_t st) {
     launch(tgnk::k_dh_scatter, nb, tgnk::kDhBlock, sm, st, wd, s.dh);
 }
 void dh_pull(const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
-    const unsigned grid = unsigned((std::size_t(s.dh_max_chunks) * 32 + 255) / 256);
+    // grid-stride, at most one 8-warp block per SM
+    const unsigned grid = unsigned(std::min<std::size_t>((std::size_t(s.dh_max_chunks) * 32 + 255) / 256, 148));
     auto go = [&](auto k) {
         launch(k, grid, 256, 0, st, s.dh, d, static_cast<const float*>(s.alpha.p),
                static_cast<const float*>(s.dsc.p), static_cast<const float*>(s.dxbar.p),
@@ -413,8 +415,8 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         data_error("InvalidParams", "n_neighbors must lie in [1, 16]");
     if (cfg.n_heads > 4 || ((cfg.d_mem + cfg.d_time) / cfg.n_heads) % 4)
         data_error("InvalidParams", "n_heads must be <= 4 with a head width that is a multiple of 4");
-    if (cfg.d_mem + cfg.d_time > 256 || cfg.d_edge + 1 > 384)
-        data_error("InvalidParams", "need d_mem + d_time <= 256 and d_edge < 384");
+    if (cfg.d_mem + cfg.d_time > 256 || cfg.d_edge + 1 > 384 || cfg.d_mem > 192)
+        data_error("InvalidParams", "need d_mem + d_time <= 256, d_mem <= 192 and d_edge < 384");
     if (cfg.batch_size < 1) data_error("InvalidParams", "need batch_size >= 1");
     if (world < 1 || rank < 0 || rank >= world) data_error("InvalidParams", "bad rank/world");
     require_device(device);
@@ -536,11 +538,19 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.dm_in.alloc(std::size_t(R) * d.ld_m); s.dctx.alloc(std::size_t(R) * d.ld_Q);
     s.dQ.alloc(std::size_t(R) * d.ld_Q); s.dq_in.alloc(std::size_t(R) * d.ld_q);
     s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
+    s.decw.alloc(std::size_t((B + tgnk::kDecWgEv - 1) / tgnk::kDecWgEv) *
+                 (std::size_t(D) * (2 * D + 1) + D + 1));
     s.trows = 16;
     s.troot_blocks = (R + s.trows - 1) / s.trows;
-    s.tattn_blocks = (R + tgnk::attn_x_roots_per_block() - 1) / tgnk::attn_x_roots_per_block();
+    // k_attn_time_grad: grid-stride over the roots on one block per SM (a
+    // side kernel; full grids crowded the query backward's GEMMs off the SMs)
+    s.tattn_blocks = std::min((R + tgnk::attn_x_roots_per_block() - 1) / tgnk::attn_x_roots_per_block(), 148);
     s.tpart.alloc(std::size_t(s.troot_blocks + s.tattn_blocks) * 2 * d.T);
     s.dh.nbr_node = s.nbr_node.p; s.dh.cnt = s.cnt.p; s.dh.roots = s.roots.p;
+    {
+        const char* e = std::getenv("SPD_GRU_FUSED");
+        gru_fused_ = !(e && *e == '0');
+    }
     {  // fused head (tgn_head.cu): one 227 KB CTA per 16 events; opt-in (SPD_FUSED_HEAD=1):
        // GDELT B = 2000 step 0.483 ms with it vs 0.411 ms with the separate kernels
         const char* e = std::getenv("SPD_FUSED_HEAD");
@@ -866,6 +876,12 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
     launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
         wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
     if (after_gather) after_gather();
+    if (tc && gru_fused_) {  // both gate GEMMs and the cell in one tcgen05 kernel (umma_gru.cuh)
+        umma::gru_fused(s.x_gru.p, d.ld_x, d.DM + 1, s.h_gru.p, d.ld_h, d.D + 1, PW + lay_.gru_ih.off,
+                        lay_.gru_ih.ld, PW + lay_.gru_hh.off, lay_.gru_hh.ld, d.D, s.U, w.nU(), w.mem.p,
+                        w.pend[w.cur].pU.p, s.mem_new.p, train ? s.gsave.p : nullptr, stream_);
+        return;
+    }
     // the two gate GEMMs are independent: the hidden-side one on the aux stream
     SPD_CUDA(cudaEventRecord(ev_aux_fork_, stream_));
     SPD_CUDA(cudaStreamWaitEvent(aux_, ev_aux_fork_, 0));
@@ -1013,7 +1029,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
             dec_smem_set = dsm;
         }
         launch(tgnk::k_decoder, unsigned((B + tgnk::kDecEv - 1) / tgnk::kDecEv),
-               unsigned((3 * d.D + 31) / 32 * 32), dsm, st, d, B, static_cast<const float*>(s.emb.p),
+               unsigned((4 * d.D + 31) / 32 * 32), dsm, st, d, B, static_cast<const float*>(s.emb.p),
                static_cast<const float*>(P + lay_.dec1.off), lay_.dec1.ld,
                static_cast<const float*>(P + lay_.dec2.off), s.D1.p, s.dlogit.p, s.lossv.p, s.dD1.p,
                s.logits.p, s.d_emb.p, train ? 1 : 0);
@@ -1076,15 +1092,34 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fuse
         cudaEvent_t at = mark();
         proj_dgrad(tc, s.d_emb.p, d.D, PW + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
                    nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z, tc);
-        side_from(at, [&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off,
-                                                        lay_.dec2.ld, 1, d.D + 1, 2 * B, nullptr, ws_cur_,
-                                                        wsn_cur_, sd); });
-        side_from(at, [&](cudaStream_t sd) {
-            // the gathered decoder input [z_u | z_v | 1] is only needed here
-            launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, sd, d, B,
-                   s.emb.p, s.d_in.p);
-            gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
-                   2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
+        if (d.D <= 112) {  // decoder weight gradients: chunk partials + fixed-order sum (FFMA)
+            side_from(at, [&](cudaStream_t sd) {
+                static std::size_t wg_smem_set = 0;
+                const std::size_t sm = tgnk::dec_wgrad_smem_bytes(d);
+                if (sm > wg_smem_set) {
+                    SPD_CUDA(cudaFuncSetAttribute(tgnk::k_dec_wgrad_part,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+                    wg_smem_set = sm;
+                }
+                const int nblk = (B + tgnk::kDecWgEv - 1) / tgnk::kDecWgEv;
+                launch(tgnk::k_dec_wgrad_part, unsigned(nblk), 256, sm, sd, d, B,
+                       static_cast<const float*>(s.emb.p), static_cast<const float*>(s.dD1.p),
+                       static_cast<const float*>(s.dlogit.p), static_cast<const float*>(s.D1.p), s.decw.p);
+                const int per = d.D * (2 * d.D + 1) + d.D + 1;
+                launch(tgnk::k_dec_wgrad_reduce, unsigned((per + 255) / 256), 256, 0, sd, d, nblk,
+                       static_cast<const float*>(s.decw.p), G + lay_.dec1.off, lay_.dec1.ld, G + lay_.dec2.off);
+            });
+        } else {
+            side_from(at, [&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off,
+                                                            lay_.dec2.ld, 1, d.D + 1, 2 * B, nullptr, ws_cur_,
+                                                            wsn_cur_, sd); });
+            side_from(at, [&](cudaStream_t sd) {
+                // the gathered decoder input [z_u | z_v | 1] is only needed here
+                launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, sd, d, B,
+                       s.emb.p, s.d_in.p);
+                gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
+                       2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
+        }
         side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off,
                                                         lay_.mrg2.ld, d.D, d.D + 1, R, nullptr, ws_cur_,
                                                         wsn_cur_, sd); });

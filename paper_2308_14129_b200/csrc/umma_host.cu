@@ -12,6 +12,7 @@
 #include "cuda_util.hpp"
 #include "gemm_simt.cuh"
 #include "umma_gemm.cuh"
+#include "umma_gru.cuh"
 #include "umma_host.hpp"
 
 namespace spd {
@@ -270,6 +271,45 @@ void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw
     dispatch<true, true>(bn, maps, a,
                          dim3((K_in + bn - 1) / bn, (N_out + BM - 1) / BM, split * bt.n), s);
     if (split > 1) reduce(ws, split, N_out, K_in, ldws, dW, ldw, bt, s);
+}
+
+void gru_fused(const float* x, int ldx, int K1, const float* h, int ldh, int K2, const float* Wih,
+               int ldwih, const float* Whh, int ldwhh, int D, int M, const int* M_dev,
+               const float* mem, const std::uint32_t* nodes, float* mem_new, float* save,
+               cudaStream_t s) {
+    if (!M || !D) return;
+    constexpr int UB = kGruUB;
+    using C_ = GruCfg<UB>;
+    GruMaps maps{};
+    maps.x = make_map(x, K1, M, ldx, BM);
+    maps.h = make_map(h, K2, M, ldh, BM);
+    maps.wih = make_map(Wih, K1, 3 * D, ldwih, UB);
+    maps.whh = make_map(Whh, K2, 3 * D, ldwhh, UB);
+    GruArgs a{};
+    a.M = M; a.M_dev = M_dev; a.K1 = K1; a.K2 = K2; a.D = D;
+    a.mem = mem; a.nodes = nodes; a.mem_new = mem_new; a.save = save;
+    auto kern = umma_gru_kernel<UB>;
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
+    });
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned((D + UB - 1) / UB), unsigned((M + BM - 1) / BM), 1);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int prio = 0;
+    SPD_CUDA(cudaStreamGetPriority(s, &prio));
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = prio;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
+    g_launch_counter.fetch_add(1, std::memory_order_relaxed);
+    SPD_CUDA(cudaGetLastError());
 }
 
 }  // namespace umma

@@ -27,6 +27,13 @@ void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, 
 void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
            int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap, cudaStream_t s,
            const Batch& bt = {});
+// Fused GRUCell on tensor cores (umma_gru.cuh): both gate GEMMs (x: [M x K1],
+// h: [M x K2], augmented weights [3D x K]) and the cell; writes mem_new [M x D]
+// and, when save != null, the backward's gate values [M x 4D] (r | z | n | Gh_n).
+void gru_fused(const float* x, int ldx, int K1, const float* h, int ldh, int K2, const float* Wih,
+               int ldwih, const float* Whh, int ldwhh, int D, int M, const int* M_dev,
+               const float* mem, const std::uint32_t* nodes, float* mem_new, float* save,
+               cudaStream_t s);
 std::uint64_t launches();
 
 }  // namespace umma
