@@ -325,6 +325,19 @@ spd_status spd_tgn_seek(spd_tgn_trainer* t, uint64_t step);
  * start from zero (reset at every loop start, pac_sim.cpp:238); evaluation
  * views must be set again. ConfigMismatch if the worker count differs. */
 spd_status spd_tgn_rebind(spd_tgn_trainer* t, const spd_subgraphs* subs);
+/* Shuffle-combine on the device (K13; pac_sim.cpp:134-160, :280-329): attach
+ * the time-ordered training stream (global ids) and the small SEP parts'
+ * node lists (CSR small_off[n_small + 1] / small_nodes, as spd_shuffle_combine
+ * takes them; n_small a multiple of the worker count, workers <= 64) once;
+ * then spd_tgn_shuffle_epoch regroups the parts with shuffle_combine's seeded
+ * permutation (epoch_seed = shuffle_seed + epoch, as simulate) and induces
+ * every worker's subgraph in HBM — events, neighbour CSR, negative pool,
+ * feature rows — with the same result as spd_shuffle_combine +
+ * spd_induce_groups + spd_tgn_rebind, and the same `recovered` count.
+ * Parameters and Adam state carry over; memory starts from zero. */
+spd_status spd_tgn_attach_stream(spd_tgn_trainer* t, const spd_edge* e, uint64_t n, uint32_t node_count,
+                                 const uint64_t* small_off, const uint32_t* small_nodes, int32_t n_small);
+spd_status spd_tgn_shuffle_epoch(spd_tgn_trainer* t, uint64_t epoch_seed, uint64_t* recovered);
 /* One global step: every local worker trains one batch, gradients are
  * all-reduced (mean over all workers), Adam updates. loss_out: per local
  * worker mean BCE of the batch (device->host read), may be NULL. */
@@ -410,6 +423,8 @@ spd_status spd_tgn_sync(spd_tgn_trainer* t);
 spd_status spd_tgn_next_batch(const spd_tgn_trainer* t, int32_t worker, uint64_t* lo,
                               uint64_t* hi, int32_t* feat_stride);
 spd_status spd_tgn_worker_events(const spd_tgn_trainer* t, int32_t worker, spd_edge* out);
+/* Number of training events of worker (the length spd_tgn_worker_events fills). */
+spd_status spd_tgn_worker_event_count(const spd_tgn_trainer* t, int32_t worker, uint64_t* n);
 /* Host<->device bytes moved by spd_tgn_step_host so far. */
 spd_status spd_tgn_io_bytes(const spd_tgn_trainer* t, uint64_t* h2d, uint64_t* d2h);
 /* Host copy of the synthetic bf16 feature rows (row stride `stride`, pad 0) of

@@ -785,6 +785,24 @@ class TGNTrainer:
     def close(self):
         self.__del__()
 
+    def attach_stream(self, stream: "EdgeStream", small: Sequence[Sequence[int]]):
+        """Keep the training stream and the small SEP parts (node lists) in HBM
+        for device-side shuffle-combine (spd_tgn_attach_stream)."""
+        e = _edges(stream)
+        off = np.zeros(len(small) + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([len(v) for v in small])
+        flat = np.array([x for v in small for x in v] or [0], dtype=np.uint32)
+        _check(lib.spd_tgn_attach_stream(self._h, e.ctypes.data if len(e) else None, len(e),
+                                         stream.node_count, ptr(off, u64), ptr(flat, u32), len(small)))
+
+    def shuffle_epoch(self, epoch_seed: int) -> int:
+        """Regroup the attached small parts (shuffle_combine's permutation for
+        epoch_seed) and re-induce every worker on the device; returns the
+        `recovered` count (spd_tgn_shuffle_epoch)."""
+        r = u64()
+        _check(lib.spd_tgn_shuffle_epoch(self._h, epoch_seed, C.byref(r)))
+        return r.value
+
     def set_surrogate(self, model: "ModelParams"):
         """Bridge backbone: the reference's surrogate MSG/UPD replaces the GRU
         in this trainer's schedule (spd_tgn_set_surrogate)."""
@@ -947,7 +965,9 @@ class TGNTrainer:
         return out
 
     def _n_events(self, w: int) -> int:
-        return self._events_per_worker[w]
+        n = u64()
+        _check(lib.spd_tgn_worker_event_count(self._h, w, C.byref(n)))
+        return n.value
 
     def step_host(self, events: list, feats: list | None) -> np.ndarray:
         """End-to-end step: per local worker, its next batch's events (local ids)

@@ -113,6 +113,9 @@ _SIGS = {
     "spd_nccl_unique_id": (i32, [P]),
     "spd_tgn_peer_blob_bytes": (u64, []),
     "spd_tgn_set_surrogate": (i32, [P, i32, P, P, f64]),
+    "spd_tgn_attach_stream": (i32, [P, P, u64, u32, P, P, i32]),
+    "spd_tgn_shuffle_epoch": (i32, [P, u64, P]),
+    "spd_tgn_worker_event_count": (i32, [P, i32, P]),
     "spd_tgn_peer_export": (i32, [P, P]),
     "spd_tgn_peer_connect": (i32, [P, P]),
     "spd_tgn_epoch_steps": (i32, [P, pu64]),

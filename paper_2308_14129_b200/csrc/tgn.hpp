@@ -96,6 +96,19 @@ struct Worker {
 
 struct Scratch;  // per-step activations (sized for one batch)
 
+// The training stream resident on the device for shuffle-combine
+// re-induction (tgn_induce.cu): SoA events, per-node small-part bitmasks and
+// the per-edge "induced by some small part" flags (for `recovered`).
+struct DevStream {
+    std::uint64_t E = 0;
+    NodeId N = 0;
+    int n_small = 0, words = 0;
+    DevBuf<std::uint32_t> src, dst;
+    DevBuf<double> ts;
+    DevBuf<std::uint64_t> bits;  // N x words
+    DevBuf<std::uint8_t> in_small;
+};
+
 std::uint64_t kernel_launches();  // process-wide count of TGN-path kernel launches
 int debug_gemm(int impl, int which, const float* A, int lda, const float* B, int ldb, float* C,
                int ldc, int M, int N, int K, float* ws, std::size_t ws_cap);
@@ -149,6 +162,12 @@ public:
     // (pac_sim.cpp:50-104) replaces the GRU in this trainer's schedule; steps
     // apply the pending messages only (no embedding, loss, gradients)
     void set_surrogate(int d, const double* w_m, const double* omega, double gamma);
+    // Shuffle-combine on the device (tgn_induce.cu): keep the training stream
+    // and the small SEP parts in HBM, then re-induce every epoch's regrouped
+    // worker subgraphs there (pac_sim.cpp:134-160, :280-329)
+    void attach_stream(const spd_edge* e, std::uint64_t n, NodeId node_count, const std::uint64_t* off,
+                       const NodeId* nodes, int n_small);
+    void shuffle_epoch(std::uint64_t seed, std::uint64_t* recovered);
     void peer_export(unsigned char* out) const;
     void peer_connect(const unsigned char* blobs);
     void step_host(const spd_edge* const* events, const std::uint16_t* const* feats,
@@ -167,6 +186,8 @@ public:
 
 private:
     void build_workers(const SubGraphs& subs, const std::vector<int>& ids);
+    void init_worker_state(Worker& w);  // memory, clocks, pending sets, shared-row map
+    std::unique_ptr<DevStream> dstream_;
     void worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx,
                      bool post = true);
     void worker_post_kernels(Worker& w);

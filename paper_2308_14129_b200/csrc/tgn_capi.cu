@@ -49,6 +49,20 @@ spd_status spd_tgn_set_surrogate(spd_tgn_trainer* t, int32_t d, const double* w_
     });
 }
 
+spd_status spd_tgn_attach_stream(spd_tgn_trainer* t, const spd_edge* e, uint64_t n, uint32_t node_count,
+                                 const uint64_t* small_off, const uint32_t* small_nodes, int32_t n_small) {
+    GUARD({
+        if (!t || (n && !e) || !small_off || !small_nodes) usage_error("null argument");
+        t->t->attach_stream(e, n, node_count, small_off, small_nodes, n_small);
+    });
+}
+spd_status spd_tgn_shuffle_epoch(spd_tgn_trainer* t, uint64_t epoch_seed, uint64_t* recovered) {
+    GUARD({
+        if (!t) usage_error("null argument");
+        t->t->shuffle_epoch(epoch_seed, recovered);
+    });
+}
+
 uint64_t spd_tgn_peer_blob_bytes(void) { return PeerComm::kBlobBytes; }
 spd_status spd_tgn_peer_export(const spd_tgn_trainer* t, void* out) {
     GUARD({
@@ -188,6 +202,12 @@ spd_status spd_tgn_worker_events(const spd_tgn_trainer* t, int32_t worker, spd_e
     GUARD({
         Worker& w = t->t->worker(worker);
         std::copy(w.ev_host.begin(), w.ev_host.end(), out);
+    });
+}
+spd_status spd_tgn_worker_event_count(const spd_tgn_trainer* t, int32_t worker, uint64_t* n) {
+    GUARD({
+        if (!t || !n) usage_error("null argument");
+        *n = t->t->worker(worker).E;
     });
 }
 spd_status spd_tgn_io_bytes(const spd_tgn_trainer* t, uint64_t* h2d, uint64_t* d2h) {

@@ -724,28 +724,35 @@ void TGNTrainer::build_workers(const SubGraphs& subs, const std::vector<int>& id
             SPD_CUDA(cudaGetLastError());
             SPD_CUDA(cudaStreamSynchronize(stream_));
         }
-        const std::size_t N = std::max<std::size_t>(1, w.N);
-        w.mem.alloc(N * D); w.mem.zero(stream_);
-        w.mem_snap.alloc(N * D); w.mem_snap.zero(stream_);
-        w.lu.alloc(N); w.lu.zero(stream_);
-        w.lu_snap.alloc(N); w.lu_snap.zero(stream_);
-        w.slot.alloc(N);
-        SPD_CUDA(cudaMemsetAsync(w.slot.p, 0xFF, w.slot.bytes(), stream_));
-        w.lastpos.alloc(N);
-        SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
-        for (auto& ps : w.pend) {
-            ps.pU.alloc(2 * B); ps.pOther.alloc(2 * B); ps.pEv.alloc(2 * B); ps.pTs.alloc(2 * B);
-            ps.nU.alloc(1); ps.nU.zero(stream_);
-        }
-        for (NodeId sidx : shared_) {
-            auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), sidx);
-            w.shared_local.push_back(it != w.nodes.end() && *it == sidx
-                                         ? static_cast<std::uint32_t>(it - w.nodes.begin())
-                                         : 0xFFFFFFFFu);
-        }
+        init_worker_state(w);
         w.ev_host.resize(w.E);
         for (std::uint64_t k = 0; k < w.E; ++k) w.ev_host[k] = spd_edge{src[k], dst[k], ts[k]};
         workers_.push_back(std::move(W));
+    }
+}
+
+void TGNTrainer::init_worker_state(Worker& w) {
+    const int D = lay_.D;
+    const int B = static_cast<int>(cfg_.batch_size);
+    const std::size_t N = std::max<std::size_t>(1, w.N);
+    w.mem.alloc(N * D); w.mem.zero(stream_);
+    w.mem_snap.alloc(N * D); w.mem_snap.zero(stream_);
+    w.lu.alloc(N); w.lu.zero(stream_);
+    w.lu_snap.alloc(N); w.lu_snap.zero(stream_);
+    w.slot.alloc(N);
+    SPD_CUDA(cudaMemsetAsync(w.slot.p, 0xFF, w.slot.bytes(), stream_));
+    w.lastpos.alloc(N);
+    SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
+    for (auto& ps : w.pend) {
+        ps.pU.alloc(2 * B); ps.pOther.alloc(2 * B); ps.pEv.alloc(2 * B); ps.pTs.alloc(2 * B);
+        ps.nU.alloc(1); ps.nU.zero(stream_);
+    }
+    w.shared_local.clear();
+    for (NodeId sidx : shared_) {
+        auto it = std::lower_bound(w.nodes.begin(), w.nodes.end(), sidx);
+        w.shared_local.push_back(it != w.nodes.end() && *it == sidx
+                                     ? static_cast<std::uint32_t>(it - w.nodes.begin())
+                                     : 0xFFFFFFFFu);
     }
 }
 

@@ -367,3 +367,44 @@ def test_host_fed_events_must_match_resident_stream():
     ok = np.ascontiguousarray(ev_all[lo:hi]).copy()
     assert np.all(np.isfinite(tr.step_host([ok], [ft])))
     tr.close()
+
+
+@pytest.mark.parametrize("parts,workers", [(4, 2), (8, 4), (6, 3)])
+def test_device_shuffle_combine_matches_host_rebind(parts, workers):
+    """Shuffle-combine re-induction on the device (spd_tgn_attach_stream +
+    spd_tgn_shuffle_epoch, K13) against the host path (spd_shuffle_combine +
+    spd_induce_groups + spd_tgn_rebind): identical worker events, node sets
+    and `recovered` counts every epoch, and bit-identical training (same
+    parameters and memory after each epoch)."""
+    s, split, pa, small_subs = partitioned(nodes=300, edges=4000, parts=parts, seed=3)
+    small = [g.nodes for g in small_subs]
+    cfg = small_cfg()
+    host = dev = None
+    for epoch in range(2):
+        seed = 11 + epoch
+        groups = sp.shuffle_combine(small, workers, seed)
+        subs, rec_host = sp.induce_groups(split.train, groups, small)
+        if host is None:
+            host = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+            dev = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+            dev.attach_stream(split.train, small)
+        else:
+            host.rebind(subs)
+        rec_dev = dev.shuffle_epoch(seed)
+        assert rec_dev == rec_host, (epoch, rec_dev, rec_host)
+        assert dev.epoch_steps() == host.epoch_steps()
+        for w in range(workers):
+            np.testing.assert_array_equal(dev.local_nodes(w), host.local_nodes(w))
+            a, b = dev.worker_events(w), host.worker_events(w)
+            assert a.tobytes() == b.tobytes(), (epoch, w)
+        for t in (host, dev):
+            t.begin_epoch(epoch)
+            for _ in range(t.epoch_steps()):
+                t.step(want_loss=False)
+            t.end_epoch()
+        assert np.array_equal(dev.params(), host.params()), epoch
+        for w in range(workers):
+            (m1, l1), (m2, l2) = dev.memory(w), host.memory(w)
+            assert np.array_equal(m1, m2) and np.array_equal(l1, l2), (epoch, w)
+    host.close()
+    dev.close()
