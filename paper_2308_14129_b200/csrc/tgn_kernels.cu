@@ -314,7 +314,8 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
 // column with 16-B loads while the activations broadcast. Writes D1, dlogit,
 // dD1 (the weight gradients' inputs), loss terms, logits and d_emb. bwd = 0
 // (evaluation): forward and logits only.
-__global__ void __launch_bounds__(768)
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
     k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2, float* D1,
               float* dlogit, float* lossv, float* dD1, float* logits, float* d_emb, int bwd) {
     pdl_entry();
@@ -561,6 +562,12 @@ __global__ void k_dec_wgrad_reduce(Dims d, int nblk, const float* part, float* g
 }
 
 std::size_t dec_wgrad_smem_bytes(const Dims& d) { return 4 * std::size_t(5) * kDecWgEv * (d.D + 4); }
+
+// 416 threads (d_mem <= 104) at two blocks per SM (<= 72 registers), else one
+template __global__ void k_decoder<416, 2>(Dims, int, const float*, const float*, int, const float*,
+                                           float*, float*, float*, float*, float*, float*, int);
+template __global__ void k_decoder<768, 1>(Dims, int, const float*, const float*, int, const float*,
+                                           float*, float*, float*, float*, float*, float*, int);
 
 std::size_t decoder_smem_bytes(const Dims& d) {
     const std::size_t D = d.D, ldw = 2 * D + 4, ldz = D + 4;

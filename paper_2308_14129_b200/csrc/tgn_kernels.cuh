@@ -167,6 +167,7 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
                             float* dD1, float* logits);
 constexpr int kDecEv = 8;  // events per k_decoder block
 // k_decoder launches roundup(4 d_mem, 32) threads (<= 768: d_mem <= 192)
+template <int MAXT, int MINB>
 __global__ void k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2,
                           float* D1, float* dlogit, float* lossv, float* dD1, float* logits,
                           float* d_emb, int bwd);

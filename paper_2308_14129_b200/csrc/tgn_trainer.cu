@@ -1030,12 +1030,14 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         if (lay_.dec1.off % 4 || lay_.dec1.ld % 4) internal_error("InvalidParams", "decoder rows unaligned");
         static std::size_t dec_smem_set = 0;
         const std::size_t dsm = tgnk::decoder_smem_bytes(d);
+        const bool narrow = 4 * d.D <= 416;
+        auto kdec = narrow ? tgnk::k_decoder<416, 2> : tgnk::k_decoder<768, 1>;
         if (dsm > dec_smem_set) {
-            SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(dsm)));
+            SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder<416, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
+            SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder<768, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
             dec_smem_set = dsm;
         }
-        launch(tgnk::k_decoder, unsigned((B + tgnk::kDecEv - 1) / tgnk::kDecEv),
+        launch(kdec, unsigned((B + tgnk::kDecEv - 1) / tgnk::kDecEv),
                unsigned((4 * d.D + 31) / 32 * 32), dsm, st, d, B, static_cast<const float*>(s.emb.p),
                static_cast<const float*>(P + lay_.dec1.off), lay_.dec1.ld,
                static_cast<const float*>(P + lay_.dec2.off), s.D1.p, s.dlogit.p, s.lossv.p, s.dD1.p,

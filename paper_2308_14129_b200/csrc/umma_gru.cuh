@@ -25,7 +25,7 @@ namespace spd {
 namespace umma {
 
 constexpr int kGruUB = 32;      // memory units per CTA
-constexpr int kGruStages = 4;
+constexpr int kGruStages = 7;  // 196 KB ring: one CTA per SM (<= 128 CTAs at the step's sizes), all in flight
 
 struct GruArgs {
     int M;             // row capacity (pending slots); live rows from *M_dev
@@ -64,7 +64,7 @@ __device__ __forceinline__ void tmem_ld8(std::uint32_t taddr, float (&v)[8]) {
 }
 
 template <int UB>
-__global__ void __launch_bounds__(THREADS, 2) umma_gru_kernel(const __grid_constant__ GruMaps maps, GruArgs args) {
+__global__ void __launch_bounds__(THREADS, 1) umma_gru_kernel(const __grid_constant__ GruMaps maps, GruArgs args) {
     pdl_entry();
     using C_ = GruCfg<UB>;
     constexpr int NST = kGruStages;
