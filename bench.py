@@ -335,6 +335,14 @@ def main():
     rank, world, local, pg = dist_init()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # one GPU per rank; on a box with fewer GPUs than ranks (a functional check
+    # of the N>1 path, not a measurement) ranks share devices round-robin
+    try:
+        import torch
+        ndev = max(1, torch.cuda.device_count())
+    except Exception:
+        ndev = 1
+    local = local % ndev
     verbose = rank == 0
 
     def log(msg):

@@ -147,7 +147,10 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map
 // CTA owns a 128 x (NSUB*BN) output tile and reads its A tile once. CL CTAs
 // along M form a cluster and split the B tile's TMA boxes between them, each
 // box multicast to all CL CTAs (B streamed from L2 once per cluster).
-template <bool A_MN, bool B_MN, int BN, int NSUB, int CL>
+// DEEP: one CTA per SM with the ring as deep as shared memory allows (up to 8
+// stages), so every k-block of a short-K GEMM is in flight at once — for
+// grids of at most one wave.
+template <bool A_MN, bool B_MN, int BN, int NSUB, int CL, bool DEEP = false>
 struct Cfg {
     static constexpr int NT = BN * NSUB;
     static constexpr int A_BYTES = BM * BK * 4;  // 16 KB
@@ -155,9 +158,10 @@ struct Cfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     // narrow tiles: 3 CTAs per SM (3 stages, <= 113 registers), so a CTA's
     // epilogue and its neighbours' TMA round trips overlap; wider: 2 per SM
-    static constexpr int CTAS_PER_SM = NT <= 64 ? 3 : 2;
-    static constexpr int BUDGET = (NT <= 64 ? 75 * 1024 : 227 * 1024) - 1024 - 256;
-    static constexpr int STAGES_ = BUDGET / STAGE_BYTES >= STAGES ? STAGES : BUDGET / STAGE_BYTES;
+    static constexpr int CTAS_PER_SM = DEEP ? 1 : NT <= 64 ? 3 : 2;
+    static constexpr int BUDGET = (DEEP ? 227 * 1024 : NT <= 64 ? 75 * 1024 : 227 * 1024) - 1024 - 256;
+    static constexpr int MAXST = DEEP ? 8 : STAGES;
+    static constexpr int STAGES_ = BUDGET / STAGE_BYTES >= MAXST ? MAXST : BUDGET / STAGE_BYTES;
     static constexpr int SMEM = STAGES_ * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr int TMEM_COLS = NT <= 32 ? 32 : NT <= 64 ? 64 : NT <= 128 ? 128 : NT <= 256 ? 256 : 512;
     // TMA boxes per stage for B: 32-column blocks (MN-major) or row slabs of
@@ -172,11 +176,11 @@ struct Cfg {
     static_assert(NT <= 512, "accumulator exceeds TMEM");
 };
 
-template <bool A_MN, bool B_MN, int BN, int NSUB, int CL>
-__global__ void __launch_bounds__(THREADS, (BN * NSUB <= 64 ? 3 : 2))
+template <bool A_MN, bool B_MN, int BN, int NSUB, int CL, bool DEEP = false>
+__global__ void __launch_bounds__(THREADS, (DEEP ? 1 : BN * NSUB <= 64 ? 3 : 2))
     umma_gemm_kernel(const __grid_constant__ Maps maps, Args args) {
     pdl_entry();
-    using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;
+    using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL, DEEP>;
     constexpr int NST = C_::STAGES_;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-B alignment (SWIZZLE_128B atoms) by offset, keeping shared-space provenance

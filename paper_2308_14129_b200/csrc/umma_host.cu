@@ -97,10 +97,10 @@ void reduce(const float* ws, int split, int M, int N, int ldws, float* C, int ld
     SPD_CUDA(cudaGetLastError());
 }
 
-template <bool A_MN, bool B_MN, int BN, int NSUB = 1, int CL = 1>
+template <bool A_MN, bool B_MN, int BN, int NSUB = 1, int CL = 1, bool DEEP = false>
 void run(const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
-    using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL>;
-    auto kern = umma_gemm_kernel<A_MN, B_MN, BN, NSUB, CL>;
+    using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL, DEEP>;
+    auto kern = umma_gemm_kernel<A_MN, B_MN, BN, NSUB, CL, DEEP>;
     static std::once_flag once;
     std::call_once(once, [&] {
         SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
@@ -131,8 +131,22 @@ void run(const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
     SPD_CUDA(cudaGetLastError());
 }
 
+// Deep one-wave tiles for the forward / data-gradient GEMMs (SPD_UMMA_DEEP=1):
+// 128-wide tiles, one CTA per SM, every k-block in flight (experiment knob)
+bool deep_tiles() {
+    static const bool v = [] {
+        const char* e = std::getenv("SPD_UMMA_DEEP");
+        return e && *e == '1';
+    }();
+    return v;
+}
+
 template <bool A_MN, bool B_MN>
 void dispatch(int bn, const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
+    if (bn == -128) {
+        run<A_MN, B_MN, 128, 1, 1, true>(maps, args, grid, s);
+        return;
+    }
     switch (bn) {
         case 64: run<A_MN, B_MN, 64>(maps, args, grid, s); break;
         case 128: run<A_MN, B_MN, 128>(maps, args, grid, s); break;
@@ -199,12 +213,14 @@ void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, in
         run<false, false, 208, 2, 4>(maps, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
         return;
     }
-    const int bn = pick_bn(N);
+    int bn = pick_bn(N);
+    const bool deep = deep_tiles() && long((N + 127) / 128) * mt * bt.n <= 148;
+    if (deep) bn = 128;
     for (int z = 0; z < bt.n; ++z) {
         maps.a[z] = make_map(A + z * bt.a, K, M, lda, BM);
         maps.b[z] = make_map(W + z * bt.b, K, N, ldw, bn);
     }
-    dispatch<false, false>(bn, maps, a, dim3((N + bn - 1) / bn, mt, bt.n), s);
+    dispatch<false, false>(deep ? -128 : bn, maps, a, dim3((N + bn - 1) / bn, mt, bt.n), s);
 }
 
 void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N,
@@ -224,12 +240,14 @@ void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, 
         run<false, true, 224, 1, 4>(maps, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
         return;
     }
-    const int bn = pick_bn(N);  // multiple of 32: whole MN-major column blocks
+    int bn = pick_bn(N);  // multiple of 32: whole MN-major column blocks
+    const bool deep = deep_tiles() && long((N + 127) / 128) * mt * bt.n <= 148;
+    if (deep) bn = 128;
     for (int z = 0; z < bt.n; ++z) {
         maps.a[z] = make_map(A + z * bt.a, K, M, lda, BM);
         maps.b[z] = make_map(W + z * bt.b, N, K, ldw, BK, true);  // W [K x N], N contiguous
     }
-    dispatch<false, true>(bn, maps, a, dim3((N + bn - 1) / bn, mt, bt.n), s);
+    dispatch<false, true>(deep ? -128 : bn, maps, a, dim3((N + bn - 1) / bn, mt, bt.n), s);
 }
 
 void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
