@@ -317,6 +317,9 @@ def main():
                     help="SEP partitions (default: one per GPU); more than --gpus trains several "
                          "partitions per GPU as local workers of one trainer")
     ap.add_argument("--hub-k", type=float, default=0.05, help="SEP shared-hub fraction k")
+    ap.add_argument("--backbone", default="tgn", choices=["tgn", "jodie"],
+                    help="memory-based TIG model: TGN (GRU + temporal attention) or JODIE "
+                         "(RNN + time projection), PAPER.md:373")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="N>1 gradient all-reduce: peer = fused into Adam over CUDA-IPC-mapped "
                          "peer HBM (NVLink); nccl = ncclAllReduce then Adam")
@@ -357,8 +360,9 @@ def main():
     mine = list(range(rank * (P // world), (rank + 1) * (P // world)))  # this rank's partitions
     D = T = 100
     K, H = 10, 2
+    model = "TGN" if args.backbone == "tgn" else "JODIE"
     cfg_desc = {"workload": f"{args.config}-shape synthetic TIG ({N} nodes, {E} edges, d_e={F}), "
-                            f"TGN d_mem=d_time=100 k={K} heads={H}, B={B}, SEP P={P}"
+                            f"{model} d_mem=d_time=100 k={K} heads={H}, B={B}, SEP P={P}"
                             + (f" k_hub={args.hub_k}" if args.hub_k != 0.05 else ""),
                 "nodes": N, "edges": E, "d_edge": F, "batch": B, "partitions": P,
                 "partitions_per_gpu": P // world, "hub_k": args.hub_k,
@@ -397,7 +401,7 @@ def main():
     subs_mine = [wl["subs"][w] for w in mine]
     sub_mine = subs_mine[0]
     cfg = sp.TGNConfig(d_mem=D, d_time=T, d_edge=F, n_neighbors=K, n_heads=H, batch_size=B, lr=1e-4,
-                       gemm_mode=args.gemm_mode)
+                       gemm_mode=args.gemm_mode, backbone=0 if args.backbone == "tgn" else 1)
     nccl_id = None
     if world > 1 and args.transport == "nccl":
         import torch

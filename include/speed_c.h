@@ -277,6 +277,8 @@ typedef struct spd_tgn_config {
     uint64_t seed_neg;   /* negative sampling */
     int32_t sync_average;/* epoch-end shared-node sync: 1 average (default), 0 max-ts */
     int32_t gemm_mode;   /* 0 = FP32 FFMA, 1 = tcgen05 TF32 for the GRU and attention projections (tolerance-gated) */
+    int32_t backbone;    /* 0 = TGN (GRU memory, temporal attention); 1 = JODIE (RNN memory,
+                          * time-projection embedding: PAPER.md:373's other backbones) */
 } spd_tgn_config;
 
 typedef struct spd_tgn_trainer spd_tgn_trainer;

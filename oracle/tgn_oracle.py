@@ -32,6 +32,14 @@ that the paper leaves open are fixed here once, and the CUDA path follows them:
   * PAC schedule (pac_sim.cpp:205-264): memory reset at
     every loop start, loop-end flush + snapshot, epoch-end restore + shared
     node sync (average default, max-ts optional).
+  * backbone = 1, JODIE (one of the paper's other backbones; as
+    TGN's reference implementation configures it): the same messages and
+    last-message aggregation, an RNN memory updater h' = tanh(W_ih m + b_ih +
+    W_hh h + b_hh), and the time-projection embedding
+    emb = s'(t) * (1 + log1p(t - t_last) w_tp + b_tp) (t_last = the clock after
+    this batch's memory update; log1p keeps raw timestamp gaps of up to 1e8 in
+    range where JODIE normalises them by dataset statistics); no attention or
+    merge layers; the same decoder and loss.
 """
 from __future__ import annotations
 
@@ -108,6 +116,7 @@ class TGNConfig:
     seed_feat: int = 2
     seed_neg: int = 4
     sync_average: int = 1
+    backbone: int = 0  # 0 TGN, 1 JODIE
 
 
 def ld_aug(k: int) -> int:
@@ -121,9 +130,12 @@ def linear_specs(c: TGNConfig):
     [W | b | 0-pad] matrix of row stride ld_aug(K)."""
     D, T, F = c.d_mem, c.d_time, c.d_edge
     DQ, DK, DM = D + T, D + F + T, 2 * D + F + T
-    return [("gru_ih", 3 * D, DM, D), ("gru_hh", 3 * D, D, D), ("att_q", DQ, DQ, DQ),
-            ("att_kv", 2 * DQ, DK, DK), ("att_o", DQ, DQ, DQ), ("mrg1", D, DQ + D, DQ + D),
-            ("mrg2", D, D, D), ("dec1", D, 2 * D, 2 * D), ("dec2", 1, D, D)]
+    t = c.backbone == 0  # JODIE: one RNN gate block, no attention / merge rows, time projection
+    return [("gru_ih", 3 * D if t else D, DM, D), ("gru_hh", 3 * D if t else D, D, D),
+            ("att_q", DQ if t else 0, DQ, DQ), ("att_kv", 2 * DQ if t else 0, DK, DK),
+            ("att_o", DQ if t else 0, DQ, DQ), ("mrg1", D if t else 0, DQ + D, DQ + D),
+            ("mrg2", D if t else 0, D, D), ("dec1", D, 2 * D, 2 * D), ("dec2", 1, D, D),
+            ("tproj", 0 if t else D, 1, D)]
 
 
 def param_layout(c: TGNConfig):
@@ -263,11 +275,15 @@ class TGNOracle:
         P["mrg_w2"], P["mrg_b2"] = lin("mrg2")
         P["dec_w1"], P["dec_b1"] = lin("dec1")
         P["dec_w2"], P["dec_b2"] = lin("dec2")
+        tw, tb = lin("tproj")
+        P["tp_w"], P["tp_b"] = tw[:, 0], tb
         return P
 
     def _gru(self, P, x, h):
         gi = x @ P["gru_w_ih"].T + P["gru_b_ih"]
         gh = h @ P["gru_w_hh"].T + P["gru_b_hh"]
+        if self.c.backbone == 1:  # JODIE: RNN cell
+            return torch.tanh(gi + gh)
         D = self.c.d_mem
         r = torch.sigmoid(gi[:, :D] + gh[:, :D])
         z = torch.sigmoid(gi[:, D:2 * D] + gh[:, D:2 * D])
@@ -286,7 +302,20 @@ class TGNOracle:
         x = torch.cat([mem[U], mem[other], wd.feat[ev], phi], 1).detach()
         return x, mem[U].detach(), ts
 
-    def _embed(self, w, P, memx, roots, t_roots, data=None):
+    def _embed_jodie(self, w, P, memx, roots, t_roots, upd):
+        """JODIE time projection of the roots' (updated) memory."""
+        lu = self.lu[w].copy()
+        U, mts = upd
+        if len(U):
+            lu[U] = mts
+        s = torch.from_numpy(np.log1p(np.maximum(0.0, np.asarray(t_roots, np.float64) - lu[roots]))).float()
+        emb = memx[roots] * (1 + s[:, None] * P["tp_w"] + P["tp_b"])
+        R = len(roots)
+        return emb, np.full((R, self.c.n_neighbors), -1, np.int64), np.zeros(R, np.int64)
+
+    def _embed(self, w, P, memx, roots, t_roots, data=None, upd=None):
+        if self.c.backbone == 1:
+            return self._embed_jodie(w, P, memx, roots, t_roots, upd)
         c, wd = self.c, (self.W[w] if data is None else data)
         D, T, K, H = c.d_mem, c.d_time, c.n_neighbors, c.n_heads
         R = len(roots)
@@ -413,7 +442,8 @@ class TGNOracle:
                 hn = self._gru(P, x, h)
                 memx = memx.index_put((torch.from_numpy(U),), hn)
             roots = np.concatenate([src, dst, neg])
-            emb, ids, cnt = self._embed(w, P, memx, roots, np.concatenate([ts, ts, ts]))
+            emb, ids, cnt = self._embed(w, P, memx, roots, np.concatenate([ts, ts, ts]),
+                                        upd=(U, mts if len(U) else None))
             pos_l = self._decode(P, emb[:B], emb[B:2 * B])
             neg_l = self._decode(P, emb[:B], emb[2 * B:])
             loss = torch.nn.functional.softplus(-pos_l).mean() + torch.nn.functional.softplus(neg_l).mean()
@@ -527,7 +557,7 @@ class TGNOracle:
                     hn = self._gru(P, x, h)
                     memx[U] = hn
                 emb, _, _ = self._embed(w, P, memx, np.concatenate([src, dst, ng]),
-                                        np.concatenate([ts, ts, ts]), X)
+                                        np.concatenate([ts, ts, ts]), X, upd=(U, mts if len(U) else None))
                 pos.append(self._decode(P, emb[:n], emb[n:2 * n]).numpy())
                 neg.append(self._decode(P, emb[:n], emb[2 * n:]).numpy())
                 if len(U):

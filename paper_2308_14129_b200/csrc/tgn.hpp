@@ -29,11 +29,12 @@ inline int ld_aug(int cols) { return ld32(cols + 1); }  // [x | 1 | pad]
 // (row stride ld_aug(K)); tensors start at 4-float boundaries.
 struct ParamLayout {
     struct Lin { int N, K, ld; std::size_t off; };
-    Lin gru_ih, gru_hh, att_q, att_kv, att_o, mrg1, mrg2, dec1, dec2;
+    Lin gru_ih, gru_hh, att_q, att_kv, att_o, mrg1, mrg2, dec1, dec2, tproj;
     std::size_t time_w, time_b;
     std::size_t total;
     int D, T, F, DQ, DK, DM, H, Kn;
-    void build(int d_mem, int d_time, int d_edge, int heads, int k);
+    int backbone = 0;  // 0 TGN, 1 JODIE (RNN rows, no attention/merge, time projection)
+    void build(int d_mem, int d_time, int d_edge, int heads, int k, int backbone);
 };
 
 struct StepTimes {
@@ -201,6 +202,9 @@ private:
     void step_body(const std::vector<int>& Bs);  // worker steps + all-reduce + Adam (capturable)
     void adam_prepare();
     void backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fused);
+    void decode(int B, bool train);                // k_decoder (fwd, loss, data gradient)
+    void decoder_wgrads(cudaEvent_t at, int B);    // decoder weight gradients (side streams)
+    void jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx, bool post);
     void worker_post(Worker& w);
     void flush_pending(Worker& w);
     void gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,

@@ -387,6 +387,37 @@ __global__ void __launch_bounds__(256) k_gru_bwd_dh(WorkerDev w, Dims d, DhIndex
     }
 }
 
+// JODIE: RNN cell backward on the summed memory-row gradients,
+// dGi = dGh = dH (1 - h'^2), h' saved by k_rnn_fwd in save[u][0:D]
+template <int NM>
+__global__ void __launch_bounds__(256) k_rnn_bwd_dh(WorkerDev w, Dims d, DhIndex x,
+                                                    const float* partial, const float* rpartial,
+                                                    const float* save, float* dGi, float* dGh) {
+    pdl_entry();
+    const int u = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (u >= *w.nU) return;
+    float4 g[NM];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sum_chunks<NM>(g, partial, x.chunk_off[u], x.chunk_off[u + 1], d.D, lane);
+    sum_chunks<NM>(g, rpartial, x.rchunk_off[u], x.rchunk_off[u + 1], d.D, lane);
+    const float* sv = save + (std::size_t)u * 4 * d.D;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+        const int col = 4 * (lane + 32 * i);
+        if (col >= d.D) continue;
+        const float4 h = f4(sv + col);
+        const float4 o = make_float4(rnd_if(g[i].x * (1.f - h.x * h.x), d.rnd), rnd_if(g[i].y * (1.f - h.y * h.y), d.rnd),
+                                     rnd_if(g[i].z * (1.f - h.z * h.z), d.rnd), rnd_if(g[i].w * (1.f - h.w * h.w), d.rnd));
+        *reinterpret_cast<float4*>(dGi + (std::size_t)u * d.ld_g + col) = o;
+        *reinterpret_cast<float4*>(dGh + (std::size_t)u * d.ld_g + col) = o;
+    }
+}
+template __global__ void k_rnn_bwd_dh<1>(WorkerDev, Dims, DhIndex, const float*, const float*,
+                                         const float*, float*, float*);
+template __global__ void k_rnn_bwd_dh<2>(WorkerDev, Dims, DhIndex, const float*, const float*,
+                                         const float*, float*, float*);
+
 template __global__ void k_dh_pull<1, 2>(DhIndex, Dims, const float*, const float*, const float*,
                                          const float*, float*);
 template __global__ void k_dh_pull<1, 4>(DhIndex, Dims, const float*, const float*, const float*,

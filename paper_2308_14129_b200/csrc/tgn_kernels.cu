@@ -195,6 +195,76 @@ __global__ void k_gru_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh,
     }
 }
 
+// ---- JODIE backbone (oracle/tgn_oracle.py states the model):
+// RNN memory updater h' = tanh(Gi + Gh), Gi = [x | 1] W_ih^T, Gh = [h | 1] W_hh^T
+// (TGN's "rnn" memory updater), and the time-projection embedding
+// emb = s' (1 + log1p(t - t_last) w_tp + b_tp) of the root's (updated) memory.
+__global__ void k_rnn_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh, float* save,
+                          float* mem_new) {
+    pdl_entry();
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)(*w.nU) * d.D) return;
+    const int u = static_cast<int>(i / d.D), c = static_cast<int>(i % d.D);
+    const float v = tanhf(Gi[(std::size_t)u * d.ld_g + c] + Gh[(std::size_t)u * d.ld_g + c]);
+    mem_new[(std::size_t)u * d.D + c] = v;
+    if (save) save[(std::size_t)u * 4 * d.D + c] = v;
+}
+
+// one warp per root: s_r = log1p(max(0, t_r - t_last)) in f64 (t_last = the
+// pending message's ts for a node just updated, else its clock), then the
+// projected row; s_r kept for the backward
+__global__ void k_jodie_embed(WorkerDev w, Dims d, int R, const std::uint32_t* roots,
+                              const double* root_t, const float* mem_new, const float* tp, int ldtp,
+                              float* emb, float* s_out) {
+    pdl_entry();
+    const int r = warp_id_global(), lane = lane_id();
+    if (r >= R) return;
+    const std::uint32_t n = roots[r];
+    const int sl = w.slot[n];
+    const float* m = sl >= 0 ? mem_new + (std::size_t)sl * d.D : w.mem + (std::size_t)n * d.D;
+    const double last = sl >= 0 ? w.pTs[sl] : w.lu[n];
+    const float s = static_cast<float>(log1p(fmax(0.0, root_t[r] - last)));
+    for (int c = lane; c < d.D; c += 32)
+        emb[(std::size_t)r * d.D + c] = m[c] * (1.f + s * tp[(std::size_t)c * ldtp] + tp[(std::size_t)c * ldtp + 1]);
+    if (lane == 0) s_out[r] = s;
+}
+
+// backward of the time projection: the roots' memory-row gradients go to
+// dq_in[:, :D] (dm_in[:, DQ:DQ+D] = 0), where k_dh_pull_root sums them per
+// pending row as for TGN's query / merge inputs; (w_tp, b_tp) gradients as
+// per-block f64 partials over a fixed row range (k_jodie_tp_final sums them)
+__global__ void k_jodie_bwd(WorkerDev w, Dims d, int R, const std::uint32_t* roots, const float* mem_new,
+                            const float* tp, int ldtp, const float* s_in, const float* d_emb, float* dq_in,
+                            float* dm_in, int rows_per_block, double* part) {
+    pdl_entry();
+    const int c = threadIdx.x;
+    if (c >= d.D) return;
+    const float wc = tp[(std::size_t)c * ldtp], bc = tp[(std::size_t)c * ldtp + 1];
+    double aw = 0.0, ab = 0.0;
+    const int r0 = blockIdx.x * rows_per_block, r1 = min(R, r0 + rows_per_block);
+    for (int r = r0; r < r1; ++r) {
+        const std::uint32_t n = roots[r];
+        const int sl = w.slot[n];
+        const float m = sl >= 0 ? mem_new[(std::size_t)sl * d.D + c] : w.mem[(std::size_t)n * d.D + c];
+        const float g = d_emb[(std::size_t)r * d.D + c], s = s_in[r];
+        dq_in[(std::size_t)r * d.ld_q + c] = g * (1.f + s * wc + bc);
+        dm_in[(std::size_t)r * d.ld_m + d.DQ + c] = 0.f;
+        aw += (double)(g * m * s);
+        ab += (double)(g * m);
+    }
+    part[(std::size_t)blockIdx.x * 2 * d.D + c] = aw;
+    part[(std::size_t)blockIdx.x * 2 * d.D + d.D + c] = ab;
+}
+
+__global__ void k_jodie_tp_final(int D, int nblk, const double* part, float* g, int ldtp) {
+    pdl_entry();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 2 * D) return;
+    double a = 0.0;
+    for (int b = 0; b < nblk; ++b) a += part[(std::size_t)b * 2 * D + i];
+    g[(std::size_t)(i % D) * ldtp + i / D] += static_cast<float>(a);
+}
+
 // K1 + K2 for the attention query: q_in = [s_root | phi(0)] (one warp per
 // root). The key/value rows are gathered inside the attention kernels
 // (tgn_attn.cu) and never stored.

@@ -91,6 +91,9 @@ __global__ void k_dh_pull_root(DhIndex x, Dims d, const float* dq_in, const floa
 template <int NM>
 __global__ void k_gru_bwd_dh(WorkerDev w, Dims d, DhIndex x, const float* partial,
                              const float* rpartial, const float* save, float* dGi, float* dGh);
+template <int NM>
+__global__ void k_rnn_bwd_dh(WorkerDev w, Dims d, DhIndex x, const float* partial,
+                             const float* rpartial, const float* save, float* dGi, float* dGh);
 
 // Fused embedding head (tgn_head.cu): [ctx | 1] -> ... -> loss -> dctx for
 // blocks of 16 events (48 rows), gemm_mode 1. Weights: att_o / mrg1 / mrg2
@@ -190,6 +193,13 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t
 __global__ void k_round_tf32(const float* src, float* dst, std::size_t n);
 __global__ void k_persist(WorkerDev w, int D, const float* mem_new);
 __global__ void k_pending(WorkerDev w, int B);
+__global__ void k_rnn_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh, float* save, float* mem_new);
+__global__ void k_jodie_embed(WorkerDev w, Dims d, int R, const std::uint32_t* roots, const double* root_t,
+                              const float* mem_new, const float* tp, int ldtp, float* emb, float* s_out);
+__global__ void k_jodie_bwd(WorkerDev w, Dims d, int R, const std::uint32_t* roots, const float* mem_new,
+                            const float* tp, int ldtp, const float* s_in, const float* d_emb, float* dq_in,
+                            float* dm_in, int rows_per_block, double* part);
+__global__ void k_jodie_tp_final(int D, int nblk, const double* part, float* g, int ldtp);
 __global__ void k_surrogate_update(WorkerDev w, int D, const double* w_m, const double* omega,
                                    double gamma, float* mem_new);
 __global__ void k_gen_features(__nv_bfloat16* feat, const std::uint64_t* eids, std::uint64_t E,

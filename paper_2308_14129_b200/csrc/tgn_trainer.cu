@@ -63,7 +63,8 @@ void launch(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaSt
 #define ncclGroupStart NcclApi::get().GroupStart
 #define ncclGroupEnd NcclApi::get().GroupEnd
 
-void ParamLayout::build(int d_mem, int d_time, int d_edge, int heads, int k) {
+void ParamLayout::build(int d_mem, int d_time, int d_edge, int heads, int k, int bb) {
+    backbone = bb;
     D = d_mem;
     T = d_time;
     F = d_edge;
@@ -84,18 +85,23 @@ void ParamLayout::build(int d_mem, int d_time, int d_edge, int heads, int k) {
         l.off = off;
         off += std::size_t(N) * l.ld;
     };
-    // order == oracle/tgn_oracle.py linear_specs
-    lin(gru_ih, 3 * D, DM);
-    lin(gru_hh, 3 * D, D);
-    lin(att_q, DQ, DQ);
-    lin(att_kv, 2 * DQ, DK);
-    lin(att_o, DQ, DQ);
-    lin(mrg1, D, DQ + D);
-    lin(mrg2, D, D);
+    // order == oracle/tgn_oracle.py linear_specs. JODIE: one RNN gate block,
+    // no attention / merge layers (zero rows), a time projection (1 -> D) last
+    const bool tgn = backbone == 0;
+    lin(gru_ih, tgn ? 3 * D : D, DM);
+    lin(gru_hh, tgn ? 3 * D : D, D);
+    lin(att_q, tgn ? DQ : 0, DQ);
+    lin(att_kv, tgn ? 2 * DQ : 0, DK);
+    lin(att_o, tgn ? DQ : 0, DQ);
+    lin(mrg1, tgn ? D : 0, DQ + D);
+    lin(mrg2, tgn ? D : 0, D);
     lin(dec1, D, 2 * D);
     lin(dec2, 1, D);
+    lin(tproj, tgn ? 0 : D, 1);
     total = off;
 }
+
+constexpr int kJodieRows = 64;  // roots per k_jodie_bwd block (fixed: the partials' order)
 
 // ------------------------------------------------------------ scratch
 struct Scratch {
@@ -110,6 +116,8 @@ struct Scratch {
     DevBuf<float> dD1, dd_in, d_emb, dZ1, dm_in, dctx, dxbar, dQp, dQ, dq_in;
     DevBuf<float> ws;
     DevBuf<float> decw;  // decoder weight-gradient chunk partials (k_dec_wgrad_part)
+    DevBuf<float> s_root;  // JODIE: log1p(dt) of each root
+    DevBuf<double> tp_part;  // JODIE: time-projection gradient partials [blocks][2D]
     DevBuf<double> tpart;
     // deterministic dH reduction (tgn_dh.cu): reader index + chunk partials
     DevBuf<int> dh_hist, dh_off_occ, dh_off_root, dh_chunk_off, dh_rchunk_off, dh_chunk_slot,
@@ -344,15 +352,17 @@ void dh_pull_root(const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
     if ((d.D + 127) / 128 == 1) go(tgnk::k_dh_pull_root<1>);
     else go(tgnk::k_dh_pull_root<2>);
 }
-void gru_bwd_dh(const tgnk::WorkerDev& wd, const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
+void gru_bwd_dh(const tgnk::WorkerDev& wd, const tgnk::Dims& d, const Scratch& s, cudaStream_t st,
+                bool rnn = false) {
     const unsigned grid = unsigned((std::size_t(s.U) * 32 + 255) / 256);
     auto go = [&](auto k) {
         launch(k, grid, 256, 0, st, wd, d, s.dh, static_cast<const float*>(s.dh_partial.p),
                static_cast<const float*>(s.dh_rpartial.p), static_cast<const float*>(s.gsave.p),
                s.dGi.p, s.dGh.p);
     };
-    if ((d.D + 127) / 128 == 1) go(tgnk::k_gru_bwd_dh<1>);
-    else go(tgnk::k_gru_bwd_dh<2>);
+    const bool one = (d.D + 127) / 128 == 1;
+    if (rnn) one ? go(tgnk::k_rnn_bwd_dh<1>) : go(tgnk::k_rnn_bwd_dh<2>);
+    else one ? go(tgnk::k_gru_bwd_dh<1>) : go(tgnk::k_gru_bwd_dh<2>);
 }
 
 void attn_abs_bwd(const tgnk::WorkerDev& wd, const tgnk::Dims& d, int R, const float* tw,
@@ -382,9 +392,9 @@ void init_params_host(const ParamLayout& L, std::uint64_t seed, std::vector<floa
             L.T > 1 ? std::pow(10.0, -9.0 * double(i) / double(L.T - 1)) : 1.0);
     const std::uint64_t s = mix64(seed);
     const ParamLayout::Lin* lins[] = {&L.gru_ih, &L.gru_hh, &L.att_q, &L.att_kv, &L.att_o,
-                                      &L.mrg1,   &L.mrg2,   &L.dec1,  &L.dec2};
-    const int fans[] = {L.D, L.D, L.DQ, L.DK, L.DQ, L.DQ + L.D, L.D, 2 * L.D, L.D};
-    for (int t = 0; t < 9; ++t) {
+                                      &L.mrg1,   &L.mrg2,   &L.dec1,  &L.dec2, &L.tproj};
+    const int fans[] = {L.D, L.D, L.DQ, L.DK, L.DQ, L.DQ + L.D, L.D, 2 * L.D, L.D, L.D};
+    for (int t = 0; t < 10; ++t) {
         const auto& l = *lins[t];
         const double a = 1.0 / std::sqrt(double(fans[t]));
         auto draw = [&](std::uint64_t tag, std::uint64_t i) {
@@ -440,7 +450,8 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     SPD_CUDA(cudaStreamCreateWithPriority(&zs_, cudaStreamNonBlocking, prio_lo));
     for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_dhidx_, &ev_zfork_, &ev_zero_, &ev_bwdx_, &ev_pull_})
         SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors);
+    if (cfg.backbone != 0 && cfg.backbone != 1) data_error("InvalidParams", "backbone must be 0 (TGN) or 1 (JODIE)");
+    lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors, cfg.backbone);
     feat_seed_mixed_ = mix64(cfg.seed_feat);
     const int D = lay_.D, F = lay_.F;
     const int Fp = F ? (F + 7) / 8 * 8 : 0;
@@ -540,6 +551,10 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
     s.decw.alloc(std::size_t((B + tgnk::kDecWgEv - 1) / tgnk::kDecWgEv) *
                  (std::size_t(D) * (2 * D + 1) + D + 1));
+    if (cfg.backbone == 1) {
+        s.s_root.alloc(R);
+        s.tp_part.alloc(std::size_t((R + kJodieRows - 1) / kJodieRows) * 2 * D);
+    }
     s.trows = 16;
     s.troot_blocks = (R + s.trows - 1) / s.trows;
     // k_attn_time_grad: grid-stride over the roots on one block per SM (a
@@ -549,12 +564,12 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.dh.nbr_node = s.nbr_node.p; s.dh.cnt = s.cnt.p; s.dh.roots = s.roots.p;
     {
         const char* e = std::getenv("SPD_GRU_FUSED");
-        gru_fused_ = !(e && *e == '0');
+        gru_fused_ = !(e && *e == '0') && cfg.backbone == 0;
     }
     {  // fused head (tgn_head.cu): one 227 KB CTA per 16 events; opt-in (SPD_FUSED_HEAD=1):
        // GDELT B = 2000 step 0.483 ms with it vs 0.411 ms with the separate kernels
         const char* e = std::getenv("SPD_FUSED_HEAD");
-        head_fits_ = (e && *e == '1') && d.DQ + d.D <= 320 &&
+        head_fits_ = (e && *e == '1') && cfg.backbone == 0 && d.DQ + d.D <= 320 &&
                      tgnk::head_smem_bytes(d) <= std::size_t(227) * 1024;
     }
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
@@ -883,6 +898,19 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
     launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
         wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
     if (after_gather) after_gather();
+    if (lay_.backbone == 1) {  // JODIE: RNN memory updater (one gate block)
+        SPD_CUDA(cudaEventRecord(ev_aux_fork_, stream_));
+        SPD_CUDA(cudaStreamWaitEvent(aux_, ev_aux_fork_, 0));
+        proj_fwd(tc, s.h_gru.p, d.ld_h, PW + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, d.D,
+                 d.D + 1, w.nU(), aux_);
+        proj_fwd(tc, s.x_gru.p, d.ld_x, PW + lay_.gru_ih.off, lay_.gru_ih.ld, s.Gi.p, d.ld_g, s.U, d.D,
+                 d.DM + 1, w.nU(), stream_);
+        SPD_CUDA(cudaEventRecord(ev_aux_join_, aux_));
+        SPD_CUDA(cudaStreamWaitEvent(stream_, ev_aux_join_, 0));
+        launch(tgnk::k_rnn_fwd, blocks_for(std::size_t(s.U) * d.D), 256, 0, stream_, wd, d, s.Gi.p, s.Gh.p,
+               train ? s.gsave.p : nullptr, s.mem_new.p);
+        return;
+    }
     if (tc && gru_fused_) {  // both gate GEMMs and the cell in one tcgen05 kernel (umma_gru.cuh)
         umma::gru_fused(s.x_gru.p, d.ld_x, d.DM + 1, s.h_gru.p, d.ld_h, d.D + 1, PW + lay_.gru_ih.off,
                         lay_.gru_ih.ld, PW + lay_.gru_hh.off, lay_.gru_hh.ld, d.D, s.U, w.nU(), w.mem.p,
@@ -938,7 +966,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     };
     if (profile_) timed("roots_nbrs", [&] { roots(st); });
     s.dh.R = R;  // this batch's roots and occurrences (a loop's last batch may be short)
-    s.dh.RK = R * d.K;
+    s.dh.RK = lay_.backbone == 1 ? 0 : R * d.K;  // JODIE: no neighbour readers
     // this batch's last messages into the other pending set (K3): depends only
     // on the batch's events, off the critical path (the GRU below reads the
     // current set); eval steps run it in their post phase
@@ -968,6 +996,10 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     if (!profile_) fork_roots();
     if (profile_ && train) timed("dh_index", [&] { dh_index(wd, s, st); });
     if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_roots_, 0));
+    if (lay_.backbone == 1) {  // JODIE: time projection + decoder (no attention)
+        jodie_rest(w, wd, B, train, slot_idx, post);
+        return;
+    }
     timed("query_gather", [&] {
         launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
                P + lay_.time_w, P + lay_.time_b, s.roots.p, s.mem_new.p, s.q_in.p,
@@ -1025,23 +1057,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
                  d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU, nullptr, 0, tc);
         proj_fwd(tc, s.Z1.p, d.ld_z, PW + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
                  nullptr, st);
-        // the decoder, its loss and its data gradient: one FFMA kernel (k_decoder;
-        // its TMA row copies need 16-B aligned weight rows)
-        if (lay_.dec1.off % 4 || lay_.dec1.ld % 4) internal_error("InvalidParams", "decoder rows unaligned");
-        static std::size_t dec_smem_set = 0;
-        const std::size_t dsm = tgnk::decoder_smem_bytes(d);
-        const bool narrow = 4 * d.D <= 416;
-        auto kdec = narrow ? tgnk::k_decoder<416, 2> : tgnk::k_decoder<768, 1>;
-        if (dsm > dec_smem_set) {
-            SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder<416, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
-            SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder<768, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
-            dec_smem_set = dsm;
-        }
-        launch(kdec, unsigned((B + tgnk::kDecEv - 1) / tgnk::kDecEv),
-               unsigned((4 * d.D + 31) / 32 * 32), dsm, st, d, B, static_cast<const float*>(s.emb.p),
-               static_cast<const float*>(P + lay_.dec1.off), lay_.dec1.ld,
-               static_cast<const float*>(P + lay_.dec2.off), s.D1.p, s.dlogit.p, s.lossv.p, s.dD1.p,
-               s.logits.p, s.d_emb.p, train ? 1 : 0);
+        decode(B, train);
     });
     // the batch loss is only read by the host after the step: off the critical path
     auto sum_loss = [&](cudaStream_t sx) {
@@ -1053,6 +1069,132 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     // persist this batch's memory update and store its last messages now,
     // while the scratch still holds this worker's rows (K11, K3); the last
     // worker of a training step defers it to step_body (beside the optimizer)
+    if (!post) return;
+    timed("post", [&] {
+        launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
+        if (!train) launch(tgnk::k_pending, 1, 1024, 0, st, wd, B);
+    });
+}
+
+// Decoder weight gradients on side streams forked from `at` (both backbones).
+void TGNTrainer::decoder_wgrads(cudaEvent_t at, int B) {
+    Scratch& s = *s_;
+    const auto& d = s.d;
+    float* G = grads_.p;
+    if (d.D <= 112) {  // decoder weight gradients: chunk partials + fixed-order sum (FFMA)
+        side_from(at, [&](cudaStream_t sd) {
+            static std::size_t wg_smem_set = 0;
+            const std::size_t sm = tgnk::dec_wgrad_smem_bytes(d);
+            if (sm > wg_smem_set) {
+                SPD_CUDA(cudaFuncSetAttribute(tgnk::k_dec_wgrad_part,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+                wg_smem_set = sm;
+            }
+            const int nblk = (B + tgnk::kDecWgEv - 1) / tgnk::kDecWgEv;
+            launch(tgnk::k_dec_wgrad_part, unsigned(nblk), 256, sm, sd, d, B,
+                   static_cast<const float*>(s.emb.p), static_cast<const float*>(s.dD1.p),
+                   static_cast<const float*>(s.dlogit.p), static_cast<const float*>(s.D1.p), s.decw.p);
+            const int per = d.D * (2 * d.D + 1) + d.D + 1;
+            launch(tgnk::k_dec_wgrad_reduce, unsigned((per + 255) / 256), 256, 0, sd, d, nblk,
+                   static_cast<const float*>(s.decw.p), G + lay_.dec1.off, lay_.dec1.ld, G + lay_.dec2.off);
+        });
+    } else {
+        side_from(at, [&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off,
+                                                        lay_.dec2.ld, 1, d.D + 1, 2 * B, nullptr, ws_cur_,
+                                                        wsn_cur_, sd); });
+        side_from(at, [&](cudaStream_t sd) {
+            // the gathered decoder input [z_u | z_v | 1] is only needed here
+            launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, sd, d, B,
+                   s.emb.p, s.d_in.p);
+            gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
+                   2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
+    }
+}
+
+// The decoder, its loss and its data gradient: one FFMA kernel (k_decoder)
+// on the trainer stream (both backbones).
+void TGNTrainer::decode(int B, bool train) {
+    Scratch& s = *s_;
+    const auto& d = s.d;
+    const float* P = params_.p;
+    cudaStream_t st = stream_;
+    // (its TMA row copies need 16-B aligned weight rows)
+    if (lay_.dec1.off % 4 || lay_.dec1.ld % 4) internal_error("InvalidParams", "decoder rows unaligned");
+    static std::size_t dec_smem_set = 0;
+    const std::size_t dsm = tgnk::decoder_smem_bytes(d);
+    const bool narrow = 4 * d.D <= 416;
+    auto kdec = narrow ? tgnk::k_decoder<416, 2> : tgnk::k_decoder<768, 1>;
+    if (dsm > dec_smem_set) {
+        SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder<416, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
+        SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder<768, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
+        dec_smem_set = dsm;
+    }
+    launch(kdec, unsigned((B + tgnk::kDecEv - 1) / tgnk::kDecEv),
+           unsigned((4 * d.D + 31) / 32 * 32), dsm, st, d, B, static_cast<const float*>(s.emb.p),
+           static_cast<const float*>(P + lay_.dec1.off), lay_.dec1.ld,
+           static_cast<const float*>(P + lay_.dec2.off), s.D1.p, s.dlogit.p, s.lossv.p, s.dD1.p,
+           s.logits.p, s.d_emb.p, train ? 1 : 0);
+}
+
+// JODIE after the memory update: time-projection embedding, decoder, loss and
+// (training) the backward — decoder weight gradients, time projection, the
+// roots' memory-row gradients summed per pending row (tgn_dh.cu), RNN cell
+// backward and its weight gradients; then the post phase.
+void TGNTrainer::jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx,
+                            bool post) {
+    Scratch& s = *s_;
+    const auto& d = s.d;
+    const int R = 3 * B;
+    float* P = params_.p;
+    float* G = grads_.p;
+    cudaStream_t st = stream_;
+    const bool tc = cfg_.gemm_mode == 1;
+    const float* TP = P + lay_.tproj.off;
+    const int ldtp = lay_.tproj.ld;
+    timed("jodie_embed", [&] {
+        launch(tgnk::k_jodie_embed, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R, s.roots.p,
+               static_cast<const double*>(s.root_t.p), static_cast<const float*>(s.mem_new.p), TP, ldtp,
+               s.emb.p, s.s_root.p);
+    });
+    timed("head_fwd", [&] { decode(B, train); });
+    auto sum_loss = [&](cudaStream_t sx) {
+        launch(tgnk::k_sum_loss, 1, 1024, 0, sx, s.lossv.p, 2 * B, s.loss.p + slot_idx);
+    };
+    if (train) side(sum_loss);
+    else sum_loss(st);
+    if (train) {
+        SPD_CUDA(cudaStreamWaitEvent(st, ev_zero_, 0));  // gradients cleared (step_body)
+        const bool fresh = scratch_zeroed_;
+        scratch_zeroed_ = false;
+        timed("head_bwd", [&] {
+            cudaEvent_t at = mark();
+            const int nblk = (R + kJodieRows - 1) / kJodieRows;
+            launch(tgnk::k_jodie_bwd, unsigned(nblk), unsigned((d.D + 31) / 32 * 32), 0, st, wd, d, R,
+                   s.roots.p, static_cast<const float*>(s.mem_new.p), TP, ldtp,
+                   static_cast<const float*>(s.s_root.p), static_cast<const float*>(s.d_emb.p), s.dq_in.p,
+                   s.dm_in.p, kJodieRows, s.tp_part.p);
+            cudaEvent_t at_tp = mark();
+            side_from(at_tp, [&](cudaStream_t sd) {
+                launch(tgnk::k_jodie_tp_final, blocks_for(std::size_t(2) * d.D), 256, 0, sd, d.D, nblk,
+                       static_cast<const double*>(s.tp_part.p), G + lay_.tproj.off, ldtp);
+            });
+            decoder_wgrads(at, B);
+        });
+        timed("gru_bwd", [&] {
+            if (tc && !fresh) {
+                s.dGi.zero(st);
+                s.dGh.zero(st);
+            }
+            if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_dhidx_, 0));  // the dH reader index
+            dh_pull_root(d, s, st);
+            gru_bwd_dh(wd, d, s, st, true);
+            side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off,
+                                                   lay_.gru_ih.ld, d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
+            side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off,
+                                                   lay_.gru_hh.ld, d.D, d.D + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
+        });
+        join_side();
+    }
     if (!post) return;
     timed("post", [&] {
         launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
@@ -1101,34 +1243,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fuse
         cudaEvent_t at = mark();
         proj_dgrad(tc, s.d_emb.p, d.D, PW + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
                    nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z, tc);
-        if (d.D <= 112) {  // decoder weight gradients: chunk partials + fixed-order sum (FFMA)
-            side_from(at, [&](cudaStream_t sd) {
-                static std::size_t wg_smem_set = 0;
-                const std::size_t sm = tgnk::dec_wgrad_smem_bytes(d);
-                if (sm > wg_smem_set) {
-                    SPD_CUDA(cudaFuncSetAttribute(tgnk::k_dec_wgrad_part,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-                    wg_smem_set = sm;
-                }
-                const int nblk = (B + tgnk::kDecWgEv - 1) / tgnk::kDecWgEv;
-                launch(tgnk::k_dec_wgrad_part, unsigned(nblk), 256, sm, sd, d, B,
-                       static_cast<const float*>(s.emb.p), static_cast<const float*>(s.dD1.p),
-                       static_cast<const float*>(s.dlogit.p), static_cast<const float*>(s.D1.p), s.decw.p);
-                const int per = d.D * (2 * d.D + 1) + d.D + 1;
-                launch(tgnk::k_dec_wgrad_reduce, unsigned((per + 255) / 256), 256, 0, sd, d, nblk,
-                       static_cast<const float*>(s.decw.p), G + lay_.dec1.off, lay_.dec1.ld, G + lay_.dec2.off);
-            });
-        } else {
-            side_from(at, [&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off,
-                                                            lay_.dec2.ld, 1, d.D + 1, 2 * B, nullptr, ws_cur_,
-                                                            wsn_cur_, sd); });
-            side_from(at, [&](cudaStream_t sd) {
-                // the gathered decoder input [z_u | z_v | 1] is only needed here
-                launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, sd, d, B,
-                       s.emb.p, s.d_in.p);
-                gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
-                       2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
-        }
+        decoder_wgrads(at, B);
         side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off,
                                                         lay_.mrg2.ld, d.D, d.D + 1, R, nullptr, ws_cur_,
                                                         wsn_cur_, sd); });
@@ -1224,6 +1339,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fuse
             s.dGi.zero(st);
             s.dGh.zero(st);
         }
+        if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_dhidx_, 0));  // the dH reader index
         dh_pull_root(d, s, st);
         if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_pull_, 0));  // occurrence chunk partials
         gru_bwd_dh(wd, d, s, st);

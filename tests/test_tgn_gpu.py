@@ -408,3 +408,47 @@ def test_device_shuffle_combine_matches_host_rebind(parts, workers):
             assert np.array_equal(m1, m2) and np.array_equal(l1, l2), (epoch, w)
     host.close()
     dev.close()
+
+
+@pytest.mark.parametrize("gemm_mode", [0, 1])
+@pytest.mark.parametrize("parts", [1, 2])
+def test_jodie_backbone_matches_oracle(parts, gemm_mode):
+    """JODIE backbone (spd_tgn_config.backbone = 1): RNN memory
+    updater + time-projection embedding on the same message, last-message,
+    decoder and PAC-schedule kernels. Per-step embeddings, losses, first-step
+    gradients, parameters, memory and clocks against the oracle's JODIE, a
+    whole epoch with the epoch-end restore + shared-hub sync included."""
+    _, _, pa, subs = partitioned(parts=parts)
+    cfg = small_cfg(backbone=1, gemm_mode=gemm_mode)
+    tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+    o = oracle_for(cfg, subs, pa.shared)
+    assert tr.n_params == o.total and np.array_equal(tr.params(), o.flat.numpy())
+    tr.set_debug(True)
+    step_tol = TOL_STEP if gemm_mode == 0 else TOL_TF32_STEP
+    traj_tol = TOL_TRAJ if gemm_mode == 0 else TOL_TF32
+    tr.begin_epoch(0)
+    o.begin_epoch(0)
+    for step in range(o.epoch_steps()):
+        gl = tr.step()
+        ol = o.step()
+        tol = step_tol if step == 0 else traj_tol
+        for w in range(parts):
+            if np.isnan(ol[w]):
+                continue
+            t = tr.last_step(w)
+            assert np.array_equal(t["neg"], glob(o, w, o.last[w]["neg"]))
+            assert rel_err(t["emb"], o.last[w]["emb"]) < tol, (step, w, rel_err(t["emb"], o.last[w]["emb"]))
+            assert abs(gl[w] - ol[w]) <= tol * max(1.0, abs(ol[w])), (step, gl[w], ol[w])
+        if step == 0:
+            assert rel_err(tr.grads(), o.grad.numpy()) < (TOL_GRAD if gemm_mode == 0 else TOL_TF32_GRAD)
+        assert rel_err(tr.params(), o.flat.numpy()) < traj_tol, step
+    tr.end_epoch()
+    o.end_epoch()
+    # memory after a whole epoch: TF32 GEMM differences accumulate through
+    # every RNN update of a row (parameters stay within the trajectory bar)
+    mem_tol = traj_tol if gemm_mode == 0 else 6e-2
+    for w in range(parts):
+        m, lu = tr.memory(w)
+        assert np.array_equal(lu, o.lu[w])
+        assert rel_err(m, o.mem[w].numpy()) < mem_tol
+    tr.close()

@@ -24,7 +24,7 @@ def oracle_for(cfg: sp.TGNConfig, subs, shared):
                      n_neighbors=cfg.n_neighbors, n_heads=cfg.n_heads, batch_size=cfg.batch_size,
                      lr=cfg.lr, beta1=cfg.beta1, beta2=cfg.beta2, adam_eps=cfg.adam_eps,
                      seed_init=cfg.seed_init, seed_feat=cfg.seed_feat, seed_neg=cfg.seed_neg,
-                     sync_average=cfg.sync_average)
+                     sync_average=cfg.sync_average, backbone=cfg.backbone)
     ws = [T.WorkerData(g.nodes, g.edges, g.eids, oc.d_edge, oc.seed_feat) for g in subs]
     return T.TGNOracle(oc, ws, list(shared))
 
