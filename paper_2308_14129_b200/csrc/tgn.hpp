@@ -201,7 +201,7 @@ private:
     void commit_ctl();
     void step_body(const std::vector<int>& Bs);  // worker steps + all-reduce + Adam (capturable)
     void adam_prepare();
-    void backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fused);
+    void backward(Worker& w, const tgnk::WorkerDev& wd, int B);
     void decode(int B, bool train);                // k_decoder (fwd, loss, data gradient)
     void decoder_wgrads(cudaEvent_t at, int B);    // decoder weight gradients (side streams)
     void jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx, bool post);
@@ -250,7 +250,6 @@ private:
     cudaEvent_t ev_bwdx_ = nullptr;  // attention time-encoder partials done
     cudaEvent_t ev_pull_ = nullptr;  // dH chunk partials done (tgn_dh.cu)
     bool scratch_zeroed_ = false;    // dGi/dGh cleared by this step's k_zero_list
-    bool head_fits_ = false;         // the fused head (tgn_head.cu) supports these dims
     bool gru_fused_ = true;          // gemm_mode 1: fused tcgen05 GRU (SPD_GRU_FUSED=0: two GEMMs + cell)
 
     spd_tgn_config cfg_;

@@ -95,27 +95,6 @@ template <int NM>
 __global__ void k_rnn_bwd_dh(WorkerDev w, Dims d, DhIndex x, const float* partial,
                              const float* rpartial, const float* save, float* dGi, float* dGh);
 
-// Fused embedding head (tgn_head.cu): [ctx | 1] -> ... -> loss -> dctx for
-// blocks of 16 events (48 rows), gemm_mode 1. Weights: att_o / mrg1 / mrg2
-// tf32-rounded (tensor cores), dec1 / dec2 FP32 (FFMA).
-struct HeadArgs {
-    Dims d;
-    int B;
-    WorkerDev w;
-    const float* ctx;
-    const int* cnt;
-    const std::uint32_t* roots;
-    const float* mem_new;
-    const float* Wo; int ldo;
-    const float* Wm1; int ldm1;
-    const float* Wm2; int ldm2;
-    const float* Wd1; int ldd1;
-    const float* wd2;
-    float *m_in, *Z1, *emb, *D1, *dlogit, *lossv, *logits, *dD1, *d_emb, *dZ1, *dm_in, *dctx;
-};
-__global__ void k_head(HeadArgs h);
-std::size_t head_smem_bytes(const Dims& d);
-int head_events_per_block();
 
 // --- kernels (definitions in tgn_kernels.cu) -------------------------------
 __global__ void k_init_aug(float* buf, int rows, int cols, int ld);

@@ -566,12 +566,6 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         const char* e = std::getenv("SPD_GRU_FUSED");
         gru_fused_ = !(e && *e == '0') && cfg.backbone == 0;
     }
-    {  // fused head (tgn_head.cu): one 227 KB CTA per 16 events; opt-in (SPD_FUSED_HEAD=1):
-       // GDELT B = 2000 step 0.483 ms with it vs 0.411 ms with the separate kernels
-        const char* e = std::getenv("SPD_FUSED_HEAD");
-        head_fits_ = (e && *e == '1') && cfg.backbone == 0 && d.DQ + d.D <= 320 &&
-                     tgnk::head_smem_bytes(d) <= std::size_t(227) * 1024;
-    }
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
     SPD_CUDA(cudaStreamSynchronize(stream_));
 
@@ -1003,7 +997,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     timed("query_gather", [&] {
         launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
                P + lay_.time_w, P + lay_.time_b, s.roots.p, s.mem_new.p, s.q_in.p,
-               train && tc && head_fits_ ? nullptr : s.m_in.p);
+               s.m_in.p);
     });
     timed("gemm_q", [&] {
         proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
@@ -1025,29 +1019,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
         proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
                  nullptr, 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
     });
-    // gemm_mode 1 training steps: the fused head (tgn_head.cu), ctx -> loss -> dctx
-    const bool fused = train && tc && head_fits_;
-    if (fused) timed("head_fused", [&] {
-        tgnk::HeadArgs h{};
-        h.d = d; h.B = B; h.w = wd; h.ctx = s.ctx.p; h.cnt = s.cnt.p; h.roots = s.roots.p;
-        h.mem_new = s.mem_new.p;
-        h.Wo = PW + lay_.att_o.off; h.ldo = lay_.att_o.ld;
-        h.Wm1 = PW + lay_.mrg1.off; h.ldm1 = lay_.mrg1.ld;
-        h.Wm2 = PW + lay_.mrg2.off; h.ldm2 = lay_.mrg2.ld;
-        h.Wd1 = P + lay_.dec1.off; h.ldd1 = lay_.dec1.ld; h.wd2 = P + lay_.dec2.off;
-        h.m_in = s.m_in.p; h.Z1 = s.Z1.p; h.emb = s.emb.p; h.D1 = s.D1.p; h.dlogit = s.dlogit.p;
-        h.lossv = s.lossv.p; h.logits = s.logits.p; h.dD1 = s.dD1.p; h.d_emb = s.d_emb.p;
-        h.dZ1 = s.dZ1.p; h.dm_in = s.dm_in.p; h.dctx = s.dctx.p;
-        const std::size_t sm = tgnk::head_smem_bytes(d);
-        static std::size_t set = 0;
-        if (sm > set) {
-            SPD_CUDA(cudaFuncSetAttribute(tgnk::k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-            set = sm;
-        }
-        const int eb = tgnk::head_events_per_block();
-        launch(tgnk::k_head, unsigned((B + eb - 1) / eb), 256, sm, st, h);
-    });
-    else timed("head_fwd", [&] {
+    timed("head_fwd", [&] {
         // O = [ctx | 1] W_o^T straight into the MergeLayer input's attention
         // columns, 0 for roots without neighbours (the s_root columns came
         // with the query gather)
@@ -1065,7 +1037,7 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     };
     if (train) side(sum_loss);
     else sum_loss(st);
-    if (train) backward(w, wd, B, fused);
+    if (train) backward(w, wd, B);
     // persist this batch's memory update and store its last messages now,
     // while the scratch still holds this worker's rows (K11, K3); the last
     // worker of a training step defers it to step_body (beside the optimizer)
@@ -1204,7 +1176,7 @@ void TGNTrainer::jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool tr
 
 // Hand-written backward of one worker's batch; weight-gradient GEMMs go to the
 // side stream and are joined before the post phase rewrites their inputs.
-void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fused) {
+void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     Scratch& s = *s_;
     const auto& d = s.d;
     const int R = 3 * B;
@@ -1218,24 +1190,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B, bool fuse
     // first backward; later local workers reuse the scratch and clear them
     const bool fresh = scratch_zeroed_;
     scratch_zeroed_ = false;
-    if (fused) {  // the head's data gradients are done (k_head): its weight gradients only
-        side([&](cudaStream_t sd) { gemm_wgrad(s.dlogit.p, 4, s.D1.p, d.ld_d1, G + lay_.dec2.off,
-                                               lay_.dec2.ld, 1, d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd); });
-        side([&](cudaStream_t sd) {
-            launch(tgnk::k_dec_gather, blocks_for(std::size_t(2 * B) * 32), 256, 0, sd, d, B,
-                   s.emb.p, s.d_in.p);
-            gemm_wgrad(s.dD1.p, d.D, s.d_in.p, d.ld_din, G + lay_.dec1.off, lay_.dec1.ld, d.D,
-                       2 * d.D + 1, 2 * B, nullptr, ws_cur_, wsn_cur_, sd);
-        });
-        side([&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off,
-                                               lay_.mrg2.ld, d.D, d.D + 1, R, nullptr, ws_cur_, wsn_cur_, sd); });
-        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dZ1.p, d.D, s.m_in.p, d.ld_m, G + lay_.mrg1.off,
-                                               lay_.mrg1.ld, d.D, d.DQ + d.D + 1, R, nullptr, ws_cur_,
-                                               wsn_cur_, sd); });
-        side([&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off,
-                                               lay_.att_o.ld, d.DQ, d.DQ + 1, R, nullptr, ws_cur_,
-                                               wsn_cur_, sd); });
-    } else timed("head_bwd", [&] {
+    timed("head_bwd", [&] {
         // (d_emb came with the forward: k_decoder). Each data-gradient GEMM is
         // created before the weight-gradient side work forked from the same
         // point, so replays hand the critical path its SMs first.

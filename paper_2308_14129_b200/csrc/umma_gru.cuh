@@ -155,12 +155,27 @@ __global__ void __launch_bounds__(THREADS, 1) umma_gru_kernel(const __grid_const
         // thread one row, 8 units at a time: 6 x 8 accumulator values
         const int quad = warp & 3;
         const int row = m0 + quad * 32 + lane;
-        mbar_wait(tmem_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;");
         const bool live = row < M;
         const int D = args.D;
-        const float* hrow = live ? args.mem + (std::size_t)args.nodes[row] * D : nullptr;
-#pragma unroll 1
+        // the row's exact h values (a gather from the memory store) are loaded
+        // while the MMAs run, not after
+        float hall[UB];
+        {
+            const float* hrow = live ? args.mem + (std::size_t)args.nodes[row] * D : nullptr;
+#pragma unroll
+            for (int j = 0; j < UB; j += 4) {
+                if (live && u0 + j + 4 <= D) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(hrow + u0 + j));
+                    hall[j] = v.x; hall[j + 1] = v.y; hall[j + 2] = v.z; hall[j + 3] = v.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) hall[j + q] = live && u0 + j + q < D ? hrow[u0 + j + q] : 0.f;
+                }
+            }
+        }
+        mbar_wait(tmem_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
         for (int c0 = 0; c0 < UB; c0 += 8) {
             if (u0 + c0 >= D) break;
             const std::uint32_t base = tmem + (static_cast<std::uint32_t>(quad * 32) << 16) + c0;
@@ -173,11 +188,10 @@ __global__ void __launch_bounds__(THREADS, 1) umma_gru_kernel(const __grid_const
             tmem_ld8(base + C_::ACC_H + 2 * UB, hn);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (!live) continue;
-            float hv[8], o[8], rr[8], zz[8], nn[8];
+            float o[8], rr[8], zz[8], nn[8];
+            const float* hv = hall + c0;
             const int u = u0 + c0;
             const bool full8 = u + 8 <= D;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) hv[j] = (full8 || u + j < D) ? hrow[u + j] : 0.f;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 rr[j] = 1.f / (1.f + expf(-(ir[j] + hr[j])));
