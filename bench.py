@@ -346,6 +346,17 @@ def main():
     except Exception:
         ndev = 1
     local = local % ndev
+    if world > 1 and args.impl == "ours" and args.transport == "peer" and ndev > 1:
+        # the peer-memory transport maps every rank's HBM: needs P2P between the GPUs
+        import torch
+        others = {r % ndev for r in range(world)} - {local}
+        if not all(torch.cuda.can_device_access_peer(local, o) for o in others):
+            print(f"[bench] rank {rank}: no P2P access between GPUs, using NCCL", file=sys.stderr)
+            args.transport = "nccl"
+        flags = [None] * world  # every rank must agree on the transport
+        pg.all_gather_object(flags, args.transport)
+        if "nccl" in flags:
+            args.transport = "nccl"
     verbose = rank == 0
 
     def log(msg):
