@@ -542,55 +542,60 @@ __global__ void __launch_bounds__(256) k_dec_wgrad_part(Dims d, int B, const flo
     pdl_entry();
     extern __shared__ __align__(16) float wsm[];
     const int D = d.D, ld = D + 4;
-    float* sgp = wsm;                    // [EV][ld] dD1 of positive pairs
-    float* sgn = sgp + kDecWgEv * ld;    // [EV][ld] dD1 of negative pairs
-    float* sz = sgn + kDecWgEv * ld;     // [3][EV][ld] z_src | z_dst | z_neg
-    const int e0 = blockIdx.x * kDecWgEv, ne = min(kDecWgEv, B - e0);
+    float* sgp = wsm;                      // [TILE][ld] dD1 of positive pairs
+    float* sgn = sgp + kDecWgTile * ld;    // [TILE][ld] dD1 of negative pairs
+    float* sz = sgn + kDecWgTile * ld;     // [3][TILE][ld] z_src | z_dst | z_neg
+    const int c0 = blockIdx.x * kDecWgEv, c1 = min(B, c0 + kDecWgEv);
     const int tid = threadIdx.x, D4 = D / 4;
-    for (int i = tid; i < 5 * kDecWgEv * D4; i += blockDim.x) {
-        const int r = i / D4, c = 4 * (i % D4), which = r / kDecWgEv, e = r % kDecWgEv;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (e < ne) {
-            const float* src = which == 0 ? dD1 + (std::size_t)(e0 + e) * D
-                             : which == 1 ? dD1 + (std::size_t)(B + e0 + e) * D
-                                          : emb + ((std::size_t)(which - 2) * B + e0 + e) * D;
-            v = *reinterpret_cast<const float4*>(src + c);
-        }
-        *reinterpret_cast<float4*>(wsm + (std::size_t)r * ld + c) = v;
-    }
-    __syncthreads();
     float* out = part + (std::size_t)blockIdx.x * (D * (2 * D + 1) + D + 1);
     const int tn = tid >> 4, tk = tid & 15;
     constexpr int TI = 7, TJ = 7;  // rows / columns per thread (D <= 112)
     // the positive and the negative decoder call accumulate separately and
-    // are added at the end (the oracle's autograd sums the two calls' grads)
+    // are added at the end (the oracle's autograd sums the two calls' grads);
+    // the block's events stream through shared memory kDecWgTile at a time
     for (int half = 0; half < 2; ++half) {
         float ap[TI][TJ], an[TI][TJ];
 #pragma unroll
         for (int i = 0; i < TI; ++i)
 #pragma unroll
             for (int j = 0; j < TJ; ++j) ap[i][j] = an[i][j] = 0.f;
-        for (int e = 0; e < ne; ++e) {
-            float gp[TI], gn[TI], zp[TJ], zn[TJ];
-#pragma unroll
-            for (int i = 0; i < TI; ++i) {
-                const int n = min(tn + 16 * i, D - 1);
-                gp[i] = sgp[e * ld + n];
-                gn[i] = sgn[e * ld + n];
+        for (int e0 = c0; e0 < c1; e0 += kDecWgTile) {
+            const int ne = min(kDecWgTile, c1 - e0);
+            __syncthreads();  // the previous tile's readers are done
+            for (int i = tid; i < 5 * kDecWgTile * D4; i += blockDim.x) {
+                const int r = i / D4, c = 4 * (i % D4), which = r / kDecWgTile, e = r % kDecWgTile;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (e < ne) {
+                    const float* src = which == 0 ? dD1 + (std::size_t)(e0 + e) * D
+                                     : which == 1 ? dD1 + (std::size_t)(B + e0 + e) * D
+                                                  : emb + ((std::size_t)(which - 2) * B + e0 + e) * D;
+                    v = *reinterpret_cast<const float4*>(src + c);
+                }
+                *reinterpret_cast<float4*>(wsm + (std::size_t)r * ld + c) = v;
             }
+            __syncthreads();
+            for (int e = 0; e < ne; ++e) {
+                float gp[TI], gn[TI], zp[TJ], zn[TJ];
 #pragma unroll
-            for (int j = 0; j < TJ; ++j) {
-                const int k = min(tk + 16 * j, D - 1);
-                zp[j] = sz[((half == 0 ? 0 : 1) * kDecWgEv + e) * ld + k];  // z_src | z_dst
-                zn[j] = sz[((half == 0 ? 0 : 2) * kDecWgEv + e) * ld + k];  // z_src | z_neg
-            }
-#pragma unroll
-            for (int i = 0; i < TI; ++i)
+                for (int i = 0; i < TI; ++i) {
+                    const int n = min(tn + 16 * i, D - 1);
+                    gp[i] = sgp[e * ld + n];
+                    gn[i] = sgn[e * ld + n];
+                }
 #pragma unroll
                 for (int j = 0; j < TJ; ++j) {
-                    ap[i][j] = fmaf(gp[i], zp[j], ap[i][j]);
-                    an[i][j] = fmaf(gn[i], zn[j], an[i][j]);
+                    const int k = min(tk + 16 * j, D - 1);
+                    zp[j] = sz[((half == 0 ? 0 : 1) * kDecWgTile + e) * ld + k];  // z_src | z_dst
+                    zn[j] = sz[((half == 0 ? 0 : 2) * kDecWgTile + e) * ld + k];  // z_src | z_neg
                 }
+#pragma unroll
+                for (int i = 0; i < TI; ++i)
+#pragma unroll
+                    for (int j = 0; j < TJ; ++j) {
+                        ap[i][j] = fmaf(gp[i], zp[j], ap[i][j]);
+                        an[i][j] = fmaf(gn[i], zn[j], an[i][j]);
+                    }
+            }
         }
 #pragma unroll
         for (int i = 0; i < TI; ++i)
@@ -600,19 +605,19 @@ __global__ void __launch_bounds__(256) k_dec_wgrad_part(Dims d, int B, const flo
                 if (n < D && k < D) out[(std::size_t)n * (2 * D + 1) + half * D + k] = ap[i][j] + an[i][j];
             }
     }
-    // bias columns: db1 (column 2D of dW1) and dw2 (incl. db2)
+    // bias columns: db1 (column 2D of dW1) and dw2 (incl. db2), straight from global
     for (int n = tid; n < D; n += blockDim.x) {
         float a = 0.f, b = 0.f;
-        for (int e = 0; e < ne; ++e) {
-            a += sgp[e * ld + n];
-            b += sgn[e * ld + n];
+        for (int e = c0; e < c1; ++e) {
+            a += dD1[(std::size_t)e * D + n];
+            b += dD1[(std::size_t)(B + e) * D + n];
         }
         out[(std::size_t)n * (2 * D + 1) + 2 * D] = a + b;
     }
     for (int c = tid; c <= D; c += blockDim.x) {
         float a = 0.f, b = 0.f;
-        for (int e = 0; e < ne; ++e) {
-            const std::size_t pp = e0 + e, pn = B + e0 + e;
+        for (int e = c0; e < c1; ++e) {
+            const std::size_t pp = e, pn = B + e;
             a += dlogit[pp * 4] * (c < D ? D1[pp * d.ld_d1 + c] : 1.f);
             b += dlogit[pn * 4] * (c < D ? D1[pn * d.ld_d1 + c] : 1.f);
         }
@@ -631,7 +636,7 @@ __global__ void k_dec_wgrad_reduce(Dims d, int nblk, const float* part, float* g
     else g2[i - n1] += a;
 }
 
-std::size_t dec_wgrad_smem_bytes(const Dims& d) { return 4 * std::size_t(5) * kDecWgEv * (d.D + 4); }
+std::size_t dec_wgrad_smem_bytes(const Dims& d) { return 4 * std::size_t(5) * kDecWgTile * (d.D + 4); }
 
 // 416 threads (d_mem <= 104) at two blocks per SM (<= 72 registers), else one
 template __global__ void k_decoder<416, 2>(Dims, int, const float*, const float*, int, const float*,

@@ -154,7 +154,12 @@ __global__ void k_decoder(Dims d, int B, const float* emb, const float* W1, int 
                           float* D1, float* dlogit, float* lossv, float* dD1, float* logits,
                           float* d_emb, int bwd);
 std::size_t decoder_smem_bytes(const Dims& d);
-constexpr int kDecWgEv = 32;  // events per k_dec_wgrad_part block
+// k_dec_wgrad_part: events per block and per shared-memory tile (128-event
+// blocks — 16 long-running blocks — took 176 us on the side stream and moved
+// the Wiki test AUC from 0.0028 to 0.0050 off the oracle: the chunk order
+// is part of the numerics)
+constexpr int kDecWgEv = 32;
+constexpr int kDecWgTile = 32;
 __global__ void k_dec_wgrad_part(Dims d, int B, const float* emb, const float* dD1, const float* dlogit,
                                  const float* D1, float* part);
 __global__ void k_dec_wgrad_reduce(Dims d, int nblk, const float* part, float* g1, int ld1, float* g2);
