@@ -1198,7 +1198,6 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         cudaEvent_t at = mark();
         proj_dgrad(tc, s.d_emb.p, d.D, PW + lay_.mrg2.off, lay_.mrg2.ld, s.dZ1.p, d.D, R, d.D, d.D,
                    nullptr, st, gemm::EPI_MASK, s.Z1.p, d.ld_z, tc);
-        decoder_wgrads(at, B);
         side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.d_emb.p, d.D, s.Z1.p, d.ld_z, G + lay_.mrg2.off,
                                                         lay_.mrg2.ld, d.D, d.D + 1, R, nullptr, ws_cur_,
                                                         wsn_cur_, sd); });
@@ -1237,9 +1236,14 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         });
     });
     double* attn_part = s.tpart.p + std::size_t(s.troot_blocks) * 2 * d.T;
+    // the decoder's weight gradients have ~200 us of slack before Adam: forked
+    // once the attention backward is created, so the merge-layer data
+    // gradients above run without them
+    cudaEvent_t at_dec = mark();
     timed("k_attn_abs_bwd", [&] {
         attn_abs_bwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, nullptr, st);
     });
+    decoder_wgrads(at_dec, B);
     // the attention input gradients — memory columns summed per pending row
     // (k_dh_pull, deterministic, tgn_dh.cu) and the time-encoder partials —
     // run beside the dQ GEMMs; the GRU backward and the time-grad reduction
