@@ -555,6 +555,21 @@ def main():
     step_roof = {"bytes_per_edge": bpe, "achieved_gbs_per_gpu": value / world * bpe / 1e9,
                  "frac_of_hbm": value / world * bpe / 1e9 / hbm_peak,
                  "roofline_edges_per_s_per_gpu": hbm_peak * 1e9 / bpe}
+    # tensor-core roofline of one projection GEMM: the attention's per-head
+    # key projection Qp_h = Q_h [W_K,h | b_K,h] (one batched tcgen05 launch,
+    # 2 R x dh x (DK+1) x H FLOP) over its CUDA-event time; TF32 peak taken as
+    # half the measured dense BF16 rate (tcgen05 kind::tf32 issues at half the
+    # kind::f16 rate)
+    gemm = None
+    if args.gemm_mode == 1 and kern.get("gemm_qp"):
+        flop = 2.0 * R_ * (D + T) / H * (DK + 1) * H
+        bf16 = peaks.get("bf16_tflops") or 1590.0
+        ach = flop / (kern["gemm_qp"] / 1e3) / 1e12
+        gemm = {"bound": "tensor", "kernel": "umma_gemm_kernel (Qp: attention key projection, TF32)",
+                "achieved": ach, "peak": bf16 / 2, "unit": "TFLOP/s", "frac": ach / (bf16 / 2),
+                "flop_per_launch": flop, "launch_ms": kern["gemm_qp"],
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2" if peaks else "fallback 1590 / 2",
+                "tensor_pipe_pct_ncu": "profiles/r2/kernel_table_final.txt (sm__pipe_tensor_cycles_active)"}
 
     # the same workload in FP32 FFMA (gemm_mode 0): the evidence behind the
     # TF32 tensor-core choice for the GRU / attention projections
@@ -611,6 +626,7 @@ def main():
             "data": "synthetic (gen_powerlaw topology seed 1, hashed bf16-exact edge features seed 2, "
                     "random-init TGN seed 3)",
             "config": cfg_desc, "e2e": e2e, "roofline": roof, "step_roofline": step_roof,
+            "gemm_roofline": gemm,
             "cpu_baseline": cpu, "fp32_ffma": fp32, "gpu_launches": launches, "clocks": clk.summary(),
             "effective_edges_per_s": wl["train_edges"] / (tr.epoch_steps() * ms_per_step / 1e3),
             "device_memory_per_gpu": mem_gb,

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 
@@ -22,6 +24,27 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // Fails loudly (status 3) when there is no usable sm_100 device: the product
 // path has no CPU fallback.
 void require_device(int device);
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the current device
+// (the attribute is per device: a process driving several GPUs sets it on
+// each); optionally prefer the maximum shared-memory carveout.
+template <class K>
+void ensure_smem(K kern, std::size_t bytes, bool max_carveout = false) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, std::size_t> done;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    std::size_t& have = done[{reinterpret_cast<const void*>(kern), dev}];
+    if (bytes <= have) return;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)),
+               "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    if (max_carveout)
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        int(cudaSharedmemCarveoutMaxShared)),
+                   "cudaFuncSetAttribute(PreferredSharedMemoryCarveout)");
+    have = bytes;
+}
 
 template <class T>
 struct DevBuf {

@@ -249,14 +249,8 @@ void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, floa
 // Absorbed-projection attention kernels (tgn_attn.cu), instantiated for lane
 // slots NM, NT in {1, 2} (NM + NT <= 3), NF in {1, 2, 3} and H <= 2 or 4.
 template <class Kern, class... Args>
-void attn_launch(Kern k, std::size_t& set, unsigned grid, std::size_t smem, cudaStream_t st,
-                 Args&&... args) {
-    if (smem > set) {  // opt in to > 48 KB shared memory (once per kernel and size)
-        SPD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        SPD_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                      int(cudaSharedmemCarveoutMaxShared)));
-        set = smem;
-    }
+void attn_launch(Kern k, unsigned grid, std::size_t smem, cudaStream_t st, Args&&... args) {
+    ensure_smem(k, smem, true);  // > 48 KB shared memory
     launch(k, grid, 32 * tgnk::attn_roots_per_block(), smem, st, std::forward<Args>(args)...);
 }
 
@@ -264,13 +258,12 @@ template <int NM, int NT, int NF, int HM>
 void attn_pick(bool bwd, unsigned grid, cudaStream_t st, const tgnk::WorkerDev& wd,
                const tgnk::Dims& d, int R, const float* tw, const float* tb, const Scratch& s,
                double* part) {
-    static std::size_t set_fwd = 0, set_bwd = 0;  // per kernel instantiation
     if (!bwd)
-        attn_launch(&tgnk::k_attn_abs_fwd<NM, NT, NF, HM>, set_fwd, grid, tgnk::attn_smem_bytes(d, false), st,
+        attn_launch(&tgnk::k_attn_abs_fwd<NM, NT, NF, HM>, grid, tgnk::attn_smem_bytes(d, false), st,
                     wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
                     s.Qp.p, s.alpha.p, s.xbar.p);
     else
-        attn_launch(&tgnk::k_attn_abs_bwd<NM, NT, NF, HM>, set_bwd, grid, tgnk::attn_smem_bytes(d, true), st,
+        attn_launch(&tgnk::k_attn_abs_bwd<NM, NT, NF, HM>, grid, tgnk::attn_smem_bytes(d, true), st,
                     wd, d, R, tw, tb, s.nbr_node.p, s.nbr_ev.p, s.nbr_dt.p, s.cnt.p, s.mem_new.p,
                     s.Qp.p, s.alpha.p, s.dxbar.p, s.dQp.p, s.dsc.p);
 }
@@ -319,11 +312,9 @@ void attn_time_grad(const tgnk::Dims& d, int R, const float* tw, const float* tb
 // memory-row gradients of the GRU outputs, deterministic (tgn_dh.cu)
 void dh_index(const tgnk::WorkerDev& wd, const Scratch& s, cudaStream_t st) {
     const std::size_t sm = std::size_t(s.dh.U_cap) * sizeof(int);
-    static std::size_t set = 0;
-    if (sm > 48 * 1024 && sm > set) {
-        SPD_CUDA(cudaFuncSetAttribute(tgnk::k_dh_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        SPD_CUDA(cudaFuncSetAttribute(tgnk::k_dh_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-        set = sm;
+    if (sm > 48 * 1024) {
+        ensure_smem(tgnk::k_dh_hist, sm);
+        ensure_smem(tgnk::k_dh_scatter, sm);
     }
     const unsigned nb = unsigned(s.dh.nb_occ + s.dh.nb_root);
     launch(tgnk::k_dh_hist, nb, tgnk::kDhBlock, sm, st, wd, s.dh);
@@ -1055,13 +1046,8 @@ void TGNTrainer::decoder_wgrads(cudaEvent_t at, int B) {
     float* G = grads_.p;
     if (d.D <= 112) {  // decoder weight gradients: chunk partials + fixed-order sum (FFMA)
         side_from(at, [&](cudaStream_t sd) {
-            static std::size_t wg_smem_set = 0;
             const std::size_t sm = tgnk::dec_wgrad_smem_bytes(d);
-            if (sm > wg_smem_set) {
-                SPD_CUDA(cudaFuncSetAttribute(tgnk::k_dec_wgrad_part,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-                wg_smem_set = sm;
-            }
+            ensure_smem(tgnk::k_dec_wgrad_part, sm);
             const int nblk = (B + tgnk::kDecWgEv - 1) / tgnk::kDecWgEv;
             launch(tgnk::k_dec_wgrad_part, unsigned(nblk), 256, sm, sd, d, B,
                    static_cast<const float*>(s.emb.p), static_cast<const float*>(s.dD1.p),
@@ -1092,15 +1078,10 @@ void TGNTrainer::decode(int B, bool train) {
     cudaStream_t st = stream_;
     // (its TMA row copies need 16-B aligned weight rows)
     if (lay_.dec1.off % 4 || lay_.dec1.ld % 4) internal_error("InvalidParams", "decoder rows unaligned");
-    static std::size_t dec_smem_set = 0;
     const std::size_t dsm = tgnk::decoder_smem_bytes(d);
     const bool narrow = 4 * d.D <= 416;
     auto kdec = narrow ? tgnk::k_decoder<416, 2> : tgnk::k_decoder<768, 1>;
-    if (dsm > dec_smem_set) {
-        SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder<416, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
-        SPD_CUDA(cudaFuncSetAttribute(tgnk::k_decoder<768, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)));
-        dec_smem_set = dsm;
-    }
+    ensure_smem(kdec, dsm);
     launch(kdec, unsigned((B + tgnk::kDecEv - 1) / tgnk::kDecEv),
            unsigned((4 * d.D + 31) / 32 * 32), dsm, st, d, B, static_cast<const float*>(s.emb.p),
            static_cast<const float*>(P + lay_.dec1.off), lay_.dec1.ld,

@@ -101,10 +101,7 @@ template <bool A_MN, bool B_MN, int BN, int NSUB = 1, int CL = 1, bool DEEP = fa
 void run(const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
     using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL, DEEP>;
     auto kern = umma_gemm_kernel<A_MN, B_MN, BN, NSUB, CL, DEEP>;
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
-    });
+    ensure_smem(kern, C_::SMEM);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(THREADS);
@@ -307,10 +304,7 @@ void gru_fused(const float* x, int ldx, int K1, const float* h, int ldh, int K2,
     a.M = M; a.M_dev = M_dev; a.K1 = K1; a.K2 = K2; a.D = D;
     a.mem = mem; a.nodes = nodes; a.mem_new = mem_new; a.save = save;
     auto kern = umma_gru_kernel<UB>;
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        SPD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
-    });
+    ensure_smem(kern, C_::SMEM);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned((D + UB - 1) / UB), unsigned((M + BM - 1) / BM), 1);
     cfg.blockDim = dim3(THREADS);
