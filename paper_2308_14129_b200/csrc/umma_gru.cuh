@@ -24,8 +24,7 @@
 namespace spd {
 namespace umma {
 
-constexpr int kGruUB = 32;      // memory units per CTA
-constexpr int kGruStages = 7;  // 196 KB ring: one CTA per SM (<= 128 CTAs at the step's sizes), all in flight
+constexpr int kGruUB = 32;  // memory units per CTA (SPD_GRU_UB=16: twice the CTAs, two per SM)
 
 struct GruArgs {
     int M;             // row capacity (pending slots); live rows from *M_dev
@@ -47,7 +46,11 @@ struct GruCfg {
     static constexpr int A_BYTES = BM * BK * 4;
     static constexpr int B_BYTES = N * BK * 4;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int SMEM = kGruStages * STAGE_BYTES + 1024 + 256;
+    // UB 32: a 7-stage (196 KB) ring, one CTA per SM (<= 128 CTAs at the
+    // step's sizes, all in flight); UB 16: 4 stages, two CTAs per SM
+    static constexpr int CTAS = UB >= 32 ? 1 : 2;
+    static constexpr int STAGES = UB >= 32 ? 7 : 4;
+    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
     static constexpr int ACC_H = N <= 128 ? 128 : 256;  // TMEM column of the hidden-side accumulator
     static constexpr int TMEM_COLS = 2 * ACC_H;
     static_assert(N % 16 == 0 && N <= 256, "MMA N");
@@ -64,10 +67,10 @@ __device__ __forceinline__ void tmem_ld8(std::uint32_t taddr, float (&v)[8]) {
 }
 
 template <int UB>
-__global__ void __launch_bounds__(THREADS, 1) umma_gru_kernel(const __grid_constant__ GruMaps maps, GruArgs args) {
+__global__ void __launch_bounds__(THREADS, GruCfg<UB>::CTAS) umma_gru_kernel(const __grid_constant__ GruMaps maps, GruArgs args) {
     pdl_entry();
     using C_ = GruCfg<UB>;
-    constexpr int NST = kGruStages;
+    constexpr int NST = C_::STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + NST * C_::STAGE_BYTES);

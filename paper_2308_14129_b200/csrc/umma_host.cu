@@ -288,12 +288,12 @@ void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw
     if (split > 1) reduce(ws, split, N_out, K_in, ldws, dW, ldw, bt, s);
 }
 
-void gru_fused(const float* x, int ldx, int K1, const float* h, int ldh, int K2, const float* Wih,
+template <int UB>
+void gru_fused_t(const float* x, int ldx, int K1, const float* h, int ldh, int K2, const float* Wih,
                int ldwih, const float* Whh, int ldwhh, int D, int M, const int* M_dev,
                const float* mem, const std::uint32_t* nodes, float* mem_new, float* save,
                cudaStream_t s) {
     if (!M || !D) return;
-    constexpr int UB = kGruUB;
     using C_ = GruCfg<UB>;
     GruMaps maps{};
     maps.x = make_map(x, K1, M, ldx, BM);
@@ -322,6 +322,21 @@ void gru_fused(const float* x, int ldx, int K1, const float* h, int ldh, int K2,
     SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
+}
+
+// UB (memory units per CTA) from SPD_GRU_UB (16 or 32; default kGruUB)
+void gru_fused(const float* x, int ldx, int K1, const float* h, int ldh, int K2, const float* Wih,
+               int ldwih, const float* Whh, int ldwhh, int D, int M, const int* M_dev,
+               const float* mem, const std::uint32_t* nodes, float* mem_new, float* save,
+               cudaStream_t s) {
+    static const int ub = [] {
+        const char* e = std::getenv("SPD_GRU_UB");
+        return e && std::atoi(e) == 16 ? 16 : kGruUB;
+    }();
+    if (ub == 16)
+        gru_fused_t<16>(x, ldx, K1, h, ldh, K2, Wih, ldwih, Whh, ldwhh, D, M, M_dev, mem, nodes, mem_new, save, s);
+    else
+        gru_fused_t<kGruUB>(x, ldx, K1, h, ldh, K2, Wih, ldwih, Whh, ldwhh, D, M, M_dev, mem, nodes, mem_new, save, s);
 }
 
 }  // namespace umma
