@@ -167,12 +167,13 @@ int max_bn() {
 }
 
 // widest tile with the least padding of N (ties -> wider)
-int pick_bn(int N) {
+int pick_bn(int N, int cap = 0) {
     const int cands[] = {256, 224, 128, 64};
     int best = 64;
     long best_pad = 1L << 40;
+    if (cap <= 0) cap = max_bn();
     for (int c : cands) {
-        if (c > max_bn() && c != 64) continue;
+        if (c > cap && c != 64) continue;
         const long tiles = (N + c - 1) / c;
         const long pad = tiles * c - N + tiles * 8;  // small per-tile overhead term
         if (pad < best_pad) {
@@ -181,6 +182,18 @@ int pick_bn(int N) {
         }
     }
     return best;
+}
+
+// GEMMs whose 64-wide tiles would take more than one wave at 3 CTAs per SM
+// (the per-head Qp / dxbar launches: 658 CTAs) use tiles up to 224 wide
+// instead (SPD_UMMA_WIDE_BIG=0 disables)
+int bn_for(int N, long mt, int nb) {
+    static const bool wide = [] {
+        const char* e = std::getenv("SPD_UMMA_WIDE_BIG");
+        return !(e && *e == '0');
+    }();
+    const long ctas64 = long((N + 63) / 64) * mt * nb;
+    return wide && ctas64 > 3L * 148 ? pick_bn(N, 224) : pick_bn(N);
 }
 
 void check_batch(const Batch& b) {
@@ -210,7 +223,7 @@ void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, in
         run<false, false, 208, 2, 4>(maps, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
         return;
     }
-    int bn = pick_bn(N);
+    int bn = bn_for(N, mt, bt.n);
     const bool deep = deep_tiles() && long((N + 127) / 128) * mt * bt.n <= 148;
     if (deep) bn = 128;
     for (int z = 0; z < bt.n; ++z) {
@@ -237,7 +250,7 @@ void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, 
         run<false, true, 224, 1, 4>(maps, a, dim3(1, (mt + 3) / 4 * 4, 1), s);
         return;
     }
-    int bn = pick_bn(N);  // multiple of 32: whole MN-major column blocks
+    int bn = bn_for(N, mt, bt.n);  // multiple of 32: whole MN-major column blocks
     const bool deep = deep_tiles() && long((N + 127) / 128) * mt * bt.n <= 148;
     if (deep) bn = 128;
     for (int z = 0; z < bt.n; ++z) {
