@@ -740,23 +740,47 @@ __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb
     gb[c] += (float)acc[T + c];
 }
 
+// Adam over the flat buffer, 4 parameters per thread (128-bit loads and
+// stores; the flat layout is a multiple of 4 floats, a scalar tail otherwise)
+__device__ __forceinline__ float adam_one(float& p, float g, float& m, float& v, float scale, float lr,
+                                          float b1, float one_m_b1, float b2, float one_m_b2, float bc1,
+                                          float bc2, float eps) {
+    const float gi = g / scale;
+    const float mi = b1 * m + one_m_b1 * gi;
+    const float vi = b2 * v + one_m_b2 * gi * gi;
+    m = mi;
+    v = vi;
+    const float mh = mi / bc1;
+    const float vh = vi / bc2;
+    p = p - lr * mh / (sqrtf(vh) + eps);
+    return p;
+}
 __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
                        float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
                        float eps, float* p_tc) {
     pdl_entry();
-    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const std::size_t i4 = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const std::size_t i = 4 * i4;
     if (i >= n) return;
     const float bc1 = bc[0], bc2 = bc[1];  // bias corrections of this step (host-written)
-    const float gi = g[i] / scale;
-    const float mi = b1 * m[i] + one_m_b1 * gi;
-    const float vi = b2 * v[i] + one_m_b2 * gi * gi;
-    m[i] = mi;
-    v[i] = vi;
-    const float mh = mi / bc1;
-    const float vh = vi / bc2;
-    const float pn = p[i] - lr * mh / (sqrtf(vh) + eps);
-    p[i] = pn;
-    if (p_tc) p_tc[i] = tf32r(pn);
+    if (i + 4 <= n) {
+        float4 pp = *reinterpret_cast<float4*>(p + i), mm = *reinterpret_cast<float4*>(m + i);
+        float4 vv = *reinterpret_cast<float4*>(v + i);
+        const float4 gg = *reinterpret_cast<const float4*>(g + i);
+        adam_one(pp.x, gg.x, mm.x, vv.x, scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
+        adam_one(pp.y, gg.y, mm.y, vv.y, scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
+        adam_one(pp.z, gg.z, mm.z, vv.z, scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
+        adam_one(pp.w, gg.w, mm.w, vv.w, scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
+        *reinterpret_cast<float4*>(p + i) = pp;
+        *reinterpret_cast<float4*>(m + i) = mm;
+        *reinterpret_cast<float4*>(v + i) = vv;
+        if (p_tc) *reinterpret_cast<float4*>(p_tc + i) = make_float4(tf32r(pp.x), tf32r(pp.y), tf32r(pp.z), tf32r(pp.w));
+        return;
+    }
+    for (std::size_t k = i; k < n; ++k) {
+        adam_one(p[k], g[k], m[k], v[k], scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
+        if (p_tc) p_tc[k] = tf32r(p[k]);
+    }
 }
 
 __global__ void k_round_tf32(const float* src, float* dst, std::size_t n) {

@@ -1531,7 +1531,7 @@ void TGNTrainer::adam(cudaStream_t st) {
                          cfg_.gemm_mode == 1 ? params_tc_.p : nullptr, st);
         return;
     }
-    launch(tgnk::k_adam, blocks_for(lay_.total), 256, 0, st,
+    launch(tgnk::k_adam, blocks_for((lay_.total + 3) / 4), 256, 0, st,
         params_.p, grads_.p, adam_m_.p, adam_v_.p, lay_.total, float(total_workers_), cfg_.lr,
         cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2),
         adam_bc_, cfg_.adam_eps,

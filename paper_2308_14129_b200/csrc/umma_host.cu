@@ -184,13 +184,13 @@ int pick_bn(int N, int cap = 0) {
     return best;
 }
 
-// GEMMs whose 64-wide tiles would take more than one wave at 3 CTAs per SM
-// (the per-head Qp / dxbar launches: 658 CTAs) use tiles up to 224 wide
-// instead (SPD_UMMA_WIDE_BIG=0 disables)
+// SPD_UMMA_WIDE_BIG=1: GEMMs whose 64-wide tiles take more than one wave at
+// 3 CTAs per SM (the per-head Qp / dxbar launches: 658 CTAs) use tiles up to
+// 224 wide (experiment knob: measured 0.363 vs 0.358 ms per GDELT step)
 int bn_for(int N, long mt, int nb) {
     static const bool wide = [] {
         const char* e = std::getenv("SPD_UMMA_WIDE_BIG");
-        return !(e && *e == '0');
+        return e && *e == '1';
     }();
     const long ctas64 = long((N + 63) / 64) * mt * nb;
     return wide && ctas64 > 3L * 148 ? pick_bn(N, 224) : pick_bn(N);
