@@ -51,11 +51,12 @@ def ap_auc(pos, neg):
     return average_precision_score(y, s), roc_auc_score(y, s)
 
 
+@pytest.mark.parametrize("backbone", [0, 1])
 @pytest.mark.parametrize("gemm_mode", [0, 1])
-def test_eval_scores_match_oracle(gemm_mode):
+def test_eval_scores_match_oracle(gemm_mode, backbone):
     pa, subs, ev, r = build(400, 6000, 2)
     cfg = sp.TGNConfig(d_mem=32, d_time=16, d_edge=12, n_neighbors=5, n_heads=2, batch_size=64,
-                       lr=1e-3, gemm_mode=gemm_mode)
+                       lr=1e-3, gemm_mode=gemm_mode, backbone=backbone)
     tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
     o = oracle_for(cfg, subs, pa.shared)
     tr.run_epoch(0)

@@ -1,11 +1,11 @@
-"""World-2 TGN training through the peer-memory transport (spd_tgn_peer_*),
-two processes on cuda:0 (ranks sharing one GPU map each other's HBM through
+"""World-2 and world-3 TGN training through the peer-memory transport
+(spd_tgn_peer_*), one process per rank on cuda:0 (ranks sharing one GPU map each other's HBM through
 CUDA IPC exactly as ranks on different GPUs do over NVLink): the per-step
 gradient all-reduce fused into Adam and the epoch-end shared-hub sync must
 reproduce one process training both partitions as local workers
 (Alg. 2; run_epoch / sync_shared, pac_sim.cpp:162-264).
 
-Bars: parameters of the two ranks bit-identical to each other (same rank-order
+Bars: parameters of all ranks bit-identical to each other (same rank-order
 sum on every rank); against the single-process run the FP32 trajectory bar
 (2e-3; the only difference is where the per-worker gradient sum is rounded);
 shared-hub rows identical across the ranks after end_epoch."""
@@ -69,35 +69,37 @@ def _rank(rank, world, port, sync_average, gemm_mode, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("sync_average", [1, 0])
-def test_two_ranks_peer_transport_match_one_process(sync_average):
+@pytest.mark.parametrize("world,sync_average", [(2, 1), (2, 0), (3, 1)])
+def test_ranks_peer_transport_match_one_process(world, sync_average):
     gemm_mode = 0
-    _, _, pa, subs = partitioned(nodes=300, edges=4000, parts=2)
+    _, _, pa, subs = partitioned(nodes=300, edges=4000, parts=world)
     assert len(pa.shared) > 0
     one = sp.TGNTrainer(_cfg(sync_average, gemm_mode), subs, shared=pa.shared, device=0)
     ref_losses = _train(one, EPOCHS)
     ref_params = one.params()
-    ref_mem = [one.memory(w) for w in range(2)]
-    ref_nodes = [one.local_nodes(w) for w in range(2)]
+    ref_mem = [one.memory(w) for w in range(world)]
+    ref_nodes = [one.local_nodes(w) for w in range(world)]
     one.close()
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, sync_average, gemm_mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, sync_average, gemm_mode, q))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
-    for _ in range(2):
+    for _ in range(world):
         r = q.get(timeout=600)
         res[r[0]] = r
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    p0, p1 = res[0][1], res[1][1]
-    assert np.array_equal(p0, p1), "replicated parameters diverged across ranks"
+    p0 = res[0][1]
+    for r in range(1, world):
+        assert np.array_equal(p0, res[r][1]), "replicated parameters diverged across ranks"
     assert rel_err(p0, ref_params) < 2e-3
-    for w in range(2):
+    for w in range(world):
         _, _, losses, nodes, mem, lu = res[w]
         np.testing.assert_array_equal(nodes, ref_nodes[w])
         ref_loss_w = [float(l[w]) for l in ref_losses]
@@ -105,10 +107,12 @@ def test_two_ranks_peer_transport_match_one_process(sync_average):
         assert rel_err(mem, ref_mem[w][0]) < 2e-3
         np.testing.assert_array_equal(lu, ref_mem[w][1])
     # shared-hub rows agree across the ranks after the epoch-end sync
-    n0, n1 = res[0][3], res[1][3]
-    common = np.intersect1d(np.intersect1d(n0, n1), np.asarray(pa.shared, np.uint32))
-    assert len(common) > 0
-    i0 = np.searchsorted(n0, common)
-    i1 = np.searchsorted(n1, common)
-    np.testing.assert_array_equal(res[0][4][i0], res[1][4][i1])
-    np.testing.assert_array_equal(res[0][5][i0], res[1][5][i1])
+    n0 = res[0][3]
+    for r in range(1, world):
+        n1 = res[r][3]
+        common = np.intersect1d(np.intersect1d(n0, n1), np.asarray(pa.shared, np.uint32))
+        assert len(common) > 0
+        i0 = np.searchsorted(n0, common)
+        i1 = np.searchsorted(n1, common)
+        np.testing.assert_array_equal(res[0][4][i0], res[r][4][i1])
+        np.testing.assert_array_equal(res[0][5][i0], res[r][5][i1])
