@@ -317,6 +317,9 @@ def main():
                     help="SEP partitions (default: one per GPU); more than --gpus trains several "
                          "partitions per GPU as local workers of one trainer")
     ap.add_argument("--hub-k", type=float, default=0.05, help="SEP shared-hub fraction k")
+    ap.add_argument("--concurrent", action="store_true",
+                    help="with --parts > --gpus: a GPU's partitions train concurrently (one "
+                         "stream set and parameter replica each, in-process peer all-reduce)")
     ap.add_argument("--backbone", default="tgn", choices=["tgn", "jodie"],
                     help="memory-based TIG model: TGN (GRU + temporal attention) or JODIE "
                          "(RNN + time projection), PAPER.md:373")
@@ -377,7 +380,8 @@ def main():
                             + (f" k_hub={args.hub_k}" if args.hub_k != 0.05 else ""),
                 "nodes": N, "edges": E, "d_edge": F, "batch": B, "partitions": P,
                 "partitions_per_gpu": P // world, "hub_k": args.hub_k,
-                "parallelism": f"sep{P}" + (f" ({P // world} per GPU)" if P > world else ""),
+                "parallelism": f"sep{P}" + (f" ({P // world} per GPU{', concurrent' if args.concurrent else ''})"
+                                            if P > world else ""),
                 "transport": (args.transport if world > 1 else None),
                 "timed_from": "mid-epoch (spd_tgn_seek to epoch_steps/2)",
                 "l2": "inputs larger than L2 (50-100 GB feature "
@@ -412,7 +416,8 @@ def main():
     subs_mine = [wl["subs"][w] for w in mine]
     sub_mine = subs_mine[0]
     cfg = sp.TGNConfig(d_mem=D, d_time=T, d_edge=F, n_neighbors=K, n_heads=H, batch_size=B, lr=1e-4,
-                       gemm_mode=args.gemm_mode, backbone=0 if args.backbone == "tgn" else 1)
+                       gemm_mode=args.gemm_mode, backbone=0 if args.backbone == "tgn" else 1,
+                       concurrent=1 if args.concurrent else 0)
     nccl_id = None
     if world > 1 and args.transport == "nccl":
         import torch

@@ -279,6 +279,11 @@ typedef struct spd_tgn_config {
     int32_t gemm_mode;   /* 0 = FP32 FFMA, 1 = tcgen05 TF32 for the GRU and attention projections (tolerance-gated) */
     int32_t backbone;    /* 0 = TGN (GRU memory, temporal attention); 1 = JODIE (RNN memory,
                           * time-projection embedding: PAPER.md:373's other backbones) */
+    int32_t concurrent;  /* 1: a process's local workers (several SEP partitions on one GPU,
+                          * world 1) train concurrently, each on its own streams with its own
+                          * scratch and parameter replica; gradients meet in the fused
+                          * all-reduce + Adam of the peer transport (in-process). 0: one after
+                          * another in one scratch (default). */
 } spd_tgn_config;
 
 typedef struct spd_tgn_trainer spd_tgn_trainer;

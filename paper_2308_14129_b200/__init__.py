@@ -732,12 +732,13 @@ class TGNConfig:
     sync_average: int = 1
     gemm_mode: int = 0
     backbone: int = 0  # 0 TGN, 1 JODIE
+    concurrent: int = 0  # 1: local workers train concurrently (world 1)
 
     def c(self) -> TGNConfigC:
         return TGNConfigC(self.d_mem, self.d_time, self.d_edge, self.n_neighbors, self.n_heads,
                           self.batch_size, self.lr, self.beta1, self.beta2, self.adam_eps,
                           self.seed_init, self.seed_feat, self.seed_neg, self.sync_average,
-                          self.gemm_mode, self.backbone)
+                          self.gemm_mode, self.backbone, self.concurrent)
 
 
 def nccl_unique_id() -> bytes:

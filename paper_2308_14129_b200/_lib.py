@@ -48,7 +48,8 @@ class TGNConfigC(C.Structure):
     _fields_ = [("d_mem", i32), ("d_time", i32), ("d_edge", i32), ("n_neighbors", i32),
                 ("n_heads", i32), ("batch_size", u64), ("lr", f32), ("beta1", f32),
                 ("beta2", f32), ("adam_eps", f32), ("seed_init", u64), ("seed_feat", u64),
-                ("seed_neg", u64), ("sync_average", i32), ("gemm_mode", i32), ("backbone", i32)]
+                ("seed_neg", u64), ("sync_average", i32), ("gemm_mode", i32), ("backbone", i32),
+                ("concurrent", i32)]
 
 
 # name -> (restype, argtypes); spd_status is int32.

@@ -121,6 +121,20 @@ void PeerComm::export_blob(unsigned char* out) const {
     std::memcpy(out + 3 * 64 + 8, &sb, sizeof sb);
 }
 
+void PeerComm::connect_local(const std::vector<PeerComm*>& all) {
+    if (connected_) usage_error("peer transport already connected");
+    if (static_cast<int>(all.size()) != world_) internal_error("InvalidParams", "connect_local: one transport per rank");
+    for (int r = 0; r < world_; ++r) {
+        const PeerComm& o = *all[r];
+        if (o.rank_ != r || o.world_ != world_ || o.sbuf_bytes_ != sbuf_bytes_)
+            internal_error("InvalidParams", "connect_local: mismatched transports");
+        v_.grads[r] = o.v_.grads[r];
+        v_.flags_of[r] = o.flags_;
+        v_.sbuf[r] = o.sbuf_;
+    }
+    connected_ = true;
+}
+
 void PeerComm::connect(const unsigned char* blobs) {
     if (connected_) usage_error("peer transport already connected");
     DeviceGuard g(device_);

@@ -122,6 +122,7 @@ public:
     ~TGNTrainer();
 
     std::uint64_t epoch_steps() const { return epoch_steps_; }
+    bool concurrent() const { return !lanes_.empty(); }
     std::uint64_t batch_size() const { return cfg_.batch_size; }
     void begin_epoch(int epoch);
     void seek(std::uint64_t step);
@@ -130,7 +131,7 @@ public:
                          float* loss_pinned);
     void sync();  // shuffle-combine: next epoch's regrouped subgraphs
     void step(float* loss_out);
-    void end_epoch();
+    void end_epoch(bool wait = true);
     void run_epoch(int epoch, double* mean_loss);
     // Evaluation events (routed val then test edges, global ids, time-ordered)
     // appended after the worker's training events: the full-graph neighbour
@@ -154,7 +155,7 @@ public:
     std::size_t debug_scratch(const char* name, float* out, std::size_t cap);
     void last_step(int w, std::uint64_t* b, float* emb, std::uint32_t* negs, std::uint32_t* nbr,
                    float* loss);
-    const StepTimes& times() const { return times_; }
+    const StepTimes& times() const { return lanes_.empty() ? times_ : lanes_[0]->times_; }
     float run_steps(std::uint64_t n);
     // peer-memory transport (world > 1 without an NCCL id, peer_comm.hpp):
     // every rank exports its blob, the caller exchanges them, every rank connects
@@ -173,20 +174,46 @@ public:
     void peer_connect(const unsigned char* blobs);
     void step_host(const spd_edge* const* events, const std::uint16_t* const* feats,
                    float* loss_out);
-    std::uint64_t h2d_bytes() const { return h2d_bytes_; }
-    std::uint64_t d2h_bytes() const { return d2h_bytes_; }
-    std::uint64_t step_in_epoch() const { return step_in_epoch_; }
-    int epoch() const { return epoch_; }
+    std::uint64_t h2d_bytes() const {
+        std::uint64_t n = h2d_bytes_;
+        for (auto& l : lanes_) n += l->h2d_bytes_;
+        return n;
+    }
+    std::uint64_t d2h_bytes() const {
+        std::uint64_t n = d2h_bytes_;
+        for (auto& l : lanes_) n += l->d2h_bytes_;
+        return n;
+    }
+    std::uint64_t step_in_epoch() const { return lanes_.empty() ? step_in_epoch_ : lanes_[0]->step_in_epoch_; }
+    int epoch() const { return lanes_.empty() ? epoch_ : lanes_[0]->epoch_; }
     int feat_stride() const;
-    void set_debug(bool on) { debug_ = on; }
-    void set_profile(bool on) { profile_ = on; }
-    void set_graph(bool on) { use_graph_ = on; }
+    void set_debug(bool on) {
+        debug_ = on;
+        for (auto& l : lanes_) l->set_debug(on);
+    }
+    void set_profile(bool on) {
+        profile_ = on;
+        for (auto& l : lanes_) l->set_profile(on);
+    }
+    void set_graph(bool on) {
+        use_graph_ = on;
+        for (auto& l : lanes_) l->set_graph(on);
+    }
     void set_gemm_mode(int mode);
     int device() const { return device_; }
-    cudaStream_t stream() const { return stream_; }
+    cudaStream_t stream() const { return lanes_.empty() ? stream_ : lanes_[0]->stream_; }
+    float* loss_dev() const;  // device per-local-worker loss slots
 
 private:
     void build_workers(const SubGraphs& subs, const std::vector<int>& ids);
+    // concurrent local workers (tgn_lanes.cu): one child trainer per worker
+    std::vector<std::unique_ptr<TGNTrainer>> lanes_;
+    void build_lanes(const SubGraphs& subs, const std::vector<int>& workers, NodeId node_count);
+    TGNTrainer* lane_of(int gid);
+    void lanes_wait();
+    void lanes_losses(float* loss_out);
+    void lanes_step(float* loss_out);
+    float lanes_run_steps(std::uint64_t n);
     void init_worker_state(Worker& w);  // memory, clocks, pending sets, shared-row map
     std::unique_ptr<DevStream> dstream_;
     void worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx,
@@ -211,7 +238,7 @@ private:
                      const std::function<void()>& after_gather = {});
     void allreduce_grads(cudaStream_t st);
     void adam(cudaStream_t st);
-    void sync_shared();
+    void sync_shared(bool wait = true);
     void timed(const char* name, const std::function<void()>& f);
     // weight-gradient GEMMs run on a side stream forked from the main stream at
     // the point their inputs exist, and joined back once per worker step
@@ -259,6 +286,12 @@ private:
     cudaStream_t stream_ = nullptr;
     void* nccl_ = nullptr;  // ncclComm_t
     std::unique_ptr<PeerComm> peer_;  // peer-memory transport instead of NCCL
+    struct SyncBufs {  // epoch-end shared-hub sync scratch (persistent)
+        DevBuf<float> sum, mn, mx;
+        DevBuf<double> tmin, tmax;
+        DevBuf<int> owner;
+        std::vector<DevBuf<std::uint32_t>> rows;  // per local worker; cleared when workers change
+    } syncbuf_;
     bool surrogate_ = false;          // bridge backbone (set_surrogate)
     DevBuf<double> sur_w_, sur_om_;
     double sur_gamma_ = 0.0;

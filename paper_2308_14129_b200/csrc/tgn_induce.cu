@@ -137,6 +137,10 @@ struct Temp {
 void TGNTrainer::attach_stream(const spd_edge* e, std::uint64_t n, NodeId node_count,
                                const std::uint64_t* off, const NodeId* nodes, int n_small) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        for (auto& l : lanes_) l->attach_stream(e, n, node_count, off, nodes, n_small);
+        return;
+    }
     if (n_small < 1 || n_small > 64 * 64) data_error("InvalidParams", "need 1 <= small parts <= 4096");
     if (total_workers_ > 64) data_error("InvalidParams", "device re-induction supports <= 64 workers");
     if (n_small % total_workers_)
@@ -177,6 +181,12 @@ void TGNTrainer::attach_stream(const spd_edge* e, std::uint64_t n, NodeId node_c
 
 void TGNTrainer::shuffle_epoch(std::uint64_t seed, std::uint64_t* recovered) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        lanes_wait();
+        for (auto& l : lanes_) l->shuffle_epoch(seed, recovered);
+        epoch_steps_ = lanes_[0]->epoch_steps_;
+        return;
+    }
     if (!dstream_) usage_error("shuffle_epoch needs spd_tgn_attach_stream first");
     auto& S = *dstream_;
     const int G = total_workers_;
@@ -213,6 +223,7 @@ void TGNTrainer::shuffle_epoch(std::uint64_t seed, std::uint64_t* recovered) {
     std::vector<int> ids;
     for (const auto& w : workers_) ids.push_back(w->gid);
     workers_.clear();
+    syncbuf_.rows.clear();
     all_batches_.assign(G, 0);
     for (int k = 0; k < G; ++k) all_batches_[k] = (cnt[k] + cfg_.batch_size - 1) / cfg_.batch_size;
     epoch_steps_ = G ? *std::max_element(all_batches_.begin(), all_batches_.end()) : 0;

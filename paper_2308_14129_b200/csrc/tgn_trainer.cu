@@ -447,6 +447,10 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     const int D = lay_.D, F = lay_.F;
     const int Fp = F ? (F + 7) / 8 * 8 : 0;
     const int B = static_cast<int>(cfg.batch_size);
+    if (cfg.concurrent && world == 1 && workers.size() > 1) {  // concurrent lanes (tgn_lanes.cu)
+        build_lanes(subs, workers, node_count);
+        return;
+    }
     build_workers(subs, workers);
 
     // parameters + optimiser state
@@ -573,7 +577,8 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     }
 }
 
-int TGNTrainer::feat_stride() const { return s_->d.Fp; }
+int TGNTrainer::feat_stride() const { return lanes_.empty() ? s_->d.Fp : lanes_[0]->feat_stride(); }
+float* TGNTrainer::loss_dev() const { return s_->loss.p; }
 
 // Fork f onto a side stream (round-robin unless `which` pins one) at the
 // current point of the main stream; f's split-K GEMMs use ws_cur_/wsn_cur_.
@@ -646,6 +651,7 @@ TGNTrainer::~TGNTrainer() {
 // Per-worker device state from the subgraphs: local ids, time-sorted CSR,
 // destination pool, features (generated on device), memory and pending sets.
 void TGNTrainer::build_workers(const SubGraphs& subs, const std::vector<int>& ids) {
+    syncbuf_.rows.clear();  // (shared-row maps of the previous workers)
     const int D = lay_.D, F = lay_.F;
     const int Fp = F ? (F + 7) / 8 * 8 : 0;
     const int B = static_cast<int>(cfg_.batch_size);
@@ -762,6 +768,12 @@ void TGNTrainer::init_worker_state(Worker& w) {
 // evaluation views are rebuilt.
 void TGNTrainer::rebind(const SubGraphs& subs) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        lanes_wait();
+        for (auto& l : lanes_) l->rebind(subs);
+        epoch_steps_ = lanes_[0]->epoch_steps_;
+        return;
+    }
     if (static_cast<int>(subs.g.size()) != total_workers_)
         data_error("ConfigMismatch", "rebind needs one subgraph per worker (" +
                                          std::to_string(total_workers_) + ")");
@@ -785,6 +797,7 @@ void TGNTrainer::rebind(const SubGraphs& subs) {
 }
 
 Worker& TGNTrainer::worker(int w) {
+    if (!lanes_.empty()) return lane_of(w)->worker(w);
     for (auto& p : workers_)
         if (p->gid == w) return *p;
     usage_error("worker " + std::to_string(w) + " is not owned by this trainer");
@@ -812,6 +825,10 @@ void TGNTrainer::timed(const char* name, const std::function<void()>& f) {
 // -------------------------------------------------------------- schedule
 void TGNTrainer::begin_epoch(int epoch) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        for (auto& l : lanes_) l->begin_epoch(epoch);
+        return;
+    }
     epoch_ = epoch;
     step_in_epoch_ = 0;
     for (auto& wp : workers_) {
@@ -829,6 +846,10 @@ void TGNTrainer::begin_epoch(int epoch) {
 
 void TGNTrainer::seek(std::uint64_t step) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        for (auto& l : lanes_) l->seek(step);
+        return;
+    }
     if (step >= epoch_steps_) usage_error("seek past the end of the epoch");
     step_in_epoch_ = step;
     for (auto& wp : workers_) {
@@ -846,6 +867,11 @@ void TGNTrainer::seek(std::uint64_t step) {
 
 void TGNTrainer::set_surrogate(int d, const double* w_m, const double* omega, double gamma) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        lanes_wait();
+        for (auto& l : lanes_) l->set_surrogate(d, w_m, omega, gamma);
+        return;
+    }
     if (d != lay_.D) data_error("ConfigMismatch", "surrogate dimension must equal d_mem");
     sur_w_.alloc(std::size_t(3) * d * d);
     sur_w_.upload(w_m, sur_w_.n, stream_);
@@ -1321,6 +1347,7 @@ std::uint64_t kernel_launches() { return g_kernel_launches.load() + umma::launch
 // bracketed by CUDA events on the trainer's stream: device time in ms.
 float TGNTrainer::run_steps(std::uint64_t n) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) return lanes_run_steps(n);
     cudaEvent_t a, b;
     SPD_CUDA(cudaEventCreate(&a));
     SPD_CUDA(cudaEventCreate(&b));
@@ -1347,6 +1374,12 @@ float TGNTrainer::run_steps(std::uint64_t n) {
 void TGNTrainer::step_host(const spd_edge* const* events, const std::uint16_t* const* feats,
                            float* loss_out) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {  // lane k feeds local worker k; losses once every lane is enqueued
+        for (std::size_t k = 0; k < lanes_.size(); ++k)
+            lanes_[k]->step_host(events + k, feats ? feats + k : nullptr, nullptr);
+        if (loss_out) lanes_losses(loss_out);
+        return;
+    }
     if (step_in_epoch_ >= epoch_steps_) {
         end_epoch();
         begin_epoch(epoch_ + 1);
@@ -1396,6 +1429,12 @@ void TGNTrainer::step_host(const spd_edge* const* events, const std::uint16_t* c
 void TGNTrainer::step_host_async(const spd_edge* const* events, const std::uint16_t* const* feats,
                                  float* loss_pinned) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        for (std::size_t k = 0; k < lanes_.size(); ++k)
+            lanes_[k]->step_host_async(events + k, feats ? feats + k : nullptr,
+                                       loss_pinned ? loss_pinned + k : nullptr);
+        return;
+    }
     if (step_in_epoch_ >= epoch_steps_) {
         end_epoch();
         begin_epoch(epoch_ + 1);
@@ -1475,6 +1514,10 @@ void TGNTrainer::check_host_events(const Worker& w, std::uint64_t lo, std::uint6
 
 void TGNTrainer::sync() {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        for (auto& l : lanes_) l->sync();
+        return;
+    }
     SPD_CUDA(cudaStreamSynchronize(stream_));
     if (copy_) SPD_CUDA(cudaStreamSynchronize(copy_));
 }
@@ -1610,6 +1653,11 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
     // gradient all-reduce + Adam touch disjoint state: run them side by side
     if (profile_ || last == workers_.size()) {
         if (last != workers_.size()) worker_post_kernels(*workers_[last]);
+        if (peer_) {  // (its waits on the peers must not block the host: untimed)
+            allreduce_grads(stream_);
+            adam(stream_);
+            return;
+        }
         timed("allreduce", [&] { allreduce_grads(stream_); });
         timed("adam", [&] { adam(stream_); });
         return;
@@ -1623,11 +1671,13 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
 }
 
 void TGNTrainer::peer_export(unsigned char* out) const {
+    if (!lanes_.empty()) usage_error("peer transport: concurrent local workers use an in-process group");
     if (!peer_) usage_error("peer transport: trainer was created with an NCCL id or world 1");
     peer_->export_blob(out);
 }
 
 void TGNTrainer::peer_connect(const unsigned char* blobs) {
+    if (!lanes_.empty()) usage_error("peer transport: concurrent local workers use an in-process group");
     if (!peer_) usage_error("peer transport: trainer was created with an NCCL id or world 1");
     peer_->connect(blobs);
 }
@@ -1645,6 +1695,10 @@ void TGNTrainer::coll(void* data, std::size_t count, int type, int op, cudaStrea
 
 void TGNTrainer::step(float* loss_out) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        lanes_step(loss_out);
+        return;
+    }
     if (peer_ && !peer_->connected())
         usage_error("peer transport not connected (spd_tgn_peer_export / spd_tgn_peer_connect)");
     ++step_in_epoch_;
@@ -1711,21 +1765,26 @@ void TGNTrainer::step(float* loss_out) {
     }
 }
 
-void TGNTrainer::end_epoch() {
+void TGNTrainer::end_epoch(bool wait) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {  // every lane's restore + sync enqueued before any wait
+        for (auto& l : lanes_) l->end_epoch(false);
+        if (wait) lanes_wait();
+        return;
+    }
     for (auto& wp : workers_) {  // drop partial loops (pac_sim.cpp:259)
         Worker& w = *wp;
         SPD_CUDA(cudaMemcpyAsync(w.mem.p, w.mem_snap.p, w.mem.bytes(), cudaMemcpyDeviceToDevice, stream_));
         SPD_CUDA(cudaMemcpyAsync(w.lu.p, w.lu_snap.p, w.lu.bytes(), cudaMemcpyDeviceToDevice, stream_));
         for (auto& ps : w.pend) ps.nU.zero(stream_);
     }
-    sync_shared();
-    SPD_CUDA(cudaStreamSynchronize(stream_));
+    sync_shared(wait);
+    if (wait) SPD_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void TGNTrainer::run_epoch(int epoch, double* mean_loss) {
     begin_epoch(epoch);
-    std::vector<float> l(workers_.size());
+    std::vector<float> l(lanes_.empty() ? workers_.size() : lanes_.size());
     double sum = 0.0;
     std::uint64_t n = 0;
     for (std::uint64_t k = 0; k < epoch_steps_; ++k) {
@@ -1744,6 +1803,7 @@ void TGNTrainer::run_epoch(int epoch, double* mean_loss) {
 // ---------------------------------------------------------- introspection
 void TGNTrainer::get_params(float* out) const {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) return lanes_[0]->get_params(out);  // replicas are bit-identical
     SPD_CUDA(cudaStreamSynchronize(stream_));
     params_.download(out, lay_.total, stream_);
     SPD_CUDA(cudaStreamSynchronize(stream_));
@@ -1755,6 +1815,12 @@ void TGNTrainer::refresh_tc_weights() {
 
 void TGNTrainer::set_gemm_mode(int mode) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        lanes_wait();
+        for (auto& l : lanes_) l->set_gemm_mode(mode);
+        cfg_.gemm_mode = mode;
+        return;
+    }
     SPD_CUDA(cudaStreamSynchronize(stream_));
     for (auto& ge : graph_exec_)
         if (ge) {
@@ -1773,12 +1839,28 @@ void TGNTrainer::set_gemm_mode(int mode) {
 
 void TGNTrainer::set_params(const float* in) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {
+        lanes_wait();
+        for (auto& l : lanes_) l->set_params(in);
+        return;
+    }
     params_.upload(in, lay_.total, stream_);
     refresh_tc_weights();
     SPD_CUDA(cudaStreamSynchronize(stream_));
 }
 void TGNTrainer::get_grads(float* out) const {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) {  // each lane holds its own worker's gradient: mean in lane order
+        std::vector<float> sum(lay_.total, 0.f), one(lay_.total);
+        for (auto& l : lanes_) {
+            SPD_CUDA(cudaStreamSynchronize(l->stream_));
+            l->grads_.download(one.data(), lay_.total, l->stream_);
+            SPD_CUDA(cudaStreamSynchronize(l->stream_));
+            for (std::size_t i = 0; i < lay_.total; ++i) sum[i] += one[i];
+        }
+        for (std::size_t i = 0; i < lay_.total; ++i) out[i] = sum[i] / float(total_workers_);
+        return;
+    }
     SPD_CUDA(cudaStreamSynchronize(stream_));
     grads_.download(out, lay_.total, stream_);
     SPD_CUDA(cudaStreamSynchronize(stream_));
@@ -1786,6 +1868,7 @@ void TGNTrainer::get_grads(float* out) const {
     for (std::size_t i = 0; i < lay_.total; ++i) out[i] /= float(total_workers_);
 }
 void TGNTrainer::get_memory(int wid, float* mem, double* lu) {
+    if (!lanes_.empty()) return lane_of(wid)->get_memory(wid, mem, lu);
     Worker& w = worker(wid);
     DeviceGuard g(device_);
     SPD_CUDA(cudaStreamSynchronize(stream_));
@@ -1794,6 +1877,7 @@ void TGNTrainer::get_memory(int wid, float* mem, double* lu) {
     SPD_CUDA(cudaStreamSynchronize(stream_));
 }
 void TGNTrainer::set_memory(int wid, const float* mem, const double* lu) {
+    if (!lanes_.empty()) return lane_of(wid)->set_memory(wid, mem, lu);
     Worker& w = worker(wid);
     DeviceGuard g(device_);
     if (mem) w.mem.upload(mem, std::size_t(w.N) * lay_.D, stream_);
@@ -1802,6 +1886,7 @@ void TGNTrainer::set_memory(int wid, const float* mem, const double* lu) {
 }
 std::size_t TGNTrainer::debug_scratch(const char* name, float* out, std::size_t cap) {
     DeviceGuard g(device_);
+    if (!lanes_.empty()) return lanes_[0]->debug_scratch(name, out, cap);
     Scratch& s = *s_;
     const std::string n(name ? name : "");
     const DevBuf<float>* b = n == "x_gru" ? &s.x_gru : n == "h_gru" ? &s.h_gru : n == "Gi" ? &s.Gi
@@ -1818,6 +1903,7 @@ std::size_t TGNTrainer::debug_scratch(const char* name, float* out, std::size_t 
 
 void TGNTrainer::last_step(int wid, std::uint64_t* b, float* emb, std::uint32_t* negs,
                            std::uint32_t* nbr, float* loss) {
+    if (!lanes_.empty()) return lane_of(wid)->last_step(wid, b, emb, negs, nbr, loss);
     Worker& w = worker(wid);
     if (!debug_) usage_error("debug taps are off (spd_tgn_set_debug)");
     const std::uint64_t B = w.last_b;
@@ -1934,18 +2020,28 @@ __global__ void k_sync_apply_max(float* mem, double* lu, const std::uint32_t* ro
 }
 }  // namespace
 
-void TGNTrainer::sync_shared() {
+void TGNTrainer::sync_shared(bool wait) {
     const int S = static_cast<int>(shared_.size());
     if (total_workers_ < 2 || S == 0) return;
     const int D = lay_.D;
     cudaStream_t st = stream_;
-    DevBuf<float> sum(std::size_t(S) * D), mn(std::size_t(S) * D), mx(std::size_t(S) * D);
-    DevBuf<double> tmin(S), tmax(S);
-    std::vector<DevBuf<std::uint32_t>> rows(workers_.size());
-    for (std::size_t k = 0; k < workers_.size(); ++k) {
-        rows[k].alloc(S);
-        rows[k].upload(workers_[k]->shared_local.data(), S, st);
+    // persistent buffers: no allocation (and no cudaFree's device-wide sync)
+    // while the collectives' peer waits are in flight
+    auto& SB = syncbuf_;
+    if (SB.sum.n != std::size_t(S) * D) {
+        SB.sum.alloc(std::size_t(S) * D); SB.mn.alloc(std::size_t(S) * D); SB.mx.alloc(std::size_t(S) * D);
+        SB.tmin.alloc(S); SB.tmax.alloc(S); SB.owner.alloc(S);
     }
+    if (SB.rows.size() != workers_.size()) {
+        SB.rows.clear();
+        SB.rows.resize(workers_.size());
+        for (std::size_t k = 0; k < workers_.size(); ++k) {
+            SB.rows[k].alloc(S);
+            SB.rows[k].upload(workers_[k]->shared_local.data(), S, st);
+        }
+    }
+    auto& sum = SB.sum; auto& mn = SB.mn; auto& mx = SB.mx; auto& tmin = SB.tmin; auto& tmax = SB.tmax;
+    auto& rows = SB.rows;
     // local reduction in worker order (the reference's summation order)
     const bool have_local = !workers_.empty();
     if (!have_local) {  // identities of sum / min / max, so the collectives see only the peers
@@ -1974,7 +2070,7 @@ void TGNTrainer::sync_shared() {
         }
     } else {
         coll(tmax.p, S, kF64, kOpMax, st);
-        DevBuf<int> owner(S);
+        auto& owner = SB.owner;
         SPD_CUDA(cudaMemsetAsync(owner.p, 0x7F, owner.bytes(), st));
         for (std::size_t k = 0; k < workers_.size(); ++k)
             launch(k_sync_owner, blocks_for(S), 256, 0, st, workers_[k]->lu.p, rows[k].p, S, tmax.p,
@@ -1990,7 +2086,7 @@ void TGNTrainer::sync_shared() {
                 workers_[k]->mem.p, workers_[k]->lu.p, rows[k].p, S, D, sum.p, tmax.p);
     }
     SPD_CUDA(cudaGetLastError());
-    SPD_CUDA(cudaStreamSynchronize(st));
+    if (wait) SPD_CUDA(cudaStreamSynchronize(st));
 }
 
 namespace {
@@ -2022,6 +2118,10 @@ void build_adj(const std::vector<std::uint32_t>& src, const std::vector<std::uin
 
 void TGNTrainer::set_eval_events(int wid, const spd_edge* e, const std::uint64_t* eids,
                                  std::uint64_t n) {
+    if (!lanes_.empty()) {
+        lanes_wait();
+        return lane_of(wid)->set_eval_events(wid, e, eids, n);
+    }
     Worker& w = worker(wid);
     DeviceGuard g(device_);
     const std::uint64_t E = w.E, Et = E + n;
@@ -2082,6 +2182,10 @@ void TGNTrainer::set_eval_events(int wid, const spd_edge* e, const std::uint64_t
 
 void TGNTrainer::evaluate(int wid, std::uint64_t lo, std::uint64_t hi, std::uint64_t neg_seed,
                           float* pos, float* neg) {
+    if (!lanes_.empty()) {
+        lanes_wait();
+        return lane_of(wid)->evaluate(wid, lo, hi, neg_seed, pos, neg);
+    }
     Worker& w = worker(wid);
     if (hi > w.E_eval || lo > hi) usage_error("eval range outside the eval events");
     DeviceGuard g(device_);

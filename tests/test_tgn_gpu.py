@@ -452,3 +452,38 @@ def test_jodie_backbone_matches_oracle(parts, gemm_mode):
         assert np.array_equal(lu, o.lu[w])
         assert rel_err(m, o.mem[w].numpy()) < mem_tol
     tr.close()
+
+
+@pytest.mark.parametrize("parts,sync_average", [(2, 1), (3, 0)])
+def test_concurrent_workers_match_oracle(parts, sync_average):
+    """spd_tgn_config.concurrent = 1: a process's local workers train as
+    concurrent lanes (own streams, scratch, graphs and parameter replica; an
+    in-process peer group for the fused all-reduce + Adam and the epoch-end
+    sync). Two epochs against the oracle at the FP32 trajectory bar, graph
+    replay on, losses / parameters / memory / clocks, and the evaluation path."""
+    _, _, pa, subs = partitioned(parts=parts)
+    cfg = small_cfg(concurrent=1, sync_average=sync_average)
+    tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+    o = oracle_for(cfg, subs, pa.shared)
+    assert np.array_equal(tr.params(), o.flat.numpy())
+    for epoch in range(2):
+        tr.begin_epoch(epoch)
+        o.begin_epoch(epoch)
+        assert tr.epoch_steps() == o.epoch_steps()
+        for _ in range(o.epoch_steps()):
+            gl = tr.step()
+            ol = o.step()
+            for w in range(parts):
+                if not np.isnan(ol[w]):
+                    assert abs(gl[w] - ol[w]) <= TOL_TRAJ * max(1.0, abs(ol[w])), (epoch, gl, ol)
+        tr.end_epoch()
+        o.end_epoch()
+        assert rel_err(tr.params(), o.flat.numpy()) < TOL_TRAJ, epoch
+        for w in range(parts):
+            m, lu = tr.memory(w)
+            assert np.array_equal(lu, o.lu[w]), (epoch, w)
+            assert rel_err(m, o.mem[w].numpy()) < TOL_TRAJ, (epoch, w)
+    # timed steps across an epoch boundary run every lane
+    ms = tr.run_steps(o.epoch_steps() + 3)
+    assert ms > 0
+    tr.close()
