@@ -12,6 +12,7 @@
 //
 // Host discipline: a lane's step enqueues waits for its peers' flags, so every
 // lane's work of a global step is enqueued before the host waits on any lane.
+#include "pdl.cuh"
 #include "tgn.hpp"
 
 namespace spd {
@@ -28,6 +29,10 @@ void TGNTrainer::build_lanes(const SubGraphs& subs, const std::vector<int>& work
     std::vector<PeerComm*> all;
     for (auto& l : lanes_) all.push_back(l->peer_.get());
     for (auto& l : lanes_) l->peer_->connect_local(all);
+    // no programmatic dependent launch: early-launched dependents waiting on a
+    // spinning peer wait would hold the SM slots the other lanes need to
+    // raise its flag (pdl.cuh; process-wide, SPD_PDL=1 overrides at your risk)
+    pdl_auto() = false;
     epoch_steps_ = lanes_[0]->epoch_steps_;
     total_workers_ = lanes_[0]->total_workers_;
 }
