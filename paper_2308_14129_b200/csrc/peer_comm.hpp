@@ -53,6 +53,7 @@ public:
     // map every peer's buffers directly, no IPC; all[r] = rank r's transport
     void connect_local(const std::vector<PeerComm*>& all);
     bool connected() const { return connected_; }
+    const unsigned* flags_dev() const { return flags_; }
     const PeerView& view() const { return v_; }
 
     // In-graph step protocol (seq read from *seq_dev, the step's control word)

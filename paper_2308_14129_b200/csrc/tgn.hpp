@@ -80,6 +80,7 @@ struct Worker {
     // schedule
     std::uint64_t batches = 0, pos = 0, loops = 0;
     bool done = false;
+    bool flush_due = false;  // (lanes) loop ended: flush + snapshot after the group Adam
     double last_loss = 0.0;
     std::uint64_t last_b = 0;
     // evaluation view: train + eval events, their features and full-graph CSR
@@ -211,9 +212,16 @@ private:
     void build_lanes(const SubGraphs& subs, const std::vector<int>& workers, NodeId node_count);
     TGNTrainer* lane_of(int gid);
     void lanes_wait();
+    void lanes_after(cudaEvent_t ev);
+    void lanes_join();
     void lanes_losses(float* loss_out);
     void lanes_step(float* loss_out);
+    void lanes_adam_step();
+    void lanes_end_epoch(bool wait);
     float lanes_run_steps(std::uint64_t n);
+    std::vector<cudaEvent_t> lane_end_;
+    cudaEvent_t lanes_adam_ = nullptr;  // lane 0's point after the parent's Adam (or sync)
+    bool lanes_adam_valid_ = false;
     void init_worker_state(Worker& w);  // memory, clocks, pending sets, shared-row map
     std::unique_ptr<DevStream> dstream_;
     void worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx,
@@ -233,12 +241,15 @@ private:
     void decoder_wgrads(cudaEvent_t at, int B);    // decoder weight gradients (side streams)
     void jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx, bool post);
     void worker_post(Worker& w);
+    void loop_end_flush(Worker& w);
     void flush_pending(Worker& w);
     void gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
                      const std::function<void()>& after_gather = {});
     void allreduce_grads(cudaStream_t st);
     void adam(cudaStream_t st);
     void sync_shared(bool wait = true);
+    void sync_workers(const std::vector<Worker*>& wlist, cudaStream_t st);
+    bool lane_ = false;  // a lane of a concurrent parent: no Adam, no shared sync of its own
     void timed(const char* name, const std::function<void()>& f);
     // weight-gradient GEMMs run on a side stream forked from the main stream at
     // the point their inputs exist, and joined back once per worker step

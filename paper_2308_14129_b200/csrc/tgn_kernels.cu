@@ -783,6 +783,20 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t
     }
 }
 
+// Adam on the sum of several gradient buffers (concurrent local workers,
+// tgn_lanes.cu), summed in list order — the order the peer transport uses.
+__global__ void k_adam_multi(float* p, GradList gl, float* m, float* v, std::size_t n, float scale,
+                             float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
+                             float eps, float* p_tc) {
+    pdl_entry();
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float g = gl.g[0][i];
+    for (int r = 1; r < gl.n; ++r) g += gl.g[r][i];
+    adam_one(p[i], g, m[i], v[i], scale, lr, b1, one_m_b1, b2, one_m_b2, bc[0], bc[1], eps);
+    if (p_tc) p_tc[i] = tf32r(p[i]);
+}
+
 __global__ void k_round_tf32(const float* src, float* dst, std::size_t n) {
     pdl_entry();
     const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;

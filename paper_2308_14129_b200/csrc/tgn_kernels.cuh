@@ -175,6 +175,13 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t
                        float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
                        float eps, float* p_tc);
 __global__ void k_round_tf32(const float* src, float* dst, std::size_t n);
+struct GradList {
+    const float* g[8];
+    int n;
+};
+__global__ void k_adam_multi(float* p, GradList gl, float* m, float* v, std::size_t n, float scale,
+                             float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
+                             float eps, float* p_tc);
 __global__ void k_persist(WorkerDev w, int D, const float* mem_new);
 __global__ void k_pending(WorkerDev w, int B);
 __global__ void k_rnn_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh, float* save, float* mem_new);

@@ -619,6 +619,12 @@ void TGNTrainer::join_side() {
 }
 
 TGNTrainer::~TGNTrainer() {
+    if (!lanes_.empty()) {
+        for (auto& l : lanes_) cudaStreamSynchronize(l->stream_);
+        for (auto e : lane_end_)
+            if (e) cudaEventDestroy(e);
+        if (lanes_adam_) cudaEventDestroy(lanes_adam_);
+    }
     for (auto g : graph_exec_)
         if (g) cudaGraphExecDestroy(g);
     if (stream_) cudaStreamSynchronize(stream_);
@@ -1375,8 +1381,10 @@ void TGNTrainer::step_host(const spd_edge* const* events, const std::uint16_t* c
                            float* loss_out) {
     DeviceGuard g(device_);
     if (!lanes_.empty()) {  // lane k feeds local worker k; losses once every lane is enqueued
+        if (lanes_adam_valid_) lanes_after(lanes_adam_);
         for (std::size_t k = 0; k < lanes_.size(); ++k)
             lanes_[k]->step_host(events + k, feats ? feats + k : nullptr, nullptr);
+        lanes_adam_step();
         if (loss_out) lanes_losses(loss_out);
         return;
     }
@@ -1430,9 +1438,11 @@ void TGNTrainer::step_host_async(const spd_edge* const* events, const std::uint1
                                  float* loss_pinned) {
     DeviceGuard g(device_);
     if (!lanes_.empty()) {
+        if (lanes_adam_valid_) lanes_after(lanes_adam_);
         for (std::size_t k = 0; k < lanes_.size(); ++k)
             lanes_[k]->step_host_async(events + k, feats ? feats + k : nullptr,
                                        loss_pinned ? loss_pinned + k : nullptr);
+        lanes_adam_step();
         return;
     }
     if (step_in_epoch_ >= epoch_steps_) {
@@ -1526,13 +1536,20 @@ void TGNTrainer::worker_post(Worker& w) {
     w.cur ^= 1;  // the set k_pending just filled holds the messages to apply next
     ++w.pos;
     if (w.pos == w.batches) {  // loop_end: flush (new params) + snapshot (pac_sim.cpp:248-255)
-        flush_pending(w);
-        SPD_CUDA(cudaMemcpyAsync(w.mem_snap.p, w.mem.p, w.mem.bytes(), cudaMemcpyDeviceToDevice, stream_));
-        SPD_CUDA(cudaMemcpyAsync(w.lu_snap.p, w.lu.p, w.lu.bytes(), cudaMemcpyDeviceToDevice, stream_));
+        // (a lane's step has no Adam yet: its parent flushes after the group Adam)
+        if (lane_) w.flush_due = true;
+        else loop_end_flush(w);
         ++w.loops;
         w.done = true;
         w.pos = 0;
     }
+}
+
+void TGNTrainer::loop_end_flush(Worker& w) {
+    flush_pending(w);
+    SPD_CUDA(cudaMemcpyAsync(w.mem_snap.p, w.mem.p, w.mem.bytes(), cudaMemcpyDeviceToDevice, stream_));
+    SPD_CUDA(cudaMemcpyAsync(w.lu_snap.p, w.lu.p, w.lu.bytes(), cudaMemcpyDeviceToDevice, stream_));
+    w.flush_due = false;
 }
 
 void TGNTrainer::allreduce_grads(cudaStream_t st) {
@@ -1653,9 +1670,9 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
     // gradient all-reduce + Adam touch disjoint state: run them side by side
     if (profile_ || last == workers_.size()) {
         if (last != workers_.size()) worker_post_kernels(*workers_[last]);
-        if (peer_) {  // (its waits on the peers must not block the host: untimed)
+        if (peer_ || lane_) {  // (peer waits must not block the host: untimed)
             allreduce_grads(stream_);
-            adam(stream_);
+            if (!lane_) adam(stream_);  // (a lane's Adam is its parent's, tgn_lanes.cu)
             return;
         }
         timed("allreduce", [&] { allreduce_grads(stream_); });
@@ -1664,7 +1681,7 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
     }
     side([&](cudaStream_t sd) {
         allreduce_grads(sd);
-        adam(sd);
+        if (!lane_) adam(sd);
     });
     worker_post_kernels(*workers_[last]);
     join_side();
@@ -1767,9 +1784,8 @@ void TGNTrainer::step(float* loss_out) {
 
 void TGNTrainer::end_epoch(bool wait) {
     DeviceGuard g(device_);
-    if (!lanes_.empty()) {  // every lane's restore + sync enqueued before any wait
-        for (auto& l : lanes_) l->end_epoch(false);
-        if (wait) lanes_wait();
+    if (!lanes_.empty()) {
+        lanes_end_epoch(wait);
         return;
     }
     for (auto& wp : workers_) {  // drop partial loops (pac_sim.cpp:259)
@@ -2021,10 +2037,19 @@ __global__ void k_sync_apply_max(float* mem, double* lu, const std::uint32_t* ro
 }  // namespace
 
 void TGNTrainer::sync_shared(bool wait) {
+    if (lane_) return;  // (the parent syncs every lane's worker, tgn_lanes.cu)
+    std::vector<Worker*> ws;
+    for (auto& w : workers_) ws.push_back(w.get());
+    sync_workers(ws, stream_);
+    if (wait) SPD_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// The shared-hub sync over `wlist` (this process's workers, in worker order),
+// then across ranks (coll), on stream st.
+void TGNTrainer::sync_workers(const std::vector<Worker*>& wlist, cudaStream_t st) {
     const int S = static_cast<int>(shared_.size());
     if (total_workers_ < 2 || S == 0) return;
     const int D = lay_.D;
-    cudaStream_t st = stream_;
     // persistent buffers: no allocation (and no cudaFree's device-wide sync)
     // while the collectives' peer waits are in flight
     auto& SB = syncbuf_;
@@ -2032,24 +2057,24 @@ void TGNTrainer::sync_shared(bool wait) {
         SB.sum.alloc(std::size_t(S) * D); SB.mn.alloc(std::size_t(S) * D); SB.mx.alloc(std::size_t(S) * D);
         SB.tmin.alloc(S); SB.tmax.alloc(S); SB.owner.alloc(S);
     }
-    if (SB.rows.size() != workers_.size()) {
+    if (SB.rows.size() != wlist.size()) {
         SB.rows.clear();
-        SB.rows.resize(workers_.size());
-        for (std::size_t k = 0; k < workers_.size(); ++k) {
+        SB.rows.resize(wlist.size());
+        for (std::size_t k = 0; k < wlist.size(); ++k) {
             SB.rows[k].alloc(S);
-            SB.rows[k].upload(workers_[k]->shared_local.data(), S, st);
+            SB.rows[k].upload(wlist[k]->shared_local.data(), S, st);
         }
     }
     auto& sum = SB.sum; auto& mn = SB.mn; auto& mx = SB.mx; auto& tmin = SB.tmin; auto& tmax = SB.tmax;
     auto& rows = SB.rows;
     // local reduction in worker order (the reference's summation order)
-    const bool have_local = !workers_.empty();
+    const bool have_local = !wlist.empty();
     if (!have_local) {  // identities of sum / min / max, so the collectives see only the peers
         sum.zero(st);
         launch(k_sync_fill, blocks_for(mn.n), 256, 0, st, mn.p, mx.p, mn.n, tmin.p, tmax.p, S);
     }
-    for (std::size_t k = 0; k < workers_.size(); ++k) {
-        Worker& w = *workers_[k];
+    for (std::size_t k = 0; k < wlist.size(); ++k) {
+        Worker& w = *wlist[k];
         launch(k_sync_pack, blocks_for(std::size_t(S) * (D + 1)), 256, 0, st, 
             w.mem.p, w.lu.p, rows[k].p, S, D, k == 0, sum.p, mn.p, mx.p, tmax.p);
         launch(k_sync_ts_minmax, blocks_for(S), 256, 0, st, w.lu.p, rows[k].p, S, k == 0, tmin.p, tmax.p);
@@ -2063,8 +2088,8 @@ void TGNTrainer::sync_shared(bool wait) {
         coll(tmin.p, S, kF64, kOpMin, st);
         coll(tmax.p, S, kF64, kOpMax, st);
         if (world_ > 1 && !peer_) SPD_NCCL(ncclGroupEnd());
-        for (std::size_t k = 0; k < workers_.size(); ++k) {
-            Worker& w = *workers_[k];
+        for (std::size_t k = 0; k < wlist.size(); ++k) {
+            Worker& w = *wlist[k];
             launch(k_sync_apply_avg, S, 128, 0, st, w.mem.p, w.lu.p, rows[k].p, S, D, sum.p, mn.p, mx.p,
                                                 tmin.p, tmax.p, 1.f / float(total_workers_));
         }
@@ -2072,21 +2097,20 @@ void TGNTrainer::sync_shared(bool wait) {
         coll(tmax.p, S, kF64, kOpMax, st);
         auto& owner = SB.owner;
         SPD_CUDA(cudaMemsetAsync(owner.p, 0x7F, owner.bytes(), st));
-        for (std::size_t k = 0; k < workers_.size(); ++k)
-            launch(k_sync_owner, blocks_for(S), 256, 0, st, workers_[k]->lu.p, rows[k].p, S, tmax.p,
-                                                        workers_[k]->gid, owner.p);
+        for (std::size_t k = 0; k < wlist.size(); ++k)
+            launch(k_sync_owner, blocks_for(S), 256, 0, st, wlist[k]->lu.p, rows[k].p, S, tmax.p,
+                                                        wlist[k]->gid, owner.p);
         coll(owner.p, S, kI32, kOpMin, st);
         sum.zero(st);
-        for (std::size_t k = 0; k < workers_.size(); ++k)
+        for (std::size_t k = 0; k < wlist.size(); ++k)
             launch(k_sync_owner_pack, blocks_for(std::size_t(S) * D), 256, 0, st, 
-                workers_[k]->mem.p, rows[k].p, S, D, owner.p, workers_[k]->gid, sum.p);
+                wlist[k]->mem.p, rows[k].p, S, D, owner.p, wlist[k]->gid, sum.p);
         coll(sum.p, sum.n, kF32, kOpSum, st);
-        for (std::size_t k = 0; k < workers_.size(); ++k)
+        for (std::size_t k = 0; k < wlist.size(); ++k)
             launch(k_sync_apply_max, blocks_for(std::size_t(S) * D), 256, 0, st, 
-                workers_[k]->mem.p, workers_[k]->lu.p, rows[k].p, S, D, sum.p, tmax.p);
+                wlist[k]->mem.p, wlist[k]->lu.p, rows[k].p, S, D, sum.p, tmax.p);
     }
     SPD_CUDA(cudaGetLastError());
-    if (wait) SPD_CUDA(cudaStreamSynchronize(st));
 }
 
 namespace {
