@@ -237,10 +237,21 @@ void proj_dgrad(bool tc, const float* A, int lda, const float* B, int ldb, float
         gemm_dgrad(A + z * bt.a, lda, B + z * bt.b, ldb, C + z * bt.c, ldc, M, N, K, M_dev, s, epi,
                    mask, ldmask);
 }
+// split-K target grid of the GRU weight gradients (SPD_GRU_WGRAD_CTAS; 64 = the side default)
+long tgru_ctas() {
+    static const long v = [] {
+        const char* e = std::getenv("SPD_GRU_WGRAD_CTAS");
+        return e ? std::atol(e) : 64L;
+    }();
+    return v;
+}
+
 void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw,
                 int N_out, int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
-                cudaStream_t s, const umma::Batch& bt = {}) {
-    if (tc) return umma::wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s, bt);
+                cudaStream_t s, const umma::Batch& bt = {}, int target_ctas = 64) {
+    if (tc)
+        return umma::wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s, bt,
+                           target_ctas);
     for (int z = 0; z < bt.n; ++z)
         gemm_wgrad(dY + z * bt.a, ldy, X + z * bt.b, ldx, dW + z * bt.c, ldw, N_out, K_in, rows,
                    rows_dev, ws, ws_cap, s);
@@ -1315,10 +1326,13 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         dh_pull_root(d, s, st);
         if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_pull_, 0));  // occurrence chunk partials
         gru_bwd_dh(wd, d, s, st);
+        // the step's last weight gradients (Adam waits for them): a grid of
+        // about one wave each instead of the side streams' 64 CTAs
+        const int gru_ctas = int(tgru_ctas());
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
-                   3 * d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
+                   3 * d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd, {}, gru_ctas); });
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
-                   3 * d.D, d.D + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
+                   3 * d.D, d.D + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd, {}, gru_ctas); });
     });
     // side-stream weight grads read the pending set (nU, GRU inputs) that the
     // post phase rewrites: join first

@@ -262,7 +262,7 @@ void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, 
 
 void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
            int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
-           cudaStream_t s, const Batch& bt) {
+           cudaStream_t s, const Batch& bt, int target_ctas) {
     if (!rows || !N_out || !K_in) return;
     check_batch(bt);
     const int mt = (N_out + BM - 1) / BM;
@@ -289,7 +289,7 @@ void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw
     const int tiles = ((N_out + BM - 1) / BM) * ((K_in + bn - 1) / bn) * bt.n;
     // ~64 CTAs: enough K-parallelism for these small outputs without a split-K
     // partial traffic (split x |dW|) that the reduce then has to stream back
-    int split = std::max(1, std::min(rows / (4 * BK), (64 + tiles - 1) / tiles));
+    int split = std::max(1, std::min(rows / (4 * BK), (target_ctas + tiles - 1) / tiles));
     while (split > 1 && std::size_t(split) * bt.n * N_out * ldws > ws_cap) --split;
     for (int z = 0; z < bt.n; ++z) {
         maps.a[z] = make_map(dY + z * bt.a, N_out, rows, ldy, BK, true);  // dY [rows x N_out]

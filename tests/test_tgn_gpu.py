@@ -455,15 +455,15 @@ def test_jodie_backbone_matches_oracle(parts, gemm_mode):
 
 
 @pytest.mark.parametrize("concurrent", [1, 0])
-@pytest.mark.parametrize("parts,sync_average", [(2, 1), (3, 0)])
-def test_concurrent_workers_match_oracle(parts, sync_average, concurrent):
+@pytest.mark.parametrize("parts,sync_average,backbone", [(2, 1, 0), (3, 0, 0), (2, 1, 1)])
+def test_concurrent_workers_match_oracle(parts, sync_average, backbone, concurrent):
     """spd_tgn_config.concurrent = 1: a process's local workers train as
     concurrent lanes (own streams, scratch, graphs and parameter replica; an
     in-process peer group for the fused all-reduce + Adam and the epoch-end
     sync). Two epochs against the oracle at the FP32 trajectory bar, graph
     replay on, losses / parameters / memory / clocks, and the evaluation path."""
     _, _, pa, subs = partitioned(parts=parts)
-    cfg = small_cfg(concurrent=concurrent, sync_average=sync_average)
+    cfg = small_cfg(concurrent=concurrent, sync_average=sync_average, backbone=backbone)
     tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
     o = oracle_for(cfg, subs, pa.shared)
     assert np.array_equal(tr.params(), o.flat.numpy())
