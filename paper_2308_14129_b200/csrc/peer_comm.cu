@@ -8,7 +8,11 @@
 #include "host.hpp"
 #include "pdl.cuh"
 
+#include <atomic>
+
 namespace spd {
+
+extern std::atomic<std::uint64_t> g_kernel_launches;  // (tgn_trainer.cu)
 
 namespace {
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
@@ -121,20 +125,6 @@ void PeerComm::export_blob(unsigned char* out) const {
     std::memcpy(out + 3 * 64 + 8, &sb, sizeof sb);
 }
 
-void PeerComm::connect_local(const std::vector<PeerComm*>& all) {
-    if (connected_) usage_error("peer transport already connected");
-    if (static_cast<int>(all.size()) != world_) internal_error("InvalidParams", "connect_local: one transport per rank");
-    for (int r = 0; r < world_; ++r) {
-        const PeerComm& o = *all[r];
-        if (o.rank_ != r || o.world_ != world_ || o.sbuf_bytes_ != sbuf_bytes_)
-            internal_error("InvalidParams", "connect_local: mismatched transports");
-        v_.grads[r] = o.v_.grads[r];
-        v_.flags_of[r] = o.flags_;
-        v_.sbuf[r] = o.sbuf_;
-    }
-    connected_ = true;
-}
-
 void PeerComm::connect(const unsigned char* blobs) {
     if (connected_) usage_error("peer transport already connected");
     DeviceGuard g(device_);
@@ -164,22 +154,24 @@ void PeerComm::connect(const unsigned char* blobs) {
 
 void PeerComm::signal(int kind, const std::uint64_t* seq_dev, std::int64_t offset, cudaStream_t st) {
     k_peer_signal<<<1, 32, 0, st>>>(v_, kind, seq_dev, 0, offset);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
 }
 void PeerComm::wait(int kind, const std::uint64_t* seq_dev, std::int64_t offset, cudaStream_t st) {
     k_peer_wait<<<1, 32, 0, st>>>(v_, kind, seq_dev, 0, offset);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
 }
 
 void PeerComm::adam_step(const std::uint64_t* seq_dev, float* p, float* m, float* v, std::size_t n,
                          float scale, float lr, float b1, float one_m_b1, float b2, float one_m_b2,
-                   const float* bc, float eps,
-                         float* p_tc, cudaStream_t st) {
+                         const float* bc, float eps, float* p_tc, cudaStream_t st) {
     if (!connected_) usage_error("peer transport not connected (spd_tgn_peer_connect)");
     signal(kReady, seq_dev, 0, st);
     wait(kReady, seq_dev, 0, st);
     k_adam_peer<<<unsigned((n + 255) / 256), 256, 0, st>>>(p, v_, m, v, n, scale, lr, b1, one_m_b1, b2,
                                                            one_m_b2, bc, eps, p_tc);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
     signal(kDone, seq_dev, 0, st);
 }
@@ -192,14 +184,19 @@ void PeerComm::allreduce(void* data, std::size_t count, int type, int op, cudaSt
     const std::uint64_t seq = ++sync_seq_;
     // every peer has finished reading my exchange buffer (previous collective)
     k_peer_wait<<<1, 32, 0, st>>>(v_, kSyncDone, nullptr, seq - 1, 0);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaMemcpyAsync(sbuf_, data, count * esz, cudaMemcpyDeviceToDevice, st));
     k_peer_signal<<<1, 32, 0, st>>>(v_, kSyncReady, nullptr, seq, 0);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_peer_wait<<<1, 32, 0, st>>>(v_, kSyncReady, nullptr, seq, 0);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     const unsigned grid = unsigned(std::min<std::size_t>((count + 255) / 256, 1184));
     if (type == kF32) k_peer_reduce<float><<<grid, 256, 0, st>>>(v_, static_cast<float*>(data), count, op);
     else if (type == kF64) k_peer_reduce<double><<<grid, 256, 0, st>>>(v_, static_cast<double*>(data), count, op);
     else k_peer_reduce<int><<<grid, 256, 0, st>>>(v_, static_cast<int*>(data), count, op);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     k_peer_signal<<<1, 32, 0, st>>>(v_, kSyncDone, nullptr, seq, 0);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
 }
 

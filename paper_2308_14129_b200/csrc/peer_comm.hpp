@@ -49,11 +49,7 @@ public:
     static constexpr std::size_t kBlobBytes = 3 * 64 + 16;
     void export_blob(unsigned char* out) const;  // kBlobBytes
     void connect(const unsigned char* blobs);    // world * kBlobBytes, rank order
-    // ranks living in one process (concurrent local workers on one device):
-    // map every peer's buffers directly, no IPC; all[r] = rank r's transport
-    void connect_local(const std::vector<PeerComm*>& all);
     bool connected() const { return connected_; }
-    const unsigned* flags_dev() const { return flags_; }
     const PeerView& view() const { return v_; }
 
     // In-graph step protocol (seq read from *seq_dev, the step's control word)

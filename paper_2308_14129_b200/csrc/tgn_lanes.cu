@@ -12,11 +12,14 @@
 //
 // So a small-batch step (launch/latency bound: one batch far from filling the
 // GPU) overlaps with the other partitions' steps.
+#include <atomic>
 #include <cmath>
 
 #include "tgn.hpp"
 
 namespace spd {
+
+extern std::atomic<std::uint64_t> g_kernel_launches;  // (tgn_trainer.cu)
 
 void TGNTrainer::build_lanes(const SubGraphs& subs, const std::vector<int>& workers,
                              NodeId node_count) {
@@ -98,6 +101,7 @@ void TGNTrainer::lanes_adam_step() {
         static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2), l0.adam_bc_, cfg_.adam_eps,
         tc ? l0.params_tc_.p : nullptr);
     SPD_CUDA(cudaGetLastError());
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     for (std::size_t k = 1; k < lanes_.size(); ++k) {
         SPD_CUDA(cudaMemcpyAsync(lanes_[k]->params_.p, l0.params_.p, n * sizeof(float),
                                  cudaMemcpyDeviceToDevice, l0.stream_));
