@@ -10,6 +10,8 @@
 // Without the attribute both device instructions are no-ops.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdlib>
 
 namespace spd {
@@ -33,6 +35,27 @@ inline bool& pdl_auto() {
 inline bool pdl_enabled() {
     const int m = pdl_forced();
     return m >= 0 ? m == 1 : pdl_auto();
+}
+// SPD_PDL_MAIN=1 (experiment): PDL only on the high-priority (critical-path)
+// streams, whose kernels then overlap their predecessors' tails, while the
+// side streams' kernels launch normally
+inline bool pdl_main_only() {
+    static const bool on = [] {
+        const char* e = std::getenv("SPD_PDL_MAIN");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+// whether a launch on a stream of priority `prio` uses PDL
+inline bool pdl_for(int prio) {
+    if (pdl_enabled()) return true;
+    if (!pdl_main_only()) return false;
+    static const int hi = [] {
+        int lo = 0, h = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &h);
+        return h;
+    }();
+    return prio == hi;
 }
 
 }  // namespace spd

@@ -52,7 +52,7 @@ void launch(void (*k)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaSt
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.numAttrs = pdl_for(prio) ? 2 : 1;
     SPD_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(std::forward<Args>(args))...));
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }

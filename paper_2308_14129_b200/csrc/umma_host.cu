@@ -90,7 +90,7 @@ void reduce(const float* ws, int split, int M, int N, int ldws, float* C, int ld
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.numAttrs = pdl_for(prio) ? 2 : 1;
     SPD_CUDA(cudaLaunchKernelEx(&cfg, k_splitk_reduce, ws, split, M, N, ldws, C, ldc,
                                 static_cast<long long>(bt.c), bt.n));
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
@@ -120,7 +120,7 @@ void run(const Maps& maps, const Args& args, dim3 grid, cudaStream_t s) {
     attr[2].val.programmaticStreamSerializationAllowed = 1;
     int na = 1;
     if (CL > 1) attr[na++] = attr[1];
-    if (pdl_enabled()) attr[na++] = attr[2];
+    if (pdl_for(prio)) attr[na++] = attr[2];
     cfg.attrs = attr;
     cfg.numAttrs = na;
     SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, args));
@@ -331,7 +331,7 @@ void gru_fused_t(const float* x, int ldx, int K1, const float* h, int ldh, int K
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // pdl.cuh
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.numAttrs = pdl_for(prio) ? 2 : 1;
     SPD_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, a));
     g_launch_counter.fetch_add(1, std::memory_order_relaxed);
     SPD_CUDA(cudaGetLastError());
