@@ -2,11 +2,12 @@
 // launched with cudaLaunchAttributeProgrammaticStreamSerialization, so their
 // dependents begin launching at once and each kernel waits for its
 // predecessors' completion and memory before its first global access.
-// Measured: slower on the GDELT step (B = 2000: waiting dependent CTAs hold SM
-// slots the side-stream weight-gradient GEMMs would use, 0.525 vs 0.500 ms),
-// faster on small batches whose step is launch-latency bound (B = 200:
-// Reddit 0.197 -> 0.186 ms, LastFM 0.180 -> 0.174 ms). Default: on for
-// batches <= 512 (set by the trainer); SPD_PDL=1 / SPD_PDL=0 force it.
+// On every stream: slower on the GDELT step (B = 2000: waiting dependent CTAs
+// hold SM slots the side-stream weight-gradient GEMMs would use, 0.525 vs
+// 0.500 ms), faster on small batches whose step is launch-latency bound
+// (B = 200: Reddit 0.197 -> 0.186 ms, LastFM 0.180 -> 0.174 ms): on for
+// batches <= 512 (set by the trainer); SPD_PDL=1 / SPD_PDL=0 force it. On the
+// critical-path streams only: see pdl_main_only.
 // Without the attribute both device instructions are no-ops.
 #pragma once
 
@@ -36,13 +37,14 @@ inline bool pdl_enabled() {
     const int m = pdl_forced();
     return m >= 0 ? m == 1 : pdl_auto();
 }
-// SPD_PDL_MAIN=1 (experiment): PDL only on the high-priority (critical-path)
-// streams, whose kernels then overlap their predecessors' tails, while the
-// side streams' kernels launch normally
+// PDL on the high-priority (critical-path) streams at every batch size: their
+// kernels' launches overlap their predecessors' tails while the side streams'
+// kernels launch normally and hold no SM slots waiting (GDELT B = 2000:
+// 0.349 vs 0.364 ms per step). SPD_PDL_MAIN=0 turns it off.
 inline bool pdl_main_only() {
     static const bool on = [] {
         const char* e = std::getenv("SPD_PDL_MAIN");
-        return e && e[0] == '1';
+        return !(e && e[0] == '0');
     }();
     return on;
 }
