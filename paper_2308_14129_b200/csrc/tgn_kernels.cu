@@ -371,7 +371,7 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
 }
 
 // K7 fused decoder (FP32 FFMA, the north star's rule for the decoder): per
-// block of kDecEv events, from the embeddings of their src / dst / negative
+// block of EV events (kDecEv, or kDecEvSmall for small batches), from the embeddings of their src / dst / negative
 // roots to the data gradient of those embeddings, in one launch —
 //   Y_src = W_a z_src, Y_dst = W_b z_dst, Y_neg = W_b z_neg
 //   D1 = relu(Y_src + Y_{dst|neg} + b1); logit = D1 . w2 + b2; BCE terms
@@ -380,11 +380,11 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
 // (the MergeLayer of oracle/tgn_oracle.py _decode applied to [z_u | z_v] by
 // input halves). W1 = [W_a | W_b | b1] rows (row stride ld1) are staged in
 // shared memory once per block; thread (kind, n) owns output column n of the
-// block's kDecEv rows of one kind (src, dst, neg) and reads its weight row /
+// block's EV rows of one kind (src, dst, neg) and reads its weight row /
 // column with 16-B loads while the activations broadcast. Writes D1, dlogit,
 // dD1 (the weight gradients' inputs), loss terms, logits and d_emb. bwd = 0
 // (evaluation): forward and logits only.
-template <int MAXT, int MINB>
+template <int MAXT, int MINB, int EV>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2, float* D1,
               float* dlogit, float* lossv, float* dD1, float* logits, float* d_emb, int bwd) {
@@ -393,14 +393,14 @@ __global__ void __launch_bounds__(MAXT, MINB)
     const int D = d.D, ldw = 2 * D + 4, ldz = D + 4;
     float* sW = dsm;                                  // [D][ldw]: W_a | W_b | b1
     float* sZ = sW + (std::size_t)D * ldw;            // [3 EV][ldz]: z rows; later dD1 [2 EV]
-    float* sY = sZ + 3 * kDecEv * ldz;                // [3 EV][ldz]
-    float* sD1 = sY + 3 * kDecEv * ldz;               // [2 EV][ldz]
-    float* sw2 = sD1 + 2 * kDecEv * ldz;              // [ldz]
+    float* sY = sZ + 3 * EV * ldz;                // [3 EV][ldz]
+    float* sD1 = sY + 3 * EV * ldz;               // [2 EV][ldz]
+    float* sw2 = sD1 + 2 * EV * ldz;              // [ldz]
     float* sg = sw2 + ldz;                            // [2 EV]
     float* sdD1 = sZ;
     __shared__ __align__(8) std::uint64_t bar;
-    const int i0 = blockIdx.x * kDecEv;
-    const int nev = min(kDecEv, B - i0);
+    const int i0 = blockIdx.x * EV;
+    const int nev = min(EV, B - i0);
     const int tid = threadIdx.x, nt = blockDim.x;
     // stage the weight rows (cols 0 .. 2D+3: W_a | W_b | b1 | pad) and the
     // block's embedding rows with TMA bulk copies issued by warp 0 on one mbarrier
@@ -414,13 +414,13 @@ __global__ void __launch_bounds__(MAXT, MINB)
             bulk_g2s(sW + (std::size_t)n * ldw, W1 + (std::size_t)n * ld1, unsigned(ldw * 4), &bar);
         for (int r = tid; r < 3 * nev; r += 32) {
             const int kind = r / nev, e = r % nev;
-            bulk_g2s(sZ + (std::size_t)(kind * kDecEv + e) * ldz, emb + ((std::size_t)kind * B + i0 + e) * D,
+            bulk_g2s(sZ + (std::size_t)(kind * EV + e) * ldz, emb + ((std::size_t)kind * B + i0 + e) * D,
                      unsigned(D * 4), &bar);
         }
     }
-    for (int i = tid; i < 3 * (kDecEv - nev) * D; i += nt) {  // rows past the batch: zero
-        const int r = i / D, kind = r / (kDecEv - nev), e = nev + r % (kDecEv - nev);
-        sZ[(std::size_t)(kind * kDecEv + e) * ldz + i % D] = 0.f;
+    for (int i = tid; i < 3 * (EV - nev) * D; i += nt) {  // rows past the batch: zero
+        const int r = i / D, kind = r / (EV - nev), e = nev + r % (EV - nev);
+        sZ[(std::size_t)(kind * EV + e) * ldz + i % D] = 0.f;
     }
     for (int i = tid; i <= D; i += nt) sw2[i] = w2[i];
     __syncthreads();  // (barrier initialised before anyone waits)
@@ -429,15 +429,15 @@ __global__ void __launch_bounds__(MAXT, MINB)
     if (tid < 3 * D) {
         const int kind = tid / D, n = tid % D;
         const float* wr = sW + (std::size_t)n * ldw + (kind ? D : 0);
-        const float* z = sZ + (std::size_t)kind * kDecEv * ldz;
-        float acc[kDecEv];
+        const float* z = sZ + (std::size_t)kind * EV * ldz;
+        float acc[EV];
 #pragma unroll
-        for (int e = 0; e < kDecEv; ++e) acc[e] = 0.f;
+        for (int e = 0; e < EV; ++e) acc[e] = 0.f;
 #pragma unroll 2
         for (int k = 0; k < D; k += 4) {
             const float4 w = *reinterpret_cast<const float4*>(wr + k);
 #pragma unroll
-            for (int e = 0; e < kDecEv; ++e) {
+            for (int e = 0; e < EV; ++e) {
                 const float4 x = *reinterpret_cast<const float4*>(z + (std::size_t)e * ldz + k);
                 acc[e] = fmaf(x.x, w.x, acc[e]);
                 acc[e] = fmaf(x.y, w.y, acc[e]);
@@ -446,29 +446,29 @@ __global__ void __launch_bounds__(MAXT, MINB)
             }
         }
 #pragma unroll
-        for (int e = 0; e < kDecEv; ++e) sY[(std::size_t)(kind * kDecEv + e) * ldz + n] = acc[e];
+        for (int e = 0; e < EV; ++e) sY[(std::size_t)(kind * EV + e) * ldz + n] = acc[e];
     }
     __syncthreads();
     // D1 rows: p < EV positive (src, dst), p >= EV negative (src, neg)
-    for (int i = tid; i < 2 * kDecEv * D; i += nt) {
-        const int p = i / D, n = i % D, e = p % kDecEv;
-        const float v = sY[(std::size_t)e * ldz + n] + sY[(std::size_t)((p < kDecEv ? 1 : 2) * kDecEv + e) * ldz + n] +
+    for (int i = tid; i < 2 * EV * D; i += nt) {
+        const int p = i / D, n = i % D, e = p % EV;
+        const float v = sY[(std::size_t)e * ldz + n] + sY[(std::size_t)((p < EV ? 1 : 2) * EV + e) * ldz + n] +
                         sW[(std::size_t)n * ldw + 2 * D];
         const float x = fmaxf(v, 0.f);
         sD1[(std::size_t)p * ldz + n] = x;
-        if (bwd && e < nev) D1[(std::size_t)((p < kDecEv ? 0 : B) + i0 + e) * d.ld_d1 + n] = x;
+        if (bwd && e < nev) D1[(std::size_t)((p < EV ? 0 : B) + i0 + e) * d.ld_d1 + n] = x;
     }
     __syncthreads();
     // logits and BCE terms: one warp per pair row
     {
         const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-        for (int p = warp; p < 2 * kDecEv; p += nw) {
-            const int e = p % kDecEv;
+        for (int p = warp; p < 2 * EV; p += nw) {
+            const int e = p % EV;
             const float* x = sD1 + (std::size_t)p * ldz;
             float acc = 0.f;
             for (int c = lane; c < D; c += 32) acc += x[c] * sw2[c];
             acc = warp_sum(acc) + sw2[D];
-            const bool pos = p < kDecEv;
+            const bool pos = p < EV;
             const float g = (sigmoidf_(acc) - (pos ? 1.f : 0.f)) / (float)B;
             if (lane == 0) {
                 sg[p] = g;
@@ -483,30 +483,30 @@ __global__ void __launch_bounds__(MAXT, MINB)
     }
     if (!bwd) return;
     __syncthreads();
-    for (int i = tid; i < 2 * kDecEv * D; i += nt) {  // dD1 -> global (the weight gradients' input)
-        const int p = i / D, n = i % D, e = p % kDecEv;
+    for (int i = tid; i < 2 * EV * D; i += nt) {  // dD1 -> global (the weight gradients' input)
+        const int p = i / D, n = i % D, e = p % EV;
         const float v = sD1[(std::size_t)p * ldz + n] > 0.f ? sg[p] * sw2[n] : 0.f;
         sD1[(std::size_t)p * ldz + n] = v;  // (D1 itself is no longer read)
-        if (e < nev) dD1[(std::size_t)((p < kDecEv ? 0 : B) + i0 + e) * D + n] = v;
+        if (e < nev) dD1[(std::size_t)((p < EV ? 0 : B) + i0 + e) * D + n] = v;
     }
     __syncthreads();
     // data gradients, as the oracle's autograd forms them (two decoder calls,
     // pos and neg): thread (q, k), q = 0 dD1_pos W_a, 1 dD1_neg W_a, 2 dD1_pos W_b,
     // 3 dD1_neg W_b; d_src = q0 + q1 (summed through shared memory over the
     // z rows, no longer read), d_dst = q2, d_neg = q3
-    float acc[kDecEv];
+    float acc[EV];
     const int q = tid / D, k = tid % D;
     if (tid < 4 * D) {
         const float* wc = sW + (q >= 2 ? D : 0) + k;  // column k of W_a / W_b
-        const float* g = sD1 + (std::size_t)(q & 1) * kDecEv * ldz;
+        const float* g = sD1 + (std::size_t)(q & 1) * EV * ldz;
 #pragma unroll
-        for (int e = 0; e < kDecEv; ++e) acc[e] = 0.f;
+        for (int e = 0; e < EV; ++e) acc[e] = 0.f;
 #pragma unroll 2
         for (int n = 0; n < D; n += 4) {
             const float w0 = wc[(std::size_t)n * ldw], w1 = wc[(std::size_t)(n + 1) * ldw],
                         w2_ = wc[(std::size_t)(n + 2) * ldw], w3 = wc[(std::size_t)(n + 3) * ldw];
 #pragma unroll
-            for (int e = 0; e < kDecEv; ++e) {
+            for (int e = 0; e < EV; ++e) {
                 const float4 x = *reinterpret_cast<const float4*>(g + (std::size_t)e * ldz + n);
                 acc[e] = fmaf(x.x, w0, acc[e]);
                 acc[e] = fmaf(x.y, w1, acc[e]);
@@ -516,13 +516,13 @@ __global__ void __launch_bounds__(MAXT, MINB)
         }
         if (q == 1)
 #pragma unroll
-            for (int e = 0; e < kDecEv; ++e) sdD1[(std::size_t)e * ldz + k] = acc[e];
+            for (int e = 0; e < EV; ++e) sdD1[(std::size_t)e * ldz + k] = acc[e];
     }
     __syncthreads();
     if (tid < 4 * D && q != 1) {
         const int kind = q == 0 ? 0 : q - 1;
 #pragma unroll
-        for (int e = 0; e < kDecEv; ++e) {
+        for (int e = 0; e < EV; ++e) {
             const float v = q == 0 ? acc[e] + sdD1[(std::size_t)e * ldz + k] : acc[e];
             if (e < nev) d_emb[((std::size_t)kind * B + i0 + e) * D + k] = rnd_if(v, d.rnd);
         }
@@ -535,7 +535,10 @@ __global__ void __launch_bounds__(MAXT, MINB)
 //   db1 += sum dD1_pos + sum dD1_neg,            dw2 += dlogit^T [D1 | 1]
 // (the MergeLayer weight gradient of oracle/tgn_oracle.py by input halves);
 // k_dec_wgrad_reduce adds the partials in block order to the gradients.
-// Thread (tn, tk) of 16 x 16 owns rows tn + 16 i, columns tk + 16 j.
+// blockIdx.y = (row half rs, input half): the block's 16 x 16 threads own
+// rows tn + 16 (4 rs + i), columns half * D + tk + 16 j of dW1 (the same
+// per-element summation order as one block per chunk, with 4x the blocks:
+// a B = 200 batch has only 7 chunks).
 __global__ void __launch_bounds__(256) k_dec_wgrad_part(Dims d, int B, const float* emb,
                                                         const float* dD1, const float* dlogit,
                                                         const float* D1, float* part) {
@@ -549,11 +552,12 @@ __global__ void __launch_bounds__(256) k_dec_wgrad_part(Dims d, int B, const flo
     const int tid = threadIdx.x, D4 = D / 4;
     float* out = part + (std::size_t)blockIdx.x * (D * (2 * D + 1) + D + 1);
     const int tn = tid >> 4, tk = tid & 15;
-    constexpr int TI = 7, TJ = 7;  // rows / columns per thread (D <= 112)
+    constexpr int TI = 4, TJ = 7;  // rows / columns per thread (D <= 112)
+    const int half = blockIdx.y & 1, rb = 16 * TI * (blockIdx.y >> 1);  // input half, first row
     // the positive and the negative decoder call accumulate separately and
     // are added at the end (the oracle's autograd sums the two calls' grads);
     // the block's events stream through shared memory kDecWgTile at a time
-    for (int half = 0; half < 2; ++half) {
+    if (rb < D) {
         float ap[TI][TJ], an[TI][TJ];
 #pragma unroll
         for (int i = 0; i < TI; ++i)
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(256) k_dec_wgrad_part(Dims d, int B, const flo
                 float gp[TI], gn[TI], zp[TJ], zn[TJ];
 #pragma unroll
                 for (int i = 0; i < TI; ++i) {
-                    const int n = min(tn + 16 * i, D - 1);
+                    const int n = min(rb + tn + 16 * i, D - 1);
                     gp[i] = sgp[e * ld + n];
                     gn[i] = sgn[e * ld + n];
                 }
@@ -601,11 +605,13 @@ __global__ void __launch_bounds__(256) k_dec_wgrad_part(Dims d, int B, const flo
         for (int i = 0; i < TI; ++i)
 #pragma unroll
             for (int j = 0; j < TJ; ++j) {
-                const int n = tn + 16 * i, k = tk + 16 * j;
+                const int n = rb + tn + 16 * i, k = tk + 16 * j;
                 if (n < D && k < D) out[(std::size_t)n * (2 * D + 1) + half * D + k] = ap[i][j] + an[i][j];
             }
     }
-    // bias columns: db1 (column 2D of dW1) and dw2 (incl. db2), straight from global
+    if (blockIdx.y > 1) return;
+    // bias columns: db1 (column 2D of dW1; y = 0) and dw2 (incl. db2; y = 1), straight from global
+    if (blockIdx.y == 0)
     for (int n = tid; n < D; n += blockDim.x) {
         float a = 0.f, b = 0.f;
         for (int e = c0; e < c1; ++e) {
@@ -614,6 +620,7 @@ __global__ void __launch_bounds__(256) k_dec_wgrad_part(Dims d, int B, const flo
         }
         out[(std::size_t)n * (2 * D + 1) + 2 * D] = a + b;
     }
+    if (blockIdx.y == 1)
     for (int c = tid; c <= D; c += blockDim.x) {
         float a = 0.f, b = 0.f;
         for (int e = c0; e < c1; ++e) {
@@ -638,15 +645,20 @@ __global__ void k_dec_wgrad_reduce(Dims d, int nblk, const float* part, float* g
 
 std::size_t dec_wgrad_smem_bytes(const Dims& d) { return 4 * std::size_t(5) * kDecWgTile * (d.D + 4); }
 
-// 416 threads (d_mem <= 104) at two blocks per SM (<= 72 registers), else one
-template __global__ void k_decoder<416, 2>(Dims, int, const float*, const float*, int, const float*,
-                                           float*, float*, float*, float*, float*, float*, int);
-template __global__ void k_decoder<768, 1>(Dims, int, const float*, const float*, int, const float*,
-                                           float*, float*, float*, float*, float*, float*, int);
+// 416 threads (d_mem <= 104) at two blocks per SM (<= 72 registers), else one;
+// 8 events per block, 4 for small batches
+#define SPD_DEC_INST(T, M, E)                                                                          \
+    template __global__ void k_decoder<T, M, E>(Dims, int, const float*, const float*, int, const float*, \
+                                                float*, float*, float*, float*, float*, float*, int);
+SPD_DEC_INST(416, 2, kDecEv)
+SPD_DEC_INST(416, 2, kDecEvSmall)
+SPD_DEC_INST(768, 1, kDecEv)
+SPD_DEC_INST(768, 1, kDecEvSmall)
+#undef SPD_DEC_INST
 
-std::size_t decoder_smem_bytes(const Dims& d) {
+std::size_t decoder_smem_bytes(const Dims& d, int ev) {
     const std::size_t D = d.D, ldw = 2 * D + 4, ldz = D + 4;
-    return 4 * (D * ldw + 8 * kDecEv * ldz + ldz + 2 * kDecEv);
+    return 4 * (D * ldw + 8 * ev * ldz + ldz + 2 * ev);
 }
 
 // Fixed-order single-block sum (deterministic loss).

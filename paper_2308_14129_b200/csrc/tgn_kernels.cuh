@@ -147,13 +147,15 @@ __global__ void k_dec_head(Dims d, int B, const float* D1, const float* w2, floa
 __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, const float* W1,
                             int ld1, const float* w2, float* D1, float* dlogit, float* lossv,
                             float* dD1, float* logits);
-constexpr int kDecEv = 8;  // events per k_decoder block
+constexpr int kDecEv = 8;       // events per k_decoder block
+constexpr int kDecEvSmall = 4;  // ... for batches of <= kDecSmallB events (twice the blocks)
+constexpr int kDecSmallB = 1024;
 // k_decoder launches roundup(4 d_mem, 32) threads (<= 768: d_mem <= 192)
-template <int MAXT, int MINB>
+template <int MAXT, int MINB, int EV>
 __global__ void k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2,
                           float* D1, float* dlogit, float* lossv, float* dD1, float* logits,
                           float* d_emb, int bwd);
-std::size_t decoder_smem_bytes(const Dims& d);
+std::size_t decoder_smem_bytes(const Dims& d, int ev);
 // k_dec_wgrad_part: events per block and per shared-memory tile (128-event
 // blocks — 16 long-running blocks — took 176 us on the side stream and moved
 // the Wiki test AUC from 0.0028 to 0.0050 off the oracle: the chunk order

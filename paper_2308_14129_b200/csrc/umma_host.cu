@@ -337,15 +337,18 @@ void gru_fused_t(const float* x, int ldx, int K1, const float* h, int ldh, int K
     SPD_CUDA(cudaGetLastError());
 }
 
-// UB (memory units per CTA) from SPD_GRU_UB (16 or 32; default kGruUB)
+// UB (memory units per CTA): 16 for small pending sets (<= 1,024 rows: twice
+// the CTAs of a latency-bound launch; Reddit / LastFM B = 200 GRU 27.6 -> 24
+// us), else kGruUB (GDELT: 32 measured faster); SPD_GRU_UB = 16 | 32 overrides
 void gru_fused(const float* x, int ldx, int K1, const float* h, int ldh, int K2, const float* Wih,
                int ldwih, const float* Whh, int ldwhh, int D, int M, const int* M_dev,
                const float* mem, const std::uint32_t* nodes, float* mem_new, float* save,
                cudaStream_t s) {
-    static const int ub = [] {
+    static const int forced = [] {
         const char* e = std::getenv("SPD_GRU_UB");
-        return e && std::atoi(e) == 16 ? 16 : kGruUB;
+        return e ? std::atoi(e) : 0;
     }();
+    const int ub = forced == 16 || forced == 32 ? forced : M <= 1024 ? 16 : kGruUB;
     if (ub == 16)
         gru_fused_t<16>(x, ldx, K1, h, ldh, K2, Wih, ldwih, Whh, ldwhh, D, M, M_dev, mem, nodes, mem_new, save, s);
     else
