@@ -333,9 +333,18 @@ void dh_index(const tgnk::WorkerDev& wd, const Scratch& s, cudaStream_t st) {
     launch(tgnk::k_dh_scan, 1, 1024, 0, st, s.dh);
     launch(tgnk::k_dh_scatter, nb, tgnk::kDhBlock, sm, st, wd, s.dh);
 }
+// grid cap of k_dh_pull (grid-stride; SPD_DHPULL_CTAS, default 148: one
+// 8-warp block per SM; 296 / 592 run it faster but slow the dQ GEMMs beside
+// it: 0.351 / 0.350 vs 0.337 ms per GDELT step)
+std::size_t dhpull_ctas() {
+    static const std::size_t v = [] {
+        const char* e = std::getenv("SPD_DHPULL_CTAS");
+        return e ? std::size_t(std::atol(e)) : std::size_t(148);
+    }();
+    return v;
+}
 void dh_pull(const tgnk::Dims& d, const Scratch& s, cudaStream_t st) {
-    // grid-stride, at most one 8-warp block per SM
-    const unsigned grid = unsigned(std::min<std::size_t>((std::size_t(s.dh_max_chunks) * 32 + 255) / 256, 148));
+    const unsigned grid = unsigned(std::min<std::size_t>((std::size_t(s.dh_max_chunks) * 32 + 255) / 256, dhpull_ctas()));
     auto go = [&](auto k) {
         launch(k, grid, 256, 0, st, s.dh, d, static_cast<const float*>(s.alpha.p),
                static_cast<const float*>(s.dsc.p), static_cast<const float*>(s.dxbar.p),
@@ -565,7 +574,13 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.troot_blocks = (R + s.trows - 1) / s.trows;
     // k_attn_time_grad: grid-stride over the roots on one block per SM (a
     // side kernel; full grids crowded the query backward's GEMMs off the SMs)
-    s.tattn_blocks = std::min((R + tgnk::attn_x_roots_per_block() - 1) / tgnk::attn_x_roots_per_block(), 148);
+    // (grid cap of the attention time-encoder partials, SPD_TATTN_CTAS: 296
+    // measured 0.3346 vs 0.3366 ms per GDELT step against 148)
+    static const int tattn_cap = [] {
+        const char* e = std::getenv("SPD_TATTN_CTAS");
+        return e ? std::atoi(e) : 296;
+    }();
+    s.tattn_blocks = std::min((R + tgnk::attn_x_roots_per_block() - 1) / tgnk::attn_x_roots_per_block(), tattn_cap);
     s.tpart.alloc(std::size_t(s.troot_blocks + s.tattn_blocks) * 2 * d.T);
     s.dh.nbr_node = s.nbr_node.p; s.dh.cnt = s.cnt.p; s.dh.roots = s.roots.p;
     {
