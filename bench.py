@@ -320,9 +320,10 @@ def main():
     ap.add_argument("--concurrent", action="store_true",
                     help="with --parts > --gpus: a GPU's partitions train concurrently (one "
                          "stream set and parameter replica each, in-process peer all-reduce)")
-    ap.add_argument("--backbone", default="tgn", choices=["tgn", "jodie"],
-                    help="memory-based TIG model: TGN (GRU + temporal attention) or JODIE "
-                         "(RNN + time projection), PAPER.md:373")
+    ap.add_argument("--backbone", default="tgn", choices=["tgn", "jodie", "dyrep"],
+                    help="memory-based TIG model: TGN (GRU + temporal attention), JODIE "
+                         "(RNN + time projection) or DyRep (RNN + attention-embedding "
+                         "messages), PAPER.md:373")
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="N>1 gradient all-reduce: peer = fused into Adam over CUDA-IPC-mapped "
                          "peer HBM (NVLink); nccl = ncclAllReduce then Adam")
@@ -374,7 +375,7 @@ def main():
     mine = list(range(rank * (P // world), (rank + 1) * (P // world)))  # this rank's partitions
     D = T = 100
     K, H = 10, 2
-    model = "TGN" if args.backbone == "tgn" else "JODIE"
+    model = {"tgn": "TGN", "jodie": "JODIE", "dyrep": "DyRep"}[args.backbone]
     cfg_desc = {"workload": f"{args.config}-shape synthetic TIG ({N} nodes, {E} edges, d_e={F}), "
                             f"{model} d_mem=d_time=100 k={K} heads={H}, B={B}, SEP P={P}"
                             + (f" k_hub={args.hub_k}" if args.hub_k != 0.05 else ""),
@@ -416,7 +417,7 @@ def main():
     subs_mine = [wl["subs"][w] for w in mine]
     sub_mine = subs_mine[0]
     cfg = sp.TGNConfig(d_mem=D, d_time=T, d_edge=F, n_neighbors=K, n_heads=H, batch_size=B, lr=1e-4,
-                       gemm_mode=args.gemm_mode, backbone=0 if args.backbone == "tgn" else 1,
+                       gemm_mode=args.gemm_mode, backbone={"tgn": 0, "jodie": 1, "dyrep": 2}[args.backbone],
                        concurrent=1 if args.concurrent else 0)
     nccl_id = None
     if world > 1 and args.transport == "nccl":

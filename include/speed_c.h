@@ -278,7 +278,9 @@ typedef struct spd_tgn_config {
     int32_t sync_average;/* epoch-end shared-node sync: 1 average (default), 0 max-ts */
     int32_t gemm_mode;   /* 0 = FP32 FFMA, 1 = tcgen05 TF32 for the GRU and attention projections (tolerance-gated) */
     int32_t backbone;    /* 0 = TGN (GRU memory, temporal attention); 1 = JODIE (RNN memory,
-                          * time-projection embedding: PAPER.md:373's other backbones) */
+                          * time-projection embedding); 2 = DyRep (RNN memory, identity
+                          * embedding, attention-embedding messages): PAPER.md:373's
+                          * other backbones */
     int32_t concurrent;  /* 1: a process's local workers (several SEP partitions on one GPU,
                           * world 1) train concurrently, each on its own streams with its own
                           * scratch and parameter replica; gradients meet in the fused
@@ -365,6 +367,16 @@ spd_status spd_tgn_set_eval_events(spd_tgn_trainer* t, int32_t worker, const spd
                                    const uint64_t* eids, uint64_t n);
 spd_status spd_tgn_evaluate(spd_tgn_trainer* t, int32_t worker, uint64_t lo, uint64_t hi,
                             uint64_t neg_seed, float* pos_scores, float* neg_scores);
+
+/* Global link-prediction metrics over the scores of every partition / rank
+ * (SURVEY §8e(3)): the caller concatenates the routed edges' positive and
+ * negative scores of all partitions (spd_tgn_evaluate on each rank, then an
+ * all-gather); AP = sum_g (R_g - R_{g-1}) P_g over descending score groups,
+ * AUC = trapezoidal ROC area (ties one half) — sklearn's
+ * average_precision_score / roc_auc_score. Data error on empty lists or NaN.
+ * Routing reference: assign_eval_edges, partitioner.cpp:212-242. */
+spd_status spd_link_metrics(const float* pos, uint64_t n_pos, const float* neg, uint64_t n_neg,
+                            double* ap, double* auc);
 
 /* Introspection for parity tests. */
 spd_status spd_tgn_param_count(const spd_tgn_trainer* t, uint64_t* n);

@@ -40,6 +40,15 @@ that the paper leaves open are fixed here once, and the CUDA path follows them:
     this batch's memory update; log1p keeps raw timestamp gaps of up to 1e8 in
     range where JODIE normalises them by dataset statistics); no attention or
     merge layers; the same decoder and loss.
+  * backbone = 2, DyRep (the TGN framework's DyRep row: RNN
+    memory updater, identity embedding, attention message function): the
+    same RNN updater as JODIE; the decoder reads the roots' (updated) memory
+    rows directly (identity embedding); the message of endpoint i of event
+    (i, j) is [s_i || z_j || e_ij || phi(t - t_i^-)] where z_j is j's
+    temporal-attention embedding (the TGN attention layer + MergeLayer above,
+    over the updated memory) at the event's batch, stored with the pending
+    message. Message inputs are detached (as for every backbone), so the
+    attention parameters carry no gradient; they shape the messages only.
 """
 from __future__ import annotations
 
@@ -116,7 +125,7 @@ class TGNConfig:
     seed_feat: int = 2
     seed_neg: int = 4
     sync_average: int = 1
-    backbone: int = 0  # 0 TGN, 1 JODIE
+    backbone: int = 0  # 0 TGN, 1 JODIE, 2 DyRep
 
 
 def ld_aug(k: int) -> int:
@@ -130,12 +139,14 @@ def linear_specs(c: TGNConfig):
     [W | b | 0-pad] matrix of row stride ld_aug(K)."""
     D, T, F = c.d_mem, c.d_time, c.d_edge
     DQ, DK, DM = D + T, D + F + T, 2 * D + F + T
-    t = c.backbone == 0  # JODIE: one RNN gate block, no attention / merge rows, time projection
-    return [("gru_ih", 3 * D if t else D, DM, D), ("gru_hh", 3 * D if t else D, D, D),
+    g = c.backbone == 0  # GRU (TGN) or one RNN gate block (JODIE, DyRep)
+    t = c.backbone != 1  # attention + merge rows (TGN, DyRep's message embedding)
+    j = c.backbone == 1  # JODIE's time projection
+    return [("gru_ih", 3 * D if g else D, DM, D), ("gru_hh", 3 * D if g else D, D, D),
             ("att_q", DQ if t else 0, DQ, DQ), ("att_kv", 2 * DQ if t else 0, DK, DK),
             ("att_o", DQ if t else 0, DQ, DQ), ("mrg1", D if t else 0, DQ + D, DQ + D),
             ("mrg2", D if t else 0, D, D), ("dec1", D, 2 * D, 2 * D), ("dec2", 1, D, D),
-            ("tproj", 0 if t else D, 1, D)]
+            ("tproj", D if j else 0, 1, D)]
 
 
 def param_layout(c: TGNConfig):
@@ -282,7 +293,7 @@ class TGNOracle:
     def _gru(self, P, x, h):
         gi = x @ P["gru_w_ih"].T + P["gru_b_ih"]
         gh = h @ P["gru_w_hh"].T + P["gru_b_hh"]
-        if self.c.backbone == 1:  # JODIE: RNN cell
+        if self.c.backbone != 0:  # JODIE, DyRep: RNN cell
             return torch.tanh(gi + gh)
         D = self.c.d_mem
         r = torch.sigmoid(gi[:, :D] + gh[:, :D])
@@ -299,7 +310,11 @@ class TGNOracle:
         ts = np.array([pend[u][2] for u in U])
         with torch.no_grad():
             phi = time_enc(P["time_w"], P["time_b"], ts - self.lu[w][U])
-        x = torch.cat([mem[U], mem[other], wd.feat[ev], phi], 1).detach()
+        if self.c.backbone == 2:  # DyRep: the other endpoint's attention embedding
+            zo = torch.stack([pend[u][3] for u in U]) if len(U) else torch.zeros(0, self.c.d_mem)
+        else:
+            zo = mem[other]
+        x = torch.cat([mem[U], zo, wd.feat[ev], phi], 1).detach()
         return x, mem[U].detach(), ts
 
     def _embed_jodie(self, w, P, memx, roots, t_roots, upd):
@@ -316,6 +331,22 @@ class TGNOracle:
     def _embed(self, w, P, memx, roots, t_roots, data=None, upd=None):
         if self.c.backbone == 1:
             return self._embed_jodie(w, P, memx, roots, t_roots, upd)
+        if self.c.backbone == 2:  # DyRep: identity embedding
+            R = len(roots)
+            return memx[roots], np.full((R, self.c.n_neighbors), -1, np.int64), np.zeros(R, np.int64)
+        return self._embed_attn(w, P, memx, roots, t_roots, data)
+
+    def _msg_embed(self, w, P, memx, src, dst, ts, data=None):
+        """DyRep: attention embeddings of the batch's sources then destinations
+        (no gradient), the payload of the messages stored after the batch."""
+        if self.c.backbone != 2:
+            return None
+        with torch.no_grad():
+            z, _, _ = self._embed_attn(w, P, memx.detach(), np.concatenate([src, dst]),
+                                       np.concatenate([ts, ts]), data)
+        return z
+
+    def _embed_attn(self, w, P, memx, roots, t_roots, data=None):
         c, wd = self.c, (self.W[w] if data is None else data)
         D, T, K, H = c.d_mem, c.d_time, c.n_neighbors, c.n_heads
         R = len(roots)
@@ -374,11 +405,14 @@ class TGNOracle:
         self.lu[w][U] = ts
         self.pend[w] = {}
 
-    def _store_pending(self, w, src, dst, ts, ev):
+    def _store_pending(self, w, src, dst, ts, ev, z=None):
         pend = {}
-        for k in range(len(src)):  # later events overwrite: last-message wins
-            pend[int(src[k])] = (int(dst[k]), int(ev[k]), float(ts[k]))
-            pend[int(dst[k])] = (int(src[k]), int(ev[k]), float(ts[k]))
+        B = len(src)
+        for k in range(B):  # later events overwrite: last-message wins
+            zs = None if z is None else z[B + k]  # the source's message carries z_dst
+            zd = None if z is None else z[k]
+            pend[int(src[k])] = (int(dst[k]), int(ev[k]), float(ts[k]), zs)
+            pend[int(dst[k])] = (int(src[k]), int(ev[k]), float(ts[k]), zd)
         self.pend[w] = pend
 
     def batches(self, w):
@@ -444,17 +478,21 @@ class TGNOracle:
             roots = np.concatenate([src, dst, neg])
             emb, ids, cnt = self._embed(w, P, memx, roots, np.concatenate([ts, ts, ts]),
                                         upd=(U, mts if len(U) else None))
+            zmsg = self._msg_embed(w, P, memx, src, dst, ts)
             pos_l = self._decode(P, emb[:B], emb[B:2 * B])
             neg_l = self._decode(P, emb[:B], emb[2 * B:])
             loss = torch.nn.functional.softplus(-pos_l).mean() + torch.nn.functional.softplus(neg_l).mean()
-            g, = torch.autograd.grad(loss, flat)
+            g, = torch.autograd.grad(loss, flat, allow_unused=True)
+            if g is None:
+                g = torch.zeros(self.total)
             grads += g
             n_active += 1
             losses.append(float(loss.detach()))
             self.last[w] = dict(emb=emb.detach().numpy(), neg=neg, nbr_ids=ids, cnt=cnt,
                                 loss=float(loss.detach()), U=U, memx=memx.detach().numpy(),
                                 post=(U, hn.detach() if len(U) else None,
-                                      mts if len(U) else None, src, dst, ts, lo, hi))
+                                      mts if len(U) else None, src, dst, ts, lo, hi),
+                                zmsg=zmsg)
         # gradient mean over ALL workers (an idle worker contributes zeros)
         self.grad = grads / len(self.W)
         self._adam(self.grad)
@@ -467,7 +505,7 @@ class TGNOracle:
                 if len(U):
                     self.mem[w][U] = hn
                     self.lu[w][U] = mts
-            self._store_pending(w, src, dst, ts, np.arange(lo, hi))
+            self._store_pending(w, src, dst, ts, np.arange(lo, hi), self.last[w]["zmsg"])
             self.pos[w] += 1
             if self.pos[w] == self.batches(w):  # loop_end: flush (new params), snapshot
                 self._flush(w, P_new)
@@ -558,10 +596,11 @@ class TGNOracle:
                     memx[U] = hn
                 emb, _, _ = self._embed(w, P, memx, np.concatenate([src, dst, ng]),
                                         np.concatenate([ts, ts, ts]), X, upd=(U, mts if len(U) else None))
+                zmsg = self._msg_embed(w, P, memx, src, dst, ts, X)
                 pos.append(self._decode(P, emb[:n], emb[n:2 * n]).numpy())
                 neg.append(self._decode(P, emb[:n], emb[2 * n:]).numpy())
                 if len(U):
                     self.mem[w][U] = hn
                     self.lu[w][U] = mts
-                self._store_pending(w, src, dst, ts, np.arange(k0, k0 + n))
+                self._store_pending(w, src, dst, ts, np.arange(k0, k0 + n), zmsg)
         return np.concatenate(pos), np.concatenate(neg)

@@ -404,6 +404,42 @@ def assign_eval_edges(split: ChronoSplit, pa: PartitionAssignment) -> EvalRoutin
 
 
 # ------------------------------------------------------------- subgraphs
+
+def link_metrics(pos, neg) -> tuple[float, float]:
+    """Global (AP, AUC) of link-prediction scores (spd_link_metrics): positive
+    and negative scores of the routed val / test edges, concatenated over
+    every partition."""
+    p = np.ascontiguousarray(pos, dtype=np.float32).ravel()
+    n = np.ascontiguousarray(neg, dtype=np.float32).ravel()
+    ap, auc = C.c_double(), C.c_double()
+    _check(lib.spd_link_metrics(ptr(p, C.c_float), len(p), ptr(n, C.c_float), len(n),
+                                C.byref(ap), C.byref(auc)))
+    return ap.value, auc.value
+
+
+def gather_link_metrics(pos, neg, allgather=None) -> tuple[float, float]:
+    """Multi-rank evaluation: every rank scores the eval edges
+    routed to its partitions (TGNTrainer.evaluate); the score lists of all
+    ranks are gathered in rank order and the global AP / AUC computed once.
+
+    ``allgather(obj) -> list`` collects one object per rank; by default
+    torch.distributed's all_gather_object when a process group is initialised
+    (the launcher's plumbing), else the local lists alone (one rank)."""
+    mine = (np.asarray(pos, np.float32).ravel(), np.asarray(neg, np.float32).ravel())
+    if allgather is None:
+        try:
+            import torch.distributed as dist
+            ready = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+        except ImportError:
+            ready = False
+        if ready:
+            def allgather(obj):
+                out = [None] * dist.get_world_size()
+                dist.all_gather_object(out, obj)
+                return out
+    parts = allgather(mine) if allgather is not None else [mine]
+    return link_metrics(np.concatenate([p for p, _ in parts]), np.concatenate([n for _, n in parts]))
+
 @dataclass
 class SubGraph:  # pac_sim.hpp:12-15 (+ stream positions for feature lookup)
     nodes: np.ndarray
@@ -731,7 +767,7 @@ class TGNConfig:
     seed_neg: int = 4
     sync_average: int = 1
     gemm_mode: int = 0
-    backbone: int = 0  # 0 TGN, 1 JODIE
+    backbone: int = 0  # 0 TGN, 1 JODIE, 2 DyRep
     concurrent: int = 0  # 1: local workers train concurrently (world 1)
 
     def c(self) -> TGNConfigC:

@@ -83,6 +83,7 @@ _SIGS = {
     "spd_assign_eval_edges": (i32, [P, u64, P, u64, P, PP]),
     "spd_eval_routing_counts": (i32, [P, i32, pu64, pu64]),
     "spd_eval_routing_edges": (i32, [P, i32, pu64]),
+    "spd_link_metrics": (i32, [pf32, u64, pf32, u64, pf64, pf64]),
     "spd_eval_routing_destroy": (None, [P]),
     "spd_induce_subgraphs": (i32, [P, u64, u32, pu64, pi32, u32, i32, PP]),
     "spd_induce_groups": (i32, [P, u64, u32, pu64, pu32, i32, pu64, pu32, i32, PP, pu64]),

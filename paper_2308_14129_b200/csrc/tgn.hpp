@@ -70,6 +70,7 @@ struct Worker {
     struct PendingSet {
         DevBuf<std::uint32_t> pU, pOther, pEv;
         DevBuf<double> pTs;
+        DevBuf<float> pZ;         // DyRep: the other endpoint's attention embedding (<= 2B x D)
         DevBuf<std::int32_t> nU;  // device-resident |pending|
     } pend[2];
     int cur = 0;
@@ -240,6 +241,7 @@ private:
     void decode(int B, bool train);                // k_decoder (fwd, loss, data gradient)
     void decoder_wgrads(cudaEvent_t at, int B);    // decoder weight gradients (side streams)
     void jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool train, int slot_idx, bool post);
+    void dyrep_messages(const tgnk::WorkerDev& wd, int B, bool train);
     void worker_post(Worker& w);
     void loop_end_flush(Worker& w);
     void flush_pending(Worker& w);
@@ -287,6 +289,7 @@ private:
     cudaEvent_t ev_zfork_ = nullptr, ev_zero_ = nullptr;
     cudaEvent_t ev_bwdx_ = nullptr;  // attention time-encoder partials done
     cudaEvent_t ev_pull_ = nullptr;  // dH chunk partials done (tgn_dh.cu)
+    cudaEvent_t ev_pend_ = nullptr;  // (DyRep) this batch's last messages selected
     bool scratch_zeroed_ = false;    // dGi/dGh cleared by this step's k_zero_list
     bool gru_fused_ = true;          // gemm_mode 1: fused tcgen05 GRU (SPD_GRU_FUSED=0: two GEMMs + cell)
 

@@ -130,7 +130,9 @@ __global__ void k_gru_gather(WorkerDev w, Dims d, const float* time_w, const flo
     float* xr = x + (std::size_t)u * d.ld_x;
     float* hr = h + (std::size_t)u * d.ld_h;
     const float4* mn = reinterpret_cast<const float4*>(w.mem + (std::size_t)node * d.D);
-    const float4* mo = reinterpret_cast<const float4*>(w.mem + (std::size_t)other * d.D);
+    // (DyRep: the other endpoint's attention embedding stored with the message)
+    const float4* mo = reinterpret_cast<const float4*>(w.pZ ? w.pZ + (std::size_t)u * d.D
+                                                            : w.mem + (std::size_t)other * d.D);
     for (int c4 = lane; c4 < d.D / 4; c4 += 32) {
         const float4 v = rnd4_if(__ldg(mn + c4), d.rnd);
         reinterpret_cast<float4*>(xr)[c4] = v;
@@ -223,10 +225,33 @@ __global__ void k_jodie_embed(WorkerDev w, Dims d, int R, const std::uint32_t* r
     const int sl = w.slot[n];
     const float* m = sl >= 0 ? mem_new + (std::size_t)sl * d.D : w.mem + (std::size_t)n * d.D;
     const double last = sl >= 0 ? w.pTs[sl] : w.lu[n];
+    if (!tp) {  // DyRep: identity embedding (128-bit rows, D % 4 == 0)
+        for (int c4 = lane; c4 < d.D / 4; c4 += 32)
+            reinterpret_cast<float4*>(emb + (std::size_t)r * d.D)[c4] = reinterpret_cast<const float4*>(m)[c4];
+        return;
+    }
     const float s = static_cast<float>(log1p(fmax(0.0, root_t[r] - last)));
     for (int c = lane; c < d.D; c += 32)
         emb[(std::size_t)r * d.D + c] = m[c] * (1.f + s * tp[(std::size_t)c * ldtp] + tp[(std::size_t)c * ldtp + 1]);
     if (lane == 0) s_out[r] = s;
+}
+
+// DyRep message payload: after k_pending filled the other pending set with
+// this batch's last messages, copy each record's other-endpoint attention
+// embedding (z = [z_src rows | z_dst rows] of the batch) beside it. Record of
+// node u from event e = lo + k: u is the source (other = destination, row
+// B + k) unless it is only the destination (other = source, row k); a
+// self-loop's two rows are the same node at the same time, hence equal.
+__global__ void k_dyrep_stash(WorkerDev w, int D, int B, const float* z) {
+    pdl_entry();
+    const int i = warp_id_global(), lane = lane_id();
+    if (i >= *w.nxN) return;
+    const std::uint64_t e = w.nxEv[i];
+    const int k = static_cast<int>(e - w.ctl[0]);
+    const int row = w.ev_src[e] == w.nxU[i] ? B + k : k;
+    const float4* zr = reinterpret_cast<const float4*>(z + (std::size_t)row * D);
+    float4* o = reinterpret_cast<float4*>(w.nxZ + (std::size_t)i * D);
+    for (int c4 = lane; c4 < D / 4; c4 += 32) o[c4] = zr[c4];
 }
 
 // backward of the time projection: the roots' memory-row gradients go to
@@ -239,6 +264,14 @@ __global__ void k_jodie_bwd(WorkerDev w, Dims d, int R, const std::uint32_t* roo
     pdl_entry();
     const int c = threadIdx.x;
     if (c >= d.D) return;
+    if (!tp) {  // DyRep: identity embedding, d(memory row) = d_emb
+        const int r0 = blockIdx.x * rows_per_block, r1 = min(R, r0 + rows_per_block);
+        for (int r = r0; r < r1; ++r) {
+            dq_in[(std::size_t)r * d.ld_q + c] = d_emb[(std::size_t)r * d.D + c];
+            dm_in[(std::size_t)r * d.ld_m + d.DQ + c] = 0.f;
+        }
+        return;
+    }
     const float wc = tp[(std::size_t)c * ldtp], bc = tp[(std::size_t)c * ldtp + 1];
     double aw = 0.0, ab = 0.0;
     const int r0 = blockIdx.x * rows_per_block, r1 = min(R, r0 + rows_per_block);

@@ -50,6 +50,10 @@ struct WorkerDev {
     std::uint32_t* nxEv;
     double* nxTs;
     std::int32_t* nxN;
+    // DyRep: the other endpoint's attention embedding of each pending message
+    // (current set, read by the gather) and of the set k_pending fills
+    const float* pZ;
+    float* nxZ;
     // per-step control written by the host before each step (stream-ordered,
     // so a captured CUDA graph replays with fresh values): [0] first event of
     // the batch, [1] negative-sampling base (oracle: negatives())
@@ -189,6 +193,7 @@ __global__ void k_pending(WorkerDev w, int B);
 __global__ void k_rnn_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh, float* save, float* mem_new);
 __global__ void k_jodie_embed(WorkerDev w, Dims d, int R, const std::uint32_t* roots, const double* root_t,
                               const float* mem_new, const float* tp, int ldtp, float* emb, float* s_out);
+__global__ void k_dyrep_stash(WorkerDev w, int D, int B, const float* z);
 __global__ void k_jodie_bwd(WorkerDev w, Dims d, int R, const std::uint32_t* roots, const float* mem_new,
                             const float* tp, int ldtp, const float* s_in, const float* d_emb, float* dq_in,
                             float* dm_in, int rows_per_block, double* part);

@@ -86,18 +86,20 @@ void ParamLayout::build(int d_mem, int d_time, int d_edge, int heads, int k, int
         off += std::size_t(N) * l.ld;
     };
     // order == oracle/tgn_oracle.py linear_specs. JODIE: one RNN gate block,
-    // no attention / merge layers (zero rows), a time projection (1 -> D) last
-    const bool tgn = backbone == 0;
-    lin(gru_ih, tgn ? 3 * D : D, DM);
-    lin(gru_hh, tgn ? 3 * D : D, D);
-    lin(att_q, tgn ? DQ : 0, DQ);
-    lin(att_kv, tgn ? 2 * DQ : 0, DK);
-    lin(att_o, tgn ? DQ : 0, DQ);
-    lin(mrg1, tgn ? D : 0, DQ + D);
-    lin(mrg2, tgn ? D : 0, D);
+    // no attention / merge layers (zero rows), a time projection (1 -> D) last;
+    // DyRep: one RNN gate block, the attention + merge layers (its message
+    // embedding), no time projection
+    const bool gru = backbone == 0, att = backbone != 1, tp = backbone == 1;
+    lin(gru_ih, gru ? 3 * D : D, DM);
+    lin(gru_hh, gru ? 3 * D : D, D);
+    lin(att_q, att ? DQ : 0, DQ);
+    lin(att_kv, att ? 2 * DQ : 0, DK);
+    lin(att_o, att ? DQ : 0, DQ);
+    lin(mrg1, att ? D : 0, DQ + D);
+    lin(mrg2, att ? D : 0, D);
     lin(dec1, D, 2 * D);
     lin(dec2, 1, D);
-    lin(tproj, tgn ? 0 : D, 1);
+    lin(tproj, tp ? D : 0, 1);
     total = off;
 }
 
@@ -117,6 +119,7 @@ struct Scratch {
     DevBuf<float> ws;
     DevBuf<float> decw;  // decoder weight-gradient chunk partials (k_dec_wgrad_part)
     DevBuf<float> s_root;  // JODIE: log1p(dt) of each root
+    DevBuf<float> zmsg;    // DyRep: attention embeddings of the batch's sources, destinations
     DevBuf<double> tp_part;  // JODIE: time-projection gradient partials [blocks][2D]
     DevBuf<double> tpart;
     // deterministic dH reduction (tgn_dh.cu): reader index + chunk partials
@@ -392,6 +395,7 @@ tgnk::WorkerDev devview(Worker& w) {
     v.lastpos = w.lastpos.p; v.pU = c.pU.p; v.pOther = c.pOther.p; v.pEv = c.pEv.p; v.pTs = c.pTs.p;
     v.nU = c.nU.p;
     v.nxU = n.pU.p; v.nxOther = n.pOther.p; v.nxEv = n.pEv.p; v.nxTs = n.pTs.p; v.nxN = n.nU.p;
+    v.pZ = c.pZ.p; v.nxZ = n.pZ.p;  // (null unless DyRep)
     v.ctl = w.ctl;
     return v;
 }
@@ -459,9 +463,10 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
 
     SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
     SPD_CUDA(cudaStreamCreateWithPriority(&zs_, cudaStreamNonBlocking, prio_lo));
-    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_dhidx_, &ev_zfork_, &ev_zero_, &ev_bwdx_, &ev_pull_})
+    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_dhidx_, &ev_zfork_, &ev_zero_, &ev_bwdx_, &ev_pull_, &ev_pend_})
         SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    if (cfg.backbone != 0 && cfg.backbone != 1) data_error("InvalidParams", "backbone must be 0 (TGN) or 1 (JODIE)");
+    if (cfg.backbone < 0 || cfg.backbone > 2)
+        data_error("InvalidParams", "backbone must be 0 (TGN), 1 (JODIE) or 2 (DyRep)");
     lay_.build(cfg.d_mem, cfg.d_time, cfg.d_edge, cfg.n_heads, cfg.n_neighbors, cfg.backbone);
     feat_seed_mixed_ = mix64(cfg.seed_feat);
     const int D = lay_.D, F = lay_.F;
@@ -566,7 +571,8 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     s.ws.alloc(std::size_t(64) * 1024 * 1024 / 4 * 4);  // 64 MiB split-K workspace
     s.decw.alloc(std::size_t((B + tgnk::kDecWgEv - 1) / tgnk::kDecWgEv) *
                  (std::size_t(D) * (2 * D + 1) + D + 1));
-    if (cfg.backbone == 1) {
+    if (cfg.backbone == 2) s.zmsg.alloc(std::size_t(2) * B * D);  // DyRep message embeddings
+    if (cfg.backbone != 0) {
         s.s_root.alloc(R);
         s.tp_part.alloc(std::size_t((R + kJodieRows - 1) / kJodieRows) * 2 * D);
     }
@@ -665,7 +671,7 @@ TGNTrainer::~TGNTrainer() {
         if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
         if (sides_[k]) cudaStreamDestroy(sides_[k]);
     }
-    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_dhidx_, ev_zfork_, ev_zero_, ev_bwdx_, ev_pull_})
+    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_dhidx_, ev_zfork_, ev_zero_, ev_bwdx_, ev_pull_, ev_pend_})
         if (e) cudaEventDestroy(e);
     if (aux_) cudaStreamDestroy(aux_);
     for (auto& p : aring_)
@@ -783,6 +789,7 @@ void TGNTrainer::init_worker_state(Worker& w) {
     SPD_CUDA(cudaMemsetAsync(w.lastpos.p, 0xFF, w.lastpos.bytes(), stream_));
     for (auto& ps : w.pend) {
         ps.pU.alloc(2 * B); ps.pOther.alloc(2 * B); ps.pEv.alloc(2 * B); ps.pTs.alloc(2 * B);
+        if (lay_.backbone == 2) ps.pZ.alloc(std::size_t(2) * B * D);
         ps.nU.alloc(1); ps.nU.zero(stream_);
     }
     w.shared_local.clear();
@@ -941,7 +948,7 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
     launch(tgnk::k_gru_gather, blocks_for(std::size_t(s.U) * 32), 256, 0, stream_, 
         wd, d, P + lay_.time_w, P + lay_.time_b, s.x_gru.p, s.h_gru.p, 1);
     if (after_gather) after_gather();
-    if (lay_.backbone == 1) {  // JODIE: RNN memory updater (one gate block)
+    if (lay_.backbone != 0) {  // JODIE, DyRep: RNN memory updater (one gate block)
         SPD_CUDA(cudaEventRecord(ev_aux_fork_, stream_));
         SPD_CUDA(cudaStreamWaitEvent(aux_, ev_aux_fork_, 0));
         proj_fwd(tc, s.h_gru.p, d.ld_h, PW + lay_.gru_hh.off, lay_.gru_hh.ld, s.Gh.p, d.ld_g, s.U, d.D,
@@ -1009,12 +1016,15 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     };
     if (profile_) timed("roots_nbrs", [&] { roots(st); });
     s.dh.R = R;  // this batch's roots and occurrences (a loop's last batch may be short)
-    s.dh.RK = lay_.backbone == 1 ? 0 : R * d.K;  // JODIE: no neighbour readers
+    s.dh.RK = lay_.backbone != 0 ? 0 : R * d.K;  // JODIE, DyRep: no neighbour readers with gradient
     // this batch's last messages into the other pending set (K3): depends only
     // on the batch's events, off the critical path (the GRU below reads the
     // current set); eval steps run it in their post phase
     if (train)
-        side([&](cudaStream_t sd) { launch(tgnk::k_pending, 1, 1024, 0, sd, wd, B); });
+        side([&](cudaStream_t sd) {
+            launch(tgnk::k_pending, 1, 1024, 0, sd, wd, B);
+            if (lay_.backbone == 2) SPD_CUDA(cudaEventRecord(ev_pend_, sd));  // DyRep's stash waits
+        });
     // (the side-stream branch is forked after the GRU's first kernel is
     // enqueued: graph replays submit independent branches in creation order)
     cudaEvent_t at_gather = nullptr;
@@ -1039,7 +1049,8 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     if (!profile_) fork_roots();
     if (profile_ && train) timed("dh_index", [&] { dh_index(wd, s, st); });
     if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_roots_, 0));
-    if (lay_.backbone == 1) {  // JODIE: time projection + decoder (no attention)
+    if (lay_.backbone == 2) dyrep_messages(wd, B, train);  // DyRep: attention embeddings -> messages
+    if (lay_.backbone != 0) {  // JODIE / DyRep: time projection or identity + decoder
         jodie_rest(w, wd, B, train, slot_idx, post);
         return;
     }
@@ -1165,7 +1176,7 @@ void TGNTrainer::jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool tr
     float* G = grads_.p;
     cudaStream_t st = stream_;
     const bool tc = cfg_.gemm_mode == 1;
-    const float* TP = P + lay_.tproj.off;
+    const float* TP = lay_.backbone == 1 ? P + lay_.tproj.off : nullptr;  // null: identity (DyRep)
     const int ldtp = lay_.tproj.ld;
     timed("jodie_embed", [&] {
         launch(tgnk::k_jodie_embed, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R, s.roots.p,
@@ -1189,11 +1200,13 @@ void TGNTrainer::jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool tr
                    s.roots.p, static_cast<const float*>(s.mem_new.p), TP, ldtp,
                    static_cast<const float*>(s.s_root.p), static_cast<const float*>(s.d_emb.p), s.dq_in.p,
                    s.dm_in.p, kJodieRows, s.tp_part.p);
-            cudaEvent_t at_tp = mark();
-            side_from(at_tp, [&](cudaStream_t sd) {
-                launch(tgnk::k_jodie_tp_final, blocks_for(std::size_t(2) * d.D), 256, 0, sd, d.D, nblk,
-                       static_cast<const double*>(s.tp_part.p), G + lay_.tproj.off, ldtp);
-            });
+            if (TP) {
+                cudaEvent_t at_tp = mark();
+                side_from(at_tp, [&](cudaStream_t sd) {
+                    launch(tgnk::k_jodie_tp_final, blocks_for(std::size_t(2) * d.D), 256, 0, sd, d.D, nblk,
+                           static_cast<const double*>(s.tp_part.p), G + lay_.tproj.off, ldtp);
+                });
+            }
             decoder_wgrads(at, B);
         });
         timed("gru_bwd", [&] {
@@ -1214,7 +1227,53 @@ void TGNTrainer::jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool tr
     if (!post) return;
     timed("post", [&] {
         launch(tgnk::k_persist, blocks_for(std::size_t(s.U) * 32), 256, 0, st, wd, d.D, s.mem_new.p);
-        if (!train) launch(tgnk::k_pending, 1, 1024, 0, st, wd, B);
+        if (!train) {
+            launch(tgnk::k_pending, 1, 1024, 0, st, wd, B);
+            if (lay_.backbone == 2)
+                launch(tgnk::k_dyrep_stash, blocks_for(std::size_t(2) * B * 32), 256, 0, st, wd, d.D, B,
+                       static_cast<const float*>(s.zmsg.p));
+        }
+    });
+}
+
+// DyRep's message function: the temporal-attention embedding (the TGN layer,
+// forward only — message inputs carry no gradient) of the batch's sources and
+// destinations over the updated memory, into s.zmsg; in training the
+// records k_pending selected (side stream) get their payload rows here.
+void TGNTrainer::dyrep_messages(const tgnk::WorkerDev& wd, int B, bool train) {
+    Scratch& s = *s_;
+    const auto& d = s.d;
+    const int R = 2 * B;  // sources then destinations (the first 2B roots)
+    const float* P = params_.p;
+    cudaStream_t st = stream_;
+    const bool tc = cfg_.gemm_mode == 1;
+    const float* PW = tc ? params_tc_.p : params_.p;
+    timed("dyrep_attn", [&] {
+        launch(tgnk::k_query_gather, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d, R,
+               P + lay_.time_w, P + lay_.time_b, s.roots.p, s.mem_new.p, s.q_in.p, s.m_in.p);
+        proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
+                 d.DQ + 1, nullptr, st, 0, nullptr, 0, tc);
+        const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
+        const float* WK = PW + lay_.att_kv.off;
+        const float* WV = WK + std::size_t(d.DQ) * lay_.att_kv.ld;
+        const int ldw = lay_.att_kv.ld;
+        const std::ptrdiff_t wst = std::ptrdiff_t(dh) * ldw;
+        proj_dgrad(tc, s.Q.p, d.ld_Q, WK, ldw, s.Qp.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0, nullptr,
+                   0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
+        attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st);
+        proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
+                 nullptr, 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
+        proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.m_in.p, d.ld_m, R, d.DQ,
+                 d.DQ + 1, nullptr, st, gemm::EPI_ROWMASK, reinterpret_cast<const float*>(s.cnt.p), d.DQ, tc);
+        proj_fwd(tc, s.m_in.p, d.ld_m, PW + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
+                 d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU, nullptr, 0, tc);
+        proj_fwd(tc, s.Z1.p, d.ld_z, PW + lay_.mrg2.off, lay_.mrg2.ld, s.zmsg.p, d.D, R, d.D, d.D + 1,
+                 nullptr, st);
+        if (train) {
+            if (!profile_) SPD_CUDA(cudaStreamWaitEvent(st, ev_pend_, 0));  // k_pending's records
+            launch(tgnk::k_dyrep_stash, blocks_for(std::size_t(R) * 32), 256, 0, st, wd, d.D, B,
+                   static_cast<const float*>(s.zmsg.p));
+        }
     });
 }
 

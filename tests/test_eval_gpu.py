@@ -51,7 +51,7 @@ def ap_auc(pos, neg):
     return average_precision_score(y, s), roc_auc_score(y, s)
 
 
-@pytest.mark.parametrize("backbone", [0, 1])
+@pytest.mark.parametrize("backbone", [0, 1, 2])
 @pytest.mark.parametrize("gemm_mode", [0, 1])
 def test_eval_scores_match_oracle(gemm_mode, backbone):
     pa, subs, ev, r = build(400, 6000, 2)

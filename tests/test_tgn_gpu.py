@@ -410,16 +410,20 @@ def test_device_shuffle_combine_matches_host_rebind(parts, workers):
     dev.close()
 
 
+@pytest.mark.parametrize("backbone", [1, 2])
 @pytest.mark.parametrize("gemm_mode", [0, 1])
 @pytest.mark.parametrize("parts", [1, 2])
-def test_jodie_backbone_matches_oracle(parts, gemm_mode):
-    """JODIE backbone (spd_tgn_config.backbone = 1): RNN memory
-    updater + time-projection embedding on the same message, last-message,
-    decoder and PAC-schedule kernels. Per-step embeddings, losses, first-step
-    gradients, parameters, memory and clocks against the oracle's JODIE, a
-    whole epoch with the epoch-end restore + shared-hub sync included."""
+def test_jodie_backbone_matches_oracle(parts, gemm_mode, backbone):
+    """JODIE and DyRep backbones (spd_tgn_config.backbone = 1 / 2):
+    RNN memory updater + time-projection (JODIE) or identity (DyRep) embedding
+    on the same message, last-message, decoder and PAC-schedule kernels;
+    DyRep's messages carry the other endpoint's temporal-attention embedding
+    (the TGN attention kernels, forward only). Per-step embeddings, losses,
+    first-step gradients, parameters, memory and clocks against the oracle's
+    JODIE / DyRep, a whole epoch with the epoch-end restore + shared-hub sync
+    included."""
     _, _, pa, subs = partitioned(parts=parts)
-    cfg = small_cfg(backbone=1, gemm_mode=gemm_mode)
+    cfg = small_cfg(backbone=backbone, gemm_mode=gemm_mode)
     tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
     o = oracle_for(cfg, subs, pa.shared)
     assert tr.n_params == o.total and np.array_equal(tr.params(), o.flat.numpy())
@@ -455,7 +459,7 @@ def test_jodie_backbone_matches_oracle(parts, gemm_mode):
 
 
 @pytest.mark.parametrize("concurrent", [1, 0])
-@pytest.mark.parametrize("parts,sync_average,backbone", [(2, 1, 0), (3, 0, 0), (2, 1, 1)])
+@pytest.mark.parametrize("parts,sync_average,backbone", [(2, 1, 0), (3, 0, 0), (2, 1, 1), (2, 1, 2)])
 def test_concurrent_workers_match_oracle(parts, sync_average, backbone, concurrent):
     """spd_tgn_config.concurrent = 1: a process's local workers train as
     concurrent lanes (own streams, scratch, graphs and parameter replica; an
