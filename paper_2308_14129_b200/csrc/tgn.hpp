@@ -16,6 +16,7 @@
 #include "host.hpp"
 #include "peer_comm.hpp"
 #include "tgn_kernels.cuh"
+#include "umma_host.hpp"
 
 namespace spd {
 
@@ -290,6 +291,10 @@ private:
     cudaEvent_t ev_bwdx_ = nullptr;  // attention time-encoder partials done
     cudaEvent_t ev_pull_ = nullptr;  // dH chunk partials done (tgn_dh.cu)
     cudaEvent_t ev_pend_ = nullptr;  // (DyRep) this batch's last messages selected
+    // deferred split-K sums of the step's last GRU weight gradients (fused_finalize)
+    umma::SplitK fin_sk_[2];
+    bool fin_defer_ = false;
+    bool fused_finalize() const;
     bool scratch_zeroed_ = false;    // dGi/dGh cleared by this step's k_zero_list
     bool gru_fused_ = true;          // gemm_mode 1: fused tcgen05 GRU (SPD_GRU_FUSED=0: two GEMMs + cell)
 

@@ -42,6 +42,11 @@ namespace {
 #endif
 constexpr int kRootsPerBlock = SPD_ATTN_ROOTS;
 constexpr int kRootsX = 4;  // roots per 128-thread block of the scatter kernel
+// blocks per SM the staged rows allow at GDELT dims (6 x ~36.5 KB): registers
+// capped to match for up to 4 slots and 2 heads, so shared memory stays the
+// only residency limit (wider rows / more heads keep the compiler's choice)
+template <int NM, int NT, int NF, int HMAX>
+constexpr int attn_min_blocks() { return HMAX <= 2 && NM + NT + NF <= 4 ? 6 : 1; }
 
 __device__ __forceinline__ float dot4acc(const float4& a, const float4& b, float acc) {
     return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, fmaf(a.x, b.x, acc))));
@@ -57,7 +62,7 @@ __device__ __forceinline__ float4 rnd4(float4 v, int rnd) {
 // One staged neighbour row: [mem f32 D | cos f32 T | sin f32 T (bwd) | feat bf16 Fp]
 // (each part one bulk copy: the memory row, the phi row, the feature row)
 __host__ __device__ __forceinline__ int row_bytes(const Dims& d, bool with_sin) {
-    return 4 * (d.D + d.T) + (with_sin ? 4 * d.T : 0) + 2 * d.Fp;
+    return 4 * (d.D + d.T) + (with_sin ? 4 * d.T : 0) + 2 * d.Fp + 16;  // + 16 zero bytes (slot_offsets)
 }
 __host__ __device__ __forceinline__ int feat_off(const Dims& d, bool with_sin) {
     return 4 * (d.D + d.T) + (with_sin ? 4 * d.T : 0);
@@ -84,20 +89,34 @@ struct Slots {
 };
 
 // Slot i of a staged row: columns col(i)..+3 of [s_nbr | phi | e], the
-// constant-1 bias column excluded. Its terms drop out of the kernels exactly:
-// <q'_h, e_bias> = <q_h, b_K,h> is the same for every neighbour, so softmax
-// (shift invariant) ignores it and its gradient sum_j ds_hj is 0; in xbar it
-// is sum_j a_hj = 1, set directly (set_bias).
+// constant-1 bias column excluded (it reads as 0). Its terms drop out of the
+// kernels exactly: <q'_h, e_bias> = <q_h, b_K,h> is the same for every
+// neighbour, so softmax (shift invariant) ignores it and its gradient
+// sum_j ds_hj is 0; in xbar it is sum_j a_hj = 1, set directly (set_bias).
+// Byte offset of each slot's columns within a staged row, once per lane: a
+// lane whose slot lies past its region reads the row's 16 zero tail bytes
+// (zeroed at kernel start, after the feature row), so the inner loops are
+// branch-free loads.
 template <class S>
-__device__ __forceinline__ float4 x_slot(const Dims& d, int i, int lane, const unsigned char* row,
-                                         int foff) {
-    const int o = 4 * (lane + 32 * S::local(i));
-    if (S::region(i) == 0) return o < d.D ? *reinterpret_cast<const float4*>(row + 4 * o) : z4();
-    if (S::region(i) == 1) return o < d.T ? *reinterpret_cast<const float4*>(row + 4 * (d.D + o)) : z4();
-    if (o >= d.Fp) return z4();  // Fp % 8 == 0: 4 bf16 never straddle the row end; pad is 0
-    const uint2 raw = *reinterpret_cast<const uint2*>(row + foff + 2 * o);
+__device__ __forceinline__ void slot_offsets(int (&o)[S::N], const Dims& d, int lane, int foff) {
+    const int tail = foff + 2 * d.Fp;
+#pragma unroll
+    for (int i = 0; i < S::N; ++i) {
+        const int c = 4 * (lane + 32 * S::local(i));
+        if (S::region(i) == 0) o[i] = c < d.D ? 4 * c : tail;
+        else if (S::region(i) == 1) o[i] = c < d.T ? 4 * (d.D + c) : tail;
+        else o[i] = c < d.Fp ? foff + 2 * c : tail;
+    }
+}
+template <class S>
+__device__ __forceinline__ float4 x_at(int i, const unsigned char* p) {
+    if (S::region(i) != 2) return *reinterpret_cast<const float4*>(p);
+    const uint2 raw = *reinterpret_cast<const uint2*>(p);
     return make_float4(__uint_as_float(raw.x << 16), __uint_as_float(raw.x & 0xFFFF0000u),
                        __uint_as_float(raw.y << 16), __uint_as_float(raw.y & 0xFFFF0000u));
+}
+__device__ __forceinline__ void zero_tails(const Dims& d, int lane, unsigned char* xs, int RB, int foff) {
+    if (lane < d.K) *reinterpret_cast<float4*>(xs + (std::size_t)lane * RB + foff + 2 * d.Fp) = z4();
 }
 
 // Put value c into the bias column (feature index F) of every head's slots.
@@ -182,7 +201,7 @@ __device__ __forceinline__ void stage_rows(const WorkerDev& w, const Dims& d, in
 }
 
 // Time columns of the staged rows: each lane writes cos(w dt_j + b) of its own
-// time slots (the columns its x_slot reads) for every neighbour j < c_n.
+// time slots (the columns its x_at reads) for every neighbour j < c_n.
 template <class S>
 __device__ __forceinline__ void fill_cos(const Dims& d, int lane, int c_n, double m_dt,
                                          const float* time_w, const float* time_b,
@@ -251,6 +270,8 @@ __device__ __forceinline__ void dots(const float4 (&v)[HMAX][S::N], const Dims& 
                                      const unsigned char* xs, int RB, int foff, int c_n, float* sc,
                                      float scale) {
     constexpr int G = 8, V = G * HMAX;
+    int off[S::N];
+    slot_offsets<S>(off, d, lane, foff);
     const int vi = vidx<V>(lane);
     const int hv = vi / G, gv = vi % G;
     const bool writer = (lane & ((32 / V) - 1)) == 0;
@@ -265,7 +286,7 @@ __device__ __forceinline__ void dots(const float4 (&v)[HMAX][S::N], const Dims& 
                 const unsigned char* row = xs + (std::size_t)(j0 + g) * RB;
 #pragma unroll
                 for (int i = 0; i < S::N; ++i) {
-                    const float4 x = x_slot<S>(d, i, lane, row, foff);
+                    const float4 x = x_at<S>(i, row + off[i]);
 #pragma unroll
                     for (int h = 0; h < HMAX; ++h) p[h * G + g] = dot4acc(v[h][i], x, p[h * G + g]);
                 }
@@ -280,6 +301,8 @@ template <class S, int HMAX>
 __device__ __forceinline__ void axpys(float4 (&v)[HMAX][S::N], const Dims& d, int lane,
                                       const unsigned char* xs, int RB, int foff, int c_n,
                                       const float* coef) {
+    int off[S::N];
+    slot_offsets<S>(off, d, lane, foff);
 #pragma unroll 2
     for (int j = 0; j < c_n; ++j) {
         const unsigned char* row = xs + (std::size_t)j * RB;
@@ -288,7 +311,7 @@ __device__ __forceinline__ void axpys(float4 (&v)[HMAX][S::N], const Dims& d, in
         for (int h = 0; h < HMAX; ++h) a[h] = h < d.H ? coef[h * d.K + j] : 0.f;
 #pragma unroll
         for (int i = 0; i < S::N; ++i) {
-            const float4 x = x_slot<S>(d, i, lane, row, foff);
+            const float4 x = x_at<S>(i, row + off[i]);
 #pragma unroll
             for (int h = 0; h < HMAX; ++h) axpy4(v[h][i], a[h], x);
         }
@@ -310,7 +333,7 @@ int attn_x_roots_per_block() { return kRootsX; }
 // (tf32-rounded when it feeds a tensor-core GEMM). Roots without neighbours
 // get xbar = 0 (bias slot 0 too: ctx = 0; the oracle masks them).
 template <int NM, int NT, int NF, int HMAX>
-__global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R,
+__global__ void __launch_bounds__(32 * kRootsPerBlock, (attn_min_blocks<NM, NT, NF, HMAX>())) k_attn_abs_fwd(WorkerDev w, Dims d, int R,
                                                       const float* time_w, const float* time_b,
                                                       const std::uint32_t* nbr_node,
                                                       const std::uint32_t* nbr_ev,
@@ -329,6 +352,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
     std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(smem + attn_smem_bytes(d, BWD)) - kRootsPerBlock + warp;
     float* sc = reinterpret_cast<float*>(bar - warp) - kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
     if (lane == 0) bar_init(bar);
+    zero_tails(d, lane, xs, RB, feat_off(d, BWD));
     __syncwarp();
     const int c_n = cnt[r];
     const std::size_t row0 = (std::size_t)r * d.H * d.ld_p;
@@ -392,7 +416,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_fwd(WorkerDev w, Dims d, int R
 //   fixed order). Neither needs staged rows: only per-root vectors, alpha,
 //   ds and the neighbours' dt.
 template <int NM, int NT, int NF, int HMAX>
-__global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R,
+__global__ void __launch_bounds__(32 * kRootsPerBlock, (attn_min_blocks<NM, NT, NF, HMAX>())) k_attn_abs_bwd(WorkerDev w, Dims d, int R,
                                                       const float* time_w, const float* time_b,
                                                       const std::uint32_t* nbr_node,
                                                       const std::uint32_t* nbr_ev,
@@ -412,6 +436,7 @@ __global__ void __launch_bounds__(128) k_attn_abs_bwd(WorkerDev w, Dims d, int R
     std::uint64_t* bar = reinterpret_cast<std::uint64_t*>(smem + attn_smem_bytes(d, true)) - kRootsPerBlock + warp;
     float* sc = reinterpret_cast<float*>(bar - warp) - kRootsPerBlock * 2 * d.H * d.K + warp * 2 * d.H * d.K;
     if (lane == 0) bar_init(bar);
+    zero_tails(d, lane, xs, RB, feat_off(d, BWD));
     __syncwarp();
     float* aa = sc + d.H * d.K;  // alpha of this root
     const int c_n = cnt[r];

@@ -800,9 +800,32 @@ __device__ __forceinline__ float adam_one(float& p, float g, float& m, float& v,
     p = p - lr * mh / (sqrtf(vh) + eps);
     return p;
 }
-__global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
+// the flat gradient of parameter k with the deferred terms added as the
+// kernels they replace would have (k_time_grad_apply: g + (float)acc;
+// k_splitk_reduce: g + (((0 + w_0) + w_1) + ...))
+__device__ __forceinline__ float fin_grad(float g, std::size_t k, const AdamFin& f) {
+    if (f.tacc) {
+        if (k >= f.tw && k < f.tw + f.T) return g + (float)f.tacc[k - f.tw];
+        if (k >= f.tb && k < f.tb + f.T) return g + (float)f.tacc[f.T + (k - f.tb)];
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        if (q >= f.nsk) break;
+        const AdamFin::SK& s = f.sk[q];
+        if (k < s.off || k >= s.off + (std::size_t)s.M * s.ldc) continue;
+        const int m = static_cast<int>((k - s.off) / s.ldc), c = static_cast<int>((k - s.off) % s.ldc);
+        if (c >= s.N) return g;
+        const float* w = s.ws + (std::size_t)m * s.ldws + c;
+        float acc = 0.f;
+        for (int z = 0; z < s.split; ++z) acc += w[(std::size_t)z * s.M * s.ldws];
+        return g + acc;
+    }
+    return g;
+}
+
+__global__ void k_adam(float* p, float* g, float* m, float* v, std::size_t n, float scale,
                        float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
-                       float eps, float* p_tc) {
+                       float eps, float* p_tc, AdamFin fin) {
     pdl_entry();
     const std::size_t i4 = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const std::size_t i = 4 * i4;
@@ -811,7 +834,37 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t
     if (i + 4 <= n) {
         float4 pp = *reinterpret_cast<float4*>(p + i), mm = *reinterpret_cast<float4*>(m + i);
         float4 vv = *reinterpret_cast<float4*>(v + i);
-        const float4 gg = *reinterpret_cast<const float4*>(g + i);
+        float4 gg = *reinterpret_cast<float4*>(g + i);
+        if (fin.tacc || fin.nsk) {  // (finalized gradients written back: introspection reads them)
+            bool hit = false;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {  // split-K rows: 4 columns of one row per float4
+                if (q >= fin.nsk) break;
+                const AdamFin::SK& sk = fin.sk[q];
+                if (i < sk.off || i >= sk.off + (std::size_t)sk.M * sk.ldc) continue;
+                const int mr = static_cast<int>((i - sk.off) / sk.ldc), c = static_cast<int>((i - sk.off) % sk.ldc);
+                if (c + 4 <= sk.N && sk.ldws % 4 == 0 && sk.ldc % 4 == 0) {
+                    const float* w = sk.ws + (std::size_t)mr * sk.ldws + c;
+                    float4 acc = *reinterpret_cast<const float4*>(w);
+#pragma unroll 8
+                    for (int z = 1; z < sk.split; ++z) {
+                        const float4 t = *reinterpret_cast<const float4*>(w + (std::size_t)z * sk.M * sk.ldws);
+                        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+                    }
+                    gg.x += acc.x; gg.y += acc.y; gg.z += acc.z; gg.w += acc.w;
+                    hit = true;
+                }
+            }
+            if (!hit) {
+                const float4 g0 = gg;
+                gg.x = fin_grad(gg.x, i, fin);
+                gg.y = fin_grad(gg.y, i + 1, fin);
+                gg.z = fin_grad(gg.z, i + 2, fin);
+                gg.w = fin_grad(gg.w, i + 3, fin);
+                hit = g0.x != gg.x || g0.y != gg.y || g0.z != gg.z || g0.w != gg.w;
+            }
+            if (hit) *reinterpret_cast<float4*>(g + i) = gg;
+        }
         adam_one(pp.x, gg.x, mm.x, vv.x, scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
         adam_one(pp.y, gg.y, mm.y, vv.y, scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
         adam_one(pp.z, gg.z, mm.z, vv.z, scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
@@ -823,6 +876,7 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t
         return;
     }
     for (std::size_t k = i; k < n; ++k) {
+        g[k] = fin_grad(g[k], k, fin);
         adam_one(p[k], g[k], m[k], v[k], scale, lr, b1, one_m_b1, b2, one_m_b2, bc1, bc2, eps);
         if (p_tc) p_tc[k] = tf32r(p[k]);
     }

@@ -177,9 +177,23 @@ __global__ void k_root_grad(Dims d, int R, const float* dq_in, const float* time
                             int rows_per_block, double* part);
 __global__ void k_time_grad_final(int T, int nblocks, const double* part, double* acc);
 __global__ void k_time_grad_apply(int T, const double* acc, float* gw, float* gb);
-__global__ void k_adam(float* p, const float* g, float* m, float* v, std::size_t n, float scale,
+// Gradient terms not yet in the flat buffer when the optimizer runs on one
+// process (tgn_trainer.cu adam): the time-encoder f64 accumulators and up to
+// two deferred split-K weight gradients (fixed-order partial sums).
+struct AdamFin {
+    const double* tacc = nullptr;  // [2T]: d time_w then d time_b (null: none)
+    int T = 0;
+    std::size_t tw = 0, tb = 0;    // their flat offsets
+    int nsk = 0;
+    struct SK {
+        const float* ws;
+        int split, M, N, ldws, ldc;
+        std::size_t off;           // flat offset of dW
+    } sk[2];
+};
+__global__ void k_adam(float* p, float* g, float* m, float* v, std::size_t n, float scale,
                        float lr, float b1, float one_m_b1, float b2, float one_m_b2, const float* bc,
-                       float eps, float* p_tc);
+                       float eps, float* p_tc, AdamFin fin);
 __global__ void k_round_tf32(const float* src, float* dst, std::size_t n);
 struct GradList {
     const float* g[8];

@@ -251,10 +251,12 @@ long tgru_ctas() {
 
 void proj_wgrad(bool tc, const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw,
                 int N_out, int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
-                cudaStream_t s, const umma::Batch& bt = {}, int target_ctas = 64) {
+                cudaStream_t s, const umma::Batch& bt = {}, int target_ctas = 64,
+                umma::SplitK* defer = nullptr) {
+    if (defer) defer->split = 0;
     if (tc)
         return umma::wgrad(dY, ldy, X, ldx, dW, ldw, N_out, K_in, rows, rows_dev, ws, ws_cap, s, bt,
-                           target_ctas);
+                           target_ctas, defer);
     for (int z = 0; z < bt.n; ++z)
         gemm_wgrad(dY + z * bt.a, ldy, X + z * bt.b, ldx, dW + z * bt.c, ldw, N_out, K_in, rows,
                    rows_dev, ws, ws_cap, s);
@@ -1218,9 +1220,11 @@ void TGNTrainer::jodie_rest(Worker& w, const tgnk::WorkerDev& wd, int B, bool tr
             dh_pull_root(d, s, st);
             gru_bwd_dh(wd, d, s, st, true);
             side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off,
-                                                   lay_.gru_ih.ld, d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
+                                                   lay_.gru_ih.ld, d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd,
+                                                   {}, 64, fin_defer_ ? &fin_sk_[0] : nullptr); });
             side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off,
-                                                   lay_.gru_hh.ld, d.D, d.D + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd); });
+                                                   lay_.gru_hh.ld, d.D, d.D + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd,
+                                                   {}, 64, fin_defer_ ? &fin_sk_[1] : nullptr); });
         });
         join_side();
     }
@@ -1408,10 +1412,13 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         // the step's last weight gradients (Adam waits for them): a grid of
         // about one wave each instead of the side streams' 64 CTAs
         const int gru_ctas = int(tgru_ctas());
+        // (the step's last worker leaves their split-K sums to Adam: fin_defer_)
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGi.p, d.ld_g, s.x_gru.p, d.ld_x, G + lay_.gru_ih.off, lay_.gru_ih.ld,
-                   3 * d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd, {}, gru_ctas); });
+                   3 * d.D, d.DM + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd, {}, gru_ctas,
+                   fin_defer_ ? &fin_sk_[0] : nullptr); });
         side([&](cudaStream_t sd) { proj_wgrad(tc, s.dGh.p, d.ld_g, s.h_gru.p, d.ld_h, G + lay_.gru_hh.off, lay_.gru_hh.ld,
-                   3 * d.D, d.D + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd, {}, gru_ctas); });
+                   3 * d.D, d.D + 1, s.U, w.nU(), ws_cur_, wsn_cur_, sd, {}, gru_ctas,
+                   fin_defer_ ? &fin_sk_[1] : nullptr); });
     });
     // side-stream weight grads read the pending set (nU, GRU inputs) that the
     // post phase rewrites: join first
@@ -1645,10 +1652,16 @@ void TGNTrainer::loop_end_flush(Worker& w) {
     w.flush_due = false;
 }
 
+// One process, no lanes: the optimizer itself folds the time-encoder
+// accumulators and the step's last split-K sums into the gradients (k_adam's
+// AdamFin) — two or three fewer launches on the step's critical tail.
+bool TGNTrainer::fused_finalize() const { return world_ == 1 && !peer_ && !lane_ && !profile_; }
+
 void TGNTrainer::allreduce_grads(cudaStream_t st) {
     // time-encoder grads (f64 accumulators) into the flat buffer first
-    launch(tgnk::k_time_grad_apply, blocks_for(lay_.T), 256, 0, st, 
-        lay_.T, tgrad_.p, grads_.p + lay_.time_w, grads_.p + lay_.time_b);
+    if (!fused_finalize())
+        launch(tgnk::k_time_grad_apply, blocks_for(lay_.T), 256, 0, st,
+               lay_.T, tgrad_.p, grads_.p + lay_.time_w, grads_.p + lay_.time_b);
     SPD_CUDA(cudaGetLastError());
     if (world_ > 1 && !peer_) {  // (the peer transport sums inside its Adam kernel)
         SPD_NCCL(ncclAllReduce(grads_.p, grads_.p, lay_.total, ncclFloat, ncclSum,
@@ -1684,11 +1697,25 @@ void TGNTrainer::adam(cudaStream_t st) {
                          cfg_.gemm_mode == 1 ? params_tc_.p : nullptr, st);
         return;
     }
+    tgnk::AdamFin fin{};
+    if (fused_finalize()) {
+        fin.tacc = tgrad_.p;
+        fin.T = lay_.T;
+        fin.tw = lay_.time_w;
+        fin.tb = lay_.time_b;
+        for (const umma::SplitK& k : fin_sk_) {
+            if (k.split <= 1) continue;
+            auto& o = fin.sk[fin.nsk++];
+            o.ws = k.ws; o.split = k.split; o.M = k.M; o.N = k.N; o.ldws = k.ldws; o.ldc = k.ldc;
+            o.off = static_cast<std::size_t>(k.C - grads_.p);
+        }
+    }
+    for (auto& k : fin_sk_) k.split = 0;
     launch(tgnk::k_adam, blocks_for((lay_.total + 3) / 4), 256, 0, st,
         params_.p, grads_.p, adam_m_.p, adam_v_.p, lay_.total, float(total_workers_), cfg_.lr,
         cfg_.beta1, static_cast<float>(1.0 - b1), cfg_.beta2, static_cast<float>(1.0 - b2),
         adam_bc_, cfg_.adam_eps,
-        cfg_.gemm_mode == 1 ? params_tc_.p : nullptr);
+        cfg_.gemm_mode == 1 ? params_tc_.p : nullptr, fin);
     SPD_CUDA(cudaGetLastError());
 }
 
@@ -1744,7 +1771,9 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
     for (std::size_t k = 0; k < workers_.size(); ++k) {
         Worker& w = *workers_[k];
         if (Bs[k] == 0) continue;
+        fin_defer_ = k == last && fused_finalize();
         worker_step(w, devview(w), Bs[k], true, static_cast<int>(k), k != last);
+        fin_defer_ = false;
         if (debug_) {  // taps before the next worker reuses the scratch
             const std::uint64_t B = w.last_b;
             const int D = lay_.D, K = lay_.Kn;

@@ -262,8 +262,17 @@ void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, 
 
 void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
            int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap,
-           cudaStream_t s, const Batch& bt, int target_ctas) {
+           cudaStream_t s, const Batch& bt, int target_ctas, SplitK* defer) {
+    if (defer) defer->split = 0;
     if (!rows || !N_out || !K_in) return;
+    auto finish = [&](int split, int ldws) {
+        if (split <= 1) return;
+        if (defer && bt.n == 1) {
+            *defer = SplitK{ws, split, N_out, K_in, ldws, dW, ldw};
+            return;
+        }
+        reduce(ws, split, N_out, K_in, ldws, dW, ldw, bt, s);
+    };
     check_batch(bt);
     const int mt = (N_out + BM - 1) / BM;
     const int ldws = (K_in + 3) / 4 * 4;
@@ -282,7 +291,7 @@ void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw
         const int cl = mt <= 2 ? 2 : 4;
         if (cl == 2) run<true, true, 224, 2, 2>(maps, a, dim3(1, 2, split), s);
         else run<true, true, 224, 2, 4>(maps, a, dim3(1, 4, split), s);
-        if (split > 1) reduce(ws, split, N_out, K_in, ldws, dW, ldw, bt, s);
+        finish(split, ldws);
         return;
     }
     const int bn = K_in <= 64 ? 64 : (K_in <= 128 ? 128 : 224);
@@ -298,7 +307,7 @@ void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw
     a.k_split = split; a.mode = split > 1 ? PARTIAL : ACCUM;
     dispatch<true, true>(bn, maps, a,
                          dim3((K_in + bn - 1) / bn, (N_out + BM - 1) / BM, split * bt.n), s);
-    if (split > 1) reduce(ws, split, N_out, K_in, ldws, dW, ldw, bt, s);
+    finish(split, ldws);
 }
 
 template <int UB>

@@ -24,11 +24,20 @@ void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, in
 void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, int M, int N,
            int K, const int* M_dev, cudaStream_t s, int epi = 0, const float* mask = nullptr,
            int ldmask = 0, int rnd = 0, const Batch& bt = {});
+// A split-K weight gradient whose fixed-order partial sum is left to a later
+// kernel (the optimizer, k_adam): dW[m][n] += sum_z ws[z][m][n] for n < N.
+struct SplitK {
+    const float* ws = nullptr;
+    int split = 0, M = 0, N = 0, ldws = 0;
+    float* C = nullptr;
+    int ldc = 0;
+};
 // target_ctas: the split-K grid aimed at (64: side-stream weight gradients;
-// more for one on the step's critical tail)
+// more for one on the step's critical tail). defer != null: a split-K result
+// is described there instead of reduced (defer->split = 0 when none).
 void wgrad(const float* dY, int ldy, const float* X, int ldx, float* dW, int ldw, int N_out,
            int K_in, int rows, const int* rows_dev, float* ws, std::size_t ws_cap, cudaStream_t s,
-           const Batch& bt = {}, int target_ctas = 64);
+           const Batch& bt = {}, int target_ctas = 64, SplitK* defer = nullptr);
 // Fused GRUCell on tensor cores (umma_gru.cuh): both gate GEMMs (x: [M x K1],
 // h: [M x K2], augmented weights [3D x K]) and the cell; writes mem_new [M x D]
 // and, when save != null, the backward's gate values [M x 4D] (r | z | n | Gh_n).
