@@ -262,39 +262,53 @@ __device__ __forceinline__ void store_slots(const float4 (&v)[HMAX][S::N], float
     }
 }
 
-// sc[h*K + j] = scale * <v[h], x~_j> for every valid neighbour j, in groups
-// of 8 neighbours whose 8*HMAX partial dot products share one multi-value
-// warp reduction.
+// One group of G neighbours j0 .. j0+G-1 (all valid): their G*HMAX partial dot
+// products share one multi-value warp reduction.
+template <class S, int HMAX, int G>
+__device__ __forceinline__ void dots_group(const float4 (&v)[HMAX][S::N], const Dims& d, int lane,
+                                           const unsigned char* xs, int RB, const int (&off)[S::N],
+                                           int j0, float* sc, float scale) {
+    constexpr int V = G * HMAX;
+    float p[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) p[k] = 0.f;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const unsigned char* row = xs + (std::size_t)(j0 + g) * RB;
+#pragma unroll
+        for (int i = 0; i < S::N; ++i) {
+            const float4 x = x_at<S>(i, row + off[i]);
+#pragma unroll
+            for (int h = 0; h < HMAX; ++h) p[h * G + g] = dot4acc(v[h][i], x, p[h * G + g]);
+        }
+    }
+    const float r = warp_reduce_multi<V>(p, lane);
+    const int vi = vidx<V>(lane);
+    const int hv = vi / G, gv = vi % G;
+    if ((lane & ((32 / V) - 1)) == 0 && hv < d.H) sc[hv * d.K + j0 + gv] = r * scale;
+}
+
+// sc[h*K + j] = scale * <v[h], x~_j> for every valid neighbour j: full groups
+// of 8, then groups of 4, 2, 1 for the rest (no per-neighbour guards; every
+// reduction carries only valid neighbours).
 template <class S, int HMAX>
 __device__ __forceinline__ void dots(const float4 (&v)[HMAX][S::N], const Dims& d, int lane,
                                      const unsigned char* xs, int RB, int foff, int c_n, float* sc,
                                      float scale) {
-    constexpr int G = 8, V = G * HMAX;
     int off[S::N];
     slot_offsets<S>(off, d, lane, foff);
-    const int vi = vidx<V>(lane);
-    const int hv = vi / G, gv = vi % G;
-    const bool writer = (lane & ((32 / V) - 1)) == 0;
+    int j0 = 0;
 #pragma unroll 1
-    for (int j0 = 0; j0 < c_n; j0 += G) {
-        float p[V];
-#pragma unroll
-        for (int k = 0; k < V; ++k) p[k] = 0.f;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-            if (j0 + g < c_n) {
-                const unsigned char* row = xs + (std::size_t)(j0 + g) * RB;
-#pragma unroll
-                for (int i = 0; i < S::N; ++i) {
-                    const float4 x = x_at<S>(i, row + off[i]);
-#pragma unroll
-                    for (int h = 0; h < HMAX; ++h) p[h * G + g] = dot4acc(v[h][i], x, p[h * G + g]);
-                }
-            }
-        }
-        const float r = warp_reduce_multi<V>(p, lane);
-        if (writer && hv < d.H && j0 + gv < c_n) sc[hv * d.K + j0 + gv] = r * scale;
+    for (; j0 + 8 <= c_n; j0 += 8) dots_group<S, HMAX, 8>(v, d, lane, xs, RB, off, j0, sc, scale);
+    if (j0 + 4 <= c_n) {
+        dots_group<S, HMAX, 4>(v, d, lane, xs, RB, off, j0, sc, scale);
+        j0 += 4;
     }
+    if (j0 + 2 <= c_n) {
+        dots_group<S, HMAX, 2>(v, d, lane, xs, RB, off, j0, sc, scale);
+        j0 += 2;
+    }
+    if (j0 < c_n) dots_group<S, HMAX, 1>(v, d, lane, xs, RB, off, j0, sc, scale);
 }
 
 template <class S, int HMAX>
