@@ -21,6 +21,14 @@ __device__ __forceinline__ void pdl_entry() {
     asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// The two halves of pdl_entry, for a kernel with a prologue that reads only
+// data no kernel of the current step writes: parameters, whose writer (the
+// optimizer, or the lanes' replica copy) is always followed by non-GEMM
+// kernels (gathers, persist) before any kernel that prefetches them, so it
+// has completed when such a kernel launches (k_decoder, umma_gru_kernel,
+// umma_gemm_kernel with Args::b_static).
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 inline int pdl_forced() {  // -1 auto, 0 off, 1 on
     static const int m = [] {

@@ -420,8 +420,11 @@ __global__ void k_dec_head2(Dims d, int B, const float* Ya, const float* Yb, con
 template <int MAXT, int MINB, int EV>
 __global__ void __launch_bounds__(MAXT, MINB)
     k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2, float* D1,
-              float* dlogit, float* lossv, float* dD1, float* logits, float* d_emb, int bwd) {
-    pdl_entry();
+              float* dlogit, float* lossv, float* dD1, float* logits, float* d_emb, int bwd, int pre) {
+    // pre: the weight staging (parameters only) is issued before the wait for
+    // the producer of emb (PDL), overlapping that kernel's tail
+    pdl_launch();
+    if (!pre) pdl_wait();
     extern __shared__ __align__(16) float dsm[];
     const int D = d.D, ldw = 2 * D + 4, ldz = D + 4;
     float* sW = dsm;                                  // [D][ldw]: W_a | W_b | b1
@@ -445,6 +448,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
         __syncwarp();
         for (int n = tid; n < D; n += 32)
             bulk_g2s(sW + (std::size_t)n * ldw, W1 + (std::size_t)n * ld1, unsigned(ldw * 4), &bar);
+        if (pre) pdl_wait();
         for (int r = tid; r < 3 * nev; r += 32) {
             const int kind = r / nev, e = r % nev;
             bulk_g2s(sZ + (std::size_t)(kind * EV + e) * ldz, emb + ((std::size_t)kind * B + i0 + e) * D,
@@ -456,6 +460,7 @@ __global__ void __launch_bounds__(MAXT, MINB)
         sZ[(std::size_t)(kind * EV + e) * ldz + i % D] = 0.f;
     }
     for (int i = tid; i <= D; i += nt) sw2[i] = w2[i];
+    if (pre && tid >= 32) pdl_wait();  // (warp 0 waited before its embedding-row copies)
     __syncthreads();  // (barrier initialised before anyone waits)
     bar_wait(&bar, 0);
     // forward projections: thread (kind, n)
@@ -682,7 +687,7 @@ std::size_t dec_wgrad_smem_bytes(const Dims& d) { return 4 * std::size_t(5) * kD
 // 8 events per block, 4 for small batches
 #define SPD_DEC_INST(T, M, E)                                                                          \
     template __global__ void k_decoder<T, M, E>(Dims, int, const float*, const float*, int, const float*, \
-                                                float*, float*, float*, float*, float*, float*, int);
+                                                float*, float*, float*, float*, float*, float*, int, int);
 SPD_DEC_INST(416, 2, kDecEv)
 SPD_DEC_INST(416, 2, kDecEvSmall)
 SPD_DEC_INST(768, 1, kDecEv)

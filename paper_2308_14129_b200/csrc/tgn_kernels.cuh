@@ -158,7 +158,7 @@ constexpr int kDecSmallB = 1024;
 template <int MAXT, int MINB, int EV>
 __global__ void k_decoder(Dims d, int B, const float* emb, const float* W1, int ld1, const float* w2,
                           float* D1, float* dlogit, float* lossv, float* dD1, float* logits,
-                          float* d_emb, int bwd);
+                          float* d_emb, int bwd, int pre);
 std::size_t decoder_smem_bytes(const Dims& d, int ev);
 // k_dec_wgrad_part: events per block and per shared-memory tile (128-event
 // blocks — 16 long-running blocks — took 176 us on the side stream and moved

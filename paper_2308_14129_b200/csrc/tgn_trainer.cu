@@ -1162,7 +1162,7 @@ void TGNTrainer::decode(int B, bool train) {
            unsigned((4 * d.D + 31) / 32 * 32), dsm, st, d, B, static_cast<const float*>(s.emb.p),
            static_cast<const float*>(P + lay_.dec1.off), lay_.dec1.ld,
            static_cast<const float*>(P + lay_.dec2.off), s.D1.p, s.dlogit.p, s.lossv.p, s.dD1.p,
-           s.logits.p, s.d_emb.p, train ? 1 : 0);
+           s.logits.p, s.d_emb.p, train ? 1 : 0, umma::prefetch_knob(2));
 }
 
 // JODIE after the memory update: time-projection embedding, decoder, loss and

@@ -56,6 +56,9 @@ struct Args {
     // C + b * c_bstride; operands through maps.a[b] / maps.b[b]
     int batch;
     long long c_bstride;
+    // B is a parameter tensor (forward / data-gradient GEMMs): its first
+    // stages are loaded before the PDL wait, overlapping the producer of A
+    int b_static;
 };
 
 constexpr int kMaxBatch = 4;
@@ -179,7 +182,8 @@ struct Cfg {
 template <bool A_MN, bool B_MN, int BN, int NSUB, int CL, bool DEEP = false>
 __global__ void __launch_bounds__(THREADS, (DEEP ? 1 : BN * NSUB <= 64 ? 3 : 2))
     umma_gemm_kernel(const __grid_constant__ Maps maps, Args args) {
-    pdl_entry();
+    pdl_launch();
+    if (!args.b_static) pdl_wait();  // (else below, after the set-up and the weight prefetch)
     using C_ = Cfg<A_MN, B_MN, BN, NSUB, CL, DEEP>;
     constexpr int NST = C_::STAGES_;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -232,21 +236,16 @@ __global__ void __launch_bounds__(THREADS, (DEEP ? 1 : BN * NSUB <= 64 ? 3 : 2))
     asm volatile("tcgen05.fence::after_thread_sync;");
     const std::uint32_t tmem = *tmem_slot;
 
+    if (!(warp == 0 && lane == 0)) pdl_wait();
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < n_k; ++kb) {
+            // stage s: expect its bytes once, then the B boxes (this CTA's
+            // share when multicast) and the A tile
+            auto load_b = [&](int kb) {
                 const int s = kb % NST;
-                if (kb >= NST) mbar_wait(empty + s, ((kb / NST) - 1) & 1);
-                unsigned char* a_s = smem + s * C_::STAGE_BYTES;
-                unsigned char* b_s = a_s + C_::A_BYTES;
-                mbar_expect_tx(full + s, C_::STAGE_BYTES);
+                unsigned char* b_s = smem + s * C_::STAGE_BYTES + C_::A_BYTES;
                 const int kc = k_begin + kb * BK;
-                if (!A_MN) {
-                    tma_load_2d(a_s, tmA, full + s, kc, m0);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < BM / 32; ++j) tma_load_2d(a_s + j * 32 * 128, tmA, full + s, m0 + 32 * j, kc);
-                }
+                mbar_expect_tx(full + s, C_::STAGE_BYTES);
 #pragma unroll
                 for (int j = 0; j < C_::B_BOXES; ++j) {
                     if (CL > 1 && (j % CL) != (int)crank) continue;
@@ -255,6 +254,22 @@ __global__ void __launch_bounds__(THREADS, (DEEP ? 1 : BN * NSUB <= 64 ? 3 : 2))
                     const int c1 = B_MN ? kc : n0 + j * C_::KROWS;
                     if (CL > 1) tma_load_2d_mc(dst, tmB, full + s, c0, c1, (1u << CL) - 1);
                     else tma_load_2d(dst, tmB, full + s, c0, c1);
+                }
+            };
+            const int pre = args.b_static ? (n_k < NST ? n_k : NST) : 0;
+            for (int kb = 0; kb < pre; ++kb) load_b(kb);
+            pdl_wait();
+            for (int kb = 0; kb < n_k; ++kb) {
+                const int s = kb % NST;
+                if (kb >= NST) mbar_wait(empty + s, ((kb / NST) - 1) & 1);
+                if (kb >= pre) load_b(kb);
+                unsigned char* a_s = smem + s * C_::STAGE_BYTES;
+                const int kc = k_begin + kb * BK;
+                if (!A_MN) {
+                    tma_load_2d(a_s, tmA, full + s, kc, m0);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BM / 32; ++j) tma_load_2d(a_s + j * 32 * 128, tmA, full + s, m0 + 32 * j, kc);
                 }
             }
         }

@@ -35,6 +35,7 @@ struct GruArgs {
     const std::uint32_t* nodes;  // pending node id per row (w.pU)
     float* mem_new;              // [M][D]
     float* save;                 // [M][4D]: r | z | n | Gh_n, or null (no backward)
+    int prefetch;                // issue the first stages' weight tiles before the PDL wait
 };
 struct GruMaps {
     CUtensorMap x, h, wih, whh;
@@ -68,7 +69,11 @@ __device__ __forceinline__ void tmem_ld8(std::uint32_t taddr, float (&v)[8]) {
 
 template <int UB>
 __global__ void __launch_bounds__(THREADS, GruCfg<UB>::CTAS) umma_gru_kernel(const __grid_constant__ GruMaps maps, GruArgs args) {
-    pdl_entry();
+    // PDL: the set-up (barriers, TMEM) and the first stages' weight tiles
+    // (parameters and the pending count, both final before this step's graph
+    // began) overlap the gather kernel's tail; the gathered rows wait
+    pdl_launch();
+    if (!args.prefetch) pdl_wait();
     using C_ = GruCfg<UB>;
     constexpr int NST = C_::STAGES;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -104,21 +109,31 @@ __global__ void __launch_bounds__(THREADS, GruCfg<UB>::CTAS) umma_gru_kernel(con
     asm volatile("tcgen05.fence::after_thread_sync;");
     const std::uint32_t tmem = *tmem_slot;
 
+    if (!(warp == 0 && lane == 0)) pdl_wait();
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < n_k; ++kb) {
+            auto weights = [&](int kb) {
                 const int s = kb % NST;
-                if (kb >= NST) mbar_wait(empty + s, ((kb / NST) - 1) & 1);
-                unsigned char* a_s = smem + s * C_::STAGE_BYTES;
-                unsigned char* b_s = a_s + C_::A_BYTES;
+                unsigned char* b_s = smem + s * C_::STAGE_BYTES + C_::A_BYTES;
                 mbar_expect_tx(full + s, C_::STAGE_BYTES);
                 const bool hid = kb >= nk1;
                 const int kc = (hid ? kb - nk1 : kb) * BK;
-                tma_load_2d(a_s, hid ? &maps.h : &maps.x, full + s, kc, m0);
 #pragma unroll
                 for (int g = 0; g < 3; ++g)  // gate blocks r, z, n of W: rows g*D + u0 ..
                     tma_load_2d(b_s + g * UB * 128, hid ? &maps.whh : &maps.wih, full + s, kc,
                                 g * args.D + u0);
+            };
+            const int pre = args.prefetch ? (n_k < NST ? n_k : NST) : 0;
+            for (int kb = 0; kb < pre; ++kb) weights(kb);
+            pdl_wait();
+            for (int kb = 0; kb < n_k; ++kb) {
+                const int s = kb % NST;
+                if (kb >= NST) mbar_wait(empty + s, ((kb / NST) - 1) & 1);
+                if (kb >= pre) weights(kb);
+                unsigned char* a_s = smem + s * C_::STAGE_BYTES;
+                const bool hid = kb >= nk1;
+                const int kc = (hid ? kb - nk1 : kb) * BK;
+                tma_load_2d(a_s, hid ? &maps.h : &maps.x, full + s, kc, m0);
             }
         }
     } else if (warp == 1) {

@@ -18,6 +18,20 @@
 namespace spd {
 namespace umma {
 
+// Parameter prefetch before the PDL wait (umma_gemm.cuh Args::b_static,
+// GruArgs::prefetch): SPD_PREFETCH = bitmask, bit 0 the forward / data-gradient
+// GEMMs' weight operand, bit 1 the fused GRU's gate weights, bit 2 the
+// decoder's W1 rows (tgn_trainer.cu). GDELT step (ms): none 0.3346 / 0.3350,
+// GEMMs 0.3537 (their early CTAs hold shared memory and TMEM while waiting),
+// GRU 0.3330, decoder 0.3316, GRU + decoder 0.3306 — the default (6).
+int prefetch_knob(int bit) {
+    static const int m = [] {
+        const char* e = std::getenv("SPD_PREFETCH");
+        return e ? std::atoi(e) : 6;
+    }();
+    return (m >> bit) & 1;
+}
+
 extern std::atomic<std::uint64_t> g_launch_counter;
 std::atomic<std::uint64_t> g_launch_counter{0};
 
@@ -213,6 +227,7 @@ void fwd(const float* A, int lda, const float* W, int ldw, float* C, int ldc, in
     a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
     a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask; a.rnd = rnd;
     a.batch = bt.n; a.c_bstride = bt.c;
+    a.b_static = prefetch_knob(0);  // W: a parameter tensor (umma_gemm.cuh Args)
     const int mt = (M + BM - 1) / BM;
     Maps maps{};
     if (mt >= 64 && N > 256 && N <= 416 && !M_dev && bt.n == 1) {
@@ -243,6 +258,7 @@ void dgrad(const float* A, int lda, const float* W, int ldw, float* C, int ldc, 
     a.C = C; a.ldc = ldc; a.M = M; a.N = N; a.K = K; a.M_dev = M_dev; a.k_split = 1;
     a.mode = STORE; a.epi = epi; a.mask = mask; a.ldmask = ldmask; a.rnd = rnd;
     a.batch = bt.n; a.c_bstride = bt.c;
+    a.b_static = prefetch_knob(0);  // W: a parameter tensor (umma_gemm.cuh Args)
     const int mt = (M + BM - 1) / BM;
     if (mt >= 64 && N <= 224 && !M_dev && bt.n == 1) {  // big: W multicast to CTA pairs
         maps.a[0] = make_map(A, K, M, lda, BM);
@@ -324,6 +340,7 @@ void gru_fused_t(const float* x, int ldx, int K1, const float* h, int ldh, int K
     maps.whh = make_map(Whh, K2, 3 * D, ldwhh, UB);
     GruArgs a{};
     a.M = M; a.M_dev = M_dev; a.K1 = K1; a.K2 = K2; a.D = D;
+    a.prefetch = prefetch_knob(1);
     a.mem = mem; a.nodes = nodes; a.mem_new = mem_new; a.save = save;
     auto kern = umma_gru_kernel<UB>;
     ensure_smem(kern, C_::SMEM);

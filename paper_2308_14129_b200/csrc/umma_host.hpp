@@ -46,6 +46,7 @@ void gru_fused(const float* x, int ldx, int K1, const float* h, int ldh, int K2,
                const float* mem, const std::uint32_t* nodes, float* mem_new, float* save,
                cudaStream_t s);
 std::uint64_t launches();
+int prefetch_knob(int bit);  // SPD_PREFETCH bit (umma_host.cu)
 
 }  // namespace umma
 }  // namespace spd
