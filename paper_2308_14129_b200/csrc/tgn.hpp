@@ -291,6 +291,11 @@ private:
     cudaEvent_t ev_bwdx_ = nullptr;  // attention time-encoder partials done
     cudaEvent_t ev_pull_ = nullptr;  // dH chunk partials done (tgn_dh.cu)
     cudaEvent_t ev_pend_ = nullptr;  // (DyRep) this batch's last messages selected
+    cudaEvent_t ev_wc_ = nullptr;    // the step's folded output x value projection built
+    cudaEvent_t ev_ctx_ = nullptr;   // ctx (dW_o's input) computed beside the folded O GEMM
+    bool fold_o_ = false;
+    DevBuf<float> wc_;               // DQ x H ld_p (build_wc)
+    void build_wc(cudaStream_t sx);
     // deferred split-K sums of the step's last GRU weight gradients (fused_finalize)
     umma::SplitK fin_sk_[2];
     bool fin_defer_ = false;

@@ -236,6 +236,18 @@ __global__ void k_jodie_embed(WorkerDev w, Dims d, int R, const std::uint32_t* r
     if (lane == 0) s_out[r] = s;
 }
 
+// Folded output x value projection (tgn_trainer.cu build_wc): add b_o to head
+// 0's bias column and round the product to tf32 when it feeds tensor cores.
+__global__ void k_wc_fix(float* wc, int rows, int ld, int DK, const float* b_o, int ld_o, int rnd) {
+    pdl_entry();
+    const std::size_t i = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (std::size_t)rows * ld) return;
+    const int n = static_cast<int>(i / ld), c = static_cast<int>(i % ld);
+    float v = wc[i];
+    if (c == DK) v += b_o[(std::size_t)n * ld_o];
+    wc[i] = rnd ? tf32r(v) : v;
+}
+
 // DyRep message payload: after k_pending filled the other pending set with
 // this batch's last messages, copy each record's other-endpoint attention
 // embedding (z = [z_src rows | z_dst rows] of the batch) beside it. Record of

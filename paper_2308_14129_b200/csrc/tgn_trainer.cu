@@ -465,7 +465,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
 
     SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
     SPD_CUDA(cudaStreamCreateWithPriority(&zs_, cudaStreamNonBlocking, prio_lo));
-    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_dhidx_, &ev_zfork_, &ev_zero_, &ev_bwdx_, &ev_pull_, &ev_pend_})
+    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_dhidx_, &ev_zfork_, &ev_zero_, &ev_bwdx_, &ev_pull_, &ev_pend_, &ev_wc_, &ev_ctx_})
         SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     if (cfg.backbone < 0 || cfg.backbone > 2)
         data_error("InvalidParams", "backbone must be 0 (TGN), 1 (JODIE) or 2 (DyRep)");
@@ -595,6 +595,14 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
         const char* e = std::getenv("SPD_GRU_FUSED");
         gru_fused_ = !(e && *e == '0') && cfg.backbone == 0;
     }
+    {  // folded output x value projection (build_wc); SPD_FOLD_O=0: separate ctx and O GEMMs
+        const char* e = std::getenv("SPD_FOLD_O");
+        fold_o_ = !(e && *e == '0') && cfg.backbone == 0;
+        if (fold_o_) {
+            wc_.alloc(std::size_t(d.DQ) * d.H * d.ld_p);
+            wc_.zero(stream_);  // the per-head pad columns stay 0
+        }
+    }
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
     SPD_CUDA(cudaStreamSynchronize(stream_));
 
@@ -673,7 +681,7 @@ TGNTrainer::~TGNTrainer() {
         if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
         if (sides_[k]) cudaStreamDestroy(sides_[k]);
     }
-    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_dhidx_, ev_zfork_, ev_zero_, ev_bwdx_, ev_pull_, ev_pend_})
+    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_dhidx_, ev_zfork_, ev_zero_, ev_bwdx_, ev_pull_, ev_pend_, ev_wc_, ev_ctx_})
         if (e) cudaEventDestroy(e);
     if (aux_) cudaStreamDestroy(aux_);
     for (auto& p : aring_)
@@ -983,6 +991,23 @@ void TGNTrainer::gru_forward(Worker& w, const tgnk::WorkerDev& wd, bool train,
     SPD_CUDA(cudaGetLastError());
 }
 
+// Wc = [W_o,0 [W_V,0 | b_V,0] | W_o,1 [W_V,1 | b_V,1] | ...] (DQ x H ld_p,
+// per-head pads 0) + b_o in head 0's bias column: O = [xbar_0 | xbar_1 ...] Wc^T
+// (xbar_h's bias slot is sum_j a_hj = 1, or 0 with xbar = 0 for a root without
+// neighbours) and dxbar = dO Wc. Built from the FP32 parameters each step
+// (FFMA, ~8 MFLOP), rounded to tf32 for the tensor cores.
+void TGNTrainer::build_wc(cudaStream_t sx) {
+    const auto& d = s_->d;
+    const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
+    const float* P = params_.p;
+    const float* WV = P + lay_.att_kv.off + std::size_t(d.DQ) * lay_.att_kv.ld;
+    for (int h = 0; h < d.H; ++h)
+        gemm_dgrad(P + lay_.att_o.off + h * dh, lay_.att_o.ld, WV + std::size_t(h) * dh * lay_.att_kv.ld,
+                   lay_.att_kv.ld, wc_.p + std::size_t(h) * d.ld_p, ldhp, d.DQ, d.DK + 1, dh, nullptr, sx);
+    launch(tgnk::k_wc_fix, blocks_for(std::size_t(d.DQ) * ldhp), 256, 0, sx, wc_.p, d.DQ, ldhp, d.DK,
+           static_cast<const float*>(P + lay_.att_o.off + d.DQ), lay_.att_o.ld, cfg_.gemm_mode == 1 ? 1 : 0);
+}
+
 // One batch of one worker: events [lo, lo+B) of the view's event list.
 // train: forward + backward (weight grads accumulate into grads_) + post;
 // eval (train = false): forward + post (scores in s.logits), no gradients.
@@ -1077,16 +1102,36 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
                    0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
     });
     timed("k_attn_abs_fwd", [&] { attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st); });
-    timed("gemm_ctx", [&] {
-        proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
+    auto ctx_gemm = [&](cudaStream_t sx) {
+        proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, sx, 0,
                  nullptr, 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
-    });
+    };
+    if (fold_o_) {
+        // O = [xbar_0 | xbar_1] Wc^T in one GEMM (Wc: the step's value x output
+        // projection product, build_wc); roots without neighbours have xbar = 0
+        // (bias slot too), hence O = 0 without a row mask. ctx itself is only
+        // read by dW_o: computed beside it when training.
+        if (train) {
+            cudaEvent_t at_x = mark();
+            side_from(at_x, [&](cudaStream_t sd) {
+                ctx_gemm(sd);
+                SPD_CUDA(cudaEventRecord(ev_ctx_, sd));
+            });
+        }
+        SPD_CUDA(cudaStreamWaitEvent(st, ev_wc_, 0));
+    } else {
+        timed("gemm_ctx", [&] { ctx_gemm(st); });
+    }
     timed("head_fwd", [&] {
         // O = [ctx | 1] W_o^T straight into the MergeLayer input's attention
         // columns, 0 for roots without neighbours (the s_root columns came
         // with the query gather)
-        proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.m_in.p, d.ld_m, R, d.DQ,
-                 d.DQ + 1, nullptr, st, gemm::EPI_ROWMASK, reinterpret_cast<const float*>(s.cnt.p), d.DQ, tc);
+        if (fold_o_)
+            proj_fwd(tc, s.xbar.p, ldhp, wc_.p, ldhp, s.m_in.p, d.ld_m, R, d.DQ, ldhp, nullptr, st, 0,
+                     nullptr, 0, tc);
+        else
+            proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.m_in.p, d.ld_m, R, d.DQ,
+                     d.DQ + 1, nullptr, st, gemm::EPI_ROWMASK, reinterpret_cast<const float*>(s.cnt.p), d.DQ, tc);
         proj_fwd(tc, s.m_in.p, d.ld_m, PW + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
                  d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU, nullptr, 0, tc);
         proj_fwd(tc, s.Z1.p, d.ld_z, PW + lay_.mrg2.off, lay_.mrg2.ld, s.emb.p, d.D, R, d.D, d.D + 1,
@@ -1318,12 +1363,14 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
                                                         lay_.mrg1.ld, d.D, d.DQ + d.D + 1, R, nullptr,
                                                         ws_cur_, wsn_cur_, sd); });
         // output projection
-        at = mark();
-        proj_dgrad(tc, s.dm_in.p, d.ld_m, PW + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R, d.DQ,
-                   d.DQ, nullptr, st, 0, nullptr, 0, tc);
-        side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx,
-                                                        G + lay_.att_o.off, lay_.att_o.ld, d.DQ, d.DQ + 1,
-                                                        R, nullptr, ws_cur_, wsn_cur_, sd); });
+        if (!fold_o_) {
+            at = mark();
+            proj_dgrad(tc, s.dm_in.p, d.ld_m, PW + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R, d.DQ,
+                       d.DQ, nullptr, st, 0, nullptr, 0, tc);
+            side_from(at, [&](cudaStream_t sd) { proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx,
+                                                            G + lay_.att_o.off, lay_.att_o.ld, d.DQ, d.DQ + 1,
+                                                            R, nullptr, ws_cur_, wsn_cur_, sd); });
+        }
     });
     const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
     const float* WK = PW + lay_.att_kv.off;
@@ -1333,6 +1380,25 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     float* GV = GK + std::size_t(d.DQ) * ldw;
     const std::ptrdiff_t wst = std::ptrdiff_t(dh) * ldw;  // per-head weight slab
     timed("gemm_dxbar", [&] {
+        if (fold_o_) {
+            // dxbar = dO Wc (one GEMM for the output and value projections);
+            // beside it dctx = dO W_o for dW_o and dW_V,h += dctx_h^T xbar_h
+            cudaEvent_t at = mark();
+            proj_dgrad(tc, s.dm_in.p, d.ld_m, wc_.p, ldhp, s.dxbar.p, ldhp, R, ldhp, d.DQ, nullptr, st, 0,
+                       nullptr, 0, 0);
+            side_from(at, [&](cudaStream_t sd) {
+                SPD_CUDA(cudaStreamWaitEvent(sd, ev_ctx_, 0));
+                proj_wgrad(tc, s.dm_in.p, d.ld_m, s.ctx.p, d.ld_ctx, G + lay_.att_o.off, lay_.att_o.ld,
+                           d.DQ, d.DQ + 1, R, nullptr, ws_cur_, wsn_cur_, sd);
+            });
+            side_from(at, [&](cudaStream_t sd) {
+                proj_dgrad(tc, s.dm_in.p, d.ld_m, PW + lay_.att_o.off, lay_.att_o.ld, s.dctx.p, d.ld_Q, R,
+                           d.DQ, d.DQ, nullptr, sd, 0, nullptr, 0, tc);
+                proj_wgrad(tc, s.dctx.p, d.ld_Q, s.xbar.p, ldhp, GV, ldw, dh, d.DK + 1, R, nullptr, ws_cur_,
+                           wsn_cur_, sd, umma::Batch{d.H, dh, d.ld_p, wst});
+            });
+            return;
+        }
         // dW_V,h += dctx_h^T xbar_h ; dxbar_h = dctx_h [W_V,h | b_V,h]
         cudaEvent_t at = mark();
         proj_dgrad(tc, s.dctx.p, d.ld_Q, WV, ldw, s.dxbar.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0,
@@ -1765,6 +1831,10 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
         scratch_zeroed_ = true;  // the first backward of this step skips its own zeroing
     }
     SPD_CUDA(cudaEventRecord(ev_zero_, zs_));
+    if (fold_o_) side([&](cudaStream_t sd) {  // the step's Wc, beside the memory update
+        build_wc(sd);
+        SPD_CUDA(cudaEventRecord(ev_wc_, sd));
+    });
     std::size_t last = workers_.size();
     for (std::size_t k = 0; k < workers_.size(); ++k)
         if (Bs[k] > 0) last = k;
@@ -2345,6 +2415,10 @@ void TGNTrainer::evaluate(int wid, std::uint64_t lo, std::uint64_t hi, std::uint
     int slot_idx = 0;
     for (std::size_t k = 0; k < workers_.size(); ++k)
         if (workers_[k].get() == &w) slot_idx = static_cast<int>(k);
+    if (fold_o_) {
+        build_wc(stream_);
+        SPD_CUDA(cudaEventRecord(ev_wc_, stream_));
+    }
     std::vector<float> lg;
     for (std::uint64_t b0 = lo; b0 < hi; b0 += cfg_.batch_size) {
         const int B = static_cast<int>(std::min<std::uint64_t>(hi, b0 + cfg_.batch_size) - b0);
