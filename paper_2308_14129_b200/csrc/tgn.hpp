@@ -296,6 +296,10 @@ private:
     bool fold_o_ = false;
     DevBuf<float> wc_;               // DQ x H ld_p (build_wc)
     void build_wc(cudaStream_t sx);
+    cudaEvent_t ev_q_ = nullptr;     // Q (dW_K's input) computed beside the folded Qp GEMM
+    bool fold_q_ = false;
+    DevBuf<float> wqk_;              // (DQ + 1) x H ld_p (build_wqk)
+    void build_wqk(cudaStream_t sx);
     // deferred split-K sums of the step's last GRU weight gradients (fused_finalize)
     umma::SplitK fin_sk_[2];
     bool fin_defer_ = false;

@@ -236,6 +236,23 @@ __global__ void k_jodie_embed(WorkerDev w, Dims d, int R, const std::uint32_t* r
     if (lane == 0) s_out[r] = s;
 }
 
+// Per-head A_h^T B_h (A_h, B_h: rows h dh .. (h+1) dh of A and B): out[i][h
+// hstride + k] = sum_c A[h dh + c][i] B[h dh + c][k], i < rows, k < cols, in c
+// order (tgn_trainer.cu build_wqk); tf32-rounded when it feeds tensor cores.
+__global__ void k_wprod_t(float* out, int ldo, int hstride, const float* A, int lda, const float* B, int ldb,
+                          int rows, int cols, int dh, int H, int rnd) {
+    pdl_entry();
+    const std::size_t t = (std::size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (std::size_t)H * rows * cols) return;
+    const int k = static_cast<int>(t % cols), i = static_cast<int>((t / cols) % rows);
+    const int h = static_cast<int>(t / ((std::size_t)rows * cols));
+    const float* a = A + (std::size_t)h * dh * lda + i;
+    const float* b = B + (std::size_t)h * dh * ldb + k;
+    float acc = 0.f;
+    for (int c = 0; c < dh; ++c) acc = fmaf(a[(std::size_t)c * lda], b[(std::size_t)c * ldb], acc);
+    out[(std::size_t)i * ldo + (std::size_t)h * hstride + k] = rnd ? tf32r(acc) : acc;
+}
+
 // Folded output x value projection (tgn_trainer.cu build_wc): add b_o to head
 // 0's bias column and round the product to tf32 when it feeds tensor cores.
 __global__ void k_wc_fix(float* wc, int rows, int ld, int DK, const float* b_o, int ld_o, int rnd) {

@@ -208,6 +208,8 @@ __global__ void k_rnn_fwd(WorkerDev w, Dims d, const float* Gi, const float* Gh,
 __global__ void k_jodie_embed(WorkerDev w, Dims d, int R, const std::uint32_t* roots, const double* root_t,
                               const float* mem_new, const float* tp, int ldtp, float* emb, float* s_out);
 __global__ void k_dyrep_stash(WorkerDev w, int D, int B, const float* z);
+__global__ void k_wprod_t(float* out, int ldo, int hstride, const float* A, int lda, const float* B, int ldb,
+                          int rows, int cols, int dh, int H, int rnd);
 __global__ void k_wc_fix(float* wc, int rows, int ld, int DK, const float* b_o, int ld_o, int rnd);
 __global__ void k_jodie_bwd(WorkerDev w, Dims d, int R, const std::uint32_t* roots, const float* mem_new,
                             const float* tp, int ldtp, const float* s_in, const float* d_emb, float* dq_in,

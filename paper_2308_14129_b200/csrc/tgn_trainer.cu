@@ -465,7 +465,7 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
 
     SPD_CUDA(cudaStreamCreateWithPriority(&aux_, cudaStreamNonBlocking, prio_hi));
     SPD_CUDA(cudaStreamCreateWithPriority(&zs_, cudaStreamNonBlocking, prio_lo));
-    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_dhidx_, &ev_zfork_, &ev_zero_, &ev_bwdx_, &ev_pull_, &ev_pend_, &ev_wc_, &ev_ctx_})
+    for (cudaEvent_t* e : {&ev_aux_fork_, &ev_aux_join_, &ev_roots_, &ev_dhidx_, &ev_zfork_, &ev_zero_, &ev_bwdx_, &ev_pull_, &ev_pend_, &ev_wc_, &ev_ctx_, &ev_q_})
         SPD_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     if (cfg.backbone < 0 || cfg.backbone > 2)
         data_error("InvalidParams", "backbone must be 0 (TGN), 1 (JODIE) or 2 (DyRep)");
@@ -597,10 +597,20 @@ TGNTrainer::TGNTrainer(const spd_tgn_config& cfg, const SubGraphs& subs,
     }
     {  // folded output x value projection (build_wc); SPD_FOLD_O=0: separate ctx and O GEMMs
         const char* e = std::getenv("SPD_FOLD_O");
+        // (TGN only: DyRep's forward-only message embedding measured 0.2148 folded
+        // vs 0.2120 ms — the per-step build is not repaid by one forward GEMM)
         fold_o_ = !(e && *e == '0') && cfg.backbone == 0;
         if (fold_o_) {
             wc_.alloc(std::size_t(d.DQ) * d.H * d.ld_p);
             wc_.zero(stream_);  // the per-head pad columns stay 0
+        }
+        // (the query x key fold measured slower: GDELT 0.361 vs 0.326 ms — its
+        // long-K data-gradient GEMM and the side Q / dQ GEMMs; SPD_FOLD_Q=1)
+        const char* q = std::getenv("SPD_FOLD_Q");
+        fold_q_ = (q && *q == '1') && cfg.backbone == 0;
+        if (fold_q_) {
+            wqk_.alloc(std::size_t(d.DQ + 1) * d.H * d.ld_p);
+            wqk_.zero(stream_);
         }
     }
     s.loss.alloc(std::max<std::size_t>(1, workers_.size()));
@@ -681,7 +691,7 @@ TGNTrainer::~TGNTrainer() {
         if (ev_join_[k]) cudaEventDestroy(ev_join_[k]);
         if (sides_[k]) cudaStreamDestroy(sides_[k]);
     }
-    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_dhidx_, ev_zfork_, ev_zero_, ev_bwdx_, ev_pull_, ev_pend_, ev_wc_, ev_ctx_})
+    for (cudaEvent_t e : {ev_aux_fork_, ev_aux_join_, ev_roots_, ev_dhidx_, ev_zfork_, ev_zero_, ev_bwdx_, ev_pull_, ev_pend_, ev_wc_, ev_ctx_, ev_q_})
         if (e) cudaEventDestroy(e);
     if (aux_) cudaStreamDestroy(aux_);
     for (auto& p : aring_)
@@ -1008,6 +1018,19 @@ void TGNTrainer::build_wc(cudaStream_t sx) {
            static_cast<const float*>(P + lay_.att_o.off + d.DQ), lay_.att_o.ld, cfg_.gemm_mode == 1 ? 1 : 0);
 }
 
+// Wqk_h = [W_q,h | b_q,h]^T [W_K,h | b_K,h] ((DQ + 1) x (DK + 1) per head, at
+// column h ld_p of a (DQ + 1) x H ld_p matrix, pads 0): Qp = [q_in | 1] Wqk and
+// dq_in = dQp Wqk^T (rows < DQ).
+void TGNTrainer::build_wqk(cudaStream_t sx) {
+    const auto& d = s_->d;
+    const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
+    const float* P = params_.p;
+    launch(tgnk::k_wprod_t, blocks_for(std::size_t(d.H) * (d.DQ + 1) * (d.DK + 1)), 256, 0, sx, wqk_.p,
+           ldhp, d.ld_p, static_cast<const float*>(P + lay_.att_q.off), lay_.att_q.ld,
+           static_cast<const float*>(P + lay_.att_kv.off), lay_.att_kv.ld, d.DQ + 1, d.DK + 1, dh, d.H,
+           cfg_.gemm_mode == 1 ? 1 : 0);
+}
+
 // One batch of one worker: events [lo, lo+B) of the view's event list.
 // train: forward + backward (weight grads accumulate into grads_) + post;
 // eval (train = false): forward + post (scores in s.logits), no gradients.
@@ -1086,10 +1109,6 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
                P + lay_.time_w, P + lay_.time_b, s.roots.p, s.mem_new.p, s.q_in.p,
                s.m_in.p);
     });
-    timed("gemm_q", [&] {
-        proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
-                 d.DQ + 1, nullptr, st, 0, nullptr, 0, tc);
-    });
     // attention with absorbed key/value projections (tgn_attn.cu):
     //   Qp_h = Q_h [W_K,h | b_K,h]; kernel -> alpha, xbar_h; ctx_h = xbar_h [W_V,h | b_V,h]^T
     const int dh = d.DQ / d.H, ldhp = d.H * d.ld_p;
@@ -1097,10 +1116,33 @@ void TGNTrainer::worker_step(Worker& w, const tgnk::WorkerDev& wd, int B, bool t
     const float* WV = WK + std::size_t(d.DQ) * lay_.att_kv.ld;
     const int ldw = lay_.att_kv.ld;
     const std::ptrdiff_t wst = std::ptrdiff_t(dh) * ldw;  // per-head weight slab
-    timed("gemm_qp", [&] {
-        proj_dgrad(tc, s.Q.p, d.ld_Q, WK, ldw, s.Qp.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0, nullptr,
-                   0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
-    });
+    auto q_gemm = [&](cudaStream_t sx) {
+        proj_fwd(tc, s.q_in.p, d.ld_q, PW + lay_.att_q.off, lay_.att_q.ld, s.Q.p, d.ld_Q, R, d.DQ,
+                 d.DQ + 1, nullptr, sx, 0, nullptr, 0, tc);
+    };
+    if (fold_q_) {
+        // Qp = [q_in | 1] Wqk in one GEMM (Wqk: the step's query x key
+        // projection product, build_wc); Q itself is only read by dW_K:
+        // computed beside it when training
+        if (train) {
+            cudaEvent_t at_q = mark();
+            side_from(at_q, [&](cudaStream_t sd) {
+                q_gemm(sd);
+                SPD_CUDA(cudaEventRecord(ev_q_, sd));
+            });
+        }
+        SPD_CUDA(cudaStreamWaitEvent(st, ev_wc_, 0));
+        timed("gemm_qp", [&] {
+            proj_dgrad(tc, s.q_in.p, d.ld_q, wqk_.p, ldhp, s.Qp.p, ldhp, R, ldhp, d.DQ + 1, nullptr, st, 0,
+                       nullptr, 0, 0);
+        });
+    } else {
+        timed("gemm_q", [&] { q_gemm(st); });
+        timed("gemm_qp", [&] {
+            proj_dgrad(tc, s.Q.p, d.ld_Q, WK, ldw, s.Qp.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0, nullptr,
+                       0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
+        });
+    }
     timed("k_attn_abs_fwd", [&] { attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st); });
     auto ctx_gemm = [&](cudaStream_t sx) {
         proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, sx, 0,
@@ -1310,10 +1352,16 @@ void TGNTrainer::dyrep_messages(const tgnk::WorkerDev& wd, int B, bool train) {
         proj_dgrad(tc, s.Q.p, d.ld_Q, WK, ldw, s.Qp.p, ldhp, R, d.DK + 1, dh, nullptr, st, 0, nullptr,
                    0, 0, umma::Batch{d.H, dh, wst, d.ld_p});
         attn_abs_fwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, st);
-        proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
-                 nullptr, 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
-        proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.m_in.p, d.ld_m, R, d.DQ,
-                 d.DQ + 1, nullptr, st, gemm::EPI_ROWMASK, reinterpret_cast<const float*>(s.cnt.p), d.DQ, tc);
+        if (fold_o_) {  // O = [xbar_0 | xbar_1] Wc^T (build_wc; no backward reads ctx here)
+            SPD_CUDA(cudaStreamWaitEvent(st, ev_wc_, 0));
+            proj_fwd(tc, s.xbar.p, ldhp, wc_.p, ldhp, s.m_in.p, d.ld_m, R, d.DQ, ldhp, nullptr, st, 0,
+                     nullptr, 0, tc);
+        } else {
+            proj_fwd(tc, s.xbar.p, ldhp, WV, ldw, s.ctx.p, d.ld_ctx, R, dh, d.DK + 1, nullptr, st, 0,
+                     nullptr, 0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
+            proj_fwd(tc, s.ctx.p, d.ld_ctx, PW + lay_.att_o.off, lay_.att_o.ld, s.m_in.p, d.ld_m, R, d.DQ,
+                     d.DQ + 1, nullptr, st, gemm::EPI_ROWMASK, reinterpret_cast<const float*>(s.cnt.p), d.DQ, tc);
+        }
         proj_fwd(tc, s.m_in.p, d.ld_m, PW + lay_.mrg1.off, lay_.mrg1.ld, s.Z1.p, d.ld_z, R, d.D,
                  d.DQ + d.D + 1, nullptr, st, gemm::EPI_RELU, nullptr, 0, tc);
         proj_fwd(tc, s.Z1.p, d.ld_z, PW + lay_.mrg2.off, lay_.mrg2.ld, s.zmsg.p, d.D, R, d.D, d.D + 1,
@@ -1426,11 +1474,12 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
         timed("attn_time_grad", [&] { attn_time_grad(d, R, P + lay_.time_w, P + lay_.time_b, s, attn_part, st); });
     }
     cudaEvent_t at_bwd = mark();  // the attention backward is done
-    timed("gemm_dq", [&] {
+    auto dq_gemm = [&](cudaStream_t sx) {
         // dQ_h = dQp_h [W_K,h | b_K,h]^T
-        proj_fwd(tc, s.dQp.p, ldhp, WK, ldw, s.dQ.p, d.ld_Q, R, dh, d.DK + 1, nullptr, st, 0, nullptr,
+        proj_fwd(tc, s.dQp.p, ldhp, WK, ldw, s.dQ.p, d.ld_Q, R, dh, d.DK + 1, nullptr, sx, 0, nullptr,
                  0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
-    });
+    };
+    if (!fold_q_) timed("gemm_dq", [&] { dq_gemm(st); });
     if (!profile_) {
         // the attention input gradients (dH pull, time-encoder partials) and
         // dW_K beside the query backward: created after the dQ GEMM
@@ -1444,6 +1493,24 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
             SPD_CUDA(cudaEventRecord(ev_bwdx_, sd));
         });
     }
+    if (fold_q_) {
+        // dq_in = dQp Wqk^T (one GEMM for the key and query projections);
+        // beside it dQ for dW_q, and dW_K,h += Q_h^T dQp_h
+        timed("q_bwd", [&] {
+            proj_fwd(tc, s.dQp.p, ldhp, wqk_.p, ldhp, s.dq_in.p, d.ld_q, R, d.DQ, ldhp, nullptr, st, 0,
+                     nullptr, 0, 0);
+        });
+        side_from(at_bwd, [&](cudaStream_t sd) {
+            dq_gemm(sd);
+            proj_wgrad(tc, s.dQ.p, d.ld_Q, s.q_in.p, d.ld_q, G + lay_.att_q.off, lay_.att_q.ld, d.DQ,
+                       d.DQ + 1, R, nullptr, ws_cur_, wsn_cur_, sd);
+        });
+        side_from(at_bwd, [&](cudaStream_t sd) {
+            SPD_CUDA(cudaStreamWaitEvent(sd, ev_q_, 0));
+            proj_wgrad(tc, s.Q.p, d.ld_Q, s.dQp.p, ldhp, GK, ldw, dh, d.DK + 1, R, nullptr, ws_cur_,
+                       wsn_cur_, sd, umma::Batch{d.H, dh, d.ld_p, wst});
+        });
+    } else {
     // dW_K,h += Q_h^T dQp_h
     side_from(at_bwd, [&](cudaStream_t sd) {
         proj_wgrad(tc, s.Q.p, d.ld_Q, s.dQp.p, ldhp, GK, ldw, dh, d.DK + 1, R, nullptr, ws_cur_,
@@ -1457,6 +1524,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
                                                         lay_.att_q.ld, d.DQ, d.DQ + 1, R, nullptr, ws_cur_,
                                                         wsn_cur_, sd); });
     });
+    }
     // root-side time-encoder partials and their reduction with the attention
     // partials: only the all-reduce reads the result, so off the critical path
     side([&](cudaStream_t sd) {
@@ -1831,8 +1899,9 @@ void TGNTrainer::step_body(const std::vector<int>& Bs) {
         scratch_zeroed_ = true;  // the first backward of this step skips its own zeroing
     }
     SPD_CUDA(cudaEventRecord(ev_zero_, zs_));
-    if (fold_o_) side([&](cudaStream_t sd) {  // the step's Wc, beside the memory update
-        build_wc(sd);
+    if (fold_o_ || fold_q_) side([&](cudaStream_t sd) {  // the step's Wc / Wqk, beside the memory update
+        if (fold_o_) build_wc(sd);
+        if (fold_q_) build_wqk(sd);
         SPD_CUDA(cudaEventRecord(ev_wc_, sd));
     });
     std::size_t last = workers_.size();
@@ -2415,8 +2484,9 @@ void TGNTrainer::evaluate(int wid, std::uint64_t lo, std::uint64_t hi, std::uint
     int slot_idx = 0;
     for (std::size_t k = 0; k < workers_.size(); ++k)
         if (workers_[k].get() == &w) slot_idx = static_cast<int>(k);
-    if (fold_o_) {
-        build_wc(stream_);
+    if (fold_o_ || fold_q_) {
+        if (fold_o_) build_wc(stream_);
+        if (fold_q_) build_wqk(stream_);
         SPD_CUDA(cudaEventRecord(ev_wc_, stream_));
     }
     std::vector<float> lg;
