@@ -492,8 +492,44 @@ __global__ void __launch_bounds__(MAXT, MINB)
     if (pre && tid >= 32) pdl_wait();  // (warp 0 waited before its embedding-row copies)
     __syncthreads();  // (barrier initialised before anyone waits)
     bar_wait(&bar, 0);
-    // forward projections: thread (kind, n)
-    if (tid < 3 * D) {
+    // forward projections: thread (kind, n); for even D each thread owns the
+    // output pair (n, n + D/2), sharing its activation loads (half the shared-
+    // memory traffic; each output's summation order unchanged)
+    const bool blk = (D & 1) == 0;
+    const int Dh = D >> 1;
+    if (blk) {
+        if (tid < 3 * Dh) {
+            const int kind = tid / Dh, n = tid % Dh;
+            const float* wr0 = sW + (std::size_t)n * ldw + (kind ? D : 0);
+            const float* wr1 = wr0 + (std::size_t)Dh * ldw;
+            const float* z = sZ + (std::size_t)kind * EV * ldz;
+            float a0[EV], a1[EV];
+#pragma unroll
+            for (int e = 0; e < EV; ++e) a0[e] = a1[e] = 0.f;
+#pragma unroll 1
+            for (int k = 0; k < D; k += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(wr0 + k);
+                const float4 u = *reinterpret_cast<const float4*>(wr1 + k);
+#pragma unroll
+                for (int e = 0; e < EV; ++e) {
+                    const float4 x = *reinterpret_cast<const float4*>(z + (std::size_t)e * ldz + k);
+                    a0[e] = fmaf(x.x, w.x, a0[e]);
+                    a0[e] = fmaf(x.y, w.y, a0[e]);
+                    a0[e] = fmaf(x.z, w.z, a0[e]);
+                    a0[e] = fmaf(x.w, w.w, a0[e]);
+                    a1[e] = fmaf(x.x, u.x, a1[e]);
+                    a1[e] = fmaf(x.y, u.y, a1[e]);
+                    a1[e] = fmaf(x.z, u.z, a1[e]);
+                    a1[e] = fmaf(x.w, u.w, a1[e]);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < EV; ++e) {
+                sY[(std::size_t)(kind * EV + e) * ldz + n] = a0[e];
+                sY[(std::size_t)(kind * EV + e) * ldz + n + Dh] = a1[e];
+            }
+        }
+    } else if (tid < 3 * D) {
         const int kind = tid / D, n = tid % D;
         const float* wr = sW + (std::size_t)n * ldw + (kind ? D : 0);
         const float* z = sZ + (std::size_t)kind * EV * ldz;
