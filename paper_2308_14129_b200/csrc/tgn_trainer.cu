@@ -1464,7 +1464,14 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
     timed("k_attn_abs_bwd", [&] {
         attn_abs_bwd(wd, d, R, P + lay_.time_w, P + lay_.time_b, s, nullptr, st);
     });
-    decoder_wgrads(at_dec, B);
+    // ... forked after the dQ GEMM is created (their shared-memory-heavy blocks
+    // held SMs the dQ GEMM then waited for: 0.3228 / 0.3232 vs 0.3236 / 0.3235
+    // ms per GDELT step); SPD_DECWG_LATE=0 forks them here
+    static const bool decwg_late = [] {
+        const char* e = std::getenv("SPD_DECWG_LATE");
+        return !(e && *e == '0');
+    }();
+    if (!decwg_late) decoder_wgrads(at_dec, B);
     // the attention input gradients — memory columns summed per pending row
     // (k_dh_pull, deterministic, tgn_dh.cu) and the time-encoder partials —
     // run beside the dQ GEMMs; the GRU backward and the time-grad reduction
@@ -1480,6 +1487,7 @@ void TGNTrainer::backward(Worker& w, const tgnk::WorkerDev& wd, int B) {
                  0, tc, umma::Batch{d.H, d.ld_p, wst, dh});
     };
     if (!fold_q_) timed("gemm_dq", [&] { dq_gemm(st); });
+    if (decwg_late) decoder_wgrads(mark(), B);
     if (!profile_) {
         // the attention input gradients (dH pull, time-encoder partials) and
         // dW_K beside the query backward: created after the dQ GEMM
