@@ -493,3 +493,33 @@ def test_concurrent_workers_match_oracle(parts, sync_average, backbone, concurre
     ms = tr.run_steps(o.epoch_steps() + 3)
     assert ms > 0
     tr.close()
+
+
+@pytest.mark.parametrize("gemm_mode", [0, 1])
+@pytest.mark.parametrize("fold_o,fold_q", [("0", "0"), ("1", "1")])
+def test_projection_fold_variants_match_oracle(gemm_mode, fold_o, fold_q, monkeypatch):
+    """The per-step folded projections (DESIGN §3: O = [xbar] Wc^T, default on;
+    Qp = [q_in | 1] Wqk, SPD_FOLD_Q=1) and the unfolded chains all meet the
+    oracle's bars: embeddings, losses, first-step gradients and parameters."""
+    monkeypatch.setenv("SPD_FOLD_O", fold_o)
+    monkeypatch.setenv("SPD_FOLD_Q", fold_q)
+    _, _, pa, subs = partitioned(parts=2)
+    cfg = small_cfg(gemm_mode=gemm_mode)
+    tr = sp.TGNTrainer(cfg, subs, shared=pa.shared)
+    tr.set_debug(True)
+    o = oracle_for(cfg, subs, pa.shared)
+    step_tol, traj_tol = (TOL_STEP, TOL_TRAJ) if gemm_mode == 0 else (TOL_TF32_STEP, TOL_TF32)
+    tr.begin_epoch(0)
+    o.begin_epoch(0)
+    for step in range(6):
+        gl = tr.step()
+        ol = o.step()
+        tol = step_tol if step == 0 else traj_tol
+        for w in range(2):
+            e = rel_err(tr.last_step(w)["emb"], o.last[w]["emb"])
+            assert e < tol, (step, w, e)
+            assert abs(gl[w] - ol[w]) <= tol * max(1.0, abs(ol[w]))
+        if step == 0:
+            assert rel_err(tr.grads(), o.grad.numpy()) < (TOL_GRAD if gemm_mode == 0 else TOL_TF32_GRAD)
+    assert rel_err(tr.params(), o.flat.numpy()) < traj_tol
+    tr.close()
